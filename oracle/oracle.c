@@ -1,0 +1,724 @@
+/*
+ * oracle.c -- plain, slow, scalar CPU oracle for the 2-party nonlinear-operator
+ * path of arxiv 2511.19711 (CrypTorch / CrypTen++).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load this library.  It shares no code,
+ * header, table or constant generator with the CUDA path under
+ * paper_2511_19711_b200/ and includes nothing from it.
+ *
+ * Citations: "P:n" = line n of /root/reference/PAPER.md, "S:n" = line n of
+ * /root/reference/SPEC.md, "R<k>" = reading k in DESIGN.md section 3 (the
+ * places where the paper is silent and we fixed a reading).
+ *
+ * Every operation simulates BOTH parties in lockstep on plain arrays
+ * (x0[i], x1[i]) of uint64 ring elements of Z_2^64 (P:997-1000, P:1026:
+ * "CrypTen uses s=2^16 and a 64-bit integer ring").  Steps of each schedule are
+ * executed in the order DESIGN.md section 2 lists them, over the whole array,
+ * one step at a time (no fusion, no blocking).
+ *
+ * Pinning: every function here is pinned by tests/test_oracle_*.py against
+ * closed forms, brute force, the paper's printed values and invariants
+ * (DESIGN.md section 4).  None is "parity unpinned".
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef uint32_t u32;
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon et al., SC'11; the Random123 reference algorithm).   */
+/* Reading R8: the paper's TTP dealer and SPEC's "own seed"  */
+/* fix no generator; we fix Philox4x32-10 with counter (unit_lo, unit_hi,     */
+/* step, slot) and a 64-bit key (lo32, hi32).                                 */
+/* ------------------------------------------------------------------------ */
+void orc_philox4x32_10(const u32 ctr_in[4], const u32 key_in[2], u32 out[4])
+{
+    u32 c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    u32 k[2] = {key_in[0], key_in[1]};
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k[0] += 0x9E3779B9u; k[1] += 0xBB67AE85u; }
+        u64 p0 = (u64)0xD2511F53u * (u64)c[0];
+        u64 p1 = (u64)0xCD9E8D57u * (u64)c[2];
+        u32 hi0 = (u32)(p0 >> 32), lo0 = (u32)p0;
+        u32 hi1 = (u32)(p1 >> 32), lo1 = (u32)p1;
+        u32 n0 = hi1 ^ c[1] ^ k[0];
+        u32 n1 = lo1;
+        u32 n2 = hi0 ^ c[3] ^ k[1];
+        u32 n3 = lo0;
+        c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+/* PRG(key, unit, step, slot) -> 4 words. */
+static void prg(u64 key, u64 unit, u64 step, u32 slot, u32 w[4])
+{
+    u32 ctr[4] = {(u32)unit, (u32)(unit >> 32), (u32)step, slot};
+    u32 k[2] = {(u32)key, (u32)(key >> 32)};
+    orc_philox4x32_10(ctr, k, w);
+}
+static u64 w64(u32 lo, u32 hi) { return (u64)lo | ((u64)hi << 32); }
+
+typedef struct {
+    u64 key_share, key_p0, key_p1;   /* K_s, K_0, K_1 */
+    u64 step;                        /* next unused step id */
+} orc_ctx;
+
+/* ------------------------------------------------------------------------ */
+/* Fixed-point encoding E(c) = round-half-even(c * 2^16)  ("round it  */
+/* to the nearest integer"; reading R2: ties to even).                       */
+/* ------------------------------------------------------------------------ */
+#define FRAC 16
+i64 orc_encode(double c) { return (i64)nearbyint(c * 65536.0); }
+
+/* per-share arithmetic shift (local truncation; R3: floor) */
+static u64 shr(u64 v, int k) { return (u64)(((i64)v) >> k); }
+
+/* ------------------------------------------------------------------------ */
+/* S1 share: owner's share = v - r, other = r, r from the pairwise key K_s   */
+/* ("[x]_0 = x - r and [x]_1 = r").  One step per call.           */
+/* ------------------------------------------------------------------------ */
+void orc_share(orc_ctx* ctx, const double* x, int owner, u64* s0, u64* s1, i64 n, i64 off)
+{
+    u64 s = ctx->step++;
+    for (i64 i = 0; i < n; ++i) {
+        u32 w[4];
+        prg(ctx->key_share, (u64)(off + i), s, 0, w);
+        u64 r = w64(w[0], w[1]);
+        u64 v = (u64)orc_encode(x[i]);
+        if (owner == 0) { s0[i] = v - r; s1[i] = r; }
+        else            { s0[i] = r;     s1[i] = v - r; }
+    }
+}
+
+/* S2 open: rec = x0 + x1 mod 2^64; decode (int64)rec / 2^scale_bits */
+void orc_open(const u64* s0, const u64* s1, i64 n, u64* ring, double* f, int scale_bits)
+{
+    for (i64 i = 0; i < n; ++i) {
+        u64 v = s0[i] + s1[i];
+        if (ring) ring[i] = v;
+        if (f) f[i] = (double)(i64)v / (double)((u64)1 << scale_bits);
+    }
+}
+
+/* ------------------------------------------------------------------------ */
+/* S3 + S4: Beaver multiplication with a trusted-dealer triple (P:1009-1011,  */
+/* S:432-440).  Triple layout:                               */
+/*   (a0,b0) = PRG(K0, u, s, 0) ;  (a1,b1) = PRG(K1, u, s, 0)                 */
+/*   c0      = half (u&1) of PRG(K0, u>>1, s, 1) ; c1 = (a0+a1)(b0+b1) - c0  */
+/* e = open(x - a), f = open(y - b);                                          */
+/* z0 = c0 + e*b0 + f*a0 + e*f  (party 0 adds e*f, R6) ; z1 = c1 + e*b1 + f*a1 */
+/* ------------------------------------------------------------------------ */
+static void beaver_triple(const orc_ctx* ctx, u64 s, u64 u,
+                          u64* a0, u64* b0, u64* c0, u64* a1, u64* b1, u64* c1)
+{
+    u32 w[4];
+    prg(ctx->key_p0, u, s, 0, w); *a0 = w64(w[0], w[1]); *b0 = w64(w[2], w[3]);
+    prg(ctx->key_p1, u, s, 0, w); *a1 = w64(w[0], w[1]); *b1 = w64(w[2], w[3]);
+    prg(ctx->key_p0, u >> 1, s, 1, w);
+    *c0 = (u & 1) ? w64(w[2], w[3]) : w64(w[0], w[1]);
+    *c1 = (*a0 + *a1) * (*b0 + *b1) - *c0;   /* dealer correction to party 1 (R7) */
+}
+
+/* BM over an array; element i uses unit units0 + i.  One step. */
+static void BM(orc_ctx* ctx, i64 n, u64 units0,
+               const u64* x0, const u64* x1, const u64* y0, const u64* y1, u64* z0, u64* z1)
+{
+    u64 s = ctx->step++;
+    for (i64 i = 0; i < n; ++i) {
+        u64 a0, b0, c0, a1, b1, c1;
+        beaver_triple(ctx, s, units0 + (u64)i, &a0, &b0, &c0, &a1, &b1, &c1);
+        /* each party masks its own shares; the opening is the sum (one round) */
+        u64 e = (x0[i] - a0) + (x1[i] - a1);
+        u64 f = (y0[i] - b0) + (y1[i] - b1);
+        u64 r0 = c0 + e * b0 + f * a0 + e * f;
+        u64 r1 = c1 + e * b1 + f * a1;
+        z0[i] = r0; z1[i] = r1;
+    }
+}
+
+/* MT(x,y) = trunc(BM(x,y), 16): Sec-Sec Mul rule ("mul_MPC then trunc by s_min") */
+static void MT(orc_ctx* ctx, i64 n, u64 units0,
+               const u64* x0, const u64* x1, const u64* y0, const u64* y1, u64* z0, u64* z1)
+{
+    BM(ctx, n, units0, x0, x1, y0, y1, z0, z1);
+    for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], FRAC); z1[i] = shr(z1[i], FRAC); }
+}
+
+void orc_mul(orc_ctx* ctx, const u64* x0, const u64* x1, const u64* y0, const u64* y1,
+             u64* z0, u64* z1, i64 n, i64 off, int trunc_bits)
+{
+    BM(ctx, n, (u64)off, x0, x1, y0, y1, z0, z1);
+    if (trunc_bits)
+        for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], trunc_bits); z1[i] = shr(z1[i], trunc_bits); }
+}
+
+/* S5 local truncation: z_i = (int64)x_i >> k at each party */
+void orc_trunc(const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, int bits)
+{
+    for (i64 i = 0; i < n; ++i) { z0[i] = shr(x0[i], bits); z1[i] = shr(x1[i], bits); }
+}
+
+/* ------------------------------------------------------------------------ */
+/* S7 LTZ: GMW sign bit realised as A2B + Kogge-Stone carry    */
+/* circuit + daBit B2A (readings R9, R10, R11, R12).        */
+/*                                                                           */
+/* Per element, with m = w-1 carry positions and L = ceil(log2 m) levels:     */
+/*   p_j = x0_j ^ x1_j   (XOR-shared as (x0_j, x1_j), local)                  */
+/*   g_j = x0_j & x1_j   (AND gate on ((x0_j,0),(0,x1_j)))                    */
+/*   level k, d = 2^k, j in [d, m):  G_j ^= P_j & G_{j-d};  P_j &= P_{j-d}     */
+/*   b = p_{w-1} ^ G_{m-1}            (b = p_0 when w == 1)                    */
+/* The triple WORDS of each gate are defined per 32-element group q (bit l of */
+/* a word belongs to element 32q+l); the oracle reads the element's bit.      */
+/* Gate triple layout:                                        */
+/*   SLOT(lv, j, c) = 64 + 128*lv + 2*j + c                                   */
+/*   g-layer plane j:   (a0,b0,c0)=PRG(K0,q,s,SLOT(0,j,0))[0..2],             */
+/*                      (a1,b1)   =PRG(K1,q,s,SLOT(0,j,0))[0..1]              */
+/*   level k plane j:   G-gate (a0,b0,c0)=PRG(K0,q,s,SLOT(k+1,j,0))[0..2]     */
+/*                      P-gate (a0,b0,c0)=PRG(K0,q,s,SLOT(k+1,j,1))[0..2]     */
+/*                      T1 = PRG(K1,q,s,SLOT(k+1,j,0)):                       */
+/*                        G-gate (a1,b1)=T1[0..1], P-gate (a1,b1)=T1[2..3]     */
+/*   c1 = ((a0^a1)&(b0^b1))^c0  (dealer correction to party 1)                */
+/* daBit of element l:  D0=PRG(K0,q,s,2+l): r0A=w64(D0[0],D0[1]), r0B=D0[2]&1 */
+/*                      r1B = bit l of PRG(K1,q,s,1)[0] ; r=r0B^r1B ; r1A=r-r0A */
+/* B2A: c = open(b ^ r); z0 = c + (1-2c) r0A ; z1 = (1-2c) r1A                 */
+/* ------------------------------------------------------------------------ */
+#define SLOT(lv, j, c) (64u + 128u * (u32)(lv) + 2u * (u32)(j) + (u32)(c))
+
+typedef struct { u32 a0, b0, c0, a1, b1, c1; } btriple;
+
+static btriple and_triple_words(const u32 t0[4], u32 a1, u32 b1)
+{
+    btriple t;
+    t.a0 = t0[0]; t.b0 = t0[1]; t.c0 = t0[2];
+    t.a1 = a1; t.b1 = b1;
+    t.c1 = ((t.a0 ^ t.a1) & (t.b0 ^ t.b1)) ^ t.c0;
+    return t;
+}
+
+/* AND of XOR-shared bits (x0^x1)&(y0^y1) with a bit-triple (one round).      */
+static void and_gate(int x0, int x1, int y0, int y1, const btriple* t, int l, int* z0, int* z1)
+{
+    int a0 = (t->a0 >> l) & 1, b0 = (t->b0 >> l) & 1, c0 = (t->c0 >> l) & 1;
+    int a1 = (t->a1 >> l) & 1, b1 = (t->b1 >> l) & 1, c1 = (t->c1 >> l) & 1;
+    int d = (x0 ^ a0) ^ (x1 ^ a1);     /* opened */
+    int e = (y0 ^ b0) ^ (y1 ^ b1);     /* opened */
+    *z0 = c0 ^ (d & b0) ^ (e & a0) ^ (d & e);
+    *z1 = c1 ^ (d & b1) ^ (e & a1);
+}
+
+static int ceil_log2(int m) { int L = 0; while ((1 << L) < m) ++L; return L; }
+
+/* Number of AND gates of the full Kogge-Stone LTZ at window w (R9). */
+int orc_ltz_gate_count(int w)
+{
+    int m = w - 1;
+    if (m <= 0) return 0;
+    int L = ceil_log2(m), g = m;
+    for (int k = 0; k < L; ++k) g += 2 * (m - (1 << k));
+    return g;
+}
+
+/* the group's triples, generated once per (q, s) and then read bit by bit  */
+typedef struct {
+    btriple g[64];          /* g-layer, plane j */
+    btriple G[7][64];       /* level k, plane j: G-gate */
+    btriple P[7][64];       /* level k, plane j: P-gate */
+} ltz_group_triples;
+
+static void gen_group_triples(const orc_ctx* ctx, u64 s, u64 q, int w, ltz_group_triples* T)
+{
+    int m = w - 1, L = (m > 0) ? ceil_log2(m) : 0;
+    u32 t0[4], t0p[4], t1[4];
+    for (int j = 0; j < m; ++j) {
+        prg(ctx->key_p0, q, s, SLOT(0, j, 0), t0);
+        prg(ctx->key_p1, q, s, SLOT(0, j, 0), t1);
+        T->g[j] = and_triple_words(t0, t1[0], t1[1]);
+    }
+    for (int k = 0; k < L; ++k)
+        for (int j = (1 << k); j < m; ++j) {
+            prg(ctx->key_p0, q, s, SLOT(k + 1, j, 0), t0);
+            prg(ctx->key_p0, q, s, SLOT(k + 1, j, 1), t0p);
+            prg(ctx->key_p1, q, s, SLOT(k + 1, j, 0), t1);
+            T->G[k][j] = and_triple_words(t0, t1[0], t1[1]);
+            T->P[k][j] = and_triple_words(t0p, t1[2], t1[3]);
+        }
+}
+
+/* LTZ over an array whose element i has unit units0 + i.  One step.         */
+/* Output: arithmetic shares of b = bit (w-1) of rec(x), at scale 1.          */
+static void LTZ(orc_ctx* ctx, i64 n, u64 units0, int w,
+                const u64* x0, const u64* x1, u64* z0, u64* z1)
+{
+    u64 s = ctx->step++;
+    int m = w - 1, L = (m > 0) ? ceil_log2(m) : 0;
+    ltz_group_triples* T = (ltz_group_triples*)malloc(sizeof(ltz_group_triples));
+    u64 cur_q = ~(u64)0;
+    u32 r1b_word = 0;
+    for (i64 i = 0; i < n; ++i) {
+        u64 u = units0 + (u64)i, q = u >> 5;
+        int l = (int)(u & 31);
+        if (q != cur_q) {
+            gen_group_triples(ctx, s, q, w, T);
+            u32 d1[4];
+            prg(ctx->key_p1, q, s, 1, d1);
+            r1b_word = d1[0];
+            cur_q = q;
+        }
+        /* A2B: each party bit-decomposes its own share (local) */
+        int X0[64], X1[64];
+        for (int j = 0; j < w; ++j) { X0[j] = (int)((x0[i] >> j) & 1); X1[j] = (int)((x1[i] >> j) & 1); }
+        int G0[64], G1[64], P0[64], P1[64];
+        for (int j = 0; j < m; ++j) {
+            P0[j] = X0[j]; P1[j] = X1[j];                            /* p_j shares */
+            and_gate(X0[j], 0, 0, X1[j], &T->g[j], l, &G0[j], &G1[j]); /* g_j = x0_j & x1_j */
+        }
+        for (int k = 0; k < L; ++k) {
+            int d = 1 << k;
+            int nG0[64], nG1[64], nP0[64], nP1[64];
+            for (int j = 0; j < m; ++j) { nG0[j] = G0[j]; nG1[j] = G1[j]; nP0[j] = P0[j]; nP1[j] = P1[j]; }
+            for (int j = d; j < m; ++j) {     /* G-updates */
+                int t0, t1;
+                and_gate(P0[j], P1[j], G0[j - d], G1[j - d], &T->G[k][j], l, &t0, &t1);
+                nG0[j] = G0[j] ^ t0; nG1[j] = G1[j] ^ t1;
+            }
+            for (int j = d; j < m; ++j)       /* P-updates */
+                and_gate(P0[j], P1[j], P0[j - d], P1[j - d], &T->P[k][j], l, &nP0[j], &nP1[j]);
+            memcpy(G0, nG0, sizeof G0); memcpy(G1, nG1, sizeof G1);
+            memcpy(P0, nP0, sizeof P0); memcpy(P1, nP1, sizeof P1);
+        }
+        int b0, b1;
+        if (m == 0) { b0 = X0[0]; b1 = X1[0]; }
+        else        { b0 = X0[w - 1] ^ G0[m - 1]; b1 = X1[w - 1] ^ G1[m - 1]; }
+        /* daBit + B2A */
+        u32 d0[4];
+        prg(ctx->key_p0, q, s, 2u + (u32)l, d0);
+        u64 r0A = w64(d0[0], d0[1]);
+        int r0B = (int)(d0[2] & 1u);
+        int r1B = (int)((r1b_word >> l) & 1u);
+        u64 r = (u64)(r0B ^ r1B);
+        u64 r1A = r - r0A;
+        u64 c = (u64)((b0 ^ r0B) ^ (b1 ^ r1B));     /* opened bit */
+        u64 sgn = (u64)1 - 2 * c;                    /* 1 - 2c mod 2^64 */
+        z0[i] = c + sgn * r0A;
+        z1[i] = sgn * r1A;
+    }
+    free(T);
+}
+
+void orc_ltz(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off, int w)
+{
+    LTZ(ctx, n, (u64)off, w, x0, x1, z0, z1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Local public operations (rules P:398-483)          */
+/* ------------------------------------------------------------------------ */
+static void addP(u64* x0, i64 n, double c) { u64 e = (u64)orc_encode(c); for (i64 i = 0; i < n; ++i) x0[i] += e; }
+static void notmask(u64* b0, u64* b1, i64 n) { for (i64 i = 0; i < n; ++i) { b0[i] = 1 - b0[i]; b1[i] = (u64)0 - b1[i]; } }
+static void pmulF(u64* x0, u64* x1, i64 n, double c)
+{
+    u64 e = (u64)orc_encode(c);
+    for (i64 i = 0; i < n; ++i) { x0[i] = shr(x0[i] * e, FRAC); x1[i] = shr(x1[i] * e, FRAC); }
+}
+
+/* per-share floor division by a public positive integer (reading R25) */
+static i64 floordiv(i64 a, i64 d) { i64 q = a / d; if ((a % d) != 0 && (a < 0)) --q; return q; }
+static void divP(u64* x0, u64* x1, i64 n, i64 d)
+{
+    for (i64 i = 0; i < n; ++i) { x0[i] = (u64)floordiv((i64)x0[i], d); x1[i] = (u64)floordiv((i64)x1[i], d); }
+}
+
+static u64* A(i64 n) { return (u64*)malloc(sizeof(u64) * (size_t)(n > 0 ? n : 1)); }
+
+/* S8 ReLU = BM(x, NOT(LTZ(x)))  ("x x (x >= 0)"; no truncation: */
+/* the mask has scale 1, s_min = 1, R5).  2 steps.                            */
+void orc_relu(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off, int w)
+{
+    u64 *l0 = A(n), *l1 = A(n);
+    LTZ(ctx, n, (u64)off, w, x0, x1, l0, l1);
+    notmask(l0, l1, n);
+    BM(ctx, n, (u64)off, x0, x1, l0, l1, z0, z1);
+    free(l0); free(l1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* S10 EXP(x; t, clamp, w): (1 + x/2^t)^(2^t) (Fig. pass_lang)*/
+/*   y = addP(shr(x,t), 1.0)            x/2^t as a shift (R4)                 */
+/*   clamp: y = BM(y, NOT(LTZ_w(addP(x, 2^t))))     mask [x >= -2^t] (R13)     */
+/*   t times: y = MT(y, y)                                                    */
+/* Steps: t + 2*clamp.                                                        */
+/* ------------------------------------------------------------------------ */
+static void EXP(orc_ctx* ctx, i64 n, u64 units0, int t, int clamp, int w,
+                const u64* x0, const u64* x1, u64* y0, u64* y1)
+{
+    u64 e1 = (u64)orc_encode(1.0);
+    u64 *c0 = A(n), *c1 = A(n);                       /* x + 2^t, taken before y may alias x */
+    memcpy(c0, x0, sizeof(u64) * (size_t)n); memcpy(c1, x1, sizeof(u64) * (size_t)n);
+    addP(c0, n, ldexp(1.0, t));
+    for (i64 i = 0; i < n; ++i) { y0[i] = shr(x0[i], t) + e1; y1[i] = shr(x1[i], t); }
+    if (clamp) {
+        u64 *l0 = A(n), *l1 = A(n);
+        LTZ(ctx, n, units0, w, c0, c1, l0, l1);
+        notmask(l0, l1, n);
+        BM(ctx, n, units0, y0, y1, l0, l1, y0, y1);
+        free(l0); free(l1);
+    }
+    free(c0); free(c1);
+    for (int k = 0; k < t; ++k) MT(ctx, n, units0, y0, y1, y0, y1, y0, y1);
+}
+
+void orc_exp(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
+             int t, int clamp, int w)
+{
+    EXP(ctx, n, (u64)off, t, clamp, w, x0, x1, z0, z1);
+}
+
+/* S11 RECIP: Newton-Raphson y <- y(2 - x y) from y0 = 3 exp(0.5 - x) + 0.003  */
+/* ("Newton-Raphson method"; S:208-216, S:240 initialisation).          */
+static void RECIP(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, int w,
+                  const u64* x0, const u64* x1, u64* y0, u64* y1)
+{
+    u64 *g0 = A(n), *g1 = A(n), *p0 = A(n), *p1 = A(n);
+    for (i64 i = 0; i < n; ++i) { g0[i] = (u64)0 - x0[i]; g1[i] = (u64)0 - x1[i]; }
+    addP(g0, n, 0.5);
+    EXP(ctx, n, units0, t, clamp, w, g0, g1, g0, g1);
+    for (i64 i = 0; i < n; ++i) { y0[i] = g0[i] * 3; y1[i] = g1[i] * 3; }   /* pmulI(g,3) */
+    addP(y0, n, 0.003);
+    for (int it = 0; it < iters; ++it) {
+        MT(ctx, n, units0, x0, x1, y0, y1, p0, p1);                             /* p = x*y */
+        for (i64 i = 0; i < n; ++i) { p0[i] = (u64)0 - p0[i]; p1[i] = (u64)0 - p1[i]; }
+        addP(p0, n, 2.0);                                                       /* 2 - p */
+        MT(ctx, n, units0, y0, y1, p0, p1, y0, y1);                             /* y*(2-p) */
+    }
+    free(g0); free(g1); free(p0); free(p1);
+}
+
+void orc_recip(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
+               int iters, int t, int clamp, int w)
+{
+    RECIP(ctx, n, (u64)off, iters, t, clamp, w, x0, x1, z0, z1);
+}
+
+/* S12 RSQRT: y <- y (3 - x y^2) / 2 from y0 = 2.2 exp(-(x/2 + 0.2)) + 0.2     */
+/* ("uses e^x in its approximation of inverse sqrt").  */
+static void RSQRT(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, int w,
+                  const u64* x0, const u64* x1, u64* y0, u64* y1)
+{
+    u64 *g0 = A(n), *g1 = A(n), *q0 = A(n), *q1 = A(n), *p0 = A(n), *p1 = A(n);
+    for (i64 i = 0; i < n; ++i) { g0[i] = shr(x0[i], 1); g1[i] = shr(x1[i], 1); }
+    addP(g0, n, 0.2);
+    for (i64 i = 0; i < n; ++i) { g0[i] = (u64)0 - g0[i]; g1[i] = (u64)0 - g1[i]; }
+    EXP(ctx, n, units0, t, clamp, w, g0, g1, g0, g1);
+    memcpy(y0, g0, sizeof(u64) * (size_t)n); memcpy(y1, g1, sizeof(u64) * (size_t)n);
+    pmulF(y0, y1, n, 2.2);
+    addP(y0, n, 0.2);
+    for (int it = 0; it < iters; ++it) {
+        MT(ctx, n, units0, y0, y1, y0, y1, q0, q1);                 /* q = y*y  */
+        MT(ctx, n, units0, x0, x1, q0, q1, p0, p1);                 /* p = x*q  */
+        for (i64 i = 0; i < n; ++i) { p0[i] = (u64)0 - p0[i]; p1[i] = (u64)0 - p1[i]; }
+        addP(p0, n, 3.0);                                            /* 3 - p    */
+        MT(ctx, n, units0, y0, y1, p0, p1, y0, y1);                 /* u = y*(3-p) */
+        pmulF(y0, y1, n, 0.5);                                       /* y = u*0.5 */
+    }
+    free(g0); free(g1); free(q0); free(q1); free(p0); free(p1);
+}
+
+void orc_rsqrt(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
+               int iters, int t, int clamp, int w)
+{
+    RSQRT(ctx, n, (u64)off, iters, t, clamp, w, x0, x1, z0, z1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* S13 segment polynomials ("order-4 polynomial from BOLT ...   */
+/* order-2 polynomial and ReLU").                                   */
+/* HORNER(v; c_0..c_d), d >= 1:  h = addP(pmulF(v, c_d), c_{d-1});            */
+/*   for k = d-2..0: h = addP(MT(h, v), c_k).   d-1 steps.                      */
+/* ------------------------------------------------------------------------ */
+static void HORNER(orc_ctx* ctx, i64 n, u64 units0, const u64* v0, const u64* v1,
+                   const double* c, int d, u64* h0, u64* h1)
+{
+    memcpy(h0, v0, sizeof(u64) * (size_t)n); memcpy(h1, v1, sizeof(u64) * (size_t)n);
+    pmulF(h0, h1, n, c[d]);
+    addP(h0, n, c[d - 1]);
+    for (int k = d - 2; k >= 0; --k) {
+        MT(ctx, n, units0, h0, h1, v0, v1, h0, h1);
+        addP(h0, n, c[k]);
+    }
+}
+
+enum { ACT_GELU = 0, ACT_SILU = 1, ACT_SIGMOID = 2 };
+enum { FORM_POLY_X = 0, FORM_POLY_ABS = 1, FORM_RELU = 2, FORM_ERF = 3 };
+
+/* segment masks + final masked sum shared by the x-, |x|- and erf- forms:   */
+/*   l1 = LTZ(x + B), l2 = LTZ(x - B)   (two steps, listed order)              */
+/*   out = BM(inner, l2 - l1) + tail,  tail = BM(x, NOT(l2)) (GELU/SiLU) or    */
+/*                                     pmulI(NOT(l2), 2^16) (Sigmoid, local)   */
+void orc_act(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
+             int act, int form, int degree, double B, const double* coeffs, int erf_terms, int w)
+{
+    u64 U = (u64)off;
+    u64 *l0 = A(n), *l1 = A(n), *m0 = A(n), *m1 = A(n), *h0 = A(n), *h1 = A(n), *t0 = A(n), *t1 = A(n);
+    if (form == FORM_RELU || degree == 0) {
+        /* degree 0: ReLU for GELU/SiLU, unit step 1 - ltz(x) for Sigmoid */
+        LTZ(ctx, n, U, w, x0, x1, l0, l1);
+        notmask(l0, l1, n);
+        if (act == ACT_SIGMOID) {
+            for (i64 i = 0; i < n; ++i) { z0[i] = l0[i] << FRAC; z1[i] = l1[i] << FRAC; }
+        } else {
+            BM(ctx, n, U, x0, x1, l0, l1, z0, z1);
+        }
+        goto done;
+    }
+    {
+        u64 *s0 = NULL, *s1 = NULL;
+        if (form == FORM_POLY_ABS) {                     /* s = ltz(x) first */
+            s0 = A(n); s1 = A(n);
+            LTZ(ctx, n, U, w, x0, x1, s0, s1);
+        }
+        memcpy(t0, x0, sizeof(u64) * (size_t)n); memcpy(t1, x1, sizeof(u64) * (size_t)n);
+        addP(t0, n, B);
+        LTZ(ctx, n, U, w, t0, t1, l0, l1);               /* l1 = [x < -B] */
+        memcpy(t0, x0, sizeof(u64) * (size_t)n); memcpy(t1, x1, sizeof(u64) * (size_t)n);
+        addP(t0, n, -B);
+        LTZ(ctx, n, U, w, t0, t1, m0, m1);               /* l2 = [x < B]  */
+        if (form == FORM_POLY_X) {
+            HORNER(ctx, n, U, x0, x1, coeffs, degree, h0, h1);
+        } else if (form == FORM_POLY_ABS) {
+            /* |x| = BM(x, 1 - 2s) ; h = 0.5 x + P(|x|) (BOLT structure) */
+            u64 *sg0 = A(n), *sg1 = A(n), *ax0 = A(n), *ax1 = A(n);
+            for (i64 i = 0; i < n; ++i) { sg0[i] = 1 - 2 * s0[i]; sg1[i] = (u64)0 - 2 * s1[i]; }
+            BM(ctx, n, U, x0, x1, sg0, sg1, ax0, ax1);
+            HORNER(ctx, n, U, ax0, ax1, coeffs, degree, h0, h1);
+            memcpy(t0, x0, sizeof(u64) * (size_t)n); memcpy(t1, x1, sizeof(u64) * (size_t)n);
+            pmulF(t0, t1, n, 0.5);
+            for (i64 i = 0; i < n; ++i) { h0[i] += t0[i]; h1[i] += t1[i]; }
+            free(sg0); free(sg1); free(ax0); free(ax1);
+        } else { /* FORM_ERF: GELU(x) = 0.5 x (1 + erf(x/sqrt2)), Maclaurin erf (R21) */
+            int K = erf_terms;
+            double* a = (double*)malloc(sizeof(double) * (size_t)K);
+            double fact = 1.0;
+            for (int k = 0; k < K; ++k) {
+                if (k > 0) fact *= (double)k;
+                a[k] = ((k & 1) ? -1.0 : 1.0) / (fact * (double)(2 * k + 1));
+            }
+            u64 *zz0 = A(n), *zz1 = A(n), *z20 = A(n), *z21 = A(n), *S0 = A(n), *S1 = A(n);
+            memcpy(zz0, x0, sizeof(u64) * (size_t)n); memcpy(zz1, x1, sizeof(u64) * (size_t)n);
+            pmulF(zz0, zz1, n, 1.0 / sqrt(2.0));                     /* z = x / sqrt 2 */
+            MT(ctx, n, U, zz0, zz1, zz0, zz1, z20, z21);             /* z^2 */
+            HORNER(ctx, n, U, z20, z21, a, K - 1, S0, S1);           /* sum a_k z^(2k) */
+            MT(ctx, n, U, zz0, zz1, S0, S1, t0, t1);                 /* z * S */
+            pmulF(t0, t1, n, 2.0 / sqrt(M_PI));                      /* erf */
+            addP(t0, n, 1.0);                                        /* 1 + erf */
+            MT(ctx, n, U, x0, x1, t0, t1, h0, h1);                   /* x (1 + erf) */
+            pmulF(h0, h1, n, 0.5);
+            free(a); free(zz0); free(zz1); free(z20); free(z21); free(S0); free(S1);
+        }
+        /* segment mask (l2 - l1) and masked sum */
+        for (i64 i = 0; i < n; ++i) { t0[i] = m0[i] - l0[i]; t1[i] = m1[i] - l1[i]; }
+        BM(ctx, n, U, h0, h1, t0, t1, z0, z1);
+        notmask(m0, m1, n);
+        if (act == ACT_SIGMOID) {
+            for (i64 i = 0; i < n; ++i) { z0[i] += m0[i] << FRAC; z1[i] += m1[i] << FRAC; }
+        } else {
+            BM(ctx, n, U, x0, x1, m0, m1, t0, t1);
+            for (i64 i = 0; i < n; ++i) { z0[i] += t0[i]; z1[i] += t1[i]; }
+        }
+        if (s0) { free(s0); free(s1); }
+    }
+done:
+    free(l0); free(l1); free(m0); free(m1); free(h0); free(h1); free(t0); free(t1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* S9 MAX_row: half-split tree (R22) with mux y + c (x - y) ("one       */
+/* (y + c x (x - y))").  Level with m live entries: h = m/2;       */
+/*   d_i = x_i - x_{i+h};  c_i = NOT(LTZ(d_i));  x_i' = x_{i+h} + BM(d_i, c_i) */
+/*   units row*h + i (global row); odd m: last entry carried to position h.   */
+/* Each level: 2 steps, batched over all rows.                                 */
+/* ------------------------------------------------------------------------ */
+static int max_levels(i64 cols) { int L = 0; i64 m = cols; while (m > 1) { m = (m + 1) / 2; ++L; } return L; }
+
+static void MAXROW(orc_ctx* ctx, i64 rows, i64 cols, i64 row_off, int w,
+                   const u64* x0, const u64* x1, u64* mx0, u64* mx1)
+{
+    u64 *v0 = A(rows * cols), *v1 = A(rows * cols);
+    memcpy(v0, x0, sizeof(u64) * (size_t)(rows * cols));
+    memcpy(v1, x1, sizeof(u64) * (size_t)(rows * cols));
+    i64 m = cols;
+    while (m > 1) {
+        i64 h = m / 2;
+        i64 nn = rows * h;
+        u64 *d0 = A(nn), *d1 = A(nn), *c0 = A(nn), *c1 = A(nn), *p0 = A(nn), *p1 = A(nn);
+        for (i64 r = 0; r < rows; ++r)
+            for (i64 i = 0; i < h; ++i) {
+                d0[r * h + i] = v0[r * cols + i] - v0[r * cols + i + h];
+                d1[r * h + i] = v1[r * cols + i] - v1[r * cols + i + h];
+            }
+        u64 U = (u64)(row_off * h);
+        LTZ(ctx, nn, U, w, d0, d1, c0, c1);
+        notmask(c0, c1, nn);
+        BM(ctx, nn, U, d0, d1, c0, c1, p0, p1);
+        for (i64 r = 0; r < rows; ++r) {
+            for (i64 i = 0; i < h; ++i) {
+                u64 y0 = v0[r * cols + i + h], y1 = v1[r * cols + i + h];
+                v0[r * cols + i] = y0 + p0[r * h + i];
+                v1[r * cols + i] = y1 + p1[r * h + i];
+            }
+            if (m & 1) { v0[r * cols + h] = v0[r * cols + m - 1]; v1[r * cols + h] = v1[r * cols + m - 1]; }
+        }
+        m = h + (m & 1);
+        free(d0); free(d1); free(c0); free(c1); free(p0); free(p1);
+    }
+    for (i64 r = 0; r < rows; ++r) { mx0[r] = v0[r * cols]; mx1[r] = v1[r * cols]; }
+    free(v0); free(v1);
+}
+
+void orc_max(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 rows, i64 cols,
+             i64 row_off, int w)
+{
+    if (rows <= 0 || cols <= 0) { ctx->step += 2 * (u64)max_levels(cols); return; }
+    MAXROW(ctx, rows, cols, row_off, w, x0, x1, z0, z1);
+}
+
+int orc_max_levels(i64 cols) { return max_levels(cols); }
+
+/* MaxPool2d: each output window (public zero padding, R26) becomes one row of */
+/* k*k entries, row index = global output index; then MAX_row.   */
+void orc_maxpool2d(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
+                   int N, int C, int H, int W, int k, int stride, int pad, i64 img_off, int w)
+{
+    int Ho = (H + 2 * pad - k) / stride + 1, Wo = (W + 2 * pad - k) / stride + 1;
+    i64 rows = (i64)N * C * Ho * Wo, cols = (i64)k * k;
+    u64 *r0 = A(rows * cols), *r1 = A(rows * cols);
+    for (i64 o = 0; o < rows; ++o) {
+        i64 ow = o % Wo, oh = (o / Wo) % Ho, c = (o / ((i64)Wo * Ho)) % C, nimg = o / ((i64)Wo * Ho * C);
+        for (int dy = 0; dy < k; ++dy)
+            for (int dx = 0; dx < k; ++dx) {
+                i64 iy = oh * stride - pad + dy, ix = ow * stride - pad + dx;
+                u64 a = 0, b = 0;
+                if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
+                    i64 idx = ((nimg * C + c) * H + iy) * W + ix;
+                    a = x0[idx]; b = x1[idx];
+                }
+                r0[o * cols + dy * k + dx] = a; r1[o * cols + dy * k + dx] = b;
+            }
+    }
+    i64 row_off = img_off * (i64)C * Ho * Wo;
+    orc_max(ctx, r0, r1, z0, z1, rows, cols, row_off, w);
+    free(r0); free(r1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* S14 SOFTMAX: e^{x - max} / sum e^{x - max} (P:604 footnote)     */
+/*   m = MAX_row(x); d = x - m; e = EXP(d) [units: element index];             */
+/*   S = rowsum(e); r = RECIP(S) [units: row]; out = MT(e, bcast r) [element]  */
+/* ------------------------------------------------------------------------ */
+void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
+                 i64 rows, i64 cols, i64 row_off, int w,
+                 int exp_t, int exp_clamp, int exp_w,
+                 int rc_iters, int rc_t, int rc_clamp, int rc_w)
+{
+    i64 n = rows * cols;
+    u64 *mx0 = A(rows), *mx1 = A(rows), *e0 = A(n), *e1 = A(n), *S0 = A(rows), *S1 = A(rows);
+    u64 *r0 = A(rows), *r1 = A(rows), *b0 = A(n), *b1 = A(n);
+    if (rows > 0 && cols > 0) MAXROW(ctx, rows, cols, row_off, w, x0, x1, mx0, mx1);
+    else ctx->step += 2 * (u64)max_levels(cols);
+    for (i64 r = 0; r < rows; ++r)
+        for (i64 j = 0; j < cols; ++j) {
+            e0[r * cols + j] = x0[r * cols + j] - mx0[r];
+            e1[r * cols + j] = x1[r * cols + j] - mx1[r];
+        }
+    u64 Ue = (u64)(row_off * cols);
+    EXP(ctx, n, Ue, exp_t, exp_clamp, exp_w, e0, e1, e0, e1);
+    for (i64 r = 0; r < rows; ++r) {
+        u64 a = 0, b = 0;
+        for (i64 j = 0; j < cols; ++j) { a += e0[r * cols + j]; b += e1[r * cols + j]; }
+        S0[r] = a; S1[r] = b;
+    }
+    RECIP(ctx, rows, (u64)row_off, rc_iters, rc_t, rc_clamp, rc_w, S0, S1, r0, r1);
+    for (i64 r = 0; r < rows; ++r)
+        for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
+    MT(ctx, n, Ue, e0, e1, b0, b1, z0, z1);
+    free(mx0); free(mx1); free(e0); free(e1); free(S0); free(S1); free(r0); free(r1); free(b0); free(b1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* S15 LAYERNORM (mean as Sec-PubFloat Mul by 1/d):          */
+/*   mean_mode 0: x 1/d as pmulF(., 1/d)  (E(1/768) = 85, R25)      */
+/*   mean_mode 1: per-share floor division by the public integer d (R25),       */
+/*                same wrap probability as local truncation           */
+/*   mu = pmulF(rowsum(x), 1/d); c = x - mu;                                   */
+/*   v = addP(pmulF(rowsum(MT(c,c)), 1/d), eps); r = RSQRT(v) [units: row];    */
+/*   out = MT(c, bcast r) [units: element]                                     */
+/* ------------------------------------------------------------------------ */
+void orc_layernorm(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
+                   i64 rows, i64 cols, i64 row_off, double eps, int mean_mode,
+                   int rs_iters, int rs_t, int rs_clamp, int rs_w)
+{
+    i64 n = rows * cols;
+    u64 *mu0 = A(rows), *mu1 = A(rows), *c0 = A(n), *c1 = A(n), *q0 = A(n), *q1 = A(n);
+    u64 *v0 = A(rows), *v1 = A(rows), *r0 = A(rows), *r1 = A(rows), *b0 = A(n), *b1 = A(n);
+    double inv_d = 1.0 / (double)cols;
+    for (i64 r = 0; r < rows; ++r) {
+        u64 a = 0, b = 0;
+        for (i64 j = 0; j < cols; ++j) { a += x0[r * cols + j]; b += x1[r * cols + j]; }
+        mu0[r] = a; mu1[r] = b;
+    }
+    if (mean_mode == 0) pmulF(mu0, mu1, rows, inv_d);
+    else divP(mu0, mu1, rows, cols);
+    for (i64 r = 0; r < rows; ++r)
+        for (i64 j = 0; j < cols; ++j) {
+            c0[r * cols + j] = x0[r * cols + j] - mu0[r];
+            c1[r * cols + j] = x1[r * cols + j] - mu1[r];
+        }
+    u64 Ue = (u64)(row_off * cols);
+    MT(ctx, n, Ue, c0, c1, c0, c1, q0, q1);
+    for (i64 r = 0; r < rows; ++r) {
+        u64 a = 0, b = 0;
+        for (i64 j = 0; j < cols; ++j) { a += q0[r * cols + j]; b += q1[r * cols + j]; }
+        v0[r] = a; v1[r] = b;
+    }
+    if (mean_mode == 0) pmulF(v0, v1, rows, inv_d);
+    else divP(v0, v1, rows, cols);
+    addP(v0, rows, eps);
+    RSQRT(ctx, rows, (u64)row_off, rs_iters, rs_t, rs_clamp, rs_w, v0, v1, r0, r1);
+    for (i64 r = 0; r < rows; ++r)
+        for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
+    MT(ctx, n, Ue, c0, c1, b0, b1, z0, z1);
+    free(mu0); free(mu1); free(c0); free(c1); free(q0); free(q1);
+    free(v0); free(v1); free(r0); free(r1); free(b0); free(b1);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Small-ring truncation statistics (acceptance 4): ring Z_2^N with    */
+/* N < 64, shares uniform in the ring, per-share arithmetic shift by k bits.  */
+/* Returns the number of trials whose reconstruction is not within            */
+/* {floor(x/2^k), floor(x/2^k) - 1} mod 2^N.  Uses its own PRG key stream.    */
+/* ------------------------------------------------------------------------ */
+i64 orc_trunc_wrap_trials(int N, int k, i64 x, i64 trials, u64 key)
+{
+    u64 mask = (N == 64) ? ~(u64)0 : (((u64)1 << N) - 1);
+    i64 bad = 0;
+    for (i64 t = 0; t < trials; ++t) {
+        u32 wd[4];
+        prg(key, (u64)t, 0, 0, wd);
+        u64 r = w64(wd[0], wd[1]) & mask;
+        u64 xv = (u64)x & mask;
+        u64 s0 = (xv - r) & mask, s1 = r;
+        /* signed interpretation of an N-bit share, then arithmetic shift */
+        i64 v0 = (i64)(s0 << (64 - N)) >> (64 - N);
+        i64 v1 = (i64)(s1 << (64 - N)) >> (64 - N);
+        u64 z = ((u64)(v0 >> k) + (u64)(v1 >> k)) & mask;
+        i64 zs = (i64)(z << (64 - N)) >> (64 - N);
+        i64 expect = x >> k;
+        if (!(zs == expect || zs == expect - 1)) ++bad;
+    }
+    return bad;
+}

@@ -1,0 +1,320 @@
+"""Pins for the oracle's approximation schedules (exp, reciprocal, rsqrt, segment
+polynomials, erf series, max / maxpool, softmax, layernorm).
+
+Tolerances are derived in DESIGN.md section 5 from the fixed-point arithmetic
+(ulp = 2^-16; each local truncation of a product errs by (-2, 0] ulp):
+  exp      |y - f| <= 4 * 2^t ulp * max(1, f)             (error doubles per squaring)
+  recip    |y - f| <= 4 ulp * (1 + 1/x)                    (NR fixed-point offset)
+  rsqrt    |y - f| <= 64 ulp * max(1, y) (3 iters), 16 ulp (10 iters)
+  Horner   |y - f| <= 2.5 ulp * sum_{k<d} |v|^k + 0.5 ulp |v|^d   (+2 ulp for |x|-form)
+Exact pins: t=0+clamp is ReLU(1+x) (R14); degree 0 is ReLU / unit step; outside the
+segment the output is x / 0 / 1 exactly; max and maxpool are exact; softmax output
+shares are bit-identical under a public shift of party 0's input shares.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import workloads
+from oracle import Oracle, encode, max_levels
+from oracle import float_ref as fr
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+COEFFS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)), "fixtures",
+                                     "coeffs.json")))["fits"]
+ULP = 2.0 ** -16
+M64 = (1 << 64) - 1
+
+
+def O(cfg=1, step=0):
+    return Oracle.for_cfg(workloads.keys(cfg), step)
+
+
+def dec(s):
+    return Oracle.open(*s)[1]
+
+
+def ring(s):
+    return Oracle.open(*s)[0].view(np.int64)
+
+
+# ------------------------------------------------------------------ exp ----
+@pytest.mark.parametrize("t,clamp", [(8, 0), (8, 1), (6, 0), (4, 0), (2, 1), (2, 0), (1, 0)])
+def test_exp_vs_formula(t, clamp):
+    o = O()
+    x = workloads.exp_inputs(4096, tail_frac=0.05 if clamp else 0.0)
+    s = o.share(x)
+    xd = dec(s)
+    y = dec(o.exp(s, t=t, clamp=clamp))
+    f = fr.exp_limit(xd, t, clamp)
+    m = np.ones_like(xd, bool) if clamp else xd >= -(2.0 ** t)
+    tol = 4 * 2 ** t * ULP * np.maximum(1.0, np.abs(f))
+    assert np.all(np.abs(y - f)[m] <= tol[m])
+    assert o.step == 1 + t + 2 * clamp
+
+
+def test_exp_t8_true_function_budget():
+    o = O()
+    x = np.linspace(-10, 0, 2001)
+    s = o.share(x)
+    y = dec(o.exp(s, t=8))
+    assert np.max(np.abs(y - np.exp(dec(s)))) <= 1.1e-3 + 4 * 256 * ULP
+
+
+def test_exp_golden_values():
+    g = GOLD["exp_t8_xm1"]
+    assert abs(fr.exp_limit(g["x"], g["t"]) - g["value"]) < 5e-8
+    o = O()
+    y = dec(o.exp(o.share([g["x"]]), t=g["t"]))[0]
+    assert abs(y - g["value"]) <= 4 * 256 * ULP
+    d = GOLD["exp_t8_xm600_diverges"]
+    assert abs(fr.exp_limit(d["x"], d["t"])) >= d["min_abs"]
+    yd = dec(o.exp(o.share([d["x"]]), t=d["t"]))[0]
+    assert abs(yd) > 1.0                  # unclamped: nowhere near e^-600 (wraps in the ring)
+    yc = dec(o.exp(o.share([d["x"]]), t=d["t"], clamp=1))[0]
+    assert abs(yc) <= 4 * 256 * ULP       # clamped: zero
+
+
+def test_exp_t0_clamp_is_relu_of_1_plus_x_exactly():
+    # reading R14: t=0+clamp = max(0, 1+x) (not 1+ReLU(x)); exact in the ring
+    o = O()
+    x = np.concatenate([np.linspace(-3, 3, 1201), [-1.0, -2.0, -0.5]])
+    s = o.share(x)
+    xr = ring(s)
+    y = ring(o.exp(s, t=0, clamp=1))
+    assert np.array_equal(y, np.maximum(0, xr + 65536))
+    assert list(dec(o.exp(o.share([-2.0, -1.0, -0.5]), t=0, clamp=1))) == [0.0, 0.0, 0.5]
+
+
+def test_exp_clamp_agrees_with_unclamped_above_minus_2t():
+    o = O()
+    x = np.linspace(-2.0 ** 4, 2, 999)
+    s = o.share(x)
+    a = dec(o.exp(s, t=4, clamp=0))
+    b = dec(o.exp(s, t=4, clamp=1))
+    assert np.max(np.abs(a - b)) <= 2 * 4 * 16 * ULP * max(1, np.exp(2))
+    # the plaintext formulas agree EXACTLY
+    assert np.array_equal(fr.exp_limit(x, 4, False), fr.exp_limit(x, 4, True))
+
+
+# ---------------------------------------------------------- reciprocal ----
+def test_recip_vs_formula_and_true():
+    o = O()
+    x = workloads.recip_inputs(4096)
+    s = o.share(x)
+    xd = dec(s)
+    y = dec(o.recip(s, iters=10, t=8))
+    f = fr.recip_nr(xd, 10, 8)
+    assert np.all(np.abs(y - f) <= 4 * ULP * (1 + 1 / xd))
+    assert np.max(np.abs(y * xd - 1)) <= 1e-2
+    assert o.step == 1 + 8 + 2 * 10
+
+
+def test_recip_golden_and_monotone():
+    g = GOLD["recip_1"]
+    for it in range(g["min_iters"], 13):
+        assert abs(fr.recip_nr(g["x"], it) - 1.0) <= g["tol"]
+    o = O()
+    assert abs(dec(o.recip(o.share([1.0]), iters=10))[0] - 1.0) <= 8 * ULP
+    # S:216 knob monotonicity at x = 3: error strictly larger at iters=1
+    assert abs(fr.recip_nr(3.0, 1) - 1 / 3) > abs(fr.recip_nr(3.0, 10) - 1 / 3)
+
+
+# --------------------------------------------------------------- rsqrt ----
+@pytest.mark.parametrize("iters,tol_ulp", [(3, 64), (10, 16)])
+def test_rsqrt_vs_formula(iters, tol_ulp):
+    o = O()
+    x = workloads.rsqrt_inputs(4096)
+    s = o.share(x)
+    xd = dec(s)
+    y = dec(o.rsqrt(s, iters=iters))
+    f = fr.rsqrt_nr(xd, iters)
+    assert np.all(np.abs(y - f) <= tol_ulp * ULP * np.maximum(1, f))
+    assert np.max(np.abs(y * np.sqrt(xd) - 1)) <= (2e-3 if iters == 3 else 2e-4) * 1.5
+
+
+def test_rsqrt_golden():
+    g = GOLD["rsqrt_4"]
+    assert abs(fr.rsqrt_nr(g["x"], g["iters"]) - g["value"]) <= g["tol"]
+    o = O()
+    assert abs(dec(o.rsqrt(o.share([g["x"]]), iters=g["iters"]))[0] - g["value"]) <= g["tol"]
+
+
+# -------------------------------------------------------- segment polys ----
+def horner_tol(v, d, abs_form=False):
+    v = np.abs(v)
+    t = 0.5 * v ** d + sum(2.5 * v ** k for k in range(d))
+    return (t + (2 if abs_form else 0) + 1) * ULP
+
+
+@pytest.mark.parametrize("fit", [f for f in COEFFS if f["form"] != "erf"],
+                         ids=lambda f: f"{f['op']}-{f['form']}-{f['degree']}")
+def test_poly_vs_formula_and_true(fit):
+    o = O()
+    B = fit["interval"][1]
+    x = workloads.act_inputs(4096)
+    s = o.share(x)
+    xd = dec(s)
+    y = dec(o.act(s, fit["op"], fit["form"], fit["degree"], B, fit["coefficients"]))
+    f = fr.act_formula(xd, fit["op"], fit["form"], fit["degree"], B, fit["coefficients"])
+    assert np.all(np.abs(y - f) <= horner_tol(xd, fit["degree"], fit["form"] == "poly_abs"))
+    true = fr.TRUE_ACT[fit["op"]](xd)
+    assert np.max(np.abs(y - true)) <= fit["max_abs_error"] + np.max(horner_tol(B, fit["degree"], True))
+    # outside [-B, B) the output is EXACT: x (or 1) above, 0 below
+    xr = ring(s)
+    yr = ring(o.act(s, fit["op"], fit["form"], fit["degree"], B, fit["coefficients"]))
+    hi, lo = xd >= B + 1e-3, xd < -B - 1e-3
+    top = 65536 if fit["op"] == "sigmoid" else xr[hi]
+    assert np.all(yr[hi] == top) and np.all(yr[lo] == 0)
+
+
+@pytest.mark.parametrize("K", [4, 6, 8])
+def test_erf_gelu(K):
+    o = O()
+    B = 2.5
+    x = workloads.act_inputs(4096)
+    s = o.share(x)
+    xd = dec(s)
+    y = dec(o.act(s, "gelu", "erf", 0 + 1, B, None, K))
+    f = fr.act_formula(xd, "gelu", "erf", 1, B, None, K)
+    z2 = np.minimum(xd * xd / 2, B * B / 2)
+    assert np.all(np.abs(y - f) <= horner_tol(z2, K - 1) * (1 + np.abs(xd)) + 8 * ULP)
+    fit = [f for f in COEFFS if f["form"] == "erf" and f["erf_terms"] == K][0]
+    assert np.max(np.abs(y - fr.gelu(xd))) <= fit["max_abs_error"] + np.max(
+        horner_tol(B * B / 2, K - 1) * (1 + B) + 8 * ULP)
+
+
+def test_degree0_is_relu_and_unit_step_exactly():
+    o = O()
+    x = np.concatenate([np.linspace(-4, 4, 801), [2.0, -3.0]])
+    s = o.share(x)
+    xr = ring(s)
+    for act in ("gelu", "silu"):
+        assert np.array_equal(ring(o.act(s, act, "poly_x", 0, 5.0, [0.0])), np.maximum(xr, 0))
+        assert np.array_equal(ring(o.act(s, act, "relu", 4, 5.0, [0.0])), np.maximum(xr, 0))
+    st = ring(o.act(s, "sigmoid", "poly_x", 0, 5.0, [0.0]))
+    assert np.array_equal(st, np.where(xr >= 0, 65536, 0))
+    assert dec(o.act(o.share([GOLD["gelu_deg0_2"]["x"]]), "gelu", "relu"))[0] == GOLD["gelu_deg0_2"]["value"]
+    assert dec(o.act(o.share([GOLD["sigmoid_deg0_m3"]["x"]]), "sigmoid", "relu"))[0] == GOLD["sigmoid_deg0_m3"]["value"]
+
+
+def test_act_step_counts():
+    o = O()
+    s = o.share(np.zeros(64))
+    st = o.step
+    o.act(s, "gelu", "poly_x", 4, 5.0, [0, 0, 0, 0, 0]); assert o.step - st == 2 + 3 + 2
+    st = o.step
+    o.act(s, "gelu", "poly_abs", 4, 3.0, [0, 0, 0, 0, 0]); assert o.step - st == 3 + 1 + 3 + 2
+    st = o.step
+    o.act(s, "sigmoid", "poly_x", 2, 5.0, [0, 0, 0]); assert o.step - st == 2 + 1 + 1
+    st = o.step
+    o.act(s, "gelu", "erf", 1, 2.5, None, 8); assert o.step - st == 2 + 1 + 6 + 1 + 1 + 2
+    st = o.step
+    o.act(s, "gelu", "relu", 0, 5.0, [0.0]); assert o.step - st == 2
+
+
+# ------------------------------------------------------------ max / pool ----
+def test_max_golden():
+    g = GOLD["max_3141"]
+    o = O()
+    s = o.share(g["x"])
+    st = o.step
+    z = o.max(s, 1, 4)
+    assert dec(z)[0] == g["max"]
+    assert o.step - st == 2 * g["levels"] and max_levels(4) == g["levels"]
+    assert max_levels(GOLD["max_n8"]["n"]) == GOLD["max_n8"]["levels"]
+    assert max_levels(1) == 0
+
+
+@pytest.mark.parametrize("cols", [1, 2, 3, 5, 9, 31, 128, 200])
+def test_max_exact(cols):
+    rows = 64
+    o = O(2)
+    x = workloads.softmax_inputs(rows, cols)
+    s = o.share(x)
+    z = o.max(s, rows, cols, row_off=32)
+    assert np.array_equal(ring(z), ring(s).reshape(rows, cols).max(axis=1))
+
+
+def test_maxpool_exact():
+    N, C, H, W = 2, 3, 9, 10
+    o = O(4)
+    x = workloads.maxpool_inputs((N, C, H, W)) - 0.3    # include negatives too
+    s = o.share(x)
+    xr = ring(s).reshape(N, C, H, W)
+    z = ring(o.maxpool2d(s, N, C, H, W, 3, 2, 1))
+    Ho, Wo = (H + 2 - 3) // 2 + 1, (W + 2 - 3) // 2 + 1
+    pad = np.zeros((N, C, H + 2, W + 2), np.int64)
+    pad[:, :, 1:-1, 1:-1] = xr
+    ref = np.full((N, C, Ho, Wo), np.iinfo(np.int64).min)
+    for dy in range(3):
+        for dx in range(3):
+            ref = np.maximum(ref, pad[:, :, dy:dy + 2 * Ho:2, dx:dx + 2 * Wo:2])
+    assert np.array_equal(z.reshape(N, C, Ho, Wo), ref)
+
+
+# -------------------------------------------------------------- softmax ----
+def test_softmax_golden():
+    g = GOLD["softmax_00"]
+    o = O(2)
+    y = dec(o.softmax(o.share(g["x"]), 1, 2))
+    assert np.max(np.abs(y - g["out"])) <= 1e-2
+
+
+@pytest.mark.parametrize("rows,cols,tol_true", [(64, 128, 1.1e-2), (32, 1024, 2.35e-2), (40, 77, 1.1e-2)])
+def test_softmax_vs_formula_and_true(rows, cols, tol_true):
+    o = O(2)
+    x = workloads.softmax_inputs(rows, cols)
+    s = o.share(x)
+    xd = dec(s).reshape(rows, cols)
+    y = dec(o.softmax(s, rows, cols)).reshape(rows, cols)
+    assert np.max(np.abs(y - fr.softmax_formula(xd))) <= 2 * 4 * 256 * ULP + 8 * ULP
+    assert np.max(np.abs(y - fr.softmax(xd))) <= tol_true
+    assert np.max(np.abs(y.sum(1) - 1)) <= 3e-2
+
+
+def test_softmax_shift_invariance_bit_identical():
+    rows, cols = 32, 64
+    o = O(2)
+    s = o.share(workloads.softmax_inputs(rows, cols))
+    a = O(2, 100).softmax(s, rows, cols)
+    c = np.uint64(encode(3.25))
+    b = O(2, 100).softmax((s[0] + c, s[1]), rows, cols)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_softmax_clamped_variant():
+    rows, cols = 32, 128
+    o = O(2)
+    x = workloads.softmax_inputs(rows, cols, spike=True)
+    s = o.share(x)
+    y = dec(o.softmax(s, rows, cols, exp_t=8, exp_clamp=1)).reshape(rows, cols)
+    assert np.max(np.abs(y - fr.softmax(dec(s).reshape(rows, cols)))) <= 1.1e-2
+
+
+# ------------------------------------------------------------ layernorm ----
+@pytest.mark.parametrize("mean_mode,iters", [(0, 3), (1, 3), (1, 10)])
+def test_layernorm(mean_mode, iters):
+    rows, cols = 64, 768
+    o = O(5)
+    s = o.share(workloads.layernorm_inputs(rows, cols))
+    xd = dec(s).reshape(rows, cols)
+    y = dec(o.layernorm(s, rows, cols, mean_mode=mean_mode, rsqrt_iters=iters)).reshape(rows, cols)
+    f = fr.layernorm_formula(xd, iters=iters, mean_mode=mean_mode)
+    assert np.max(np.abs(y - f)) <= 2e-3
+    # vs true: mode 0 carries E(1/768)'s -0.39% scale (R25); 3 NR iterations leave 2e-3 rel.
+    tol_true = 1.3e-2 if mean_mode == 0 else (8e-3 if iters == 3 else 1e-3)
+    assert np.max(np.abs(y - fr.layernorm(xd))) <= tol_true
+
+
+def test_layernorm_constant_row():
+    # constant row -> ~0 (exact division by d, mean_mode=1; or d a power of two)
+    o = O(5)
+    x = np.tile(np.array([[0.75], [-1.25], [3.0]]), (1, 768))
+    y = dec(o.layernorm(o.share(x), 3, 768, mean_mode=1))
+    assert np.max(np.abs(y)) <= 1e-3
+    x2 = np.tile(np.array([[0.75], [-1.25]]), (1, 256))
+    y2 = dec(o.layernorm(o.share(x2), 2, 256, mean_mode=0))
+    assert np.max(np.abs(y2)) <= 1e-3
