@@ -1,0 +1,202 @@
+/*
+ * mpc200.h -- C ABI of the B200-native two-party nonlinear-operator library.
+ *
+ * Method: arxiv 2511.19711 (CrypTorch / CrypTen++), the approximated nonlinear
+ * operators its characterization finds dominant, over
+ * 2-party additive secret shares in Z_2^64 with 16 fractional bits,
+ * trusted-dealer Beaver triples, local truncation and a
+ * GMW comparison.  The bit-exact contract every entry point
+ * implements is DESIGN.md section 2 (PRG layout 2.3, schedules 2.5).
+ *
+ * Conventions for every compute entry point:
+ *  - All data pointers are DEVICE pointers on the context's device, owned and
+ *    allocated by the caller; the library never frees caller memory.  Shares are
+ *    uint64_t arrays (ring elements of Z_2^64), 8-byte aligned, dense, row-major.
+ *  - mpc_shares carries one pointer per party.  MPC_MODE_BOTH (one GPU holds
+ *    both parties) needs sh[0] and sh[1]; a PAIR mode needs sh[party] only.
+ *  - Every call is ASYNCHRONOUS on the context's CUDA stream (cudaStream_t passed
+ *    as void*); results are valid after the stream is synchronized.
+ *  - `off` / `row_off` is the global index of this shard's first element / row:
+ *    the PRG is keyed by global unit, so shards reproduce the unsharded shares.
+ *    Ops that contain a comparison need off (and row_off * per-row units)
+ *    divisible by 32 (MPC_ERR_INVALID otherwise).
+ *  - In-place operation (z == x) is allowed for element-wise ops and softmax.
+ *  - Each randomness-consuming primitive advances the context's step counter by
+ *    one; the step counts of every op are listed below.
+ *  - Errors: the call returns a status and leaves the step counter unchanged;
+ *    mpc_last_error() gives a message.  CUDA launch errors surface as
+ *    MPC_ERR_CUDA at the call (or, for asynchronous faults, at the next call).
+ */
+#ifndef MPC200_H
+#define MPC200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MPC_OK = 0,
+    MPC_ERR_INVALID = 1,   /* null / misaligned pointer, bad shape, bad mode      */
+    MPC_ERR_RANGE = 2,     /* knob out of range, step counter exhausted (2^32)    */
+    MPC_ERR_CUDA = 3,      /* CUDA runtime or launch failure                       */
+    MPC_ERR_NCCL = 4,      /* exchange failure in a PAIR mode                      */
+    MPC_ERR_PROTOCOL = 5,  /* parties disagree on the op header (debug mode)      */
+    MPC_ERR_REUSE = 6,     /* set_step below the current step (triple reuse)      */
+    MPC_ERR_TIMEOUT = 7,
+    MPC_ERR_NOMEM = 8,
+    MPC_ERR_UNSUPPORTED = 9
+} mpc_status;
+
+typedef enum {
+    MPC_MODE_BOTH = 0,       /* one GPU simulates both parties; openings add in registers */
+    MPC_MODE_PAIR_HOST = 1   /* one GPU per party; openings exchanged between rounds      */
+} mpc_mode;
+
+typedef struct {
+    int mode;               /* mpc_mode                                              */
+    int party;              /* 0 | 1 (ignored in MPC_MODE_BOTH)                       */
+    int frac_bits;          /* must be 16                                    */
+    int device;             /* CUDA device ordinal                                    */
+    uint64_t key_share;     /* K_s: pairwise share-mask key          */
+    uint64_t key_p0;        /* K_0: dealer -> party 0 key                             */
+    uint64_t key_p1;        /* K_1: dealer -> party 1 key                             */
+    void* cuda_stream;      /* cudaStream_t the calls are enqueued on (NULL = legacy) */
+    void* exchange;         /* PAIR modes: an mpc_exchange (see mpc200_pair.h); else NULL */
+} mpc_config;
+
+typedef struct mpc_ctx mpc_ctx;
+
+typedef struct { uint64_t* sh[2]; } mpc_shares;
+
+typedef struct {
+    uint64_t steps;          /* step ids consumed                                        */
+    uint64_t philox_calls;   /* Philox4x32-10 blocks generated (algorithmic count)        */
+    uint64_t bytes_per_party;/* bytes each party sends in a PAIR execution (model; 2.4)   */
+    uint64_t rounds;         /* communication rounds                                     */
+    uint64_t launches;       /* kernels launched                                         */
+    uint64_t calls;          /* ABI calls                                                */
+} mpc_stats;
+
+/* ---- context -------------------------------------------------------------- */
+mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out);
+mpc_status mpc_ctx_destroy(mpc_ctx* ctx);
+/* Replay support: set the next step id.  Below the current step -> MPC_ERR_REUSE
+ * unless force != 0 (the triple-reuse analogue of S:440). */
+mpc_status mpc_ctx_set_step(mpc_ctx* ctx, uint64_t step, int force);
+uint64_t   mpc_ctx_get_step(const mpc_ctx* ctx);
+mpc_status mpc_ctx_set_stream(mpc_ctx* ctx, void* cuda_stream);
+mpc_status mpc_ctx_stats(const mpc_ctx* ctx, mpc_stats* out);
+mpc_status mpc_ctx_reset_stats(mpc_ctx* ctx);
+const char* mpc_last_error(const mpc_ctx* ctx);
+const char* mpc_version(void);
+/* Philox4x32-10 blocks generated per element by each op (algorithmic),
+ * used for the ALU roofline.  Returns the count for the last call on ctx. */
+uint64_t mpc_last_call_philox(const mpc_ctx* ctx);
+
+/* Per-launch timing (for the roofline in bench.py): when enabled, every kernel the
+ * context launches is bracketed by CUDA events on the context stream and tagged with
+ * its algorithmic Philox4x32-10 block count.  mpc_ctx_kernel_times synchronizes on
+ * the last event, copies up to cap records (oldest first), clears the list and
+ * returns the number copied (-1 on a null ctx). */
+typedef struct { const char* name; float ms; uint64_t philox; uint64_t units; } mpc_kernel_time;
+mpc_status mpc_ctx_enable_kernel_timing(mpc_ctx* ctx, int on);
+int        mpc_ctx_kernel_times(mpc_ctx* ctx, mpc_kernel_time* out, int cap);
+
+/* ---- S3: the device PRG itself (known-answer tests, rate microbenchmark) ----
+ * out[4*i .. 4*i+3] = Philox4x32-10(key, ctr = (lo32(unit0+i), hi32(unit0+i), step, slot))
+ * for i < n.  `reps` > 1 chains the counter through the generator reps times
+ * (out = the last block) to measure the generator rate without memory traffic. */
+mpc_status mpc_prg_fill(mpc_ctx* ctx, uint64_t key, uint64_t unit0, uint32_t step, uint32_t slot,
+                        uint32_t* out, int64_t n, int reps);
+
+/* ---- S1 / S2 ---------------------------------------------------------------- */
+/* S1 share: v = E(x) = round-half-even(x * 2^16) (|x| < 2^31);
+ * owner's share = v - r, the other party's = r, r = PRG(K_s, off+i, step, 0).
+ * x: device float (x_is_f64 = 0) or double (1) array of n; 1 step. */
+mpc_status mpc_share(mpc_ctx* ctx, const void* x, int x_is_f64, int owner, mpc_shares out,
+                     int64_t n, int64_t off);
+/* S2 open: ring_out[i] = x0+x1 mod 2^64 (may be NULL);
+ * f64_out[i] = (int64)ring / 2^scale_bits (may be NULL).  No step. */
+mpc_status mpc_open(mpc_ctx* ctx, mpc_shares in, int64_t n, uint64_t* ring_out,
+                    double* f64_out, int scale_bits);
+
+/* ---- S4 / S5 ---------------------------------------------------------------- */
+/* S4 Beaver multiply: z = x*y mod 2^64, then per-share
+ * arithmetic shift by trunc_bits (0 or 16).  1 step, 1 round, 16 B/elem/party. */
+mpc_status mpc_mul(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z, int64_t n,
+                   int64_t off, int trunc_bits);
+/* S5 local truncation: z_i = (int64)x_i >> bits, bits in [0,63].
+ * No step, no communication. */
+mpc_status mpc_trunc(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int bits);
+
+/* ---- S7 / S8 ---------------------------------------------------------------- */
+/* S7 comparison: z = [x < 0] as a scale-1 arithmetic
+ * sharing; exactly bit (window-1) of rec(x), so correct for rec(x) in
+ * [-2^(window-1), 2^(window-1)) (HummingBird window).  window in [1,64].
+ * 1 step; 2 + ceil(log2(window-1)) rounds. */
+mpc_status mpc_cmp(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off, int window);
+/* S8 ReLU: z = BM(x, 1 - ltz(x)), exact (no truncation).  2 steps. */
+mpc_status mpc_relu(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off, int window);
+
+/* ---- S10 - S13 ------------------------------------------------------------------ */
+typedef struct { int t; int clamp; int window; } mpc_exp_p;  /* t in [0,8] */
+typedef struct { int iters; mpc_exp_p exp; } mpc_nr_p;       /* iters in [1,12]          */
+
+/* S10 exp-limit: (1 + x/2^t)^(2^t), zeroed below -2^t when clamp.
+ * Steps t + 2*clamp. */
+mpc_status mpc_exp(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off,
+                   const mpc_exp_p* p);
+/* S11 Newton-Raphson reciprocal. Steps exp + 2*iters. */
+mpc_status mpc_recip(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off,
+                     const mpc_nr_p* p);
+/* S12 Newton-Raphson inverse square root. Steps exp + 3*iters. */
+mpc_status mpc_rsqrt(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off,
+                     const mpc_nr_p* p);
+
+typedef enum { MPC_FORM_POLY_X = 0, MPC_FORM_POLY_ABS = 1, MPC_FORM_RELU = 2, MPC_FORM_ERF = 3 } mpc_act_form;
+/* The segment table of S13: inside [-B, B) the value is
+ * the form's polynomial, outside its asymptote.  coeffs: HOST array of degree+1
+ * doubles, low -> high (POLY_X / POLY_ABS); erf_terms K in [2,12] for ERF. */
+typedef struct {
+    int form; int degree; double B; const double* coeffs; int erf_terms; int window;
+} mpc_act_p;
+/* S13 GELU: POLY_X steps 2+(d-1)+2, POLY_ABS 3+1+(d-1)+2, ERF 2+1+(K-2)+1+1+2,
+ * RELU or degree 0: 2. */
+mpc_status mpc_gelu(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off,
+                    const mpc_act_p* p);
+/* S13 SiLU: forms POLY_X, POLY_ABS, RELU. */
+mpc_status mpc_silu(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off,
+                    const mpc_act_p* p);
+/* S13 Sigmoid: forms POLY_X, RELU (unit step); tail is the public 1 (R30). */
+mpc_status mpc_sigmoid(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off,
+                       const mpc_act_p* p);
+
+/* ---- S9 ---------------------------------------------------------------------------- */
+/* S9 row max: x is rows x cols, z is rows; exact.
+ * 2 * ceil(log2(cols)) steps. */
+mpc_status mpc_max(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols,
+                   int64_t row_off, int window);
+/* S9 MaxPool2d over NCHW (public zero padding, R26); z is N x C x Ho x Wo.
+ * img_off = global index of the first image.  2 * ceil(log2(k*k)) steps. */
+mpc_status mpc_maxpool2d(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int N, int C, int H, int W,
+                         int k, int stride, int pad, int64_t img_off, int window);
+
+/* ---- S14 / S15 ---------------------------------------------------------------------- */
+typedef struct { int window; mpc_exp_p exp; mpc_nr_p recip; } mpc_softmax_p;
+/* S14 softmax over rows (P:604 footnote).  Steps: 2*levels(cols) + exp +
+ * recip + 1.  The library allocates row scratch on the context's device. */
+mpc_status mpc_softmax(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols,
+                       int64_t row_off, const mpc_softmax_p* p);
+typedef struct { double eps; int mean_mode; mpc_nr_p rsqrt; } mpc_ln_p;
+/* S15 layernorm over rows, without the public affine.
+ * mean_mode 0: x E(1/d) (SPEC); 1: per-share floor division by d (R25).
+ * Steps 1 + rsqrt + 1. */
+mpc_status mpc_layernorm(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols,
+                         int64_t row_off, const mpc_ln_p* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPC200_H */

@@ -1,0 +1,347 @@
+"""Thin ctypes binding of include/mpc200.h (argument marshalling only).
+
+Every compute step runs in libmpc200.so's CUDA kernels; this module only passes
+torch tensor device pointers, the current CUDA stream and knob structs.  There is
+no CPU fallback: importing fails loudly if the shared library is missing.
+Names follow the C ABI (mpc_share, mpc_open, mpc_mul, ...), exposed as methods of
+`Ctx` without the prefix.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmpc200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libmpc200.so not found at {LIB_PATH}: run `python paper_2511_19711_b200/build.py` "
+                      "(there is no CPU fallback)")
+_L = ctypes.CDLL(LIB_PATH)
+
+u64 = ctypes.c_uint64
+i64 = ctypes.c_int64
+INT = ctypes.c_int
+VP = ctypes.c_void_p
+
+MODE_BOTH, MODE_PAIR_HOST = 0, 1
+FORM = {"poly_x": 0, "poly_abs": 1, "relu": 2, "erf": 3}
+STATUS = {0: "OK", 1: "INVALID", 2: "RANGE", 3: "CUDA", 4: "NCCL", 5: "PROTOCOL", 6: "REUSE",
+          7: "TIMEOUT", 8: "NOMEM", 9: "UNSUPPORTED"}
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("mode", INT), ("party", INT), ("frac_bits", INT), ("device", INT),
+                ("key_share", u64), ("key_p0", u64), ("key_p1", u64),
+                ("cuda_stream", VP), ("exchange", VP)]
+
+
+class Shares(ctypes.Structure):
+    _fields_ = [("sh", VP * 2)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("steps", u64), ("philox_calls", u64), ("bytes_per_party", u64), ("rounds", u64),
+                ("launches", u64), ("calls", u64)]
+
+
+class KernelTime(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("ms", ctypes.c_float), ("philox", u64), ("units", u64)]
+
+
+class ExpP(ctypes.Structure):
+    _fields_ = [("t", INT), ("clamp", INT), ("window", INT)]
+
+
+class NrP(ctypes.Structure):
+    _fields_ = [("iters", INT), ("exp", ExpP)]
+
+
+class ActP(ctypes.Structure):
+    _fields_ = [("form", INT), ("degree", INT), ("B", ctypes.c_double),
+                ("coeffs", ctypes.POINTER(ctypes.c_double)), ("erf_terms", INT), ("window", INT)]
+
+
+class SoftmaxP(ctypes.Structure):
+    _fields_ = [("window", INT), ("exp", ExpP), ("recip", NrP)]
+
+
+class LnP(ctypes.Structure):
+    _fields_ = [("eps", ctypes.c_double), ("mean_mode", INT), ("rsqrt", NrP)]
+
+
+C = ctypes.POINTER
+_SIGS = {
+    "mpc_ctx_create": [C(Config), C(VP)],
+    "mpc_ctx_destroy": [VP],
+    "mpc_ctx_set_step": [VP, u64, INT],
+    "mpc_ctx_get_step": [VP],
+    "mpc_ctx_set_stream": [VP, VP],
+    "mpc_ctx_stats": [VP, C(Stats)],
+    "mpc_ctx_reset_stats": [VP],
+    "mpc_last_error": [VP],
+    "mpc_version": [],
+    "mpc_last_call_philox": [VP],
+    "mpc_ctx_enable_kernel_timing": [VP, INT],
+    "mpc_ctx_kernel_times": [VP, VP, INT],
+    "mpc_prg_fill": [VP, u64, u64, ctypes.c_uint32, ctypes.c_uint32, VP, i64, INT],
+    "mpc_share": [VP, VP, INT, INT, Shares, i64, i64],
+    "mpc_open": [VP, Shares, i64, VP, VP, INT],
+    "mpc_mul": [VP, Shares, Shares, Shares, i64, i64, INT],
+    "mpc_trunc": [VP, Shares, Shares, i64, INT],
+    "mpc_cmp": [VP, Shares, Shares, i64, i64, INT],
+    "mpc_relu": [VP, Shares, Shares, i64, i64, INT],
+    "mpc_exp": [VP, Shares, Shares, i64, i64, C(ExpP)],
+    "mpc_recip": [VP, Shares, Shares, i64, i64, C(NrP)],
+    "mpc_rsqrt": [VP, Shares, Shares, i64, i64, C(NrP)],
+    "mpc_gelu": [VP, Shares, Shares, i64, i64, C(ActP)],
+    "mpc_silu": [VP, Shares, Shares, i64, i64, C(ActP)],
+    "mpc_sigmoid": [VP, Shares, Shares, i64, i64, C(ActP)],
+    "mpc_max": [VP, Shares, Shares, i64, i64, i64, INT],
+    "mpc_maxpool2d": [VP, Shares, Shares, INT, INT, INT, INT, INT, INT, INT, i64, INT],
+    "mpc_softmax": [VP, Shares, Shares, i64, i64, i64, C(SoftmaxP)],
+    "mpc_layernorm": [VP, Shares, Shares, i64, i64, i64, C(LnP)],
+}
+_RESTYPE = {"mpc_ctx_get_step": u64, "mpc_last_error": ctypes.c_char_p, "mpc_version": ctypes.c_char_p,
+            "mpc_last_call_philox": u64}
+for _n, _a in _SIGS.items():
+    _f = getattr(_L, _n)
+    _f.argtypes = _a
+    _f.restype = _RESTYPE.get(_n, INT)
+
+EXPORTS = sorted(_SIGS)
+
+
+def version() -> str:
+    return _L.mpc_version().decode()
+
+
+def load_coeffs():
+    path = os.path.join(os.path.dirname(_PKG), "fixtures", "coeffs.json")
+    return json.load(open(path))["fits"]
+
+
+def default_act(act="gelu", form="poly_x", degree=4, erf_terms=8, window=33, B=None, coeffs=None):
+    """Knob struct for S13 using fixtures/coeffs.json (SPEC S:239 least-squares fits)."""
+    if form == "erf":
+        return dict(form="erf", degree=0, B=2.5 if B is None else B, coeffs=None, erf_terms=erf_terms,
+                    window=window)
+    if form == "relu" or degree == 0:
+        return dict(form=form, degree=0, B=5.0 if B is None else B, coeffs=None, erf_terms=0, window=window)
+    if coeffs is None:
+        fit = [f for f in load_coeffs() if f["op"] == act and f["form"] == form and f.get("degree") == degree]
+        if not fit:
+            raise ValueError(f"no fitted coefficients for {act}/{form}/deg {degree}")
+        coeffs, B = fit[0]["coefficients"], fit[0]["interval"][1]
+    return dict(form=form, degree=degree, B=B, coeffs=list(coeffs), erf_terms=0, window=window)
+
+
+class MPCError(RuntimeError):
+    pass
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("mpc200 compute calls take CUDA tensors")
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return t.data_ptr()
+
+
+def _sh(pair):
+    s = Shares()
+    s.sh[0] = _ptr(pair[0]) if pair[0] is not None else None
+    s.sh[1] = _ptr(pair[1]) if pair[1] is not None else None
+    return s
+
+
+class Ctx:
+    """An mpc_ctx: keys, step counter, stream.  MODE_BOTH holds both parties on one GPU."""
+
+    def __init__(self, key_share: int, key_p0: int, key_p1: int, device: int = 0, mode: int = MODE_BOTH,
+                 party: int = 0, exchange: int | None = None):
+        self.device = torch.device("cuda", device)
+        self.mode, self.party = mode, party
+        cfg = Config(mode, party, 16, device, key_share, key_p0, key_p1, None, exchange)
+        h = VP()
+        st = _L.mpc_ctx_create(ctypes.byref(cfg), ctypes.byref(h))
+        if st != 0:
+            raise MPCError(f"mpc_ctx_create: {STATUS.get(st, st)}")
+        self._h = h
+
+    @classmethod
+    def for_cfg(cls, keys: dict, device: int = 0, **kw):
+        return cls(keys["key_share"], keys["key_p0"], keys["key_p1"], device, **kw)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _L.mpc_ctx_destroy(h)
+            self._h = None
+
+    # ---- bookkeeping ----
+    def _chk(self, st, name):
+        if st != 0:
+            raise MPCError(f"{name}: {STATUS.get(st, st)}: {_L.mpc_last_error(self._h).decode()}")
+
+    def _stream(self):
+        _L.mpc_ctx_set_stream(self._h, torch.cuda.current_stream(self.device).cuda_stream)
+
+    @property
+    def step(self) -> int:
+        return int(_L.mpc_ctx_get_step(self._h))
+
+    def set_step(self, step: int, force: bool = False):
+        self._chk(_L.mpc_ctx_set_step(self._h, step, int(force)), "mpc_ctx_set_step")
+
+    def stats(self) -> dict:
+        s = Stats()
+        self._chk(_L.mpc_ctx_stats(self._h, ctypes.byref(s)), "mpc_ctx_stats")
+        return {k: int(getattr(s, k)) for k, _ in Stats._fields_}
+
+    def reset_stats(self):
+        _L.mpc_ctx_reset_stats(self._h)
+
+    def enable_kernel_timing(self, on: bool = True):
+        self._chk(_L.mpc_ctx_enable_kernel_timing(self._h, int(on)), "mpc_ctx_enable_kernel_timing")
+
+    def kernel_times(self, cap: int = 65536):
+        """Drain per-launch records: list of (name, ms, philox_blocks, units)."""
+        buf = (KernelTime * cap)()
+        n = _L.mpc_ctx_kernel_times(self._h, ctypes.cast(buf, VP), cap)
+        return [(buf[i].name.decode(), float(buf[i].ms), int(buf[i].philox), int(buf[i].units))
+                for i in range(max(n, 0))]
+
+    def last_call_philox(self) -> int:
+        return int(_L.mpc_last_call_philox(self._h))
+
+    def _empty(self, n):
+        mk = lambda: torch.empty(n, dtype=torch.uint64, device=self.device)  # noqa: E731
+        if self.mode == MODE_BOTH:
+            return (mk(), mk())
+        return (mk(), None) if self.party == 0 else (None, mk())
+
+    # ---- S3 ----
+    def prg_fill(self, key: int, unit0: int, step: int, slot: int, n: int, reps: int = 1):
+        out = torch.empty(4 * n, dtype=torch.int32, device=self.device)
+        self._stream()
+        self._chk(_L.mpc_prg_fill(self._h, key, unit0, step, slot, out.data_ptr(), n, reps), "mpc_prg_fill")
+        return out
+
+    # ---- S1 / S2 ----
+    def share(self, x: torch.Tensor | None, owner: int = 0, off: int = 0, n: int | None = None):
+        if x is not None:
+            if x.dtype not in (torch.float32, torch.float64):
+                raise ValueError("share takes float32 / float64")
+            x = x.contiguous().view(-1)
+            n = x.numel()
+        z = self._empty(n)
+        self._stream()
+        self._chk(_L.mpc_share(self._h, _ptr(x) if x is not None else None,
+                               int(x is not None and x.dtype == torch.float64), owner, _sh(z), n, off),
+                  "mpc_share")
+        return z
+
+    def open(self, s, scale_bits: int = 16, want_ring=True, want_f64=True):
+        n = (s[0] if s[0] is not None else s[1]).numel()
+        ring = torch.empty(n, dtype=torch.uint64, device=self.device) if want_ring else None
+        f = torch.empty(n, dtype=torch.float64, device=self.device) if want_f64 else None
+        self._stream()
+        self._chk(_L.mpc_open(self._h, _sh(s), n, _ptr(ring), _ptr(f), scale_bits), "mpc_open")
+        return ring, f
+
+    # ---- S4 / S5 ----
+    def mul(self, x, y, off=0, trunc_bits=0, out=None):
+        n = x[0].numel() if x[0] is not None else x[1].numel()
+        z = out if out is not None else self._empty(n)
+        self._stream()
+        self._chk(_L.mpc_mul(self._h, _sh(x), _sh(y), _sh(z), n, off, trunc_bits), "mpc_mul")
+        return z
+
+    def trunc(self, x, bits=16, out=None):
+        n = x[0].numel() if x[0] is not None else x[1].numel()
+        z = out if out is not None else self._empty(n)
+        self._stream()
+        self._chk(_L.mpc_trunc(self._h, _sh(x), _sh(z), n, bits), "mpc_trunc")
+        return z
+
+    # ---- element-wise ops ----
+    def _un(self, fn, name, x, out, *args):
+        n = x[0].numel() if x[0] is not None else x[1].numel()
+        z = out if out is not None else self._empty(n)
+        self._stream()
+        self._chk(fn(self._h, _sh(x), _sh(z), n, *args), name)
+        return z
+
+    def cmp(self, x, off=0, window=33, out=None):
+        return self._un(_L.mpc_cmp, "mpc_cmp", x, out, off, window)
+
+    def relu(self, x, off=0, window=33, out=None):
+        return self._un(_L.mpc_relu, "mpc_relu", x, out, off, window)
+
+    def exp(self, x, off=0, t=8, clamp=0, window=33, out=None):
+        return self._un(_L.mpc_exp, "mpc_exp", x, out, off, ctypes.byref(ExpP(t, int(clamp), window)))
+
+    def recip(self, x, off=0, iters=10, t=8, clamp=0, window=33, out=None):
+        p = NrP(iters, ExpP(t, int(clamp), window))
+        return self._un(_L.mpc_recip, "mpc_recip", x, out, off, ctypes.byref(p))
+
+    def rsqrt(self, x, off=0, iters=3, t=8, clamp=0, window=33, out=None):
+        p = NrP(iters, ExpP(t, int(clamp), window))
+        return self._un(_L.mpc_rsqrt, "mpc_rsqrt", x, out, off, ctypes.byref(p))
+
+    def _act(self, fn, name, x, off, knobs, out):
+        k = dict(knobs)
+        coeffs = k.get("coeffs")
+        arr = (ctypes.c_double * len(coeffs))(*coeffs) if coeffs else None
+        p = ActP(FORM[k["form"]], int(k.get("degree", 0)), float(k.get("B", 5.0)),
+                 ctypes.cast(arr, ctypes.POINTER(ctypes.c_double)) if arr is not None else None,
+                 int(k.get("erf_terms", 0)), int(k.get("window", 33)))
+        return self._un(fn, name, x, out, off, ctypes.byref(p))
+
+    def gelu(self, x, off=0, out=None, **knobs):
+        return self._act(_L.mpc_gelu, "mpc_gelu", x, off, default_act("gelu", **knobs), out)
+
+    def silu(self, x, off=0, out=None, **knobs):
+        return self._act(_L.mpc_silu, "mpc_silu", x, off, default_act("silu", **knobs), out)
+
+    def sigmoid(self, x, off=0, out=None, **knobs):
+        return self._act(_L.mpc_sigmoid, "mpc_sigmoid", x, off, default_act("sigmoid", **knobs), out)
+
+    # ---- row ops ----
+    def max(self, x, rows, cols, row_off=0, window=33, out=None):
+        z = out if out is not None else self._empty(rows)
+        self._stream()
+        self._chk(_L.mpc_max(self._h, _sh(x), _sh(z), rows, cols, row_off, window), "mpc_max")
+        return z
+
+    def maxpool2d(self, x, N, C, H, W, k=3, stride=2, pad=1, img_off=0, window=33, out=None):
+        Ho, Wo = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+        z = out if out is not None else self._empty(N * C * Ho * Wo)
+        self._stream()
+        self._chk(_L.mpc_maxpool2d(self._h, _sh(x), _sh(z), N, C, H, W, k, stride, pad, img_off, window),
+                  "mpc_maxpool2d")
+        return z
+
+    def softmax(self, x, rows, cols, row_off=0, window=33, exp_t=8, exp_clamp=0, exp_window=33,
+                recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, out=None):
+        p = SoftmaxP(window, ExpP(exp_t, int(exp_clamp), exp_window),
+                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window)))
+        z = out if out is not None else self._empty(rows * cols)
+        self._stream()
+        self._chk(_L.mpc_softmax(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)), "mpc_softmax")
+        return z
+
+    def layernorm(self, x, rows, cols, row_off=0, eps=1e-5, mean_mode=0, rsqrt_iters=3, rsqrt_t=8,
+                  rsqrt_clamp=0, rsqrt_window=33, out=None):
+        p = LnP(eps, mean_mode, NrP(rsqrt_iters, ExpP(rsqrt_t, int(rsqrt_clamp), rsqrt_window)))
+        z = out if out is not None else self._empty(rows * cols)
+        self._stream()
+        self._chk(_L.mpc_layernorm(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)),
+                  "mpc_layernorm")
+        return z

@@ -1,0 +1,84 @@
+// dev_common.cuh -- L0 device primitives for sm_100a: Philox4x32-10, ring helpers,
+// warp bit-plane transpose.  (DESIGN.md 2.1 / 2.3.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mpc {
+
+typedef uint64_t u64;
+typedef int64_t i64;
+typedef unsigned int u32;
+
+constexpr u32 FULL = 0xffffffffu;
+constexpr int FRAC = 16;
+
+// A 64-bit Philox key split into (lo32, hi32).
+struct Key { u32 lo, hi; };
+
+struct Keys {
+    Key ks, k0, k1;   // K_s, K_0, K_1
+};
+
+// Philox4x32-10 (Salmon et al. SC'11).  Counter (c0..c3), key (k0, k1); the key is
+// bumped by the Weyl constants before every round but the first.  The multiplies
+// are 32x32->64 (IMAD.WIDE.U32); keys are warp-uniform so the key schedule lives
+// in uniform registers.
+__device__ __forceinline__ uint4 philox(Key key, u32 c0, u32 c1, u32 c2, u32 c3)
+{
+    u32 k0 = key.lo, k1 = key.hi;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const u64 p0 = (u64)0xD2511F53u * (u64)c0;
+        const u64 p1 = (u64)0xCD9E8D57u * (u64)c2;
+        const u32 n0 = (u32)(p1 >> 32) ^ c1 ^ k0;
+        const u32 n2 = (u32)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (u32)p1;
+        c3 = (u32)p0;
+        c0 = n0;
+        c2 = n2;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+// PRG(K, unit, step, slot) of DESIGN.md 2.3.
+__device__ __forceinline__ uint4 prg(Key key, u64 unit, u32 step, u32 slot)
+{
+    return philox(key, (u32)unit, (u32)(unit >> 32), step, slot);
+}
+
+__device__ __forceinline__ u64 w64(u32 lo, u32 hi) { return (u64)lo | ((u64)hi << 32); }
+
+// per-share arithmetic shift (local truncation)
+__device__ __forceinline__ u64 shr(u64 v, int k) { return (u64)(((i64)v) >> k); }
+
+// LTZ gate slot
+__device__ __forceinline__ u32 ltz_slot(int lv, int j, int c)
+{
+    return 64u + 128u * (u32)lv + 2u * (u32)j + (u32)c;
+}
+
+// 32x32 bit-matrix transpose across a warp: lane l holds row l (bit j = column j);
+// on return lane j holds column j (bit l = row l).  5 butterfly stages.
+__device__ __forceinline__ u32 transpose32(u32 v, int lane)
+{
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const u32 m = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu
+                    : (s == 4) ? 0x0F0F0F0Fu : (s == 2) ? 0x33333333u : 0x55555555u;
+        const u32 o = __shfl_xor_sync(FULL, v, s);
+        v = (lane & s) ? ((v & ~m) | ((o >> s) & m)) : ((v & m) | ((o << s) & ~m));
+    }
+    return v;
+}
+
+__host__ __device__ inline int ceil_log2i(int m)
+{
+    int L = 0;
+    while ((1 << L) < m) ++L;
+    return L;
+}
+
+}  // namespace mpc

@@ -1,0 +1,169 @@
+// proto_both.cuh -- L1 protocol steps, MPC_MODE_BOTH: one thread holds both parties'
+// shares of an element; an "opening" is the sum of the two masked shares, formed in
+// registers (the value each party would send and receive in a PAIR execution).
+// Contract: DESIGN.md 2.3 (PRG layout) and 2.4 (protocol steps).
+#pragma once
+#include "dev_common.cuh"
+
+namespace mpc {
+
+struct Sh { u64 s0, s1; };   // [x]_0, [x]_1
+
+__device__ __forceinline__ Sh sh_add(Sh a, Sh b) { return {a.s0 + b.s0, a.s1 + b.s1}; }
+__device__ __forceinline__ Sh sh_sub(Sh a, Sh b) { return {a.s0 - b.s0, a.s1 - b.s1}; }
+__device__ __forceinline__ Sh sh_neg(Sh a) { return {0ull - a.s0, 0ull - a.s1}; }
+__device__ __forceinline__ Sh sh_addp(Sh a, u64 e) { return {a.s0 + e, a.s1}; }        // addP: party 0
+__device__ __forceinline__ Sh sh_shr(Sh a, int k) { return {shr(a.s0, k), shr(a.s1, k)}; }
+__device__ __forceinline__ Sh sh_muli(Sh a, u64 k) { return {a.s0 * k, a.s1 * k}; }    // pmulI
+__device__ __forceinline__ Sh sh_mulf(Sh a, u64 e) { return {shr(a.s0 * e, FRAC), shr(a.s1 * e, FRAC)}; } // pmulF
+__device__ __forceinline__ Sh sh_not(Sh b) { return {1ull - b.s0, 0ull - b.s1}; }      // 1 - bit
+
+// Beaver step on element-unit u at step s.
+// (a0,b0) = PRG(K0,u,s,0); (a1,b1) = PRG(K1,u,s,0); c0 = half (u&1) of PRG(K0,u>>1,s,1).
+__device__ __forceinline__ Sh bm_with_c0(const Keys& K, u64 u, u32 s, Sh x, Sh y, u64 c0)
+{
+    const uint4 A0 = prg(K.k0, u, s, 0);
+    const uint4 A1 = prg(K.k1, u, s, 0);
+    const u64 a0 = w64(A0.x, A0.y), b0 = w64(A0.z, A0.w);
+    const u64 a1 = w64(A1.x, A1.y), b1 = w64(A1.z, A1.w);
+    const u64 c1 = (a0 + a1) * (b0 + b1) - c0;        // dealer correction -> party 1
+    const u64 e = (x.s0 - a0) + (x.s1 - a1);           // open(x - a)
+    const u64 f = (y.s0 - b0) + (y.s1 - b1);           // open(y - b)
+    return {c0 + e * b0 + f * a0 + e * f, c1 + e * b1 + f * a1};
+}
+
+__device__ __forceinline__ u64 beaver_c0(const Keys& K, u64 u, u32 s)
+{
+    const uint4 C = prg(K.k0, u >> 1, s, 1);
+    return (u & 1) ? w64(C.z, C.w) : w64(C.x, C.y);
+}
+
+__device__ __forceinline__ Sh bm(const Keys& K, u64 u, u32 s, Sh x, Sh y)
+{
+    return bm_with_c0(K, u, s, x, y, beaver_c0(K, u, s));
+}
+__device__ __forceinline__ Sh mt(const Keys& K, u64 u, u32 s, Sh x, Sh y)
+{
+    return sh_shr(bm(K, u, s, x, y), FRAC);
+}
+
+// Two consecutive units (u even, u+1) share one c0 block: 5 Philox blocks per pair.
+__device__ __forceinline__ void bm2(const Keys& K, u64 u, u32 s, Sh x0, Sh y0, Sh x1, Sh y1,
+                                   Sh& z0, Sh& z1)
+{
+    const uint4 C = prg(K.k0, u >> 1, s, 1);
+    z0 = bm_with_c0(K, u, s, x0, y0, w64(C.x, C.y));
+    z1 = bm_with_c0(K, u + 1, s, x1, y1, w64(C.z, C.w));
+}
+
+// AND on XOR-shared 32-bit plane words with triple (a0,b0,c0 | a1,b1).
+__device__ __forceinline__ void and_both(u32 x0, u32 x1, u32 y0, u32 y1,
+                                         u32 a0, u32 b0, u32 c0, u32 a1, u32 b1,
+                                         u32& z0, u32& z1)
+{
+    const u32 c1 = ((a0 ^ a1) & (b0 ^ b1)) ^ c0;       // dealer correction -> party 1
+    const u32 d = (x0 ^ a0) ^ (x1 ^ a1);                // open(x ^ a)
+    const u32 e = (y0 ^ b0) ^ (y1 ^ b1);                // open(y ^ b)
+    z0 = c0 ^ (d & b0) ^ (e & a0) ^ (d & e);
+    z1 = c1 ^ (d & b1) ^ (e & a1);
+}
+
+// LTZ_w on the warp's 32-element group q (lane l <-> element 32q+l); DESIGN.md 2.4.
+// All 32 lanes must call it (tail lanes with any value).  Returns the scale-1
+// arithmetic sharing of bit (w-1) of rec(x).  WIDE: w > 33 (two planes per lane).
+template <bool WIDE>
+__device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int lane)
+{
+    const int m = w - 1;
+    // A2B (local): lane j receives plane j of both parties' shares.
+    u32 P0[2], P1[2], G0[2], G1[2];
+    P0[0] = transpose32((u32)x.s0, lane);
+    P1[0] = transpose32((u32)x.s1, lane);
+    if (WIDE) {
+        P0[1] = transpose32((u32)(x.s0 >> 32), lane);
+        P1[1] = transpose32((u32)(x.s1 >> 32), lane);
+    }
+    constexpr int H = WIDE ? 2 : 1;
+    // g-layer: g_j = AND((x0_j, 0), (0, x1_j))
+#pragma unroll
+    for (int h = 0; h < H; ++h) {
+        const int j = lane + 32 * h;
+        G0[h] = 0; G1[h] = 0;
+        if (j < m) {
+            const uint4 t0 = prg(K.k0, q, s, ltz_slot(0, j, 0));
+            const uint4 t1 = prg(K.k1, q, s, ltz_slot(0, j, 0));
+            and_both(P0[h], 0u, 0u, P1[h], t0.x, t0.y, t0.z, t1.x, t1.y, G0[h], G1[h]);
+        }
+    }
+    // Kogge-Stone levels: G_j ^= P_j & G_{j-d};  P_j &= P_{j-d}   (old values)
+    const int L = (m > 0) ? ceil_log2i(m) : 0;
+    for (int k = 0; k < L; ++k) {
+        const int d = 1 << k;
+        u32 sG0[2], sG1[2], sP0[2], sP1[2];
+        const int src = (lane - d) & 31;
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            sG0[h] = __shfl_sync(FULL, G0[h], src);
+            sG1[h] = __shfl_sync(FULL, G1[h], src);
+            sP0[h] = __shfl_sync(FULL, P0[h], src);
+            sP1[h] = __shfl_sync(FULL, P1[h], src);
+        }
+#pragma unroll
+        for (int h = 0; h < H; ++h) {
+            const int j = lane + 32 * h;
+            if (j >= d && j < m) {
+                // source plane j-d lives in lane src, half h (if lane >= d) or h-1
+                int hs = h;
+                if (d < 32) hs = (lane >= d) ? h : h - 1;
+                else hs = h - 1;                       // d == 32 (WIDE only): same lane, lower half
+                u32 g0 = sG0[0], g1 = sG1[0], p0 = sP0[0], p1 = sP1[0];
+                if (WIDE && hs == 1) { g0 = sG0[1]; g1 = sG1[1]; p0 = sP0[1]; p1 = sP1[1]; }
+                if (WIDE && d == 32) { g0 = G0[0]; g1 = G1[0]; p0 = P0[0]; p1 = P1[0]; }
+                const uint4 tg = prg(K.k0, q, s, ltz_slot(k + 1, j, 0));
+                const uint4 tp = prg(K.k0, q, s, ltz_slot(k + 1, j, 1));
+                const uint4 t1 = prg(K.k1, q, s, ltz_slot(k + 1, j, 0));
+                u32 ng0, ng1, np0, np1;
+                and_both(P0[h], P1[h], g0, g1, tg.x, tg.y, tg.z, t1.x, t1.y, ng0, ng1);
+                and_both(P0[h], P1[h], p0, p1, tp.x, tp.y, tp.z, t1.z, t1.w, np0, np1);
+                G0[h] ^= ng0; G1[h] ^= ng1;
+                P0[h] = np0; P1[h] = np1;
+            }
+        }
+    }
+    // sign: b = p_{w-1} ^ G_{m-1}
+    u32 b0, b1;
+    if (m == 0) {
+        b0 = (u32)(x.s0 & 1ull); b1 = (u32)(x.s1 & 1ull);
+    } else {
+        const int jm = m - 1;
+        u32 gm0 = G0[0], gm1 = G1[0];
+        if (WIDE && jm >= 32) { gm0 = G0[1]; gm1 = G1[1]; }
+        gm0 = __shfl_sync(FULL, gm0, jm & 31);
+        gm1 = __shfl_sync(FULL, gm1, jm & 31);
+        b0 = (u32)((x.s0 >> (w - 1)) & 1ull) ^ ((gm0 >> lane) & 1u);
+        b1 = (u32)((x.s1 >> (w - 1)) & 1ull) ^ ((gm1 >> lane) & 1u);
+    }
+    // daBit + B2A: c = open(b ^ r); z0 = c + (1-2c) r0A; z1 = (1-2c) r1A
+    const uint4 D0 = prg(K.k0, q, s, 2u + (u32)lane);
+    const uint4 D1 = prg(K.k1, q, s, 1u);
+    const u64 r0A = w64(D0.x, D0.y);
+    const u32 r0B = D0.z & 1u;
+    const u32 r1B = (D1.x >> lane) & 1u;
+    const u64 r1A = (u64)(r0B ^ r1B) - r0A;
+    const u64 c = (u64)((b0 ^ r0B) ^ (b1 ^ r1B));
+    const u64 sg = 1ull - 2ull * c;
+    return {c + sg * r0A, sg * r1A};
+}
+
+// Philox blocks used per 32-element group by LTZ_w (algorithmic count).
+__host__ __device__ inline u64 ltz_philox_per_group(int w)
+{
+    const int m = w - 1;
+    if (m <= 0) return 32 + 1;
+    const int L = ceil_log2i(m);
+    u64 c = 2ull * (u64)m + 32 + 1;
+    for (int k = 0; k < L; ++k) c += 3ull * (u64)(m - (1 << k));
+    return c;
+}
+
+}  // namespace mpc

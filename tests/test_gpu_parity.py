@@ -1,0 +1,308 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact on every
+uint64 share of both parties, on seeded inputs (DESIGN.md section 2 contract).
+
+Small cases span several warps/tiles and a ragged tail; full BASELINE sizes are
+checked on sampled 32-row / 32-element-aligned slices, which the oracle reproduces
+exactly because the PRG is keyed by global unit (shard invariance).
+"""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import Oracle
+from oracle import float_ref as fr
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def mpc():
+    import paper_2511_19711_b200 as m
+    return m
+
+
+def np_(t):
+    return t.cpu().numpy()
+
+
+def gpu_pair(s):
+    return (torch.from_numpy(np.ascontiguousarray(s[0])).cuda(), torch.from_numpy(np.ascontiguousarray(s[1])).cuda())
+
+
+def same(g, o):
+    a0, a1 = np_(g[0]), np_(g[1])
+    assert a0.shape == o[0].shape
+    bad = np.nonzero((a0 != o[0]) | (a1 != o[1]))[0]
+    assert bad.size == 0, f"{bad.size} mismatching shares, first at {bad[:5]}"
+
+
+def pair_ctx(mpc, cfg=1, step=0):
+    keys = workloads.keys(cfg)
+    c = mpc.Ctx.for_cfg(keys)
+    c.set_step(step)
+    return c, Oracle.for_cfg(keys, step)
+
+
+# ----------------------------------------------------------------- PRG ----
+@pytest.mark.parametrize("ctr,key,out", [
+    ((0, 0, 0, 0), 0, (0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8)),
+    ((0xffffffff,) * 4, 0xffffffffffffffff, (0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd)),
+    ((0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344), 0x299f31d0a4093822,
+     (0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1)),
+])
+def test_device_philox_kat(mpc, ctr, key, out):
+    c, _ = pair_ctx(mpc)
+    unit0 = ctr[0] | (ctr[1] << 32)
+    w = c.prg_fill(key, unit0, ctr[2], ctr[3], 1)
+    torch.cuda.synchronize()
+    got = tuple(int(v) & 0xffffffff for v in w.cpu().tolist())
+    assert got == out
+
+
+# ------------------------------------------------------------ share/open ----
+@pytest.mark.parametrize("n", [1, 31, 33, 4113, 100_003])
+@pytest.mark.parametrize("owner", [0, 1])
+def test_share_open(mpc, n, owner):
+    c, o = pair_ctx(mpc, step=5)
+    x = workloads.act_inputs(n) * 1000
+    g = c.share(torch.from_numpy(x).cuda(), owner=owner, off=7)
+    r = o.share(x, owner=owner, off=7)
+    same(g, r)
+    x32 = x.astype(np.float32)
+    g32 = c.share(torch.from_numpy(x32).cuda(), owner=owner, off=7)
+    same(g32, o.share(x32.astype(np.float64), owner=owner, off=7))
+    ring, f = c.open(g)
+    oring, of = Oracle.open(*r)
+    assert np.array_equal(np_(ring), oring) and np.array_equal(np_(f), of)
+    assert c.step == o.step
+
+
+# ------------------------------------------------------------- mul/trunc ----
+@pytest.mark.parametrize("n,off", [(1, 0), (2, 1), (257, 3), (4096, 64), (100_001, 12345)])
+@pytest.mark.parametrize("tb", [0, 16])
+def test_mul(mpc, n, off, tb):
+    c, o = pair_ctx(mpc, step=11)
+    x = workloads.act_inputs(n)
+    y = workloads.recip_inputs(n)
+    gx, gy = c.share(torch.from_numpy(x).cuda()), c.share(torch.from_numpy(y).cuda(), owner=1)
+    ox, oy = o.share(x), o.share(y, owner=1)
+    same(c.mul(gx, gy, off=off, trunc_bits=tb), o.mul(ox, oy, off=off, trunc_bits=tb))
+    same(c.trunc(gx, 16), Oracle.trunc(ox, 16))
+    same(c.trunc(gy, 5), Oracle.trunc(oy, 5))
+
+
+# --------------------------------------------------------------- cmp/relu ----
+@pytest.mark.parametrize("w", [1, 2, 13, 33, 34, 63, 64])
+def test_cmp_windows(mpc, w):
+    c, o = pair_ctx(mpc, step=3)
+    n = 1000
+    x = workloads.act_inputs(n) * 3
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.cmp(gx, off=64, window=w), o.ltz(ox, off=64, window=w))
+
+
+@pytest.mark.parametrize("n", [1, 32, 45, 4096 + 7, 65536])
+def test_relu_and_cmp(mpc, n):
+    c, o = pair_ctx(mpc, step=9)
+    x = workloads.relu_inputs(n)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.cmp(gx, off=32), o.ltz(ox, off=32))
+    same(c.relu(gx, off=0), o.relu(ox, off=0))
+    assert c.step == o.step
+
+
+# ------------------------------------------------------------- exp/recip ----
+@pytest.mark.parametrize("t,clamp", [(8, 0), (8, 1), (4, 0), (2, 1), (0, 1), (1, 0), (0, 0)])
+def test_exp(mpc, t, clamp):
+    c, o = pair_ctx(mpc, step=2)
+    n = 4096 + 13
+    x = workloads.exp_inputs(n, tail_frac=0.05)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.exp(gx, off=96, t=t, clamp=clamp), o.exp(ox, off=96, t=t, clamp=clamp))
+    assert c.step == o.step
+
+
+@pytest.mark.parametrize("iters,t,clamp", [(10, 8, 0), (3, 8, 1), (7, 4, 0)])
+def test_recip(mpc, iters, t, clamp):
+    c, o = pair_ctx(mpc, step=2)
+    n = 3000
+    x = workloads.recip_inputs(n)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.recip(gx, off=32, iters=iters, t=t, clamp=clamp), o.recip(ox, off=32, iters=iters, t=t, clamp=clamp))
+
+
+@pytest.mark.parametrize("iters,t,clamp", [(3, 8, 0), (10, 8, 1), (3, 0, 0)])
+def test_rsqrt(mpc, iters, t, clamp):
+    c, o = pair_ctx(mpc, step=2)
+    n = 3000
+    x = workloads.rsqrt_inputs(n)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.rsqrt(gx, off=32, iters=iters, t=t, clamp=clamp), o.rsqrt(ox, off=32, iters=iters, t=t, clamp=clamp))
+
+
+# ------------------------------------------------------------ activations ----
+ACTS = [("gelu", "poly_x", 4), ("gelu", "poly_x", 2), ("gelu", "poly_abs", 4), ("gelu", "poly_abs", 2),
+        ("gelu", "relu", 0), ("gelu", "erf", 8), ("gelu", "erf", 4), ("silu", "poly_x", 4),
+        ("silu", "poly_abs", 4), ("silu", "relu", 0), ("sigmoid", "poly_x", 4), ("sigmoid", "poly_x", 2),
+        ("sigmoid", "relu", 0)]
+
+
+@pytest.mark.parametrize("act,form,deg", ACTS)
+def test_activations(mpc, act, form, deg):
+    c, o = pair_ctx(mpc, step=4)
+    n = 4096 + 99
+    x = workloads.act_inputs(n)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    if form == "erf":
+        knobs = mpc.default_act(act, "erf", erf_terms=deg)
+        g = getattr(c, act)(gx, off=0, form="erf", erf_terms=deg)
+        r = o.act(ox, act, "erf", 1, knobs["B"], None, deg)
+    else:
+        knobs = mpc.default_act(act, form, degree=deg)
+        g = getattr(c, act)(gx, off=0, form=form, degree=deg)
+        r = o.act(ox, act, form, knobs["degree"], knobs["B"], knobs["coeffs"] or [0.0])
+    same(g, r)
+    assert c.step == o.step
+
+
+# -------------------------------------------------------------- row ops ----
+@pytest.mark.parametrize("rows,cols", [(64, 1), (64, 2), (33, 3), (40, 9), (96, 128), (7, 200)])
+def test_max(mpc, rows, cols):
+    c, o = pair_ctx(mpc, 2, step=1)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.max(gx, rows, cols, row_off=32), o.max(ox, rows, cols, row_off=32))
+    assert c.step == o.step
+
+
+def test_maxpool(mpc):
+    N, C, H, W = 2, 16, 14, 15
+    c, o = pair_ctx(mpc, 4, step=1)
+    x = workloads.maxpool_inputs((N, C, H, W)) - 0.25
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.maxpool2d(gx, N, C, H, W, 3, 2, 1, img_off=2), o.maxpool2d(ox, N, C, H, W, 3, 2, 1, img_off=2))
+
+
+@pytest.mark.parametrize("rows,cols,clamp", [(64, 128, 0), (32, 1024, 0), (45, 77, 1), (96, 128, 1)])
+def test_softmax(mpc, rows, cols, clamp):
+    c, o = pair_ctx(mpc, 2, step=1)
+    x = workloads.softmax_inputs(rows, cols, spike=bool(clamp))
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    kw = dict(exp_clamp=clamp, recip_clamp=clamp)
+    same(c.softmax(gx, rows, cols, row_off=64, **kw), o.softmax(ox, rows, cols, row_off=64, **kw))
+    assert c.step == o.step
+
+
+@pytest.mark.parametrize("mean_mode,iters,clamp", [(0, 3, 0), (1, 3, 1), (1, 10, 0)])
+def test_layernorm(mpc, mean_mode, iters, clamp):
+    rows, cols = 70, 768
+    c, o = pair_ctx(mpc, 5, step=1)
+    x = workloads.layernorm_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    kw = dict(mean_mode=mean_mode, rsqrt_iters=iters, rsqrt_clamp=clamp)
+    same(c.layernorm(gx, rows, cols, row_off=32, **kw), o.layernorm(ox, rows, cols, row_off=32, **kw))
+
+
+# --------------------------------------------------- fused = composed ----
+def test_relu_equals_cmp_then_mul(mpc):
+    c, _ = pair_ctx(mpc, step=20)
+    n = 5000
+    gx = c.share(torch.from_numpy(workloads.relu_inputs(n)).cuda())
+    s0 = c.step
+    a = c.relu(gx, off=0)
+    c.set_step(s0, force=True)
+    l = c.cmp(gx, off=0)
+    notl = ((1 - l[0].to(torch.int64)).to(torch.uint64), (-l[1].to(torch.int64)).to(torch.uint64))
+    b = c.mul(gx, notl, off=0)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_determinism(mpc):
+    c, _ = pair_ctx(mpc, 2, step=0)
+    rows, cols = 64, 128
+    gx = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    a = c.softmax(gx, rows, cols)
+    c.set_step(1, force=True)
+    b = c.softmax(gx, rows, cols)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ---------------------------------------------- full BASELINE sizes, sampled ----
+def test_softmax_cfg2_full_size_sampled(mpc):
+    rows, cols = workloads.SHAPES["cfg2_softmax"]
+    keys = workloads.keys(2)
+    c = mpc.Ctx.for_cfg(keys)
+    x = workloads.softmax_inputs(rows, cols)
+    gx = c.share(torch.from_numpy(x).cuda())
+    s0 = c.step
+    z = c.softmax(gx, rows, cols)
+    z0, z1 = np_(z[0]).reshape(rows, cols), np_(z[1]).reshape(rows, cols)
+    x0, x1 = np_(gx[0]).reshape(rows, cols), np_(gx[1]).reshape(rows, cols)
+    for r0 in (0, 4096, rows - 32):
+        o = Oracle.for_cfg(keys, s0)
+        sl = slice(r0, r0 + 32)
+        r = o.softmax((x0[sl].ravel(), x1[sl].ravel()), 32, cols, row_off=r0)
+        assert np.array_equal(z0[sl].ravel(), r[0]) and np.array_equal(z1[sl].ravel(), r[1])
+    # reconstructed floats vs the true softmax
+    _, f = c.open(z)
+    y = np_(f).reshape(rows, cols)
+    xd = np_(c.open(gx)[1]).reshape(rows, cols)
+    assert np.max(np.abs(y - fr.softmax(xd))) <= 1.1e-2
+
+
+def test_gelu_cfg3_full_size_sampled(mpc):
+    n = workloads.SHAPES["cfg3_gelu"]
+    keys = workloads.keys(3)
+    c = mpc.Ctx.for_cfg(keys)
+    x = workloads.normal_inputs(n, 3)
+    gx = c.share(torch.from_numpy(x).cuda())
+    s0 = c.step
+    z = c.gelu(gx, form="poly_abs", degree=4)
+    knobs = mpc.default_act("gelu", "poly_abs", degree=4)
+    z0, z1 = np_(z[0]), np_(z[1])
+    x0, x1 = np_(gx[0]), np_(gx[1])
+    for off in (0, 1_000_000 - 1_000_000 % 32, n - 4096):
+        o = Oracle.for_cfg(keys, s0)
+        sl = slice(off, off + 4096)
+        r = o.act((x0[sl], x1[sl]), "gelu", "poly_abs", 4, knobs["B"], knobs["coeffs"], off=off)
+        assert np.array_equal(z0[sl], r[0]) and np.array_equal(z1[sl], r[1])
+    _, f = c.open(z)
+    xd = np_(c.open(gx)[1])
+    assert np.max(np.abs(np_(f) - fr.gelu(xd))) <= 4.2e-3 + 1e-3
+
+
+def test_relu_cfg4_first_layer_sampled(mpc):
+    N, C, H, W = workloads.SHAPES["cfg4_relu_first"]
+    n = N * C * H * W // 4          # one 8-image shard of the first ReLU layer (4 pairs)
+    keys = workloads.keys(4)
+    c = mpc.Ctx.for_cfg(keys)
+    x = workloads.relu_inputs(n)
+    gx = c.share(torch.from_numpy(x).cuda())
+    s0 = c.step
+    z = c.relu(gx)
+    ring = np_(c.open(z)[0]).view(np.int64)
+    xr = np_(c.open(gx)[0]).view(np.int64)
+    assert np.array_equal(ring, np.maximum(xr, 0))      # ReLU is exact
+    z0, z1 = np_(z[0]), np_(z[1])
+    for off in (0, n // 2 - (n // 2) % 32, n - 8192):
+        o = Oracle.for_cfg(keys, s0)
+        sl = slice(off, off + 8192)
+        r = o.relu((np_(gx[0])[sl], np_(gx[1])[sl]), off=off)
+        assert np.array_equal(z0[sl], r[0]) and np.array_equal(z1[sl], r[1])
+
+
+def test_bad_args_raise(mpc):
+    c, _ = pair_ctx(mpc)
+    gx = c.share(torch.zeros(64, dtype=torch.float64).cuda())
+    with pytest.raises(mpc.MPCError):
+        c.cmp(gx, off=3)
+    with pytest.raises(mpc.MPCError):
+        c.exp(gx, t=9)
+    with pytest.raises(mpc.MPCError):
+        c.set_step(0)
+    st = c.step
+    with pytest.raises(mpc.MPCError):
+        c.cmp(gx, window=65)
+    assert c.step == st
