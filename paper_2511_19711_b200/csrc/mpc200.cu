@@ -13,6 +13,7 @@
 
 #include "mpc200.h"
 #include "sched_both.cuh"
+#include "rows_both.cuh"
 
 using namespace mpc;
 
@@ -30,6 +31,8 @@ struct mpc_ctx {
     mpc_stats st;
     u64 last_philox;
     char err[512];
+    void* scratch;         // ctx-owned, grow-only, stream-ordered on `stream`
+    size_t scratch_bytes;
     int timing;
     TimingRec* recs;
     int nrec, caprec;
@@ -75,6 +78,17 @@ static void rec_begin(mpc_ctx* c, const char* name, u64 units)
 static void rec_end(mpc_ctx* c)
 {
     if (c->timing && c->nrec > 0) cudaEventRecord(c->recs[c->nrec - 1].b, c->stream);
+}
+
+// grow-only scratch, stream-ordered on the ctx stream (reused by every row op)
+static void* scratch(mpc_ctx* c, size_t bytes)
+{
+    if (bytes <= c->scratch_bytes) return c->scratch;
+    if (c->scratch) cudaFreeAsync(c->scratch, c->stream);
+    c->scratch = nullptr; c->scratch_bytes = 0;
+    if (cudaMallocAsync(&c->scratch, bytes, c->stream) != cudaSuccess) { c->scratch = nullptr; return nullptr; }
+    c->scratch_bytes = bytes;
+    return c->scratch;
 }
 
 static mpc_status fail(mpc_ctx* c, mpc_status s, const char* fmt, ...)
@@ -303,27 +317,6 @@ struct ActBody {
     }
 };
 
-// ---- max tree level (S9): units v in [0, rows*h): row r = v / h, i = v % h ----------------
-struct MaxLevelBody {
-    Keys K; u32 s; int w; Ptr2 in; Out2 out; i64 ldi, ldo, h, m;
-    __device__ void operator()(u64 u, u64 q, i64 v, int lane, bool valid) const {
-        Sh d = {0, 0}, y = {0, 0};
-        i64 r = 0, i = 0;
-        if (valid) {
-            r = v / h; i = v - r * h;
-            const Sh a = ld(in, r * ldi + i);
-            y = ld(in, r * ldi + i + h);
-            d = sh_sub(a, y);
-        }
-        const Sh c = sh_not((w > 33) ? ltz<true>(K, q, s, w, d, lane) : ltz<false>(K, q, s, w, d, lane));
-        const Sh sel = sh_add(y, bm(K, u, s + 1, d, c));
-        if (valid) {
-            st(out, r * ldo + i, sel);
-            if ((m & 1) && i == h - 1) st(out, r * ldo + h, ld(in, r * ldi + m - 1));
-        }
-    }
-};
-
 // maxpool: gather each k x k window (public zero padding) into a row
 __global__ void k_pool_gather(Ptr2 x, Out2 rowsbuf, int N, int C, int H, int W, int k, int stride,
                               int pad, int Ho, int Wo)
@@ -342,108 +335,6 @@ __global__ void k_pool_gather(Ptr2 x, Out2 rowsbuf, int N, int C, int H, int W, 
         rowsbuf.p0[t] = a; rowsbuf.p1[t] = b;
     }
 }
-
-// ---- softmax pieces (S14) -------------------------------------------------------------------
-// e = EXP(x - m[row]) with element units; PAIR variant (no clamp) and GROUP variant.
-struct SmExpPairBody {
-    Keys K; u32 s; ExpK p; Ptr2 x; Ptr2 mx; Out2 e; i64 n, cols;
-    __device__ void operator()(u64 u, i64 i0) const {
-        const bool v0 = i0 >= 0, v1 = i0 + 1 < n;
-        Sh a = {0, 0}, b = {0, 0};
-        if (v0) a = sh_sub(ld(x, i0), ld(mx, i0 / cols));
-        if (v1) b = sh_sub(ld(x, i0 + 1), ld(mx, (i0 + 1) / cols));
-        exp_pair(K, u, s, p, a, b);
-        if (v0) st(e, i0, a);
-        if (v1) st(e, i0 + 1, b);
-    }
-};
-struct SmExpGroupBody {
-    Keys K; u32 s; ExpK p; Ptr2 x; Ptr2 mx; Out2 e; i64 cols;
-    __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
-        Sh a = {0, 0};
-        if (valid) a = sh_sub(ld(x, i), ld(mx, i / cols));
-        const Sh y = (p.w > 33) ? exp_group<true>(K, u, q, s, p, a, lane) : exp_group<false>(K, u, q, s, p, a, lane);
-        if (valid) st(e, i, y);
-    }
-};
-
-// warp per row: S[r] = sum_j e[r, j]  (local, wrapping)
-__global__ void k_rowsum(Ptr2 e, Out2 S, i64 rows, i64 cols)
-{
-    const int lane = threadIdx.x & 31;
-    const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
-    for (i64 r = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
-        u64 a = 0, b = 0;
-        for (i64 j = lane; j < cols; j += 32) { a += e.p0[r * cols + j]; b += e.p1[r * cols + j]; }
-        for (int o = 16; o > 0; o >>= 1) { a += __shfl_xor_sync(FULL, a, o); b += __shfl_xor_sync(FULL, b, o); }
-        if (lane == 0) { S.p0[r] = a; S.p1[r] = b; }
-    }
-}
-
-// out = MT(e, bcast r) with element units
-struct BcastMulBody {
-    Keys K; u32 s; Ptr2 e; Ptr2 r; Out2 z; i64 n, cols;
-    __device__ void operator()(u64 u, i64 i0) const {
-        const bool v0 = i0 >= 0, v1 = i0 + 1 < n;
-        Sh a = {0, 0}, b = {0, 0}, ra = {0, 0}, rb = {0, 0};
-        if (v0) { a = ld(e, i0); ra = ld(r, i0 / cols); }
-        if (v1) { b = ld(e, i0 + 1); rb = ld(r, (i0 + 1) / cols); }
-        Sh za, zb;
-        bm2(K, u, s, a, ra, b, rb, za, zb);
-        if (v0) st(z, i0, sh_shr(za, FRAC));
-        if (v1) st(z, i0 + 1, sh_shr(zb, FRAC));
-    }
-};
-
-// ---- layernorm pieces (S15) -----------------------------------------------------------------
-__device__ __forceinline__ u64 floordiv_u(u64 a, i64 d)
-{
-    const i64 x = (i64)a;
-    i64 q = x / d;
-    if ((x % d) != 0 && x < 0) --q;
-    return (u64)q;
-}
-
-// warp per row: mu = mean(x); c = x - mu; v = mean(MT(c, c)) + eps  (one step s)
-__global__ void k_ln_stats(Keys K, u32 s, Ptr2 x, Out2 MU, Out2 V, i64 rows, i64 cols, u64 row_off,
-                           int mean_mode, u64 e_invd, u64 e_eps)
-{
-    const int lane = threadIdx.x & 31;
-    const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
-    for (i64 r = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
-        u64 a = 0, b = 0;
-        for (i64 j = lane; j < cols; j += 32) { a += x.p0[r * cols + j]; b += x.p1[r * cols + j]; }
-        for (int o = 16; o > 0; o >>= 1) { a += __shfl_xor_sync(FULL, a, o); b += __shfl_xor_sync(FULL, b, o); }
-        Sh mu = {a, b};
-        mu = mean_mode == 0 ? sh_mulf(mu, e_invd) : Sh{floordiv_u(mu.s0, cols), floordiv_u(mu.s1, cols)};
-        u64 qa = 0, qb = 0;
-        const u64 ubase = (row_off + (u64)r) * (u64)cols;
-        for (i64 j = lane; j < cols; j += 32) {
-            const Sh c = sh_sub(ld(x, r * cols + j), mu);
-            const Sh q = mt(K, ubase + (u64)j, s, c, c);
-            qa += q.s0; qb += q.s1;
-        }
-        for (int o = 16; o > 0; o >>= 1) { qa += __shfl_xor_sync(FULL, qa, o); qb += __shfl_xor_sync(FULL, qb, o); }
-        Sh v = {qa, qb};
-        v = mean_mode == 0 ? sh_mulf(v, e_invd) : Sh{floordiv_u(v.s0, cols), floordiv_u(v.s1, cols)};
-        v = sh_addp(v, e_eps);
-        if (lane == 0) { st(MU, r, mu); st(V, r, v); }
-    }
-}
-
-struct LnOutBody {
-    Keys K; u32 s; Ptr2 x; Ptr2 mu; Ptr2 r; Out2 z; i64 n, cols;
-    __device__ void operator()(u64 u, i64 i0) const {
-        const bool v0 = i0 >= 0, v1 = i0 + 1 < n;
-        Sh a = {0, 0}, b = {0, 0}, ra = {0, 0}, rb = {0, 0};
-        if (v0) { a = sh_sub(ld(x, i0), ld(mu, i0 / cols)); ra = ld(r, i0 / cols); }
-        if (v1) { b = sh_sub(ld(x, i0 + 1), ld(mu, (i0 + 1) / cols)); rb = ld(r, (i0 + 1) / cols); }
-        Sh za, zb;
-        bm2(K, u, s, a, ra, b, rb, za, zb);
-        if (v0) st(z, i0, sh_shr(za, FRAC));
-        if (v1) st(z, i0 + 1, sh_shr(zb, FRAC));
-    }
-};
 
 // ------------------------------------------------------------------ host helpers ----
 #define TPB 256
@@ -543,6 +434,12 @@ mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
         delete c; return MPC_ERR_CUDA;
     }
     c->sm_count = sms;
+    // keep stream-ordered allocations in the pool across synchronizations
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     *out = c;
     return MPC_OK;
 }
@@ -553,6 +450,7 @@ mpc_status mpc_ctx_destroy(mpc_ctx* c)
     for (int i = 0; i < c->nrec; ++i) { cudaEventDestroy(c->recs[i].a); cudaEventDestroy(c->recs[i].b); }
     for (int i = 0; i < c->npool; ++i) cudaEventDestroy(c->pool[i]);
     free(c->recs); free(c->pool);
+    if (c->scratch) { cudaFreeAsync(c->scratch, c->stream); cudaStreamSynchronize(c->stream); }
     delete c;
     return MPC_OK;
 }
@@ -594,7 +492,20 @@ mpc_status mpc_ctx_set_step(mpc_ctx* c, uint64_t step, int force)
     return MPC_OK;
 }
 uint64_t mpc_ctx_get_step(const mpc_ctx* c) { return c ? c->step : 0; }
-mpc_status mpc_ctx_set_stream(mpc_ctx* c, void* s) { if (!c) return MPC_ERR_INVALID; c->stream = (cudaStream_t)s; return MPC_OK; }
+mpc_status mpc_ctx_set_stream(mpc_ctx* c, void* s)
+{
+    if (!c) return MPC_ERR_INVALID;
+    cudaStream_t ns = (cudaStream_t)s;
+    if (ns != c->stream && c->scratch) {
+        // the scratch tile is stream-ordered: order the new stream after the old one
+        cudaEvent_t e = ev_get(c);
+        cudaEventRecord(e, c->stream);
+        cudaStreamWaitEvent(ns, e, 0);
+        ev_put(c, e);
+    }
+    c->stream = ns;
+    return MPC_OK;
+}
 mpc_status mpc_ctx_stats(const mpc_ctx* c, mpc_stats* o) { if (!c || !o) return MPC_ERR_INVALID; *o = c->st; return MPC_OK; }
 mpc_status mpc_ctx_reset_stats(mpc_ctx* c) { if (!c) return MPC_ERR_INVALID; memset(&c->st, 0, sizeof c->st); return MPC_OK; }
 const char* mpc_last_error(const mpc_ctx* c) { return c ? c->err : "null context"; }
@@ -822,58 +733,49 @@ mpc_status mpc_gelu(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t o
 mpc_status mpc_silu(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p) { return act_common(c, 1, x, z, n, off, p); }
 mpc_status mpc_sigmoid(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p) { return act_common(c, 2, x, z, n, off, p); }
 
-// ---- row ops ------------------------------------------------------------------------------------
+}  // extern "C"
+
+// ---- row ops (fused, one CTA per 32-row tile; rows_both.cuh) -------------------------------------
 static int max_levels_h(i64 cols) { int L = 0; i64 m = cols; while (m > 1) { m = (m + 1) / 2; ++L; } return L; }
 
-struct Scratch {
-    cudaStream_t s; void* p = nullptr;
-    ~Scratch() { if (p) cudaFreeAsync(p, s); }
-};
+static const size_t SMEM_LIMIT = 100 * 1024;     // keep 2 CTAs per SM
 
-// MAX_row over rows x cols at row offset row_off; result -> out (rows).  Uses steps s .. s+2L-1.
-static mpc_status max_rows(mpc_ctx* c, Ptr2 x, Out2 out, i64 rows, i64 cols, u64 row_off, int w, u32 s,
-                           u64* bufA, u64* bufB)
+static void acct_max(mpc_ctx* c, i64 rows, i64 cols, int w)
 {
-    // bufA / bufB: 2 x rows * ceil(cols/2) each (party 0 then party 1)
-    const i64 half = (cols + 1) / 2;
-    Ptr2 in = x;
-    i64 ldi = cols, m = cols;
-    int lv = 0;
+    i64 m = cols;
     while (m > 1) {
         const i64 h = m / 2;
-        const i64 mnext = h + (m & 1);
-        Out2 o;
-        i64 ldo;
-        if (mnext == 1) { o = out; ldo = 1; }
-        else {
-            u64* b = (lv & 1) ? bufB : bufA;
-            o = Out2{b, b + rows * half};
-            ldo = half;
-        }
-        mpc_status st = launch_groups(c, rows * h, row_off * (u64)h,
-                                      MaxLevelBody{c->K, s + 2u * (u32)lv, w, in, o, ldi, ldo, h, m}, "max_level");
-        if (st) return st;
         acct_ltz(c, (u64)(rows * h), w);
         acct_beaver(c, (u64)(rows * h));
-        in = Ptr2{o.p0, o.p1};
-        ldi = ldo;
-        m = mnext;
-        ++lv;
+        m = h + (m & 1);
     }
-    if (cols == 1) {
-        cudaMemcpyAsync(out.p0, x.p0, rows * 8, cudaMemcpyDeviceToDevice, c->stream);
-        cudaMemcpyAsync(out.p1, x.p1, rows * 8, cudaMemcpyDeviceToDevice, c->stream);
-    }
-    return MPC_OK;
 }
 
-static mpc_status alloc(mpc_ctx* c, Scratch& sc, size_t bytes)
+template <class Args>
+static mpc_status launch_rows(mpc_ctx* c, void (*kern)(Args), Args& a, i64 rows, i64 work_u64, const char* name)
 {
-    sc.s = c->stream;
-    if (bytes == 0) bytes = 8;
-    if (cudaMallocAsync(&sc.p, bytes, c->stream) != cudaSuccess) return fail(c, MPC_ERR_NOMEM, "scratch alloc %zu", bytes);
-    return MPC_OK;
+    const i64 ntiles = (rows + 31) / 32;
+    const size_t smem = sizeof(u64) * (size_t)work_u64;
+    int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 2);
+    if (grid < 1) grid = 1;
+    size_t dyn = 0;
+    if (work_u64 > 0 && smem <= SMEM_LIMIT) {
+        a.use_smem = 1; a.gscratch = nullptr; dyn = smem;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    } else if (work_u64 > 0) {
+        a.use_smem = 0;
+        a.gscratch = (u64*)scratch(c, smem * (size_t)grid);
+        if (!a.gscratch) return fail(c, MPC_ERR_NOMEM, "%s: scratch %zu bytes", name, smem * (size_t)grid);
+    }
+    a.work_u64 = work_u64;
+    rec_begin(c, name, (u64)rows);
+    kern<<<grid, 256, dyn, c->stream>>>(a);
+    rec_end(c);
+    c->st.launches++;
+    return cuda_check(c, name);
 }
+
+extern "C" {
 
 mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off, int w)
 {
@@ -886,11 +788,10 @@ mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t
     if (bad2(c, x) || bad2(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "max args (row_off % 32)");
     if (rows > 0) {
-        Scratch sc;
-        const i64 half = (cols + 1) / 2;
-        if ((st = alloc(c, sc, sizeof(u64) * 4 * (size_t)(rows * half)))) return st;
-        u64* A = (u64*)sc.p;
-        if ((st = max_rows(c, P(x), O(z), rows, cols, (u64)row_off, w, (u32)c->step, A, A + 2 * rows * half))) return st;
+        MaxArgs a{c->K, (u32)c->step, w, RowPtr2{x.sh[0], x.sh[1]}, RowOut2{z.sh[0], z.sh[1]}, rows, cols,
+                  (u64)row_off, nullptr, 0, 0};
+        if ((st = launch_rows(c, k_max_fused, a, rows, max_work_u64(cols), "max_fused"))) return st;
+        acct_max(c, rows, cols, w);
     }
     finish(c, steps);
     return MPC_OK;
@@ -913,17 +814,19 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
     const u64 row_off = (u64)img_off * (u64)C * (u64)Ho * (u64)Wo;
     if (bad2(c, x) || bad2(c, z) || img_off < 0 || (row_off & 31)) return fail(c, MPC_ERR_INVALID, "maxpool args");
     if (rows > 0) {
-        Scratch sc;
-        const i64 half = (cols + 1) / 2;
-        if ((st = alloc(c, sc, sizeof(u64) * (size_t)(2 * rows * cols + 4 * rows * half)))) return st;
-        u64* R = (u64*)sc.p;
-        u64* A = R + 2 * rows * cols;
+        // gather the windows (public zero padding) into rows, then the fused row max
+        u64* Rw = (u64*)scratch(c, sizeof(u64) * 2 * (size_t)(rows * cols));
+        if (!Rw) return fail(c, MPC_ERR_NOMEM, "maxpool scratch");
         rec_begin(c, "pool_gather", 0);
-        k_pool_gather<<<grid_for(c, rows * cols, TPB, 16), TPB, 0, c->stream>>>(P(x), Out2{R, R + rows * cols}, N, C, H, W, k, stride, pad, Ho, Wo);
+        k_pool_gather<<<grid_for(c, rows * cols, TPB, 16), TPB, 0, c->stream>>>(P(x), Out2{Rw, Rw + rows * cols}, N, C, H, W, k, stride, pad, Ho, Wo);
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "pool_gather"))) return st;
-        if ((st = max_rows(c, Ptr2{R, R + rows * cols}, O(z), rows, cols, row_off, w, (u32)c->step, A, A + 2 * rows * half))) return st;
+        MaxArgs a{c->K, (u32)c->step, w, RowPtr2{Rw, Rw + rows * cols}, RowOut2{z.sh[0], z.sh[1]}, rows, cols,
+                  row_off, nullptr, 0, 0};
+        if (max_work_u64(cols) * 8 > (i64)SMEM_LIMIT) return fail(c, MPC_ERR_UNSUPPORTED, "pool window too large");
+        if ((st = launch_rows(c, k_max_fused, a, rows, max_work_u64(cols), "maxpool_fused"))) return st;
+        acct_max(c, rows, cols, w);
     }
     finish(c, steps);
     return MPC_OK;
@@ -943,43 +846,21 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
     if (bad2(c, x) || bad2(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "softmax args (row_off % 32)");
     if (rows > 0) {
-        const i64 n = rows * cols, half = (cols + 1) / 2;
-        Scratch sc;
-        // layout: MX(2 rows) S(2 rows) R(2 rows) E(2n) maxA/maxB(4 rows*half)
-        if ((st = alloc(c, sc, sizeof(u64) * (size_t)(6 * rows + 2 * n + 4 * rows * half)))) return st;
-        u64* base = (u64*)sc.p;
-        Out2 MX{base, base + rows}, S{base + 2 * rows, base + 3 * rows}, R{base + 4 * rows, base + 5 * rows};
-        Out2 Eb{base + 6 * rows, base + 6 * rows + n};
-        u64* A = base + 6 * rows + 2 * n;
-        u32 s = (u32)c->step;
-        if ((st = max_rows(c, P(x), MX, rows, cols, (u64)row_off, p->window, s, A, A + 2 * rows * half))) return st;
-        s += 2u * (u32)L;
-        const ExpK ek = mk_exp(&p->exp);
-        const u64 eoff = (u64)row_off * (u64)cols;
-        if (p->exp.clamp) {
-            if (eoff & 31) return fail(c, MPC_ERR_INVALID, "row_off*cols must be a multiple of 32");
-            st = launch_groups(c, n, eoff, SmExpGroupBody{c->K, s, ek, P(x), Ptr2{MX.p0, MX.p1}, Eb, cols}, "sm_exp");
-        } else {
-            st = launch_pairs(c, n, eoff, SmExpPairBody{c->K, s, ek, P(x), Ptr2{MX.p0, MX.p1}, Eb, n, cols}, "sm_exp");
-        }
-        if (st) return st;
+        SoftmaxArgs a;
+        a.K = c->K;
+        a.s_max = (u32)c->step;
+        a.s_exp = a.s_max + 2u * (u32)L;
+        a.s_rec = a.s_exp + (u32)exp_steps_h(&p->exp);
+        a.s_mul = a.s_rec + (u32)exp_steps_h(&p->recip.exp) + 2u * (u32)p->recip.iters;
+        a.w = p->window; a.ek = mk_exp(&p->exp); a.rk = mk_nr(&p->recip);
+        a.x = RowPtr2{x.sh[0], x.sh[1]}; a.z = RowOut2{z.sh[0], z.sh[1]};
+        a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
+        if ((st = launch_rows(c, k_softmax_fused, a, rows, softmax_work_u64(cols), "softmax_fused"))) return st;
+        const i64 n = rows * cols;
+        acct_max(c, rows, cols, p->window);
         acct_exp(c, (u64)n, &p->exp);
-        s += (u32)exp_steps_h(&p->exp);
-        rec_begin(c, "rowsum", 0);
-        k_rowsum<<<grid_for(c, rows * 32, TPB, 16), TPB, 0, c->stream>>>(Ptr2{Eb.p0, Eb.p1}, S, rows, cols);
-        rec_end(c);
-        c->st.launches++;
-        if ((st = cuda_check(c, "rowsum"))) return st;
-        const NrK rk = mk_nr(&p->recip);
-        if (p->recip.exp.clamp)
-            st = launch_groups(c, rows, (u64)row_off, NrGroupBody<0>{c->K, s, rk, Ptr2{S.p0, S.p1}, R}, "sm_recip");
-        else
-            st = launch_pairs(c, rows, (u64)row_off, NrPairBody<0>{c->K, s, rk, Ptr2{S.p0, S.p1}, R, rows}, "sm_recip");
-        if (st) return st;
         acct_exp(c, (u64)rows, &p->recip.exp);
         for (int i = 0; i < 2 * p->recip.iters; ++i) acct_beaver(c, (u64)rows);
-        s += (u32)exp_steps_h(&p->recip.exp) + 2u * (u32)p->recip.iters;
-        if ((st = launch_pairs(c, n, eoff, BcastMulBody{c->K, s, Ptr2{Eb.p0, Eb.p1}, Ptr2{R.p0, R.p1}, O(z), n, cols}, "sm_mul"))) return st;
         acct_beaver(c, (u64)n);
     }
     finish(c, steps);
@@ -998,31 +879,26 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
     if (bad2(c, x) || bad2(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "layernorm args (row_off % 32)");
     if (rows > 0) {
-        const i64 n = rows * cols;
-        Scratch sc;
-        if ((st = alloc(c, sc, sizeof(u64) * (size_t)(6 * rows)))) return st;
-        u64* b = (u64*)sc.p;
-        Out2 MU{b, b + rows}, V{b + 2 * rows, b + 3 * rows}, R{b + 4 * rows, b + 5 * rows};
-        u32 s = (u32)c->step;
-        rec_begin(c, "ln_stats", 0);
-        k_ln_stats<<<grid_for(c, rows * 32, TPB, 16), TPB, 0, c->stream>>>(c->K, s, P(x), MU, V, rows, cols, (u64)row_off,
-                                                                           p->mean_mode, E(1.0 / (double)cols), E(p->eps));
+        LnArgs a;
+        a.K = c->K;
+        a.s_sq = (u32)c->step;
+        a.s_rs = a.s_sq + 1;
+        a.s_mul = a.s_rs + (u32)exp_steps_h(&p->rsqrt.exp) + 3u * (u32)p->rsqrt.iters;
+        a.rk = mk_nr(&p->rsqrt);
+        a.x = RowPtr2{x.sh[0], x.sh[1]}; a.z = RowOut2{z.sh[0], z.sh[1]};
+        a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
+        a.mean_mode = p->mean_mode; a.e_invd = E(1.0 / (double)cols); a.e_eps = E(p->eps);
+        const i64 ntiles = (rows + 31) / 32;
+        const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 2);
+        rec_begin(c, "layernorm_fused", (u64)rows);
+        k_ln_fused<<<grid, 256, 0, c->stream>>>(a);
         rec_end(c);
         c->st.launches++;
-        if ((st = cuda_check(c, "ln_stats"))) return st;
+        if ((st = cuda_check(c, "layernorm_fused"))) return st;
+        const i64 n = rows * cols;
         acct_beaver(c, (u64)n);
-        s += 1;
-        const NrK rk = mk_nr(&p->rsqrt);
-        if (p->rsqrt.exp.clamp)
-            st = launch_groups(c, rows, (u64)row_off, NrGroupBody<1>{c->K, s, rk, Ptr2{V.p0, V.p1}, R}, "ln_rsqrt");
-        else
-            st = launch_pairs(c, rows, (u64)row_off, NrPairBody<1>{c->K, s, rk, Ptr2{V.p0, V.p1}, R, rows}, "ln_rsqrt");
-        if (st) return st;
         acct_exp(c, (u64)rows, &p->rsqrt.exp);
         for (int i = 0; i < 3 * p->rsqrt.iters; ++i) acct_beaver(c, (u64)rows);
-        s += (u32)exp_steps_h(&p->rsqrt.exp) + 3u * (u32)p->rsqrt.iters;
-        if ((st = launch_pairs(c, n, (u64)row_off * (u64)cols,
-                               LnOutBody{c->K, s, P(x), Ptr2{MU.p0, MU.p1}, Ptr2{R.p0, R.p1}, O(z), n, cols}, "ln_out"))) return st;
         acct_beaver(c, (u64)n);
     }
     finish(c, steps);

@@ -245,11 +245,13 @@ def test_softmax_cfg2_full_size_sampled(mpc):
         sl = slice(r0, r0 + 32)
         r = o.softmax((x0[sl].ravel(), x1[sl].ravel()), 32, cols, row_off=r0)
         assert np.array_equal(z0[sl].ravel(), r[0]) and np.array_equal(z1[sl].ravel(), r[1])
-    # reconstructed floats vs the true softmax
+    # reconstructed floats vs the true softmax: the exp-limit formula itself is
+    # 1.02e-2 from the true softmax on the full cfg2 input; fixed point adds <= 2e-3
     _, f = c.open(z)
     y = np_(f).reshape(rows, cols)
     xd = np_(c.open(gx)[1]).reshape(rows, cols)
-    assert np.max(np.abs(y - fr.softmax(xd))) <= 1.1e-2
+    assert np.max(np.abs(y - fr.softmax_formula(xd))) <= 2e-3
+    assert np.max(np.abs(y - fr.softmax(xd))) <= 1.25e-2
 
 
 def test_gelu_cfg3_full_size_sampled(mpc):
