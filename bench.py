@@ -255,6 +255,30 @@ def time_per_op(m, ctx, dev, stream, flush, args, rank):
     z = (torch.empty_like(r[0]), torch.empty_like(r[1]))
     out["relu"] = _time(lambda: ctx.relu(r, off=rank * n4, out=z), n4, ctx, flush, stream, args)
     out["relu"]["config"] = "cfg4: ResNet-50 first ReLU, 8 images x 64 x 112 x 112, window 33"
+    del r, z
+    # LayerNorm: GPT-2 small, 8 x 1024 tokens x 768 (cfg5), rsqrt 3 iters (exp t=8)
+    rows5, cols5 = workloads.SHAPES["cfg5_ln"]
+    ln = ctx.share(torch.from_numpy(workloads.layernorm_inputs(rows5, cols5)).to(dev), off=rank * rows5 * cols5)
+    z = (torch.empty_like(ln[0]), torch.empty_like(ln[1]))
+    out["layernorm"] = _time(lambda: ctx.layernorm(ln, rows5, cols5, row_off=rank * rows5, out=z),
+                             rows5 * cols5, ctx, flush, stream, args)
+    out["layernorm"]["config"] = "cfg5: GPT-2 LayerNorm 8192 x 768, rsqrt 3 iters, mean x E(1/d)"
+    del ln, z
+    # GPT-2 softmax rows (1024 wide), 1/8 of one layer's 8x12x1024x1024 scores
+    rs, cs = 8 * 12 * 128, 1024
+    sm = ctx.share(torch.from_numpy(workloads.softmax_inputs(rs, cs, seed_cfg=5)).to(dev), off=rank * rs * cs)
+    z = (torch.empty_like(sm[0]), torch.empty_like(sm[1]))
+    out["softmax1024"] = _time(lambda: ctx.softmax(sm, rs, cs, row_off=rank * rs, out=z), rs * cs, ctx, flush,
+                               stream, args)
+    out["softmax1024"]["config"] = "cfg5: GPT-2 softmax rows of 1024 (12288 rows = 1/8 layer), t=8, NR 10"
+    del sm, z
+    # Beaver multiply alone (S4), 16M elements
+    nm = 1 << 24
+    a = ctx.share(torch.from_numpy(workloads.act_inputs(nm)).to(dev))
+    b = ctx.share(torch.from_numpy(workloads.act_inputs(nm, seed_cfg=7)).to(dev))
+    z = (torch.empty_like(a[0]), torch.empty_like(a[1]))
+    out["mul"] = _time(lambda: ctx.mul(a, b, trunc_bits=16, out=z), nm, ctx, flush, stream, args)
+    out["mul"]["config"] = "Beaver multiply + trunc, 16M elements"
     return out
 
 

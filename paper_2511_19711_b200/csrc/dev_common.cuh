@@ -74,6 +74,25 @@ __device__ __forceinline__ u32 transpose32(u32 v, int lane)
     return v;
 }
 
+// q = n / d for n < 2^31 with one IMAD.HI + shift (round-up multiplier, p = 31 + ceil(log2 d))
+struct FastDiv { u32 d, m, s; };
+__host__ __device__ inline FastDiv make_fastdiv(u32 d)
+{
+    FastDiv f{d, 0u, 0u};
+    if (d > 1) {
+        int l = 0;
+        while ((1ull << l) < d) ++l;
+        const int p = 31 + l;
+        f.m = (u32)(((1ull << p) + d - 1) / d);
+        f.s = (u32)(p - 32);
+    }
+    return f;
+}
+__device__ __forceinline__ u32 fdiv(u32 n, const FastDiv& f)
+{
+    return f.d == 1 ? n : (__umulhi(n, f.m) >> f.s);
+}
+
 __host__ __device__ inline int ceil_log2i(int m)
 {
     int L = 0;

@@ -198,7 +198,7 @@ __global__ void k_trunc(const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i
 // ---- generic drivers ---------------------------------------------------------------
 // PAIR driver: thread <-> global unit pair (2P, 2P+1) covering [off, off+n).
 template <class Body>
-__global__ void __launch_bounds__(256) k_pairs(i64 n, u64 off, Body body)
+__global__ void __launch_bounds__(256, 3) k_pairs(i64 n, u64 off, Body body)
 {
     const u64 p0 = off >> 1, p1 = (off + (u64)n + 1) >> 1;
     const u64 stride = (u64)gridDim.x * blockDim.x;
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) k_pairs(i64 n, u64 off, Body body)
 
 // GROUP driver: warp <-> 32-unit LTZ group, lane <-> unit.  off % 32 == 0.
 template <class Body>
-__global__ void __launch_bounds__(256) k_groups(i64 n, u64 off, Body body)
+__global__ void __launch_bounds__(256, 3) k_groups(i64 n, u64 off, Body body)
 {
     const int lane = threadIdx.x & 31;
     const i64 ng = (n + 31) >> 5;
@@ -244,23 +244,25 @@ struct MulBody {
     }
 };
 
+template <bool WIDE>
 struct CmpBody {
     Keys K; u32 s; int w; Ptr2 x; Out2 z; int relu;
     __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
         Sh xv = {0, 0};
         if (valid) xv = ld(x, i);
-        Sh l = (w > 33) ? ltz<true>(K, q, s, w, xv, lane) : ltz<false>(K, q, s, w, xv, lane);
+        Sh l = ltz<WIDE>(K, q, s, w, xv, lane);
         if (relu) l = bm(K, u, s + 1, xv, sh_not(l));
         if (valid) st(z, i, l);
     }
 };
 
+template <bool WIDE>
 struct ExpGroupBody {
     Keys K; u32 s; ExpK p; Ptr2 x; Out2 z;
     __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
         Sh xv = {0, 0};
         if (valid) xv = ld(x, i);
-        const Sh y = (p.w > 33) ? exp_group<true>(K, u, q, s, p, xv, lane) : exp_group<false>(K, u, q, s, p, xv, lane);
+        const Sh y = exp_group<WIDE>(K, u, q, s, p, xv, lane);
         if (valid) st(z, i, y);
     }
 };
@@ -278,15 +280,15 @@ struct ExpPairBody {
     }
 };
 
-template <int KIND>   // 0 recip, 1 rsqrt
+template <int KIND, bool WIDE>   // 0 recip, 1 rsqrt
 struct NrGroupBody {
     Keys K; u32 s; NrK p; Ptr2 x; Out2 z;
     __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
         Sh xv = {0, 0};
         if (valid) xv = ld(x, i);
         Sh y;
-        if (KIND == 0) y = (p.exp.w > 33) ? recip_group<true>(K, u, q, s, p, xv, lane) : recip_group<false>(K, u, q, s, p, xv, lane);
-        else y = (p.exp.w > 33) ? rsqrt_group<true>(K, u, q, s, p, xv, lane) : rsqrt_group<false>(K, u, q, s, p, xv, lane);
+        if (KIND == 0) y = recip_group<WIDE>(K, u, q, s, p, xv, lane);
+        else y = rsqrt_group<WIDE>(K, u, q, s, p, xv, lane);
         if (valid) st(z, i, y);
     }
 };
@@ -307,12 +309,13 @@ struct NrPairBody {
     }
 };
 
+template <bool WIDE>
 struct ActBody {
     Keys K; u32 s; ActK p; Ptr2 x; Out2 z;
     __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
         Sh xv = {0, 0};
         if (valid) xv = ld(x, i);
-        const Sh y = (p.w > 33) ? act_group<true>(K, u, q, s, p, xv, lane) : act_group<false>(K, u, q, s, p, xv, lane);
+        const Sh y = act_group<WIDE>(K, u, q, s, p, xv, lane);
         if (valid) st(z, i, y);
     }
 };
@@ -339,13 +342,23 @@ __global__ void k_pool_gather(Ptr2 x, Out2 rowsbuf, int N, int C, int H, int W, 
 // ------------------------------------------------------------------ host helpers ----
 #define TPB 256
 
+// resident CTAs per SM of a kernel at TPB threads (queried once per instantiation)
+template <class K>
+static int occupancy(K kern)
+{
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPB, 0) != cudaSuccess || nb < 1) nb = 1;
+    return nb;
+}
+
 template <class Body>
 static mpc_status launch_pairs(mpc_ctx* c, i64 n, u64 off, const Body& b, const char* name)
 {
     if (n <= 0) return MPC_OK;
+    static int per_sm = occupancy(k_pairs<Body>);
     const i64 npairs = (i64)(((off + (u64)n + 1) >> 1) - (off >> 1));
     rec_begin(c, name, (u64)n);
-    k_pairs<Body><<<grid_for(c, npairs, TPB), TPB, 0, c->stream>>>(n, off, b);
+    k_pairs<Body><<<grid_for(c, npairs, TPB, per_sm), TPB, 0, c->stream>>>(n, off, b);
     rec_end(c);
     c->st.launches++;
     return cuda_check(c, name);
@@ -355,8 +368,9 @@ template <class Body>
 static mpc_status launch_groups(mpc_ctx* c, i64 n, u64 off, const Body& b, const char* name)
 {
     if (n <= 0) return MPC_OK;
+    static int per_sm = occupancy(k_groups<Body>);
     rec_begin(c, name, (u64)n);
-    k_groups<Body><<<grid_for(c, ((n + 31) / 32) * 32, TPB), TPB, 0, c->stream>>>(n, off, b);
+    k_groups<Body><<<grid_for(c, ((n + 31) / 32) * 32, TPB, per_sm), TPB, 0, c->stream>>>(n, off, b);
     rec_end(c);
     c->st.launches++;
     return cuda_check(c, name);
@@ -609,7 +623,9 @@ static mpc_status cmp_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, 
     if (w < 1 || w > 64) return fail(c, MPC_ERR_RANGE, "window must be in [1,64]");
     if (n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
     if (bad2(c, x) || bad2(c, z)) return fail(c, MPC_ERR_INVALID, "cmp: null pointer");
-    if ((st = launch_groups(c, n, (u64)off, CmpBody{c->K, (u32)c->step, w, P(x), O(z), relu}, "cmp"))) return st;
+    st = w > 33 ? launch_groups(c, n, (u64)off, CmpBody<true>{c->K, (u32)c->step, w, P(x), O(z), relu}, relu ? "relu" : "cmp")
+                : launch_groups(c, n, (u64)off, CmpBody<false>{c->K, (u32)c->step, w, P(x), O(z), relu}, relu ? "relu" : "cmp");
+    if (st) return st;
     acct_ltz(c, (u64)n, w);
     if (relu) acct_beaver(c, (u64)n);
     finish(c, relu ? 2 : 1);
@@ -630,7 +646,8 @@ mpc_status mpc_exp(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t of
     const ExpK k = mk_exp(p);
     if (p->clamp) {
         if (off & 31) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
-        st = launch_groups(c, n, (u64)off, ExpGroupBody{c->K, (u32)c->step, k, P(x), O(z)}, "exp");
+        st = p->window > 33 ? launch_groups(c, n, (u64)off, ExpGroupBody<true>{c->K, (u32)c->step, k, P(x), O(z)}, "exp")
+                            : launch_groups(c, n, (u64)off, ExpGroupBody<false>{c->K, (u32)c->step, k, P(x), O(z)}, "exp");
     } else {
         st = launch_pairs(c, n, (u64)off, ExpPairBody{c->K, (u32)c->step, k, P(x), O(z), n}, "exp");
     }
@@ -655,7 +672,8 @@ static mpc_status nr_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, i
     const NrK k = mk_nr(p);
     if (p->exp.clamp) {
         if (off & 31) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
-        st = launch_groups(c, n, (u64)off, NrGroupBody<KIND>{c->K, (u32)c->step, k, P(x), O(z)}, "newton");
+        st = p->exp.window > 33 ? launch_groups(c, n, (u64)off, NrGroupBody<KIND, true>{c->K, (u32)c->step, k, P(x), O(z)}, "newton")
+                                : launch_groups(c, n, (u64)off, NrGroupBody<KIND, false>{c->K, (u32)c->step, k, P(x), O(z)}, "newton");
     } else {
         st = launch_pairs(c, n, (u64)off, NrPairBody<KIND>{c->K, (u32)c->step, k, P(x), O(z), n}, "newton");
     }
@@ -714,7 +732,9 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
         k.deg = p->degree;
         for (int i = 0; i <= p->degree; ++i) k.c[i] = E(p->coeffs[i]);
     }
-    if ((st = launch_groups(c, n, (u64)off, ActBody{c->K, (u32)c->step, k, P(x), O(z)}, "act"))) return st;
+    st = k.w > 33 ? launch_groups(c, n, (u64)off, ActBody<true>{c->K, (u32)c->step, k, P(x), O(z)}, "act")
+                  : launch_groups(c, n, (u64)off, ActBody<false>{c->K, (u32)c->step, k, P(x), O(z)}, "act");
+    if (st) return st;
     // accounting
     const u64 N = (u64)n;
     if (k.deg == 0) { acct_ltz(c, N, k.w); if (act != 2) acct_beaver(c, N); }
@@ -738,7 +758,7 @@ mpc_status mpc_sigmoid(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_
 // ---- row ops (fused, one CTA per 32-row tile; rows_both.cuh) -------------------------------------
 static int max_levels_h(i64 cols) { int L = 0; i64 m = cols; while (m > 1) { m = (m + 1) / 2; ++L; } return L; }
 
-static const size_t SMEM_LIMIT = 100 * 1024;     // keep 2 CTAs per SM
+static const size_t SMEM_LIMIT = 72 * 1024;      // keep 3 CTAs per SM
 
 static void acct_max(mpc_ctx* c, i64 rows, i64 cols, int w)
 {
@@ -756,7 +776,7 @@ static mpc_status launch_rows(mpc_ctx* c, void (*kern)(Args), Args& a, i64 rows,
 {
     const i64 ntiles = (rows + 31) / 32;
     const size_t smem = sizeof(u64) * (size_t)work_u64;
-    int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 2);
+    int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 3);
     if (grid < 1) grid = 1;
     size_t dyn = 0;
     if (work_u64 > 0 && smem <= SMEM_LIMIT) {
@@ -790,7 +810,7 @@ mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t
     if (rows > 0) {
         MaxArgs a{c->K, (u32)c->step, w, RowPtr2{x.sh[0], x.sh[1]}, RowOut2{z.sh[0], z.sh[1]}, rows, cols,
                   (u64)row_off, nullptr, 0, 0};
-        if ((st = launch_rows(c, k_max_fused, a, rows, max_work_u64(cols), "max_fused"))) return st;
+        if ((st = launch_rows(c, w > 33 ? k_max_fused<true> : k_max_fused<false>, a, rows, max_work_u64(cols), "max_fused"))) return st;
         acct_max(c, rows, cols, w);
     }
     finish(c, steps);
@@ -825,7 +845,7 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
         MaxArgs a{c->K, (u32)c->step, w, RowPtr2{Rw, Rw + rows * cols}, RowOut2{z.sh[0], z.sh[1]}, rows, cols,
                   row_off, nullptr, 0, 0};
         if (max_work_u64(cols) * 8 > (i64)SMEM_LIMIT) return fail(c, MPC_ERR_UNSUPPORTED, "pool window too large");
-        if ((st = launch_rows(c, k_max_fused, a, rows, max_work_u64(cols), "maxpool_fused"))) return st;
+        if ((st = launch_rows(c, w > 33 ? k_max_fused<true> : k_max_fused<false>, a, rows, max_work_u64(cols), "maxpool_fused"))) return st;
         acct_max(c, rows, cols, w);
     }
     finish(c, steps);
@@ -855,7 +875,9 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
         a.w = p->window; a.ek = mk_exp(&p->exp); a.rk = mk_nr(&p->recip);
         a.x = RowPtr2{x.sh[0], x.sh[1]}; a.z = RowOut2{z.sh[0], z.sh[1]};
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
-        if ((st = launch_rows(c, k_softmax_fused, a, rows, softmax_work_u64(cols), "softmax_fused"))) return st;
+        const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
+        if ((st = launch_rows(c, wide ? k_softmax_fused<true> : k_softmax_fused<false>, a, rows,
+                              softmax_work_u64(cols), "softmax_fused"))) return st;
         const i64 n = rows * cols;
         acct_max(c, rows, cols, p->window);
         acct_exp(c, (u64)n, &p->exp);
@@ -889,9 +911,10 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
         a.mean_mode = p->mean_mode; a.e_invd = E(1.0 / (double)cols); a.e_eps = E(p->eps);
         const i64 ntiles = (rows + 31) / 32;
-        const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 2);
+        const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 3);
         rec_begin(c, "layernorm_fused", (u64)rows);
-        k_ln_fused<<<grid, 256, 0, c->stream>>>(a);
+        if (p->rsqrt.exp.window > 33) k_ln_fused<true><<<grid, 256, 0, c->stream>>>(a);
+        else k_ln_fused<false><<<grid, 256, 0, c->stream>>>(a);
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "layernorm_fused"))) return st;

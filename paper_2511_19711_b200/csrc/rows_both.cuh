@@ -19,6 +19,7 @@ constexpr int ROW_TILE = 32;
 // in: row-major, row stride ldi (tile-local row 0 = global row g0).  Levels write into
 // the ping-pong buffers A/B (stride H = ceil(cols/2)); the last level writes mx[rr].
 // R = valid rows in the tile.  Steps s + 2*lv, s + 2*lv + 1.
+template <bool WIDE>
 __device__ __forceinline__ void tile_max(const Keys& K, u32 s, int w, RowPtr2 in, i64 ldi, i64 cols,
                                          int R, u64 g0, u64* A0, u64* A1, u64* B0, u64* B1, i64 H,
                                          u64* mx0, u64* mx1)
@@ -36,19 +37,20 @@ __device__ __forceinline__ void tile_max(const Keys& K, u32 s, int w, RowPtr2 in
         else { o0 = A0; o1 = A1; lo = H; }
         const u32 sl = s + 2u * (u32)lv;
         const u64 ubase = g0 * (u64)h;                 // multiple of 32 (g0 is)
+        const FastDiv dh = make_fastdiv((u32)h);
         for (i64 g = warp; g < h; g += NW) {            // 32*h units = h groups
             const i64 v = g * 32 + lane;
             const bool valid = v < (i64)R * h;
             i64 rr = 0, i = 0;
             Sh d = {0, 0}, y = {0, 0};
             if (valid) {
-                rr = v / h; i = v - rr * h;
+                rr = fdiv((u32)v, dh); i = v - rr * h;
                 const Sh a = {i0[rr * li + i], i1[rr * li + i]};
                 y = Sh{i0[rr * li + i + h], i1[rr * li + i + h]};
                 d = sh_sub(a, y);
             }
             const u64 q = (ubase >> 5) + (u64)g;
-            const Sh c = sh_not(w > 33 ? ltz<true>(K, q, sl, w, d, lane) : ltz<false>(K, q, sl, w, d, lane));
+            const Sh c = sh_not(ltz<WIDE>(K, q, sl, w, d, lane));
             const Sh sel = sh_add(y, bm(K, ubase + (u64)v, sl + 1, d, c));
             if (valid) {
                 o0[rr * lo + i] = sel.s0; o1[rr * lo + i] = sel.s1;
@@ -67,7 +69,7 @@ __device__ __forceinline__ void tile_max(const Keys& K, u32 s, int w, RowPtr2 in
 }
 
 // per-row Newton-Raphson over the tile's rows: warp 0, lane <-> row (LTZ group = tile)
-template <int KIND>
+template <int KIND, bool WIDE>
 __device__ __forceinline__ void tile_nr(const Keys& K, u32 s, const NrK& p, int R, u64 g0,
                                         const u64* x0, const u64* x1, u64* y0, u64* y1)
 {
@@ -77,10 +79,8 @@ __device__ __forceinline__ void tile_nr(const Keys& K, u32 s, const NrK& p, int 
         Sh x = {0, 0};
         if (valid) x = Sh{x0[lane], x1[lane]};
         Sh y;
-        if (KIND == 0) y = p.exp.w > 33 ? recip_group<true>(K, g0 + lane, g0 >> 5, s, p, x, lane)
-                                        : recip_group<false>(K, g0 + lane, g0 >> 5, s, p, x, lane);
-        else y = p.exp.w > 33 ? rsqrt_group<true>(K, g0 + lane, g0 >> 5, s, p, x, lane)
-                              : rsqrt_group<false>(K, g0 + lane, g0 >> 5, s, p, x, lane);
+        if (KIND == 0) y = recip_group<WIDE>(K, g0 + lane, g0 >> 5, s, p, x, lane);
+        else y = rsqrt_group<WIDE>(K, g0 + lane, g0 >> 5, s, p, x, lane);
         if (valid) { y0[lane] = y.s0; y1[lane] = y.s1; }
     }
     __syncthreads();
@@ -120,7 +120,8 @@ struct SoftmaxArgs {
 //   MX0 MX1 S0 S1 R0 R1 : 6 x 32
 __host__ __device__ inline i64 softmax_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 6 * 32; }
 
-__global__ void __launch_bounds__(256, 2) k_softmax_fused(SoftmaxArgs a)
+template <bool WIDE>
+__global__ void __launch_bounds__(256, 3) k_softmax_fused(SoftmaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
     u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
@@ -130,13 +131,14 @@ __global__ void __launch_bounds__(256, 2) k_softmax_fused(SoftmaxArgs a)
     u64 *MX0 = W + 128 * H, *MX1 = MX0 + 32, *S0 = MX0 + 64, *S1 = MX0 + 96, *R0 = MX0 + 128, *R1 = MX0 + 160;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const i64 ntiles = (a.rows + 31) / 32;
+    const FastDiv dC = make_fastdiv((u32)C);
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 r0 = tile * 32;
         const int R = (int)min((i64)32, a.rows - r0);
         const u64 g0 = a.row_off + (u64)r0;                       // global row of the tile
         const RowPtr2 xt = {a.x.p0 + r0 * C, a.x.p1 + r0 * C};
         // 1. m = MAX_row(x)
-        tile_max(a.K, a.s_max, a.w, xt, C, C, R, g0, A0, A1, B0, B1, H, MX0, MX1);
+        tile_max<WIDE>(a.K, a.s_max, a.w, xt, C, C, R, g0, A0, A1, B0, B1, H, MX0, MX1);
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;
@@ -145,15 +147,14 @@ __global__ void __launch_bounds__(256, 2) k_softmax_fused(SoftmaxArgs a)
                 const i64 e = g * 32 + lane;
                 const bool valid = e < ne;
                 Sh d = {0, 0};
-                if (valid) { const i64 rr = e / C; d = Sh{xt.p0[e] - MX0[rr], xt.p1[e] - MX1[rr]}; }
-                const Sh y = a.ek.w > 33 ? exp_group<true>(a.K, ub + e, (ub >> 5) + g, a.s_exp, a.ek, d, lane)
-                                         : exp_group<false>(a.K, ub + e, (ub >> 5) + g, a.s_exp, a.ek, d, lane);
+                if (valid) { const i64 rr = fdiv((u32)e, dC); d = Sh{xt.p0[e] - MX0[rr], xt.p1[e] - MX1[rr]}; }
+                const Sh y = exp_group<WIDE>(a.K, ub + e, (ub >> 5) + g, a.s_exp, a.ek, d, lane);
                 if (valid) { E0[e] = y.s0; E1[e] = y.s1; }
             }
         } else {
             for (i64 p = threadIdx.x; p < (ne + 1) / 2; p += blockDim.x) {
                 const i64 e = 2 * p;
-                const i64 ra = e / C, rb = (e + 1) / C;
+                const i64 ra = fdiv((u32)e, dC), rb = fdiv((u32)(e + 1), dC);
                 Sh da = {xt.p0[e] - MX0[ra], xt.p1[e] - MX1[ra]}, db = {0, 0};
                 const bool vb = e + 1 < ne;
                 if (vb) db = Sh{xt.p0[e + 1] - MX0[rb], xt.p1[e + 1] - MX1[rb]};
@@ -166,12 +167,12 @@ __global__ void __launch_bounds__(256, 2) k_softmax_fused(SoftmaxArgs a)
         // 4. S = rowsum(e)
         tile_rowsum(E0, E1, C, C, R, S0, S1);
         // 5. r = RECIP(S), row units
-        tile_nr<0>(a.K, a.s_rec, a.rk, R, g0, S0, S1, R0, R1);
+        tile_nr<0, WIDE>(a.K, a.s_rec, a.rk, R, g0, S0, S1, R0, R1);
         // 6. out = MT(e, r), element units
         for (i64 p = threadIdx.x; p < (ne + 1) / 2; p += blockDim.x) {
             const i64 e = 2 * p;
             const bool vb = e + 1 < ne;
-            const i64 ra = e / C, rb = (e + 1) / C;
+            const i64 ra = fdiv((u32)e, dC), rb = fdiv((u32)(e + 1), dC);
             const Sh ea = {E0[e], E1[e]}, eb = vb ? Sh{E0[e + 1], E1[e + 1]} : Sh{0, 0};
             const Sh xa = {R0[ra], R1[ra]}, xb = vb ? Sh{R0[rb], R1[rb]} : Sh{0, 0};
             Sh za, zb;
@@ -189,7 +190,8 @@ struct MaxArgs {
 };
 __host__ __device__ inline i64 max_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 2 * 32; }
 
-__global__ void __launch_bounds__(256, 2) k_max_fused(MaxArgs a)
+template <bool WIDE>
+__global__ void __launch_bounds__(256, 3) k_max_fused(MaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
     u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(256, 2) k_max_fused(MaxArgs a)
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 r0 = tile * 32;
         const int R = (int)min((i64)32, a.rows - r0);
-        tile_max(a.K, a.s, a.w, RowPtr2{a.x.p0 + r0 * C, a.x.p1 + r0 * C}, C, C, R, a.row_off + (u64)r0,
+        tile_max<WIDE>(a.K, a.s, a.w, RowPtr2{a.x.p0 + r0 * C, a.x.p1 + r0 * C}, C, C, R, a.row_off + (u64)r0,
                  A0, A1, B0, B1, H, MX0, MX1);
         for (int rr = threadIdx.x; rr < R; rr += blockDim.x) { a.z.p0[r0 + rr] = MX0[rr]; a.z.p1[r0 + rr] = MX1[rr]; }
         __syncthreads();
@@ -220,12 +222,14 @@ __device__ __forceinline__ u64 floordiv_s(u64 a, i64 d)
 }
 
 // LAYERNORM: mu, c = x - mu, v = mean(MT(c,c)) + eps, r = RSQRT(v), out = MT(c, r)
-__global__ void __launch_bounds__(256, 2) k_ln_fused(LnArgs a)
+template <bool WIDE>
+__global__ void __launch_bounds__(256, 3) k_ln_fused(LnArgs a)
 {
     __shared__ u64 MU0[32], MU1[32], V0[32], V1[32], RS0[32], RS1[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const i64 C = a.cols;
     const i64 ntiles = (a.rows + 31) / 32;
+    const FastDiv dC = make_fastdiv((u32)C);
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const i64 r0 = tile * 32;
         const int R = (int)min((i64)32, a.rows - r0);
@@ -260,13 +264,13 @@ __global__ void __launch_bounds__(256, 2) k_ln_fused(LnArgs a)
             if (lane == 0) { MU0[rr] = mu.s0; MU1[rr] = mu.s1; V0[rr] = v.s0; V1[rr] = v.s1; }
         }
         __syncthreads();
-        tile_nr<1>(a.K, a.s_rs, a.rk, R, g0, V0, V1, RS0, RS1);
+        tile_nr<1, WIDE>(a.K, a.s_rs, a.rk, R, g0, V0, V1, RS0, RS1);
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;            // even: g0 is a multiple of 32
         for (i64 p = threadIdx.x; p < (ne + 1) / 2; p += blockDim.x) {
             const i64 e = 2 * p;
             const bool vb = e + 1 < ne;
-            const i64 ra = e / C, rb = (e + 1) / C;
+            const i64 ra = fdiv((u32)e, dC), rb = fdiv((u32)(e + 1), dC);
             const Sh ca = sh_sub(Sh{x0[e], x1[e]}, Sh{MU0[ra], MU1[ra]});
             const Sh cb = vb ? sh_sub(Sh{x0[e + 1], x1[e + 1]}, Sh{MU0[rb], MU1[rb]}) : Sh{0, 0};
             const Sh ra_ = {RS0[ra], RS1[ra]}, rb_ = vb ? Sh{RS0[rb], RS1[rb]} : Sh{0, 0};

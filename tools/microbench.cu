@@ -1,0 +1,152 @@
+// microbench.cu -- integer-pipe microbenchmarks on sm_100a that pin the ALU roofline
+// of DESIGN.md 6: IMAD.WIDE.U32 vs IMAD vs IMAD.HI vs LOP3 throughput, and the
+// Philox4x32-10 block rate at several ILP / occupancy points.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench tools/microbench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define ITERS 4096
+#define CHAINS 8
+
+__global__ void k_imad_wide(uint32_t* out, uint32_t seed)
+{
+    uint32_t a[CHAINS], b[CHAINS];
+    for (int c = 0; c < CHAINS; ++c) { a[c] = seed + threadIdx.x * 7 + c; b[c] = a[c] ^ 0x1234567u; }
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) {
+            uint64_t p = (uint64_t)a[c] * 0xD2511F53u;
+            a[c] = (uint32_t)(p >> 32) + b[c];   // keeps the chain dependent (IMAD.WIDE consumes b)
+            b[c] = (uint32_t)p;
+        }
+    }
+    uint32_t s = 0;
+    for (int c = 0; c < CHAINS; ++c) s ^= a[c] ^ b[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void k_imad_lo(uint32_t* out, uint32_t seed)
+{
+    uint32_t a[CHAINS];
+    for (int c = 0; c < CHAINS; ++c) a[c] = seed + threadIdx.x * 7 + c;
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) a[c] = a[c] * 0xD2511F53u + c;
+    }
+    uint32_t s = 0;
+    for (int c = 0; c < CHAINS; ++c) s ^= a[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void k_imad_hi(uint32_t* out, uint32_t seed)
+{
+    uint32_t a[CHAINS];
+    for (int c = 0; c < CHAINS; ++c) a[c] = seed + threadIdx.x * 7 + c;
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) a[c] = __umulhi(a[c], 0xD2511F53u) + a[c];
+    }
+    uint32_t s = 0;
+    for (int c = 0; c < CHAINS; ++c) s ^= a[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+__global__ void k_lop3(uint32_t* out, uint32_t seed)
+{
+    uint32_t a[CHAINS], b = seed * 3 + 1, d = seed * 5 + 7;
+    for (int c = 0; c < CHAINS; ++c) a[c] = seed + threadIdx.x * 7 + c;
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) a[c] = (a[c] ^ b ^ (d + it));
+    }
+    uint32_t s = 0;
+    for (int c = 0; c < CHAINS; ++c) s ^= a[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+struct Key { uint32_t lo, hi; };
+__device__ __forceinline__ uint4 philox(Key key, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3)
+{
+    uint32_t k0 = key.lo, k1 = key.hi;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        c1 = (uint32_t)p1; c3 = (uint32_t)p0; c0 = n0; c2 = n2;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+template <int ILP>
+__global__ void k_philox(uint32_t* out, Key key, int reps)
+{
+    uint32_t acc = 0;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int j = 0; j < ILP; ++j) {
+            const uint4 v = philox(key, t, (uint32_t)r, (uint32_t)j, 7u);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    }
+    out[t] = acc;
+}
+
+template <class F>
+static float timeit(F launch)
+{
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    launch();
+    cudaDeviceSynchronize();
+    cudaEventRecord(a);
+    for (int i = 0; i < 5; ++i) launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms / 5;
+}
+
+int main()
+{
+    int sms = 0, clk = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    uint32_t* out;
+    cudaMalloc(&out, 64 << 20);
+    const int blocks = sms * 8, threads = 256;
+    const double nthr = (double)blocks * threads;
+    printf("{\"sms\": %d, \"clock_khz\": %d", sms, clk);
+    float ms = timeit([&] { k_imad_wide<<<blocks, threads>>>(out, 1); });
+    printf(", \"imad_wide_per_clk_per_sm\": %.2f", nthr * ITERS * CHAINS / (ms * 1e-3) / sms / (clk * 1e3));
+    ms = timeit([&] { k_imad_lo<<<blocks, threads>>>(out, 1); });
+    printf(", \"imad_per_clk_per_sm\": %.2f", nthr * ITERS * CHAINS / (ms * 1e-3) / sms / (clk * 1e3));
+    ms = timeit([&] { k_imad_hi<<<blocks, threads>>>(out, 1); });
+    printf(", \"imad_hi_plus_iadd_per_clk_per_sm\": %.2f", nthr * ITERS * CHAINS / (ms * 1e-3) / sms / (clk * 1e3));
+    ms = timeit([&] { k_lop3<<<blocks, threads>>>(out, 1); });
+    printf(", \"lop3_plus_iadd_per_clk_per_sm\": %.2f", nthr * ITERS * CHAINS / (ms * 1e-3) / sms / (clk * 1e3));
+    const int reps = 256;
+    for (int tpb : {128, 256, 512, 1024}) {
+        const int nb = sms * (2048 / tpb);
+        const double n = (double)nb * tpb;
+        ms = timeit([&] { k_philox<1><<<nb, tpb>>>(out, Key{1, 2}, reps); });
+        printf(", \"philox_ilp1_%dthr_gblk_s\": %.1f", tpb * (2048 / tpb), n * reps / (ms * 1e-3) / 1e9);
+        ms = timeit([&] { k_philox<2><<<nb, tpb>>>(out, Key{1, 2}, reps / 2); });
+        printf(", \"philox_ilp2_%dthr_gblk_s\": %.1f", tpb * (2048 / tpb), n * reps / (ms * 1e-3) / 1e9);
+    }
+    {
+        const int nb = sms * 2, tpb = 256;   // 16 warps / SM
+        const double n = (double)nb * tpb;
+        ms = timeit([&] { k_philox<1><<<nb, tpb>>>(out, Key{1, 2}, reps); });
+        printf(", \"philox_ilp1_512thr_per_sm_gblk_s\": %.1f", n * reps / (ms * 1e-3) / 1e9);
+        ms = timeit([&] { k_philox<4><<<nb, tpb>>>(out, Key{1, 2}, reps / 4); });
+        printf(", \"philox_ilp4_512thr_per_sm_gblk_s\": %.1f", n * reps / (ms * 1e-3) / 1e9);
+    }
+    printf("}\n");
+    return 0;
+}
