@@ -12,8 +12,8 @@
  *  - All data pointers are DEVICE pointers on the context's device, owned and
  *    allocated by the caller; the library never frees caller memory.  Shares are
  *    uint64_t arrays (ring elements of Z_2^64), 8-byte aligned, dense, row-major.
- *  - mpc_shares carries one pointer per party.  MPC_MODE_BOTH (one GPU holds
- *    both parties) needs sh[0] and sh[1]; a PAIR mode needs sh[party] only.
+ *  - mpc_shares carries one pointer per party.  MPC_MODE_BOTH and
+ *    MPC_MODE_PAIR_LOOPBACK need sh[0] and sh[1]; MPC_MODE_PAIR needs sh[party] only.
  *  - Every call is ASYNCHRONOUS on the context's CUDA stream (cudaStream_t passed
  *    as void*); results are valid after the stream is synchronized.
  *  - `off` / `row_off` is the global index of this shard's first element / row:
@@ -50,8 +50,11 @@ typedef enum {
 } mpc_status;
 
 typedef enum {
-    MPC_MODE_BOTH = 0,       /* one GPU simulates both parties; openings add in registers */
-    MPC_MODE_PAIR_HOST = 1   /* one GPU per party; openings exchanged between rounds      */
+    MPC_MODE_BOTH = 0,          /* one GPU simulates both parties; openings add in registers   */
+    MPC_MODE_PAIR = 1,          /* one GPU (process) per party; every opening is exchanged by  *
+                                 * the fused kernels through NVLink peer memory */
+    MPC_MODE_PAIR_LOOPBACK = 2  /* both parties' PAIR kernels in one launch on one GPU,        *
+                                 * exchanging through local memory (same code path; tests)    */
 } mpc_mode;
 
 typedef struct {
@@ -63,7 +66,7 @@ typedef struct {
     uint64_t key_p0;        /* K_0: dealer -> party 0 key                             */
     uint64_t key_p1;        /* K_1: dealer -> party 1 key                             */
     void* cuda_stream;      /* cudaStream_t the calls are enqueued on (NULL = legacy) */
-    void* exchange;         /* PAIR modes: an mpc_exchange (see mpc200_pair.h); else NULL */
+    void* reserved;         /* must be NULL                                            */
 } mpc_config;
 
 typedef struct mpc_ctx mpc_ctx;
@@ -95,6 +98,20 @@ const char* mpc_version(void);
  * used for the ALU roofline.  Returns the count for the last call on ctx. */
 uint64_t mpc_last_call_philox(const mpc_ctx* ctx);
 
+/* ---- PAIR mode plumbing ---------------------------------------------------------
+ * MPC_MODE_PAIR: each party's context allocates its exchange memory (receive buffers and
+ * flags) at creation; the parties swap the opaque handles out of band
+ * (bench/binding use torch.distributed) and connect.  Both parties must then issue the
+ * same sequence of calls with the same shapes; each fused kernel exchanges its openings
+ * with the peer kernel through peer memory.  An exchange that does not complete within
+ * 20 s poisons the context (results undefined) and mpc_ctx_sync returns MPC_ERR_TIMEOUT. */
+#define MPC_PAIR_HANDLE_BYTES 64
+mpc_status mpc_pair_export(mpc_ctx* ctx, void* handle_out /* MPC_PAIR_HANDLE_BYTES */);
+mpc_status mpc_pair_connect(mpc_ctx* ctx, const void* peer_handle);
+/* Synchronize the context stream; MPC_ERR_TIMEOUT if a PAIR exchange timed out,
+ * MPC_ERR_CUDA on an asynchronous CUDA error. */
+mpc_status mpc_ctx_sync(mpc_ctx* ctx);
+
 /* Per-launch timing (for the roofline in bench.py): when enabled, every kernel the
  * context launches is bracketed by CUDA events on the context stream and tagged with
  * its algorithmic Philox4x32-10 block count.  mpc_ctx_kernel_times synchronizes on
@@ -118,7 +135,8 @@ mpc_status mpc_prg_fill(mpc_ctx* ctx, uint64_t key, uint64_t unit0, uint32_t ste
 mpc_status mpc_share(mpc_ctx* ctx, const void* x, int x_is_f64, int owner, mpc_shares out,
                      int64_t n, int64_t off);
 /* S2 open: ring_out[i] = x0+x1 mod 2^64 (may be NULL);
- * f64_out[i] = (int64)ring / 2^scale_bits (may be NULL).  No step. */
+ * f64_out[i] = (int64)ring / 2^scale_bits (may be NULL).  No step.  In MPC_MODE_PAIR both
+ * parties exchange their shares (1 round, 8 B/element) and both receive the result. */
 mpc_status mpc_open(mpc_ctx* ctx, mpc_shares in, int64_t n, uint64_t* ring_out,
                     double* f64_out, int scale_bits);
 

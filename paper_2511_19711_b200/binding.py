@@ -27,7 +27,8 @@ i64 = ctypes.c_int64
 INT = ctypes.c_int
 VP = ctypes.c_void_p
 
-MODE_BOTH, MODE_PAIR_HOST = 0, 1
+MODE_BOTH, MODE_PAIR, MODE_PAIR_LOOPBACK = 0, 1, 2
+PAIR_HANDLE_BYTES = 64
 FORM = {"poly_x": 0, "poly_abs": 1, "relu": 2, "erf": 3}
 STATUS = {0: "OK", 1: "INVALID", 2: "RANGE", 3: "CUDA", 4: "NCCL", 5: "PROTOCOL", 6: "REUSE",
           7: "TIMEOUT", 8: "NOMEM", 9: "UNSUPPORTED"}
@@ -36,7 +37,7 @@ STATUS = {0: "OK", 1: "INVALID", 2: "RANGE", 3: "CUDA", 4: "NCCL", 5: "PROTOCOL"
 class Config(ctypes.Structure):
     _fields_ = [("mode", INT), ("party", INT), ("frac_bits", INT), ("device", INT),
                 ("key_share", u64), ("key_p0", u64), ("key_p1", u64),
-                ("cuda_stream", VP), ("exchange", VP)]
+                ("cuda_stream", VP), ("reserved", VP)]
 
 
 class Shares(ctypes.Structure):
@@ -86,6 +87,9 @@ _SIGS = {
     "mpc_version": [],
     "mpc_last_call_philox": [VP],
     "mpc_ctx_enable_kernel_timing": [VP, INT],
+    "mpc_pair_export": [VP, VP],
+    "mpc_pair_connect": [VP, VP],
+    "mpc_ctx_sync": [VP],
     "mpc_ctx_kernel_times": [VP, VP, INT],
     "mpc_prg_fill": [VP, u64, u64, ctypes.c_uint32, ctypes.c_uint32, VP, i64, INT],
     "mpc_share": [VP, VP, INT, INT, Shares, i64, i64],
@@ -164,10 +168,10 @@ class Ctx:
     """An mpc_ctx: keys, step counter, stream.  MODE_BOTH holds both parties on one GPU."""
 
     def __init__(self, key_share: int, key_p0: int, key_p1: int, device: int = 0, mode: int = MODE_BOTH,
-                 party: int = 0, exchange: int | None = None):
+                 party: int = 0):
         self.device = torch.device("cuda", device)
         self.mode, self.party = mode, party
-        cfg = Config(mode, party, 16, device, key_share, key_p0, key_p1, None, exchange)
+        cfg = Config(mode, party, 16, device, key_share, key_p0, key_p1, None, None)
         h = VP()
         st = _L.mpc_ctx_create(ctypes.byref(cfg), ctypes.byref(h))
         if st != 0:
@@ -188,6 +192,20 @@ class Ctx:
     def _chk(self, st, name):
         if st != 0:
             raise MPCError(f"{name}: {STATUS.get(st, st)}: {_L.mpc_last_error(self._h).decode()}")
+
+    # ---- PAIR plumbing ----
+    def pair_export(self) -> bytes:
+        buf = ctypes.create_string_buffer(PAIR_HANDLE_BYTES)
+        self._chk(_L.mpc_pair_export(self._h, ctypes.cast(buf, VP)), "mpc_pair_export")
+        return buf.raw
+
+    def pair_connect(self, peer_handle: bytes):
+        buf = ctypes.create_string_buffer(bytes(peer_handle), PAIR_HANDLE_BYTES)
+        self._chk(_L.mpc_pair_connect(self._h, ctypes.cast(buf, VP)), "mpc_pair_connect")
+
+    def sync(self):
+        self._stream()
+        self._chk(_L.mpc_ctx_sync(self._h), "mpc_ctx_sync")
 
     def _stream(self):
         _L.mpc_ctx_set_stream(self._h, torch.cuda.current_stream(self.device).cuda_stream)
@@ -222,7 +240,7 @@ class Ctx:
 
     def _empty(self, n):
         mk = lambda: torch.empty(n, dtype=torch.uint64, device=self.device)  # noqa: E731
-        if self.mode == MODE_BOTH:
+        if self.mode in (MODE_BOTH, MODE_PAIR_LOOPBACK):
             return (mk(), mk())
         return (mk(), None) if self.party == 0 else (None, mk())
 

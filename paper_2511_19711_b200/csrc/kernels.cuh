@@ -1,0 +1,452 @@
+// kernels.cuh -- every kernel of the library, written once against a launch policy PA:
+//   BothA : MPC_MODE_BOTH (policy BothP)
+//   PairA : MPC_MODE_PAIR (one party per GPU, grid = that party's CTAs) and
+//           MPC_MODE_PAIR_LOOPBACK (one launch, CTAs [0,G) are party 0 and [G,2G) party 1,
+//           exchanging through local memory -- the same code path as two GPUs).
+// All loops that contain an opening are warp-uniform (PairP exchanges per warp).
+#pragma once
+#include "sched.cuh"
+
+namespace mpc {
+
+// ------------------------------------------------------------------ launch policies ----
+struct BothA {
+    Keys K;
+    __device__ __forceinline__ BothP make(int& cta, int& ncta) const { cta = blockIdx.x; ncta = gridDim.x; return BothP{K}; }
+    __device__ __forceinline__ void done(BothP&) const {}
+};
+
+struct PairA {
+    Keys K;
+    int party;        // remote mode: this GPU's party
+    int loopback;     // 1: both parties in one launch
+    int G;            // CTAs per party
+    XMem xm[2];       // exchange memory of party 0 / 1 (remote: xm[0] only)
+    __device__ __forceinline__ PairP make(int& cta, int& ncta) const {
+        PairP p;
+        p.K = K;
+        int slot_cta;
+        if (loopback) { p.pty = blockIdx.x >= (unsigned)G ? 1 : 0; slot_cta = blockIdx.x - p.pty * G; }
+        else { p.pty = party; slot_cta = blockIdx.x; }
+        cta = slot_cta; ncta = G;
+        p.bind(xm[loopback ? p.pty : 0], slot_cta * (blockDim.x >> 5) + (threadIdx.x >> 5));
+        return p;
+    }
+    __device__ __forceinline__ void done(PairP& p) const { p.unbind(threadIdx.x & 31); }
+};
+
+// ------------------------------------------------------------------ drivers ----
+// GROUP driver: warp <-> 32-unit LTZ group, lane <-> unit.  off % 32 == 0.
+template <class PA, class Body>
+__global__ void __launch_bounds__(256, 3) k_groups(PA pa, i64 n, u64 off, Body body)
+{
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    const int lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+    const i64 ng = (n + 31) >> 5;
+    for (i64 g = (i64)cta * NW + (threadIdx.x >> 5); g < ng; g += (i64)ncta * NW) {
+        const i64 i = g * 32 + lane;
+        body(pr, off + (u64)i, (off >> 5) + (u64)g, i, lane, i < n);
+    }
+    pa.done(pr);
+}
+
+// PAIR driver: lane <-> global unit pair (2P, 2P+1) covering [off, off+n); warp-uniform loop.
+template <class PA, class Body>
+__global__ void __launch_bounds__(256, 3) k_pairs(PA pa, i64 n, u64 off, Body body)
+{
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    const int lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+    const u64 p0 = off >> 1, p1 = (off + (u64)n + 1) >> 1;
+    for (u64 base = ((u64)cta * NW + (threadIdx.x >> 5)) * 32; p0 + base < p1; base += (u64)ncta * NW * 32) {
+        const u64 P = p0 + base + lane;
+        const u64 u = 2 * P;
+        body(pr, u, (i64)(u - off), P < p1);
+    }
+    pa.done(pr);
+}
+
+// ------------------------------------------------------------------ element-wise bodies ----
+struct MulBody {
+    u32 s; SP x, y; SO z; i64 n; int tb;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
+        using S = typename P::S;
+        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
+        S xa = pr.zero(), ya = pr.zero(), xb = pr.zero(), yb = pr.zero();
+        if (v0) { xa = pr.ld(x, i0); ya = pr.ld(y, i0); }
+        if (v1) { xb = pr.ld(x, i0 + 1); yb = pr.ld(y, i0 + 1); }
+        S za, zb;
+        pr.bm2(u, s, xa, ya, xb, yb, za, zb);
+        if (tb) { za = pr.shr_(za, tb); zb = pr.shr_(zb, tb); }
+        if (v0) pr.st(z, i0, za);
+        if (v1) pr.st(z, i0 + 1, zb);
+    }
+};
+
+template <bool WIDE>
+struct CmpBody {
+    u32 s; int w; SP x; SO z; int relu;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
+        typename P::S xv = pr.zero();
+        if (valid) xv = pr.ld(x, i);
+        typename P::S l = pr.template ltz<WIDE>(q, s, w, xv, lane);
+        if (relu) l = pr.bm(u, s + 1, xv, pr.notb(l));
+        if (valid) pr.st(z, i, l);
+    }
+};
+
+template <bool WIDE>
+struct ExpGroupBody {
+    u32 s; ExpK p; SP x; SO z;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
+        typename P::S xv = pr.zero();
+        if (valid) xv = pr.ld(x, i);
+        const typename P::S y = exp_group<WIDE>(pr, u, q, s, p, xv, lane);
+        if (valid) pr.st(z, i, y);
+    }
+};
+
+struct ExpPairBody {
+    u32 s; ExpK p; SP x; SO z; i64 n;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
+        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
+        typename P::S a = pr.zero(), b = pr.zero();
+        if (v0) a = pr.ld(x, i0);
+        if (v1) b = pr.ld(x, i0 + 1);
+        exp_pair(pr, u, s, p, a, b);
+        if (v0) pr.st(z, i0, a);
+        if (v1) pr.st(z, i0 + 1, b);
+    }
+};
+
+template <int KIND, bool WIDE>   // 0 recip, 1 rsqrt
+struct NrGroupBody {
+    u32 s; NrK p; SP x; SO z;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
+        typename P::S xv = pr.zero();
+        if (valid) xv = pr.ld(x, i);
+        typename P::S y;
+        if (KIND == 0) y = recip_group<WIDE>(pr, u, q, s, p, xv, lane);
+        else y = rsqrt_group<WIDE>(pr, u, q, s, p, xv, lane);
+        if (valid) pr.st(z, i, y);
+    }
+};
+
+template <int KIND>
+struct NrPairBody {
+    u32 s; NrK p; SP x; SO z; i64 n;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
+        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
+        typename P::S a = pr.zero(), b = pr.zero(), ya, yb;
+        if (v0) a = pr.ld(x, i0);
+        if (v1) b = pr.ld(x, i0 + 1);
+        if (KIND == 0) recip_pair(pr, u, s, p, a, b, ya, yb);
+        else rsqrt_pair(pr, u, s, p, a, b, ya, yb);
+        if (v0) pr.st(z, i0, ya);
+        if (v1) pr.st(z, i0 + 1, yb);
+    }
+};
+
+template <bool WIDE>
+struct ActBody {
+    u32 s; ActK p; SP x; SO z;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
+        typename P::S xv = pr.zero();
+        if (valid) xv = pr.ld(x, i);
+        const typename P::S y = act_group<WIDE>(pr, u, q, s, p, xv, lane);
+        if (valid) pr.st(z, i, y);
+    }
+};
+
+// S2 in PAIR modes: exchange the shares, both parties learn rec (reveal_to both)
+struct OpenBody {
+    SP x; u64* ring; double* f; i64 n; double inv; int writer;   // writer: party that stores (-1: own)
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
+        (void)u; (void)q;
+        typename P::S mine = pr.zero();
+        if (valid) mine = pr.ld(x, i);
+        const u64 v = pr.open(mine);
+        if (valid && (writer < 0 || pr.party() == writer)) {
+            if (ring) ring[i] = v;
+            if (f) f[i] = (double)(i64)v * inv;
+        }
+    }
+};
+
+// ------------------------------------------------------------------ row tiles ----
+// One CTA owns a tile of 32 consecutive rows (32-aligned global row index); persistent loop.
+
+// MAX_row tree (R22): levels ping-pong in A/B (stride H = ceil(cols/2));
+// the last level writes mx[rr].  Steps s + 2*lv (LTZ), s + 2*lv + 1 (mux BM).
+template <bool WIDE, class P>
+__device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i64 cols, int R, u64 g0,
+                                         SO A, SO B, i64 H, SO mx)
+{
+    using S = typename P::S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    i64 m = cols;
+    int lv = 0;
+    SP cur = in;
+    i64 li = ldi;
+    while (m > 1) {
+        const i64 h = m / 2, mn = h + (m & 1);
+        SO o; i64 lo;
+        if (mn == 1) { o = mx; lo = 1; }
+        else if (lv & 1) { o = B; lo = H; }
+        else { o = A; lo = H; }
+        const u32 sl = s + 2u * (u32)lv;
+        const u64 ubase = g0 * (u64)h;                 // multiple of 32 (g0 is)
+        const FastDiv dh = make_fastdiv((u32)h);
+        for (i64 g = warp; g < h; g += NW) {            // 32*h units = h groups
+            const i64 v = g * 32 + lane;
+            const bool valid = v < (i64)R * h;
+            i64 rr = 0, i = 0;
+            S d = pr.zero(), y = pr.zero();
+            if (valid) {
+                rr = fdiv((u32)v, dh); i = v - rr * h;
+                y = pr.ld(cur, rr * li + i + h);
+                d = pr.sub(pr.ld(cur, rr * li + i), y);
+            }
+            const u64 q = (ubase >> 5) + (u64)g;
+            const S c = pr.notb(pr.template ltz<WIDE>(q, sl, w, d, lane));
+            const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
+            if (valid) {
+                pr.st(o, rr * lo + i, sel);
+                if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, pr.ld(cur, rr * li + m - 1));
+            }
+        }
+        __syncthreads();
+        cur = SP{{o.p[0], o.p[1]}};
+        li = lo;
+        m = mn;
+        ++lv;
+    }
+    if (cols == 1) {
+        for (int rr = threadIdx.x; rr < R; rr += blockDim.x) pr.st(mx, rr, pr.ld(in, rr * ldi));
+        __syncthreads();
+    }
+}
+
+// per-row Newton-Raphson over the tile's rows: warp 0, lane <-> row (LTZ group = the tile)
+template <int KIND, bool WIDE, class P>
+__device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g0, SP x, SO y)
+{
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const bool valid = lane < R;
+        typename P::S xv = pr.zero();
+        if (valid) xv = pr.ld(x, lane);
+        typename P::S r;
+        if (KIND == 0) r = recip_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
+        else r = rsqrt_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
+        if (valid) pr.st(y, lane, r);
+    }
+    __syncthreads();
+}
+
+struct SoftmaxArgs {
+    u32 s_max, s_exp, s_rec, s_mul;
+    int w;
+    ExpK ek;
+    NrK rk;
+    SP x;
+    SO z;
+    i64 rows, cols;
+    u64 row_off;
+    u64* gscratch;          // per-CTA work tiles when they do not fit in shared memory
+    i64 work_u64;           // u64 words of one work tile
+    int use_smem;
+};
+
+// work tile (u64 words), H = ceil(cols/2): A0 A1 B0 B1 (4 x 32H; reused as E0 E1 = 2 x 32 cols),
+// MX0 MX1 S0 S1 R0 R1 (6 x 32)
+__host__ __device__ inline i64 softmax_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 6 * 32; }
+
+template <bool WIDE, class PA>
+__global__ void __launch_bounds__(256, 3) k_softmax(PA pa, SoftmaxArgs a)
+{
+    extern __shared__ __align__(16) u64 smem[];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using S = typename decltype(pr)::S;
+    // loopback: the two parties' CTAs need separate tiles of scratch
+    const int wslot = blockIdx.x;
+    u64* W = a.use_smem ? smem : a.gscratch + (i64)wslot * a.work_u64;
+    const i64 C = a.cols, H = (C + 1) / 2;
+    SO A{{W, W + 32 * H}}, B{{W + 64 * H, W + 96 * H}}, E{{W, W + 32 * C}};
+    u64* X = W + 128 * H;
+    SO MX{{X, X + 32}}, SS{{X + 64, X + 96}}, RR{{X + 128, X + 160}};
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const i64 ntiles = (a.rows + 31) / 32;
+    const FastDiv dC = make_fastdiv((u32)C);
+    for (i64 tile = cta; tile < ntiles; tile += ncta) {
+        const i64 r0 = tile * 32;
+        const int R = (int)min((i64)32, a.rows - r0);
+        const u64 g0 = a.row_off + (u64)r0;                       // global row of the tile
+        const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        // 1. m = MAX_row(x)
+        tile_max<WIDE>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, H, MX);
+        // 2-3. e = EXP(x - m), element units g0*C + e
+        const i64 ne = (i64)R * C;
+        const u64 ub = g0 * (u64)C;
+        const SP MXc{{MX.p[0], MX.p[1]}};
+        if (a.ek.clamp) {
+            for (i64 g = warp; g < (ne + 31) / 32; g += NW) {
+                const i64 e = g * 32 + lane;
+                const bool valid = e < ne;
+                S d = pr.zero();
+                if (valid) d = pr.sub(pr.ld(xt, e), pr.ld(MXc, fdiv((u32)e, dC)));
+                const S y = exp_group<WIDE>(pr, ub + e, (ub >> 5) + g, a.s_exp, a.ek, d, lane);
+                if (valid) pr.st(E, e, y);
+            }
+        } else {
+            for (i64 base = (i64)warp * 32; base < (ne + 1) / 2; base += (i64)NW * 32) {
+                const i64 e = 2 * (base + lane);
+                const bool va = e < ne, vb = e + 1 < ne;
+                S da = pr.zero(), db = pr.zero();
+                if (va) da = pr.sub(pr.ld(xt, e), pr.ld(MXc, fdiv((u32)e, dC)));
+                if (vb) db = pr.sub(pr.ld(xt, e + 1), pr.ld(MXc, fdiv((u32)(e + 1), dC)));
+                exp_pair(pr, ub + e, a.s_exp, a.ek, da, db);
+                if (va) pr.st(E, e, da);
+                if (vb) pr.st(E, e + 1, db);
+            }
+        }
+        __syncthreads();
+        // 4. S = rowsum(e) (local): warp per row
+        const SP Ec{{E.p[0], E.p[1]}};
+        for (int rr = warp; rr < R; rr += NW) {
+            S acc = pr.zero();
+            for (i64 j = lane; j < C; j += 32) acc = pr.add(acc, pr.ld(Ec, rr * C + j));
+            acc = pr.sumw(acc);
+            if (lane == 0) pr.st(SS, rr, acc);
+        }
+        __syncthreads();
+        // 5. r = RECIP(S), row units
+        tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR);
+        // 6. out = MT(e, r), element units
+        const SP Rc{{RR.p[0], RR.p[1]}};
+        for (i64 base = (i64)warp * 32; base < (ne + 1) / 2; base += (i64)NW * 32) {
+            const i64 e = 2 * (base + lane);
+            const bool va = e < ne, vb = e + 1 < ne;
+            S ea = pr.zero(), eb = pr.zero(), ra = pr.zero(), rb = pr.zero();
+            if (va) { ea = pr.ld(Ec, e); ra = pr.ld(Rc, fdiv((u32)e, dC)); }
+            if (vb) { eb = pr.ld(Ec, e + 1); rb = pr.ld(Rc, fdiv((u32)(e + 1), dC)); }
+            S za, zb;
+            pr.bm2(ub + e, a.s_mul, ea, ra, eb, rb, za, zb);
+            const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
+            if (va) pr.st(zt, e, pr.shr_(za, FRAC));
+            if (vb) pr.st(zt, e + 1, pr.shr_(zb, FRAC));
+        }
+        __syncthreads();
+    }
+    pa.done(pr);
+}
+
+struct MaxArgs {
+    u32 s; int w; SP x; SO z; i64 rows, cols; u64 row_off;
+    u64* gscratch; i64 work_u64; int use_smem;
+};
+__host__ __device__ inline i64 max_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 2 * 32; }
+
+template <bool WIDE, class PA>
+__global__ void __launch_bounds__(256, 3) k_max(PA pa, MaxArgs a)
+{
+    extern __shared__ __align__(16) u64 smem[];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
+    const i64 C = a.cols, H = (C + 1) / 2;
+    SO A{{W, W + 32 * H}}, B{{W + 64 * H, W + 96 * H}}, MX{{W + 128 * H, W + 128 * H + 32}};
+    const i64 ntiles = (a.rows + 31) / 32;
+    for (i64 tile = cta; tile < ntiles; tile += ncta) {
+        const i64 r0 = tile * 32;
+        const int R = (int)min((i64)32, a.rows - r0);
+        const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        tile_max<WIDE>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, H, MX);
+        const SP MXc{{MX.p[0], MX.p[1]}};
+        const SO zt{{a.z.p[0] ? a.z.p[0] + r0 : nullptr, a.z.p[1] ? a.z.p[1] + r0 : nullptr}};
+        for (int rr = threadIdx.x; rr < R; rr += blockDim.x) pr.st(zt, rr, pr.ld(MXc, rr));
+        __syncthreads();
+    }
+    pa.done(pr);
+}
+
+struct LnArgs {
+    u32 s_sq, s_rs, s_mul; NrK rk; SP x; SO z; i64 rows, cols; u64 row_off;
+    int mean_mode; u64 e_invd, e_eps;
+};
+
+// LAYERNORM: mu, c = x - mu, v = mean(MT(c,c)) + eps, r = RSQRT(v), out = MT(c, r)
+template <bool WIDE, class PA>
+__global__ void __launch_bounds__(256, 3) k_ln(PA pa, LnArgs a)
+{
+    __shared__ u64 MU[2][32], V[2][32], RS[2][32];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using S = typename decltype(pr)::S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const i64 C = a.cols;
+    const i64 ntiles = (a.rows + 31) / 32;
+    const FastDiv dC = make_fastdiv((u32)C);
+    const SO MUo{{MU[0], MU[1]}}, Vo{{V[0], V[1]}}, RSo{{RS[0], RS[1]}};
+    const SP MUc{{MU[0], MU[1]}}, Vc{{V[0], V[1]}}, RSc{{RS[0], RS[1]}};
+    for (i64 tile = cta; tile < ntiles; tile += ncta) {
+        const i64 r0 = tile * 32;
+        const int R = (int)min((i64)32, a.rows - r0);
+        const u64 g0 = a.row_off + (u64)r0;
+        const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        for (int rr = warp; rr < R; rr += NW) {
+            S acc = pr.zero();
+            for (i64 j = lane; j < C; j += 32) acc = pr.add(acc, pr.ld(xt, rr * C + j));
+            S mu = pr.sumw(acc);
+            mu = a.mean_mode == 0 ? pr.mulf(mu, a.e_invd) : pr.divp(mu, C);
+            // q = MT(c, c) over the row, element units; lanes take unit pairs (2j, 2j+1)
+            S qs = pr.zero();
+            const u64 ub = (g0 + (u64)rr) * (u64)C;
+            const i64 j0 = -(i64)(ub & 1);
+            for (i64 j = j0 + 2 * lane, jb = j0; jb < C; j += 64, jb += 64) {
+                const bool va = j >= 0 && j < C, vb = j + 1 >= 0 && j + 1 < C;
+                S ca = pr.zero(), cb = pr.zero();
+                if (va) ca = pr.sub(pr.ld(xt, rr * C + j), mu);
+                if (vb) cb = pr.sub(pr.ld(xt, rr * C + j + 1), mu);
+                S za, zb;
+                pr.bm2(ub + (u64)j, a.s_sq, ca, ca, cb, cb, za, zb);
+                if (va) qs = pr.add(qs, pr.shr_(za, FRAC));
+                if (vb) qs = pr.add(qs, pr.shr_(zb, FRAC));
+            }
+            S v = pr.sumw(qs);
+            v = a.mean_mode == 0 ? pr.mulf(v, a.e_invd) : pr.divp(v, C);
+            v = pr.addp(v, a.e_eps);
+            if (lane == 0) { pr.st(MUo, rr, mu); pr.st(Vo, rr, v); }
+        }
+        __syncthreads();
+        tile_nr<1, WIDE>(pr, a.s_rs, a.rk, R, g0, Vc, RSo);
+        const i64 ne = (i64)R * C;
+        const u64 ub = g0 * (u64)C;            // even: g0 is a multiple of 32
+        for (i64 base = (i64)warp * 32; base < (ne + 1) / 2; base += (i64)NW * 32) {
+            const i64 e = 2 * (base + lane);
+            const bool va = e < ne, vb = e + 1 < ne;
+            S ca = pr.zero(), cb = pr.zero(), ra = pr.zero(), rb = pr.zero();
+            if (va) { const i64 r = fdiv((u32)e, dC); ca = pr.sub(pr.ld(xt, e), pr.ld(MUc, r)); ra = pr.ld(RSc, r); }
+            if (vb) { const i64 r = fdiv((u32)(e + 1), dC); cb = pr.sub(pr.ld(xt, e + 1), pr.ld(MUc, r)); rb = pr.ld(RSc, r); }
+            S za, zb;
+            pr.bm2(ub + e, a.s_mul, ca, ra, cb, rb, za, zb);
+            const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
+            if (va) pr.st(zt, e, pr.shr_(za, FRAC));
+            if (vb) pr.st(zt, e + 1, pr.shr_(zb, FRAC));
+        }
+        __syncthreads();
+    }
+    pa.done(pr);
+}
+
+}  // namespace mpc

@@ -1,9 +1,13 @@
-// mpc200.cu -- kernels (MPC_MODE_BOTH) and the C ABI of include/mpc200.h.
+// mpc200.cu -- the C ABI of include/mpc200.h: validation, step accounting, launches.
 //
-// Every kernel here executes the protocol of DESIGN.md section 2 for BOTH parties
-// and the dealer on one GPU: Philox triples in registers, masked values formed
-// and "opened" in registers, both parties' share updates.  No tensor cores: the
-// path is element-wise / bitwise integer work.
+// Kernels (kernels.cuh) are written once against a launch policy:
+//   MPC_MODE_BOTH          BothA: one GPU executes both parties and the dealer; openings
+//                          are formed in registers.
+//   MPC_MODE_PAIR          PairA: this GPU is one party; every opening is a warp-level
+//                          exchange with the peer party's kernel through NVLink peer memory
+//                          (cooperative launch, so every CTA is resident on both GPUs).
+//   MPC_MODE_PAIR_LOOPBACK PairA with both parties' CTAs in one launch on one GPU.
+// No tensor cores: the path is element-wise / bitwise integer work.
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -12,15 +16,22 @@
 #include <cuda_runtime.h>
 
 #include "mpc200.h"
-#include "sched_both.cuh"
-#include "rows_both.cuh"
+#include "kernels.cuh"
 
 using namespace mpc;
 
-// ------------------------------------------------------------------ context ----
-// per-launch timing records (mpc_ctx_enable_kernel_timing): CUDA events on the ctx
-// stream around every launch, plus the launch's algorithmic Philox count.
+#define TPB 256
+#define NWARPS (TPB / 32)
+
+// per-launch timing records (mpc_ctx_enable_kernel_timing)
 struct TimingRec { const char* name; cudaEvent_t a, b; u64 philox_at; u64 philox; u64 units; };
+
+// one party's exchange memory (single cudaMalloc so it can be exported with cudaIpc)
+struct XAlloc {
+    void* base;
+    size_t bytes;
+    u64 rx_off, flag_off, round_off, err_off;
+};
 
 struct mpc_ctx {
     mpc_config cfg;
@@ -31,14 +42,22 @@ struct mpc_ctx {
     mpc_stats st;
     u64 last_philox;
     char err[512];
-    void* scratch;         // ctx-owned, grow-only, stream-ordered on `stream`
+    void* scratch;          // ctx-owned, grow-only, stream-ordered on `stream`
     size_t scratch_bytes;
     int timing;
     TimingRec* recs;
     int nrec, caprec;
     cudaEvent_t* pool;
     int npool, cappool;
+    // PAIR modes
+    int slots;              // warp slots of the exchange memory
+    XAlloc xa[2];           // own (and, loopback, the other party's) exchange memory
+    void* peer_base;        // MPC_MODE_PAIR: the peer's exchange memory (cudaIpc-mapped)
+    int connected;
 };
+
+static bool is_pair(const mpc_ctx* c) { return c->cfg.mode != MPC_MODE_BOTH; }
+static bool is_loop(const mpc_ctx* c) { return c->cfg.mode == MPC_MODE_PAIR_LOOPBACK; }
 
 static cudaEvent_t ev_get(mpc_ctx* c)
 {
@@ -124,7 +143,7 @@ static int gate_count(int w)
     return g;
 }
 
-// accounting of one primitive over n units (DESIGN.md 2.3 / 2.4 cost model)
+// accounting of one primitive over n units (DESIGN.md 2.3 / 2.4 cost model; both parties + dealer)
 static void acct_beaver(mpc_ctx* c, u64 n)
 {
     c->last_philox += 2 * n + (n + 1) / 2;
@@ -148,7 +167,7 @@ static int grid_for(const mpc_ctx* c, i64 work_items, int threads, int per_sm = 
     return (int)b;
 }
 
-// ------------------------------------------------------------------ kernels ----
+// ------------------------------------------------------------------ simple kernels ----
 __global__ void k_prg_fill(Key key, u64 unit0, u32 step, u32 slot, u32* out, i64 n, int reps)
 {
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
@@ -159,9 +178,9 @@ __global__ void k_prg_fill(Key key, u64 unit0, u32 step, u32 slot, u32* out, i64
     }
 }
 
-// S1: v = E(x); owner share v - r, other r; r = PRG(K_s, off+i, s, 0)
-__global__ void k_share(const void* x, int f64, int owner, u64* s0, u64* s1, i64 n, u64 off,
-                        u32 s, Key ks)
+// S1: v = E(x); owner share v - r, other r; r = PRG(K_s, off+i, s, 0).  A PAIR party writes only
+// its own share (x may be NULL on the non-owner).
+__global__ void k_share(const void* x, int f64, int owner, u64* s0, u64* s1, i64 n, u64 off, u32 s, Key ks)
 {
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
         const uint4 R = prg(ks, off + (u64)i, s, 0);
@@ -187,142 +206,16 @@ __global__ void k_open(const u64* s0, const u64* s1, i64 n, u64* ring, double* f
     }
 }
 
-__global__ void k_trunc(const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, int bits)
+__global__ void k_trunc(SP x, SO z, i64 n, int bits)
 {
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-        z0[i] = shr(x0[i], bits);
-        z1[i] = shr(x1[i], bits);
+        if (z.p[0]) z.p[0][i] = shr(x.p[0][i], bits);
+        if (z.p[1]) z.p[1][i] = shr(x.p[1][i], bits);
     }
 }
-
-// ---- generic drivers ---------------------------------------------------------------
-// PAIR driver: thread <-> global unit pair (2P, 2P+1) covering [off, off+n).
-template <class Body>
-__global__ void __launch_bounds__(256, 3) k_pairs(i64 n, u64 off, Body body)
-{
-    const u64 p0 = off >> 1, p1 = (off + (u64)n + 1) >> 1;
-    const u64 stride = (u64)gridDim.x * blockDim.x;
-    for (u64 P = p0 + blockIdx.x * (u64)blockDim.x + threadIdx.x; P < p1; P += stride) {
-        const u64 u = 2 * P;
-        const i64 i0 = (i64)(u - off);    // may be -1 when off is odd
-        body(u, i0);
-    }
-}
-
-// GROUP driver: warp <-> 32-unit LTZ group, lane <-> unit.  off % 32 == 0.
-template <class Body>
-__global__ void __launch_bounds__(256, 3) k_groups(i64 n, u64 off, Body body)
-{
-    const int lane = threadIdx.x & 31;
-    const i64 ng = (n + 31) >> 5;
-    const i64 nw = ((i64)gridDim.x * blockDim.x) >> 5;
-    for (i64 g = ((i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5; g < ng; g += nw) {
-        const i64 i = g * 32 + lane;
-        body(off + (u64)i, (off >> 5) + (u64)g, i, lane, i < n);
-    }
-}
-
-struct Ptr2 { const u64* p0; const u64* p1; };
-struct Out2 { u64* p0; u64* p1; };
-
-__device__ __forceinline__ Sh ld(Ptr2 a, i64 i) { return {a.p0[i], a.p1[i]}; }
-__device__ __forceinline__ void st(Out2 a, i64 i, Sh v) { a.p0[i] = v.s0; a.p1[i] = v.s1; }
-
-// ---- element-wise bodies ----------------------------------------------------------------
-struct MulBody {
-    Keys K; u32 s; Ptr2 x, y; Out2 z; i64 n; int tb;
-    __device__ void operator()(u64 u, i64 i0) const {
-        const bool v0 = i0 >= 0, v1 = i0 + 1 < n;
-        Sh xa = {0, 0}, ya = {0, 0}, xb = {0, 0}, yb = {0, 0};
-        if (v0) { xa = ld(x, i0); ya = ld(y, i0); }
-        if (v1) { xb = ld(x, i0 + 1); yb = ld(y, i0 + 1); }
-        Sh za, zb;
-        bm2(K, u, s, xa, ya, xb, yb, za, zb);
-        if (tb) { za = sh_shr(za, tb); zb = sh_shr(zb, tb); }
-        if (v0) st(z, i0, za);
-        if (v1) st(z, i0 + 1, zb);
-    }
-};
-
-template <bool WIDE>
-struct CmpBody {
-    Keys K; u32 s; int w; Ptr2 x; Out2 z; int relu;
-    __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
-        Sh xv = {0, 0};
-        if (valid) xv = ld(x, i);
-        Sh l = ltz<WIDE>(K, q, s, w, xv, lane);
-        if (relu) l = bm(K, u, s + 1, xv, sh_not(l));
-        if (valid) st(z, i, l);
-    }
-};
-
-template <bool WIDE>
-struct ExpGroupBody {
-    Keys K; u32 s; ExpK p; Ptr2 x; Out2 z;
-    __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
-        Sh xv = {0, 0};
-        if (valid) xv = ld(x, i);
-        const Sh y = exp_group<WIDE>(K, u, q, s, p, xv, lane);
-        if (valid) st(z, i, y);
-    }
-};
-
-struct ExpPairBody {
-    Keys K; u32 s; ExpK p; Ptr2 x; Out2 z; i64 n;
-    __device__ void operator()(u64 u, i64 i0) const {
-        const bool v0 = i0 >= 0, v1 = i0 + 1 < n;
-        Sh a = {0, 0}, b = {0, 0};
-        if (v0) a = ld(x, i0);
-        if (v1) b = ld(x, i0 + 1);
-        exp_pair(K, u, s, p, a, b);
-        if (v0) st(z, i0, a);
-        if (v1) st(z, i0 + 1, b);
-    }
-};
-
-template <int KIND, bool WIDE>   // 0 recip, 1 rsqrt
-struct NrGroupBody {
-    Keys K; u32 s; NrK p; Ptr2 x; Out2 z;
-    __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
-        Sh xv = {0, 0};
-        if (valid) xv = ld(x, i);
-        Sh y;
-        if (KIND == 0) y = recip_group<WIDE>(K, u, q, s, p, xv, lane);
-        else y = rsqrt_group<WIDE>(K, u, q, s, p, xv, lane);
-        if (valid) st(z, i, y);
-    }
-};
-
-template <int KIND>
-struct NrPairBody {
-    Keys K; u32 s; NrK p; Ptr2 x; Out2 z; i64 n;
-    __device__ void operator()(u64 u, i64 i0) const {
-        const bool v0 = i0 >= 0, v1 = i0 + 1 < n;
-        Sh a = {0, 0}, b = {0, 0};
-        if (v0) a = ld(x, i0);
-        if (v1) b = ld(x, i0 + 1);
-        Sh ya, yb;
-        if (KIND == 0) recip_pair(K, u, s, p, a, b, ya, yb);
-        else rsqrt_pair(K, u, s, p, a, b, ya, yb);
-        if (v0) st(z, i0, ya);
-        if (v1) st(z, i0 + 1, yb);
-    }
-};
-
-template <bool WIDE>
-struct ActBody {
-    Keys K; u32 s; ActK p; Ptr2 x; Out2 z;
-    __device__ void operator()(u64 u, u64 q, i64 i, int lane, bool valid) const {
-        Sh xv = {0, 0};
-        if (valid) xv = ld(x, i);
-        const Sh y = act_group<WIDE>(K, u, q, s, p, xv, lane);
-        if (valid) st(z, i, y);
-    }
-};
 
 // maxpool: gather each k x k window (public zero padding) into a row
-__global__ void k_pool_gather(Ptr2 x, Out2 rowsbuf, int N, int C, int H, int W, int k, int stride,
-                              int pad, int Ho, int Wo)
+__global__ void k_pool_gather(SP x, SO rowsbuf, int N, int C, int H, int W, int k, int stride, int pad, int Ho, int Wo)
 {
     const i64 rows = (i64)N * C * Ho * Wo, kk = (i64)k * k;
     for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < rows * kk; t += (i64)gridDim.x * blockDim.x) {
@@ -330,24 +223,76 @@ __global__ void k_pool_gather(Ptr2 x, Out2 rowsbuf, int N, int C, int H, int W, 
         const int dy = (int)(e / k), dx = (int)(e - (i64)dy * k);
         const i64 ow = o % Wo, oh = (o / Wo) % Ho, c = (o / ((i64)Wo * Ho)) % C, img = o / ((i64)Wo * Ho * C);
         const i64 iy = oh * stride - pad + dy, ix = ow * stride - pad + dx;
-        u64 a = 0, b = 0;
-        if (iy >= 0 && iy < H && ix >= 0 && ix < W) {
-            const i64 idx = ((img * C + c) * H + iy) * W + ix;
-            a = x.p0[idx]; b = x.p1[idx];
-        }
-        rowsbuf.p0[t] = a; rowsbuf.p1[t] = b;
+        const bool in = iy >= 0 && iy < H && ix >= 0 && ix < W;
+        const i64 idx = ((img * C + c) * H + iy) * W + ix;
+        for (int p = 0; p < 2; ++p)
+            if (rowsbuf.p[p]) rowsbuf.p[p][t] = in ? x.p[p][idx] : 0ull;
     }
 }
 
-// ------------------------------------------------------------------ host helpers ----
-#define TPB 256
+// ------------------------------------------------------------------ launch machinery ----
+static XMem xmem_of(const mpc_ctx* c, int which)
+{
+    const XAlloc& a = c->xa[which];
+    char* b = (char*)a.base;
+    XMem m;
+    m.rx = (u64*)(b + a.rx_off); m.flag = (u64*)(b + a.flag_off); m.round = (u64*)(b + a.round_off);
+    m.err = (int*)(b + a.err_off); m.slots = c->slots;
+    if (is_loop(c)) {
+        const XAlloc& o = c->xa[1 - which];
+        char* ob = (char*)o.base;
+        m.prx = (u64*)(ob + o.rx_off); m.pflag = (u64*)(ob + o.flag_off);
+    } else {
+        char* pb = (char*)c->peer_base;
+        m.prx = (u64*)(pb + a.rx_off); m.pflag = (u64*)(pb + a.flag_off);
+    }
+    return m;
+}
 
-// resident CTAs per SM of a kernel at TPB threads (queried once per instantiation)
-template <class K>
-static int occupancy(K kern)
+static PairA pair_args(const mpc_ctx* c, int G)
+{
+    PairA pa;
+    pa.K = c->K;
+    pa.party = c->cfg.party;
+    pa.loopback = is_loop(c) ? 1 : 0;
+    pa.G = G;
+    pa.xm[0] = xmem_of(c, 0);
+    pa.xm[1] = is_loop(c) ? xmem_of(c, 1) : pa.xm[0];
+    return pa;
+}
+
+// CTAs per party for a PAIR launch: every CTA of both parties must be co-resident
+template <class Kern>
+static int pair_ctas(mpc_ctx* c, Kern kern, size_t dyn, i64 want)
 {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPB, 0) != cudaSuccess || nb < 1) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPB, dyn) != cudaSuccess || nb < 1) nb = 1;
+    i64 cap = (i64)nb * c->sm_count / (is_loop(c) ? 2 : 1);
+    cap = std::min<i64>(cap, c->slots / NWARPS);
+    i64 G = std::min<i64>(want, cap);
+    return (int)std::max<i64>(G, 1);
+}
+
+template <class Kern, class... Args>
+static mpc_status launch_pair_kernel(mpc_ctx* c, Kern kern, int G, size_t dyn, const char* name, Args... args)
+{
+    if (!is_loop(c) && !c->connected) return fail(c, MPC_ERR_INVALID, "%s: PAIR context not connected", name);
+    PairA pa = pair_args(c, G);
+    void* argv[] = {(void*)&pa, (void*)&args...};
+    const int grid = G * (is_loop(c) ? 2 : 1);
+    rec_begin(c, name, 0);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, grid, TPB, argv, dyn, c->stream);
+    rec_end(c);
+    c->st.launches++;
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: cooperative launch: %s", name, cudaGetErrorString(e));
+    return cuda_check(c, name);
+}
+
+template <class K>
+static int occupancy(K kern, size_t dyn = 0)
+{
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPB, dyn) != cudaSuccess || nb < 1) nb = 1;
     return nb;
 }
 
@@ -355,37 +300,92 @@ template <class Body>
 static mpc_status launch_pairs(mpc_ctx* c, i64 n, u64 off, const Body& b, const char* name)
 {
     if (n <= 0) return MPC_OK;
-    static int per_sm = occupancy(k_pairs<Body>);
     const i64 npairs = (i64)(((off + (u64)n + 1) >> 1) - (off >> 1));
-    rec_begin(c, name, (u64)n);
-    k_pairs<Body><<<grid_for(c, npairs, TPB, per_sm), TPB, 0, c->stream>>>(n, off, b);
-    rec_end(c);
-    c->st.launches++;
-    return cuda_check(c, name);
+    if (!is_pair(c)) {
+        static int per_sm = occupancy(k_pairs<BothA, Body>);
+        rec_begin(c, name, (u64)n);
+        k_pairs<BothA, Body><<<grid_for(c, npairs, TPB, per_sm), TPB, 0, c->stream>>>(BothA{c->K}, n, off, b);
+        rec_end(c);
+        c->st.launches++;
+        return cuda_check(c, name);
+    }
+    const int G = pair_ctas(c, k_pairs<PairA, Body>, 0, (npairs + TPB - 1) / TPB);
+    return launch_pair_kernel(c, k_pairs<PairA, Body>, G, 0, name, n, off, b);
 }
 
 template <class Body>
 static mpc_status launch_groups(mpc_ctx* c, i64 n, u64 off, const Body& b, const char* name)
 {
     if (n <= 0) return MPC_OK;
-    static int per_sm = occupancy(k_groups<Body>);
-    rec_begin(c, name, (u64)n);
-    k_groups<Body><<<grid_for(c, ((n + 31) / 32) * 32, TPB, per_sm), TPB, 0, c->stream>>>(n, off, b);
+    if (!is_pair(c)) {
+        static int per_sm = occupancy(k_groups<BothA, Body>);
+        rec_begin(c, name, (u64)n);
+        k_groups<BothA, Body><<<grid_for(c, ((n + 31) / 32) * 32, TPB, per_sm), TPB, 0, c->stream>>>(BothA{c->K}, n, off, b);
+        rec_end(c);
+        c->st.launches++;
+        return cuda_check(c, name);
+    }
+    const int G = pair_ctas(c, k_groups<PairA, Body>, 0, (((n + 31) / 32) * 32 + TPB - 1) / TPB);
+    return launch_pair_kernel(c, k_groups<PairA, Body>, G, 0, name, n, off, b);
+}
+
+static const size_t SMEM_LIMIT = 72 * 1024;      // keep 3 CTAs per SM
+
+// fused row kernels: work tile in shared memory when it fits, else a per-CTA global tile
+template <class Args, class KB, class KP>
+static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 work_u64, const char* name)
+{
+    const i64 ntiles = (rows + 31) / 32;
+    const size_t wbytes = sizeof(u64) * (size_t)work_u64;
+    const bool smem = work_u64 > 0 && wbytes <= SMEM_LIMIT;
+    const size_t dyn = smem ? wbytes : 0;
+    if (smem) {
+        cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes);
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes);
+    }
+    int grid;
+    if (!is_pair(c)) grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(kb, dyn));
+    else grid = pair_ctas(c, kp, dyn, ntiles);
+    const int launched = grid * (is_loop(c) ? 2 : 1);
+    a.use_smem = smem ? 1 : 0;
+    a.gscratch = nullptr;
+    a.work_u64 = work_u64;
+    if (!smem && work_u64 > 0) {
+        a.gscratch = (u64*)scratch(c, wbytes * (size_t)launched);
+        if (!a.gscratch) return fail(c, MPC_ERR_NOMEM, "%s: scratch %zu bytes", name, wbytes * (size_t)launched);
+    }
+    if (is_pair(c)) return launch_pair_kernel(c, kp, grid, dyn, name, a);
+    rec_begin(c, name, (u64)rows);
+    kb<<<grid, TPB, dyn, c->stream>>>(BothA{c->K}, a);
     rec_end(c);
     c->st.launches++;
     return cuda_check(c, name);
 }
 
-static bool bad2(const mpc_ctx* c, mpc_shares s)
+// ------------------------------------------------------------------ validation helpers ----
+// shares argument valid for the mode: both pointers (BOTH / LOOPBACK) or sh[party] (PAIR)
+static bool bad_sh(const mpc_ctx* c, mpc_shares s)
 {
-    (void)c;
+    if (c->cfg.mode == MPC_MODE_PAIR) {
+        const uint64_t* p = s.sh[c->cfg.party];
+        return !p || ((uintptr_t)p & 7);
+    }
     return !s.sh[0] || !s.sh[1] || ((uintptr_t)s.sh[0] & 7) || ((uintptr_t)s.sh[1] & 7);
 }
+static SP spv(const mpc_ctx* c, mpc_shares s)
+{
+    SP r{{s.sh[0], s.sh[1]}};
+    if (c->cfg.mode == MPC_MODE_PAIR) r.p[1 - c->cfg.party] = nullptr;
+    return r;
+}
+static SO sov(const mpc_ctx* c, mpc_shares s)
+{
+    SO r{{s.sh[0], s.sh[1]}};
+    if (c->cfg.mode == MPC_MODE_PAIR) r.p[1 - c->cfg.party] = nullptr;
+    return r;
+}
 
-static Ptr2 P(mpc_shares s) { return Ptr2{s.sh[0], s.sh[1]}; }
-static Out2 O(mpc_shares s) { return Out2{s.sh[0], s.sh[1]}; }
-
-// common prologue of a compute call: validates mode and step budget, resets counters
+// common prologue of a compute call: validates the step budget, resets the per-call counter
 static mpc_status begin(mpc_ctx* c, u64 steps_needed)
 {
     if (!c) return MPC_ERR_INVALID;
@@ -426,17 +426,45 @@ static void acct_exp(mpc_ctx* c, u64 n, const mpc_exp_p* p)
     for (int k = 0; k < p->t; ++k) acct_beaver(c, n);
 }
 
+static int max_levels_h(i64 cols) { int L = 0; i64 m = cols; while (m > 1) { m = (m + 1) / 2; ++L; } return L; }
+
+static void acct_max(mpc_ctx* c, i64 rows, i64 cols, int w)
+{
+    i64 m = cols;
+    while (m > 1) {
+        const i64 h = m / 2;
+        acct_ltz(c, (u64)(rows * h), w);
+        acct_beaver(c, (u64)(rows * h));
+        m = h + (m & 1);
+    }
+}
+
+// ------------------------------------------------------------------ PAIR memory ----
+static mpc_status xalloc(mpc_ctx* c, XAlloc& a)
+{
+    const size_t S = (size_t)c->slots;
+    a.rx_off = 0;
+    a.flag_off = a.rx_off + S * XSLOT_RX * sizeof(u64);
+    a.round_off = a.flag_off + S * 4 * sizeof(u64);
+    a.err_off = a.round_off + S * sizeof(u64);
+    a.bytes = a.err_off + 256;
+    if (cudaMalloc(&a.base, a.bytes) != cudaSuccess) { a.base = nullptr; return MPC_ERR_NOMEM; }
+    if (cudaMemset(a.base, 0, a.bytes) != cudaSuccess) return MPC_ERR_CUDA;
+    return MPC_OK;
+}
+
 // ------------------------------------------------------------------ ABI ----
 extern "C" {
 
-const char* mpc_version(void) { return "mpc200 0.1 (sm_100a; BOTH + PAIR_HOST)"; }
+const char* mpc_version(void) { return "mpc200 0.2 (sm_100a; BOTH, PAIR over peer memory, PAIR_LOOPBACK)"; }
 
 mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
 {
     if (!cfg || !out) return MPC_ERR_INVALID;
     if (cfg->frac_bits != 16) return MPC_ERR_RANGE;
-    if (cfg->mode != MPC_MODE_BOTH && cfg->mode != MPC_MODE_PAIR_HOST) return MPC_ERR_INVALID;
-    if (cfg->mode != MPC_MODE_BOTH) return MPC_ERR_UNSUPPORTED;   /* PAIR modes: mpc200_pair */
+    if (cfg->mode != MPC_MODE_BOTH && cfg->mode != MPC_MODE_PAIR && cfg->mode != MPC_MODE_PAIR_LOOPBACK)
+        return MPC_ERR_INVALID;
+    if (cfg->mode == MPC_MODE_PAIR && (cfg->party < 0 || cfg->party > 1)) return MPC_ERR_INVALID;
     mpc_ctx* c = new mpc_ctx();
     memset(c, 0, sizeof *c);
     c->cfg = *cfg;
@@ -454,6 +482,12 @@ mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    if (cfg->mode != MPC_MODE_BOTH) {
+        c->slots = sms * 8 * NWARPS;       // up to 8 resident CTAs per SM
+        mpc_status st = xalloc(c, c->xa[0]);
+        if (!st && cfg->mode == MPC_MODE_PAIR_LOOPBACK) st = xalloc(c, c->xa[1]);
+        if (st) { mpc_ctx_destroy(c); return st; }
+    }
     *out = c;
     return MPC_OK;
 }
@@ -461,11 +495,52 @@ mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
 mpc_status mpc_ctx_destroy(mpc_ctx* c)
 {
     if (!c) return MPC_OK;
+    cudaStreamSynchronize(c->stream);
     for (int i = 0; i < c->nrec; ++i) { cudaEventDestroy(c->recs[i].a); cudaEventDestroy(c->recs[i].b); }
     for (int i = 0; i < c->npool; ++i) cudaEventDestroy(c->pool[i]);
     free(c->recs); free(c->pool);
     if (c->scratch) { cudaFreeAsync(c->scratch, c->stream); cudaStreamSynchronize(c->stream); }
+    if (c->peer_base) cudaIpcCloseMemHandle(c->peer_base);
+    for (int i = 0; i < 2; ++i) if (c->xa[i].base) cudaFree(c->xa[i].base);
     delete c;
+    return MPC_OK;
+}
+
+mpc_status mpc_pair_export(mpc_ctx* c, void* handle_out)
+{
+    if (!c || !handle_out || c->cfg.mode != MPC_MODE_PAIR) return MPC_ERR_INVALID;
+    static_assert(sizeof(cudaIpcMemHandle_t) <= MPC_PAIR_HANDLE_BYTES, "handle size");
+    cudaIpcMemHandle_t h;
+    if (cudaIpcGetMemHandle(&h, c->xa[0].base) != cudaSuccess) return fail(c, MPC_ERR_CUDA, "cudaIpcGetMemHandle");
+    memset(handle_out, 0, MPC_PAIR_HANDLE_BYTES);
+    memcpy(handle_out, &h, sizeof h);
+    return MPC_OK;
+}
+
+mpc_status mpc_pair_connect(mpc_ctx* c, const void* peer_handle)
+{
+    if (!c || !peer_handle || c->cfg.mode != MPC_MODE_PAIR) return MPC_ERR_INVALID;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, peer_handle, sizeof h);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    c->peer_base = p;
+    c->connected = 1;
+    return MPC_OK;
+}
+
+mpc_status mpc_ctx_sync(mpc_ctx* c)
+{
+    if (!c) return MPC_ERR_INVALID;
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "sync: %s", cudaGetErrorString(e));
+    for (int i = 0; i < 2; ++i) {
+        if (!c->xa[i].base) continue;
+        int err = 0;
+        cudaMemcpy(&err, (char*)c->xa[i].base + c->xa[i].err_off, sizeof err, cudaMemcpyDeviceToHost);
+        if (err) return fail(c, MPC_ERR_TIMEOUT, "PAIR exchange timed out (peer not running the same op?)");
+    }
     return MPC_OK;
 }
 
@@ -510,8 +585,8 @@ mpc_status mpc_ctx_set_stream(mpc_ctx* c, void* s)
 {
     if (!c) return MPC_ERR_INVALID;
     cudaStream_t ns = (cudaStream_t)s;
-    if (ns != c->stream && c->scratch) {
-        // the scratch tile is stream-ordered: order the new stream after the old one
+    if (ns != c->stream) {
+        // scratch and exchange memory are stream-ordered: order the new stream after the old one
         cudaEvent_t e = ev_get(c);
         cudaEventRecord(e, c->stream);
         cudaStreamWaitEvent(ns, e, 0);
@@ -531,32 +606,28 @@ mpc_status mpc_prg_fill(mpc_ctx* c, uint64_t key, uint64_t unit0, uint32_t step,
     if (!c || !out || n < 0 || reps < 1) return MPC_ERR_INVALID;
     if (n == 0) return MPC_OK;
     c->last_philox = (u64)n * (u64)reps;
-    rec_begin(c, "prg_fill", 0);
+    rec_begin(c, "prg_fill", (u64)n);
     k_prg_fill<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(mkkey(key), unit0, step, slot, out, n, reps);
     rec_end(c);
     c->st.launches++;
     return cuda_check(c, "prg_fill");
 }
 
-mpc_status mpc_share(mpc_ctx* c, const void* x, int x_is_f64, int owner, mpc_shares out,
-                     int64_t n, int64_t off)
+mpc_status mpc_share(mpc_ctx* c, const void* x, int x_is_f64, int owner, mpc_shares out, int64_t n, int64_t off)
 {
     mpc_status st = begin(c, 1);
     if (st) return st;
     if (owner != 0 && owner != 1) return fail(c, MPC_ERR_INVALID, "owner must be 0 or 1");
     if (n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "bad n/off");
-    if (c->cfg.mode == MPC_MODE_BOTH) {
-        if (bad2(c, out) || (!x && n > 0)) return fail(c, MPC_ERR_INVALID, "share: null pointer");
-    } else {
-        if (!out.sh[c->cfg.party] || (c->cfg.party == owner && !x && n > 0))
-            return fail(c, MPC_ERR_INVALID, "share: null pointer");
-    }
-    u64* s0 = c->cfg.mode == MPC_MODE_BOTH || c->cfg.party == 0 ? out.sh[0] : nullptr;
-    u64* s1 = c->cfg.mode == MPC_MODE_BOTH || c->cfg.party == 1 ? out.sh[1] : nullptr;
-    const void* xin = (c->cfg.mode == MPC_MODE_BOTH || c->cfg.party == owner) ? x : nullptr;
+    const bool pair = c->cfg.mode == MPC_MODE_PAIR;
+    if (bad_sh(c, out)) return fail(c, MPC_ERR_INVALID, "share: null/misaligned output");
+    const bool need_x = !pair || c->cfg.party == owner;
+    if (need_x && !x && n > 0) return fail(c, MPC_ERR_INVALID, "share: the owner needs x");
+    u64* s0 = !pair || c->cfg.party == 0 ? out.sh[0] : nullptr;
+    u64* s1 = !pair || c->cfg.party == 1 ? out.sh[1] : nullptr;
     if (n > 0) {
-        rec_begin(c, "share", 0);
-        k_share<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(xin, x_is_f64, owner, s0, s1, n, (u64)off, (u32)c->step, c->K.ks);
+        rec_begin(c, "share", (u64)n);
+        k_share<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(need_x ? x : nullptr, x_is_f64, owner, s0, s1, n, (u64)off, (u32)c->step, c->K.ks);
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "share"))) return st;
@@ -571,16 +642,23 @@ mpc_status mpc_open(mpc_ctx* c, mpc_shares in, int64_t n, uint64_t* ring_out, do
     mpc_status st = begin(c, 0);
     if (st) return st;
     if (n < 0 || scale_bits < 0 || scale_bits > 62) return fail(c, MPC_ERR_INVALID, "bad n/scale");
-    if (bad2(c, in)) return fail(c, MPC_ERR_INVALID, "open: null pointer");
+    if (bad_sh(c, in)) return fail(c, MPC_ERR_INVALID, "open: null pointer");
     if (n > 0) {
-        rec_begin(c, "open", 0);
-        k_open<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(in.sh[0], in.sh[1], n, ring_out, f64_out, scale_bits);
-        rec_end(c);
-        c->st.launches++;
-        if ((st = cuda_check(c, "open"))) return st;
+        if (is_pair(c)) {
+            st = launch_groups(c, n, 0, OpenBody{spv(c, in), ring_out, f64_out, n, 1.0 / (double)(1ull << scale_bits),
+                                                 is_loop(c) ? 0 : -1}, "open");
+        } else {
+            rec_begin(c, "open", (u64)n);
+            k_open<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(in.sh[0], in.sh[1], n, ring_out, f64_out, scale_bits);
+            rec_end(c);
+            c->st.launches++;
+            st = cuda_check(c, "open");
+        }
+        if (st) return st;
     }
     c->st.bytes_per_party += 8ull * (u64)n;
     c->st.rounds += 1;
+    rec_close(c);
     return MPC_OK;
 }
 
@@ -589,19 +667,17 @@ mpc_status mpc_trunc(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int bits
     mpc_status st = begin(c, 0);
     if (st) return st;
     if (bits < 0 || bits > 63) return fail(c, MPC_ERR_RANGE, "bits");
-    if (bad2(c, x) || bad2(c, z) || n < 0) return fail(c, MPC_ERR_INVALID, "trunc args");
+    if (bad_sh(c, x) || bad_sh(c, z) || n < 0) return fail(c, MPC_ERR_INVALID, "trunc args");
     if (n > 0) {
-        rec_begin(c, "trunc", 0);
-        k_trunc<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(x.sh[0], x.sh[1], z.sh[0], z.sh[1], n, bits);
+        rec_begin(c, "trunc", (u64)n);
+        k_trunc<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(spv(c, x), sov(c, z), n, bits);
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "trunc"))) return st;
     }
+    rec_close(c);
     return MPC_OK;
 }
-
-#define CHECK_BOTH_ONLY(c) \
-    if ((c)->cfg.mode != MPC_MODE_BOTH) return fail((c), MPC_ERR_UNSUPPORTED, "op not available in this mode")
 
 mpc_status mpc_mul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int64_t n, int64_t off, int tb)
 {
@@ -609,8 +685,8 @@ mpc_status mpc_mul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int64_t
     if (st) return st;
     if (tb != 0 && tb != 16) return fail(c, MPC_ERR_RANGE, "trunc_bits must be 0 or 16");
     if (n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "bad n/off");
-    if (bad2(c, x) || bad2(c, y) || bad2(c, z)) return fail(c, MPC_ERR_INVALID, "mul: null pointer");
-    if ((st = launch_pairs(c, n, (u64)off, MulBody{c->K, (u32)c->step, P(x), P(y), O(z), n, tb}, "mul"))) return st;
+    if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "mul: null pointer");
+    if ((st = launch_pairs(c, n, (u64)off, MulBody{(u32)c->step, spv(c, x), spv(c, y), sov(c, z), n, tb}, "mul"))) return st;
     acct_beaver(c, (u64)n);
     finish(c, 1);
     return MPC_OK;
@@ -622,9 +698,10 @@ static mpc_status cmp_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, 
     if (st) return st;
     if (w < 1 || w > 64) return fail(c, MPC_ERR_RANGE, "window must be in [1,64]");
     if (n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
-    if (bad2(c, x) || bad2(c, z)) return fail(c, MPC_ERR_INVALID, "cmp: null pointer");
-    st = w > 33 ? launch_groups(c, n, (u64)off, CmpBody<true>{c->K, (u32)c->step, w, P(x), O(z), relu}, relu ? "relu" : "cmp")
-                : launch_groups(c, n, (u64)off, CmpBody<false>{c->K, (u32)c->step, w, P(x), O(z), relu}, relu ? "relu" : "cmp");
+    if (bad_sh(c, x) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "cmp: null pointer");
+    const char* name = relu ? "relu" : "cmp";
+    st = w > 33 ? launch_groups(c, n, (u64)off, CmpBody<true>{(u32)c->step, w, spv(c, x), sov(c, z), relu}, name)
+                : launch_groups(c, n, (u64)off, CmpBody<false>{(u32)c->step, w, spv(c, x), sov(c, z), relu}, name);
     if (st) return st;
     acct_ltz(c, (u64)n, w);
     if (relu) acct_beaver(c, (u64)n);
@@ -641,15 +718,14 @@ mpc_status mpc_exp(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t of
     if (!exp_ok(p)) return fail(c, MPC_ERR_RANGE, "exp knobs out of range");
     mpc_status st = begin(c, exp_steps_h(p));
     if (st) return st;
-    CHECK_BOTH_ONLY(c);
-    if (bad2(c, x) || bad2(c, z) || n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "exp args");
+    if (bad_sh(c, x) || bad_sh(c, z) || n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "exp args");
     const ExpK k = mk_exp(p);
     if (p->clamp) {
         if (off & 31) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
-        st = p->window > 33 ? launch_groups(c, n, (u64)off, ExpGroupBody<true>{c->K, (u32)c->step, k, P(x), O(z)}, "exp")
-                            : launch_groups(c, n, (u64)off, ExpGroupBody<false>{c->K, (u32)c->step, k, P(x), O(z)}, "exp");
+        st = p->window > 33 ? launch_groups(c, n, (u64)off, ExpGroupBody<true>{(u32)c->step, k, spv(c, x), sov(c, z)}, "exp")
+                            : launch_groups(c, n, (u64)off, ExpGroupBody<false>{(u32)c->step, k, spv(c, x), sov(c, z)}, "exp");
     } else {
-        st = launch_pairs(c, n, (u64)off, ExpPairBody{c->K, (u32)c->step, k, P(x), O(z), n}, "exp");
+        st = launch_pairs(c, n, (u64)off, ExpPairBody{(u32)c->step, k, spv(c, x), sov(c, z), n}, "exp");
     }
     if (st) return st;
     acct_exp(c, (u64)n, p);
@@ -667,15 +743,15 @@ static mpc_status nr_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, i
     const u64 steps = exp_steps_h(&p->exp) + (KIND == 0 ? 2u : 3u) * (u64)p->iters;
     mpc_status st = begin(c, steps);
     if (st) return st;
-    CHECK_BOTH_ONLY(c);
-    if (bad2(c, x) || bad2(c, z) || n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "newton args");
+    if (bad_sh(c, x) || bad_sh(c, z) || n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "newton args");
     const NrK k = mk_nr(p);
+    const char* name = KIND == 0 ? "recip" : "rsqrt";
     if (p->exp.clamp) {
         if (off & 31) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
-        st = p->exp.window > 33 ? launch_groups(c, n, (u64)off, NrGroupBody<KIND, true>{c->K, (u32)c->step, k, P(x), O(z)}, "newton")
-                                : launch_groups(c, n, (u64)off, NrGroupBody<KIND, false>{c->K, (u32)c->step, k, P(x), O(z)}, "newton");
+        st = p->exp.window > 33 ? launch_groups(c, n, (u64)off, NrGroupBody<KIND, true>{(u32)c->step, k, spv(c, x), sov(c, z)}, name)
+                                : launch_groups(c, n, (u64)off, NrGroupBody<KIND, false>{(u32)c->step, k, spv(c, x), sov(c, z)}, name);
     } else {
-        st = launch_pairs(c, n, (u64)off, NrPairBody<KIND>{c->K, (u32)c->step, k, P(x), O(z), n}, "newton");
+        st = launch_pairs(c, n, (u64)off, NrPairBody<KIND>{(u32)c->step, k, spv(c, x), sov(c, z), n}, name);
     }
     if (st) return st;
     acct_exp(c, (u64)n, &p->exp);
@@ -683,9 +759,6 @@ static mpc_status nr_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, i
     finish(c, steps);
     return MPC_OK;
 }
-extern "C" {
-mpc_status mpc_recip(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_nr_p* p) { return nr_common<0>(c, x, z, n, off, p); }
-mpc_status mpc_rsqrt(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_nr_p* p) { return nr_common<1>(c, x, z, n, off, p); }
 
 static u64 act_steps(int act, const mpc_act_p* p)
 {
@@ -711,8 +784,7 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
     const u64 steps = act_steps(act, p);
     mpc_status st = begin(c, steps);
     if (st) return st;
-    CHECK_BOTH_ONLY(c);
-    if (bad2(c, x) || bad2(c, z) || n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "act args (off % 32)");
+    if (bad_sh(c, x) || bad_sh(c, z) || n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "act args (off % 32)");
     ActK k;
     memset(&k, 0, sizeof k);
     k.act = act; k.form = p->form; k.w = p->window;
@@ -732,10 +804,10 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
         k.deg = p->degree;
         for (int i = 0; i <= p->degree; ++i) k.c[i] = E(p->coeffs[i]);
     }
-    st = k.w > 33 ? launch_groups(c, n, (u64)off, ActBody<true>{c->K, (u32)c->step, k, P(x), O(z)}, "act")
-                  : launch_groups(c, n, (u64)off, ActBody<false>{c->K, (u32)c->step, k, P(x), O(z)}, "act");
+    const char* name = act == 0 ? "gelu" : act == 1 ? "silu" : "sigmoid";
+    st = k.w > 33 ? launch_groups(c, n, (u64)off, ActBody<true>{(u32)c->step, k, spv(c, x), sov(c, z)}, name)
+                  : launch_groups(c, n, (u64)off, ActBody<false>{(u32)c->step, k, spv(c, x), sov(c, z)}, name);
     if (st) return st;
-    // accounting
     const u64 N = (u64)n;
     if (k.deg == 0) { acct_ltz(c, N, k.w); if (act != 2) acct_beaver(c, N); }
     else {
@@ -749,68 +821,29 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
     finish(c, steps);
     return MPC_OK;
 }
+
+extern "C" {
+mpc_status mpc_recip(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_nr_p* p) { return nr_common<0>(c, x, z, n, off, p); }
+mpc_status mpc_rsqrt(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_nr_p* p) { return nr_common<1>(c, x, z, n, off, p); }
 mpc_status mpc_gelu(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p) { return act_common(c, 0, x, z, n, off, p); }
 mpc_status mpc_silu(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p) { return act_common(c, 1, x, z, n, off, p); }
 mpc_status mpc_sigmoid(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p) { return act_common(c, 2, x, z, n, off, p); }
 
-}  // extern "C"
-
-// ---- row ops (fused, one CTA per 32-row tile; rows_both.cuh) -------------------------------------
-static int max_levels_h(i64 cols) { int L = 0; i64 m = cols; while (m > 1) { m = (m + 1) / 2; ++L; } return L; }
-
-static const size_t SMEM_LIMIT = 72 * 1024;      // keep 3 CTAs per SM
-
-static void acct_max(mpc_ctx* c, i64 rows, i64 cols, int w)
-{
-    i64 m = cols;
-    while (m > 1) {
-        const i64 h = m / 2;
-        acct_ltz(c, (u64)(rows * h), w);
-        acct_beaver(c, (u64)(rows * h));
-        m = h + (m & 1);
-    }
-}
-
-template <class Args>
-static mpc_status launch_rows(mpc_ctx* c, void (*kern)(Args), Args& a, i64 rows, i64 work_u64, const char* name)
-{
-    const i64 ntiles = (rows + 31) / 32;
-    const size_t smem = sizeof(u64) * (size_t)work_u64;
-    int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 3);
-    if (grid < 1) grid = 1;
-    size_t dyn = 0;
-    if (work_u64 > 0 && smem <= SMEM_LIMIT) {
-        a.use_smem = 1; a.gscratch = nullptr; dyn = smem;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    } else if (work_u64 > 0) {
-        a.use_smem = 0;
-        a.gscratch = (u64*)scratch(c, smem * (size_t)grid);
-        if (!a.gscratch) return fail(c, MPC_ERR_NOMEM, "%s: scratch %zu bytes", name, smem * (size_t)grid);
-    }
-    a.work_u64 = work_u64;
-    rec_begin(c, name, (u64)rows);
-    kern<<<grid, 256, dyn, c->stream>>>(a);
-    rec_end(c);
-    c->st.launches++;
-    return cuda_check(c, name);
-}
-
-extern "C" {
-
+// ---- row ops (fused, one CTA per 32-row tile) ---------------------------------------------------
 mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off, int w)
 {
     if (!c) return MPC_ERR_INVALID;
     const u64 steps = 2ull * (u64)max_levels_h(cols);
     mpc_status st = begin(c, steps);
     if (st) return st;
-    CHECK_BOTH_ONLY(c);
     if (w < 1 || w > 64) return fail(c, MPC_ERR_RANGE, "window");
-    if (bad2(c, x) || bad2(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
+    if (bad_sh(c, x) || bad_sh(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "max args (row_off % 32)");
     if (rows > 0) {
-        MaxArgs a{c->K, (u32)c->step, w, RowPtr2{x.sh[0], x.sh[1]}, RowOut2{z.sh[0], z.sh[1]}, rows, cols,
-                  (u64)row_off, nullptr, 0, 0};
-        if ((st = launch_rows(c, w > 33 ? k_max_fused<true> : k_max_fused<false>, a, rows, max_work_u64(cols), "max_fused"))) return st;
+        MaxArgs a{(u32)c->step, w, spv(c, x), sov(c, z), rows, cols, (u64)row_off, nullptr, 0, 0};
+        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), "max")
+                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), "max");
+        if (st) return st;
         acct_max(c, rows, cols, w);
     }
     finish(c, steps);
@@ -829,23 +862,25 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
     const u64 steps = 2ull * (u64)max_levels_h(cols);
     mpc_status st = begin(c, steps);
     if (st) return st;
-    CHECK_BOTH_ONLY(c);
     if (w < 1 || w > 64) return fail(c, MPC_ERR_RANGE, "window");
     const u64 row_off = (u64)img_off * (u64)C * (u64)Ho * (u64)Wo;
-    if (bad2(c, x) || bad2(c, z) || img_off < 0 || (row_off & 31)) return fail(c, MPC_ERR_INVALID, "maxpool args");
+    if (bad_sh(c, x) || bad_sh(c, z) || img_off < 0 || (row_off & 31)) return fail(c, MPC_ERR_INVALID, "maxpool args");
+    if (max_work_u64(cols) * 8 > (i64)SMEM_LIMIT) return fail(c, MPC_ERR_UNSUPPORTED, "pool window too large");
     if (rows > 0) {
         // gather the windows (public zero padding) into rows, then the fused row max
-        u64* Rw = (u64*)scratch(c, sizeof(u64) * 2 * (size_t)(rows * cols));
+        const size_t gb = sizeof(u64) * (size_t)(rows * cols);
+        u64* Rw = (u64*)scratch(c, 2 * gb);
         if (!Rw) return fail(c, MPC_ERR_NOMEM, "maxpool scratch");
-        rec_begin(c, "pool_gather", 0);
-        k_pool_gather<<<grid_for(c, rows * cols, TPB, 16), TPB, 0, c->stream>>>(P(x), Out2{Rw, Rw + rows * cols}, N, C, H, W, k, stride, pad, Ho, Wo);
+        SO rowsbuf = sov(c, mpc_shares{{Rw, Rw + rows * cols}});
+        rec_begin(c, "pool_gather", (u64)rows);
+        k_pool_gather<<<grid_for(c, rows * cols, TPB, 16), TPB, 0, c->stream>>>(spv(c, x), rowsbuf, N, C, H, W, k, stride, pad, Ho, Wo);
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "pool_gather"))) return st;
-        MaxArgs a{c->K, (u32)c->step, w, RowPtr2{Rw, Rw + rows * cols}, RowOut2{z.sh[0], z.sh[1]}, rows, cols,
-                  row_off, nullptr, 0, 0};
-        if (max_work_u64(cols) * 8 > (i64)SMEM_LIMIT) return fail(c, MPC_ERR_UNSUPPORTED, "pool window too large");
-        if ((st = launch_rows(c, w > 33 ? k_max_fused<true> : k_max_fused<false>, a, rows, max_work_u64(cols), "maxpool_fused"))) return st;
+        MaxArgs a{(u32)c->step, w, SP{{rowsbuf.p[0], rowsbuf.p[1]}}, sov(c, z), rows, cols, row_off, nullptr, 0, 0};
+        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), "maxpool")
+                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), "maxpool");
+        if (st) return st;
         acct_max(c, rows, cols, w);
     }
     finish(c, steps);
@@ -862,22 +897,21 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
     const u64 steps = 2ull * (u64)L + exp_steps_h(&p->exp) + exp_steps_h(&p->recip.exp) + 2ull * (u64)p->recip.iters + 1;
     mpc_status st = begin(c, steps);
     if (st) return st;
-    CHECK_BOTH_ONLY(c);
-    if (bad2(c, x) || bad2(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
+    if (bad_sh(c, x) || bad_sh(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "softmax args (row_off % 32)");
     if (rows > 0) {
         SoftmaxArgs a;
-        a.K = c->K;
         a.s_max = (u32)c->step;
         a.s_exp = a.s_max + 2u * (u32)L;
         a.s_rec = a.s_exp + (u32)exp_steps_h(&p->exp);
         a.s_mul = a.s_rec + (u32)exp_steps_h(&p->recip.exp) + 2u * (u32)p->recip.iters;
         a.w = p->window; a.ek = mk_exp(&p->exp); a.rk = mk_nr(&p->recip);
-        a.x = RowPtr2{x.sh[0], x.sh[1]}; a.z = RowOut2{z.sh[0], z.sh[1]};
+        a.x = spv(c, x); a.z = sov(c, z);
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
         const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
-        if ((st = launch_rows(c, wide ? k_softmax_fused<true> : k_softmax_fused<false>, a, rows,
-                              softmax_work_u64(cols), "softmax_fused"))) return st;
+        st = wide ? launch_rows(c, k_softmax<true, BothA>, k_softmax<true, PairA>, a, rows, softmax_work_u64(cols), "softmax")
+                  : launch_rows(c, k_softmax<false, BothA>, k_softmax<false, PairA>, a, rows, softmax_work_u64(cols), "softmax");
+        if (st) return st;
         const i64 n = rows * cols;
         acct_max(c, rows, cols, p->window);
         acct_exp(c, (u64)n, &p->exp);
@@ -897,27 +931,33 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
     const u64 steps = 1 + exp_steps_h(&p->rsqrt.exp) + 3ull * (u64)p->rsqrt.iters + 1;
     mpc_status st = begin(c, steps);
     if (st) return st;
-    CHECK_BOTH_ONLY(c);
-    if (bad2(c, x) || bad2(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
+    if (bad_sh(c, x) || bad_sh(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "layernorm args (row_off % 32)");
     if (rows > 0) {
         LnArgs a;
-        a.K = c->K;
         a.s_sq = (u32)c->step;
         a.s_rs = a.s_sq + 1;
         a.s_mul = a.s_rs + (u32)exp_steps_h(&p->rsqrt.exp) + 3u * (u32)p->rsqrt.iters;
         a.rk = mk_nr(&p->rsqrt);
-        a.x = RowPtr2{x.sh[0], x.sh[1]}; a.z = RowOut2{z.sh[0], z.sh[1]};
+        a.x = spv(c, x); a.z = sov(c, z);
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
         a.mean_mode = p->mean_mode; a.e_invd = E(1.0 / (double)cols); a.e_eps = E(p->eps);
         const i64 ntiles = (rows + 31) / 32;
-        const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * 3);
-        rec_begin(c, "layernorm_fused", (u64)rows);
-        if (p->rsqrt.exp.window > 33) k_ln_fused<true><<<grid, 256, 0, c->stream>>>(a);
-        else k_ln_fused<false><<<grid, 256, 0, c->stream>>>(a);
-        rec_end(c);
-        c->st.launches++;
-        if ((st = cuda_check(c, "layernorm_fused"))) return st;
+        const bool wide = p->rsqrt.exp.window > 33;
+        if (!is_pair(c)) {
+            const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(wide ? k_ln<true, BothA> : k_ln<false, BothA>));
+            rec_begin(c, "layernorm", (u64)rows);
+            if (wide) k_ln<true, BothA><<<grid, TPB, 0, c->stream>>>(BothA{c->K}, a);
+            else k_ln<false, BothA><<<grid, TPB, 0, c->stream>>>(BothA{c->K}, a);
+            rec_end(c);
+            c->st.launches++;
+            st = cuda_check(c, "layernorm");
+        } else if (wide) {
+            st = launch_pair_kernel(c, k_ln<true, PairA>, pair_ctas(c, k_ln<true, PairA>, 0, ntiles), 0, "layernorm", a);
+        } else {
+            st = launch_pair_kernel(c, k_ln<false, PairA>, pair_ctas(c, k_ln<false, PairA>, 0, ntiles), 0, "layernorm", a);
+        }
+        if (st) return st;
         const i64 n = rows * cols;
         acct_beaver(c, (u64)n);
         acct_exp(c, (u64)rows, &p->rsqrt.exp);

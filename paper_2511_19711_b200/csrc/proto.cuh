@@ -1,0 +1,333 @@
+// proto.cuh -- the two protocol "policies" every schedule is written against.
+//
+//  BothP : MPC_MODE_BOTH -- one thread holds both parties' shares of a unit; an opening
+//          is the sum of the two masked shares, formed in registers (proto_both.cuh).
+//  PairP : MPC_MODE_PAIR / MPC_MODE_PAIR_LOOPBACK -- a thread holds ITS party's share;
+//          each opening is a warp-level exchange with the matching warp of the peer
+//          party through NVLink peer memory (or, loopback, through local memory):
+//          every lane stores its masked words into the peer's receive buffer, fences at
+//          system scope, lane 0 publishes a monotonically increasing round number in the
+//          peer's flag word and waits (acquire, with a timeout) for the peer's flag.
+//          Receive buffers are double-buffered by round parity; the round counter of each
+//          warp slot persists across launches, so consecutive ops never alias.
+// Both policies implement exactly the contract of DESIGN.md 2.3 / 2.4, so their output
+// shares are bit-identical (test T4).
+#pragma once
+#include "proto_both.cuh"
+
+namespace mpc {
+
+// ---- shares in memory: one pointer per party ------------------------------------------------
+struct SP { const u64* p[2]; };
+struct SO { u64* p[2]; };
+
+// ================================================================================ BOTH ====
+struct BothP {
+    Keys K;
+    using S = Sh;
+    static constexpr bool kPair = false;
+    __device__ __forceinline__ int party() const { return -1; }
+    __device__ __forceinline__ S zero() const { return {0, 0}; }
+    __device__ __forceinline__ S ld(SP a, i64 i) const { return {a.p[0][i], a.p[1][i]}; }
+    __device__ __forceinline__ void st(SO a, i64 i, S v) const { a.p[0][i] = v.s0; a.p[1][i] = v.s1; }
+    __device__ __forceinline__ S add(S a, S b) const { return sh_add(a, b); }
+    __device__ __forceinline__ S sub(S a, S b) const { return sh_sub(a, b); }
+    __device__ __forceinline__ S neg(S a) const { return sh_neg(a); }
+    __device__ __forceinline__ S addp(S a, u64 e) const { return sh_addp(a, e); }
+    __device__ __forceinline__ S shr_(S a, int k) const { return sh_shr(a, k); }
+    __device__ __forceinline__ S muli(S a, u64 k) const { return sh_muli(a, k); }
+    __device__ __forceinline__ S mulf(S a, u64 e) const { return sh_mulf(a, e); }
+    __device__ __forceinline__ S notb(S b) const { return sh_not(b); }
+    __device__ __forceinline__ S pm1(S s) const { return {1ull - 2ull * s.s0, 0ull - 2ull * s.s1}; }   // 1 - 2s
+    __device__ __forceinline__ S shl(S a, int k) const { return {a.s0 << k, a.s1 << k}; }
+    __device__ __forceinline__ S sumw(S a) const {                     // warp sum (local)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) { a.s0 += __shfl_xor_sync(FULL, a.s0, o); a.s1 += __shfl_xor_sync(FULL, a.s1, o); }
+        return a;
+    }
+    __device__ __forceinline__ S divp(S a, i64 d) const;               // per-share floor division
+    __device__ __forceinline__ S bm(u64 u, u32 s, S x, S y) { return mpc::bm(K, u, s, x, y); }
+    __device__ __forceinline__ void bm2(u64 u, u32 s, S x0, S y0, S x1, S y1, S& z0, S& z1) {
+        mpc::bm2(K, u, s, x0, y0, x1, y1, z0, z1);
+    }
+    template <bool WIDE>
+    __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(K, q, s, w, x, lane); }
+    __device__ __forceinline__ u64 open(S x) const { return x.s0 + x.s1; }
+};
+
+__device__ __forceinline__ u64 floordiv_share(u64 a, i64 d)
+{
+    const i64 x = (i64)a;
+    i64 q = x / d;
+    if ((x % d) != 0 && x < 0) --q;
+    return (u64)q;
+}
+__device__ __forceinline__ Sh BothP::divp(Sh a, i64 d) const { return {floordiv_share(a.s0, d), floordiv_share(a.s1, d)}; }
+
+// ================================================================================ PAIR ====
+constexpr int XW = 4;                // u64 words per lane per round (max)
+constexpr int XSLOT_RX = 2 * 32 * XW; // u64 per warp slot receive buffer (double-buffered)
+
+// Device view of one party's exchange memory.
+struct XMem {
+    u64* rx;          // [slots][2][32][XW]  receive buffers (peer writes)
+    u64* flag;        // [slots][4]          my flags (peer writes word 0)
+    u64* round;       // [slots]             persistent round counters (local only)
+    int* err;         // error word (1 = exchange timeout)
+    u64* prx;         // peer's rx   (remote or, loopback, the other party's local buffer)
+    u64* pflag;       // peer's flag
+    int slots;
+};
+
+__device__ __forceinline__ u64 ld_acquire_sys(const u64* p)
+{
+    u64 v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(u64* p, u64 v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ u64 ld_volatile(const u64* p)
+{
+    u64 v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ u64 globaltimer()
+{
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct PairP {
+    Keys K;
+    int pty;                 // 0 | 1
+    // per-warp exchange state (set by bind())
+    u64* rx; u64* prx; u64* flag; u64* pflag; u64* rstate; int* err;
+    u64 rnd;
+    int dead;
+    using S = u64;
+    static constexpr bool kPair = true;
+    static constexpr u64 kTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s, then poison
+
+    __device__ __forceinline__ void bind(const XMem& m, int slot) {
+        rx = m.rx + (i64)slot * XSLOT_RX;
+        prx = m.prx + (i64)slot * XSLOT_RX;
+        flag = m.flag + (i64)slot * 4;
+        pflag = m.pflag + (i64)slot * 4;
+        rstate = m.round + slot;
+        err = m.err;
+        rnd = *rstate;
+        dead = 0;
+    }
+    __device__ __forceinline__ void unbind(int lane) {
+        if (lane == 0) *rstate = rnd;
+    }
+    __device__ __forceinline__ int party() const { return pty; }
+    // ---- exchange: put words, exch(), get peer's words ----
+    __device__ __forceinline__ void put(int lane, int k, u64 v) { prx[(rnd & 1) * (32 * XW) + lane * XW + k] = v; }
+    __device__ __forceinline__ void exch(int lane) {
+        __threadfence_system();
+        __syncwarp();
+        ++rnd;
+        if (lane == 0) {
+            st_release_sys(pflag, rnd);
+            if (!dead) {
+                const u64 t0 = globaltimer();
+                while (ld_acquire_sys(flag) < rnd) {
+                    if (globaltimer() - t0 > kTimeoutNs) { atomicExch(err, 1); dead = 1; break; }
+                }
+            }
+        }
+        dead = __shfl_sync(FULL, dead, 0);
+        __syncwarp();
+    }
+    __device__ __forceinline__ u64 get(int lane, int k) const {
+        return ld_volatile(rx + ((rnd - 1) & 1) * (32 * XW) + lane * XW + k);
+    }
+
+    // ---- local share ops (party 0 carries public addends) ----
+    __device__ __forceinline__ S zero() const { return 0; }
+    __device__ __forceinline__ S ld(SP a, i64 i) const { return a.p[pty][i]; }
+    __device__ __forceinline__ void st(SO a, i64 i, S v) const { a.p[pty][i] = v; }
+    __device__ __forceinline__ S add(S a, S b) const { return a + b; }
+    __device__ __forceinline__ S sub(S a, S b) const { return a - b; }
+    __device__ __forceinline__ S neg(S a) const { return 0ull - a; }
+    __device__ __forceinline__ S addp(S a, u64 e) const { return pty == 0 ? a + e : a; }
+    __device__ __forceinline__ S shr_(S a, int k) const { return shr(a, k); }
+    __device__ __forceinline__ S muli(S a, u64 k) const { return a * k; }
+    __device__ __forceinline__ S mulf(S a, u64 e) const { return shr(a * e, FRAC); }
+    __device__ __forceinline__ S notb(S b) const { return pty == 0 ? 1ull - b : 0ull - b; }
+    __device__ __forceinline__ S pm1(S s) const { return pty == 0 ? 1ull - 2ull * s : 0ull - 2ull * s; }
+    __device__ __forceinline__ S shl(S a, int k) const { return a << k; }
+    __device__ __forceinline__ S sumw(S a) const {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(FULL, a, o);
+        return a;
+    }
+    __device__ __forceinline__ S divp(S a, i64 d) const { return floordiv_share(a, d); }
+
+    // ---- Beaver (DESIGN.md 2.3/2.4); party 1 also plays the dealer's correction (R7) ----
+    __device__ __forceinline__ void triple(u64 u, u32 s, u64 c0, u64& a, u64& b, u64& c) const {
+        const uint4 A0 = prg(K.k0, u, s, 0);
+        if (pty == 0) {
+            a = w64(A0.x, A0.y); b = w64(A0.z, A0.w); c = c0;
+        } else {
+            const uint4 A1 = prg(K.k1, u, s, 0);
+            a = w64(A1.x, A1.y); b = w64(A1.z, A1.w);
+            c = (w64(A0.x, A0.y) + a) * (w64(A0.z, A0.w) + b) - c0;
+        }
+    }
+    __device__ __forceinline__ S bm_finish(u64 a, u64 b, u64 c, u64 e, u64 f) const {
+        return pty == 0 ? c + e * b + f * a + e * f : c + e * b + f * a;
+    }
+    __device__ __forceinline__ S bm(u64 u, u32 s, S x, S y) {
+        const int lane = threadIdx.x & 31;
+        u64 a, b, c;
+        triple(u, s, beaver_c0(K, u, s), a, b, c);
+        put(lane, 0, x - a); put(lane, 1, y - b);
+        exch(lane);
+        const u64 e = (x - a) + get(lane, 0), f = (y - b) + get(lane, 1);
+        return bm_finish(a, b, c, e, f);
+    }
+    __device__ __forceinline__ void bm2(u64 u, u32 s, S x0, S y0, S x1, S y1, S& z0, S& z1) {
+        const int lane = threadIdx.x & 31;
+        const uint4 C = prg(K.k0, u >> 1, s, 1);
+        u64 a0, b0, c0, a1, b1, c1;
+        triple(u, s, w64(C.x, C.y), a0, b0, c0);
+        triple(u + 1, s, w64(C.z, C.w), a1, b1, c1);
+        put(lane, 0, x0 - a0); put(lane, 1, y0 - b0); put(lane, 2, x1 - a1); put(lane, 3, y1 - b1);
+        exch(lane);
+        z0 = bm_finish(a0, b0, c0, (x0 - a0) + get(lane, 0), (y0 - b0) + get(lane, 1));
+        z1 = bm_finish(a1, b1, c1, (x1 - a1) + get(lane, 2), (y1 - b1) + get(lane, 3));
+    }
+
+    // ---- AND gates on XOR-shared plane words; up to 2 gates (4 words) per round ----
+    __device__ __forceinline__ void and_triple(uint4 t0, uint4 t1, int which, u32& a, u32& b, u32& c) const {
+        // which = 0: (a1,b1) = t1.x,t1.y ; 1: t1.z,t1.w
+        const u32 a1 = which ? t1.z : t1.x, b1 = which ? t1.w : t1.y;
+        if (pty == 0) { a = t0.x; b = t0.y; c = t0.z; }
+        else { a = a1; b = b1; c = ((t0.x ^ a1) & (t0.y ^ b1)) ^ t0.z; }
+    }
+    __device__ __forceinline__ u32 and_finish(u32 a, u32 b, u32 c, u32 d, u32 e) const {
+        return pty == 0 ? (c ^ (d & b) ^ (e & a) ^ (d & e)) : (c ^ (d & b) ^ (e & a));
+    }
+
+    template <bool WIDE>
+    __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) {
+        const int m = w - 1;
+        constexpr int H = WIDE ? 2 : 1;
+        u32 Pp[2], Gp[2];                                  // this party's shares of P_j, G_j
+        Pp[0] = transpose32((u32)x, lane);
+        if (WIDE) Pp[1] = transpose32((u32)(x >> 32), lane);
+        // g-layer: AND((x0_j, 0), (0, x1_j)) -- party 0 holds the x-input, party 1 the y-input
+        {
+            u32 ta[2], tb[2], tc[2], dd[2], ee[2];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const int j = lane + 32 * h;
+                ta[h] = tb[h] = tc[h] = 0;
+                if (j < m) {
+                    const uint4 t0 = prg(K.k0, q, s, ltz_slot(0, j, 0));
+                    uint4 t1 = make_uint4(0, 0, 0, 0);
+                    if (pty == 1) t1 = prg(K.k1, q, s, ltz_slot(0, j, 0));
+                    and_triple(t0, t1, 0, ta[h], tb[h], tc[h]);
+                }
+                const u32 xin = pty == 0 ? Pp[h] : 0u, yin = pty == 0 ? 0u : Pp[h];
+                dd[h] = xin ^ ta[h]; ee[h] = yin ^ tb[h];
+                put(lane, h, (u64)dd[h] | ((u64)ee[h] << 32));
+            }
+            exch(lane);
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const u64 pw = get(lane, h);
+                const u32 d = dd[h] ^ (u32)pw, e = ee[h] ^ (u32)(pw >> 32);
+                Gp[h] = (lane + 32 * h < m) ? and_finish(ta[h], tb[h], tc[h], d, e) : 0u;
+            }
+        }
+        const int L = (m > 0) ? ceil_log2i(m) : 0;
+        for (int k = 0; k < L; ++k) {
+            const int dl = 1 << k;
+            const int src = (lane - dl) & 31;
+            u32 sG[2], sP[2];
+#pragma unroll
+            for (int h = 0; h < H; ++h) { sG[h] = __shfl_sync(FULL, Gp[h], src); sP[h] = __shfl_sync(FULL, Pp[h], src); }
+            u32 ga[2], gb[2], gc[2], pa[2], pb[2], pc[2], dG[2], eG[2], dP[2], eP[2];
+            bool act[2];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const int j = lane + 32 * h;
+                act[h] = (j >= dl && j < m);
+                int hs = h;
+                if (dl < 32) hs = (lane >= dl) ? h : h - 1; else hs = h - 1;
+                u32 g = sG[0], p = sP[0];
+                if (WIDE && hs == 1) { g = sG[1]; p = sP[1]; }
+                if (WIDE && dl == 32) { g = Gp[0]; p = Pp[0]; }
+                ga[h] = gb[h] = gc[h] = pa[h] = pb[h] = pc[h] = 0;
+                if (act[h]) {
+                    const uint4 tg = prg(K.k0, q, s, ltz_slot(k + 1, j, 0));
+                    const uint4 tp = prg(K.k0, q, s, ltz_slot(k + 1, j, 1));
+                    uint4 t1 = make_uint4(0, 0, 0, 0);
+                    if (pty == 1) t1 = prg(K.k1, q, s, ltz_slot(k + 1, j, 0));
+                    and_triple(tg, t1, 0, ga[h], gb[h], gc[h]);
+                    and_triple(tp, t1, 1, pa[h], pb[h], pc[h]);
+                }
+                dG[h] = Pp[h] ^ ga[h]; eG[h] = g ^ gb[h];
+                dP[h] = Pp[h] ^ pa[h]; eP[h] = p ^ pb[h];
+                put(lane, 2 * h, (u64)dG[h] | ((u64)eG[h] << 32));
+                put(lane, 2 * h + 1, (u64)dP[h] | ((u64)eP[h] << 32));
+            }
+            exch(lane);
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                if (act[h]) {
+                    const u64 w0 = get(lane, 2 * h), w1 = get(lane, 2 * h + 1);
+                    const u32 d1 = dG[h] ^ (u32)w0, e1 = eG[h] ^ (u32)(w0 >> 32);
+                    const u32 d2 = dP[h] ^ (u32)w1, e2 = eP[h] ^ (u32)(w1 >> 32);
+                    Gp[h] ^= and_finish(ga[h], gb[h], gc[h], d1, e1);
+                    Pp[h] = and_finish(pa[h], pb[h], pc[h], d2, e2);
+                }
+            }
+        }
+        u32 bp;
+        if (m == 0) bp = (u32)(x & 1ull);
+        else {
+            const int jm = m - 1;
+            u32 gm = Gp[0];
+            if (WIDE && jm >= 32) gm = Gp[1];
+            gm = __shfl_sync(FULL, gm, jm & 31);
+            bp = (u32)((x >> (w - 1)) & 1ull) ^ ((gm >> lane) & 1u);
+        }
+        // daBit + B2A: party 0 holds (r0A, r0B); party 1 (r1A, r1B), r1A = (r0B ^ r1B) - r0A
+        const uint4 D0 = prg(K.k0, q, s, 2u + (u32)lane);
+        const u64 r0A = w64(D0.x, D0.y);
+        const u32 r0B = D0.z & 1u;
+        u64 rA;
+        u32 rB;
+        if (pty == 0) { rA = r0A; rB = r0B; }
+        else {
+            const uint4 D1 = prg(K.k1, q, s, 1u);
+            rB = (D1.x >> lane) & 1u;
+            rA = (u64)(r0B ^ rB) - r0A;
+        }
+        const u32 mine = bp ^ rB;
+        put(lane, 0, (u64)mine);
+        exch(lane);
+        const u64 c = (u64)(mine ^ ((u32)get(lane, 0) & 1u));
+        const u64 sg = 1ull - 2ull * c;
+        return pty == 0 ? c + sg * rA : sg * rA;
+    }
+
+    // ---- S2 open: exchange the shares themselves ----
+    __device__ __forceinline__ u64 open(u64 x) {
+        const int lane = threadIdx.x & 31;
+        put(lane, 0, x);
+        exch(lane);
+        return x + get(lane, 0);
+    }
+};
+
+}  // namespace mpc

@@ -1,0 +1,186 @@
+// sched.cuh -- L2 fused schedules of DESIGN.md 2.5, written once against a protocol policy
+// P (BothP or PairP, proto.cuh).  Each function consumes step ids s, s+1, ... exactly in
+// the order of the decomposition (so fused = composed).  In PairP every bm/ltz is a
+// warp-level exchange: all 32 lanes of a warp must call these functions together.
+#pragma once
+#include "proto.cuh"
+
+namespace mpc {
+
+// knobs with their public constants already encoded (E(c), host side)
+struct ExpK { int t, clamp, w; u64 e_one, e_2t; };
+struct NrK  { int iters; ExpK exp; u64 e_half, e_c003, e_two, e_three, e_02, e_22; };
+constexpr int MAX_COEF = 13;
+struct ActK {
+    int act;          // 0 gelu, 1 silu, 2 sigmoid
+    int form;         // 0 poly_x, 1 poly_abs, 2 relu, 3 erf
+    int deg;          // polynomial degree (HORNER degree for erf = K-1)
+    int w;
+    u64 e_B, e_mB, e_half, e_one, e_isqrt2, e_2sqrtpi;
+    u64 c[MAX_COEF];  // E(c_k) (poly) or E(a_k) (erf series)
+};
+
+__device__ __forceinline__ int exp_steps(const ExpK& e) { return e.t + 2 * e.clamp; }
+
+// ---- EXP(x; t, clamp, w) -------------------------------------------------
+// GROUP variant: lane <-> unit u of LTZ group q (with or without clamp).
+template <bool WIDE, class P>
+__device__ __forceinline__ typename P::S exp_group(P& pr, u64 u, u64 q, u32 s, const ExpK& p,
+                                                   typename P::S x, int lane)
+{
+    typename P::S y = pr.addp(pr.shr_(x, p.t), p.e_one);
+    if (p.clamp) {
+        const typename P::S l = pr.template ltz<WIDE>(q, s, p.w, pr.addp(x, p.e_2t), lane);
+        y = pr.bm(u, s + 1, y, pr.notb(l));
+        s += 2;
+    }
+    for (int k = 0; k < p.t; ++k) y = pr.shr_(pr.bm(u, s + k, y, y), FRAC);
+    return y;
+}
+
+// PAIR variant (no clamp): units u (even) and u+1 in one thread; one c0 block per pair.
+template <class P>
+__device__ __forceinline__ void exp_pair(P& pr, u64 u, u32 s, const ExpK& p, typename P::S& y0, typename P::S& y1)
+{
+    y0 = pr.addp(pr.shr_(y0, p.t), p.e_one);
+    y1 = pr.addp(pr.shr_(y1, p.t), p.e_one);
+    for (int k = 0; k < p.t; ++k) {
+        typename P::S a, b;
+        pr.bm2(u, s + k, y0, y0, y1, y1, a, b);
+        y0 = pr.shr_(a, FRAC); y1 = pr.shr_(b, FRAC);
+    }
+}
+
+// ---- RECIP(x; iters, exp) -------------------------------------------
+template <bool WIDE, class P>
+__device__ __forceinline__ typename P::S recip_group(P& pr, u64 u, u64 q, u32 s, const NrK& p,
+                                                     typename P::S x, int lane)
+{
+    typename P::S g = exp_group<WIDE>(pr, u, q, s, p.exp, pr.addp(pr.neg(x), p.e_half), lane);
+    s += exp_steps(p.exp);
+    typename P::S y = pr.addp(pr.muli(g, 3ull), p.e_c003);
+    for (int it = 0; it < p.iters; ++it) {
+        const typename P::S pp = pr.shr_(pr.bm(u, s, x, y), FRAC);
+        y = pr.shr_(pr.bm(u, s + 1, y, pr.addp(pr.neg(pp), p.e_two)), FRAC);
+        s += 2;
+    }
+    return y;
+}
+
+template <class P>
+__device__ __forceinline__ void recip_pair(P& pr, u64 u, u32 s, const NrK& p, typename P::S x0, typename P::S x1,
+                                           typename P::S& y0, typename P::S& y1)
+{
+    typename P::S g0 = pr.addp(pr.neg(x0), p.e_half), g1 = pr.addp(pr.neg(x1), p.e_half);
+    exp_pair(pr, u, s, p.exp, g0, g1);
+    s += exp_steps(p.exp);
+    y0 = pr.addp(pr.muli(g0, 3ull), p.e_c003);
+    y1 = pr.addp(pr.muli(g1, 3ull), p.e_c003);
+    for (int it = 0; it < p.iters; ++it) {
+        typename P::S a, b;
+        pr.bm2(u, s, x0, y0, x1, y1, a, b);
+        a = pr.addp(pr.neg(pr.shr_(a, FRAC)), p.e_two);
+        b = pr.addp(pr.neg(pr.shr_(b, FRAC)), p.e_two);
+        typename P::S c, d;
+        pr.bm2(u, s + 1, y0, a, y1, b, c, d);
+        y0 = pr.shr_(c, FRAC); y1 = pr.shr_(d, FRAC);
+        s += 2;
+    }
+}
+
+// ---- RSQRT(x; iters, exp) ---------------------------------------------
+template <bool WIDE, class P>
+__device__ __forceinline__ typename P::S rsqrt_group(P& pr, u64 u, u64 q, u32 s, const NrK& p,
+                                                     typename P::S x, int lane)
+{
+    typename P::S g = exp_group<WIDE>(pr, u, q, s, p.exp, pr.neg(pr.addp(pr.shr_(x, 1), p.e_02)), lane);
+    s += exp_steps(p.exp);
+    typename P::S y = pr.addp(pr.mulf(g, p.e_22), p.e_02);
+    for (int it = 0; it < p.iters; ++it) {
+        const typename P::S qq = pr.shr_(pr.bm(u, s, y, y), FRAC);
+        const typename P::S pp = pr.shr_(pr.bm(u, s + 1, x, qq), FRAC);
+        const typename P::S uu = pr.shr_(pr.bm(u, s + 2, y, pr.addp(pr.neg(pp), p.e_three)), FRAC);
+        y = pr.mulf(uu, p.e_half);
+        s += 3;
+    }
+    return y;
+}
+
+template <class P>
+__device__ __forceinline__ void rsqrt_pair(P& pr, u64 u, u32 s, const NrK& p, typename P::S x0, typename P::S x1,
+                                           typename P::S& y0, typename P::S& y1)
+{
+    typename P::S g0 = pr.neg(pr.addp(pr.shr_(x0, 1), p.e_02)), g1 = pr.neg(pr.addp(pr.shr_(x1, 1), p.e_02));
+    exp_pair(pr, u, s, p.exp, g0, g1);
+    s += exp_steps(p.exp);
+    y0 = pr.addp(pr.mulf(g0, p.e_22), p.e_02);
+    y1 = pr.addp(pr.mulf(g1, p.e_22), p.e_02);
+    for (int it = 0; it < p.iters; ++it) {
+        typename P::S a, b, c, d;
+        pr.bm2(u, s, y0, y0, y1, y1, a, b);
+        a = pr.shr_(a, FRAC); b = pr.shr_(b, FRAC);
+        pr.bm2(u, s + 1, x0, a, x1, b, c, d);
+        c = pr.addp(pr.neg(pr.shr_(c, FRAC)), p.e_three);
+        d = pr.addp(pr.neg(pr.shr_(d, FRAC)), p.e_three);
+        pr.bm2(u, s + 2, y0, c, y1, d, a, b);
+        y0 = pr.mulf(pr.shr_(a, FRAC), p.e_half);
+        y1 = pr.mulf(pr.shr_(b, FRAC), p.e_half);
+        s += 3;
+    }
+}
+
+// ---- HORNER(v; c_0..c_d), d >= 1 ---------------------------------------------------------------
+template <class P>
+__device__ __forceinline__ typename P::S horner(P& pr, u64 u, u32 s, const u64* c, int d, typename P::S v)
+{
+    typename P::S h = pr.addp(pr.mulf(v, c[d]), c[d - 1]);
+    for (int k = d - 2; k >= 0; --k) {
+        h = pr.addp(pr.shr_(pr.bm(u, s, h, v), FRAC), c[k]);
+        ++s;
+    }
+    return h;
+}
+
+// ---- segment forms of S13 (R21, R30) ------------------------------------
+template <bool WIDE, class P>
+__device__ __forceinline__ typename P::S act_group(P& pr, u64 u, u64 q, u32 s, const ActK& p,
+                                                   typename P::S x, int lane)
+{
+    using S = typename P::S;
+    if (p.form == 2 || p.deg == 0) {
+        const S nl = pr.notb(pr.template ltz<WIDE>(q, s, p.w, x, lane));
+        if (p.act == 2) return pr.shl(nl, FRAC);
+        return pr.bm(u, s + 1, x, nl);
+    }
+    S sgn = pr.zero();
+    if (p.form == 1) { sgn = pr.template ltz<WIDE>(q, s, p.w, x, lane); ++s; }
+    const S l1 = pr.template ltz<WIDE>(q, s, p.w, pr.addp(x, p.e_B), lane);
+    const S l2 = pr.template ltz<WIDE>(q, s + 1, p.w, pr.addp(x, p.e_mB), lane);
+    s += 2;
+    S h;
+    if (p.form == 0) {
+        h = horner(pr, u, s, p.c, p.deg, x);
+        s += p.deg - 1;
+    } else if (p.form == 1) {
+        const S ax = pr.bm(u, s, x, pr.pm1(sgn));
+        ++s;
+        h = pr.add(pr.mulf(x, p.e_half), horner(pr, u, s, p.c, p.deg, ax));
+        s += p.deg - 1;
+    } else {
+        const S z = pr.mulf(x, p.e_isqrt2);
+        const S z2 = pr.shr_(pr.bm(u, s, z, z), FRAC);
+        ++s;
+        const S Ssum = horner(pr, u, s, p.c, p.deg, z2);
+        s += p.deg - 1;
+        const S erf = pr.mulf(pr.shr_(pr.bm(u, s, z, Ssum), FRAC), p.e_2sqrtpi);
+        h = pr.mulf(pr.shr_(pr.bm(u, s + 1, x, pr.addp(erf, p.e_one)), FRAC), p.e_half);
+        s += 2;
+    }
+    S out = pr.bm(u, s, h, pr.sub(l2, l1));
+    const S nl2 = pr.notb(l2);
+    if (p.act == 2) out = pr.add(out, pr.shl(nl2, FRAC));
+    else out = pr.add(out, pr.bm(u, s + 1, x, nl2));
+    return out;
+}
+
+}  // namespace mpc
