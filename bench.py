@@ -1,16 +1,16 @@
 #!/usr/bin/env python
 """bench.py -- secret-shared elements/s of the 2-party nonlinear-operator path on B200.
 
-Step = one mpc_softmax over BASELINE config 2 (BERT-base attention softmax,
-8 x 12 x 128 x 128 scores, exp-limit t=8 + Newton-Raphson reciprocal 10 iters,
-window 33) for both parties.  N = 1: one GPU holds both parties (MPC_MODE_BOTH).
-N > 1 (torchrun): every rank runs its own batch shard (global row offset
-rank * rows, weak scaling, no data-path collective).
-Also reported (`per_op`): GELU over config 3 (8x128x3072, |x|-form deg 4) and
-ReLU over one 8-image shard of ResNet-50's first ReLU layer (config 4).
-
---impl reference times the CPU oracle (oracle/, plain C, 1 thread) on a bounded
-sample of the same workload.
+Step = one mpc_softmax over BASELINE config 2 (BERT-base attention softmax, 8 x 12 x
+128 x 128 scores, exp-limit t=8 + Newton-Raphson reciprocal 10 iters (exp t=8), window 33).
+  N = 1 : one GPU holds both parties (MPC_MODE_BOTH).
+  N > 1 : (torchrun) ranks (2k, 2k+1) form party pair k (MPC_MODE_PAIR): every opening is
+          exchanged between the pair's GPUs through NVLink peer memory inside the fused
+          kernels; pair k processes batch shard k (global row offset k*rows) -- weak
+          scaling, no inter-pair collective.  value = pairs x elements / max-over-ranks time.
+Also reported (`per_op`): GELU (cfg3), ReLU (cfg4 shard), LayerNorm and 1024-wide softmax
+(cfg5), Beaver multiply; at N = 1 also the PAIR protocol in loopback (both parties' kernels
+on one GPU).  --impl reference times the CPU oracle (plain C, 1 thread) on a bounded sample.
 """
 from __future__ import annotations
 
@@ -32,10 +32,12 @@ import workloads  # noqa: E402
 METRIC = "secret-shared elements/s per op (Softmax, GELU, ReLU) at 1/2/4/8 B200; % HBM roofline"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT, SMSP, LANES = 148, 4, 32
-# Philox4x32-10 = 10 rounds x (2 IMAD.WIDE.U32 + 2 LOP3); IMAD on the fma pipe and LOP3 on the
-# alu pipe each take 2 cycles per warp instruction (B300_MICROARCH "Pipe rates"): 40 pipe-cycles
-# per 32 blocks per SMSP on either pipe.  Peak = 148 * 4 * 32 / 40 * f_max.
+# Philox4x32-10 = 10 rounds x (2 IMAD.WIDE.U32 + 2 LOP3).  B300_MICROARCH "Pipe rates": IMAD on
+# the fma pipe, LOP3 on the alu pipe, each 2 cycles per warp instruction per SMSP -> 40 pipe
+# cycles per 32 blocks per SMSP.  Peak = 148 * 4 * 32 / 40 * f_max.
 CYCLES_PER_WARP_BLOCK = 40.0
+NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction
+PHILOX_MICROBENCH_GBS = 530.0  # tools/microbench.cu, ILP 2 at 2048 threads/SM (profiles/)
 
 
 def load_peaks():
@@ -62,10 +64,11 @@ class Clocks:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            time.sleep(0.3)
         except Exception:
             self.proc = None
 
@@ -82,11 +85,11 @@ class Clocks:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
-        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        ok = [r for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in ok]
+        mx = [float(r[2]) for r in ok if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4)
-                          if r[5 + k].lower() == "active"})
+        reasons = sorted({names[k] for r in ok for k in range(4) if r[5 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(sm)}
 
@@ -98,29 +101,126 @@ def dist_env():
     return ws, rank, local
 
 
+class Job:
+    """The run's layout: mode, party, pair index, and helpers that work in both modes."""
+
+    def __init__(self, m, torch, dist):
+        self.m, self.torch, self.dist = m, torch, dist
+        self.ws, self.rank, self.local = dist_env()
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.ws > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+            from paper_2511_19711_b200 import pair
+            self.party, self.peer, self.pair_idx, self.npairs = pair.pair_layout(self.rank, self.ws)
+            self.mode = m.binding.MODE_PAIR
+        else:
+            self.party, self.peer, self.pair_idx, self.npairs = 0, None, 0, 1
+            self.mode = m.binding.MODE_BOTH
+        self.stream = torch.cuda.current_stream(self.dev)
+
+    def ctx(self, cfg, mode=None):
+        mode = self.mode if mode is None else mode
+        c = self.m.Ctx.for_cfg(workloads.keys(cfg), device=self.local, mode=mode, party=self.party)
+        if mode == self.m.binding.MODE_PAIR:
+            from paper_2511_19711_b200 import pair
+            pair.connect(c)
+        return c
+
+    def share(self, ctx, x, off):
+        """Party 0 owns the activations: in PAIR mode party 1 derives its share r
+        from the pairwise key alone (no communication)."""
+        xt = self.torch.from_numpy(np.ascontiguousarray(x).ravel()).to(self.dev)
+        if ctx.mode == self.m.binding.MODE_PAIR and self.party == 1:
+            return ctx.share(None, owner=0, off=off, n=xt.numel())
+        return ctx.share(xt, owner=0, off=off)
+
+    def maxr(self, v):
+        if self.ws == 1:
+            return v
+        t = self.torch.tensor([v], device=self.dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+
+def timed(job, ctx, fn, steps, flush, clocks=None):
+    """K steps, CUDA events per step on the launching stream, L2 flushed between steps;
+    returns (ms per step, max over ranks), kernel records, stats delta."""
+    torch = job.torch
+    ctx.reset_stats()
+    ctx.enable_kernel_timing(True)
+    ctx.kernel_times()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    job.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    for k in range(steps):
+        flush.fill_(k)
+        evs[k][0].record(job.stream)
+        fn()
+        evs[k][1].record(job.stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
+    job.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / steps
+    kt = ctx.kernel_times()
+    ctx.enable_kernel_timing(False)
+    st = ctx.stats()
+    if ctx.mode != job.m.binding.MODE_BOTH:
+        ctx.sync()                       # raises MPC_ERR_TIMEOUT if an exchange failed
+    return job.maxr(ms), kt, st, clk
+
+
+def roofline(job, ctx_mode, kt, st, steps, ms_step, n):
+    """Dominant kernel's achieved rate vs its roofline."""
+    agg = {}
+    for name, kms, ph, _u in kt:
+        a = agg.setdefault(name, [0.0, 0, 0])
+        a[0] += kms; a[1] += ph; a[2] += 1
+    tot = sum(v[0] for v in agg.values()) or 1.0
+    dom = max(agg, key=lambda k: agg[k][0])
+    peaks = load_peaks()
+    fmax = float(peaks.get("sm_max_mhz", 1965.0))
+    peak = philox_peak_gblocks(fmax)
+    dms = agg[dom][0] / agg[dom][2]                # average launch duration
+    ach = (agg[dom][1] / agg[dom][2]) / (dms / 1e3) / 1e9
+    r = {"bound": "alu", "kernel": dom, "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "Gphilox/s",
+         "frac": round(ach / peak, 4), "traffic": None, "avg_launch_ms": round(dms, 4),
+         "share_of_step": round(agg[dom][0] / tot, 3),
+         "peak_basis": f"derived: 148 SM x 4 SMSP x 32 lanes / 40 pipe-cycles per warp-block x {fmax:.0f} MHz "
+                       f"({'measured' if not peaks.get('_fallback') else 'fallback'} sm_max); "
+                       f"measured Philox-only ceiling {PHILOX_MICROBENCH_GBS} Gphilox/s (tools/microbench.cu)",
+         "frac_of_measured_ceiling": round(ach / PHILOX_MICROBENCH_GBS, 4),
+         "hbm_frac": round(32 * n / (ms_step / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), 5)}
+    if ctx_mode != job.m.binding.MODE_BOTH:
+        bps = st["bytes_per_party"] / steps
+        r["nvlink"] = {"bytes_per_party_per_step": int(bps), "achieved_gbs": round(bps / (ms_step / 1e3) / 1e9, 2),
+                       "peak_gbs": NVLINK_PEER_GBS, "frac": round(bps / (ms_step / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
+                       "rounds_per_step": st["rounds"] // steps}
+        r["note"] = ("PAIR: philox counts both parties + dealer (the BOTH-mode work) per pair; "
+                     "each party's GPU executes its part plus party 1's dealer corrections")
+    return r
+
+
 # ---------------------------------------------------------------------------- mpc200 arm ----
 def run_mpc200(args):
     import torch
     import torch.distributed as dist
     import paper_2511_19711_b200 as m
 
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    keys = workloads.keys(2)
+    job = Job(m, torch, dist)
     rows, cols = workloads.SHAPES["cfg2_softmax"]
     n = rows * cols
-    row_off = rank * rows                      # this rank's global batch shard
-    ctx = m.Ctx.for_cfg(keys, device=local)
-    stream = torch.cuda.current_stream(dev)
-
-    # inputs: shares of synthetic scores (sharing is setup, not timed: SURVEY 8(d))
-    x = workloads.softmax_inputs(rows, cols)
-    xs = ctx.share(torch.from_numpy(x).to(dev), off=row_off * cols)
-    out = (torch.empty_like(xs[0]), torch.empty_like(xs[1]))
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)   # 512 MB > 126 MB L2
+    row_off = job.pair_idx * rows                     # this pair's global batch shard
+    ctx = job.ctx(2)
+    xs = job.share(ctx, workloads.softmax_inputs(rows, cols), row_off * cols)
+    out = ctx._empty(n)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=job.dev)   # 512 MB > 126 MB L2
     sm_kw = dict(window=33, exp_t=8, exp_clamp=0, recip_iters=10, recip_t=8)
 
     def step():
@@ -129,98 +229,51 @@ def run_mpc200(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-
-    # ---- timed region: K steps, per-step events, L2 flushed between steps ----
-    ctx.reset_stats()
-    ctx.enable_kernel_timing(True)
-    ctx.kernel_times()
-    clocks = Clocks(local)
-    clocks.start()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    for k in range(args.steps):
-        flush.fill_(k)
-        evs[k][0].record(stream)
-        step()
-        evs[k][1].record(stream)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    ms = sum(a.elapsed_time(b) for a, b in evs)
-    st = ctx.stats()
-    ktimes = ctx.kernel_times()
-    ctx.enable_kernel_timing(False)
-    if ws > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_step = ms / args.steps
-    value = ws * n / (ms_step / 1e3)
-
-    # ---- roofline of the dominant kernel (ALU bound: Philox blocks) ----
-    agg = {}
-    for name, kms, ph, _u in ktimes:
-        a = agg.setdefault(name, [0.0, 0, 0])
-        a[0] += kms; a[1] += ph; a[2] += 1
-    tot = sum(v[0] for v in agg.values()) or 1.0
-    dom = max(agg, key=lambda k: agg[k][0])
-    peaks = load_peaks()
-    fmax = float(peaks.get("sm_max_mhz", 1965.0))
-    peak = philox_peak_gblocks(fmax)
-    ach = agg[dom][1] / (agg[dom][0] / 1e3) / 1e9
-    roof = {"bound": "alu", "kernel": dom, "achieved": round(ach, 2), "peak": round(peak, 2),
-            "unit": "Gphilox/s", "frac": round(ach / peak, 4), "traffic": None,
-            "share_of_step": round(agg[dom][0] / tot, 3), "launches_per_step": agg[dom][2] // args.steps,
-            "peak_basis": f"148 SM x 4 SMSP x 32 lanes / 40 cycles per warp-block x {fmax:.0f} MHz "
-                          f"({'measured' if not peaks.get('_fallback') else 'fallback'} sm_max)",
-            "step_philox_frac": round(st["philox_calls"] / args.steps / (ms_step / 1e3) / 1e9 / peak, 4),
-            "kernels": {k: {"ms_per_step": round(v[0] / args.steps, 4), "gphilox_s": round(v[1] / (v[0] / 1e3) / 1e9, 2) if v[0] else None}
-                        for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])}}
-    hbm_bytes = 32 * n     # BOTH: read x0,x1 + write z0,z1 (algorithmic)
-    roof["hbm_frac"] = round(hbm_bytes / (ms_step / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), 5)
+    ms_step, kt, st, clk = timed(job, ctx, step, args.steps, flush, Clocks(job.local))
+    value = job.npairs * n / (ms_step / 1e3)
+    roof = roofline(job, ctx.mode, kt, st, args.steps, ms_step, n)
 
     # ---- e2e: host buffers through the public API (H2D inputs, D2H outputs inside the region) ----
-    h0 = xs[0].cpu().pin_memory(); h1 = xs[1].cpu().pin_memory()
-    o0 = torch.empty_like(h0).pin_memory(); o1 = torch.empty_like(h1).pin_memory()
-    d0, d1 = torch.empty_like(xs[0]), torch.empty_like(xs[1])
+    hin = [s.cpu().pin_memory() if s is not None else None for s in xs]
+    hout = [torch.empty_like(h).pin_memory() if h is not None else None for h in hin]
+    din = [torch.empty_like(s) if s is not None else None for s in xs]
     e2e_steps = max(3, min(args.steps, 10))
+    job.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ea.record(stream)
+    ea.record(job.stream)
     for _ in range(e2e_steps):
-        d0.copy_(h0, non_blocking=True); d1.copy_(h1, non_blocking=True)
-        ctx.softmax((d0, d1), rows, cols, row_off=row_off, out=out, **sm_kw)
-        o0.copy_(out[0], non_blocking=True); o1.copy_(out[1], non_blocking=True)
-    eb.record(stream)
+        for d, h in zip(din, hin):
+            if d is not None:
+                d.copy_(h, non_blocking=True)
+        ctx.softmax(tuple(din), rows, cols, row_off=row_off, out=out, **sm_kw)
+        for h, o in zip(hout, out):
+            if h is not None:
+                h.copy_(o, non_blocking=True)
+    eb.record(job.stream)
     torch.cuda.synchronize()
-    e_ms = ea.elapsed_time(eb) / e2e_steps
-    if ws > 1:
-        t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e_ms = float(t.item())
+    e_ms = job.maxr(ea.elapsed_time(eb) / e2e_steps)
 
-    # ---- per-op lines (GELU cfg3, ReLU cfg4 shard), same timing rules ----
-    per_op = {"softmax": {"elements": n, "elements_per_s": value / ws, "ms": round(ms_step, 4)}}
+    per_op = {"softmax": {"elements": n, "elements_per_s": value / job.npairs, "ms": round(ms_step, 4)}}
     if not args.no_per_op:
-        per_op.update(time_per_op(m, ctx, dev, stream, flush, args, rank))
+        per_op.update(time_per_op(job, m, ctx, flush, args))
+        if job.ws == 1:
+            per_op.update(time_loopback(job, m, flush, args))
 
     res = None
-    if rank == 0:
-        res = {"metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": ws, "steps": args.steps,
+    if job.rank == 0:
+        mode = ("BOTH (1 GPU holds both parties)" if job.ws == 1 else
+                f"PAIR: {job.npairs} party pair(s), openings over NVLink peer memory, batch-sharded")
+        res = {"metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": job.ws, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                "config": {"workload": "cfg2: BERT-base attention softmax 8x12x128x128 (2-party, Z_2^64, f=16)",
-                          "rows": rows, "cols": cols, "exp": "limit t=8", "recip": "NR 10 iters (exp t=8)",
-                          "window": 33, "mode": "BOTH (1 GPU holds both parties)" if ws == 1 else
-                          f"BOTH per rank, batch-sharded x{ws}", "l2": "flushed between steps (512 MB write)",
-                          "parallelism": f"dp{ws}"},
+                          "rows": rows, "cols": cols, "elements_per_pair": n, "exp": "limit t=8",
+                          "recip": "NR 10 iters (exp t=8)", "window": 33, "mode": mode,
+                          "l2": "flushed between steps (512 MB write)", "parallelism": f"pairs{job.npairs}"},
                "roofline": roof,
-               "e2e": {"value": ws * n / (e_ms / 1e3), "unit": "elements/s",
-                       "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+               "e2e": {"value": job.npairs * n / (e_ms / 1e3), "unit": "elements/s",
+                       "h2d_bytes_per_step": 16 * n * job.npairs, "d2h_bytes_per_step": 16 * n * job.npairs,
                        "ms_per_step": round(e_ms, 4)},
                "gpu_launches": st["launches"],
                "launches_per_step": st["launches"] / args.steps,
@@ -230,81 +283,84 @@ def run_mpc200(args):
                "clocks": clk, "per_op": per_op}
         if not args.no_cpu_baseline:
             res["cpu_baseline"] = cpu_baseline(args)
-    if ws > 1:
-        dist.barrier()
+    if job.ws > 1:
+        job.barrier()
         dist.destroy_process_group()
     return res
 
 
-def time_per_op(m, ctx, dev, stream, flush, args, rank):
-    import torch
+def _op_line(job, ctx, fn, n, flush, args, config):
+    for _ in range(max(1, args.warmup)):
+        fn()
+    job.torch.cuda.synchronize()
+    ms, kt, st, _ = timed(job, ctx, fn, args.steps, flush)
+    kms = sum(t[1] for t in kt) / args.steps
+    ph = st["philox_calls"] / args.steps
+    peak = philox_peak_gblocks(float(load_peaks().get("sm_max_mhz", 1965.0)))
+    line = {"elements": n, "elements_per_s": n * job.npairs / (ms / 1e3), "ms": round(ms, 4),
+            "gphilox_s": round(ph / (kms / 1e3) / 1e9, 2), "alu_frac": round(ph / (kms / 1e3) / 1e9 / peak, 4),
+            "bytes_per_party": st["bytes_per_party"] // args.steps, "rounds": st["rounds"] // args.steps,
+            "config": config}
+    if ctx.mode != job.m.binding.MODE_BOTH:
+        line["nvlink_frac"] = round(line["bytes_per_party"] / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4)
+    return line
+
+
+def time_per_op(job, m, ctx, flush, args):
+    torch = job.torch
+    k = job.pair_idx
     out = {}
-    # GELU cfg3 (|x|-form deg 4, B=3: the paper's BOLT structure)
     n3 = workloads.SHAPES["cfg3_gelu"]
-    g = ctx.share(torch.from_numpy(workloads.normal_inputs(n3, 3)).to(dev), off=rank * n3)
-    z = (torch.empty_like(g[0]), torch.empty_like(g[1]))
-    knobs = m.default_act("gelu", "poly_abs", degree=4)
-    fn = lambda: ctx._act(m.binding._L.mpc_gelu, "mpc_gelu", g, rank * n3, knobs, z)  # noqa: E731
-    out["gelu"] = _time(fn, n3, ctx, flush, stream, args)
-    out["gelu"]["config"] = "cfg3: BERT-base FFN 8x128x3072, |x|-form deg 4, B=3"
+    g = job.share(ctx, workloads.normal_inputs(n3, 3), k * n3)
+    z = ctx._empty(n3)
+    out["gelu"] = _op_line(job, ctx, lambda: ctx.gelu(g, off=k * n3, form="poly_abs", degree=4, out=z), n3, flush,
+                           args, "cfg3: BERT-base FFN 8x128x3072, |x|-form deg 4, B=3")
     del g, z
-    # ReLU: one 8-image shard of ResNet-50's first ReLU layer (32x64x112x112 / 4 pairs)
     N, C, H, W = workloads.SHAPES["cfg4_relu_first"]
     n4 = N * C * H * W // 4
-    r = ctx.share(torch.from_numpy(workloads.relu_inputs(n4)).to(dev), off=rank * n4)
-    z = (torch.empty_like(r[0]), torch.empty_like(r[1]))
-    out["relu"] = _time(lambda: ctx.relu(r, off=rank * n4, out=z), n4, ctx, flush, stream, args)
-    out["relu"]["config"] = "cfg4: ResNet-50 first ReLU, 8 images x 64 x 112 x 112, window 33"
+    r = job.share(ctx, workloads.relu_inputs(n4), k * n4)
+    z = ctx._empty(n4)
+    out["relu"] = _op_line(job, ctx, lambda: ctx.relu(r, off=k * n4, out=z), n4, flush, args,
+                           "cfg4: ResNet-50 first ReLU, 8 images x 64 x 112 x 112, window 33")
     del r, z
-    # LayerNorm: GPT-2 small, 8 x 1024 tokens x 768 (cfg5), rsqrt 3 iters (exp t=8)
     rows5, cols5 = workloads.SHAPES["cfg5_ln"]
-    ln = ctx.share(torch.from_numpy(workloads.layernorm_inputs(rows5, cols5)).to(dev), off=rank * rows5 * cols5)
-    z = (torch.empty_like(ln[0]), torch.empty_like(ln[1]))
-    out["layernorm"] = _time(lambda: ctx.layernorm(ln, rows5, cols5, row_off=rank * rows5, out=z),
-                             rows5 * cols5, ctx, flush, stream, args)
-    out["layernorm"]["config"] = "cfg5: GPT-2 LayerNorm 8192 x 768, rsqrt 3 iters, mean x E(1/d)"
+    ln = job.share(ctx, workloads.layernorm_inputs(rows5, cols5), k * rows5 * cols5)
+    z = ctx._empty(rows5 * cols5)
+    out["layernorm"] = _op_line(job, ctx, lambda: ctx.layernorm(ln, rows5, cols5, row_off=k * rows5, out=z),
+                                rows5 * cols5, flush, args, "cfg5: GPT-2 LayerNorm 8192 x 768, rsqrt 3 iters")
     del ln, z
-    # GPT-2 softmax rows (1024 wide), 1/8 of one layer's 8x12x1024x1024 scores
     rs, cs = 8 * 12 * 128, 1024
-    sm = ctx.share(torch.from_numpy(workloads.softmax_inputs(rs, cs, seed_cfg=5)).to(dev), off=rank * rs * cs)
-    z = (torch.empty_like(sm[0]), torch.empty_like(sm[1]))
-    out["softmax1024"] = _time(lambda: ctx.softmax(sm, rs, cs, row_off=rank * rs, out=z), rs * cs, ctx, flush,
-                               stream, args)
-    out["softmax1024"]["config"] = "cfg5: GPT-2 softmax rows of 1024 (12288 rows = 1/8 layer), t=8, NR 10"
+    sm = job.share(ctx, workloads.softmax_inputs(rs, cs, seed_cfg=5), k * rs * cs)
+    z = ctx._empty(rs * cs)
+    out["softmax1024"] = _op_line(job, ctx, lambda: ctx.softmax(sm, rs, cs, row_off=k * rs, out=z), rs * cs, flush,
+                                  args, "cfg5: GPT-2 softmax rows of 1024 (12288 rows = 1/8 layer), t=8, NR 10")
     del sm, z
-    # Beaver multiply alone (S4), 16M elements
     nm = 1 << 24
-    a = ctx.share(torch.from_numpy(workloads.act_inputs(nm)).to(dev))
-    b = ctx.share(torch.from_numpy(workloads.act_inputs(nm, seed_cfg=7)).to(dev))
-    z = (torch.empty_like(a[0]), torch.empty_like(a[1]))
-    out["mul"] = _time(lambda: ctx.mul(a, b, trunc_bits=16, out=z), nm, ctx, flush, stream, args)
-    out["mul"]["config"] = "Beaver multiply + trunc, 16M elements"
+    a = job.share(ctx, workloads.act_inputs(nm), k * nm)
+    b = job.share(ctx, workloads.act_inputs(nm, seed_cfg=7), k * nm)
+    z = ctx._empty(nm)
+    out["mul"] = _op_line(job, ctx, lambda: ctx.mul(a, b, off=k * nm, trunc_bits=16, out=z), nm, flush, args,
+                          "Beaver multiply + trunc, 16M elements")
+    del a, b, z
+    torch.cuda.synchronize()
     return out
 
 
-def _time(fn, n, ctx, flush, stream, args):
-    import torch
-    for _ in range(max(1, args.warmup)):
-        fn()
-    torch.cuda.synchronize()
-    ctx.enable_kernel_timing(True)
-    ctx.kernel_times()
-    ph0 = ctx.stats()["philox_calls"]
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for k in range(args.steps):
-        flush.fill_(k)
-        evs[k][0].record(stream)
-        fn()
-        evs[k][1].record(stream)
-    torch.cuda.synchronize()
-    kt = ctx.kernel_times()
-    ctx.enable_kernel_timing(False)
-    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
-    ph = (ctx.stats()["philox_calls"] - ph0) / args.steps
-    peak = philox_peak_gblocks(float(load_peaks().get("sm_max_mhz", 1965.0)))
-    kms = sum(t[1] for t in kt) / args.steps
-    return {"elements": n, "elements_per_s": n / (ms / 1e3), "ms": round(ms, 4),
-            "gphilox_s": round(ph / (kms / 1e3) / 1e9, 2), "alu_frac": round(ph / (kms / 1e3) / 1e9 / peak, 4)}
+def time_loopback(job, m, flush, args):
+    """The PAIR protocol on one GPU: both parties' kernels in one launch (MPC_MODE_PAIR_LOOPBACK),
+    every opening exchanged through memory exactly as across NVLink."""
+    rows, cols = workloads.SHAPES["cfg2_softmax"]
+    c = job.ctx(2, mode=m.binding.MODE_PAIR_LOOPBACK)
+    xs = c.share(job.torch.from_numpy(workloads.softmax_inputs(rows, cols).ravel()).to(job.dev))
+    z = c._empty(rows * cols)
+    line = _op_line(job, c, lambda: c.softmax(xs, rows, cols, out=z), rows * cols, flush, args,
+                    "cfg2 softmax, PAIR protocol in loopback (both parties on this GPU)")
+    n3 = workloads.SHAPES["cfg3_gelu"]
+    g = c.share(job.torch.from_numpy(workloads.normal_inputs(n3, 3)).to(job.dev))
+    z2 = c._empty(n3)
+    line2 = _op_line(job, c, lambda: c.gelu(g, form="poly_abs", degree=4, out=z2), n3, flush, args,
+                     "cfg3 GELU |x|-form deg 4, PAIR protocol in loopback")
+    return {"softmax_pair_loopback": line, "gelu_pair_loopback": line2}
 
 
 # ------------------------------------------------------------------------ CPU oracle ----
@@ -323,7 +379,7 @@ def _oracle_softmax_sample(rows_s):
 def cpu_baseline(args):
     """The oracle as it stands (plain C, 1 thread) on a bounded sample of cfg2."""
     rows, cols = workloads.SHAPES["cfg2_softmax"]
-    rows_s = int(os.environ.get("MPC_CPU_SAMPLE_ROWS", "2048"))
+    rows_s = int(os.environ.get("MPC_CPU_SAMPLE_ROWS", "4096"))
     dt = _oracle_softmax_sample(rows_s)
     return {"value": rows_s * cols / dt, "unit": "elements/s", "cores": 1, "kind": "oracle",
             "sample": f"{rows_s} of {rows} rows of cfg2 softmax ({rows_s * cols} elements), 1 pass, {dt:.2f} s",
@@ -335,8 +391,7 @@ def run_reference(args):
     if rank != 0:
         return None
     rows, cols = workloads.SHAPES["cfg2_softmax"]
-    # size each step so that warmup + steps finish in ~2 minutes
-    dt32 = _oracle_softmax_sample(32)
+    dt32 = _oracle_softmax_sample(32)          # size each step so the whole run takes ~2 minutes
     per_row = dt32 / 32
     budget = float(os.environ.get("MPC_REF_BUDGET_S", "120"))
     rows_s = int(max(32, min(rows, budget / (args.steps + args.warmup) / per_row)) // 32 * 32)

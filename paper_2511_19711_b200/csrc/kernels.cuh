@@ -29,6 +29,7 @@ struct PairA {
         if (loopback) { p.pty = blockIdx.x >= (unsigned)G ? 1 : 0; slot_cta = blockIdx.x - p.pty * G; }
         else { p.pty = party; slot_cta = blockIdx.x; }
         cta = slot_cta; ncta = G;
+        p.local = loopback;
         p.bind(xm[loopback ? p.pty : 0], slot_cta * (blockDim.x >> 5) + (threadIdx.x >> 5));
         return p;
     }

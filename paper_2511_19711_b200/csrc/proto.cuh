@@ -89,6 +89,16 @@ __device__ __forceinline__ void st_release_sys(u64* p, u64 v)
 {
     asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ u64 ld_acquire_gpu(const u64* p)
+{
+    u64 v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(u64* p, u64 v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ u64 ld_volatile(const u64* p)
 {
     u64 v;
@@ -109,9 +119,10 @@ struct PairP {
     u64* rx; u64* prx; u64* flag; u64* pflag; u64* rstate; int* err;
     u64 rnd;
     int dead;
+    int local;               // loopback: the peer is on this GPU -> gpu-scope release/acquire
     using S = u64;
     static constexpr bool kPair = true;
-    static constexpr u64 kTimeoutNs = 20ull * 1000 * 1000 * 1000;   // 20 s, then poison
+    static constexpr u64 kTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s, then poison
 
     __device__ __forceinline__ void bind(const XMem& m, int slot) {
         rx = m.rx + (i64)slot * XSLOT_RX;
@@ -129,16 +140,24 @@ struct PairP {
     __device__ __forceinline__ int party() const { return pty; }
     // ---- exchange: put words, exch(), get peer's words ----
     __device__ __forceinline__ void put(int lane, int k, u64 v) { prx[(rnd & 1) * (32 * XW) + lane * XW + k] = v; }
+    // The warp barrier orders every lane's stores into the peer buffer before lane 0's
+    // release of the flag (release is cumulative); the peer's acquire of the flag then
+    // makes them visible.  System scope across GPUs, GPU scope in loopback.
     __device__ __forceinline__ void exch(int lane) {
-        __threadfence_system();
+        if (!local) asm volatile("fence.acq_rel.sys;" ::: "memory");   // belt and braces across GPUs
         __syncwarp();
         ++rnd;
         if (lane == 0) {
-            st_release_sys(pflag, rnd);
+            if (local) st_release_gpu(pflag, rnd); else st_release_sys(pflag, rnd);
             if (!dead) {
-                const u64 t0 = globaltimer();
-                while (ld_acquire_sys(flag) < rnd) {
-                    if (globaltimer() - t0 > kTimeoutNs) { atomicExch(err, 1); dead = 1; break; }
+                if ((local ? ld_acquire_gpu(flag) : ld_acquire_sys(flag)) < rnd) {
+                    const u64 t0 = globaltimer();
+                    unsigned ns = 32;
+                    while ((local ? ld_acquire_gpu(flag) : ld_acquire_sys(flag)) < rnd) {
+                        __nanosleep(ns);
+                        if (ns < 256) ns <<= 1;
+                        if (globaltimer() - t0 > kTimeoutNs) { atomicExch(err, 1); dead = 1; break; }
+                    }
                 }
             }
         }
