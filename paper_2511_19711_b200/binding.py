@@ -15,7 +15,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmpc200.so")
+LIB_PATH = os.environ.get("MPC200_LIB") or os.path.join(_PKG, "libmpc200.so")   # override: A/B experiments
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libmpc200.so not found at {LIB_PATH}: run `python paper_2511_19711_b200/build.py` "

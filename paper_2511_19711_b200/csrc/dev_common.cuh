@@ -13,18 +13,22 @@ typedef unsigned int u32;
 constexpr u32 FULL = 0xffffffffu;
 constexpr int FRAC = 16;
 
-// A 64-bit Philox key split into (lo32, hi32).
+// A 64-bit Philox key split into (lo32, hi32).  Keys are warp-uniform, so the per-round
+// key bumps run on the uniform datapath (UIADD3) and LOP3 reads the key from a uniform
+// register.  (Precomputed round-key tables were tried: 40 round keys overflow the 63
+// uniform registers inside the LTZ kernels and turn into IMAD.U32 moves on the FMA pipe.)
 struct Key { u32 lo, hi; };
 
 struct Keys {
     Key ks, k0, k1;   // K_s, K_0, K_1
 };
 
+__host__ __device__ inline Key make_key(u64 k) { return Key{(u32)k, (u32)(k >> 32)}; }
+
 // Philox4x32-10 (Salmon et al. SC'11).  Counter (c0..c3), key (k0, k1); the key is
 // bumped by the Weyl constants before every round but the first.  The multiplies
-// are 32x32->64 (IMAD.WIDE.U32); keys are warp-uniform so the key schedule lives
-// in uniform registers.
-__device__ __forceinline__ uint4 philox(Key key, u32 c0, u32 c1, u32 c2, u32 c3)
+// are 32x32->64 (IMAD.WIDE.U32).
+__device__ __forceinline__ uint4 philox(const Key& key, u32 c0, u32 c1, u32 c2, u32 c3)
 {
     u32 k0 = key.lo, k1 = key.hi;
 #pragma unroll
@@ -44,7 +48,7 @@ __device__ __forceinline__ uint4 philox(Key key, u32 c0, u32 c1, u32 c2, u32 c3)
 }
 
 // PRG(K, unit, step, slot) of DESIGN.md 2.3.
-__device__ __forceinline__ uint4 prg(Key key, u64 unit, u32 step, u32 slot)
+__device__ __forceinline__ uint4 prg(const Key& key, u64 unit, u32 step, u32 slot)
 {
     return philox(key, (u32)unit, (u32)(unit >> 32), step, slot);
 }

@@ -12,7 +12,7 @@ namespace mpc {
 // ------------------------------------------------------------------ launch policies ----
 struct BothA {
     Keys K;
-    __device__ __forceinline__ BothP make(int& cta, int& ncta) const { cta = blockIdx.x; ncta = gridDim.x; return BothP{K}; }
+    __device__ __forceinline__ BothP make(int& cta, int& ncta) const { cta = blockIdx.x; ncta = gridDim.x; return BothP{&K}; }
     __device__ __forceinline__ void done(BothP&) const {}
 };
 
@@ -24,7 +24,7 @@ struct PairA {
     XMem xm[2];       // exchange memory of party 0 / 1 (remote: xm[0] only)
     __device__ __forceinline__ PairP make(int& cta, int& ncta) const {
         PairP p;
-        p.K = K;
+        p.Kp = &K;
         int slot_cta;
         if (loopback) { p.pty = blockIdx.x >= (unsigned)G ? 1 : 0; slot_cta = blockIdx.x - p.pty * G; }
         else { p.pty = party; slot_cta = blockIdx.x; }
@@ -39,7 +39,7 @@ struct PairA {
 // ------------------------------------------------------------------ drivers ----
 // GROUP driver: warp <-> 32-unit LTZ group, lane <-> unit.  off % 32 == 0.
 template <class PA, class Body>
-__global__ void __launch_bounds__(256, 3) k_groups(PA pa, i64 n, u64 off, Body body)
+__global__ void __launch_bounds__(256, 3) k_groups(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256, 3) k_groups(PA pa, i64 n, u64 off, Body b
 
 // PAIR driver: lane <-> global unit pair (2P, 2P+1) covering [off, off+n); warp-uniform loop.
 template <class PA, class Body>
-__global__ void __launch_bounds__(256, 3) k_pairs(PA pa, i64 n, u64 off, Body body)
+__global__ void __launch_bounds__(256, 3) k_pairs(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
@@ -273,7 +273,7 @@ struct SoftmaxArgs {
 __host__ __device__ inline i64 softmax_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 6 * 32; }
 
 template <bool WIDE, class PA>
-__global__ void __launch_bounds__(256, 3) k_softmax(PA pa, SoftmaxArgs a)
+__global__ void __launch_bounds__(256, 3) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
     int cta, ncta;
@@ -359,7 +359,7 @@ struct MaxArgs {
 __host__ __device__ inline i64 max_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 2 * 32; }
 
 template <bool WIDE, class PA>
-__global__ void __launch_bounds__(256, 3) k_max(PA pa, MaxArgs a)
+__global__ void __launch_bounds__(256, 3) k_max(const __grid_constant__ PA pa, MaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
     int cta, ncta;
@@ -388,7 +388,7 @@ struct LnArgs {
 
 // LAYERNORM: mu, c = x - mu, v = mean(MT(c,c)) + eps, r = RSQRT(v), out = MT(c, r)
 template <bool WIDE, class PA>
-__global__ void __launch_bounds__(256, 3) k_ln(PA pa, LnArgs a)
+__global__ void __launch_bounds__(256, 3) k_ln(const __grid_constant__ PA pa, LnArgs a)
 {
     __shared__ u64 MU[2][32], V[2][32], RS[2][32];
     int cta, ncta;

@@ -128,7 +128,7 @@ static mpc_status cuda_check(mpc_ctx* c, const char* where)
     return MPC_OK;
 }
 
-static Key mkkey(u64 k) { return Key{(u32)k, (u32)(k >> 32)}; }
+static Key mkkey(u64 k) { return make_key(k); }
 
 // E(c) = round-half-even(c * 2^16) (reading R2), host side
 static u64 E(double c) { return (u64)(long long)nearbyint(c * 65536.0); }

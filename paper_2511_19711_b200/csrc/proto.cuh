@@ -23,7 +23,8 @@ struct SO { u64* p[2]; };
 
 // ================================================================================ BOTH ====
 struct BothP {
-    Keys K;
+    const Keys* Kp;          // points into the kernel's parameter space (__grid_constant__):
+                             // round keys are read as constant-bank operands, no copies
     using S = Sh;
     static constexpr bool kPair = false;
     __device__ __forceinline__ int party() const { return -1; }
@@ -46,12 +47,12 @@ struct BothP {
         return a;
     }
     __device__ __forceinline__ S divp(S a, i64 d) const;               // per-share floor division
-    __device__ __forceinline__ S bm(u64 u, u32 s, S x, S y) { return mpc::bm(K, u, s, x, y); }
+    __device__ __forceinline__ S bm(u64 u, u32 s, S x, S y) { return mpc::bm(*Kp, u, s, x, y); }
     __device__ __forceinline__ void bm2(u64 u, u32 s, S x0, S y0, S x1, S y1, S& z0, S& z1) {
-        mpc::bm2(K, u, s, x0, y0, x1, y1, z0, z1);
+        mpc::bm2(*Kp, u, s, x0, y0, x1, y1, z0, z1);
     }
     template <bool WIDE>
-    __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(K, q, s, w, x, lane); }
+    __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(*Kp, q, s, w, x, lane); }
     __device__ __forceinline__ u64 open(S x) const { return x.s0 + x.s1; }
 };
 
@@ -113,7 +114,7 @@ __device__ __forceinline__ u64 globaltimer()
 }
 
 struct PairP {
-    Keys K;
+    const Keys* Kp;          // kernel parameter space (__grid_constant__)
     int pty;                 // 0 | 1
     // per-warp exchange state (set by bind())
     u64* rx; u64* prx; u64* flag; u64* pflag; u64* rstate; int* err;
@@ -191,11 +192,11 @@ struct PairP {
 
     // ---- Beaver (DESIGN.md 2.3/2.4); party 1 also plays the dealer's correction (R7) ----
     __device__ __forceinline__ void triple(u64 u, u32 s, u64 c0, u64& a, u64& b, u64& c) const {
-        const uint4 A0 = prg(K.k0, u, s, 0);
+        const uint4 A0 = prg(Kp->k0, u, s, 0);
         if (pty == 0) {
             a = w64(A0.x, A0.y); b = w64(A0.z, A0.w); c = c0;
         } else {
-            const uint4 A1 = prg(K.k1, u, s, 0);
+            const uint4 A1 = prg(Kp->k1, u, s, 0);
             a = w64(A1.x, A1.y); b = w64(A1.z, A1.w);
             c = (w64(A0.x, A0.y) + a) * (w64(A0.z, A0.w) + b) - c0;
         }
@@ -206,7 +207,7 @@ struct PairP {
     __device__ __forceinline__ S bm(u64 u, u32 s, S x, S y) {
         const int lane = threadIdx.x & 31;
         u64 a, b, c;
-        triple(u, s, beaver_c0(K, u, s), a, b, c);
+        triple(u, s, beaver_c0(*Kp, u, s), a, b, c);
         put(lane, 0, x - a); put(lane, 1, y - b);
         exch(lane);
         const u64 e = (x - a) + get(lane, 0), f = (y - b) + get(lane, 1);
@@ -214,7 +215,7 @@ struct PairP {
     }
     __device__ __forceinline__ void bm2(u64 u, u32 s, S x0, S y0, S x1, S y1, S& z0, S& z1) {
         const int lane = threadIdx.x & 31;
-        const uint4 C = prg(K.k0, u >> 1, s, 1);
+        const uint4 C = prg(Kp->k0, u >> 1, s, 1);
         u64 a0, b0, c0, a1, b1, c1;
         triple(u, s, w64(C.x, C.y), a0, b0, c0);
         triple(u + 1, s, w64(C.z, C.w), a1, b1, c1);
@@ -235,8 +236,81 @@ struct PairP {
         return pty == 0 ? (c ^ (d & b) ^ (e & a) ^ (d & e)) : (c ^ (d & b) ^ (e & a));
     }
 
+    // w <= 33, branch-free, daBit words in the idle slots of the last level (as ltz_narrow)
+    __device__ __forceinline__ S ltz_narrow(u64 q, u32 s, int w, S x, int lane) {
+        const int m = w - 1;
+        u32 Pp = transpose32((u32)x, lane), Gp = 0;
+        {
+            const uint4 t0 = prg(Kp->k0, q, s, ltz_slot(0, lane, 0));
+            uint4 t1 = make_uint4(0, 0, 0, 0);
+            if (pty == 1) t1 = prg(Kp->k1, q, s, ltz_slot(0, lane, 0));
+            u32 ta, tb, tc;
+            and_triple(t0, t1, 0, ta, tb, tc);
+            const u32 dd = (pty == 0 ? Pp : 0u) ^ ta, ee = (pty == 0 ? 0u : Pp) ^ tb;
+            put(lane, 0, (u64)dd | ((u64)ee << 32));
+            exch(lane);
+            const u64 pw = get(lane, 0);
+            const u32 g = and_finish(ta, tb, tc, dd ^ (u32)pw, ee ^ (u32)(pw >> 32));
+            if (lane < m) Gp = g;
+        }
+        const int L = (m > 0) ? ceil_log2i(m) : 0;
+        const bool trick = m > 16;
+        uint4 Dlo = make_uint4(0, 0, 0, 0), Dhi = make_uint4(0, 0, 0, 0);
+        u32 k1w = 0;
+        for (int k = 0; k < L; ++k) {
+            const int dl = 1 << k;
+            const int src = (lane - dl) & 31;
+            const u32 g = __shfl_sync(FULL, Gp, src), p = __shfl_sync(FULL, Pp, src);
+            const bool act = lane >= dl && lane < m;
+            const bool dab = trick && k == L - 1 && lane < 16;
+            const uint4 tg = prg(Kp->k0, q, s, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0));
+            const uint4 tp = prg(Kp->k0, q, s, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1));
+            uint4 t1 = make_uint4(0, 0, 0, 0);
+            if (pty == 1) t1 = prg(Kp->k1, q, s, dab ? 1u : ltz_slot(k + 1, lane, 0));
+            u32 ga, gb, gc, pa, pb, pc;
+            and_triple(tg, t1, 0, ga, gb, gc);
+            and_triple(tp, t1, 1, pa, pb, pc);
+            const u32 dG = Pp ^ ga, eG = g ^ gb, dP = Pp ^ pa, eP = p ^ pb;
+            put(lane, 0, (u64)dG | ((u64)eG << 32));
+            put(lane, 1, (u64)dP | ((u64)eP << 32));
+            exch(lane);
+            const u64 w0 = get(lane, 0), w1 = get(lane, 1);
+            const u32 ng = and_finish(ga, gb, gc, dG ^ (u32)w0, eG ^ (u32)(w0 >> 32));
+            const u32 np = and_finish(pa, pb, pc, dP ^ (u32)w1, eP ^ (u32)(w1 >> 32));
+            if (act) { Gp ^= ng; Pp = np; }
+            if (dab) { Dlo = tg; Dhi = tp; k1w = t1.x; }
+        }
+        u32 bp;
+        if (m == 0) bp = (u32)(x & 1ull);
+        else bp = (u32)((x >> (w - 1)) & 1ull) ^ ((__shfl_sync(FULL, Gp, m - 1) >> lane) & 1u);
+        uint4 D0;
+        u32 d1x = 0;
+        if (trick) {
+            const u32 hx = __shfl_sync(FULL, Dhi.x, lane & 15), hy = __shfl_sync(FULL, Dhi.y, lane & 15);
+            const u32 hz = __shfl_sync(FULL, Dhi.z, lane & 15);
+            D0 = lane < 16 ? Dlo : make_uint4(hx, hy, hz, 0u);
+            d1x = __shfl_sync(FULL, k1w, 0);
+        } else {
+            D0 = prg(Kp->k0, q, s, 2u + (u32)lane);
+            if (pty == 1) d1x = prg(Kp->k1, q, s, 1u).x;
+        }
+        const u64 r0A = w64(D0.x, D0.y);
+        const u32 r0B = D0.z & 1u;
+        u64 rA;
+        u32 rB;
+        if (pty == 0) { rA = r0A; rB = r0B; }
+        else { rB = (d1x >> lane) & 1u; rA = (u64)(r0B ^ rB) - r0A; }
+        const u32 mine = bp ^ rB;
+        put(lane, 0, (u64)mine);
+        exch(lane);
+        const u64 c = (u64)(mine ^ ((u32)get(lane, 0) & 1u));
+        const u64 sg = 1ull - 2ull * c;
+        return pty == 0 ? c + sg * rA : sg * rA;
+    }
+
     template <bool WIDE>
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) {
+        if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(q, s, w, x, lane);
         const int m = w - 1;
         constexpr int H = WIDE ? 2 : 1;
         u32 Pp[2], Gp[2];                                  // this party's shares of P_j, G_j
@@ -250,9 +324,9 @@ struct PairP {
                 const int j = lane + 32 * h;
                 ta[h] = tb[h] = tc[h] = 0;
                 if (j < m) {
-                    const uint4 t0 = prg(K.k0, q, s, ltz_slot(0, j, 0));
+                    const uint4 t0 = prg(Kp->k0, q, s, ltz_slot(0, j, 0));
                     uint4 t1 = make_uint4(0, 0, 0, 0);
-                    if (pty == 1) t1 = prg(K.k1, q, s, ltz_slot(0, j, 0));
+                    if (pty == 1) t1 = prg(Kp->k1, q, s, ltz_slot(0, j, 0));
                     and_triple(t0, t1, 0, ta[h], tb[h], tc[h]);
                 }
                 const u32 xin = pty == 0 ? Pp[h] : 0u, yin = pty == 0 ? 0u : Pp[h];
@@ -287,10 +361,10 @@ struct PairP {
                 if (WIDE && dl == 32) { g = Gp[0]; p = Pp[0]; }
                 ga[h] = gb[h] = gc[h] = pa[h] = pb[h] = pc[h] = 0;
                 if (act[h]) {
-                    const uint4 tg = prg(K.k0, q, s, ltz_slot(k + 1, j, 0));
-                    const uint4 tp = prg(K.k0, q, s, ltz_slot(k + 1, j, 1));
+                    const uint4 tg = prg(Kp->k0, q, s, ltz_slot(k + 1, j, 0));
+                    const uint4 tp = prg(Kp->k0, q, s, ltz_slot(k + 1, j, 1));
                     uint4 t1 = make_uint4(0, 0, 0, 0);
-                    if (pty == 1) t1 = prg(K.k1, q, s, ltz_slot(k + 1, j, 0));
+                    if (pty == 1) t1 = prg(Kp->k1, q, s, ltz_slot(k + 1, j, 0));
                     and_triple(tg, t1, 0, ga[h], gb[h], gc[h]);
                     and_triple(tp, t1, 1, pa[h], pb[h], pc[h]);
                 }
@@ -321,14 +395,14 @@ struct PairP {
             bp = (u32)((x >> (w - 1)) & 1ull) ^ ((gm >> lane) & 1u);
         }
         // daBit + B2A: party 0 holds (r0A, r0B); party 1 (r1A, r1B), r1A = (r0B ^ r1B) - r0A
-        const uint4 D0 = prg(K.k0, q, s, 2u + (u32)lane);
+        const uint4 D0 = prg(Kp->k0, q, s, 2u + (u32)lane);
         const u64 r0A = w64(D0.x, D0.y);
         const u32 r0B = D0.z & 1u;
         u64 rA;
         u32 rB;
         if (pty == 0) { rA = r0A; rB = r0B; }
         else {
-            const uint4 D1 = prg(K.k1, q, s, 1u);
+            const uint4 D1 = prg(Kp->k1, q, s, 1u);
             rB = (D1.x >> lane) & 1u;
             rA = (u64)(r0B ^ rB) - r0A;
         }

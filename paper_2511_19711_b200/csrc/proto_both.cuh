@@ -68,12 +68,80 @@ __device__ __forceinline__ void and_both(u32 x0, u32 x1, u32 y0, u32 y1,
     z1 = c1 ^ (d & b1) ^ (e & a1);
 }
 
+// LTZ_w for w <= 33 (one bit plane per lane), branch-free: every lane issues the three
+// Philox blocks of each Kogge-Stone level and keeps the result only if its plane is
+// active.  At the last level (d = 16, when w > 17) lanes 0..15 have no gate, so their
+// blocks compute the daBit words instead: D0 of element l and l+16 and the K1 word --
+// exactly the contract's blocks, issued in slots that would idle.
+__device__ __forceinline__ Sh ltz_narrow(const Keys& K, u64 q, u32 s, int w, Sh x, int lane)
+{
+    const int m = w - 1;
+    u32 P0 = transpose32((u32)x.s0, lane), P1 = transpose32((u32)x.s1, lane), G0 = 0, G1 = 0;
+    {   // g-layer: g_j = AND((x0_j, 0), (0, x1_j))
+        const uint4 t0 = prg(K.k0, q, s, ltz_slot(0, lane, 0));
+        const uint4 t1 = prg(K.k1, q, s, ltz_slot(0, lane, 0));
+        u32 g0, g1;
+        and_both(P0, 0u, 0u, P1, t0.x, t0.y, t0.z, t1.x, t1.y, g0, g1);
+        if (lane < m) { G0 = g0; G1 = g1; }
+    }
+    const int L = (m > 0) ? ceil_log2i(m) : 0;
+    const bool trick = m > 16;                      // last level has d = 16
+    uint4 Dlo = make_uint4(0, 0, 0, 0), Dhi = make_uint4(0, 0, 0, 0);
+    u32 k1w = 0;
+    for (int k = 0; k < L; ++k) {
+        const int d = 1 << k;
+        const int src = (lane - d) & 31;
+        const u32 g0 = __shfl_sync(FULL, G0, src), g1 = __shfl_sync(FULL, G1, src);
+        const u32 p0 = __shfl_sync(FULL, P0, src), p1 = __shfl_sync(FULL, P1, src);
+        const bool act = lane >= d && lane < m;
+        const bool dab = trick && k == L - 1 && lane < 16;
+        const uint4 tg = prg(K.k0, q, s, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0));
+        const uint4 tp = prg(K.k0, q, s, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1));
+        const uint4 t1 = prg(K.k1, q, s, dab ? 1u : ltz_slot(k + 1, lane, 0));
+        u32 ng0, ng1, np0, np1;
+        and_both(P0, P1, g0, g1, tg.x, tg.y, tg.z, t1.x, t1.y, ng0, ng1);
+        and_both(P0, P1, p0, p1, tp.x, tp.y, tp.z, t1.z, t1.w, np0, np1);
+        if (act) { G0 ^= ng0; G1 ^= ng1; P0 = np0; P1 = np1; }
+        if (dab) { Dlo = tg; Dhi = tp; k1w = t1.x; }
+    }
+    u32 b0, b1;
+    if (m == 0) {
+        b0 = (u32)(x.s0 & 1ull); b1 = (u32)(x.s1 & 1ull);
+    } else {
+        const u32 gm0 = __shfl_sync(FULL, G0, m - 1), gm1 = __shfl_sync(FULL, G1, m - 1);
+        b0 = (u32)((x.s0 >> (w - 1)) & 1ull) ^ ((gm0 >> lane) & 1u);
+        b1 = (u32)((x.s1 >> (w - 1)) & 1ull) ^ ((gm1 >> lane) & 1u);
+    }
+    uint4 D0;
+    u32 d1x;
+    if (trick) {
+        const u32 hx = __shfl_sync(FULL, Dhi.x, lane & 15), hy = __shfl_sync(FULL, Dhi.y, lane & 15);
+        const u32 hz = __shfl_sync(FULL, Dhi.z, lane & 15);
+        D0 = lane < 16 ? Dlo : make_uint4(hx, hy, hz, 0u);
+        d1x = __shfl_sync(FULL, k1w, 0);
+    } else {
+        D0 = prg(K.k0, q, s, 2u + (u32)lane);
+        d1x = prg(K.k1, q, s, 1u).x;
+    }
+    const u64 r0A = w64(D0.x, D0.y);
+    const u32 r0B = D0.z & 1u;
+    const u32 r1B = (d1x >> lane) & 1u;
+    const u64 r1A = (u64)(r0B ^ r1B) - r0A;
+    const u64 c = (u64)((b0 ^ r0B) ^ (b1 ^ r1B));
+    const u64 sg = 1ull - 2ull * c;
+    return {c + sg * r0A, sg * r1A};
+}
+
 // LTZ_w on the warp's 32-element group q (lane l <-> element 32q+l); DESIGN.md 2.4.
 // All 32 lanes must call it (tail lanes with any value).  Returns the scale-1
 // arithmetic sharing of bit (w-1) of rec(x).  WIDE: w > 33 (two planes per lane).
 template <bool WIDE>
 __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int lane)
 {
+#ifndef MPC_LTZ_NARROW
+#define MPC_LTZ_NARROW 0   // measured: the branchy form is 3-7% faster (register pressure)
+#endif
+    if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(K, q, s, w, x, lane);
     const int m = w - 1;
     // A2B (local): lane j receives plane j of both parties' shares.
     u32 P0[2], P1[2], G0[2], G1[2];
