@@ -189,8 +189,16 @@ def roofline(job, ctx_mode, kt, st, steps, ms_step, n):
     peak = philox_peak_gblocks(fmax)
     dms = agg[dom][0] / agg[dom][2]                # average launch duration
     ach = (agg[dom][1] / agg[dom][2]) / (dms / 1e3) / 1e9
+    traffic, tsrc = None, None
+    try:
+        tj = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        if dom in tj and ctx_mode == job.m.binding.MODE_BOTH:
+            traffic, tsrc = tj[dom]["dram_bytes"], f"profiles/{tj[dom]['report']} (ncu --set full, one launch)"
+    except Exception:
+        pass
     r = {"bound": "alu", "kernel": dom, "achieved": round(ach, 2), "peak": round(peak, 2), "unit": "Gphilox/s",
-         "frac": round(ach / peak, 4), "traffic": None, "avg_launch_ms": round(dms, 4),
+         "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": tsrc,
+         "traffic_algorithmic_bytes": 32 * n, "avg_launch_ms": round(dms, 4),
          "share_of_step": round(agg[dom][0] / tot, 3),
          "peak_basis": f"derived: 148 SM x 4 SMSP x 32 lanes / 40 pipe-cycles per warp-block x {fmax:.0f} MHz "
                        f"({'measured' if not peaks.get('_fallback') else 'fallback'} sm_max); "
