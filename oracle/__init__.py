@@ -57,18 +57,19 @@ def lib():
         L.orc_trunc.argtypes = [u64p, u64p, u64p, u64p, I64, INT]
         L.orc_ltz.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT]
         L.orc_relu.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT]
-        L.orc_exp.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT]
-        L.orc_recip.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, INT]
-        L.orc_rsqrt.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, INT]
+        L.orc_square.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT]
+        L.orc_exp.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, INT]
+        L.orc_recip.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, INT, INT]
+        L.orc_rsqrt.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, INT, INT]
         L.orc_act.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, DBL,
                               ctypes.c_void_p, INT, INT]
         L.orc_max.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, INT]
         L.orc_maxpool2d.argtypes = [CP, u64p, u64p, u64p, u64p, INT, INT, INT, INT, INT, INT, INT,
                                     I64, INT]
         L.orc_softmax.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, INT,
-                                  INT, INT, INT, INT, INT, INT, INT]
+                                  INT, INT, INT, INT, INT, INT, INT, INT, INT]
         L.orc_layernorm.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, DBL, INT,
-                                    INT, INT, INT, INT]
+                                    INT, INT, INT, INT, INT]
         L.orc_ltz_gate_count.argtypes = [INT]; L.orc_ltz_gate_count.restype = INT
         L.orc_max_levels.argtypes = [I64]; L.orc_max_levels.restype = INT
         L.orc_trunc_wrap_trials.argtypes = [INT, INT, I64, I64, ctypes.c_uint64]
@@ -166,14 +167,17 @@ class Oracle:
     def relu(self, x, off=0, window=33):
         return self._un(lib().orc_relu, x, off, window)
 
-    def exp(self, x, off=0, t=8, clamp=0, window=33):
-        return self._un(lib().orc_exp, x, off, t, clamp, window)
+    def square(self, x, off=0, trunc_bits=0):
+        return self._un(lib().orc_square, x, off, trunc_bits)
 
-    def recip(self, x, off=0, iters=10, t=8, clamp=0, window=33):
-        return self._un(lib().orc_recip, x, off, iters, t, clamp, window)
+    def exp(self, x, off=0, t=8, clamp=0, window=33, square=0):
+        return self._un(lib().orc_exp, x, off, t, clamp, window, square)
 
-    def rsqrt(self, x, off=0, iters=3, t=8, clamp=0, window=33):
-        return self._un(lib().orc_rsqrt, x, off, iters, t, clamp, window)
+    def recip(self, x, off=0, iters=10, t=8, clamp=0, window=33, square=0):
+        return self._un(lib().orc_recip, x, off, iters, t, clamp, window, square)
+
+    def rsqrt(self, x, off=0, iters=3, t=8, clamp=0, window=33, square=0):
+        return self._un(lib().orc_rsqrt, x, off, iters, t, clamp, window, square)
 
     ACT = {"gelu": 0, "silu": 1, "sigmoid": 2}
     FORM = {"poly_x": 0, "poly_abs": 1, "relu": 2, "erf": 3}
@@ -200,18 +204,18 @@ class Oracle:
         return z0, z1
 
     def softmax(self, x, rows, cols, row_off=0, window=33, exp_t=8, exp_clamp=0, exp_window=33,
-                recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33):
+                recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0, recip_square=0):
         x0, x1 = _u(x[0]), _u(x[1])
         z0, z1 = _pair(rows * cols)
         lib().orc_softmax(ctypes.byref(self.c), x0, x1, z0, z1, rows, cols, row_off, window,
-                          exp_t, exp_clamp, exp_window, recip_iters, recip_t, recip_clamp,
-                          recip_window)
+                          exp_t, exp_clamp, exp_window, exp_square, recip_iters, recip_t, recip_clamp,
+                          recip_window, recip_square)
         return z0, z1
 
     def layernorm(self, x, rows, cols, row_off=0, eps=1e-5, mean_mode=0, rsqrt_iters=3,
-                  rsqrt_t=8, rsqrt_clamp=0, rsqrt_window=33):
+                  rsqrt_t=8, rsqrt_clamp=0, rsqrt_window=33, rsqrt_square=0):
         x0, x1 = _u(x[0]), _u(x[1])
         z0, z1 = _pair(rows * cols)
         lib().orc_layernorm(ctypes.byref(self.c), x0, x1, z0, z1, rows, cols, row_off, eps,
-                            mean_mode, rsqrt_iters, rsqrt_t, rsqrt_clamp, rsqrt_window)
+                            mean_mode, rsqrt_iters, rsqrt_t, rsqrt_clamp, rsqrt_window, rsqrt_square)
         return z0, z1

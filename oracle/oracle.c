@@ -150,6 +150,45 @@ static void MT(orc_ctx* ctx, i64 n, u64 units0,
     for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], FRAC); z1[i] = shr(z1[i], FRAC); }
 }
 
+/* ------------------------------------------------------------------------ */
+/* Square with a square-pair triple (a, c = a^2) -- SURVEY 8(f) NEXT #2; the     */
+/* way CrypTen squares (its exp loop calls square(), P:653 default t=8).       */
+/* Layout: (a0, c0) = PRG(K0, u, s, 2) ; a1 = half (u&1) of     */
+/* PRG(K1, u>>1, s, 3) ; c1 = (a0+a1)^2 - c0.  e = open(y - a) (one word);      */
+/* z0 = c0 + 2 e a0 + e^2 ; z1 = c1 + 2 e a1.                                   */
+/* ------------------------------------------------------------------------ */
+static void SQ(orc_ctx* ctx, i64 n, u64 units0, const u64* y0, const u64* y1, u64* z0, u64* z1)
+{
+    u64 s = ctx->step++;
+    for (i64 i = 0; i < n; ++i) {
+        u64 u = units0 + (u64)i;
+        u32 w[4];
+        prg(ctx->key_p0, u, s, 2, w);
+        u64 a0 = w64(w[0], w[1]), c0 = w64(w[2], w[3]);
+        prg(ctx->key_p1, u >> 1, s, 3, w);
+        u64 a1 = (u & 1) ? w64(w[2], w[3]) : w64(w[0], w[1]);
+        u64 a = a0 + a1;
+        u64 c1 = a * a - c0;                        /* dealer correction -> party 1 */
+        u64 e = (y0[i] - a0) + (y1[i] - a1);        /* opened */
+        u64 r0 = c0 + 2 * e * a0 + e * e;
+        u64 r1 = c1 + 2 * e * a1;
+        z0[i] = r0; z1[i] = r1;
+    }
+}
+
+static void MS(orc_ctx* ctx, i64 n, u64 units0, const u64* y0, const u64* y1, u64* z0, u64* z1)
+{
+    SQ(ctx, n, units0, y0, y1, z0, z1);
+    for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], FRAC); z1[i] = shr(z1[i], FRAC); }
+}
+
+void orc_square(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off, int trunc_bits)
+{
+    SQ(ctx, n, (u64)off, x0, x1, z0, z1);
+    if (trunc_bits)
+        for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], trunc_bits); z1[i] = shr(z1[i], trunc_bits); }
+}
+
 void orc_mul(orc_ctx* ctx, const u64* x0, const u64* x1, const u64* y0, const u64* y1,
              u64* z0, u64* z1, i64 n, i64 off, int trunc_bits)
 {
@@ -354,7 +393,7 @@ void orc_relu(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 
 /*   t times: y = MT(y, y)                                                    */
 /* Steps: t + 2*clamp.                                                        */
 /* ------------------------------------------------------------------------ */
-static void EXP(orc_ctx* ctx, i64 n, u64 units0, int t, int clamp, int w,
+static void EXP(orc_ctx* ctx, i64 n, u64 units0, int t, int clamp, int w, int sq,
                 const u64* x0, const u64* x1, u64* y0, u64* y1)
 {
     u64 e1 = (u64)orc_encode(1.0);
@@ -370,24 +409,27 @@ static void EXP(orc_ctx* ctx, i64 n, u64 units0, int t, int clamp, int w,
         free(l0); free(l1);
     }
     free(c0); free(c1);
-    for (int k = 0; k < t; ++k) MT(ctx, n, units0, y0, y1, y0, y1, y0, y1);
+    for (int k = 0; k < t; ++k) {
+        if (sq) MS(ctx, n, units0, y0, y1, y0, y1);          /* square-pair triple (NEXT #2) */
+        else MT(ctx, n, units0, y0, y1, y0, y1, y0, y1);
+    }
 }
 
 void orc_exp(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
-             int t, int clamp, int w)
+             int t, int clamp, int w, int sq)
 {
-    EXP(ctx, n, (u64)off, t, clamp, w, x0, x1, z0, z1);
+    EXP(ctx, n, (u64)off, t, clamp, w, sq, x0, x1, z0, z1);
 }
 
 /* S11 RECIP: Newton-Raphson y <- y(2 - x y) from y0 = 3 exp(0.5 - x) + 0.003  */
 /* ("Newton-Raphson method"; S:208-216, S:240 initialisation).          */
-static void RECIP(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, int w,
+static void RECIP(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, int w, int sq,
                   const u64* x0, const u64* x1, u64* y0, u64* y1)
 {
     u64 *g0 = A(n), *g1 = A(n), *p0 = A(n), *p1 = A(n);
     for (i64 i = 0; i < n; ++i) { g0[i] = (u64)0 - x0[i]; g1[i] = (u64)0 - x1[i]; }
     addP(g0, n, 0.5);
-    EXP(ctx, n, units0, t, clamp, w, g0, g1, g0, g1);
+    EXP(ctx, n, units0, t, clamp, w, sq, g0, g1, g0, g1);
     for (i64 i = 0; i < n; ++i) { y0[i] = g0[i] * 3; y1[i] = g1[i] * 3; }   /* pmulI(g,3) */
     addP(y0, n, 0.003);
     for (int it = 0; it < iters; ++it) {
@@ -400,21 +442,21 @@ static void RECIP(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, 
 }
 
 void orc_recip(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
-               int iters, int t, int clamp, int w)
+               int iters, int t, int clamp, int w, int sq)
 {
-    RECIP(ctx, n, (u64)off, iters, t, clamp, w, x0, x1, z0, z1);
+    RECIP(ctx, n, (u64)off, iters, t, clamp, w, sq, x0, x1, z0, z1);
 }
 
 /* S12 RSQRT: y <- y (3 - x y^2) / 2 from y0 = 2.2 exp(-(x/2 + 0.2)) + 0.2     */
 /* ("uses e^x in its approximation of inverse sqrt").  */
-static void RSQRT(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, int w,
+static void RSQRT(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, int w, int sq,
                   const u64* x0, const u64* x1, u64* y0, u64* y1)
 {
     u64 *g0 = A(n), *g1 = A(n), *q0 = A(n), *q1 = A(n), *p0 = A(n), *p1 = A(n);
     for (i64 i = 0; i < n; ++i) { g0[i] = shr(x0[i], 1); g1[i] = shr(x1[i], 1); }
     addP(g0, n, 0.2);
     for (i64 i = 0; i < n; ++i) { g0[i] = (u64)0 - g0[i]; g1[i] = (u64)0 - g1[i]; }
-    EXP(ctx, n, units0, t, clamp, w, g0, g1, g0, g1);
+    EXP(ctx, n, units0, t, clamp, w, sq, g0, g1, g0, g1);
     memcpy(y0, g0, sizeof(u64) * (size_t)n); memcpy(y1, g1, sizeof(u64) * (size_t)n);
     pmulF(y0, y1, n, 2.2);
     addP(y0, n, 0.2);
@@ -430,9 +472,9 @@ static void RSQRT(orc_ctx* ctx, i64 n, u64 units0, int iters, int t, int clamp, 
 }
 
 void orc_rsqrt(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
-               int iters, int t, int clamp, int w)
+               int iters, int t, int clamp, int w, int sq)
 {
-    RSQRT(ctx, n, (u64)off, iters, t, clamp, w, x0, x1, z0, z1);
+    RSQRT(ctx, n, (u64)off, iters, t, clamp, w, sq, x0, x1, z0, z1);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -622,8 +664,8 @@ void orc_maxpool2d(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
 /* ------------------------------------------------------------------------ */
 void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
                  i64 rows, i64 cols, i64 row_off, int w,
-                 int exp_t, int exp_clamp, int exp_w,
-                 int rc_iters, int rc_t, int rc_clamp, int rc_w)
+                 int exp_t, int exp_clamp, int exp_w, int exp_sq,
+                 int rc_iters, int rc_t, int rc_clamp, int rc_w, int rc_sq)
 {
     i64 n = rows * cols;
     u64 *mx0 = A(rows), *mx1 = A(rows), *e0 = A(n), *e1 = A(n), *S0 = A(rows), *S1 = A(rows);
@@ -636,13 +678,13 @@ void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
             e1[r * cols + j] = x1[r * cols + j] - mx1[r];
         }
     u64 Ue = (u64)(row_off * cols);
-    EXP(ctx, n, Ue, exp_t, exp_clamp, exp_w, e0, e1, e0, e1);
+    EXP(ctx, n, Ue, exp_t, exp_clamp, exp_w, exp_sq, e0, e1, e0, e1);
     for (i64 r = 0; r < rows; ++r) {
         u64 a = 0, b = 0;
         for (i64 j = 0; j < cols; ++j) { a += e0[r * cols + j]; b += e1[r * cols + j]; }
         S0[r] = a; S1[r] = b;
     }
-    RECIP(ctx, rows, (u64)row_off, rc_iters, rc_t, rc_clamp, rc_w, S0, S1, r0, r1);
+    RECIP(ctx, rows, (u64)row_off, rc_iters, rc_t, rc_clamp, rc_w, rc_sq, S0, S1, r0, r1);
     for (i64 r = 0; r < rows; ++r)
         for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
     MT(ctx, n, Ue, e0, e1, b0, b1, z0, z1);
@@ -660,7 +702,7 @@ void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
 /* ------------------------------------------------------------------------ */
 void orc_layernorm(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
                    i64 rows, i64 cols, i64 row_off, double eps, int mean_mode,
-                   int rs_iters, int rs_t, int rs_clamp, int rs_w)
+                   int rs_iters, int rs_t, int rs_clamp, int rs_w, int rs_sq)
 {
     i64 n = rows * cols;
     u64 *mu0 = A(rows), *mu1 = A(rows), *c0 = A(n), *c1 = A(n), *q0 = A(n), *q1 = A(n);
@@ -688,7 +730,7 @@ void orc_layernorm(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
     if (mean_mode == 0) pmulF(v0, v1, rows, inv_d);
     else divP(v0, v1, rows, cols);
     addP(v0, rows, eps);
-    RSQRT(ctx, rows, (u64)row_off, rs_iters, rs_t, rs_clamp, rs_w, v0, v1, r0, r1);
+    RSQRT(ctx, rows, (u64)row_off, rs_iters, rs_t, rs_clamp, rs_w, rs_sq, v0, v1, r0, r1);
     for (i64 r = 0; r < rows; ++r)
         for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
     MT(ctx, n, Ue, c0, c1, b0, b1, z0, z1);

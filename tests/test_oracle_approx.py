@@ -318,3 +318,28 @@ def test_layernorm_constant_row():
     x2 = np.tile(np.array([[0.75], [-1.25]]), (1, 256))
     y2 = dec(o.layernorm(o.share(x2), 2, 256, mean_mode=0))
     assert np.max(np.abs(y2)) <= 1e-3
+
+
+@pytest.mark.parametrize("t,clamp", [(8, 0), (8, 1), (4, 0), (2, 1)])
+def test_exp_square_triples_vs_formula(t, clamp):
+    # NEXT #2: squarings with square-pair triples obey the same fixed-point bound
+    o = O()
+    x = workloads.exp_inputs(4096, tail_frac=0.05 if clamp else 0.0)
+    s = o.share(x)
+    xd = dec(s)
+    y = dec(o.exp(s, t=t, clamp=clamp, square=1))
+    f = fr.exp_limit(xd, t, clamp)
+    m = np.ones_like(xd, bool) if clamp else xd >= -(2.0 ** t)
+    assert np.all(np.abs(y - f)[m] <= (4 * 2 ** t * ULP * np.maximum(1.0, np.abs(f)))[m])
+    assert o.step == 1 + t + 2 * clamp
+
+
+def test_softmax_square_triples():
+    rows, cols = 64, 128
+    o = O(2)
+    x = workloads.softmax_inputs(rows, cols)
+    s = o.share(x)
+    y = dec(o.softmax(s, rows, cols, exp_square=1, recip_square=1)).reshape(rows, cols)
+    xd = dec(s).reshape(rows, cols)
+    assert np.max(np.abs(y - fr.softmax_formula(xd))) <= 2 * 4 * 256 * ULP + 8 * ULP
+    assert np.max(np.abs(y - fr.softmax(xd))) <= 1.1e-2

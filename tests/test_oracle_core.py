@@ -234,3 +234,16 @@ def test_shard_invariance_ltz_and_mul():
     fm = O(7).mul(x, x)
     hm = O(7).mul((x[0][100:], x[1][100:]), (x[0][100:], x[1][100:]), off=100)
     assert np.array_equal(fm[0][100:], hm[0]) and np.array_equal(fm[1][100:], hm[1])
+
+
+# ------------------------------------------------ square-pair triples (NEXT #2) ----
+def test_square_is_wrapping_square():
+    g = np.random.default_rng(31)
+    xv = [int(v) for v in g.integers(0, 2**64, 1000, dtype=np.uint64, endpoint=False)]
+    o = O(9)
+    z = o.square(shares_of(xv, 12), off=5)
+    assert rec(z) == [(a * a) & M64 for a in xv]
+    assert o.step == 10
+    # differs from the Beaver product's shares (different triple) but reconstructs the same
+    zb = O(9).mul(shares_of(xv, 12), shares_of(xv, 12), off=5)
+    assert rec(zb) == rec(z) and not np.array_equal(zb[0], z[0])
