@@ -343,6 +343,12 @@ def time_per_op(job, m, ctx, flush, args):
     out["softmax1024"] = _op_line(job, ctx, lambda: ctx.softmax(sm, rs, cs, row_off=k * rs, out=z), rs * cs, flush,
                                   args, "cfg5: GPT-2 softmax rows of 1024 (12288 rows = 1/8 layer), t=8, NR 10")
     del sm, z
+    x2 = job.share(ctx, workloads.softmax_inputs(*workloads.SHAPES["cfg2_softmax"]), k * 12288 * 128)
+    z = ctx._empty(12288 * 128)
+    out["softmax_square"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1,
+                                                                   recip_square=1, out=z), 12288 * 128, flush, args,
+                                     "cfg2 softmax with square-pair triples in every exp squaring (NEXT #2)")
+    del x2, z
     nm = 1 << 24
     a = job.share(ctx, workloads.act_inputs(nm), k * nm)
     b = job.share(ctx, workloads.act_inputs(nm, seed_cfg=7), k * nm)

@@ -145,6 +145,9 @@ mpc_status mpc_open(mpc_ctx* ctx, mpc_shares in, int64_t n, uint64_t* ring_out,
  * arithmetic shift by trunc_bits (0 or 16).  1 step, 1 round, 16 B/elem/party. */
 mpc_status mpc_mul(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z, int64_t n,
                    int64_t off, int trunc_bits);
+/* S4' square with a square-pair triple (NEXT #2): z = x*x mod 2^64, then
+ * per-share shift by trunc_bits (0 or 16).  1 step, 1 round, 8 B/elem/party. */
+mpc_status mpc_square(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off, int trunc_bits);
 /* S5 local truncation: z_i = (int64)x_i >> bits, bits in [0,63].
  * No step, no communication. */
 mpc_status mpc_trunc(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int bits);
@@ -159,7 +162,10 @@ mpc_status mpc_cmp(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t 
 mpc_status mpc_relu(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off, int window);
 
 /* ---- S10 - S13 ------------------------------------------------------------------ */
-typedef struct { int t; int clamp; int window; } mpc_exp_p;  /* t in [0,8] */
+/* exp-limit knobs: t in [0,8]; clamp 0|1; window of the clamp comparison;
+ * square 0|1: squarings with square-pair triples (NEXT #2) instead of Beaver
+ * triples -- a different (cheaper) protocol with its own output shares. */
+typedef struct { int t; int clamp; int window; int square; } mpc_exp_p;
 typedef struct { int iters; mpc_exp_p exp; } mpc_nr_p;       /* iters in [1,12]          */
 
 /* S10 exp-limit: (1 + x/2^t)^(2^t), zeroed below -2^t when clamp.

@@ -54,7 +54,7 @@ class KernelTime(ctypes.Structure):
 
 
 class ExpP(ctypes.Structure):
-    _fields_ = [("t", INT), ("clamp", INT), ("window", INT)]
+    _fields_ = [("t", INT), ("clamp", INT), ("window", INT), ("square", INT)]
 
 
 class NrP(ctypes.Structure):
@@ -95,6 +95,7 @@ _SIGS = {
     "mpc_share": [VP, VP, INT, INT, Shares, i64, i64],
     "mpc_open": [VP, Shares, i64, VP, VP, INT],
     "mpc_mul": [VP, Shares, Shares, Shares, i64, i64, INT],
+    "mpc_square": [VP, Shares, Shares, i64, i64, INT],
     "mpc_trunc": [VP, Shares, Shares, i64, INT],
     "mpc_cmp": [VP, Shares, Shares, i64, i64, INT],
     "mpc_relu": [VP, Shares, Shares, i64, i64, INT],
@@ -281,6 +282,13 @@ class Ctx:
         self._chk(_L.mpc_mul(self._h, _sh(x), _sh(y), _sh(z), n, off, trunc_bits), "mpc_mul")
         return z
 
+    def square(self, x, off=0, trunc_bits=0, out=None):
+        n = x[0].numel() if x[0] is not None else x[1].numel()
+        z = out if out is not None else self._empty(n)
+        self._stream()
+        self._chk(_L.mpc_square(self._h, _sh(x), _sh(z), n, off, trunc_bits), "mpc_square")
+        return z
+
     def trunc(self, x, bits=16, out=None):
         n = x[0].numel() if x[0] is not None else x[1].numel()
         z = out if out is not None else self._empty(n)
@@ -302,15 +310,15 @@ class Ctx:
     def relu(self, x, off=0, window=33, out=None):
         return self._un(_L.mpc_relu, "mpc_relu", x, out, off, window)
 
-    def exp(self, x, off=0, t=8, clamp=0, window=33, out=None):
-        return self._un(_L.mpc_exp, "mpc_exp", x, out, off, ctypes.byref(ExpP(t, int(clamp), window)))
+    def exp(self, x, off=0, t=8, clamp=0, window=33, square=0, out=None):
+        return self._un(_L.mpc_exp, "mpc_exp", x, out, off, ctypes.byref(ExpP(t, int(clamp), window, int(square))))
 
-    def recip(self, x, off=0, iters=10, t=8, clamp=0, window=33, out=None):
-        p = NrP(iters, ExpP(t, int(clamp), window))
+    def recip(self, x, off=0, iters=10, t=8, clamp=0, window=33, square=0, out=None):
+        p = NrP(iters, ExpP(t, int(clamp), window, int(square)))
         return self._un(_L.mpc_recip, "mpc_recip", x, out, off, ctypes.byref(p))
 
-    def rsqrt(self, x, off=0, iters=3, t=8, clamp=0, window=33, out=None):
-        p = NrP(iters, ExpP(t, int(clamp), window))
+    def rsqrt(self, x, off=0, iters=3, t=8, clamp=0, window=33, square=0, out=None):
+        p = NrP(iters, ExpP(t, int(clamp), window, int(square)))
         return self._un(_L.mpc_rsqrt, "mpc_rsqrt", x, out, off, ctypes.byref(p))
 
     def _act(self, fn, name, x, off, knobs, out):
@@ -347,17 +355,18 @@ class Ctx:
         return z
 
     def softmax(self, x, rows, cols, row_off=0, window=33, exp_t=8, exp_clamp=0, exp_window=33,
-                recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, out=None):
-        p = SoftmaxP(window, ExpP(exp_t, int(exp_clamp), exp_window),
-                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window)))
+                recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0, recip_square=0,
+                out=None):
+        p = SoftmaxP(window, ExpP(exp_t, int(exp_clamp), exp_window, int(exp_square)),
+                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))))
         z = out if out is not None else self._empty(rows * cols)
         self._stream()
         self._chk(_L.mpc_softmax(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)), "mpc_softmax")
         return z
 
     def layernorm(self, x, rows, cols, row_off=0, eps=1e-5, mean_mode=0, rsqrt_iters=3, rsqrt_t=8,
-                  rsqrt_clamp=0, rsqrt_window=33, out=None):
-        p = LnP(eps, mean_mode, NrP(rsqrt_iters, ExpP(rsqrt_t, int(rsqrt_clamp), rsqrt_window)))
+                  rsqrt_clamp=0, rsqrt_window=33, rsqrt_square=0, out=None):
+        p = LnP(eps, mean_mode, NrP(rsqrt_iters, ExpP(rsqrt_t, int(rsqrt_clamp), rsqrt_window, int(rsqrt_square))))
         z = out if out is not None else self._empty(rows * cols)
         self._stream()
         self._chk(_L.mpc_layernorm(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)),

@@ -69,6 +69,23 @@ __global__ void __launch_bounds__(256, 3) k_pairs(const __grid_constant__ PA pa,
 }
 
 // ------------------------------------------------------------------ element-wise bodies ----
+struct SquareBody {
+    u32 s; SP x; SO z; i64 n; int tb;
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
+        using S = typename P::S;
+        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
+        S xa = pr.zero(), xb = pr.zero();
+        if (v0) xa = pr.ld(x, i0);
+        if (v1) xb = pr.ld(x, i0 + 1);
+        S za, zb;
+        pr.sq2(u, s, xa, xb, za, zb);
+        if (tb) { za = pr.shr_(za, tb); zb = pr.shr_(zb, tb); }
+        if (v0) pr.st(z, i0, za);
+        if (v1) pr.st(z, i0 + 1, zb);
+    }
+};
+
 struct MulBody {
     u32 s; SP x, y; SO z; i64 n; int tb;
     template <class P>

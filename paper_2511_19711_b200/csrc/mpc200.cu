@@ -150,6 +150,12 @@ static void acct_beaver(mpc_ctx* c, u64 n)
     c->st.bytes_per_party += 16 * n;
     c->st.rounds += 1;
 }
+static void acct_square(mpc_ctx* c, u64 n)
+{
+    c->last_philox += n + (n + 1) / 2;
+    c->st.bytes_per_party += 8 * n;
+    c->st.rounds += 1;
+}
 static void acct_ltz(mpc_ctx* c, u64 n, int w)
 {
     const u64 groups = (n + 31) / 32;
@@ -403,12 +409,15 @@ static void finish(mpc_ctx* c, u64 steps)
     c->st.philox_calls += c->last_philox;
 }
 
-static bool exp_ok(const mpc_exp_p* p) { return p && p->t >= 0 && p->t <= 8 && p->window >= 1 && p->window <= 64; }
+static bool exp_ok(const mpc_exp_p* p)
+{
+    return p && p->t >= 0 && p->t <= 8 && p->window >= 1 && p->window <= 64 && (p->square == 0 || p->square == 1);
+}
 static bool nr_ok(const mpc_nr_p* p) { return p && p->iters >= 1 && p->iters <= 12 && exp_ok(&p->exp); }
 
 static ExpK mk_exp(const mpc_exp_p* p)
 {
-    return ExpK{p->t, p->clamp ? 1 : 0, p->window, E(1.0), E(ldexp(1.0, p->t))};
+    return ExpK{p->t, p->clamp ? 1 : 0, p->window, p->square ? 1 : 0, E(1.0), E(ldexp(1.0, p->t))};
 }
 static NrK mk_nr(const mpc_nr_p* p)
 {
@@ -423,7 +432,7 @@ static u64 exp_steps_h(const mpc_exp_p* p) { return (u64)p->t + (p->clamp ? 2u :
 static void acct_exp(mpc_ctx* c, u64 n, const mpc_exp_p* p)
 {
     if (p->clamp) { acct_ltz(c, n, p->window); acct_beaver(c, n); }
-    for (int k = 0; k < p->t; ++k) acct_beaver(c, n);
+    for (int k = 0; k < p->t; ++k) { if (p->square) acct_square(c, n); else acct_beaver(c, n); }
 }
 
 static int max_levels_h(i64 cols) { int L = 0; i64 m = cols; while (m > 1) { m = (m + 1) / 2; ++L; } return L; }
@@ -688,6 +697,19 @@ mpc_status mpc_mul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int64_t
     if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "mul: null pointer");
     if ((st = launch_pairs(c, n, (u64)off, MulBody{(u32)c->step, spv(c, x), spv(c, y), sov(c, z), n, tb}, "mul"))) return st;
     acct_beaver(c, (u64)n);
+    finish(c, 1);
+    return MPC_OK;
+}
+
+mpc_status mpc_square(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, int tb)
+{
+    mpc_status st = begin(c, 1);
+    if (st) return st;
+    if (tb != 0 && tb != 16) return fail(c, MPC_ERR_RANGE, "trunc_bits must be 0 or 16");
+    if (n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "bad n/off");
+    if (bad_sh(c, x) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "square: null pointer");
+    if ((st = launch_pairs(c, n, (u64)off, SquareBody{(u32)c->step, spv(c, x), sov(c, z), n, tb}, "square"))) return st;
+    acct_square(c, (u64)n);
     finish(c, 1);
     return MPC_OK;
 }

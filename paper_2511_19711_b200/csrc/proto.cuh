@@ -53,6 +53,8 @@ struct BothP {
     }
     template <bool WIDE>
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(*Kp, q, s, w, x, lane); }
+    __device__ __forceinline__ S sq(u64 u, u32 s, S y) { return mpc::sq1(*Kp, u, s, y); }
+    __device__ __forceinline__ void sq2(u64 u, u32 s, S y0, S y1, S& z0, S& z1) { mpc::sq2(*Kp, u, s, y0, y1, z0, z1); }
     __device__ __forceinline__ u64 open(S x) const { return x.s0 + x.s1; }
 };
 
@@ -223,6 +225,39 @@ struct PairP {
         exch(lane);
         z0 = bm_finish(a0, b0, c0, (x0 - a0) + get(lane, 0), (y0 - b0) + get(lane, 1));
         z1 = bm_finish(a1, b1, c1, (x1 - a1) + get(lane, 2), (y1 - b1) + get(lane, 3));
+    }
+
+    // ---- squares with square-pair triples (NEXT #2): one word per element per round ----
+    __device__ __forceinline__ void sq_triple(u64 u, u32 s, u64 a1_other_half, u64& a, u64& c) const {
+        const uint4 A0 = prg(Kp->k0, u, s, 2);
+        const u64 a0 = w64(A0.x, A0.y), c0 = w64(A0.z, A0.w);
+        if (pty == 0) { a = a0; c = c0; }
+        else { a = a1_other_half; const u64 t = a0 + a; c = t * t - c0; }
+    }
+    __device__ __forceinline__ S sq_finish(u64 a, u64 c, u64 e) const {
+        return pty == 0 ? c + 2ull * e * a + e * e : c + 2ull * e * a;
+    }
+    __device__ __forceinline__ S sq(u64 u, u32 s, S y) {
+        const int lane = threadIdx.x & 31;
+        u64 a1 = 0;
+        if (pty == 1) { const uint4 A1 = prg(Kp->k1, u >> 1, s, 3); a1 = (u & 1) ? w64(A1.z, A1.w) : w64(A1.x, A1.y); }
+        u64 a, c;
+        sq_triple(u, s, a1, a, c);
+        put(lane, 0, y - a);
+        exch(lane);
+        return sq_finish(a, c, (y - a) + get(lane, 0));
+    }
+    __device__ __forceinline__ void sq2(u64 u, u32 s, S y0, S y1, S& z0, S& z1) {
+        const int lane = threadIdx.x & 31;
+        u64 a1e = 0, a1o = 0;
+        if (pty == 1) { const uint4 A1 = prg(Kp->k1, u >> 1, s, 3); a1e = w64(A1.x, A1.y); a1o = w64(A1.z, A1.w); }
+        u64 a0, c0, a1, c1;
+        sq_triple(u, s, a1e, a0, c0);
+        sq_triple(u + 1, s, a1o, a1, c1);
+        put(lane, 0, y0 - a0); put(lane, 1, y1 - a1);
+        exch(lane);
+        z0 = sq_finish(a0, c0, (y0 - a0) + get(lane, 0));
+        z1 = sq_finish(a1, c1, (y1 - a1) + get(lane, 1));
     }
 
     // ---- AND gates on XOR-shared plane words; up to 2 gates (4 words) per round ----

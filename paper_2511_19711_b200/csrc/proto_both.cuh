@@ -56,6 +56,30 @@ __device__ __forceinline__ void bm2(const Keys& K, u64 u, u32 s, Sh x0, Sh y0, S
     z1 = bm_with_c0(K, u + 1, s, x1, y1, w64(C.z, C.w));
 }
 
+// Square with a square-pair triple:
+// (a0, c0) = PRG(K0,u,s,2); a1 = half (u&1) of PRG(K1,u>>1,s,3); c1 = (a0+a1)^2 - c0;
+// e = open(y - a); z0 = c0 + 2 e a0 + e^2; z1 = c1 + 2 e a1.  One opening, 8 B/party.
+__device__ __forceinline__ Sh sq_with_a1(const Keys& K, u64 u, u32 s, Sh y, u64 a1)
+{
+    const uint4 A0 = prg(K.k0, u, s, 2);
+    const u64 a0 = w64(A0.x, A0.y), c0 = w64(A0.z, A0.w);
+    const u64 a = a0 + a1;
+    const u64 c1 = a * a - c0;                         // dealer correction -> party 1
+    const u64 e = (y.s0 - a0) + (y.s1 - a1);           // open(y - a)
+    return {c0 + 2ull * e * a0 + e * e, c1 + 2ull * e * a1};
+}
+__device__ __forceinline__ Sh sq1(const Keys& K, u64 u, u32 s, Sh y)
+{
+    const uint4 A1 = prg(K.k1, u >> 1, s, 3);
+    return sq_with_a1(K, u, s, y, (u & 1) ? w64(A1.z, A1.w) : w64(A1.x, A1.y));
+}
+__device__ __forceinline__ void sq2(const Keys& K, u64 u, u32 s, Sh y0, Sh y1, Sh& z0, Sh& z1)
+{
+    const uint4 A1 = prg(K.k1, u >> 1, s, 3);
+    z0 = sq_with_a1(K, u, s, y0, w64(A1.x, A1.y));
+    z1 = sq_with_a1(K, u + 1, s, y1, w64(A1.z, A1.w));
+}
+
 // AND on XOR-shared 32-bit plane words with triple (a0,b0,c0 | a1,b1).
 __device__ __forceinline__ void and_both(u32 x0, u32 x1, u32 y0, u32 y1,
                                          u32 a0, u32 b0, u32 c0, u32 a1, u32 b1,

@@ -8,7 +8,7 @@
 namespace mpc {
 
 // knobs with their public constants already encoded (E(c), host side)
-struct ExpK { int t, clamp, w; u64 e_one, e_2t; };
+struct ExpK { int t, clamp, w, sq; u64 e_one, e_2t; };   // sq: square-pair triples (NEXT #2)
 struct NrK  { int iters; ExpK exp; u64 e_half, e_c003, e_two, e_three, e_02, e_22; };
 constexpr int MAX_COEF = 13;
 struct ActK {
@@ -34,7 +34,7 @@ __device__ __forceinline__ typename P::S exp_group(P& pr, u64 u, u64 q, u32 s, c
         y = pr.bm(u, s + 1, y, pr.notb(l));
         s += 2;
     }
-    for (int k = 0; k < p.t; ++k) y = pr.shr_(pr.bm(u, s + k, y, y), FRAC);
+    for (int k = 0; k < p.t; ++k) y = pr.shr_(p.sq ? pr.sq(u, s + k, y) : pr.bm(u, s + k, y, y), FRAC);
     return y;
 }
 
@@ -46,7 +46,8 @@ __device__ __forceinline__ void exp_pair(P& pr, u64 u, u32 s, const ExpK& p, typ
     y1 = pr.addp(pr.shr_(y1, p.t), p.e_one);
     for (int k = 0; k < p.t; ++k) {
         typename P::S a, b;
-        pr.bm2(u, s + k, y0, y0, y1, y1, a, b);
+        if (p.sq) pr.sq2(u, s + k, y0, y1, a, b);
+        else pr.bm2(u, s + k, y0, y0, y1, y1, a, b);
         y0 = pr.shr_(a, FRAC); y1 = pr.shr_(b, FRAC);
     }
 }

@@ -134,3 +134,13 @@ def test_pair_vs_oracle_and_long_sequence(m):
         so = o.relu(so)
     p.sync()
     assert np.array_equal(sp[0].cpu().numpy(), so[0]) and np.array_equal(sp[1].cpu().numpy(), so[1])
+
+
+def test_square_ops_loopback(m):
+    b, p = ctxs(m, 2)
+    x = b.share(torch.from_numpy(workloads.softmax_inputs(64, 128)).cuda())
+    p.set_step(b.step)
+    assert eq(b.softmax(x, 64, 128, exp_square=1, recip_square=1), p.softmax(x, 64, 128, exp_square=1, recip_square=1))
+    assert eq(b.square(x, trunc_bits=16), p.square(x, trunc_bits=16))
+    assert eq(b.exp(x, off=0, clamp=1, square=1), p.exp(x, off=0, clamp=1, square=1))
+    p.sync()

@@ -308,3 +308,40 @@ def test_bad_args_raise(mpc):
     with pytest.raises(mpc.MPCError):
         c.cmp(gx, window=65)
     assert c.step == st
+
+
+# ------------------------------------------------ square-pair triples (NEXT #2) ----
+@pytest.mark.parametrize("n,off", [(1, 0), (77, 3), (100_001, 64)])
+def test_square(mpc, n, off):
+    c, o = pair_ctx(mpc, step=13)
+    x = workloads.act_inputs(n)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.square(gx, off=off, trunc_bits=16), o.square(ox, off=off, trunc_bits=16))
+    assert c.step == o.step
+
+
+@pytest.mark.parametrize("t,clamp", [(8, 0), (8, 1), (3, 0)])
+def test_exp_square(mpc, t, clamp):
+    c, o = pair_ctx(mpc, step=2)
+    x = workloads.exp_inputs(4096 + 13, tail_frac=0.05)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.exp(gx, off=32, t=t, clamp=clamp, square=1), o.exp(ox, off=32, t=t, clamp=clamp, square=1))
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 128), (32, 1024)])
+def test_softmax_square(mpc, rows, cols):
+    c, o = pair_ctx(mpc, 2, step=1)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    kw = dict(exp_square=1, recip_square=1)
+    same(c.softmax(gx, rows, cols, **kw), o.softmax(ox, rows, cols, **kw))
+
+
+def test_rsqrt_layernorm_square(mpc):
+    c, o = pair_ctx(mpc, 5, step=1)
+    x = workloads.rsqrt_inputs(3000)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.rsqrt(gx, square=1), o.rsqrt(ox, square=1))
+    y = workloads.layernorm_inputs(40, 768)
+    gy, oy = c.share(torch.from_numpy(y).cuda()), o.share(y)
+    same(c.layernorm(gy, 40, 768, rsqrt_square=1), o.layernorm(oy, 40, 768, rsqrt_square=1))
