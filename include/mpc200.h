@@ -112,6 +112,13 @@ mpc_status mpc_pair_connect(mpc_ctx* ctx, const void* peer_handle);
  * MPC_ERR_CUDA on an asynchronous CUDA error. */
 mpc_status mpc_ctx_sync(mpc_ctx* ctx);
 
+/* LTZ carry circuit: 0 = full Kogge-Stone (the S7 contract, default),
+ * 1 = carry cone (only the carry into bit w-1: 94 AND gates at w = 33 instead of 290, same
+ * rounds), used for windows <= 33.  The output shares of every op are
+ * bit-identical under both circuits (they depend only on the sign and the daBit); only the
+ * transcript, the PRG work and the bytes sent change. */
+mpc_status mpc_ctx_set_ltz_circuit(mpc_ctx* ctx, int circuit);
+
 /* Per-launch timing (for the roofline in bench.py): when enabled, every kernel the
  * context launches is bracketed by CUDA events on the context stream and tagged with
  * its algorithmic Philox4x32-10 block count.  mpc_ctx_kernel_times synchronizes on

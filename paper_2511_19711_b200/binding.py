@@ -87,6 +87,7 @@ _SIGS = {
     "mpc_version": [],
     "mpc_last_call_philox": [VP],
     "mpc_ctx_enable_kernel_timing": [VP, INT],
+    "mpc_ctx_set_ltz_circuit": [VP, INT],
     "mpc_pair_export": [VP, VP],
     "mpc_pair_connect": [VP, VP],
     "mpc_ctx_sync": [VP],
@@ -203,6 +204,10 @@ class Ctx:
     def pair_connect(self, peer_handle: bytes):
         buf = ctypes.create_string_buffer(bytes(peer_handle), PAIR_HANDLE_BYTES)
         self._chk(_L.mpc_pair_connect(self._h, ctypes.cast(buf, VP)), "mpc_pair_connect")
+
+    def set_ltz_circuit(self, circuit: int):
+        """0 = Kogge-Stone (default, the S7 contract), 1 = carry cone (NEXT #1): same output shares."""
+        self._chk(_L.mpc_ctx_set_ltz_circuit(self._h, circuit), "mpc_ctx_set_ltz_circuit")
 
     def sync(self):
         self._stream()

@@ -6,6 +6,7 @@
 // All loops that contain an opening are warp-uniform (PairP exchanges per warp).
 #pragma once
 #include "sched.cuh"
+#include "ltz_cone.cuh"
 
 namespace mpc {
 
@@ -67,6 +68,44 @@ __global__ void __launch_bounds__(256, 3) k_pairs(const __grid_constant__ PA pa,
     }
     pa.done(pr);
 }
+
+// CONE driver: warp <-> CG consecutive 32-unit groups; shared memory for the carry trees.
+constexpr int CG = 4;
+template <class PA, class Body>
+__global__ void __launch_bounds__(256, 3) k_groups_cone(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
+{
+    __shared__ ConeSmem<CG> sm[8];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const i64 ng = (n + 31) >> 5;
+    for (i64 gb = ((i64)cta * NW + warp) * CG; gb < ng; gb += (i64)ncta * NW * CG)
+        body(pr, off, gb, lane, sm[warp]);
+    pa.done(pr);
+}
+
+// cmp / relu with the carry-cone LTZ over CG groups per warp
+struct CmpConeBody {
+    u32 s; int w; SP x; SO z; int relu; i64 n;
+    template <class P>
+    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG>& sm) const {
+        using S = typename P::S;
+        S xv[CG], l[CG];
+#pragma unroll
+        for (int g = 0; g < CG; ++g) {
+            const i64 i = (gb + g) * 32 + lane;
+            xv[g] = i < n ? pr.ld(x, i) : pr.zero();
+        }
+        pr.template ltz_cone<CG>((off >> 5) + (u64)gb, s, w, xv, l, lane, sm);
+#pragma unroll
+        for (int g = 0; g < CG; ++g) {
+            const i64 i = (gb + g) * 32 + lane;
+            S r = l[g];
+            if (relu) r = pr.bm(off + (u64)i, s + 1, xv[g], pr.notb(l[g]));
+            if (i < n) pr.st(z, i, r);
+        }
+    }
+};
 
 // ------------------------------------------------------------------ element-wise bodies ----
 struct SquareBody {

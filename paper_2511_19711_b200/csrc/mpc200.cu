@@ -54,6 +54,7 @@ struct mpc_ctx {
     XAlloc xa[2];           // own (and, loopback, the other party's) exchange memory
     void* peer_base;        // MPC_MODE_PAIR: the peer's exchange memory (cudaIpc-mapped)
     int connected;
+    int circuit;            // LTZ carry circuit: 0 Kogge-Stone, 1 carry cone (2.7)
 };
 
 static bool is_pair(const mpc_ctx* c) { return c->cfg.mode != MPC_MODE_BOTH; }
@@ -156,11 +157,13 @@ static void acct_square(mpc_ctx* c, u64 n)
     c->st.bytes_per_party += 8 * n;
     c->st.rounds += 1;
 }
+static bool use_cone(const mpc_ctx* c, int w) { return c->circuit == 1 && w <= 33; }
 static void acct_ltz(mpc_ctx* c, u64 n, int w)
 {
     const u64 groups = (n + 31) / 32;
-    c->last_philox += groups * ltz_philox_per_group(w);
-    c->st.bytes_per_party += groups * (8ull * (u64)gate_count(w) + 4ull);
+    const bool cone = use_cone(c, w);
+    c->last_philox += groups * (cone ? cone_philox_per_group(w) : ltz_philox_per_group(w));
+    c->st.bytes_per_party += groups * (8ull * (u64)(cone ? cone_gate_count(w) : gate_count(w)) + 4ull);
     c->st.rounds += 2 + (w > 1 ? ceil_log2i(w - 1) : 0);
 }
 
@@ -317,6 +320,23 @@ static mpc_status launch_pairs(mpc_ctx* c, i64 n, u64 off, const Body& b, const 
     }
     const int G = pair_ctas(c, k_pairs<PairA, Body>, 0, (npairs + TPB - 1) / TPB);
     return launch_pair_kernel(c, k_pairs<PairA, Body>, G, 0, name, n, off, b);
+}
+
+template <class Body>
+static mpc_status launch_cone(mpc_ctx* c, i64 n, u64 off, const Body& b, const char* name)
+{
+    if (n <= 0) return MPC_OK;
+    const i64 nw = (((n + 31) / 32) + CG - 1) / CG;       // warps of work
+    if (!is_pair(c)) {
+        static int per_sm = occupancy(k_groups_cone<BothA, Body>);
+        rec_begin(c, name, (u64)n);
+        k_groups_cone<BothA, Body><<<grid_for(c, nw * 32, TPB, per_sm), TPB, 0, c->stream>>>(BothA{c->K}, n, off, b);
+        rec_end(c);
+        c->st.launches++;
+        return cuda_check(c, name);
+    }
+    const int G = pair_ctas(c, k_groups_cone<PairA, Body>, 0, (nw * 32 + TPB - 1) / TPB);
+    return launch_pair_kernel(c, k_groups_cone<PairA, Body>, G, 0, name, n, off, b);
 }
 
 template <class Body>
@@ -553,6 +573,14 @@ mpc_status mpc_ctx_sync(mpc_ctx* c)
     return MPC_OK;
 }
 
+mpc_status mpc_ctx_set_ltz_circuit(mpc_ctx* c, int circuit)
+{
+    if (!c) return MPC_ERR_INVALID;
+    if (circuit != 0 && circuit != 1) return fail(c, MPC_ERR_RANGE, "circuit must be 0 (Kogge-Stone) or 1 (carry cone)");
+    c->circuit = circuit;
+    return MPC_OK;
+}
+
 mpc_status mpc_ctx_enable_kernel_timing(mpc_ctx* c, int on)
 {
     if (!c) return MPC_ERR_INVALID;
@@ -722,7 +750,9 @@ static mpc_status cmp_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, 
     if (n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
     if (bad_sh(c, x) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "cmp: null pointer");
     const char* name = relu ? "relu" : "cmp";
-    st = w > 33 ? launch_groups(c, n, (u64)off, CmpBody<true>{(u32)c->step, w, spv(c, x), sov(c, z), relu}, name)
+    if (use_cone(c, w))
+        st = launch_cone(c, n, (u64)off, CmpConeBody{(u32)c->step, w, spv(c, x), sov(c, z), relu, n}, name);
+    else st = w > 33 ? launch_groups(c, n, (u64)off, CmpBody<true>{(u32)c->step, w, spv(c, x), sov(c, z), relu}, name)
                 : launch_groups(c, n, (u64)off, CmpBody<false>{(u32)c->step, w, spv(c, x), sov(c, z), relu}, name);
     if (st) return st;
     acct_ltz(c, (u64)n, w);

@@ -21,6 +21,17 @@ namespace mpc {
 struct SP { const u64* p[2]; };
 struct SO { u64* p[2]; };
 
+// carry-cone LTZ over G groups per warp (ltz_cone.cuh)
+template <int G>
+struct ConeSmem { u32 w[G][32][4]; };
+template <int G>
+__device__ void ltz_cone_both(const Keys& K, u64 q0, u32 s, int w, const Sh (&x)[G], Sh (&z)[G], int lane,
+                              ConeSmem<G>& sm);
+struct PairP;
+template <int G>
+__device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G], u64 (&z)[G], int lane,
+                              ConeSmem<G>& sm);
+
 // ================================================================================ BOTH ====
 struct BothP {
     const Keys* Kp;          // points into the kernel's parameter space (__grid_constant__):
@@ -54,6 +65,10 @@ struct BothP {
     template <bool WIDE>
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(*Kp, q, s, w, x, lane); }
     __device__ __forceinline__ S sq(u64 u, u32 s, S y) { return mpc::sq1(*Kp, u, s, y); }
+    template <int G>
+    __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G>& sm) {
+        ltz_cone_both<G>(*Kp, q0, s, w, x, z, lane, sm);
+    }
     __device__ __forceinline__ void sq2(u64 u, u32 s, S y0, S y1, S& z0, S& z1) { mpc::sq2(*Kp, u, s, y0, y1, z0, z1); }
     __device__ __forceinline__ u64 open(S x) const { return x.s0 + x.s1; }
 };
@@ -447,6 +462,11 @@ struct PairP {
         const u64 c = (u64)(mine ^ ((u32)get(lane, 0) & 1u));
         const u64 sg = 1ull - 2ull * c;
         return pty == 0 ? c + sg * rA : sg * rA;
+    }
+
+    template <int G>
+    __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G>& sm) {
+        ltz_cone_pair<G>(*this, q0, s, w, x, z, lane, sm);
     }
 
     // ---- S2 open: exchange the shares themselves ----

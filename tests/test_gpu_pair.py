@@ -144,3 +144,16 @@ def test_square_ops_loopback(m):
     assert eq(b.square(x, trunc_bits=16), p.square(x, trunc_bits=16))
     assert eq(b.exp(x, off=0, clamp=1, square=1), p.exp(x, off=0, clamp=1, square=1))
     p.sync()
+
+
+@pytest.mark.parametrize("w", [17, 33])
+def test_cone_loopback(m, w):
+    b, p = ctxs(m, 1, step=3)
+    b.set_ltz_circuit(1)
+    p.set_ltz_circuit(1)
+    x = b.share(torch.from_numpy(workloads.act_inputs(4096 * 3 + 40) * 3).cuda())
+    p.set_step(b.step)
+    assert eq(b.relu(x, off=0, window=w), p.relu(x, off=0, window=w))
+    b2, _ = ctxs(m, 1, step=p.step)
+    assert eq(b2.cmp(x, off=0, window=w), p.cmp(x, off=0, window=w))
+    p.sync()

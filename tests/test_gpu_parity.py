@@ -345,3 +345,34 @@ def test_rsqrt_layernorm_square(mpc):
     y = workloads.layernorm_inputs(40, 768)
     gy, oy = c.share(torch.from_numpy(y).cuda()), o.share(y)
     same(c.layernorm(gy, 40, 768, rsqrt_square=1), o.layernorm(oy, 40, 768, rsqrt_square=1))
+
+
+# ------------------------------------------------ carry-cone LTZ (NEXT #1) ----
+@pytest.mark.parametrize("w", [1, 2, 3, 17, 18, 21, 32, 33])
+@pytest.mark.parametrize("n", [45, 4096 + 96 + 7])
+def test_cone_ltz_matches_oracle(mpc, w, n):
+    """The carry cone computes the same sign bit, so the output shares equal the
+    Kogge-Stone contract's (oracle) bit for bit."""
+    c, o = pair_ctx(mpc, step=3)
+    c.set_ltz_circuit(1)
+    x = workloads.act_inputs(n) * 3
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.cmp(gx, off=64, window=w), o.ltz(ox, off=64, window=w))
+    same(c.relu(gx, off=0, window=w), o.relu(ox, off=0, window=w))
+
+
+def test_cone_ltz_large_sampled(mpc):
+    n = 32 * 64 * 112 * 112 // 16
+    keys = workloads.keys(4)
+    c = mpc.Ctx.for_cfg(keys)
+    c.set_ltz_circuit(1)
+    x = workloads.relu_inputs(n)
+    gx = c.share(torch.from_numpy(x).cuda())
+    s0 = c.step
+    z = c.relu(gx)
+    z0, z1 = np_(z[0]), np_(z[1])
+    for off in (0, n // 2 - (n // 2) % 32, n - 4096):
+        o = Oracle.for_cfg(keys, s0)
+        sl = slice(off, off + 4096)
+        r = o.relu((np_(gx[0])[sl], np_(gx[1])[sl]), off=off)
+        assert np.array_equal(z0[sl], r[0]) and np.array_equal(z1[sl], r[1])

@@ -30,6 +30,9 @@ g = sh(workloads.normal_inputs(workloads.SHAPES["cfg3_gelu"], 3))
 print("gelu cfg3    ", t(c, lambda: c.gelu(g, form="poly_abs", degree=4)))
 r = sh(workloads.relu_inputs(32 * 64 * 112 * 112 // 4))
 print("relu 6.4M    ", t(c, lambda: c.relu(r)))
+c.set_ltz_circuit(1)
+print("relu cone    ", t(c, lambda: c.relu(r)))
+c.set_ltz_circuit(0)
 ln = sh(workloads.layernorm_inputs(8192, 768))
 print("ln 8192x768  ", t(c, lambda: c.layernorm(ln, 8192, 768)))
 s2 = sh(workloads.softmax_inputs(12288, 1024))
