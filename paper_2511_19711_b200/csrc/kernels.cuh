@@ -75,20 +75,22 @@ template <class PA, class Body>
 __global__ void __launch_bounds__(256, 3) k_groups_cone(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
     __shared__ ConeSmem<CG> sm[8];
+    extern __shared__ __align__(16) u64 stash[];       // per-warp staging (Body::kStash u64)
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const i64 ng = (n + 31) >> 5;
     for (i64 gb = ((i64)cta * NW + warp) * CG; gb < ng; gb += (i64)ncta * NW * CG)
-        body(pr, off, gb, lane, sm[warp]);
+        body(pr, off, gb, lane, sm[warp], stash + (i64)warp * Body::kStash);
     pa.done(pr);
 }
 
 // cmp / relu with the carry-cone LTZ over CG groups per warp
 struct CmpConeBody {
+    static constexpr int kStash = 0;
     u32 s; int w; SP x; SO z; int relu; i64 n;
     template <class P>
-    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG>& sm) const {
+    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG>& sm, u64*) const {
         using S = typename P::S;
         S xv[CG], l[CG];
 #pragma unroll
@@ -102,6 +104,61 @@ struct CmpConeBody {
             const i64 i = (gb + g) * 32 + lane;
             S r = l[g];
             if (relu) r = pr.bm(off + (u64)i, s + 1, xv[g], pr.notb(l[g]));
+            if (i < n) pr.st(z, i, r);
+        }
+    }
+};
+
+// S13 with carry-cone LTZs: the 2-3 segment comparisons of CG groups run first (stashed in
+// shared memory), then each group's polynomial / final products (act_tail), same step ids.
+struct ActConeBody {
+    static constexpr int kStash = 3 * CG * 32 * 2;      // [3 ltz][CG][32 lanes][2 words]
+    u32 s; ActK p; SP x; SO z; i64 n;
+    template <class P>
+    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG>& sm, u64* st) const {
+        using S = typename P::S;
+        static_assert(sizeof(S) <= 16, "stash holds up to two words per share");
+        S xv[CG], t[CG];
+        S* stS = reinterpret_cast<S*>(st);              // [3][CG][32]
+#pragma unroll
+        for (int g = 0; g < CG; ++g) {
+            const i64 i = (gb + g) * 32 + lane;
+            xv[g] = i < n ? pr.ld(x, i) : pr.zero();
+        }
+        const u64 q0 = (off >> 5) + (u64)gb;
+        const bool relu_form = p.form == 2 || p.deg == 0;
+        u32 sl = s;
+        if (relu_form || p.form == 1) {                 // ltz(x): the ReLU mask or the sign of x
+            pr.template ltz_cone<CG>(q0, sl, p.w, xv, t, lane, sm);
+#pragma unroll
+            for (int g = 0; g < CG; ++g) stS[(0 * CG + g) * 32 + lane] = t[g];
+            ++sl;
+        }
+        if (!relu_form) {
+#pragma unroll
+            for (int g = 0; g < CG; ++g) t[g] = pr.addp(xv[g], p.e_B);
+            pr.template ltz_cone<CG>(q0, sl, p.w, t, t, lane, sm);
+#pragma unroll
+            for (int g = 0; g < CG; ++g) stS[(1 * CG + g) * 32 + lane] = t[g];
+#pragma unroll
+            for (int g = 0; g < CG; ++g) t[g] = pr.addp(xv[g], p.e_mB);
+            pr.template ltz_cone<CG>(q0, sl + 1, p.w, t, t, lane, sm);
+#pragma unroll
+            for (int g = 0; g < CG; ++g) stS[(2 * CG + g) * 32 + lane] = t[g];
+            sl += 2;
+        }
+#pragma unroll 1
+        for (int g = 0; g < CG; ++g) {
+            const i64 i = (gb + g) * 32 + lane;
+            const u64 u = off + (u64)i;
+            S r;
+            if (relu_form) {
+                const S nl = pr.notb(stS[(0 * CG + g) * 32 + lane]);
+                r = p.act == 2 ? pr.shl(nl, FRAC) : pr.bm(u, sl, xv[g], nl);
+            } else {
+                r = act_tail(pr, u, sl, p, xv[g], stS[(0 * CG + g) * 32 + lane], stS[(1 * CG + g) * 32 + lane],
+                             stS[(2 * CG + g) * 32 + lane]);
+            }
             if (i < n) pr.st(z, i, r);
         }
     }

@@ -327,16 +327,21 @@ static mpc_status launch_cone(mpc_ctx* c, i64 n, u64 off, const Body& b, const c
 {
     if (n <= 0) return MPC_OK;
     const i64 nw = (((n + 31) / 32) + CG - 1) / CG;       // warps of work
+    const size_t dyn = sizeof(u64) * (size_t)Body::kStash * NWARPS;
     if (!is_pair(c)) {
-        static int per_sm = occupancy(k_groups_cone<BothA, Body>);
+        static int per_sm = [&] {
+            cudaFuncSetAttribute(k_groups_cone<BothA, Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            return occupancy(k_groups_cone<BothA, Body>, dyn);
+        }();
         rec_begin(c, name, (u64)n);
-        k_groups_cone<BothA, Body><<<grid_for(c, nw * 32, TPB, per_sm), TPB, 0, c->stream>>>(BothA{c->K}, n, off, b);
+        k_groups_cone<BothA, Body><<<grid_for(c, nw * 32, TPB, per_sm), TPB, dyn, c->stream>>>(BothA{c->K}, n, off, b);
         rec_end(c);
         c->st.launches++;
         return cuda_check(c, name);
     }
-    const int G = pair_ctas(c, k_groups_cone<PairA, Body>, 0, (nw * 32 + TPB - 1) / TPB);
-    return launch_pair_kernel(c, k_groups_cone<PairA, Body>, G, 0, name, n, off, b);
+    cudaFuncSetAttribute(k_groups_cone<PairA, Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    const int G = pair_ctas(c, k_groups_cone<PairA, Body>, dyn, (nw * 32 + TPB - 1) / TPB);
+    return launch_pair_kernel(c, k_groups_cone<PairA, Body>, G, dyn, name, n, off, b);
 }
 
 template <class Body>
@@ -857,7 +862,9 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
         for (int i = 0; i <= p->degree; ++i) k.c[i] = E(p->coeffs[i]);
     }
     const char* name = act == 0 ? "gelu" : act == 1 ? "silu" : "sigmoid";
-    st = k.w > 33 ? launch_groups(c, n, (u64)off, ActBody<true>{(u32)c->step, k, spv(c, x), sov(c, z)}, name)
+    if (use_cone(c, k.w))
+        st = launch_cone(c, n, (u64)off, ActConeBody{(u32)c->step, k, spv(c, x), sov(c, z), n}, name);
+    else st = k.w > 33 ? launch_groups(c, n, (u64)off, ActBody<true>{(u32)c->step, k, spv(c, x), sov(c, z)}, name)
                   : launch_groups(c, n, (u64)off, ActBody<false>{(u32)c->step, k, spv(c, x), sov(c, z)}, name);
     if (st) return st;
     const u64 N = (u64)n;

@@ -142,6 +142,10 @@ __device__ __forceinline__ typename P::S horner(P& pr, u64 u, u32 s, const u64* 
     return h;
 }
 
+template <class P>
+__device__ __forceinline__ typename P::S act_tail(P& pr, u64 u, u32 s, const ActK& p, typename P::S x,
+                                                  typename P::S sgn, typename P::S l1, typename P::S l2);
+
 // ---- segment forms of S13 (R21, R30) ------------------------------------
 template <bool WIDE, class P>
 __device__ __forceinline__ typename P::S act_group(P& pr, u64 u, u64 q, u32 s, const ActK& p,
@@ -157,7 +161,15 @@ __device__ __forceinline__ typename P::S act_group(P& pr, u64 u, u64 q, u32 s, c
     if (p.form == 1) { sgn = pr.template ltz<WIDE>(q, s, p.w, x, lane); ++s; }
     const S l1 = pr.template ltz<WIDE>(q, s, p.w, pr.addp(x, p.e_B), lane);
     const S l2 = pr.template ltz<WIDE>(q, s + 1, p.w, pr.addp(x, p.e_mB), lane);
-    s += 2;
+    return act_tail(pr, u, s + 2, p, x, sgn, l1, l2);
+}
+
+// the non-comparison part of S13 (after the segment LTZs), steps from s on
+template <class P>
+__device__ __forceinline__ typename P::S act_tail(P& pr, u64 u, u32 s, const ActK& p, typename P::S x,
+                                                  typename P::S sgn, typename P::S l1, typename P::S l2)
+{
+    using S = typename P::S;
     S h;
     if (p.form == 0) {
         h = horner(pr, u, s, p.c, p.deg, x);

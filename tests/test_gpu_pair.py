@@ -157,3 +157,14 @@ def test_cone_loopback(m, w):
     b2, _ = ctxs(m, 1, step=p.step)
     assert eq(b2.cmp(x, off=0, window=w), p.cmp(x, off=0, window=w))
     p.sync()
+
+
+@pytest.mark.parametrize("form,deg", [("poly_abs", 4), ("poly_x", 2), ("relu", 0)])
+def test_cone_act_loopback(m, form, deg):
+    b, p = ctxs(m, 1, step=3)
+    b.set_ltz_circuit(1)
+    p.set_ltz_circuit(1)
+    x = b.share(torch.from_numpy(workloads.act_inputs(4096 * 2 + 40)).cuda())
+    p.set_step(b.step)
+    assert eq(b.gelu(x, form=form, degree=deg), p.gelu(x, form=form, degree=deg))
+    p.sync()

@@ -376,3 +376,22 @@ def test_cone_ltz_large_sampled(mpc):
         sl = slice(off, off + 4096)
         r = o.relu((np_(gx[0])[sl], np_(gx[1])[sl]), off=off)
         assert np.array_equal(z0[sl], r[0]) and np.array_equal(z1[sl], r[1])
+
+
+@pytest.mark.parametrize("act,form,deg", ACTS)
+def test_cone_activations(mpc, act, form, deg):
+    c, o = pair_ctx(mpc, step=4)
+    c.set_ltz_circuit(1)
+    n = 4096 * 2 + 99
+    x = workloads.act_inputs(n)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    if form == "erf":
+        knobs = mpc.default_act(act, "erf", erf_terms=deg)
+        g = getattr(c, act)(gx, off=0, form="erf", erf_terms=deg)
+        r = o.act(ox, act, "erf", 1, knobs["B"], None, deg)
+    else:
+        knobs = mpc.default_act(act, form, degree=deg)
+        g = getattr(c, act)(gx, off=0, form=form, degree=deg)
+        r = o.act(ox, act, form, knobs["degree"], knobs["B"], knobs["coeffs"] or [0.0])
+    same(g, r)
+    assert c.step == o.step

@@ -28,6 +28,9 @@ x = sh(workloads.softmax_inputs(rows, cols))
 print("softmax cfg2 ", t(c, lambda: c.softmax(x, rows, cols)))
 g = sh(workloads.normal_inputs(workloads.SHAPES["cfg3_gelu"], 3))
 print("gelu cfg3    ", t(c, lambda: c.gelu(g, form="poly_abs", degree=4)))
+c.set_ltz_circuit(1)
+print("gelu cone    ", t(c, lambda: c.gelu(g, form="poly_abs", degree=4)))
+c.set_ltz_circuit(0)
 r = sh(workloads.relu_inputs(32 * 64 * 112 * 112 // 4))
 print("relu 6.4M    ", t(c, lambda: c.relu(r)))
 c.set_ltz_circuit(1)
