@@ -301,9 +301,11 @@ struct OpenBody {
 
 // MAX_row tree (R22): levels ping-pong in A/B (stride H = ceil(cols/2));
 // the last level writes mx[rr].  Steps s + 2*lv (LTZ), s + 2*lv + 1 (mux BM).
+// A holds levels 0, 2, 4.. (stride HA = ceil(cols/2)), B levels 1, 3, .. (stride HB = ceil(HA/2)).
+// cone: the level's LTZs use the carry-cone circuit, CG groups per warp (ltz_cone.cuh).
 template <bool WIDE, class P>
 __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i64 cols, int R, u64 g0,
-                                         SO A, SO B, i64 H, SO mx)
+                                         SO A, SO B, i64 HA, i64 HB, SO mx, ConeSmem<CG>* cone)
 {
     using S = typename P::S;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
@@ -315,11 +317,46 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
         const i64 h = m / 2, mn = h + (m & 1);
         SO o; i64 lo;
         if (mn == 1) { o = mx; lo = 1; }
-        else if (lv & 1) { o = B; lo = H; }
-        else { o = A; lo = H; }
+        else if (lv & 1) { o = B; lo = HB; }
+        else { o = A; lo = HA; }
         const u32 sl = s + 2u * (u32)lv;
         const u64 ubase = g0 * (u64)h;                 // multiple of 32 (g0 is)
         const FastDiv dh = make_fastdiv((u32)h);
+        if (!WIDE && cone) {
+            const i64 nb = (h + CG - 1) / CG;
+            for (i64 b = warp; b < nb; b += NW) {
+                S d[CG], l[CG];
+#pragma unroll
+                for (int g = 0; g < CG; ++g) {
+                    const i64 v = (b * CG + g) * 32 + lane;
+                    d[g] = pr.zero();
+                    if (b * CG + g < h && v < (i64)R * h) {
+                        const i64 rr = fdiv((u32)v, dh), i = v - rr * h;
+                        d[g] = pr.sub(pr.ld(cur, rr * li + i), pr.ld(cur, rr * li + i + h));
+                    }
+                }
+                pr.template ltz_cone<CG>((ubase >> 5) + (u64)(b * CG), sl, w, d, l, lane, cone[warp]);
+#pragma unroll
+                for (int g = 0; g < CG; ++g) {
+                    const i64 v = (b * CG + g) * 32 + lane;
+                    const bool valid = b * CG + g < h && v < (i64)R * h;
+                    i64 rr = 0, i = 0;
+                    S y = pr.zero();
+                    if (valid) { rr = fdiv((u32)v, dh); i = v - rr * h; y = pr.ld(cur, rr * li + i + h); }
+                    const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d[g], pr.notb(l[g])));
+                    if (valid) {
+                        pr.st(o, rr * lo + i, sel);
+                        if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, pr.ld(cur, rr * li + m - 1));
+                    }
+                }
+            }
+            __syncthreads();
+            cur = SP{{o.p[0], o.p[1]}};
+            li = lo;
+            m = mn;
+            ++lv;
+            continue;
+        }
         for (i64 g = warp; g < h; g += NW) {            // 32*h units = h groups
             const i64 v = g * 32 + lane;
             const bool valid = v < (i64)R * h;
@@ -379,25 +416,34 @@ struct SoftmaxArgs {
     u64* gscratch;          // per-CTA work tiles when they do not fit in shared memory
     i64 work_u64;           // u64 words of one work tile
     int use_smem;
+    u64* escratch;          // per-CTA exp tile E (2 x 32 x cols), global (L2-resident)
+    int cone;               // carry-cone LTZ in the max tree (NEXT #1)
 };
 
-// work tile (u64 words), H = ceil(cols/2): A0 A1 B0 B1 (4 x 32H; reused as E0 E1 = 2 x 32 cols),
-// MX0 MX1 S0 S1 R0 R1 (6 x 32)
-__host__ __device__ inline i64 softmax_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 6 * 32; }
+// work tile (u64 words), HA = ceil(cols/2), HB = ceil(HA/2): A0 A1 (2 x 32HA), B0 B1 (2 x 32HB),
+// MX0 MX1 S0 S1 R0 R1 (6 x 32).  E lives in escratch.
+__host__ __device__ inline i64 softmax_work_u64(i64 cols)
+{
+    const i64 HA = (cols + 1) / 2, HB = (HA + 1) / 2;
+    return 64 * HA + 64 * HB + 6 * 32;
+}
 
 template <bool WIDE, class PA>
 __global__ void __launch_bounds__(256, 3) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
+    __shared__ ConeSmem<CG> cone_sm[8];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     using S = typename decltype(pr)::S;
     // loopback: the two parties' CTAs need separate tiles of scratch
     const int wslot = blockIdx.x;
     u64* W = a.use_smem ? smem : a.gscratch + (i64)wslot * a.work_u64;
-    const i64 C = a.cols, H = (C + 1) / 2;
-    SO A{{W, W + 32 * H}}, B{{W + 64 * H, W + 96 * H}}, E{{W, W + 32 * C}};
-    u64* X = W + 128 * H;
+    const i64 C = a.cols, HA = (C + 1) / 2, HB = (HA + 1) / 2;
+    SO A{{W, W + 32 * HA}}, B{{W + 64 * HA, W + 64 * HA + 32 * HB}};
+    u64* Ew = a.escratch + (i64)wslot * 64 * C;
+    SO E{{Ew, Ew + 32 * C}};
+    u64* X = W + 64 * HA + 64 * HB;
     SO MX{{X, X + 32}}, SS{{X + 64, X + 96}}, RR{{X + 128, X + 160}};
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const i64 ntiles = (a.rows + 31) / 32;
@@ -408,7 +454,7 @@ __global__ void __launch_bounds__(256, 3) k_softmax(const __grid_constant__ PA p
         const u64 g0 = a.row_off + (u64)r0;                       // global row of the tile
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
         // 1. m = MAX_row(x)
-        tile_max<WIDE>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, H, MX);
+        tile_max<WIDE>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, HA, HB, MX, a.cone ? cone_sm : nullptr);
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;
@@ -468,24 +514,31 @@ __global__ void __launch_bounds__(256, 3) k_softmax(const __grid_constant__ PA p
 struct MaxArgs {
     u32 s; int w; SP x; SO z; i64 rows, cols; u64 row_off;
     u64* gscratch; i64 work_u64; int use_smem;
+    u64* escratch; int cone;
 };
-__host__ __device__ inline i64 max_work_u64(i64 cols) { return 4 * 32 * ((cols + 1) / 2) + 2 * 32; }
+__host__ __device__ inline i64 max_work_u64(i64 cols)
+{
+    const i64 HA = (cols + 1) / 2, HB = (HA + 1) / 2;
+    return 64 * HA + 64 * HB + 2 * 32;
+}
 
 template <bool WIDE, class PA>
 __global__ void __launch_bounds__(256, 3) k_max(const __grid_constant__ PA pa, MaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
+    __shared__ ConeSmem<CG> cone_sm[8];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
-    const i64 C = a.cols, H = (C + 1) / 2;
-    SO A{{W, W + 32 * H}}, B{{W + 64 * H, W + 96 * H}}, MX{{W + 128 * H, W + 128 * H + 32}};
+    const i64 C = a.cols, HA = (C + 1) / 2, HB = (HA + 1) / 2;
+    SO A{{W, W + 32 * HA}}, B{{W + 64 * HA, W + 64 * HA + 32 * HB}};
+    SO MX{{W + 64 * HA + 64 * HB, W + 64 * HA + 64 * HB + 32}};
     const i64 ntiles = (a.rows + 31) / 32;
     for (i64 tile = cta; tile < ntiles; tile += ncta) {
         const i64 r0 = tile * 32;
         const int R = (int)min((i64)32, a.rows - r0);
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
-        tile_max<WIDE>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, H, MX);
+        tile_max<WIDE>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, HA, HB, MX, a.cone ? cone_sm : nullptr);
         const SP MXc{{MX.p[0], MX.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 : nullptr, a.z.p[1] ? a.z.p[1] + r0 : nullptr}};
         for (int rr = threadIdx.x; rr < R; rr += blockDim.x) pr.st(zt, rr, pr.ld(MXc, rr));

@@ -360,11 +360,11 @@ static mpc_status launch_groups(mpc_ctx* c, i64 n, u64 off, const Body& b, const
     return launch_pair_kernel(c, k_groups<PairA, Body>, G, 0, name, n, off, b);
 }
 
-static const size_t SMEM_LIMIT = 72 * 1024;      // keep 3 CTAs per SM
+static const size_t SMEM_LIMIT = 56 * 1024;      // + 16 KB static cone smem: keep 3 CTAs per SM
 
 // fused row kernels: work tile in shared memory when it fits, else a per-CTA global tile
 template <class Args, class KB, class KP>
-static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 work_u64, const char* name)
+static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 work_u64, i64 esc_u64, const char* name)
 {
     const i64 ntiles = (rows + 31) / 32;
     const size_t wbytes = sizeof(u64) * (size_t)work_u64;
@@ -381,10 +381,16 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
     a.use_smem = smem ? 1 : 0;
     a.gscratch = nullptr;
     a.work_u64 = work_u64;
-    if (!smem && work_u64 > 0) {
-        a.gscratch = (u64*)scratch(c, wbytes * (size_t)launched);
-        if (!a.gscratch) return fail(c, MPC_ERR_NOMEM, "%s: scratch %zu bytes", name, wbytes * (size_t)launched);
+    // one scratch allocation: [E tiles (esc_u64 per CTA)] [global work tiles if not in smem]
+    const size_t ebytes = sizeof(u64) * (size_t)esc_u64 * (size_t)launched;
+    const size_t gbytes = smem ? 0 : wbytes * (size_t)launched;
+    u64* base = nullptr;
+    if (ebytes + gbytes > 0) {
+        base = (u64*)scratch(c, ebytes + gbytes);
+        if (!base) return fail(c, MPC_ERR_NOMEM, "%s: scratch %zu bytes", name, ebytes + gbytes);
     }
+    a.escratch = base;
+    if (!smem && work_u64 > 0) a.gscratch = base + (size_t)esc_u64 * (size_t)launched;
     if (is_pair(c)) return launch_pair_kernel(c, kp, grid, dyn, name, a);
     rec_begin(c, name, (u64)rows);
     kb<<<grid, TPB, dyn, c->stream>>>(BothA{c->K}, a);
@@ -899,9 +905,10 @@ mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t
     if (bad_sh(c, x) || bad_sh(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "max args (row_off % 32)");
     if (rows > 0) {
-        MaxArgs a{(u32)c->step, w, spv(c, x), sov(c, z), rows, cols, (u64)row_off, nullptr, 0, 0};
-        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), "max")
-                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), "max");
+        MaxArgs a{(u32)c->step, w, spv(c, x), sov(c, z), rows, cols, (u64)row_off, nullptr, 0, 0, nullptr,
+                  use_cone(c, w) ? 1 : 0};
+        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), 0, "max")
+                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), 0, "max");
         if (st) return st;
         acct_max(c, rows, cols, w);
     }
@@ -936,9 +943,10 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "pool_gather"))) return st;
-        MaxArgs a{(u32)c->step, w, SP{{rowsbuf.p[0], rowsbuf.p[1]}}, sov(c, z), rows, cols, row_off, nullptr, 0, 0};
-        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), "maxpool")
-                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), "maxpool");
+        MaxArgs a{(u32)c->step, w, SP{{rowsbuf.p[0], rowsbuf.p[1]}}, sov(c, z), rows, cols, row_off, nullptr, 0, 0,
+                  nullptr, use_cone(c, w) ? 1 : 0};
+        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), 0, "maxpool")
+                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), 0, "maxpool");
         if (st) return st;
         acct_max(c, rows, cols, w);
     }
@@ -967,9 +975,10 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
         a.w = p->window; a.ek = mk_exp(&p->exp); a.rk = mk_nr(&p->recip);
         a.x = spv(c, x); a.z = sov(c, z);
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
+        a.cone = use_cone(c, p->window) ? 1 : 0;
         const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
-        st = wide ? launch_rows(c, k_softmax<true, BothA>, k_softmax<true, PairA>, a, rows, softmax_work_u64(cols), "softmax")
-                  : launch_rows(c, k_softmax<false, BothA>, k_softmax<false, PairA>, a, rows, softmax_work_u64(cols), "softmax");
+        st = wide ? launch_rows(c, k_softmax<true, BothA>, k_softmax<true, PairA>, a, rows, softmax_work_u64(cols), 64 * cols, "softmax")
+                  : launch_rows(c, k_softmax<false, BothA>, k_softmax<false, PairA>, a, rows, softmax_work_u64(cols), 64 * cols, "softmax");
         if (st) return st;
         const i64 n = rows * cols;
         acct_max(c, rows, cols, p->window);

@@ -168,3 +168,13 @@ def test_cone_act_loopback(m, form, deg):
     p.set_step(b.step)
     assert eq(b.gelu(x, form=form, degree=deg), p.gelu(x, form=form, degree=deg))
     p.sync()
+
+
+def test_cone_softmax_loopback(m):
+    b, p = ctxs(m, 2)
+    b.set_ltz_circuit(1)
+    p.set_ltz_circuit(1)
+    x = b.share(torch.from_numpy(workloads.softmax_inputs(96, 128)).cuda())
+    p.set_step(b.step)
+    assert eq(b.softmax(x, 96, 128, exp_square=1, recip_square=1), p.softmax(x, 96, 128, exp_square=1, recip_square=1))
+    p.sync()

@@ -395,3 +395,23 @@ def test_cone_activations(mpc, act, form, deg):
         r = o.act(ox, act, form, knobs["degree"], knobs["B"], knobs["coeffs"] or [0.0])
     same(g, r)
     assert c.step == o.step
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 128), (45, 77), (32, 1024), (70, 9), (33, 3)])
+def test_cone_softmax_and_max(mpc, rows, cols):
+    c, o = pair_ctx(mpc, 2, step=1)
+    c.set_ltz_circuit(1)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.max(gx, rows, cols, row_off=32), o.max(ox, rows, cols, row_off=32))
+    same(c.softmax(gx, rows, cols, row_off=32), o.softmax(ox, rows, cols, row_off=32))
+    same(c.softmax(gx, rows, cols, exp_square=1, recip_square=1), o.softmax(ox, rows, cols, exp_square=1, recip_square=1))
+
+
+def test_cone_maxpool(mpc):
+    N, C, H, W = 2, 16, 14, 15
+    c, o = pair_ctx(mpc, 4, step=1)
+    c.set_ltz_circuit(1)
+    x = workloads.maxpool_inputs((N, C, H, W)) - 0.25
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.maxpool2d(gx, N, C, H, W, 3, 2, 1, img_off=2), o.maxpool2d(ox, N, C, H, W, 3, 2, 1, img_off=2))

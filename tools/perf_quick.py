@@ -26,6 +26,10 @@ sh = lambda x: c.share(torch.from_numpy(x.ravel()).cuda())
 rows, cols = workloads.SHAPES["cfg2_softmax"]
 x = sh(workloads.softmax_inputs(rows, cols))
 print("softmax cfg2 ", t(c, lambda: c.softmax(x, rows, cols)))
+c.set_ltz_circuit(1)
+print("softmax cone ", t(c, lambda: c.softmax(x, rows, cols)))
+print("softmax c+sq ", t(c, lambda: c.softmax(x, rows, cols, exp_square=1, recip_square=1)))
+c.set_ltz_circuit(0)
 g = sh(workloads.normal_inputs(workloads.SHAPES["cfg3_gelu"], 3))
 print("gelu cfg3    ", t(c, lambda: c.gelu(g, form="poly_abs", degree=4)))
 c.set_ltz_circuit(1)
