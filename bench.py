@@ -343,12 +343,31 @@ def time_per_op(job, m, ctx, flush, args):
     out["softmax1024"] = _op_line(job, ctx, lambda: ctx.softmax(sm, rs, cs, row_off=k * rs, out=z), rs * cs, flush,
                                   args, "cfg5: GPT-2 softmax rows of 1024 (12288 rows = 1/8 layer), t=8, NR 10")
     del sm, z
+    # NEXT #1 / #2 variants of the same ops (same approximation; the cone's output shares are
+    # bit-identical to the Kogge-Stone contract's, square triples change the shares)
     x2 = job.share(ctx, workloads.softmax_inputs(*workloads.SHAPES["cfg2_softmax"]), k * 12288 * 128)
     z = ctx._empty(12288 * 128)
     out["softmax_square"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1,
                                                                    recip_square=1, out=z), 12288 * 128, flush, args,
                                      "cfg2 softmax with square-pair triples in every exp squaring (NEXT #2)")
+    ctx.set_ltz_circuit(1)
+    out["softmax_cone"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, out=z),
+                                   12288 * 128, flush, args, "cfg2 softmax, carry-cone LTZ in the max tree (NEXT #1)")
+    out["softmax_cone_square"] = _op_line(
+        job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1, recip_square=1, out=z),
+        12288 * 128, flush, args, "cfg2 softmax, carry-cone LTZ + square-pair triples (NEXT #1 + #2)")
     del x2, z
+    g = job.share(ctx, workloads.normal_inputs(n3, 3), k * n3)
+    z = ctx._empty(n3)
+    out["gelu_cone"] = _op_line(job, ctx, lambda: ctx.gelu(g, off=k * n3, form="poly_abs", degree=4, out=z), n3,
+                                flush, args, "cfg3 GELU |x|-form deg 4, carry-cone LTZ (NEXT #1)")
+    del g, z
+    r = job.share(ctx, workloads.relu_inputs(n4), k * n4)
+    z = ctx._empty(n4)
+    out["relu_cone"] = _op_line(job, ctx, lambda: ctx.relu(r, off=k * n4, out=z), n4, flush, args,
+                                "cfg4 ReLU shard, carry-cone LTZ (NEXT #1)")
+    del r, z
+    ctx.set_ltz_circuit(0)
     nm = 1 << 24
     a = job.share(ctx, workloads.act_inputs(nm), k * nm)
     b = job.share(ctx, workloads.act_inputs(nm, seed_cfg=7), k * nm)
