@@ -53,18 +53,28 @@ __global__ void __launch_bounds__(256, 3) k_groups(const __grid_constant__ PA pa
     pa.done(pr);
 }
 
-// PAIR driver: lane <-> global unit pair (2P, 2P+1) covering [off, off+n); warp-uniform loop.
+// PAIR driver: lane <-> V = P::kV global unit pairs (2P, 2P+1) per pass (pairs base + lane + 32v),
+// covering [off, off+n); warp-uniform loop.
 template <class PA, class Body>
 __global__ void __launch_bounds__(256, 3) k_pairs(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
+    constexpr int V = decltype(pr)::kV;
     const int lane = threadIdx.x & 31, NW = blockDim.x >> 5;
     const u64 p0 = off >> 1, p1 = (off + (u64)n + 1) >> 1;
-    for (u64 base = ((u64)cta * NW + (threadIdx.x >> 5)) * 32; p0 + base < p1; base += (u64)ncta * NW * 32) {
-        const u64 P = p0 + base + lane;
-        const u64 u = 2 * P;
-        body(pr, u, (i64)(u - off), P < p1);
+    for (u64 base = ((u64)cta * NW + (threadIdx.x >> 5)) * 32 * V; p0 + base < p1; base += (u64)ncta * NW * 32 * V) {
+        u64 u[V];
+        i64 i0[V];
+        bool ok[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const u64 P = p0 + base + lane + 32 * v;
+            u[v] = 2 * P;
+            i0[v] = (i64)(u[v] - off);
+            ok[v] = P < p1;
+        }
+        body.template run<V>(pr, u, i0, ok);
     }
     pa.done(pr);
 }
@@ -167,35 +177,45 @@ struct ActConeBody {
 // ------------------------------------------------------------------ element-wise bodies ----
 struct SquareBody {
     u32 s; SP x; SO z; i64 n; int tb;
-    template <class P>
-    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
+    template <int V, class P>
+    __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
         using S = typename P::S;
-        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
-        S xa = pr.zero(), xb = pr.zero();
-        if (v0) xa = pr.ld(x, i0);
-        if (v1) xb = pr.ld(x, i0 + 1);
-        S za, zb;
-        pr.sq2(u, s, xa, xb, za, zb);
-        if (tb) { za = pr.shr_(za, tb); zb = pr.shr_(zb, tb); }
-        if (v0) pr.st(z, i0, za);
-        if (v1) pr.st(z, i0 + 1, zb);
+        S xa[V], xb[V], za[V], zb[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            xa[v] = xb[v] = pr.zero();
+            if (ok[v] && i0[v] >= 0) xa[v] = pr.ld(x, i0[v]);
+            if (ok[v] && i0[v] + 1 < n) xb[v] = pr.ld(x, i0[v] + 1);
+        }
+        pr.template sq2v<V>(u, s, xa, xb, za, zb);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (tb) { za[v] = pr.shr_(za[v], tb); zb[v] = pr.shr_(zb[v], tb); }
+            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], za[v]);
+            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, zb[v]);
+        }
     }
 };
 
 struct MulBody {
     u32 s; SP x, y; SO z; i64 n; int tb;
-    template <class P>
-    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
+    template <int V, class P>
+    __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
         using S = typename P::S;
-        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
-        S xa = pr.zero(), ya = pr.zero(), xb = pr.zero(), yb = pr.zero();
-        if (v0) { xa = pr.ld(x, i0); ya = pr.ld(y, i0); }
-        if (v1) { xb = pr.ld(x, i0 + 1); yb = pr.ld(y, i0 + 1); }
-        S za, zb;
-        pr.bm2(u, s, xa, ya, xb, yb, za, zb);
-        if (tb) { za = pr.shr_(za, tb); zb = pr.shr_(zb, tb); }
-        if (v0) pr.st(z, i0, za);
-        if (v1) pr.st(z, i0 + 1, zb);
+        S xa[V], ya[V], xb[V], yb[V], za[V], zb[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            xa[v] = ya[v] = xb[v] = yb[v] = pr.zero();
+            if (ok[v] && i0[v] >= 0) { xa[v] = pr.ld(x, i0[v]); ya[v] = pr.ld(y, i0[v]); }
+            if (ok[v] && i0[v] + 1 < n) { xb[v] = pr.ld(x, i0[v] + 1); yb[v] = pr.ld(y, i0[v] + 1); }
+        }
+        pr.template bm2v<V>(u, s, xa, ya, xb, yb, za, zb);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (tb) { za[v] = pr.shr_(za[v], tb); zb[v] = pr.shr_(zb[v], tb); }
+            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], za[v]);
+            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, zb[v]);
+        }
     }
 };
 
@@ -226,15 +246,21 @@ struct ExpGroupBody {
 
 struct ExpPairBody {
     u32 s; ExpK p; SP x; SO z; i64 n;
-    template <class P>
-    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
-        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
-        typename P::S a = pr.zero(), b = pr.zero();
-        if (v0) a = pr.ld(x, i0);
-        if (v1) b = pr.ld(x, i0 + 1);
-        exp_pair(pr, u, s, p, a, b);
-        if (v0) pr.st(z, i0, a);
-        if (v1) pr.st(z, i0 + 1, b);
+    template <int V, class P>
+    __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
+        typename P::S a[V], b[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            a[v] = b[v] = pr.zero();
+            if (ok[v] && i0[v] >= 0) a[v] = pr.ld(x, i0[v]);
+            if (ok[v] && i0[v] + 1 < n) b[v] = pr.ld(x, i0[v] + 1);
+        }
+        exp_pairv<V>(pr, u, s, p, a, b);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], a[v]);
+            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, b[v]);
+        }
     }
 };
 
@@ -255,16 +281,22 @@ struct NrGroupBody {
 template <int KIND>
 struct NrPairBody {
     u32 s; NrK p; SP x; SO z; i64 n;
-    template <class P>
-    __device__ void operator()(P& pr, u64 u, i64 i0, bool ok) const {
-        const bool v0 = ok && i0 >= 0, v1 = ok && i0 + 1 < n;
-        typename P::S a = pr.zero(), b = pr.zero(), ya, yb;
-        if (v0) a = pr.ld(x, i0);
-        if (v1) b = pr.ld(x, i0 + 1);
-        if (KIND == 0) recip_pair(pr, u, s, p, a, b, ya, yb);
-        else rsqrt_pair(pr, u, s, p, a, b, ya, yb);
-        if (v0) pr.st(z, i0, ya);
-        if (v1) pr.st(z, i0 + 1, yb);
+    template <int V, class P>
+    __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
+        typename P::S a[V], b[V], ya[V], yb[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            a[v] = b[v] = pr.zero();
+            if (ok[v] && i0[v] >= 0) a[v] = pr.ld(x, i0[v]);
+            if (ok[v] && i0[v] + 1 < n) b[v] = pr.ld(x, i0[v] + 1);
+        }
+        if (KIND == 0) recip_pairv<V>(pr, u, s, p, a, b, ya, yb);
+        else rsqrt_pairv<V>(pr, u, s, p, a, b, ya, yb);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], ya[v]);
+            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, yb[v]);
+        }
     }
 };
 
@@ -469,15 +501,25 @@ __global__ void __launch_bounds__(256, 3) k_softmax(const __grid_constant__ PA p
                 if (valid) pr.st(E, e, y);
             }
         } else {
-            for (i64 base = (i64)warp * 32; base < (ne + 1) / 2; base += (i64)NW * 32) {
-                const i64 e = 2 * (base + lane);
-                const bool va = e < ne, vb = e + 1 < ne;
-                S da = pr.zero(), db = pr.zero();
-                if (va) da = pr.sub(pr.ld(xt, e), pr.ld(MXc, fdiv((u32)e, dC)));
-                if (vb) db = pr.sub(pr.ld(xt, e + 1), pr.ld(MXc, fdiv((u32)(e + 1), dC)));
-                exp_pair(pr, ub + e, a.s_exp, a.ek, da, db);
-                if (va) pr.st(E, e, da);
-                if (vb) pr.st(E, e + 1, db);
+            constexpr int V = decltype(pr)::kV;
+            for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
+                u64 uv[V];
+                S da[V], db[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    uv[v] = ub + (u64)e;
+                    da[v] = db[v] = pr.zero();
+                    if (e < ne) da[v] = pr.sub(pr.ld(xt, e), pr.ld(MXc, fdiv((u32)e, dC)));
+                    if (e + 1 < ne) db[v] = pr.sub(pr.ld(xt, e + 1), pr.ld(MXc, fdiv((u32)(e + 1), dC)));
+                }
+                exp_pairv<V>(pr, uv, a.s_exp, a.ek, da, db);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    if (e < ne) pr.st(E, e, da[v]);
+                    if (e + 1 < ne) pr.st(E, e + 1, db[v]);
+                }
             }
         }
         __syncthreads();
@@ -494,17 +536,28 @@ __global__ void __launch_bounds__(256, 3) k_softmax(const __grid_constant__ PA p
         tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR);
         // 6. out = MT(e, r), element units
         const SP Rc{{RR.p[0], RR.p[1]}};
-        for (i64 base = (i64)warp * 32; base < (ne + 1) / 2; base += (i64)NW * 32) {
-            const i64 e = 2 * (base + lane);
-            const bool va = e < ne, vb = e + 1 < ne;
-            S ea = pr.zero(), eb = pr.zero(), ra = pr.zero(), rb = pr.zero();
-            if (va) { ea = pr.ld(Ec, e); ra = pr.ld(Rc, fdiv((u32)e, dC)); }
-            if (vb) { eb = pr.ld(Ec, e + 1); rb = pr.ld(Rc, fdiv((u32)(e + 1), dC)); }
-            S za, zb;
-            pr.bm2(ub + e, a.s_mul, ea, ra, eb, rb, za, zb);
-            const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
-            if (va) pr.st(zt, e, pr.shr_(za, FRAC));
-            if (vb) pr.st(zt, e + 1, pr.shr_(zb, FRAC));
+        const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
+        {
+            constexpr int V = decltype(pr)::kV;
+            for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
+                u64 uv[V];
+                S ea[V], eb[V], ra[V], rb[V], za[V], zb[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    uv[v] = ub + (u64)e;
+                    ea[v] = eb[v] = ra[v] = rb[v] = pr.zero();
+                    if (e < ne) { ea[v] = pr.ld(Ec, e); ra[v] = pr.ld(Rc, fdiv((u32)e, dC)); }
+                    if (e + 1 < ne) { eb[v] = pr.ld(Ec, e + 1); rb[v] = pr.ld(Rc, fdiv((u32)(e + 1), dC)); }
+                }
+                pr.template bm2v<V>(uv, a.s_mul, ea, ra, eb, rb, za, zb);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    if (e < ne) pr.st(zt, e, pr.shr_(za[v], FRAC));
+                    if (e + 1 < ne) pr.st(zt, e + 1, pr.shr_(zb[v], FRAC));
+                }
+            }
         }
         __syncthreads();
     }
@@ -599,17 +652,26 @@ __global__ void __launch_bounds__(256, 3) k_ln(const __grid_constant__ PA pa, Ln
         tile_nr<1, WIDE>(pr, a.s_rs, a.rk, R, g0, Vc, RSo);
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;            // even: g0 is a multiple of 32
-        for (i64 base = (i64)warp * 32; base < (ne + 1) / 2; base += (i64)NW * 32) {
-            const i64 e = 2 * (base + lane);
-            const bool va = e < ne, vb = e + 1 < ne;
-            S ca = pr.zero(), cb = pr.zero(), ra = pr.zero(), rb = pr.zero();
-            if (va) { const i64 r = fdiv((u32)e, dC); ca = pr.sub(pr.ld(xt, e), pr.ld(MUc, r)); ra = pr.ld(RSc, r); }
-            if (vb) { const i64 r = fdiv((u32)(e + 1), dC); cb = pr.sub(pr.ld(xt, e + 1), pr.ld(MUc, r)); rb = pr.ld(RSc, r); }
-            S za, zb;
-            pr.bm2(ub + e, a.s_mul, ca, ra, cb, rb, za, zb);
-            const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
-            if (va) pr.st(zt, e, pr.shr_(za, FRAC));
-            if (vb) pr.st(zt, e + 1, pr.shr_(zb, FRAC));
+        const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
+        constexpr int V = decltype(pr)::kV;
+        for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
+            u64 uv[V];
+            S ca[V], cb[V], ra[V], rb[V], za[V], zb[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const i64 e = 2 * (base + lane + 32 * v);
+                uv[v] = ub + (u64)e;
+                ca[v] = cb[v] = ra[v] = rb[v] = pr.zero();
+                if (e < ne) { const i64 r = fdiv((u32)e, dC); ca[v] = pr.sub(pr.ld(xt, e), pr.ld(MUc, r)); ra[v] = pr.ld(RSc, r); }
+                if (e + 1 < ne) { const i64 r = fdiv((u32)(e + 1), dC); cb[v] = pr.sub(pr.ld(xt, e + 1), pr.ld(MUc, r)); rb[v] = pr.ld(RSc, r); }
+            }
+            pr.template bm2v<V>(uv, a.s_mul, ca, ra, cb, rb, za, zb);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const i64 e = 2 * (base + lane + 32 * v);
+                if (e < ne) pr.st(zt, e, pr.shr_(za[v], FRAC));
+                if (e + 1 < ne) pr.st(zt, e + 1, pr.shr_(zb[v], FRAC));
+            }
         }
         __syncthreads();
     }

@@ -34,10 +34,10 @@ __device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G]
 
 // ================================================================================ BOTH ====
 struct BothP {
-    const Keys* Kp;          // points into the kernel's parameter space (__grid_constant__):
-                             // round keys are read as constant-bank operands, no copies
+    const Keys* Kp;          // points into the kernel's parameter space (__grid_constant__)
     using S = Sh;
     static constexpr bool kPair = false;
+    static constexpr int kV = 1;   // unit pairs per lane per pass (registers hold both parties)
     __device__ __forceinline__ int party() const { return -1; }
     __device__ __forceinline__ S zero() const { return {0, 0}; }
     __device__ __forceinline__ S ld(SP a, i64 i) const { return {a.p[0][i], a.p[1][i]}; }
@@ -71,6 +71,18 @@ struct BothP {
     }
     __device__ __forceinline__ void sq2(u64 u, u32 s, S y0, S y1, S& z0, S& z1) { mpc::sq2(*Kp, u, s, y0, y1, z0, z1); }
     __device__ __forceinline__ u64 open(S x) const { return x.s0 + x.s1; }
+    template <int V>
+    __device__ __forceinline__ void bm2v(const u64 (&u)[V], u32 s, const S (&x0)[V], const S (&y0)[V],
+                                         const S (&x1)[V], const S (&y1)[V], S (&z0)[V], S (&z1)[V]) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) mpc::bm2(*Kp, u[v], s, x0[v], y0[v], x1[v], y1[v], z0[v], z1[v]);
+    }
+    template <int V>
+    __device__ __forceinline__ void sq2v(const u64 (&u)[V], u32 s, const S (&y0)[V], const S (&y1)[V],
+                                         S (&z0)[V], S (&z1)[V]) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) mpc::sq2(*Kp, u[v], s, y0[v], y1[v], z0[v], z1[v]);
+    }
 };
 
 __device__ __forceinline__ u64 floordiv_share(u64 a, i64 d)
@@ -131,6 +143,7 @@ __device__ __forceinline__ u64 globaltimer()
 }
 
 struct PairP {
+    static constexpr int kV = 1;   // unit pairs per lane per pass (V = 4 measured slower in loopback)
     const Keys* Kp;          // kernel parameter space (__grid_constant__)
     int pty;                 // 0 | 1
     // per-warp exchange state (set by bind())
@@ -273,6 +286,50 @@ struct PairP {
         exch(lane);
         z0 = sq_finish(a0, c0, (y0 - a0) + get(lane, 0));
         z1 = sq_finish(a1, c1, (y1 - a1) + get(lane, 1));
+    }
+
+    // V unit pairs in one exchange round (4V / 2V words per lane)
+    template <int V>
+    __device__ __forceinline__ void bm2v(const u64 (&u)[V], u32 s, const S (&x0)[V], const S (&y0)[V],
+                                         const S (&x1)[V], const S (&y1)[V], S (&z0)[V], S (&z1)[V]) {
+        static_assert(4 * V <= XW, "exchange width");
+        const int lane = threadIdx.x & 31;
+        u64 a0[V], b0[V], c0[V], a1[V], b1[V], c1[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const uint4 C = prg(Kp->k0, u[v] >> 1, s, 1);
+            triple(u[v], s, w64(C.x, C.y), a0[v], b0[v], c0[v]);
+            triple(u[v] + 1, s, w64(C.z, C.w), a1[v], b1[v], c1[v]);
+            put(lane, 4 * v + 0, x0[v] - a0[v]); put(lane, 4 * v + 1, y0[v] - b0[v]);
+            put(lane, 4 * v + 2, x1[v] - a1[v]); put(lane, 4 * v + 3, y1[v] - b1[v]);
+        }
+        exch(lane);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            z0[v] = bm_finish(a0[v], b0[v], c0[v], (x0[v] - a0[v]) + get(lane, 4 * v + 0), (y0[v] - b0[v]) + get(lane, 4 * v + 1));
+            z1[v] = bm_finish(a1[v], b1[v], c1[v], (x1[v] - a1[v]) + get(lane, 4 * v + 2), (y1[v] - b1[v]) + get(lane, 4 * v + 3));
+        }
+    }
+    template <int V>
+    __device__ __forceinline__ void sq2v(const u64 (&u)[V], u32 s, const S (&y0)[V], const S (&y1)[V],
+                                         S (&z0)[V], S (&z1)[V]) {
+        static_assert(2 * V <= XW, "exchange width");
+        const int lane = threadIdx.x & 31;
+        u64 a0[V], c0[V], a1[V], c1[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            u64 a1e = 0, a1o = 0;
+            if (pty == 1) { const uint4 A1 = prg(Kp->k1, u[v] >> 1, s, 3); a1e = w64(A1.x, A1.y); a1o = w64(A1.z, A1.w); }
+            sq_triple(u[v], s, a1e, a0[v], c0[v]);
+            sq_triple(u[v] + 1, s, a1o, a1[v], c1[v]);
+            put(lane, 2 * v, y0[v] - a0[v]); put(lane, 2 * v + 1, y1[v] - a1[v]);
+        }
+        exch(lane);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            z0[v] = sq_finish(a0[v], c0[v], (y0[v] - a0[v]) + get(lane, 2 * v));
+            z1[v] = sq_finish(a1[v], c1[v], (y1[v] - a1[v]) + get(lane, 2 * v + 1));
+        }
     }
 
     // ---- AND gates on XOR-shared plane words; up to 2 gates (4 words) per round ----

@@ -52,6 +52,85 @@ __device__ __forceinline__ void exp_pair(P& pr, u64 u, u32 s, const ExpK& p, typ
     }
 }
 
+// V pairs per lane (P::kV): the same schedule on V unit pairs, one exchange per step in PAIR.
+template <int V, class P>
+__device__ __forceinline__ void exp_pairv(P& pr, const u64 (&u)[V], u32 s, const ExpK& p,
+                                          typename P::S (&y0)[V], typename P::S (&y1)[V])
+{
+#pragma unroll
+    for (int v = 0; v < V; ++v) { y0[v] = pr.addp(pr.shr_(y0[v], p.t), p.e_one); y1[v] = pr.addp(pr.shr_(y1[v], p.t), p.e_one); }
+    for (int k = 0; k < p.t; ++k) {
+        typename P::S a[V], b[V];
+        if (p.sq) pr.template sq2v<V>(u, s + k, y0, y1, a, b);
+        else pr.template bm2v<V>(u, s + k, y0, y0, y1, y1, a, b);
+#pragma unroll
+        for (int v = 0; v < V; ++v) { y0[v] = pr.shr_(a[v], FRAC); y1[v] = pr.shr_(b[v], FRAC); }
+    }
+}
+
+template <int V, class P>
+__device__ __forceinline__ void recip_pairv(P& pr, const u64 (&u)[V], u32 s, const NrK& p, const typename P::S (&x0)[V],
+                                            const typename P::S (&x1)[V], typename P::S (&y0)[V], typename P::S (&y1)[V])
+{
+    using S = typename P::S;
+    S g0[V], g1[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) { g0[v] = pr.addp(pr.neg(x0[v]), p.e_half); g1[v] = pr.addp(pr.neg(x1[v]), p.e_half); }
+    exp_pairv<V>(pr, u, s, p.exp, g0, g1);
+    s += exp_steps(p.exp);
+#pragma unroll
+    for (int v = 0; v < V; ++v) { y0[v] = pr.addp(pr.muli(g0[v], 3ull), p.e_c003); y1[v] = pr.addp(pr.muli(g1[v], 3ull), p.e_c003); }
+    for (int it = 0; it < p.iters; ++it) {
+        S a[V], b[V], c[V], d[V];
+        pr.template bm2v<V>(u, s, x0, y0, x1, y1, a, b);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            a[v] = pr.addp(pr.neg(pr.shr_(a[v], FRAC)), p.e_two);
+            b[v] = pr.addp(pr.neg(pr.shr_(b[v], FRAC)), p.e_two);
+        }
+        pr.template bm2v<V>(u, s + 1, y0, a, y1, b, c, d);
+#pragma unroll
+        for (int v = 0; v < V; ++v) { y0[v] = pr.shr_(c[v], FRAC); y1[v] = pr.shr_(d[v], FRAC); }
+        s += 2;
+    }
+}
+
+template <int V, class P>
+__device__ __forceinline__ void rsqrt_pairv(P& pr, const u64 (&u)[V], u32 s, const NrK& p, const typename P::S (&x0)[V],
+                                            const typename P::S (&x1)[V], typename P::S (&y0)[V], typename P::S (&y1)[V])
+{
+    using S = typename P::S;
+    S g0[V], g1[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        g0[v] = pr.neg(pr.addp(pr.shr_(x0[v], 1), p.e_02));
+        g1[v] = pr.neg(pr.addp(pr.shr_(x1[v], 1), p.e_02));
+    }
+    exp_pairv<V>(pr, u, s, p.exp, g0, g1);
+    s += exp_steps(p.exp);
+#pragma unroll
+    for (int v = 0; v < V; ++v) { y0[v] = pr.addp(pr.mulf(g0[v], p.e_22), p.e_02); y1[v] = pr.addp(pr.mulf(g1[v], p.e_22), p.e_02); }
+    for (int it = 0; it < p.iters; ++it) {
+        S a[V], b[V], c[V], d[V];
+        pr.template bm2v<V>(u, s, y0, y0, y1, y1, a, b);
+#pragma unroll
+        for (int v = 0; v < V; ++v) { a[v] = pr.shr_(a[v], FRAC); b[v] = pr.shr_(b[v], FRAC); }
+        pr.template bm2v<V>(u, s + 1, x0, a, x1, b, c, d);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            c[v] = pr.addp(pr.neg(pr.shr_(c[v], FRAC)), p.e_three);
+            d[v] = pr.addp(pr.neg(pr.shr_(d[v], FRAC)), p.e_three);
+        }
+        pr.template bm2v<V>(u, s + 2, y0, c, y1, d, a, b);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            y0[v] = pr.mulf(pr.shr_(a[v], FRAC), p.e_half);
+            y1[v] = pr.mulf(pr.shr_(b[v], FRAC), p.e_half);
+        }
+        s += 3;
+    }
+}
+
 // ---- RECIP(x; iters, exp) -------------------------------------------
 template <bool WIDE, class P>
 __device__ __forceinline__ typename P::S recip_group(P& pr, u64 u, u64 q, u32 s, const NrK& p,
