@@ -96,7 +96,7 @@ __device__ __forceinline__ Sh BothP::divp(Sh a, i64 d) const { return {floordiv_
 
 // ================================================================================ PAIR ====
 constexpr int XW = 4;                // u64 words per lane per round (max)
-constexpr int XSLOT_RX = 2 * 32 * XW; // u64 per warp slot receive buffer (double-buffered)
+constexpr int XSLOT_RX = 2 * 32 * XW * 2; // u64 per warp slot: [parity][lane][word][payload-half + tag]
 
 // Device view of one party's exchange memory.
 struct XMem {
@@ -170,33 +170,35 @@ struct PairP {
     }
     __device__ __forceinline__ int party() const { return pty; }
     // ---- exchange: put words, exch(), get peer's words ----
-    __device__ __forceinline__ void put(int lane, int k, u64 v) { prx[(rnd & 1) * (32 * XW) + lane * XW + k] = v; }
-    // The warp barrier orders every lane's stores into the peer buffer before lane 0's
-    // release of the flag (release is cumulative); the peer's acquire of the flag then
-    // makes them visible.  System scope across GPUs, GPU scope in loopback.
-    __device__ __forceinline__ void exch(int lane) {
-        if (!local) asm volatile("fence.acq_rel.sys;" ::: "memory");   // belt and braces across GPUs
-        __syncwarp();
-        ++rnd;
-        if (lane == 0) {
-            if (local) st_release_gpu(pflag, rnd); else st_release_sys(pflag, rnd);
-            if (!dead) {
-                if ((local ? ld_acquire_gpu(flag) : ld_acquire_sys(flag)) < rnd) {
-                    const u64 t0 = globaltimer();
-                    unsigned ns = 32;
-                    while ((local ? ld_acquire_gpu(flag) : ld_acquire_sys(flag)) < rnd) {
-                        __nanosleep(ns);
-                        if (ns < 256) ns <<= 1;
-                        if (globaltimer() - t0 > kTimeoutNs) { atomicExch(err, 1); dead = 1; break; }
-                    }
-                }
-            }
-        }
-        dead = __shfl_sync(FULL, dead, 0);
-        __syncwarp();
+    // LL exchange (the NCCL "LL" idea): every 64-bit payload travels as two 8-byte words
+    // {payload half, round tag}, written with one 16-byte store into the peer's buffer at
+    // parity (round & 1).  Aligned 8-byte stores are single-copy atomic, so the receiver
+    // polls its own words until both tags equal the round: no fences, flags or warp
+    // barriers, and no L1 invalidation.  Both parties run the same put/get pattern.
+    __device__ __forceinline__ void put(int lane, int k, u64 v) {
+        const u64 tag = (rnd + 1) << 32;
+        u64* d = prx + (((rnd + 1) & 1) * (32 * XW) + lane * XW + k) * 2;
+        const u64 lo = (v & 0xffffffffull) | tag, hi = (v >> 32) | tag;
+        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" :: "l"(d), "l"(lo), "l"(hi) : "memory");
     }
-    __device__ __forceinline__ u64 get(int lane, int k) const {
-        return ld_volatile(rx + ((rnd - 1) & 1) * (32 * XW) + lane * XW + k);
+    __device__ __forceinline__ void exch(int lane) {
+        (void)lane;
+        ++rnd;                                   // the round now being received
+    }
+    __device__ __forceinline__ u64 get(int lane, int k) {
+        const u64* sp = rx + ((rnd & 1) * (32 * XW) + lane * XW + k) * 2;
+        const u64 want = rnd & 0xffffffffull;
+        u64 lo, hi;
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
+        if (((lo >> 32) != want || (hi >> 32) != want) && !dead) {
+            const u64 t0 = globaltimer();
+            unsigned spins = 0;
+            do {                                 // (a __nanosleep backoff here measured 2x slower)
+                asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
+                if ((++spins & 1023) == 0 && globaltimer() - t0 > kTimeoutNs) { atomicExch(err, 1); dead = 1; break; }
+            } while ((lo >> 32) != want || (hi >> 32) != want);
+        }
+        return (lo & 0xffffffffull) | (hi << 32);
     }
 
     // ---- local share ops (party 0 carries public addends) ----
