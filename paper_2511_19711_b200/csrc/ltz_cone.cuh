@@ -66,8 +66,11 @@ __device__ void ltz_cone_both(const Keys& K, u64 q0, u32 s, int w, const Sh (&x)
             const bool valid = t < G * nn;
             const int g = valid ? t >> (L - 1 - k) : 0, i = valid ? t & (nn - 1) : 0;
             const int lo = i << (k + 1), hi = lo + (1 << k);
-            const u32 gl0 = sm.w[g][lo][0], gl1 = sm.w[g][lo][1], pl0 = sm.w[g][lo][2], pl1 = sm.w[g][lo][3];
-            const u32 gh0 = sm.w[g][hi][0], gh1 = sm.w[g][hi][1], ph0 = sm.w[g][hi][2], ph1 = sm.w[g][hi][3];
+            u32 gl0 = 0, gl1 = 0, pl0 = 0, pl1 = 0, gh0 = 0, gh1 = 0, ph0 = 0, ph1 = 0;
+            if (valid) {
+                gl0 = sm.w[g][lo][0]; gl1 = sm.w[g][lo][1]; pl0 = sm.w[g][lo][2]; pl1 = sm.w[g][lo][3];
+                gh0 = sm.w[g][hi][0]; gh1 = sm.w[g][hi][1]; ph0 = sm.w[g][hi][2]; ph1 = sm.w[g][hi][3];
+            }
             const u64 q = q0 + (u64)g;
             const uint4 tg = prg(K.k0, q, s, ltz_slot(k + 1, i, 0));
             const uint4 tp = prg(K.k0, q, s, ltz_slot(k + 1, i, 1));
@@ -149,7 +152,8 @@ __device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G]
             const bool valid = t < G * nn;
             const int g = valid ? t >> (L - 1 - k) : 0, i = valid ? t & (nn - 1) : 0;
             const int lo = i << (k + 1), hi = lo + (1 << k);
-            const u32 gl = sm.w[g][lo][0], pl = sm.w[g][lo][2], gh = sm.w[g][hi][0], ph = sm.w[g][hi][2];
+            u32 gl = 0, pl = 0, gh = 0, ph = 0;         // idle lanes read nothing (no benign races)
+            if (valid) { gl = sm.w[g][lo][0]; pl = sm.w[g][lo][2]; gh = sm.w[g][hi][0]; ph = sm.w[g][hi][2]; }
             const u64 q = q0 + (u64)g;
             const uint4 tg = prg(K.k0, q, s, ltz_slot(k + 1, i, 0));
             const uint4 tp = prg(K.k0, q, s, ltz_slot(k + 1, i, 1));
