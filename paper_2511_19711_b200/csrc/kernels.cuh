@@ -8,6 +8,13 @@
 #include "sched.cuh"
 #include "ltz_cone.cuh"
 
+#ifndef MPC_SM_MINB
+#define MPC_SM_MINB 2      // resident CTAs/SM the row kernels are compiled for (<= 128 regs; 3 measured slower: spills)
+#endif
+#ifndef MPC_EW_MINB
+#define MPC_EW_MINB 2      // same for the element-wise drivers
+#endif
+
 namespace mpc {
 
 // ------------------------------------------------------------------ launch policies ----
@@ -40,7 +47,7 @@ struct PairA {
 // ------------------------------------------------------------------ drivers ----
 // GROUP driver: warp <-> 32-unit LTZ group, lane <-> unit.  off % 32 == 0.
 template <class PA, class Body>
-__global__ void __launch_bounds__(256, 3) k_groups(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
+__global__ void __launch_bounds__(256, MPC_EW_MINB) k_groups(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
@@ -56,7 +63,7 @@ __global__ void __launch_bounds__(256, 3) k_groups(const __grid_constant__ PA pa
 // PAIR driver: lane <-> V = P::kV global unit pairs (2P, 2P+1) per pass (pairs base + lane + 32v),
 // covering [off, off+n); warp-uniform loop.
 template <class PA, class Body>
-__global__ void __launch_bounds__(256, 3) k_pairs(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
+__global__ void __launch_bounds__(256, MPC_EW_MINB) k_pairs(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
@@ -82,7 +89,7 @@ __global__ void __launch_bounds__(256, 3) k_pairs(const __grid_constant__ PA pa,
 // CONE driver: warp <-> CG consecutive 32-unit groups; shared memory for the carry trees.
 constexpr int CG = 4;
 template <class PA, class Body>
-__global__ void __launch_bounds__(256, 3) k_groups_cone(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
+__global__ void __launch_bounds__(256, MPC_EW_MINB) k_groups_cone(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
     __shared__ ConeSmem<CG> sm[8];
     extern __shared__ __align__(16) u64 stash[];       // per-warp staging (Body::kStash u64)
@@ -461,7 +468,7 @@ __host__ __device__ inline i64 softmax_work_u64(i64 cols)
 }
 
 template <bool WIDE, class PA>
-__global__ void __launch_bounds__(256, 3) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
+__global__ void __launch_bounds__(256, MPC_SM_MINB) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
     __shared__ ConeSmem<CG> cone_sm[8];
