@@ -11,6 +11,9 @@
 #ifndef MPC_SM_MINB
 #define MPC_SM_MINB 2      // resident CTAs/SM the row kernels are compiled for (<= 128 regs; 3 measured slower: spills)
 #endif
+#ifndef MPC_ROW_TPB
+#define MPC_ROW_TPB 256    // threads per CTA of the row kernels (softmax / max / layernorm)
+#endif
 #ifndef MPC_EW_MINB
 #define MPC_EW_MINB 2      // same for the element-wise drivers
 #endif
@@ -468,10 +471,10 @@ __host__ __device__ inline i64 softmax_work_u64(i64 cols)
 }
 
 template <bool WIDE, class PA>
-__global__ void __launch_bounds__(256, MPC_SM_MINB) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
-    __shared__ ConeSmem<CG> cone_sm[8];
+    __shared__ ConeSmem<CG> cone_sm[MPC_ROW_TPB / 32];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     using S = typename decltype(pr)::S;
@@ -583,10 +586,10 @@ __host__ __device__ inline i64 max_work_u64(i64 cols)
 }
 
 template <bool WIDE, class PA>
-__global__ void __launch_bounds__(256, 3) k_max(const __grid_constant__ PA pa, MaxArgs a)
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_max(const __grid_constant__ PA pa, MaxArgs a)
 {
     extern __shared__ __align__(16) u64 smem[];
-    __shared__ ConeSmem<CG> cone_sm[8];
+    __shared__ ConeSmem<CG> cone_sm[MPC_ROW_TPB / 32];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
@@ -614,7 +617,7 @@ struct LnArgs {
 
 // LAYERNORM: mu, c = x - mu, v = mean(MT(c,c)) + eps, r = RSQRT(v), out = MT(c, r)
 template <bool WIDE, class PA>
-__global__ void __launch_bounds__(256, 3) k_ln(const __grid_constant__ PA pa, LnArgs a)
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln(const __grid_constant__ PA pa, LnArgs a)
 {
     __shared__ u64 MU[2][32], V[2][32], RS[2][32];
     int cta, ncta;

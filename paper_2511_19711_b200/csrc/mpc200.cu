@@ -272,25 +272,34 @@ static PairA pair_args(const mpc_ctx* c, int G)
 
 // CTAs per party for a PAIR launch: every CTA of both parties must be co-resident
 template <class Kern>
-static int pair_ctas(mpc_ctx* c, Kern kern, size_t dyn, i64 want)
+static int pair_ctas(mpc_ctx* c, Kern kern, size_t dyn, i64 want, int tpb = TPB)
 {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPB, dyn) != cudaSuccess || nb < 1) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, tpb, dyn) != cudaSuccess || nb < 1) nb = 1;
     i64 cap = (i64)nb * c->sm_count / (is_loop(c) ? 2 : 1);
-    cap = std::min<i64>(cap, c->slots / NWARPS);
+    cap = std::min<i64>(cap, c->slots / (tpb / 32));
     i64 G = std::min<i64>(want, cap);
     return (int)std::max<i64>(G, 1);
 }
 
 template <class Kern, class... Args>
+static mpc_status launch_pair_kernel_tpb(mpc_ctx* c, Kern kern, int G, size_t dyn, int tpb, const char* name, Args... args);
+
+template <class Kern, class... Args>
 static mpc_status launch_pair_kernel(mpc_ctx* c, Kern kern, int G, size_t dyn, const char* name, Args... args)
+{
+    return launch_pair_kernel_tpb(c, kern, G, dyn, TPB, name, args...);
+}
+
+template <class Kern, class... Args>
+static mpc_status launch_pair_kernel_tpb(mpc_ctx* c, Kern kern, int G, size_t dyn, int tpb, const char* name, Args... args)
 {
     if (!is_loop(c) && !c->connected) return fail(c, MPC_ERR_INVALID, "%s: PAIR context not connected", name);
     PairA pa = pair_args(c, G);
     void* argv[] = {(void*)&pa, (void*)&args...};
     const int grid = G * (is_loop(c) ? 2 : 1);
     rec_begin(c, name, 0);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, grid, TPB, argv, dyn, c->stream);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, grid, tpb, argv, dyn, c->stream);
     rec_end(c);
     c->st.launches++;
     if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: cooperative launch: %s", name, cudaGetErrorString(e));
@@ -298,10 +307,10 @@ static mpc_status launch_pair_kernel(mpc_ctx* c, Kern kern, int G, size_t dyn, c
 }
 
 template <class K>
-static int occupancy(K kern, size_t dyn = 0)
+static int occupancy(K kern, size_t dyn = 0, int tpb = TPB)
 {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, TPB, dyn) != cudaSuccess || nb < 1) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, tpb, dyn) != cudaSuccess || nb < 1) nb = 1;
     return nb;
 }
 
@@ -375,8 +384,8 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
         cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes);
     }
     int grid;
-    if (!is_pair(c)) grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(kb, dyn));
-    else grid = pair_ctas(c, kp, dyn, ntiles);
+    if (!is_pair(c)) grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(kb, dyn, MPC_ROW_TPB));
+    else grid = pair_ctas(c, kp, dyn, ntiles, MPC_ROW_TPB);
     const int launched = grid * (is_loop(c) ? 2 : 1);
     a.use_smem = smem ? 1 : 0;
     a.gscratch = nullptr;
@@ -391,9 +400,9 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
     }
     a.escratch = base;
     if (!smem && work_u64 > 0) a.gscratch = base + (size_t)esc_u64 * (size_t)launched;
-    if (is_pair(c)) return launch_pair_kernel(c, kp, grid, dyn, name, a);
+    if (is_pair(c)) return launch_pair_kernel_tpb(c, kp, grid, dyn, MPC_ROW_TPB, name, a);
     rec_begin(c, name, (u64)rows);
-    kb<<<grid, TPB, dyn, c->stream>>>(BothA{c->K}, a);
+    kb<<<grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, a);
     rec_end(c);
     c->st.launches++;
     return cuda_check(c, name);
@@ -1013,17 +1022,17 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
         const i64 ntiles = (rows + 31) / 32;
         const bool wide = p->rsqrt.exp.window > 33;
         if (!is_pair(c)) {
-            const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(wide ? k_ln<true, BothA> : k_ln<false, BothA>));
+            const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(wide ? k_ln<true, BothA> : k_ln<false, BothA>, 0, MPC_ROW_TPB));
             rec_begin(c, "layernorm", (u64)rows);
-            if (wide) k_ln<true, BothA><<<grid, TPB, 0, c->stream>>>(BothA{c->K}, a);
-            else k_ln<false, BothA><<<grid, TPB, 0, c->stream>>>(BothA{c->K}, a);
+            if (wide) k_ln<true, BothA><<<grid, MPC_ROW_TPB, 0, c->stream>>>(BothA{c->K}, a);
+            else k_ln<false, BothA><<<grid, MPC_ROW_TPB, 0, c->stream>>>(BothA{c->K}, a);
             rec_end(c);
             c->st.launches++;
             st = cuda_check(c, "layernorm");
         } else if (wide) {
-            st = launch_pair_kernel(c, k_ln<true, PairA>, pair_ctas(c, k_ln<true, PairA>, 0, ntiles), 0, "layernorm", a);
+            st = launch_pair_kernel_tpb(c, k_ln<true, PairA>, pair_ctas(c, k_ln<true, PairA>, 0, ntiles, MPC_ROW_TPB), 0, MPC_ROW_TPB, "layernorm", a);
         } else {
-            st = launch_pair_kernel(c, k_ln<false, PairA>, pair_ctas(c, k_ln<false, PairA>, 0, ntiles), 0, "layernorm", a);
+            st = launch_pair_kernel_tpb(c, k_ln<false, PairA>, pair_ctas(c, k_ln<false, PairA>, 0, ntiles, MPC_ROW_TPB), 0, MPC_ROW_TPB, "layernorm", a);
         }
         if (st) return st;
         const i64 n = rows * cols;
