@@ -348,11 +348,12 @@ struct PairP {
     // w <= 33, branch-free, daBit words in the idle slots of the last level (as ltz_narrow)
     __device__ __forceinline__ S ltz_narrow(u64 q, u32 s, int w, S x, int lane) {
         const int m = w - 1;
+        const PrgQ Q0 = prg_q(Kp->k0, q, s), Q1 = prg_q(Kp->k1, q, s);
         u32 Pp = transpose32((u32)x, lane), Gp = 0;
         {
-            const uint4 t0 = prg(Kp->k0, q, s, ltz_slot(0, lane, 0));
+            const uint4 t0 = prg(Q0, ltz_slot(0, lane, 0));
             uint4 t1 = make_uint4(0, 0, 0, 0);
-            if (pty == 1) t1 = prg(Kp->k1, q, s, ltz_slot(0, lane, 0));
+            if (pty == 1) t1 = prg(Q1, ltz_slot(0, lane, 0));
             u32 ta, tb, tc;
             and_triple(t0, t1, 0, ta, tb, tc);
             const u32 dd = (pty == 0 ? Pp : 0u) ^ ta, ee = (pty == 0 ? 0u : Pp) ^ tb;
@@ -372,10 +373,10 @@ struct PairP {
             const u32 g = __shfl_sync(FULL, Gp, src), p = __shfl_sync(FULL, Pp, src);
             const bool act = lane >= dl && lane < m;
             const bool dab = trick && k == L - 1 && lane < 16;
-            const uint4 tg = prg(Kp->k0, q, s, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0));
-            const uint4 tp = prg(Kp->k0, q, s, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1));
+            const uint4 tg = prg(Q0, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0));
+            const uint4 tp = prg(Q0, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1));
             uint4 t1 = make_uint4(0, 0, 0, 0);
-            if (pty == 1) t1 = prg(Kp->k1, q, s, dab ? 1u : ltz_slot(k + 1, lane, 0));
+            if (pty == 1) t1 = prg(Q1, dab ? 1u : ltz_slot(k + 1, lane, 0));
             u32 ga, gb, gc, pa, pb, pc;
             and_triple(tg, t1, 0, ga, gb, gc);
             and_triple(tp, t1, 1, pa, pb, pc);
@@ -400,8 +401,8 @@ struct PairP {
             D0 = lane < 16 ? Dlo : make_uint4(hx, hy, hz, 0u);
             d1x = __shfl_sync(FULL, k1w, 0);
         } else {
-            D0 = prg(Kp->k0, q, s, 2u + (u32)lane);
-            if (pty == 1) d1x = prg(Kp->k1, q, s, 1u).x;
+            D0 = prg(Q0, 2u + (u32)lane);
+            if (pty == 1) d1x = prg(Q1, 1u).x;
         }
         const u64 r0A = w64(D0.x, D0.y);
         const u32 r0B = D0.z & 1u;
@@ -421,6 +422,7 @@ struct PairP {
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) {
         if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(q, s, w, x, lane);
         const int m = w - 1;
+        const PrgQ Q0 = prg_q(Kp->k0, q, s), Q1 = prg_q(Kp->k1, q, s);
         constexpr int H = WIDE ? 2 : 1;
         u32 Pp[2], Gp[2];                                  // this party's shares of P_j, G_j
         Pp[0] = transpose32((u32)x, lane);
@@ -433,9 +435,9 @@ struct PairP {
                 const int j = lane + 32 * h;
                 ta[h] = tb[h] = tc[h] = 0;
                 if (j < m) {
-                    const uint4 t0 = prg(Kp->k0, q, s, ltz_slot(0, j, 0));
+                    const uint4 t0 = prg(Q0, ltz_slot(0, j, 0));
                     uint4 t1 = make_uint4(0, 0, 0, 0);
-                    if (pty == 1) t1 = prg(Kp->k1, q, s, ltz_slot(0, j, 0));
+                    if (pty == 1) t1 = prg(Q1, ltz_slot(0, j, 0));
                     and_triple(t0, t1, 0, ta[h], tb[h], tc[h]);
                 }
                 const u32 xin = pty == 0 ? Pp[h] : 0u, yin = pty == 0 ? 0u : Pp[h];
@@ -470,10 +472,10 @@ struct PairP {
                 if (WIDE && dl == 32) { g = Gp[0]; p = Pp[0]; }
                 ga[h] = gb[h] = gc[h] = pa[h] = pb[h] = pc[h] = 0;
                 if (act[h]) {
-                    const uint4 tg = prg(Kp->k0, q, s, ltz_slot(k + 1, j, 0));
-                    const uint4 tp = prg(Kp->k0, q, s, ltz_slot(k + 1, j, 1));
+                    const uint4 tg = prg(Q0, ltz_slot(k + 1, j, 0));
+                    const uint4 tp = prg(Q0, ltz_slot(k + 1, j, 1));
                     uint4 t1 = make_uint4(0, 0, 0, 0);
-                    if (pty == 1) t1 = prg(Kp->k1, q, s, ltz_slot(k + 1, j, 0));
+                    if (pty == 1) t1 = prg(Q1, ltz_slot(k + 1, j, 0));
                     and_triple(tg, t1, 0, ga[h], gb[h], gc[h]);
                     and_triple(tp, t1, 1, pa[h], pb[h], pc[h]);
                 }
@@ -504,14 +506,14 @@ struct PairP {
             bp = (u32)((x >> (w - 1)) & 1ull) ^ ((gm >> lane) & 1u);
         }
         // daBit + B2A: party 0 holds (r0A, r0B); party 1 (r1A, r1B), r1A = (r0B ^ r1B) - r0A
-        const uint4 D0 = prg(Kp->k0, q, s, 2u + (u32)lane);
+        const uint4 D0 = prg(Q0, 2u + (u32)lane);
         const u64 r0A = w64(D0.x, D0.y);
         const u32 r0B = D0.z & 1u;
         u64 rA;
         u32 rB;
         if (pty == 0) { rA = r0A; rB = r0B; }
         else {
-            const uint4 D1 = prg(Kp->k1, q, s, 1u);
+            const uint4 D1 = prg(Q1, 1u);
             rB = (D1.x >> lane) & 1u;
             rA = (u64)(r0B ^ rB) - r0A;
         }

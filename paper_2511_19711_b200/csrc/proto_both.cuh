@@ -100,10 +100,11 @@ __device__ __forceinline__ void and_both(u32 x0, u32 x1, u32 y0, u32 y1,
 __device__ __forceinline__ Sh ltz_narrow(const Keys& K, u64 q, u32 s, int w, Sh x, int lane)
 {
     const int m = w - 1;
+    const PrgQ Q0 = prg_q(K.k0, q, s), Q1 = prg_q(K.k1, q, s);
     u32 P0 = transpose32((u32)x.s0, lane), P1 = transpose32((u32)x.s1, lane), G0 = 0, G1 = 0;
     {   // g-layer: g_j = AND((x0_j, 0), (0, x1_j))
-        const uint4 t0 = prg(K.k0, q, s, ltz_slot(0, lane, 0));
-        const uint4 t1 = prg(K.k1, q, s, ltz_slot(0, lane, 0));
+        const uint4 t0 = prg(Q0, ltz_slot(0, lane, 0));
+        const uint4 t1 = prg(Q1, ltz_slot(0, lane, 0));
         u32 g0, g1;
         and_both(P0, 0u, 0u, P1, t0.x, t0.y, t0.z, t1.x, t1.y, g0, g1);
         if (lane < m) { G0 = g0; G1 = g1; }
@@ -119,9 +120,9 @@ __device__ __forceinline__ Sh ltz_narrow(const Keys& K, u64 q, u32 s, int w, Sh 
         const u32 p0 = __shfl_sync(FULL, P0, src), p1 = __shfl_sync(FULL, P1, src);
         const bool act = lane >= d && lane < m;
         const bool dab = trick && k == L - 1 && lane < 16;
-        const uint4 tg = prg(K.k0, q, s, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0));
-        const uint4 tp = prg(K.k0, q, s, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1));
-        const uint4 t1 = prg(K.k1, q, s, dab ? 1u : ltz_slot(k + 1, lane, 0));
+        const uint4 tg = prg(Q0, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0));
+        const uint4 tp = prg(Q0, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1));
+        const uint4 t1 = prg(Q1, dab ? 1u : ltz_slot(k + 1, lane, 0));
         u32 ng0, ng1, np0, np1;
         and_both(P0, P1, g0, g1, tg.x, tg.y, tg.z, t1.x, t1.y, ng0, ng1);
         and_both(P0, P1, p0, p1, tp.x, tp.y, tp.z, t1.z, t1.w, np0, np1);
@@ -144,8 +145,8 @@ __device__ __forceinline__ Sh ltz_narrow(const Keys& K, u64 q, u32 s, int w, Sh 
         D0 = lane < 16 ? Dlo : make_uint4(hx, hy, hz, 0u);
         d1x = __shfl_sync(FULL, k1w, 0);
     } else {
-        D0 = prg(K.k0, q, s, 2u + (u32)lane);
-        d1x = prg(K.k1, q, s, 1u).x;
+        D0 = prg(Q0, 2u + (u32)lane);
+        d1x = prg(Q1, 1u).x;
     }
     const u64 r0A = w64(D0.x, D0.y);
     const u32 r0B = D0.z & 1u;
@@ -167,6 +168,7 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
 #endif
     if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(K, q, s, w, x, lane);
     const int m = w - 1;
+    const PrgQ Q0 = prg_q(K.k0, q, s), Q1 = prg_q(K.k1, q, s);
     // A2B (local): lane j receives plane j of both parties' shares.
     u32 P0[2], P1[2], G0[2], G1[2];
     P0[0] = transpose32((u32)x.s0, lane);
@@ -182,8 +184,8 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
         const int j = lane + 32 * h;
         G0[h] = 0; G1[h] = 0;
         if (j < m) {
-            const uint4 t0 = prg(K.k0, q, s, ltz_slot(0, j, 0));
-            const uint4 t1 = prg(K.k1, q, s, ltz_slot(0, j, 0));
+            const uint4 t0 = prg(Q0, ltz_slot(0, j, 0));
+            const uint4 t1 = prg(Q1, ltz_slot(0, j, 0));
             and_both(P0[h], 0u, 0u, P1[h], t0.x, t0.y, t0.z, t1.x, t1.y, G0[h], G1[h]);
         }
     }
@@ -211,9 +213,9 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
                 u32 g0 = sG0[0], g1 = sG1[0], p0 = sP0[0], p1 = sP1[0];
                 if (WIDE && hs == 1) { g0 = sG0[1]; g1 = sG1[1]; p0 = sP0[1]; p1 = sP1[1]; }
                 if (WIDE && d == 32) { g0 = G0[0]; g1 = G1[0]; p0 = P0[0]; p1 = P1[0]; }
-                const uint4 tg = prg(K.k0, q, s, ltz_slot(k + 1, j, 0));
-                const uint4 tp = prg(K.k0, q, s, ltz_slot(k + 1, j, 1));
-                const uint4 t1 = prg(K.k1, q, s, ltz_slot(k + 1, j, 0));
+                const uint4 tg = prg(Q0, ltz_slot(k + 1, j, 0));
+                const uint4 tp = prg(Q0, ltz_slot(k + 1, j, 1));
+                const uint4 t1 = prg(Q1, ltz_slot(k + 1, j, 0));
                 u32 ng0, ng1, np0, np1;
                 and_both(P0[h], P1[h], g0, g1, tg.x, tg.y, tg.z, t1.x, t1.y, ng0, ng1);
                 and_both(P0[h], P1[h], p0, p1, tp.x, tp.y, tp.z, t1.z, t1.w, np0, np1);
@@ -236,8 +238,8 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
         b1 = (u32)((x.s1 >> (w - 1)) & 1ull) ^ ((gm1 >> lane) & 1u);
     }
     // daBit + B2A: c = open(b ^ r); z0 = c + (1-2c) r0A; z1 = (1-2c) r1A
-    const uint4 D0 = prg(K.k0, q, s, 2u + (u32)lane);
-    const uint4 D1 = prg(K.k1, q, s, 1u);
+    const uint4 D0 = prg(Q0, 2u + (u32)lane);
+    const uint4 D1 = prg(Q1, 1u);
     const u64 r0A = w64(D0.x, D0.y);
     const u32 r0B = D0.z & 1u;
     const u32 r1B = (D1.x >> lane) & 1u;
