@@ -496,12 +496,17 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_softmax(const __gr
         const u64 g0 = a.row_off + (u64)r0;                       // global row of the tile
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
         // 1. m = MAX_row(x)
+#ifndef MPC_SOFTMAX_SKIP
+#define MPC_SOFTMAX_SKIP 0   // profiling only: bitmask of phases to skip (1 max, 2 exp, 4 recip, 8 mul)
+#endif
+        if (!(MPC_SOFTMAX_SKIP & 1))
         tile_max<WIDE>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, HA, HB, MX, a.cone ? cone_sm : nullptr);
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;
         const SP MXc{{MX.p[0], MX.p[1]}};
-        if (a.ek.clamp) {
+        if (MPC_SOFTMAX_SKIP & 2) {
+        } else if (a.ek.clamp) {
             for (i64 g = warp; g < (ne + 31) / 32; g += NW) {
                 const i64 e = g * 32 + lane;
                 const bool valid = e < ne;
@@ -543,11 +548,11 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_softmax(const __gr
         }
         __syncthreads();
         // 5. r = RECIP(S), row units
-        tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR);
+        if (!(MPC_SOFTMAX_SKIP & 4)) tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR);
         // 6. out = MT(e, r), element units
         const SP Rc{{RR.p[0], RR.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
-        {
+        if (!(MPC_SOFTMAX_SKIP & 8)) {
             constexpr int V = decltype(pr)::kV;
             for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
                 u64 uv[V];

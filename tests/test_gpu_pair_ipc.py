@@ -1,0 +1,19 @@
+"""MPC_MODE_PAIR across two processes: party 0 and party 1 in separate processes
+exchange every opening through cudaIpc-mapped peer memory -- the remote path bench.py takes for
+N > 1 -- and every op's output shares equal MPC_MODE_BOTH's bit for bit (tools/pair_ipc_check.py;
+on a one-GPU box both processes share cuda:0)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_pair_two_processes_bit_identical_to_both():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_ipc_check.py")],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0 and "PAIR_IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

@@ -81,6 +81,41 @@ __device__ __forceinline__ uint4 philox(Key key, uint32_t c0, uint32_t c1, uint3
     return make_uint4(c0, c1, c2, c3);
 }
 
+// same rounds with the 64-bit product split into IMAD.HI + IMAD (lo) -- tests whether the
+// low half can leave the fmaheavy pipe
+__device__ __forceinline__ uint4 philox_split(Key key, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3)
+{
+    uint32_t k0 = key.lo, k1 = key.hi;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        uint32_t h0, l0, h1, l1;
+        asm volatile("mul.hi.u32 %0, %1, 0xD2511F53;" : "=r"(h0) : "r"(c0));
+        asm volatile("mad.lo.u32 %0, %1, 0xD2511F52, %1;" : "=r"(l0) : "r"(c0));
+        asm volatile("mul.hi.u32 %0, %1, 0xCD9E8D57;" : "=r"(h1) : "r"(c2));
+        asm volatile("mad.lo.u32 %0, %1, 0xCD9E8D56, %1;" : "=r"(l1) : "r"(c2));
+        const uint32_t n0 = h1 ^ c1 ^ k0;
+        const uint32_t n2 = h0 ^ c3 ^ k1;
+        c1 = l1; c3 = l0; c0 = n0; c2 = n2;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    return make_uint4(c0, c1, c2, c3);
+}
+
+template <int ILP>
+__global__ void k_philox_split(uint32_t* out, Key key, int reps)
+{
+    uint32_t acc = 0;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int j = 0; j < ILP; ++j) {
+            const uint4 v = philox_split(key, t, (uint32_t)r, (uint32_t)j, 7u);
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    }
+    out[t] = acc;
+}
+
 template <int ILP>
 __global__ void k_philox(uint32_t* out, Key key, int reps)
 {
@@ -146,6 +181,16 @@ int main()
         printf(", \"philox_ilp1_512thr_per_sm_gblk_s\": %.1f", n * reps / (ms * 1e-3) / 1e9);
         ms = timeit([&] { k_philox<4><<<nb, tpb>>>(out, Key{1, 2}, reps / 4); });
         printf(", \"philox_ilp4_512thr_per_sm_gblk_s\": %.1f", n * reps / (ms * 1e-3) / 1e9);
+    }
+    for (int tpb : {256, 512}) {
+        const int nb = sms * (2048 / tpb);
+        const double n = (double)nb * tpb;
+        ms = timeit([&] { k_philox_split<2><<<nb, tpb>>>(out, Key{1, 2}, reps / 2); });
+        printf(", \"philox_split_ilp2_%dthr_gblk_s\": %.1f", tpb * (2048 / tpb), n * reps / (ms * 1e-3) / 1e9);
+        ms = timeit([&] { k_philox_split<4><<<nb, tpb>>>(out, Key{1, 2}, reps / 4); });
+        printf(", \"philox_split_ilp4_%dthr_gblk_s\": %.1f", tpb * (2048 / tpb), n * reps / (ms * 1e-3) / 1e9);
+        ms = timeit([&] { k_philox<4><<<nb, tpb>>>(out, Key{1, 2}, reps / 4); });
+        printf(", \"philox_ilp4_%dthr_gblk_s\": %.1f", tpb * (2048 / tpb), n * reps / (ms * 1e-3) / 1e9);
     }
     printf("}\n");
     return 0;

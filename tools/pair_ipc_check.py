@@ -1,0 +1,89 @@
+"""Two-process MPC_MODE_PAIR check: ranks 0 and 1 are party 0 and party 1 in
+separate processes, each with its own mpc_ctx, exchanging every opening through the other
+process's cudaIpc-mapped exchange memory -- the remote code path bench.py runs for N > 1.
+With one GPU both processes share cuda:0 (the driver time-slices their contexts, so every
+exchange round costs a context switch: correctness only, tiny shapes); with two or more GPUs
+rank r uses cuda:r.  Each op's output shares are gathered on rank 0 and compared bit for bit
+with MPC_MODE_BOTH on the same seeds and step ids.
+
+  python tools/pair_ipc_check.py          (prints PAIR_IPC_OK on success, exit code 0)"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+import workloads  # noqa: E402
+
+
+def ops(c, x, party, n_rows, n_cols):
+    """The op sequence both modes run; returns the list of this party's output shares."""
+    out = []
+    xs = x if x is not None else None
+    if c.mode == 1 and party == 1:
+        s = c.share(None, owner=0, n=n_rows * n_cols)
+    else:
+        s = c.share(xs, owner=0)
+    out.append(s)
+    out.append(c.mul(s, s, trunc_bits=16))
+    out.append(c.relu(s))
+    out.append(c.gelu(s, form="poly_abs", degree=4))
+    out.append(c.softmax(s, n_rows, n_cols))
+    out.append(c.layernorm(s, n_rows, n_cols))
+    c.set_ltz_circuit(1)
+    out.append(c.relu(s))
+    out.append(c.softmax(s, n_rows, n_cols, exp_square=1, recip_square=1))
+    c.set_ltz_circuit(0)
+    return out
+
+
+def worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2511_19711_b200 as m
+    from paper_2511_19711_b200 import pair
+    ngpu = torch.cuda.device_count()
+    dev = rank % ngpu
+    torch.cuda.set_device(dev)
+    rows, cols = 32, 64
+    x = torch.from_numpy(workloads.softmax_inputs(rows, cols).ravel()).cuda(dev)
+    keys = workloads.keys(2)
+    c = m.Ctx.for_cfg(keys, device=dev, mode=m.binding.MODE_PAIR, party=rank)
+    pair.connect(c)
+    res = ops(c, x if rank == 0 else None, rank, rows, cols)
+    c.sync()
+    mine = [r[rank].cpu().numpy() for r in res]
+    gathered = [None, None]
+    dist.all_gather_object(gathered, mine)
+    if rank == 0:
+        b = m.Ctx.for_cfg(keys, device=dev)
+        ref = ops(b, x, 0, rows, cols)
+        torch.cuda.synchronize()
+        bad = []
+        for k, r in enumerate(ref):
+            for p in (0, 1):
+                if not np.array_equal(gathered[p][k], r[p].cpu().numpy()):
+                    bad.append((k, p))
+        q.put(bad)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def main():
+    port = 29600 + (os.getpid() % 1000)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(worker, args=(2, port, q), nprocs=2, join=True, start_method="spawn")
+    bad = q.get(timeout=5)
+    if bad:
+        print("PAIR_IPC_MISMATCH", bad)
+        sys.exit(1)
+    print(f"PAIR_IPC_OK ({torch.cuda.device_count()} GPU(s))")
+
+
+if __name__ == "__main__":
+    main()
