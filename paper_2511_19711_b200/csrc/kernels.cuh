@@ -11,6 +11,9 @@
 #ifndef MPC_SM_MINB
 #define MPC_SM_MINB 2      // resident CTAs/SM the row kernels are compiled for (<= 128 regs; 3 measured slower: spills)
 #endif
+#ifndef MPC_SM_MINB_KS
+#define MPC_SM_MINB_KS 2   // same for the Kogge-Stone (LV 0) row kernels
+#endif
 #ifndef MPC_ROW_TPB
 #define MPC_ROW_TPB 256    // threads per CTA of the row kernels (softmax / max / layernorm)
 #endif
@@ -345,7 +348,7 @@ struct OpenBody {
 // the last level writes mx[rr].  Steps s + 2*lv (LTZ), s + 2*lv + 1 (mux BM).
 // A holds levels 0, 2, 4.. (stride HA = ceil(cols/2)), B levels 1, 3, .. (stride HB = ceil(HA/2)).
 // cone: the level's LTZs use the carry-cone circuit, CG groups per warp (ltz_cone.cuh).
-template <bool WIDE, class P>
+template <bool WIDE, bool CONE, class P>
 __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i64 cols, int R, u64 g0,
                                          SO A, SO B, i64 HA, i64 HB, SO mx, ConeSmem<CG>* cone)
 {
@@ -364,7 +367,7 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
         const u32 sl = s + 2u * (u32)lv;
         const u64 ubase = g0 * (u64)h;                 // multiple of 32 (g0 is)
         const FastDiv dh = make_fastdiv((u32)h);
-        if (!WIDE && cone) {
+        if constexpr (!WIDE && CONE) {
             const i64 nb = (h + CG - 1) / CG;
             for (i64 b = warp; b < nb; b += NW) {
                 S d[CG], l[CG];
@@ -470,11 +473,14 @@ __host__ __device__ inline i64 softmax_work_u64(i64 cols)
     return 64 * HA + 64 * HB + 6 * 32;
 }
 
-template <bool WIDE, class PA>
-__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
+// LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33) --
+// separate instantiations so the cone's registers / shared memory do not cost the others occupancy
+template <int LV, class PA>
+__global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM_MINB) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
 {
+    constexpr bool WIDE = LV == 1, CONE = LV == 2;
     extern __shared__ __align__(16) u64 smem[];
-    __shared__ ConeSmem<CG> cone_sm[MPC_ROW_TPB / 32];
+    __shared__ ConeSmem<CG> cone_sm[CONE ? MPC_ROW_TPB / 32 : 1];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     using S = typename decltype(pr)::S;
@@ -500,7 +506,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_softmax(const __gr
 #define MPC_SOFTMAX_SKIP 0   // profiling only: bitmask of phases to skip (1 max, 2 exp, 4 recip, 8 mul)
 #endif
         if (!(MPC_SOFTMAX_SKIP & 1))
-        tile_max<WIDE>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, HA, HB, MX, a.cone ? cone_sm : nullptr);
+        tile_max<WIDE, CONE>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, HA, HB, MX, cone_sm);
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;
@@ -590,11 +596,12 @@ __host__ __device__ inline i64 max_work_u64(i64 cols)
     return 64 * HA + 64 * HB + 2 * 32;
 }
 
-template <bool WIDE, class PA>
-__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_max(const __grid_constant__ PA pa, MaxArgs a)
+template <int LV, class PA>   // LV as k_softmax
+__global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM_MINB) k_max(const __grid_constant__ PA pa, MaxArgs a)
 {
+    constexpr bool WIDE = LV == 1, CONE = LV == 2;
     extern __shared__ __align__(16) u64 smem[];
-    __shared__ ConeSmem<CG> cone_sm[MPC_ROW_TPB / 32];
+    __shared__ ConeSmem<CG> cone_sm[CONE ? MPC_ROW_TPB / 32 : 1];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
@@ -606,7 +613,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_max(const __grid_c
         const i64 r0 = tile * 32;
         const int R = (int)min((i64)32, a.rows - r0);
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
-        tile_max<WIDE>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, HA, HB, MX, a.cone ? cone_sm : nullptr);
+        tile_max<WIDE, CONE>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, HA, HB, MX, cone_sm);
         const SP MXc{{MX.p[0], MX.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 : nullptr, a.z.p[1] ? a.z.p[1] + r0 : nullptr}};
         for (int rr = threadIdx.x; rr < R; rr += blockDim.x) pr.st(zt, rr, pr.ld(MXc, rr));

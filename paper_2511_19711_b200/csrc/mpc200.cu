@@ -408,6 +408,14 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
     return cuda_check(c, name);
 }
 
+static mpc_status launch_max(mpc_ctx* c, MaxArgs& a, i64 rows, i64 cols, int w, const char* name)
+{
+    const i64 wk = max_work_u64(cols);
+    if (w > 33) return launch_rows(c, k_max<1, BothA>, k_max<1, PairA>, a, rows, wk, 0, name);
+    if (a.cone) return launch_rows(c, k_max<2, BothA>, k_max<2, PairA>, a, rows, wk, 0, name);
+    return launch_rows(c, k_max<0, BothA>, k_max<0, PairA>, a, rows, wk, 0, name);
+}
+
 // ------------------------------------------------------------------ validation helpers ----
 // shares argument valid for the mode: both pointers (BOTH / LOOPBACK) or sh[party] (PAIR)
 static bool bad_sh(const mpc_ctx* c, mpc_shares s)
@@ -916,8 +924,7 @@ mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t
     if (rows > 0) {
         MaxArgs a{(u32)c->step, w, spv(c, x), sov(c, z), rows, cols, (u64)row_off, nullptr, 0, 0, nullptr,
                   use_cone(c, w) ? 1 : 0};
-        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), 0, "max")
-                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), 0, "max");
+        st = launch_max(c, a, rows, cols, w, "max");
         if (st) return st;
         acct_max(c, rows, cols, w);
     }
@@ -954,8 +961,7 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
         if ((st = cuda_check(c, "pool_gather"))) return st;
         MaxArgs a{(u32)c->step, w, SP{{rowsbuf.p[0], rowsbuf.p[1]}}, sov(c, z), rows, cols, row_off, nullptr, 0, 0,
                   nullptr, use_cone(c, w) ? 1 : 0};
-        st = w > 33 ? launch_rows(c, k_max<true, BothA>, k_max<true, PairA>, a, rows, max_work_u64(cols), 0, "maxpool")
-                    : launch_rows(c, k_max<false, BothA>, k_max<false, PairA>, a, rows, max_work_u64(cols), 0, "maxpool");
+        st = launch_max(c, a, rows, cols, w, "maxpool");
         if (st) return st;
         acct_max(c, rows, cols, w);
     }
@@ -986,8 +992,10 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
         a.cone = use_cone(c, p->window) ? 1 : 0;
         const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
-        st = wide ? launch_rows(c, k_softmax<true, BothA>, k_softmax<true, PairA>, a, rows, softmax_work_u64(cols), 64 * cols, "softmax")
-                  : launch_rows(c, k_softmax<false, BothA>, k_softmax<false, PairA>, a, rows, softmax_work_u64(cols), 64 * cols, "softmax");
+        const i64 wk = softmax_work_u64(cols), ek = 64 * cols;
+        st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax")
+           : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax")
+                    : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax");
         if (st) return st;
         const i64 n = rows * cols;
         acct_max(c, rows, cols, p->window);
