@@ -622,6 +622,127 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     pa.done(pr);
 }
 
+// Short-row MAX_row (cols <= MAXS_COLS; MaxPool windows).  The same contract as k_max (R22:
+// half-split tree with the odd entry carried, LTZ at step s + 2 lv and the mux at s + 2 lv + 1,
+// units row * h + i), but ONE WARP owns a 32-row tile: a 3x3 window's levels have h = 4, 2, 1,
+// 1 groups per tile, which would leave most of a CTA's warps idle at its level barriers.  The
+// warp's tile lives in its own shared-memory slice (levels in place: a level writes only
+// positions i < h, which no other unit of the level reads; the odd carry moves after the level)
+// and MaxPool gathers its k x k windows (public zero padding, R26) straight from the NCHW input.
+constexpr int MAXS_COLS = 16;
+struct MaxSmallArgs {
+    u32 s; int w; SP x; SO z; i64 rows, cols; u64 row_off;
+    int pool, k, stride, pad, H, W;
+    FastDiv fcol, fk, fwo, fho;        // cols, k, Wo, Ho
+};
+template <int LV, class PA>
+__global__ void __launch_bounds__(256, MPC_EW_MINB) k_max_small(const __grid_constant__ PA pa, MaxSmallArgs a)
+{
+    constexpr bool WIDE = LV == 1, CONE = LV == 2;
+    extern __shared__ __align__(16) u64 smem[];                 // per warp: 2 parties x 32 rows x cols
+    __shared__ ConeSmem<CG> cone_sm[CONE ? 8 : 1];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using S = typename decltype(pr)::S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int C = (int)a.cols;
+    u64* wb = smem + (i64)warp * 64 * C;
+    const SO X{{wb, wb + 32 * C}};
+    const SP Xc{{wb, wb + 32 * C}};
+    const i64 ntiles = (a.rows + 31) / 32;
+    for (i64 tile = (i64)cta * NW + warp; tile < ntiles; tile += (i64)ncta * NW) {
+        const i64 r0 = tile * 32;
+        const int R = (int)min((i64)32, a.rows - r0);
+        for (int t = lane; t < R * C; t += 32) {
+            const u32 rr = fdiv((u32)t, a.fcol);
+            const u32 e = (u32)t - rr * (u32)C;
+            S v;
+            if (a.pool) {                                      // window element e of output r0 + rr
+                const u32 o = (u32)(r0 + rr);
+                const u32 q1 = fdiv(o, a.fwo), ow = o - q1 * a.fwo.d;
+                const u32 q2 = fdiv(q1, a.fho), oh = q1 - q2 * a.fho.d;     // q2 = img * C + c
+                const u32 dy = fdiv(e, a.fk), dx = e - dy * a.fk.d;
+                const int iy = (int)(oh * a.stride + dy) - a.pad, ix = (int)(ow * a.stride + dx) - a.pad;
+                const bool in = iy >= 0 && iy < a.H && ix >= 0 && ix < a.W;
+                v = in ? pr.ld(a.x, ((i64)q2 * a.H + iy) * a.W + ix) : pr.zero();
+            } else {
+                v = pr.ld(a.x, (r0 + rr) * (i64)C + e);
+            }
+            pr.st(X, t, v);
+        }
+        __syncwarp();
+        const u64 g0 = a.row_off + (u64)r0;
+        int m = C, lv = 0;
+        while (m > 1) {
+            const int h = m / 2;
+            const u32 sl = a.s + 2u * (u32)lv;
+            const u64 ubase = g0 * (u64)h;                     // multiple of 32 (g0 is)
+            const FastDiv dh = make_fastdiv((u32)h);
+            if constexpr (CONE) {
+                for (int b = 0; b < h; b += CG) {
+                    S d[CG], l[CG], y[CG];
+                    int at[CG];
+#pragma unroll
+                    for (int g = 0; g < CG; ++g) {
+                        const int v = (b + g) * 32 + lane;
+                        d[g] = pr.zero(); y[g] = pr.zero(); at[g] = -1;
+                        if (b + g < h && v < R * h) {
+                            const int rr = (int)fdiv((u32)v, dh), i = v - rr * h;
+                            at[g] = rr * C + i;
+                            y[g] = pr.ld(Xc, at[g] + h);
+                            d[g] = pr.sub(pr.ld(Xc, at[g]), y[g]);
+                        }
+                    }
+                    const int ng = min(CG, h - b);
+                    const u64 q = (ubase >> 5) + (u64)b;
+                    if (ng == 1) {
+                        S d1[1] = {d[0]}, l1[1];
+                        pr.template ltz_cone<1>(q, sl, a.w, d1, l1, lane, *reinterpret_cast<ConeSmem<1>*>(&cone_sm[warp]));
+                        l[0] = l1[0];
+                    } else if (ng == 2) {
+                        S d2[2] = {d[0], d[1]}, l2[2];
+                        pr.template ltz_cone<2>(q, sl, a.w, d2, l2, lane, *reinterpret_cast<ConeSmem<2>*>(&cone_sm[warp]));
+                        l[0] = l2[0]; l[1] = l2[1];
+                    } else {
+                        pr.template ltz_cone<CG>(q, sl, a.w, d, l, lane, cone_sm[warp]);
+                    }
+#pragma unroll
+                    for (int g = 0; g < CG; ++g) {
+                        if (g >= ng) break;                    // warp-uniform
+                        const S sel = pr.add(y[g], pr.bm(ubase + (u64)((b + g) * 32 + lane), sl + 1, d[g], pr.notb(l[g])));
+                        if (at[g] >= 0) pr.st(X, at[g], sel);
+                    }
+                }
+            } else {
+                for (int g = 0; g < h; ++g) {                  // 32*h units = h groups
+                    const int v = g * 32 + lane;
+                    int at = -1;
+                    S d = pr.zero(), y = pr.zero();
+                    if (v < R * h) {
+                        const int rr = (int)fdiv((u32)v, dh), i = v - rr * h;
+                        at = rr * C + i;
+                        y = pr.ld(Xc, at + h);
+                        d = pr.sub(pr.ld(Xc, at), y);
+                    }
+                    const S c = pr.notb(pr.template ltz<WIDE>((ubase >> 5) + (u64)g, sl, a.w, d, lane));
+                    const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
+                    if (at >= 0) pr.st(X, at, sel);
+                }
+            }
+            __syncwarp();
+            if (m & 1) {
+                for (int rr = lane; rr < R; rr += 32) pr.st(X, rr * C + h, pr.ld(Xc, rr * C + m - 1));
+                __syncwarp();
+            }
+            m = h + (m & 1);
+            ++lv;
+        }
+        for (int rr = lane; rr < R; rr += 32) pr.st(a.z, r0 + rr, pr.ld(Xc, rr * C));
+        __syncwarp();
+    }
+    pa.done(pr);
+}
+
 struct LnArgs {
     u32 s_sq, s_rs, s_mul; NrK rk; SP x; SO z; i64 rows, cols; u64 row_off;
     int mean_mode; u64 e_invd, e_eps;

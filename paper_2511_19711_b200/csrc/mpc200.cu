@@ -416,6 +416,30 @@ static mpc_status launch_max(mpc_ctx* c, MaxArgs& a, i64 rows, i64 cols, int w, 
     return launch_rows(c, k_max<0, BothA>, k_max<0, PairA>, a, rows, wk, 0, name);
 }
 
+// short rows (cols <= MAXS_COLS, MaxPool windows): warp-per-tile kernel, windows gathered in-kernel
+static mpc_status launch_max_small(mpc_ctx* c, MaxSmallArgs& a, const char* name)
+{
+    const int lv = a.w > 33 ? 1 : (use_cone(c, a.w) ? 2 : 0);
+    const size_t dyn = sizeof(u64) * 64 * (size_t)a.cols * NWARPS;
+    a.fcol = make_fastdiv((u32)a.cols);
+    const i64 ntiles = (a.rows + 31) / 32;
+    const i64 nctas = (ntiles + NWARPS - 1) / NWARPS;
+    auto pick = [&](auto kb, auto kp) -> mpc_status {
+        cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (is_pair(c)) return launch_pair_kernel_tpb(c, kp, pair_ctas(c, kp, dyn, nctas, TPB), dyn, TPB, name, a);
+        const int grid = (int)std::min<i64>(nctas, (i64)c->sm_count * occupancy(kb, dyn, TPB));
+        rec_begin(c, name, (u64)a.rows);
+        kb<<<grid, TPB, dyn, c->stream>>>(BothA{c->K}, a);
+        rec_end(c);
+        c->st.launches++;
+        return cuda_check(c, name);
+    };
+    if (lv == 1) return pick(k_max_small<1, BothA>, k_max_small<1, PairA>);
+    if (lv == 2) return pick(k_max_small<2, BothA>, k_max_small<2, PairA>);
+    return pick(k_max_small<0, BothA>, k_max_small<0, PairA>);
+}
+
 // ------------------------------------------------------------------ validation helpers ----
 // shares argument valid for the mode: both pointers (BOTH / LOOPBACK) or sh[party] (PAIR)
 static bool bad_sh(const mpc_ctx* c, mpc_shares s)
@@ -921,7 +945,14 @@ mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t
     if (w < 1 || w > 64) return fail(c, MPC_ERR_RANGE, "window");
     if (bad_sh(c, x) || bad_sh(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "max args (row_off % 32)");
-    if (rows > 0) {
+    if (rows > 0 && cols <= MAXS_COLS) {
+        MaxSmallArgs a{};
+        a.s = (u32)c->step; a.w = w; a.x = spv(c, x); a.z = sov(c, z); a.rows = rows; a.cols = cols;
+        a.row_off = (u64)row_off; a.pool = 0;
+        st = launch_max_small(c, a, "max");
+        if (st) return st;
+        acct_max(c, rows, cols, w);
+    } else if (rows > 0) {
         MaxArgs a{(u32)c->step, w, spv(c, x), sov(c, z), rows, cols, (u64)row_off, nullptr, 0, 0, nullptr,
                   use_cone(c, w) ? 1 : 0};
         st = launch_max(c, a, rows, cols, w, "max");
@@ -948,7 +979,15 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
     const u64 row_off = (u64)img_off * (u64)C * (u64)Ho * (u64)Wo;
     if (bad_sh(c, x) || bad_sh(c, z) || img_off < 0 || (row_off & 31)) return fail(c, MPC_ERR_INVALID, "maxpool args");
     if (max_work_u64(cols) * 8 > (i64)SMEM_LIMIT) return fail(c, MPC_ERR_UNSUPPORTED, "pool window too large");
-    if (rows > 0) {
+    if (rows > 0 && cols <= MAXS_COLS && rows < (1ll << 31) && (i64)N * C * H * W < (1ll << 40)) {
+        MaxSmallArgs a{};
+        a.s = (u32)c->step; a.w = w; a.x = spv(c, x); a.z = sov(c, z); a.rows = rows; a.cols = cols;
+        a.row_off = row_off; a.pool = 1; a.k = k; a.stride = stride; a.pad = pad; a.H = H; a.W = W;
+        a.fk = make_fastdiv((u32)k); a.fwo = make_fastdiv((u32)Wo); a.fho = make_fastdiv((u32)Ho);
+        st = launch_max_small(c, a, "maxpool");
+        if (st) return st;
+        acct_max(c, rows, cols, w);
+    } else if (rows > 0) {
         // gather the windows (public zero padding) into rows, then the fused row max
         const size_t gb = sizeof(u64) * (size_t)(rows * cols);
         u64* Rw = (u64*)scratch(c, 2 * gb);

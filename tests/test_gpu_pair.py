@@ -117,6 +117,20 @@ def test_max_pool_ln_loopback(m):
     p.sync()
 
 
+def test_max_pool_cone_loopback(m):
+    b, p = ctxs(m, 4)
+    b.set_ltz_circuit(1)
+    p.set_ltz_circuit(1)
+    x = b.share(torch.from_numpy(workloads.softmax_inputs(70, 9)).cuda())
+    p.set_step(b.step)
+    assert eq(b.max(x, 70, 9), p.max(x, 70, 9))
+    N, C, H, W = 2, 16, 14, 15
+    y = b.share(torch.from_numpy(workloads.maxpool_inputs((N, C, H, W))).cuda())
+    p.set_step(b.step)
+    assert eq(b.maxpool2d(y, N, C, H, W), p.maxpool2d(y, N, C, H, W))
+    p.sync()
+
+
 def test_pair_vs_oracle_and_long_sequence(m):
     """Many consecutive ops on one PAIR context: the per-warp round counters persist across
     launches, so no op can read a previous op's stale message."""
