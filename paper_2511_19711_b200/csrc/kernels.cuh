@@ -133,10 +133,18 @@ struct CmpConeBody {
 };
 
 // S13 with carry-cone LTZs: the 2-3 segment comparisons of CG groups run first (stashed in
-// shared memory), then each group's polynomial / final products (act_tail), same step ids.
+// shared memory), then the polynomial / final products run in the PAIR layout -- thread <-> unit
+// pairs (2p, 2p+1), one c0 block per pair, two independent Beaver chains per thread (act_tail2).
+// Same step ids, units and output bits as act_group.  (The same body with Kogge-Stone LTZs per
+// group measured 10 % slower than ActBody, so the Kogge-Stone path keeps the group layout.)
 struct ActConeBody {
     static constexpr int kStash = 3 * CG * 32 * 2;      // [3 ltz][CG][32 lanes][2 words]
     u32 s; ActK p; SP x; SO z; i64 n;
+    template <class P>
+    __device__ __forceinline__ void ltzs(P& pr, u64 q0, u32 sl, typename P::S (&in)[CG], typename P::S (&out)[CG],
+                                         int lane, ConeSmem<CG>& sm) const {
+        pr.template ltz_cone<CG>(q0, sl, p.w, in, out, lane, sm);
+    }
     template <class P>
     __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG>& sm, u64* st) const {
         using S = typename P::S;
@@ -152,7 +160,7 @@ struct ActConeBody {
         const bool relu_form = p.form == 2 || p.deg == 0;
         u32 sl = s;
         if (relu_form || p.form == 1) {                 // ltz(x): the ReLU mask or the sign of x
-            pr.template ltz_cone<CG>(q0, sl, p.w, xv, t, lane, sm);
+            ltzs(pr, q0, sl, xv, t, lane, sm);
 #pragma unroll
             for (int g = 0; g < CG; ++g) stS[(0 * CG + g) * 32 + lane] = t[g];
             ++sl;
@@ -160,30 +168,37 @@ struct ActConeBody {
         if (!relu_form) {
 #pragma unroll
             for (int g = 0; g < CG; ++g) t[g] = pr.addp(xv[g], p.e_B);
-            pr.template ltz_cone<CG>(q0, sl, p.w, t, t, lane, sm);
+            ltzs(pr, q0, sl, t, t, lane, sm);
 #pragma unroll
             for (int g = 0; g < CG; ++g) stS[(1 * CG + g) * 32 + lane] = t[g];
 #pragma unroll
             for (int g = 0; g < CG; ++g) t[g] = pr.addp(xv[g], p.e_mB);
-            pr.template ltz_cone<CG>(q0, sl + 1, p.w, t, t, lane, sm);
+            ltzs(pr, q0, sl + 1, t, t, lane, sm);
 #pragma unroll
             for (int g = 0; g < CG; ++g) stS[(2 * CG + g) * 32 + lane] = t[g];
             sl += 2;
         }
+        __syncwarp();
 #pragma unroll 1
-        for (int g = 0; g < CG; ++g) {
-            const i64 i = (gb + g) * 32 + lane;
+        for (int j = 0; j < CG / 2; ++j) {              // pair lane + 32 j: elements e, e + 1 of the block
+            const int e = 2 * (lane + 32 * j);
+            const int o = e;                            // stash [k][g][lane]: element e of the block at k*CG*32 + e
+            const i64 i = gb * 32 + e;
             const u64 u = off + (u64)i;
-            S r;
+            const S x0 = i < n ? pr.ld(x, i) : pr.zero(), x1 = i + 1 < n ? pr.ld(x, i + 1) : pr.zero();
+            S r0, r1;
             if (relu_form) {
-                const S nl = pr.notb(stS[(0 * CG + g) * 32 + lane]);
-                r = p.act == 2 ? pr.shl(nl, FRAC) : pr.bm(u, sl, xv[g], nl);
+                const S n0 = pr.notb(stS[o]), n1 = pr.notb(stS[o + 1]);
+                if (p.act == 2) { r0 = pr.shl(n0, FRAC); r1 = pr.shl(n1, FRAC); }
+                else pr.bm2(u, sl, x0, n0, x1, n1, r0, r1);
             } else {
-                r = act_tail(pr, u, sl, p, xv[g], stS[(0 * CG + g) * 32 + lane], stS[(1 * CG + g) * 32 + lane],
-                             stS[(2 * CG + g) * 32 + lane]);
+                act_tail2(pr, u, sl, p, x0, x1, stS[o], stS[o + 1], stS[CG * 32 + o], stS[CG * 32 + o + 1],
+                          stS[2 * CG * 32 + o], stS[2 * CG * 32 + o + 1], r0, r1);
             }
-            if (i < n) pr.st(z, i, r);
+            if (i < n) pr.st(z, i, r0);
+            if (i + 1 < n) pr.st(z, i + 1, r1);
         }
+        __syncwarp();
     }
 };
 
@@ -247,18 +262,19 @@ struct CmpBody {
 
 template <bool WIDE>
 struct ExpGroupBody {
-    u32 s; ExpK p; SP x; SO z;
+    u32 s; ExpK p; SP x; SO z; int head_only;   // head_only: the clamp head (steps s, s+1) alone
     template <class P>
     __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
         typename P::S xv = pr.zero();
         if (valid) xv = pr.ld(x, i);
-        const typename P::S y = exp_group<WIDE>(pr, u, q, s, p, xv, lane);
+        const typename P::S y = head_only ? exp_clamp_head<WIDE>(pr, u, q, s, p, xv, lane)
+                                          : exp_group<WIDE>(pr, u, q, s, p, xv, lane);
         if (valid) pr.st(z, i, y);
     }
 };
 
 struct ExpPairBody {
-    u32 s; ExpK p; SP x; SO z; i64 n;
+    u32 s; ExpK p; SP x; SO z; i64 n; int sq_only;   // sq_only: x holds the clamp head's y
     template <int V, class P>
     __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
         typename P::S a[V], b[V];
@@ -268,7 +284,8 @@ struct ExpPairBody {
             if (ok[v] && i0[v] >= 0) a[v] = pr.ld(x, i0[v]);
             if (ok[v] && i0[v] + 1 < n) b[v] = pr.ld(x, i0[v] + 1);
         }
-        exp_pairv<V>(pr, u, s, p, a, b);
+        if (sq_only) exp_squarings_pairv<V>(pr, u, s, p, a, b);
+        else exp_pairv<V>(pr, u, s, p, a, b);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], a[v]);
@@ -513,13 +530,36 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         const SP MXc{{MX.p[0], MX.p[1]}};
         if (MPC_SOFTMAX_SKIP & 2) {
         } else if (a.ek.clamp) {
+            // clamp head in the LTZ group layout, then the squarings in the pair layout (E in place)
             for (i64 g = warp; g < (ne + 31) / 32; g += NW) {
                 const i64 e = g * 32 + lane;
                 const bool valid = e < ne;
                 S d = pr.zero();
                 if (valid) d = pr.sub(pr.ld(xt, e), pr.ld(MXc, fdiv((u32)e, dC)));
-                const S y = exp_group<WIDE>(pr, ub + e, (ub >> 5) + g, a.s_exp, a.ek, d, lane);
+                const S y = exp_clamp_head<WIDE>(pr, ub + e, (ub >> 5) + g, a.s_exp, a.ek, d, lane);
                 if (valid) pr.st(E, e, y);
+            }
+            __syncthreads();
+            const SP Ec{{E.p[0], E.p[1]}};
+            constexpr int V = decltype(pr)::kV;
+            for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
+                u64 uv[V];
+                S da[V], db[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    uv[v] = ub + (u64)e;
+                    da[v] = db[v] = pr.zero();
+                    if (e < ne) da[v] = pr.ld(Ec, e);
+                    if (e + 1 < ne) db[v] = pr.ld(Ec, e + 1);
+                }
+                exp_squarings_pairv<V>(pr, uv, a.s_exp + 2, a.ek, da, db);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    if (e < ne) pr.st(E, e, da[v]);
+                    if (e + 1 < ne) pr.st(E, e + 1, db[v]);
+                }
             }
         } else {
             constexpr int V = decltype(pr)::kV;

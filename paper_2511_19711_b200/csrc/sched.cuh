@@ -52,13 +52,23 @@ __device__ __forceinline__ void exp_pair(P& pr, u64 u, u32 s, const ExpK& p, typ
     }
 }
 
-// V pairs per lane (P::kV): the same schedule on V unit pairs, one exchange per step in PAIR.
-template <int V, class P>
-__device__ __forceinline__ void exp_pairv(P& pr, const u64 (&u)[V], u32 s, const ExpK& p,
-                                          typename P::S (&y0)[V], typename P::S (&y1)[V])
+// Clamp head of EXP (steps s, s+1; group layout): y = BM(addP(shr(x,t),1), NOT(LTZ_w(addP(x,2^t)))).
+// Splitting it from the squarings lets the t squarings run in the pair layout (one c0 block per
+// unit pair, 5 independent Philox blocks per thread and step) -- same units, same output bits.
+template <bool WIDE, class P>
+__device__ __forceinline__ typename P::S exp_clamp_head(P& pr, u64 u, u64 q, u32 s, const ExpK& p,
+                                                        typename P::S x, int lane)
 {
-#pragma unroll
-    for (int v = 0; v < V; ++v) { y0[v] = pr.addp(pr.shr_(y0[v], p.t), p.e_one); y1[v] = pr.addp(pr.shr_(y1[v], p.t), p.e_one); }
+    const typename P::S y = pr.addp(pr.shr_(x, p.t), p.e_one);
+    const typename P::S l = pr.template ltz<WIDE>(q, s, p.w, pr.addp(x, p.e_2t), lane);
+    return pr.bm(u, s + 1, y, pr.notb(l));
+}
+
+// The t squarings of EXP (steps s .. s+t-1) on V unit pairs per lane.
+template <int V, class P>
+__device__ __forceinline__ void exp_squarings_pairv(P& pr, const u64 (&u)[V], u32 s, const ExpK& p,
+                                                    typename P::S (&y0)[V], typename P::S (&y1)[V])
+{
     for (int k = 0; k < p.t; ++k) {
         typename P::S a[V], b[V];
         if (p.sq) pr.template sq2v<V>(u, s + k, y0, y1, a, b);
@@ -66,6 +76,16 @@ __device__ __forceinline__ void exp_pairv(P& pr, const u64 (&u)[V], u32 s, const
 #pragma unroll
         for (int v = 0; v < V; ++v) { y0[v] = pr.shr_(a[v], FRAC); y1[v] = pr.shr_(b[v], FRAC); }
     }
+}
+
+// V pairs per lane (P::kV): the same schedule on V unit pairs, one exchange per step in PAIR.
+template <int V, class P>
+__device__ __forceinline__ void exp_pairv(P& pr, const u64 (&u)[V], u32 s, const ExpK& p,
+                                          typename P::S (&y0)[V], typename P::S (&y1)[V])
+{
+#pragma unroll
+    for (int v = 0; v < V; ++v) { y0[v] = pr.addp(pr.shr_(y0[v], p.t), p.e_one); y1[v] = pr.addp(pr.shr_(y1[v], p.t), p.e_one); }
+    exp_squarings_pairv<V>(pr, u, s, p, y0, y1);
 }
 
 template <int V, class P>
@@ -273,6 +293,68 @@ __device__ __forceinline__ typename P::S act_tail(P& pr, u64 u, u32 s, const Act
     if (p.act == 2) out = pr.add(out, pr.shl(nl2, FRAC));
     else out = pr.add(out, pr.bm(u, s + 1, x, nl2));
     return out;
+}
+
+// ---- the same tails on a unit PAIR (u even, u+1) per thread: one c0 block per pair and step,
+// two independent chains per thread.  Same steps, units and output bits as act_tail.
+template <class P>
+__device__ __forceinline__ void horner2(P& pr, u64 u, u32 s, const u64* c, int d, typename P::S v0,
+                                        typename P::S v1, typename P::S& h0, typename P::S& h1)
+{
+    h0 = pr.addp(pr.mulf(v0, c[d]), c[d - 1]);
+    h1 = pr.addp(pr.mulf(v1, c[d]), c[d - 1]);
+    for (int k = d - 2; k >= 0; --k) {
+        typename P::S a, b;
+        pr.bm2(u, s, h0, v0, h1, v1, a, b);
+        h0 = pr.addp(pr.shr_(a, FRAC), c[k]);
+        h1 = pr.addp(pr.shr_(b, FRAC), c[k]);
+        ++s;
+    }
+}
+
+template <class P>
+__device__ __forceinline__ void act_tail2(P& pr, u64 u, u32 s, const ActK& p, typename P::S x0, typename P::S x1,
+                                          typename P::S sg0, typename P::S sg1, typename P::S la0, typename P::S la1,
+                                          typename P::S lb0, typename P::S lb1, typename P::S& r0, typename P::S& r1)
+{
+    using S = typename P::S;
+    S h0, h1;
+    if (p.form == 0) {
+        horner2(pr, u, s, p.c, p.deg, x0, x1, h0, h1);
+        s += p.deg - 1;
+    } else if (p.form == 1) {
+        S ax0, ax1, t0, t1;
+        pr.bm2(u, s, x0, pr.pm1(sg0), x1, pr.pm1(sg1), ax0, ax1);
+        ++s;
+        horner2(pr, u, s, p.c, p.deg, ax0, ax1, t0, t1);
+        h0 = pr.add(pr.mulf(x0, p.e_half), t0);
+        h1 = pr.add(pr.mulf(x1, p.e_half), t1);
+        s += p.deg - 1;
+    } else {
+        const S z0 = pr.mulf(x0, p.e_isqrt2), z1 = pr.mulf(x1, p.e_isqrt2);
+        S a, b, q0, q1;
+        pr.bm2(u, s, z0, z0, z1, z1, a, b);
+        ++s;
+        horner2(pr, u, s, p.c, p.deg, pr.shr_(a, FRAC), pr.shr_(b, FRAC), q0, q1);
+        s += p.deg - 1;
+        pr.bm2(u, s, z0, q0, z1, q1, a, b);
+        const S e0 = pr.mulf(pr.shr_(a, FRAC), p.e_2sqrtpi), e1 = pr.mulf(pr.shr_(b, FRAC), p.e_2sqrtpi);
+        pr.bm2(u, s + 1, x0, pr.addp(e0, p.e_one), x1, pr.addp(e1, p.e_one), a, b);
+        h0 = pr.mulf(pr.shr_(a, FRAC), p.e_half);
+        h1 = pr.mulf(pr.shr_(b, FRAC), p.e_half);
+        s += 2;
+    }
+    pr.bm2(u, s, h0, pr.sub(lb0, la0), h1, pr.sub(lb1, la1), r0, r1);
+    const S n0 = pr.notb(lb0), n1 = pr.notb(lb1);
+    if (p.act == 2) {
+        r0 = pr.add(r0, pr.shl(n0, FRAC));
+        r1 = pr.add(r1, pr.shl(n1, FRAC));
+    } else {
+        S a, b;
+        pr.bm2(u, s + 1, x0, n0, x1, n1, a, b);
+        r0 = pr.add(r0, a);
+        r1 = pr.add(r1, b);
+    }
 }
 
 }  // namespace mpc
