@@ -430,7 +430,7 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
                 d = pr.sub(pr.ld(cur, rr * li + i), y);
             }
             const u64 q = (ubase >> 5) + (u64)g;
-            const S c = pr.notb(pr.template ltz<WIDE>(q, sl, w, d, lane));
+            const S c = pr.notb(pr.template ltz_o<WIDE>(q, sl, w, d, lane));
             const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
             if (valid) {
                 pr.st(o, rr * lo + i, sel);

@@ -64,6 +64,8 @@ struct BothP {
     }
     template <bool WIDE>
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(*Kp, q, s, w, x, lane); }
+    template <bool WIDE>
+    __device__ __forceinline__ S ltz_o(u64 q, u32 s, int w, S x, int lane) { return ltz<WIDE>(q, s, w, x, lane); }
     __device__ __forceinline__ S sq(u64 u, u32 s, S y) { return mpc::sq1(*Kp, u, s, y); }
     template <int G>
     __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G>& sm) {
@@ -236,7 +238,11 @@ struct PairP {
     __device__ __forceinline__ S bm_finish(u64 a, u64 b, u64 c, u64 e, u64 f) const {
         return pty == 0 ? c + e * b + f * a + e * f : c + e * b + f * a;
     }
+#if MPC_PAIR_BM_INLINE
     __device__ __forceinline__ S bm(u64 u, u32 s, S x, S y) {
+#else
+    __device__ __noinline__ S bm(u64 u, u32 s, S x, S y) {
+#endif
         const int lane = threadIdx.x & 31;
         u64 a, b, c;
         triple(u, s, beaver_c0(*Kp, u, s), a, b, c);
@@ -245,7 +251,11 @@ struct PairP {
         const u64 e = (x - a) + get(lane, 0), f = (y - b) + get(lane, 1);
         return bm_finish(a, b, c, e, f);
     }
+#if MPC_PAIR_BM_INLINE
     __device__ __forceinline__ void bm2(u64 u, u32 s, S x0, S y0, S x1, S y1, S& z0, S& z1) {
+#else
+    __device__ __noinline__ void bm2(u64 u, u32 s, S x0, S y0, S x1, S y1, S& z0, S& z1) {
+#endif
         const int lane = threadIdx.x & 31;
         const uint4 C = prg(Kp->k0, u >> 1, s, 1);
         u64 a0, b0, c0, a1, b1, c1;
@@ -418,6 +428,15 @@ struct PairP {
         return pty == 0 ? c + sg * rA : sg * rA;
     }
 
+    // Out-of-line LTZ for schedules with several comparison sites (S13's 2-3 segment masks, the
+    // clamp inside exp / NR): one copy of the circuit and its polling loops per kernel instead of
+    // one per site.  Measured in loopback: GELU 2.6x faster (the inlined copies made the kernel's
+    // instruction fetch the top stall); single-site kernels (ReLU) stay inlined (8 % faster).
+    template <bool WIDE>
+    __device__ __noinline__ S ltz_o(u64 q, u32 s, int w, S x, int lane) { return ltz<WIDE>(q, s, w, x, lane); }
+#ifndef MPC_PAIR_BM_INLINE
+#define MPC_PAIR_BM_INLINE 1
+#endif
     template <bool WIDE>
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) {
         if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(q, s, w, x, lane);

@@ -30,7 +30,7 @@ __device__ __forceinline__ typename P::S exp_group(P& pr, u64 u, u64 q, u32 s, c
 {
     typename P::S y = pr.addp(pr.shr_(x, p.t), p.e_one);
     if (p.clamp) {
-        const typename P::S l = pr.template ltz<WIDE>(q, s, p.w, pr.addp(x, p.e_2t), lane);
+        const typename P::S l = pr.template ltz_o<WIDE>(q, s, p.w, pr.addp(x, p.e_2t), lane);
         y = pr.bm(u, s + 1, y, pr.notb(l));
         s += 2;
     }
@@ -60,7 +60,7 @@ __device__ __forceinline__ typename P::S exp_clamp_head(P& pr, u64 u, u64 q, u32
                                                         typename P::S x, int lane)
 {
     const typename P::S y = pr.addp(pr.shr_(x, p.t), p.e_one);
-    const typename P::S l = pr.template ltz<WIDE>(q, s, p.w, pr.addp(x, p.e_2t), lane);
+    const typename P::S l = pr.template ltz_o<WIDE>(q, s, p.w, pr.addp(x, p.e_2t), lane);
     return pr.bm(u, s + 1, y, pr.notb(l));
 }
 
@@ -252,14 +252,14 @@ __device__ __forceinline__ typename P::S act_group(P& pr, u64 u, u64 q, u32 s, c
 {
     using S = typename P::S;
     if (p.form == 2 || p.deg == 0) {
-        const S nl = pr.notb(pr.template ltz<WIDE>(q, s, p.w, x, lane));
+        const S nl = pr.notb(pr.template ltz_o<WIDE>(q, s, p.w, x, lane));
         if (p.act == 2) return pr.shl(nl, FRAC);
         return pr.bm(u, s + 1, x, nl);
     }
     S sgn = pr.zero();
-    if (p.form == 1) { sgn = pr.template ltz<WIDE>(q, s, p.w, x, lane); ++s; }
-    const S l1 = pr.template ltz<WIDE>(q, s, p.w, pr.addp(x, p.e_B), lane);
-    const S l2 = pr.template ltz<WIDE>(q, s + 1, p.w, pr.addp(x, p.e_mB), lane);
+    if (p.form == 1) { sgn = pr.template ltz_o<WIDE>(q, s, p.w, x, lane); ++s; }
+    const S l1 = pr.template ltz_o<WIDE>(q, s, p.w, pr.addp(x, p.e_B), lane);
+    const S l2 = pr.template ltz_o<WIDE>(q, s + 1, p.w, pr.addp(x, p.e_mB), lane);
     return act_tail(pr, u, s + 2, p, x, sgn, l1, l2);
 }
 
