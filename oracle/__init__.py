@@ -62,14 +62,15 @@ def lib():
         L.orc_recip.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, INT, INT]
         L.orc_rsqrt.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, INT, INT]
         L.orc_act.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, DBL,
-                              ctypes.c_void_p, INT, INT]
+                              ctypes.c_void_p, INT, INT, INT]
+        L.orc_mul_bcast.argtypes = [CP, u64p, u64p, u64p, u64p, u64p, u64p, I64, I64, I64, I64, INT]
         L.orc_max.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, INT]
         L.orc_maxpool2d.argtypes = [CP, u64p, u64p, u64p, u64p, INT, INT, INT, INT, INT, INT, INT,
                                     I64, INT]
         L.orc_softmax.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, INT,
-                                  INT, INT, INT, INT, INT, INT, INT, INT, INT]
+                                  INT, INT, INT, INT, INT, INT, INT, INT, INT, INT]
         L.orc_layernorm.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, DBL, INT,
-                                    INT, INT, INT, INT, INT]
+                                    INT, INT, INT, INT, INT, INT]
         L.orc_ltz_gate_count.argtypes = [INT]; L.orc_ltz_gate_count.restype = INT
         L.orc_max_levels.argtypes = [I64]; L.orc_max_levels.restype = INT
         L.orc_trunc_wrap_trials.argtypes = [INT, INT, I64, I64, ctypes.c_uint64]
@@ -148,6 +149,13 @@ class Oracle:
         lib().orc_mul(ctypes.byref(self.c), x0, x1, y0, y1, z0, z1, x0.size, off, trunc_bits)
         return z0, z1
 
+    def mul_bcast(self, x, y, rows, cols, off=0, row_off=0, trunc_bits=0):
+        """z[r, j] = x[r, j] * y[r] with a broadcast triple."""
+        (x0, x1), (y0, y1) = map(lambda p: (_u(p[0]), _u(p[1])), (x, y))
+        z0, z1 = _pair(rows * cols)
+        lib().orc_mul_bcast(ctypes.byref(self.c), x0, x1, y0, y1, z0, z1, rows, cols, off, row_off, trunc_bits)
+        return z0, z1
+
     @staticmethod
     def trunc(x, bits=16):
         x0, x1 = _u(x[0]), _u(x[1])
@@ -183,10 +191,10 @@ class Oracle:
     FORM = {"poly_x": 0, "poly_abs": 1, "relu": 2, "erf": 3}
 
     def act(self, x, act="gelu", form="poly_x", degree=4, B=5.0, coeffs=None, erf_terms=8,
-            off=0, window=33):
+            off=0, window=33, basis=0):
         c = np.ascontiguousarray(coeffs if coeffs is not None else [0.0], dtype=np.float64)
         return self._un(lib().orc_act, x, off, self.ACT[act], self.FORM[form], degree, float(B),
-                        c.ctypes.data, erf_terms, window)
+                        c.ctypes.data, erf_terms, window, basis)
 
     def max(self, x, rows, cols, row_off=0, window=33):
         x0, x1 = _u(x[0]), _u(x[1])
@@ -204,18 +212,19 @@ class Oracle:
         return z0, z1
 
     def softmax(self, x, rows, cols, row_off=0, window=33, exp_t=8, exp_clamp=0, exp_window=33,
-                recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0, recip_square=0):
+                recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0, recip_square=0,
+                bcast=0):
         x0, x1 = _u(x[0]), _u(x[1])
         z0, z1 = _pair(rows * cols)
         lib().orc_softmax(ctypes.byref(self.c), x0, x1, z0, z1, rows, cols, row_off, window,
                           exp_t, exp_clamp, exp_window, exp_square, recip_iters, recip_t, recip_clamp,
-                          recip_window, recip_square)
+                          recip_window, recip_square, bcast)
         return z0, z1
 
     def layernorm(self, x, rows, cols, row_off=0, eps=1e-5, mean_mode=0, rsqrt_iters=3,
-                  rsqrt_t=8, rsqrt_clamp=0, rsqrt_window=33, rsqrt_square=0):
+                  rsqrt_t=8, rsqrt_clamp=0, rsqrt_window=33, rsqrt_square=0, bcast=0):
         x0, x1 = _u(x[0]), _u(x[1])
         z0, z1 = _pair(rows * cols)
         lib().orc_layernorm(ctypes.byref(self.c), x0, x1, z0, z1, rows, cols, row_off, eps,
-                            mean_mode, rsqrt_iters, rsqrt_t, rsqrt_clamp, rsqrt_window, rsqrt_square)
+                            mean_mode, rsqrt_iters, rsqrt_t, rsqrt_clamp, rsqrt_window, rsqrt_square, bcast)
         return z0, z1

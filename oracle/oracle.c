@@ -197,6 +197,51 @@ void orc_mul(orc_ctx* ctx, const u64* x0, const u64* x1, const u64* y0, const u6
         for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], trunc_bits); z1[i] = shr(z1[i], trunc_bits); }
 }
 
+/* ------------------------------------------------------------------------ */
+/* Broadcast-triple product z_i = x_i * y_{row(i)} (SURVEY 8(f) NEXT #2 "a     */
+/* broadcast triple for softmax's e*r"; the expanded product of S:435 opens    */
+/* y once per ELEMENT, this one once per ROW).  Layout:        */
+/*   (a0, c0) = PRG(K0, u, s, 4) ; a1 = half (u&1) of PRG(K1, u>>1, s, 5)      */
+/*   b0 = PRG(K0, r, s, 6)[0..1] ; b1 = PRG(K1, r, s, 6)[0..1]                 */
+/*   c1 = (a0+a1)(b0+b1) - c0            (dealer correction -> party 1, R7)    */
+/* e_i = open(x_i - a_i) per element, f_r = open(y_r - b_r) per row;           */
+/* z0 = c0 + e b0 + f a0 + e f (party 0 adds e f, R6) ; z1 = c1 + e b1 + f a1. */
+/* u = element unit (units0 + i), r = row unit (row0 + row).  One step.        */
+/* ------------------------------------------------------------------------ */
+static void BMB(orc_ctx* ctx, i64 rows, i64 cols, u64 units0, u64 row0,
+                const u64* x0, const u64* x1, const u64* y0, const u64* y1, u64* z0, u64* z1)
+{
+    u64 s = ctx->step++;
+    for (i64 r = 0; r < rows; ++r) {
+        u32 w[4];
+        prg(ctx->key_p0, row0 + (u64)r, s, 6, w);
+        u64 b0 = w64(w[0], w[1]);
+        prg(ctx->key_p1, row0 + (u64)r, s, 6, w);
+        u64 b1 = w64(w[0], w[1]);
+        u64 f = (y0[r] - b0) + (y1[r] - b1);             /* opened once per row */
+        for (i64 j = 0; j < cols; ++j) {
+            i64 i = r * cols + j;
+            u64 u = units0 + (u64)i;
+            prg(ctx->key_p0, u, s, 4, w);
+            u64 a0 = w64(w[0], w[1]), c0 = w64(w[2], w[3]);
+            prg(ctx->key_p1, u >> 1, s, 5, w);
+            u64 a1 = (u & 1) ? w64(w[2], w[3]) : w64(w[0], w[1]);
+            u64 c1 = (a0 + a1) * (b0 + b1) - c0;
+            u64 e = (x0[i] - a0) + (x1[i] - a1);         /* opened per element */
+            z0[i] = c0 + e * b0 + f * a0 + e * f;
+            z1[i] = c1 + e * b1 + f * a1;
+        }
+    }
+}
+
+void orc_mul_bcast(orc_ctx* ctx, const u64* x0, const u64* x1, const u64* y0, const u64* y1,
+                   u64* z0, u64* z1, i64 rows, i64 cols, i64 off, i64 row_off, int trunc_bits)
+{
+    BMB(ctx, rows, cols, (u64)off, (u64)row_off, x0, x1, y0, y1, z0, z1);
+    if (trunc_bits)
+        for (i64 i = 0; i < rows * cols; ++i) { z0[i] = shr(z0[i], trunc_bits); z1[i] = shr(z1[i], trunc_bits); }
+}
+
 /* S5 local truncation: z_i = (int64)x_i >> k at each party */
 void orc_trunc(const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, int bits)
 {
@@ -495,6 +540,31 @@ static void HORNER(orc_ctx* ctx, i64 n, u64 units0, const u64* v0, const u64* v1
     }
 }
 
+/* POWER(v; c_0..c_d), 1 <= d <= 4 (SURVEY 8(f) NEXT #2 "power-basis polynomials   */
+/* (2 rounds instead of 3)"):  v2 = MT(v,v); v3 = MT(v2,v); v4 = MT(v2,v2) (steps   */
+/* in this order; v3 and v4 need only v2, so they share one round);                */
+/* h = addP(sum_{k=1..d} pmulF(v^k, c_k), c_0).  d-1 steps, like HORNER.            */
+static void POWER(orc_ctx* ctx, i64 n, u64 units0, const u64* v0, const u64* v1,
+                  const double* c, int d, u64* h0, u64* h1)
+{
+    u64 *p0[5] = {0}, *p1[5] = {0};
+    u64 *t0 = A(n), *t1 = A(n);
+    p0[1] = (u64*)v0; p1[1] = (u64*)v1;
+    for (int k = 2; k <= d; ++k) { p0[k] = A(n); p1[k] = A(n); }
+    if (d >= 2) MT(ctx, n, units0, v0, v1, v0, v1, p0[2], p1[2]);
+    if (d >= 3) MT(ctx, n, units0, p0[2], p1[2], v0, v1, p0[3], p1[3]);
+    if (d >= 4) MT(ctx, n, units0, p0[2], p1[2], p0[2], p1[2], p0[4], p1[4]);
+    memset(h0, 0, sizeof(u64) * (size_t)n); memset(h1, 0, sizeof(u64) * (size_t)n);
+    for (int k = 1; k <= d; ++k) {
+        memcpy(t0, p0[k], sizeof(u64) * (size_t)n); memcpy(t1, p1[k], sizeof(u64) * (size_t)n);
+        pmulF(t0, t1, n, c[k]);
+        for (i64 i = 0; i < n; ++i) { h0[i] += t0[i]; h1[i] += t1[i]; }
+    }
+    addP(h0, n, c[0]);
+    for (int k = 2; k <= d; ++k) { free(p0[k]); free(p1[k]); }
+    free(t0); free(t1);
+}
+
 enum { ACT_GELU = 0, ACT_SILU = 1, ACT_SIGMOID = 2 };
 enum { FORM_POLY_X = 0, FORM_POLY_ABS = 1, FORM_RELU = 2, FORM_ERF = 3 };
 
@@ -502,8 +572,9 @@ enum { FORM_POLY_X = 0, FORM_POLY_ABS = 1, FORM_RELU = 2, FORM_ERF = 3 };
 /*   l1 = LTZ(x + B), l2 = LTZ(x - B)   (two steps, listed order)              */
 /*   out = BM(inner, l2 - l1) + tail,  tail = BM(x, NOT(l2)) (GELU/SiLU) or    */
 /*                                     pmulI(NOT(l2), 2^16) (Sigmoid, local)   */
+/* basis: 0 HORNER, 1 POWER (x- and |x|-forms, degree <= 4) */
 void orc_act(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n, i64 off,
-             int act, int form, int degree, double B, const double* coeffs, int erf_terms, int w)
+             int act, int form, int degree, double B, const double* coeffs, int erf_terms, int w, int basis)
 {
     u64 U = (u64)off;
     u64 *l0 = A(n), *l1 = A(n), *m0 = A(n), *m1 = A(n), *h0 = A(n), *h1 = A(n), *t0 = A(n), *t1 = A(n);
@@ -531,13 +602,15 @@ void orc_act(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1, i64 n
         addP(t0, n, -B);
         LTZ(ctx, n, U, w, t0, t1, m0, m1);               /* l2 = [x < B]  */
         if (form == FORM_POLY_X) {
-            HORNER(ctx, n, U, x0, x1, coeffs, degree, h0, h1);
+            if (basis) POWER(ctx, n, U, x0, x1, coeffs, degree, h0, h1);
+            else HORNER(ctx, n, U, x0, x1, coeffs, degree, h0, h1);
         } else if (form == FORM_POLY_ABS) {
             /* |x| = BM(x, 1 - 2s) ; h = 0.5 x + P(|x|) (BOLT structure) */
             u64 *sg0 = A(n), *sg1 = A(n), *ax0 = A(n), *ax1 = A(n);
             for (i64 i = 0; i < n; ++i) { sg0[i] = 1 - 2 * s0[i]; sg1[i] = (u64)0 - 2 * s1[i]; }
             BM(ctx, n, U, x0, x1, sg0, sg1, ax0, ax1);
-            HORNER(ctx, n, U, ax0, ax1, coeffs, degree, h0, h1);
+            if (basis) POWER(ctx, n, U, ax0, ax1, coeffs, degree, h0, h1);
+            else HORNER(ctx, n, U, ax0, ax1, coeffs, degree, h0, h1);
             memcpy(t0, x0, sizeof(u64) * (size_t)n); memcpy(t1, x1, sizeof(u64) * (size_t)n);
             pmulF(t0, t1, n, 0.5);
             for (i64 i = 0; i < n; ++i) { h0[i] += t0[i]; h1[i] += t1[i]; }
@@ -665,7 +738,7 @@ void orc_maxpool2d(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
 void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
                  i64 rows, i64 cols, i64 row_off, int w,
                  int exp_t, int exp_clamp, int exp_w, int exp_sq,
-                 int rc_iters, int rc_t, int rc_clamp, int rc_w, int rc_sq)
+                 int rc_iters, int rc_t, int rc_clamp, int rc_w, int rc_sq, int bcast)
 {
     i64 n = rows * cols;
     u64 *mx0 = A(rows), *mx1 = A(rows), *e0 = A(n), *e1 = A(n), *S0 = A(rows), *S1 = A(rows);
@@ -685,9 +758,14 @@ void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
         S0[r] = a; S1[r] = b;
     }
     RECIP(ctx, rows, (u64)row_off, rc_iters, rc_t, rc_clamp, rc_w, rc_sq, S0, S1, r0, r1);
-    for (i64 r = 0; r < rows; ++r)
-        for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
-    MT(ctx, n, Ue, e0, e1, b0, b1, z0, z1);
+    if (bcast) {                                      /* NEXT #2: one opening of r per row */
+        BMB(ctx, rows, cols, Ue, (u64)row_off, e0, e1, r0, r1, z0, z1);
+        for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], FRAC); z1[i] = shr(z1[i], FRAC); }
+    } else {
+        for (i64 r = 0; r < rows; ++r)
+            for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
+        MT(ctx, n, Ue, e0, e1, b0, b1, z0, z1);
+    }
     free(mx0); free(mx1); free(e0); free(e1); free(S0); free(S1); free(r0); free(r1); free(b0); free(b1);
 }
 
@@ -702,7 +780,7 @@ void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
 /* ------------------------------------------------------------------------ */
 void orc_layernorm(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
                    i64 rows, i64 cols, i64 row_off, double eps, int mean_mode,
-                   int rs_iters, int rs_t, int rs_clamp, int rs_w, int rs_sq)
+                   int rs_iters, int rs_t, int rs_clamp, int rs_w, int rs_sq, int bcast)
 {
     i64 n = rows * cols;
     u64 *mu0 = A(rows), *mu1 = A(rows), *c0 = A(n), *c1 = A(n), *q0 = A(n), *q1 = A(n);
@@ -731,9 +809,14 @@ void orc_layernorm(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
     else divP(v0, v1, rows, cols);
     addP(v0, rows, eps);
     RSQRT(ctx, rows, (u64)row_off, rs_iters, rs_t, rs_clamp, rs_w, rs_sq, v0, v1, r0, r1);
-    for (i64 r = 0; r < rows; ++r)
-        for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
-    MT(ctx, n, Ue, c0, c1, b0, b1, z0, z1);
+    if (bcast) {                                      /* NEXT #2: one opening of r per row */
+        BMB(ctx, rows, cols, Ue, (u64)row_off, c0, c1, r0, r1, z0, z1);
+        for (i64 i = 0; i < n; ++i) { z0[i] = shr(z0[i], FRAC); z1[i] = shr(z1[i], FRAC); }
+    } else {
+        for (i64 r = 0; r < rows; ++r)
+            for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
+        MT(ctx, n, Ue, c0, c1, b0, b1, z0, z1);
+    }
     free(mu0); free(mu1); free(c0); free(c1); free(q0); free(q1);
     free(v0); free(v1); free(r0); free(r1); free(b0); free(b1);
 }
