@@ -155,6 +155,12 @@ mpc_status mpc_mul(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z, int64
 /* S4' square with a square-pair triple (NEXT #2): z = x*x mod 2^64, then
  * per-share shift by trunc_bits (0 or 16).  1 step, 1 round, 8 B/elem/party. */
 mpc_status mpc_square(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_t off, int trunc_bits);
+/* S4'' broadcast multiply (NEXT #2 "broadcast triple"): x is rows x cols
+ * (row-major), y is rows; z[r*cols+j] = x[r*cols+j] * y[r] mod 2^64, then per-share shift by
+ * trunc_bits (0 or 16).  One mask per row for y: 1 step, 1 round, 8 B/elem + 8 B/row per
+ * party.  off = global element index of x[0] (multiple of 2), row_off = global row of y[0]. */
+mpc_status mpc_mul_bcast(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z, int64_t rows,
+                         int64_t cols, int64_t off, int64_t row_off, int trunc_bits);
 /* S5 local truncation: z_i = (int64)x_i >> bits, bits in [0,63].
  * No step, no communication. */
 mpc_status mpc_trunc(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int bits);
@@ -189,9 +195,11 @@ mpc_status mpc_rsqrt(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64_
 typedef enum { MPC_FORM_POLY_X = 0, MPC_FORM_POLY_ABS = 1, MPC_FORM_RELU = 2, MPC_FORM_ERF = 3 } mpc_act_form;
 /* The segment table of S13: inside [-B, B) the value is
  * the form's polynomial, outside its asymptote.  coeffs: HOST array of degree+1
- * doubles, low -> high (POLY_X / POLY_ABS); erf_terms K in [2,12] for ERF. */
+ * doubles, low -> high (POLY_X / POLY_ABS); erf_terms K in [2,12] for ERF.
+ * basis: 0 Horner; 1 power basis (NEXT #2: v^2, then v^3 and v^4 in
+ * one round; POLY_X / POLY_ABS only) -- its own output shares, the same step count. */
 typedef struct {
-    int form; int degree; double B; const double* coeffs; int erf_terms; int window;
+    int form; int degree; double B; const double* coeffs; int erf_terms; int window; int basis;
 } mpc_act_p;
 /* S13 GELU: POLY_X steps 2+(d-1)+2, POLY_ABS 3+1+(d-1)+2, ERF 2+1+(K-2)+1+1+2,
  * RELU or degree 0: 2. */
@@ -215,12 +223,14 @@ mpc_status mpc_maxpool2d(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int N, int C,
                          int k, int stride, int pad, int64_t img_off, int window);
 
 /* ---- S14 / S15 ---------------------------------------------------------------------- */
-typedef struct { int window; mpc_exp_p exp; mpc_nr_p recip; } mpc_softmax_p;
+/* bcast: 0 the final e * r with per-element Beaver triples; 1 with the broadcast
+ * triple of mpc_mul_bcast (NEXT #2) -- its own output shares, same steps. */
+typedef struct { int window; mpc_exp_p exp; mpc_nr_p recip; int bcast; } mpc_softmax_p;
 /* S14 softmax over rows (P:604 footnote).  Steps: 2*levels(cols) + exp +
  * recip + 1.  The library allocates row scratch on the context's device. */
 mpc_status mpc_softmax(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols,
                        int64_t row_off, const mpc_softmax_p* p);
-typedef struct { double eps; int mean_mode; mpc_nr_p rsqrt; } mpc_ln_p;
+typedef struct { double eps; int mean_mode; mpc_nr_p rsqrt; int bcast; } mpc_ln_p;   /* bcast as softmax */
 /* S15 layernorm over rows, without the public affine.
  * mean_mode 0: x E(1/d) (SPEC); 1: per-share floor division by d (R25).
  * Steps 1 + rsqrt + 1. */

@@ -63,15 +63,16 @@ class NrP(ctypes.Structure):
 
 class ActP(ctypes.Structure):
     _fields_ = [("form", INT), ("degree", INT), ("B", ctypes.c_double),
-                ("coeffs", ctypes.POINTER(ctypes.c_double)), ("erf_terms", INT), ("window", INT)]
+                ("coeffs", ctypes.POINTER(ctypes.c_double)), ("erf_terms", INT), ("window", INT),
+                ("basis", INT)]
 
 
 class SoftmaxP(ctypes.Structure):
-    _fields_ = [("window", INT), ("exp", ExpP), ("recip", NrP)]
+    _fields_ = [("window", INT), ("exp", ExpP), ("recip", NrP), ("bcast", INT)]
 
 
 class LnP(ctypes.Structure):
-    _fields_ = [("eps", ctypes.c_double), ("mean_mode", INT), ("rsqrt", NrP)]
+    _fields_ = [("eps", ctypes.c_double), ("mean_mode", INT), ("rsqrt", NrP), ("bcast", INT)]
 
 
 C = ctypes.POINTER
@@ -97,6 +98,7 @@ _SIGS = {
     "mpc_open": [VP, Shares, i64, VP, VP, INT],
     "mpc_mul": [VP, Shares, Shares, Shares, i64, i64, INT],
     "mpc_square": [VP, Shares, Shares, i64, i64, INT],
+    "mpc_mul_bcast": [VP, Shares, Shares, Shares, i64, i64, i64, i64, INT],
     "mpc_trunc": [VP, Shares, Shares, i64, INT],
     "mpc_cmp": [VP, Shares, Shares, i64, i64, INT],
     "mpc_relu": [VP, Shares, Shares, i64, i64, INT],
@@ -130,19 +132,21 @@ def load_coeffs():
     return json.load(open(path))["fits"]
 
 
-def default_act(act="gelu", form="poly_x", degree=4, erf_terms=8, window=33, B=None, coeffs=None):
-    """Knob struct for S13 using fixtures/coeffs.json (SPEC S:239 least-squares fits)."""
+def default_act(act="gelu", form="poly_x", degree=4, erf_terms=8, window=33, B=None, coeffs=None, basis=0):
+    """Knob struct for S13 using fixtures/coeffs.json (SPEC S:239 least-squares fits).
+    basis: 0 Horner, 1 power basis (NEXT #2; x- and |x|-forms)."""
     if form == "erf":
         return dict(form="erf", degree=0, B=2.5 if B is None else B, coeffs=None, erf_terms=erf_terms,
-                    window=window)
+                    window=window, basis=basis)
     if form == "relu" or degree == 0:
-        return dict(form=form, degree=0, B=5.0 if B is None else B, coeffs=None, erf_terms=0, window=window)
+        return dict(form=form, degree=0, B=5.0 if B is None else B, coeffs=None, erf_terms=0, window=window,
+                    basis=basis)
     if coeffs is None:
         fit = [f for f in load_coeffs() if f["op"] == act and f["form"] == form and f.get("degree") == degree]
         if not fit:
             raise ValueError(f"no fitted coefficients for {act}/{form}/deg {degree}")
         coeffs, B = fit[0]["coefficients"], fit[0]["interval"][1]
-    return dict(form=form, degree=degree, B=B, coeffs=list(coeffs), erf_terms=0, window=window)
+    return dict(form=form, degree=degree, B=B, coeffs=list(coeffs), erf_terms=0, window=window, basis=basis)
 
 
 class MPCError(RuntimeError):
@@ -287,6 +291,14 @@ class Ctx:
         self._chk(_L.mpc_mul(self._h, _sh(x), _sh(y), _sh(z), n, off, trunc_bits), "mpc_mul")
         return z
 
+    def mul_bcast(self, x, y, rows, cols, off=0, row_off=0, trunc_bits=0, out=None):
+        """z[r, j] = x[r, j] * y[r] with the broadcast triple."""
+        z = out if out is not None else self._empty(rows * cols)
+        self._stream()
+        self._chk(_L.mpc_mul_bcast(self._h, _sh(x), _sh(y), _sh(z), rows, cols, off, row_off, trunc_bits),
+                  "mpc_mul_bcast")
+        return z
+
     def square(self, x, off=0, trunc_bits=0, out=None):
         n = x[0].numel() if x[0] is not None else x[1].numel()
         z = out if out is not None else self._empty(n)
@@ -332,7 +344,7 @@ class Ctx:
         arr = (ctypes.c_double * len(coeffs))(*coeffs) if coeffs else None
         p = ActP(FORM[k["form"]], int(k.get("degree", 0)), float(k.get("B", 5.0)),
                  ctypes.cast(arr, ctypes.POINTER(ctypes.c_double)) if arr is not None else None,
-                 int(k.get("erf_terms", 0)), int(k.get("window", 33)))
+                 int(k.get("erf_terms", 0)), int(k.get("window", 33)), int(k.get("basis", 0)))
         return self._un(fn, name, x, out, off, ctypes.byref(p))
 
     def gelu(self, x, off=0, out=None, **knobs):
@@ -361,17 +373,18 @@ class Ctx:
 
     def softmax(self, x, rows, cols, row_off=0, window=33, exp_t=8, exp_clamp=0, exp_window=33,
                 recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0, recip_square=0,
-                out=None):
+                bcast=0, out=None):
         p = SoftmaxP(window, ExpP(exp_t, int(exp_clamp), exp_window, int(exp_square)),
-                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))))
+                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))), int(bcast))
         z = out if out is not None else self._empty(rows * cols)
         self._stream()
         self._chk(_L.mpc_softmax(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)), "mpc_softmax")
         return z
 
     def layernorm(self, x, rows, cols, row_off=0, eps=1e-5, mean_mode=0, rsqrt_iters=3, rsqrt_t=8,
-                  rsqrt_clamp=0, rsqrt_window=33, rsqrt_square=0, out=None):
-        p = LnP(eps, mean_mode, NrP(rsqrt_iters, ExpP(rsqrt_t, int(rsqrt_clamp), rsqrt_window, int(rsqrt_square))))
+                  rsqrt_clamp=0, rsqrt_window=33, rsqrt_square=0, bcast=0, out=None):
+        p = LnP(eps, mean_mode, NrP(rsqrt_iters, ExpP(rsqrt_t, int(rsqrt_clamp), rsqrt_window, int(rsqrt_square))),
+                int(bcast))
         z = out if out is not None else self._empty(rows * cols)
         self._stream()
         self._chk(_L.mpc_layernorm(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)),

@@ -466,6 +466,38 @@ __device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g
     __syncthreads();
 }
 
+// out = MT(x, bcast r) over a tile of R rows x C with the BROADCAST triple (NEXT #2, DESIGN.md
+// 2.8): warp 0 opens f = r - b for the tile's 32 rows (lane <-> row, one round), the CTA then
+// forms the element products (e = x - a opened per element) on unit pairs.  val(e, row) yields
+// the element's share.  brs: 3 x 32 u64 of shared / per-CTA scratch (b0, b1, f per row).
+template <class P, class Val>
+__device__ __forceinline__ void tile_bcast_mul(P& pr, u32 s, int R, i64 C, u64 g0, const FastDiv& dC,
+                                               SP Rr, SO zt, u64* brs, Val val)
+{
+    using S = typename P::S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    if (warp == 0) {
+        const S y = lane < R ? pr.ld(Rr, lane) : pr.zero();
+        const BRow b = pr.bmb_row(g0 + (u64)lane, s, y);
+        brs[lane] = b.b0; brs[32 + lane] = b.b1; brs[64 + lane] = b.f;
+    }
+    __syncthreads();
+    const i64 ne = (i64)R * C;
+    const u64 ub = g0 * (u64)C;                         // even: g0 is a multiple of 32
+    for (i64 base = (i64)warp * 32; base < (ne + 1) / 2; base += (i64)NW * 32) {
+        const i64 e = 2 * (base + lane);
+        S xa = pr.zero(), xb = pr.zero();
+        int ra = 0, rb = 0;
+        if (e < ne) { ra = (int)fdiv((u32)e, dC); xa = val(e, ra); }
+        if (e + 1 < ne) { rb = (int)fdiv((u32)(e + 1), dC); xb = val(e + 1, rb); }
+        const BRow b0{brs[ra], brs[32 + ra], brs[64 + ra]}, b1{brs[rb], brs[32 + rb], brs[64 + rb]};
+        S za, zb;
+        pr.bmb2(ub + (u64)e, s, xa, xb, b0, b1, za, zb);
+        if (e < ne) pr.st(zt, e, pr.shr_(za, FRAC));
+        if (e + 1 < ne) pr.st(zt, e + 1, pr.shr_(zb, FRAC));
+    }
+}
+
 struct SoftmaxArgs {
     u32 s_max, s_exp, s_rec, s_mul;
     int w;
@@ -480,14 +512,15 @@ struct SoftmaxArgs {
     int use_smem;
     u64* escratch;          // per-CTA exp tile E (2 x 32 x cols), global (L2-resident)
     int cone;               // carry-cone LTZ in the max tree (NEXT #1)
+    int bcast;              // broadcast triple for the final e * r (NEXT #2)
 };
 
 // work tile (u64 words), HA = ceil(cols/2), HB = ceil(HA/2): A0 A1 (2 x 32HA), B0 B1 (2 x 32HB),
-// MX0 MX1 S0 S1 R0 R1 (6 x 32).  E lives in escratch.
+// MX0 MX1 S0 S1 R0 R1 (6 x 32), broadcast-triple rows b0 b1 f (3 x 32).  E lives in escratch.
 __host__ __device__ inline i64 softmax_work_u64(i64 cols)
 {
     const i64 HA = (cols + 1) / 2, HB = (HA + 1) / 2;
-    return 64 * HA + 64 * HB + 6 * 32;
+    return 64 * HA + 64 * HB + 9 * 32;
 }
 
 // LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33) --
@@ -598,7 +631,9 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         // 6. out = MT(e, r), element units
         const SP Rc{{RR.p[0], RR.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
-        if (!(MPC_SOFTMAX_SKIP & 8)) {
+        if (a.bcast) {
+            tile_bcast_mul(pr, a.s_mul, R, C, g0, dC, Rc, zt, X + 192, [&](i64 e, int) { return pr.ld(Ec, e); });
+        } else if (!(MPC_SOFTMAX_SKIP & 8)) {
             constexpr int V = decltype(pr)::kV;
             for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
                 u64 uv[V];
@@ -661,6 +696,47 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     }
     pa.done(pr);
 }
+
+// mpc_mul_bcast (NEXT #2): rows' masks and openings (warp <-> 32 rows), then the
+// element products on unit pairs (pairs driver) reading the row records.
+struct BmbRowsArgs { u32 s; SP y; i64 rows; u64 row_off; u64* br; };   // br: [3][rows]
+template <class PA>
+__global__ void __launch_bounds__(256, MPC_EW_MINB) k_bmb_rows(const __grid_constant__ PA pa, BmbRowsArgs a)
+{
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    const int lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+    const i64 ng = (a.rows + 31) >> 5;
+    for (i64 g = (i64)cta * NW + (threadIdx.x >> 5); g < ng; g += (i64)ncta * NW) {
+        const i64 r = g * 32 + lane;
+        const typename decltype(pr)::S y = r < a.rows ? pr.ld(a.y, r) : pr.zero();
+        const BRow b = pr.bmb_row(a.row_off + (u64)r, a.s, y);
+        u64* br = a.br + (pr.party() > 0 ? 3 * a.rows : 0);   // loopback: one record set per party
+        if (r < a.rows) { br[r] = b.b0; br[a.rows + r] = b.b1; br[2 * a.rows + r] = b.f; }
+    }
+    pa.done(pr);
+}
+struct BmbBody {
+    u32 s; SP x; SO z; i64 n; FastDiv dC; const u64* br; i64 rows; int tb;
+    template <int V, class P>
+    __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
+        using S = typename P::S;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const bool va = ok[v] && i0[v] >= 0, vb = ok[v] && i0[v] + 1 < n;
+            S xa = pr.zero(), xb = pr.zero();
+            i64 ra = 0, rb = 0;
+            if (va) { ra = fdiv((u32)i0[v], dC); xa = pr.ld(x, i0[v]); }
+            if (vb) { rb = fdiv((u32)(i0[v] + 1), dC); xb = pr.ld(x, i0[v] + 1); }
+            const u64* bp = br + (pr.party() > 0 ? 3 * rows : 0);
+            const BRow b0{bp[ra], bp[rows + ra], bp[2 * rows + ra]}, b1{bp[rb], bp[rows + rb], bp[2 * rows + rb]};
+            S za, zb;
+            pr.bmb2(u[v], s, xa, xb, b0, b1, za, zb);
+            if (va) pr.st(z, i0[v], pr.shr_(za, tb));
+            if (vb) pr.st(z, i0[v] + 1, pr.shr_(zb, tb));
+        }
+    }
+};
 
 // Short-row MAX_row (cols <= MAXS_COLS; MaxPool windows).  The same contract as k_max (R22:
 // half-split tree with the odd entry carried, LTZ at step s + 2 lv and the mux at s + 2 lv + 1,
@@ -786,13 +862,14 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_max_small(const __grid_con
 struct LnArgs {
     u32 s_sq, s_rs, s_mul; NrK rk; SP x; SO z; i64 rows, cols; u64 row_off;
     int mean_mode; u64 e_invd, e_eps;
+    int bcast;              // broadcast triple for the final c * r (NEXT #2)
 };
 
 // LAYERNORM: mu, c = x - mu, v = mean(MT(c,c)) + eps, r = RSQRT(v), out = MT(c, r)
 template <bool WIDE, class PA>
 __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln(const __grid_constant__ PA pa, LnArgs a)
 {
-    __shared__ u64 MU[2][32], V[2][32], RS[2][32];
+    __shared__ u64 MU[2][32], V[2][32], RS[2][32], BR[3 * 32];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     using S = typename decltype(pr)::S;
@@ -837,6 +914,10 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln(const __grid_co
         const u64 ub = g0 * (u64)C;            // even: g0 is a multiple of 32
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
         constexpr int V = decltype(pr)::kV;
+        if (a.bcast) {
+            tile_bcast_mul(pr, a.s_mul, R, C, g0, dC, RSc, zt, BR,
+                           [&](i64 e, int r) { return pr.sub(pr.ld(xt, e), pr.ld(MUc, r)); });
+        } else
         for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
             u64 uv[V];
             S ca[V], cb[V], ra[V], rb[V], za[V], zb[V];

@@ -157,6 +157,14 @@ static void acct_square(mpc_ctx* c, u64 n)
     c->st.bytes_per_party += 8 * n;
     c->st.rounds += 1;
 }
+// broadcast triple: 1.5 blocks per element + 2 per row; 8 B per element and per
+// row; the row openings and the element openings are separate rounds here
+static void acct_bcast(mpc_ctx* c, u64 n, u64 rows)
+{
+    c->last_philox += n + (n + 1) / 2 + 2 * rows;
+    c->st.bytes_per_party += 8 * n + 8 * rows;
+    c->st.rounds += 2;
+}
 static bool use_cone(const mpc_ctx* c, int w) { return c->circuit == 1 && w <= 33; }
 static void acct_ltz(mpc_ctx* c, u64 n, int w)
 {
@@ -794,6 +802,42 @@ mpc_status mpc_square(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t
     return MPC_OK;
 }
 
+// S4'' broadcast multiply (NEXT #2): row masks + openings, then element products
+mpc_status mpc_mul_bcast(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int64_t rows, int64_t cols,
+                         int64_t off, int64_t row_off, int tb)
+{
+    mpc_status st = begin(c, 1);
+    if (st) return st;
+    if (tb != 0 && tb != 16) return fail(c, MPC_ERR_RANGE, "trunc_bits must be 0 or 16");
+    if (rows < 0 || cols < 1 || off < 0 || row_off < 0 || rows * cols >= (1ll << 31))
+        return fail(c, MPC_ERR_INVALID, "mul_bcast: bad rows/cols/off (rows*cols < 2^31)");
+    if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "mul_bcast: null pointer");
+    const i64 n = rows * cols;
+    if (rows > 0) {
+        u64* br = (u64*)scratch(c, sizeof(u64) * 3 * (size_t)rows * (is_loop(c) ? 2 : 1));
+        if (!br) return fail(c, MPC_ERR_NOMEM, "mul_bcast scratch");
+        BmbRowsArgs ra{(u32)c->step, spv(c, y), rows, (u64)row_off, br};
+        const i64 nw = (rows + 31) / 32;
+        if (!is_pair(c)) {
+            rec_begin(c, "bcast_rows", (u64)rows);
+            k_bmb_rows<BothA><<<grid_for(c, nw * 32, TPB, 8), TPB, 0, c->stream>>>(BothA{c->K}, ra);
+            rec_end(c);
+            c->st.launches++;
+            st = cuda_check(c, "bcast_rows");
+        } else {
+            st = launch_pair_kernel(c, k_bmb_rows<PairA>, pair_ctas(c, k_bmb_rows<PairA>, 0, (nw * 32 + TPB - 1) / TPB),
+                                    0, "bcast_rows", ra);
+        }
+        if (st) return st;
+        st = launch_pairs(c, n, (u64)off, BmbBody{(u32)c->step, spv(c, x), sov(c, z), n, make_fastdiv((u32)cols),
+                                                  br, rows, tb}, "mul_bcast");
+        if (st) return st;
+        acct_bcast(c, (u64)n, (u64)rows);
+    }
+    finish(c, 1);
+    return MPC_OK;
+}
+
 static mpc_status cmp_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, int w, int relu)
 {
     mpc_status st = begin(c, relu ? 2 : 1);
@@ -888,13 +932,15 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
     if (p->form == MPC_FORM_POLY_ABS && act == 2) return fail(c, MPC_ERR_RANGE, "sigmoid has no |x|-form (R30)");
     if ((p->form == MPC_FORM_POLY_X || p->form == MPC_FORM_POLY_ABS) && p->degree > 0 && !p->coeffs)
         return fail(c, MPC_ERR_INVALID, "coeffs");
+    if (p->basis != 0 && p->basis != 1) return fail(c, MPC_ERR_RANGE, "basis must be 0 (Horner) or 1 (power)");
+    if (p->basis == 1 && p->form == MPC_FORM_ERF) return fail(c, MPC_ERR_RANGE, "power basis: x- and |x|-forms only");
     const u64 steps = act_steps(act, p);
     mpc_status st = begin(c, steps);
     if (st) return st;
     if (bad_sh(c, x) || bad_sh(c, z) || n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "act args (off % 32)");
     ActK k;
     memset(&k, 0, sizeof k);
-    k.act = act; k.form = p->form; k.w = p->window;
+    k.act = act; k.form = p->form; k.w = p->window; k.basis = p->form == MPC_FORM_ERF ? 0 : p->basis;
     k.e_B = E(p->B); k.e_mB = E(-p->B); k.e_half = E(0.5); k.e_one = E(1.0);
     k.e_isqrt2 = E(1.0 / sqrt(2.0)); k.e_2sqrtpi = E(2.0 / sqrt(M_PI));
     if (p->form == MPC_FORM_ERF) {
@@ -1033,6 +1079,7 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
         a.x = spv(c, x); a.z = sov(c, z);
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
         a.cone = use_cone(c, p->window) ? 1 : 0;
+        a.bcast = p->bcast ? 1 : 0;
         const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
         const i64 wk = softmax_work_u64(cols), ek = 64 * cols;
         st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax")
@@ -1044,7 +1091,7 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
         acct_exp(c, (u64)n, &p->exp);
         acct_exp(c, (u64)rows, &p->recip.exp);
         for (int i = 0; i < 2 * p->recip.iters; ++i) acct_beaver(c, (u64)rows);
-        acct_beaver(c, (u64)n);
+        if (p->bcast) acct_bcast(c, (u64)n, (u64)rows); else acct_beaver(c, (u64)n);
     }
     finish(c, steps);
     return MPC_OK;
@@ -1069,6 +1116,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
         a.x = spv(c, x); a.z = sov(c, z);
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
         a.mean_mode = p->mean_mode; a.e_invd = E(1.0 / (double)cols); a.e_eps = E(p->eps);
+        a.bcast = p->bcast ? 1 : 0;
         const i64 ntiles = (rows + 31) / 32;
         const bool wide = p->rsqrt.exp.window > 33;
         if (!is_pair(c)) {
@@ -1089,7 +1137,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
         acct_beaver(c, (u64)n);
         acct_exp(c, (u64)rows, &p->rsqrt.exp);
         for (int i = 0; i < 3 * p->rsqrt.iters; ++i) acct_beaver(c, (u64)rows);
-        acct_beaver(c, (u64)n);
+        if (p->bcast) acct_bcast(c, (u64)n, (u64)rows); else acct_beaver(c, (u64)n);
     }
     finish(c, steps);
     return MPC_OK;

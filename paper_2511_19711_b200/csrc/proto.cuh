@@ -64,9 +64,30 @@ struct BothP {
     }
     template <bool WIDE>
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(*Kp, q, s, w, x, lane); }
+#ifndef MPC_BOTH_LTZ_O_INLINE
+#define MPC_BOTH_LTZ_O_INLINE 1
+#endif
     template <bool WIDE>
+#if MPC_BOTH_LTZ_O_INLINE
     __device__ __forceinline__ S ltz_o(u64 q, u32 s, int w, S x, int lane) { return ltz<WIDE>(q, s, w, x, lane); }
+#else
+    __device__ __noinline__ S ltz_o(u64 q, u32 s, int w, S x, int lane) { return ltz<WIDE>(q, s, w, x, lane); }
+#endif
     __device__ __forceinline__ S sq(u64 u, u32 s, S y) { return mpc::sq1(*Kp, u, s, y); }
+    // two Beaver steps of one unit (power basis: v^3 at sA, v^4 at sB -- one round in PAIR)
+    __device__ __forceinline__ void bm_dual(u64 u, u32 sA, S xA, S yA, u32 sB, S xB, S yB, S& zA, S& zB) {
+        zA = mpc::bm(*Kp, u, sA, xA, yA); zB = mpc::bm(*Kp, u, sB, xB, yB);
+    }
+    __device__ __forceinline__ void bm2_dual(u64 u, u32 sA, S xA0, S yA0, S xA1, S yA1, u32 sB, S xB0, S yB0, S xB1,
+                                             S yB1, S& zA0, S& zA1, S& zB0, S& zB1) {
+        mpc::bm2(*Kp, u, sA, xA0, yA0, xA1, yA1, zA0, zA1);
+        mpc::bm2(*Kp, u, sB, xB0, yB0, xB1, yB1, zB0, zB1);
+    }
+    // broadcast triple: row mask + opening, then the element products
+    __device__ __forceinline__ BRow bmb_row(u64 r, u32 s, S y) { return mpc::bmb_row(*Kp, r, s, y); }
+    __device__ __forceinline__ void bmb2(u64 u, u32 s, S x0, S x1, const BRow& r0, const BRow& r1, S& z0, S& z1) {
+        mpc::bmb2(*Kp, u, s, x0, x1, r0, r1, z0, z1);
+    }
     template <int G>
     __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G>& sm) {
         ltz_cone_both<G>(*Kp, q0, s, w, x, z, lane, sm);
@@ -97,12 +118,13 @@ __device__ __forceinline__ u64 floordiv_share(u64 a, i64 d)
 __device__ __forceinline__ Sh BothP::divp(Sh a, i64 d) const { return {floordiv_share(a.s0, d), floordiv_share(a.s1, d)}; }
 
 // ================================================================================ PAIR ====
-constexpr int XW = 4;                // u64 words per lane per round (max)
-constexpr int XSLOT_RX = 2 * 32 * XW * 2; // u64 per warp slot: [parity][lane][word][payload-half + tag]
+constexpr int XW = 8;                // u64 words per lane per round (max)
+constexpr int XSLOT_RX = 2 * XW * 32 * 2; // u64 per warp slot: [parity][word][lane][payload-half + tag]
+                                          // (word-major: one put/get of word k by a warp is 512 contiguous B)
 
 // Device view of one party's exchange memory.
 struct XMem {
-    u64* rx;          // [slots][2][32][XW]  receive buffers (peer writes)
+    u64* rx;          // [slots][2][XW][32] receive buffers (peer writes)
     u64* flag;        // [slots][4]          my flags (peer writes word 0)
     u64* round;       // [slots]             persistent round counters (local only)
     int* err;         // error word (1 = exchange timeout)
@@ -179,7 +201,7 @@ struct PairP {
     // barriers, and no L1 invalidation.  Both parties run the same put/get pattern.
     __device__ __forceinline__ void put(int lane, int k, u64 v) {
         const u64 tag = (rnd + 1) << 32;
-        u64* d = prx + (((rnd + 1) & 1) * (32 * XW) + lane * XW + k) * 2;
+        u64* d = prx + ((((rnd + 1) & 1) * XW + k) * 32 + lane) * 2;
         const u64 lo = (v & 0xffffffffull) | tag, hi = (v >> 32) | tag;
         asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" :: "l"(d), "l"(lo), "l"(hi) : "memory");
     }
@@ -188,7 +210,7 @@ struct PairP {
         ++rnd;                                   // the round now being received
     }
     __device__ __forceinline__ u64 get(int lane, int k) {
-        const u64* sp = rx + ((rnd & 1) * (32 * XW) + lane * XW + k) * 2;
+        const u64* sp = rx + (((rnd & 1) * XW + k) * 32 + lane) * 2;
         const u64 want = rnd & 0xffffffffull;
         u64 lo, hi;
         asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
@@ -265,6 +287,70 @@ struct PairP {
         exch(lane);
         z0 = bm_finish(a0, b0, c0, (x0 - a0) + get(lane, 0), (y0 - b0) + get(lane, 1));
         z1 = bm_finish(a1, b1, c1, (x1 - a1) + get(lane, 2), (y1 - b1) + get(lane, 3));
+    }
+
+    // two Beaver steps of one unit / unit pair in ONE round (power basis)
+    __device__ __forceinline__ void bm_dual(u64 u, u32 sA, S xA, S yA, u32 sB, S xB, S yB, S& zA, S& zB) {
+        const int lane = threadIdx.x & 31;
+        u64 aA, bA, cA, aB, bB, cB;
+        triple(u, sA, beaver_c0(*Kp, u, sA), aA, bA, cA);
+        triple(u, sB, beaver_c0(*Kp, u, sB), aB, bB, cB);
+        put(lane, 0, xA - aA); put(lane, 1, yA - bA); put(lane, 2, xB - aB); put(lane, 3, yB - bB);
+        exch(lane);
+        zA = bm_finish(aA, bA, cA, (xA - aA) + get(lane, 0), (yA - bA) + get(lane, 1));
+        zB = bm_finish(aB, bB, cB, (xB - aB) + get(lane, 2), (yB - bB) + get(lane, 3));
+    }
+    __device__ __forceinline__ void bm2_dual(u64 u, u32 sA, S xA0, S yA0, S xA1, S yA1, u32 sB, S xB0, S yB0, S xB1,
+                                             S yB1, S& zA0, S& zA1, S& zB0, S& zB1) {
+        static_assert(8 <= XW, "exchange width");
+        const int lane = threadIdx.x & 31;
+        const uint4 CA = prg(Kp->k0, u >> 1, sA, 1), CB = prg(Kp->k0, u >> 1, sB, 1);
+        u64 a[4], b[4], c[4];
+        triple(u, sA, w64(CA.x, CA.y), a[0], b[0], c[0]);
+        triple(u + 1, sA, w64(CA.z, CA.w), a[1], b[1], c[1]);
+        triple(u, sB, w64(CB.x, CB.y), a[2], b[2], c[2]);
+        triple(u + 1, sB, w64(CB.z, CB.w), a[3], b[3], c[3]);
+        const S xs[4] = {xA0, xA1, xB0, xB1}, ys[4] = {yA0, yA1, yB0, yB1};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { put(lane, 2 * k, xs[k] - a[k]); put(lane, 2 * k + 1, ys[k] - b[k]); }
+        exch(lane);
+        S zs[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            zs[k] = bm_finish(a[k], b[k], c[k], (xs[k] - a[k]) + get(lane, 2 * k), (ys[k] - b[k]) + get(lane, 2 * k + 1));
+        zA0 = zs[0]; zA1 = zs[1]; zB0 = zs[2]; zB1 = zs[3];
+    }
+
+    // ---- broadcast triple (NEXT #2): f opened once per row, e per element ----
+    __device__ __forceinline__ BRow bmb_row(u64 r, u32 s, S y) {
+        const int lane = threadIdx.x & 31;
+        const uint4 B0 = prg(Kp->k0, r, s, 6);
+        BRow R;
+        R.b0 = w64(B0.x, B0.y); R.b1 = 0;
+        if (pty == 1) { const uint4 B1 = prg(Kp->k1, r, s, 6); R.b1 = w64(B1.x, B1.y); }
+        const u64 m = y - (pty == 0 ? R.b0 : R.b1);
+        put(lane, 0, m);
+        exch(lane);
+        R.f = m + get(lane, 0);
+        return R;
+    }
+    __device__ __forceinline__ void bmb2(u64 u, u32 s, S x0, S x1, const BRow& r0, const BRow& r1, S& z0, S& z1) {
+        const int lane = threadIdx.x & 31;
+        const uint4 Au = prg(Kp->k0, u, s, 4), Av = prg(Kp->k0, u + 1, s, 4);
+        u64 au = w64(Au.x, Au.y), cu = w64(Au.z, Au.w), av = w64(Av.x, Av.y), cv = w64(Av.z, Av.w);
+        if (pty == 1) {                                  // party 1: own a1, dealer's c1
+            const uint4 A1 = prg(Kp->k1, u >> 1, s, 5);
+            const u64 a1u = w64(A1.x, A1.y), a1v = w64(A1.z, A1.w);
+            cu = (au + a1u) * (r0.b0 + r0.b1) - cu;
+            cv = (av + a1v) * (r1.b0 + r1.b1) - cv;
+            au = a1u; av = a1v;
+        }
+        put(lane, 0, x0 - au); put(lane, 1, x1 - av);
+        exch(lane);
+        const u64 eu = (x0 - au) + get(lane, 0), ev = (x1 - av) + get(lane, 1);
+        const u64 bu = pty == 0 ? r0.b0 : r0.b1, bv = pty == 0 ? r1.b0 : r1.b1;
+        z0 = cu + eu * bu + r0.f * au + (pty == 0 ? eu * r0.f : 0ull);
+        z1 = cv + ev * bv + r1.f * av + (pty == 0 ? ev * r1.f : 0ull);
     }
 
     // ---- squares with square-pair triples (NEXT #2): one word per element per round ----

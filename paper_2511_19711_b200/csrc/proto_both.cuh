@@ -80,6 +80,35 @@ __device__ __forceinline__ void sq2(const Keys& K, u64 u, u32 s, Sh y0, Sh y1, S
     z1 = sq_with_a1(K, u + 1, s, y1, w64(A1.z, A1.w));
 }
 
+// Broadcast triple: z = x * y_row with ONE mask per row.
+// Row part: b0 = PRG(K0,r,s,6)[0..1], b1 = PRG(K1,r,s,6)[0..1], f = open(y - b).
+// Element part: (a0,c0) = PRG(K0,u,s,4); a1 = half (u&1) of PRG(K1,u>>1,s,5);
+// c1 = (a0+a1)(b0+b1) - c0 (dealer -> party 1); e = open(x - a);
+// z0 = c0 + e b0 + f a0 + e f; z1 = c1 + e b1 + f a1.
+struct BRow { u64 b0, b1, f; };   // PAIR: party 0 holds b0; party 1 b1 and (as dealer) b0
+__device__ __forceinline__ BRow bmb_row(const Keys& K, u64 r, u32 s, Sh y)
+{
+    const uint4 B0 = prg(K.k0, r, s, 6), B1 = prg(K.k1, r, s, 6);
+    const u64 b0 = w64(B0.x, B0.y), b1 = w64(B1.x, B1.y);
+    return {b0, b1, (y.s0 - b0) + (y.s1 - b1)};
+}
+__device__ __forceinline__ Sh bmb_elem(const Keys& K, u64 u, u32 s, Sh x, const BRow& r, u64 a1)
+{
+    const uint4 A0 = prg(K.k0, u, s, 4);
+    const u64 a0 = w64(A0.x, A0.y), c0 = w64(A0.z, A0.w);
+    const u64 c1 = (a0 + a1) * (r.b0 + r.b1) - c0;     // dealer correction -> party 1
+    const u64 e = (x.s0 - a0) + (x.s1 - a1);           // open(x - a)
+    return {c0 + e * r.b0 + r.f * a0 + e * r.f, c1 + e * r.b1 + r.f * a1};
+}
+// unit pair (u even, u+1): one K1 block serves both a1 halves (1.5 blocks per element)
+__device__ __forceinline__ void bmb2(const Keys& K, u64 u, u32 s, Sh x0, Sh x1, const BRow& r0, const BRow& r1,
+                                     Sh& z0, Sh& z1)
+{
+    const uint4 A1 = prg(K.k1, u >> 1, s, 5);
+    z0 = bmb_elem(K, u, s, x0, r0, w64(A1.x, A1.y));
+    z1 = bmb_elem(K, u + 1, s, x1, r1, w64(A1.z, A1.w));
+}
+
 // AND on XOR-shared 32-bit plane words with triple (a0,b0,c0 | a1,b1).
 __device__ __forceinline__ void and_both(u32 x0, u32 x1, u32 y0, u32 y1,
                                          u32 a0, u32 b0, u32 c0, u32 a1, u32 b1,

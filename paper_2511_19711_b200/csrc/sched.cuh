@@ -16,6 +16,7 @@ struct ActK {
     int form;         // 0 poly_x, 1 poly_abs, 2 relu, 3 erf
     int deg;          // polynomial degree (HORNER degree for erf = K-1)
     int w;
+    int basis;        // 0 Horner, 1 power basis (NEXT #2)
     u64 e_B, e_mB, e_half, e_one, e_isqrt2, e_2sqrtpi;
     u64 c[MAX_COEF];  // E(c_k) (poly) or E(a_k) (erf series)
 };
@@ -241,6 +242,54 @@ __device__ __forceinline__ typename P::S horner(P& pr, u64 u, u32 s, const u64* 
     return h;
 }
 
+// ---- POWER(v; c_0..c_d), 1 <= d <= 4 (NEXT #2): v2 = MT(v,v) at s; v3 = MT(v2,v)
+// at s+1 and v4 = MT(v2,v2) at s+2 in ONE exchange; h = addP(sum_k pmulF(v^k, c_k), c_0).
+template <class P>
+__device__ __forceinline__ typename P::S poly_power(P& pr, u64 u, u32 s, const u64* c, int d, typename P::S v)
+{
+    using S = typename P::S;
+    S h = pr.mulf(v, c[1]);
+    if (d >= 2) {
+        const S v2 = pr.shr_(pr.bm(u, s, v, v), FRAC);
+        h = pr.add(h, pr.mulf(v2, c[2]));
+        if (d == 3) {
+            h = pr.add(h, pr.mulf(pr.shr_(pr.bm(u, s + 1, v2, v), FRAC), c[3]));
+        } else if (d >= 4) {
+            S v3, v4;
+            pr.bm_dual(u, s + 1, v2, v, s + 2, v2, v2, v3, v4);
+            h = pr.add(h, pr.add(pr.mulf(pr.shr_(v3, FRAC), c[3]), pr.mulf(pr.shr_(v4, FRAC), c[4])));
+        }
+    }
+    return pr.addp(h, c[0]);
+}
+template <class P>
+__device__ __forceinline__ void poly_power2(P& pr, u64 u, u32 s, const u64* c, int d, typename P::S v0,
+                                            typename P::S v1, typename P::S& h0, typename P::S& h1)
+{
+    using S = typename P::S;
+    h0 = pr.mulf(v0, c[1]);
+    h1 = pr.mulf(v1, c[1]);
+    if (d >= 2) {
+        S a, b;
+        pr.bm2(u, s, v0, v0, v1, v1, a, b);
+        const S q0 = pr.shr_(a, FRAC), q1 = pr.shr_(b, FRAC);
+        h0 = pr.add(h0, pr.mulf(q0, c[2]));
+        h1 = pr.add(h1, pr.mulf(q1, c[2]));
+        if (d == 3) {
+            pr.bm2(u, s + 1, q0, v0, q1, v1, a, b);
+            h0 = pr.add(h0, pr.mulf(pr.shr_(a, FRAC), c[3]));
+            h1 = pr.add(h1, pr.mulf(pr.shr_(b, FRAC), c[3]));
+        } else if (d >= 4) {
+            S t0, t1, w0, w1;
+            pr.bm2_dual(u, s + 1, q0, v0, q1, v1, s + 2, q0, q0, q1, q1, t0, t1, w0, w1);
+            h0 = pr.add(h0, pr.add(pr.mulf(pr.shr_(t0, FRAC), c[3]), pr.mulf(pr.shr_(w0, FRAC), c[4])));
+            h1 = pr.add(h1, pr.add(pr.mulf(pr.shr_(t1, FRAC), c[3]), pr.mulf(pr.shr_(w1, FRAC), c[4])));
+        }
+    }
+    h0 = pr.addp(h0, c[0]);
+    h1 = pr.addp(h1, c[0]);
+}
+
 template <class P>
 __device__ __forceinline__ typename P::S act_tail(P& pr, u64 u, u32 s, const ActK& p, typename P::S x,
                                                   typename P::S sgn, typename P::S l1, typename P::S l2);
@@ -271,12 +320,12 @@ __device__ __forceinline__ typename P::S act_tail(P& pr, u64 u, u32 s, const Act
     using S = typename P::S;
     S h;
     if (p.form == 0) {
-        h = horner(pr, u, s, p.c, p.deg, x);
+        h = p.basis ? poly_power(pr, u, s, p.c, p.deg, x) : horner(pr, u, s, p.c, p.deg, x);
         s += p.deg - 1;
     } else if (p.form == 1) {
         const S ax = pr.bm(u, s, x, pr.pm1(sgn));
         ++s;
-        h = pr.add(pr.mulf(x, p.e_half), horner(pr, u, s, p.c, p.deg, ax));
+        h = pr.add(pr.mulf(x, p.e_half), p.basis ? poly_power(pr, u, s, p.c, p.deg, ax) : horner(pr, u, s, p.c, p.deg, ax));
         s += p.deg - 1;
     } else {
         const S z = pr.mulf(x, p.e_isqrt2);
@@ -320,13 +369,15 @@ __device__ __forceinline__ void act_tail2(P& pr, u64 u, u32 s, const ActK& p, ty
     using S = typename P::S;
     S h0, h1;
     if (p.form == 0) {
-        horner2(pr, u, s, p.c, p.deg, x0, x1, h0, h1);
+        if (p.basis) poly_power2(pr, u, s, p.c, p.deg, x0, x1, h0, h1);
+        else horner2(pr, u, s, p.c, p.deg, x0, x1, h0, h1);
         s += p.deg - 1;
     } else if (p.form == 1) {
         S ax0, ax1, t0, t1;
         pr.bm2(u, s, x0, pr.pm1(sg0), x1, pr.pm1(sg1), ax0, ax1);
         ++s;
-        horner2(pr, u, s, p.c, p.deg, ax0, ax1, t0, t1);
+        if (p.basis) poly_power2(pr, u, s, p.c, p.deg, ax0, ax1, t0, t1);
+        else horner2(pr, u, s, p.c, p.deg, ax0, ax1, t0, t1);
         h0 = pr.add(pr.mulf(x0, p.e_half), t0);
         h1 = pr.add(pr.mulf(x1, p.e_half), t1);
         s += p.deg - 1;
