@@ -331,6 +331,14 @@ def time_per_op(job, m, ctx, flush, args):
     out["relu"] = _op_line(job, ctx, lambda: ctx.relu(r, off=k * n4, out=z), n4, flush, args,
                            "cfg4: ResNet-50 first ReLU, 8 images x 64 x 112 x 112, window 33")
     del r, z
+    Np, Cp, Hp, Wp = 8, 64, 112, 112                  # one pair's 8-image shard of the MaxPool input
+    mp = job.share(ctx, workloads.maxpool_inputs((Np, Cp, Hp, Wp)), k * Np * Cp * Hp * Wp)
+    no = Np * Cp * 56 * 56
+    z = ctx._empty(no)
+    out["maxpool"] = _op_line(job, ctx, lambda: ctx.maxpool2d(mp, Np, Cp, Hp, Wp, 3, 2, 1, img_off=k * Np, out=z),
+                              no, flush, args, "cfg4: ResNet-50 MaxPool 3x3/2 pad 1, 8 x 64 x 112^2 -> 56^2 "
+                              "(elements = outputs, 8 comparisons each)")
+    del mp, z
     rows5, cols5 = workloads.SHAPES["cfg5_ln"]
     ln = job.share(ctx, workloads.layernorm_inputs(rows5, cols5), k * rows5 * cols5)
     z = ctx._empty(rows5 * cols5)
@@ -347,6 +355,11 @@ def time_per_op(job, m, ctx, flush, args):
     # bit-identical to the Kogge-Stone contract's, square triples change the shares)
     x2 = job.share(ctx, workloads.softmax_inputs(*workloads.SHAPES["cfg2_softmax"]), k * 12288 * 128)
     z = ctx._empty(12288 * 128)
+    out["softmax_clamp"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_clamp=1,
+                                                                  out=z), 12288 * 128, flush, args,
+                                    "cfg2 softmax with exp t=8+clamp (max-accuracy knob)")
+    out["softmax_bcast"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, bcast=1, out=z),
+                                    12288 * 128, flush, args, "cfg2 softmax, broadcast triple for e*r (NEXT #2)")
     out["softmax_square"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1,
                                                                    recip_square=1, out=z), 12288 * 128, flush, args,
                                      "cfg2 softmax with square-pair triples in every exp squaring (NEXT #2)")
@@ -356,11 +369,18 @@ def time_per_op(job, m, ctx, flush, args):
     out["softmax_cone_square"] = _op_line(
         job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1, recip_square=1, out=z),
         12288 * 128, flush, args, "cfg2 softmax, carry-cone LTZ + square-pair triples (NEXT #1 + #2)")
+    out["softmax_next_all"] = _op_line(
+        job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1, recip_square=1, bcast=1,
+                                      out=z),
+        12288 * 128, flush, args, "cfg2 softmax, carry cone + square-pair triples + broadcast triple (NEXT #1 + #2)")
     del x2, z
     g = job.share(ctx, workloads.normal_inputs(n3, 3), k * n3)
     z = ctx._empty(n3)
     out["gelu_cone"] = _op_line(job, ctx, lambda: ctx.gelu(g, off=k * n3, form="poly_abs", degree=4, out=z), n3,
                                 flush, args, "cfg3 GELU |x|-form deg 4, carry-cone LTZ (NEXT #1)")
+    out["gelu_cone_power"] = _op_line(
+        job, ctx, lambda: ctx.gelu(g, off=k * n3, form="poly_abs", degree=4, basis=1, out=z), n3, flush, args,
+        "cfg3 GELU |x|-form deg 4, carry-cone LTZ + power basis (NEXT #1 + #2)")
     del g, z
     r = job.share(ctx, workloads.relu_inputs(n4), k * n4)
     z = ctx._empty(n4)

@@ -870,11 +870,13 @@ mpc_status mpc_exp(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t of
     const ExpK k = mk_exp(p);
     if (p->clamp) {
         if (off & 31) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
-        // clamp head (LTZ group layout, steps s, s+1) into z, then the t squarings in the pair
-        // layout in place (steps s+2 ..): the same units and output bits as one fused pass
-        st = p->window > 33 ? launch_groups(c, n, (u64)off, ExpGroupBody<true>{(u32)c->step, k, spv(c, x), sov(c, z), 1}, "exp_clamp")
-                            : launch_groups(c, n, (u64)off, ExpGroupBody<false>{(u32)c->step, k, spv(c, x), sov(c, z), 1}, "exp_clamp");
-        if (!st && k.t > 0) st = launch_pairs(c, n, (u64)off, ExpPairBody{(u32)c->step + 2u, k, spv(c, z), sov(c, z), n, 1}, "exp");
+        // large n: the clamp head (LTZ group layout, steps s, s+1) into z, then the t squarings in
+        // the pair layout in place (steps s+2 ..) -- the same units and output bits as one fused
+        // pass, 5 % faster at 4M; small n (latency-bound, cfg1): one fused launch
+        const int head = n >= (1 << 16) ? 1 : 0;
+        st = p->window > 33 ? launch_groups(c, n, (u64)off, ExpGroupBody<true>{(u32)c->step, k, spv(c, x), sov(c, z), head}, "exp_clamp")
+                            : launch_groups(c, n, (u64)off, ExpGroupBody<false>{(u32)c->step, k, spv(c, x), sov(c, z), head}, "exp_clamp");
+        if (!st && head && k.t > 0) st = launch_pairs(c, n, (u64)off, ExpPairBody{(u32)c->step + 2u, k, spv(c, z), sov(c, z), n, 1}, "exp");
     } else {
         st = launch_pairs(c, n, (u64)off, ExpPairBody{(u32)c->step, k, spv(c, x), sov(c, z), n, 0}, "exp");
     }

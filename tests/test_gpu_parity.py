@@ -124,6 +124,17 @@ def test_exp(mpc, t, clamp):
     assert c.step == o.step
 
 
+@pytest.mark.parametrize("t", [8, 2, 0])
+def test_exp_clamp_large(mpc, t):
+    """n >= 2^16 runs the clamp head and the squarings as two launches (pair layout)."""
+    c, o = pair_ctx(mpc, step=6)
+    n = 70_000 + 5
+    x = workloads.exp_inputs(n, tail_frac=0.05)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.exp(gx, off=32, t=t, clamp=1), o.exp(ox, off=32, t=t, clamp=1))
+    assert c.step == o.step
+
+
 @pytest.mark.parametrize("iters,t,clamp", [(10, 8, 0), (3, 8, 1), (7, 4, 0)])
 def test_recip(mpc, iters, t, clamp):
     c, o = pair_ctx(mpc, step=2)

@@ -33,6 +33,11 @@ def main(which):
         x = ctx.share(torch.from_numpy(workloads.relu_inputs(n)).to(dev))
         for _ in range(2):
             ctx.relu(x)
+    if "maxpool" in which:
+        N, C, H, W = 8, 64, 112, 112          # one pair's shard of the cfg4 MaxPool input
+        x = ctx.share(torch.from_numpy(workloads.maxpool_inputs((N, C, H, W))).to(dev))
+        for _ in range(2):
+            ctx.maxpool2d(x, N, C, H, W, 3, 2, 1)
     if "ln" in which:
         rows, cols = workloads.SHAPES["cfg5_ln"]
         x = ctx.share(torch.from_numpy(workloads.layernorm_inputs(rows, cols)).to(dev))

@@ -91,6 +91,9 @@ def sec_rows(S):
     out["S2_open"] = S.line(c, lambda: c.open(x), n, "open + decode 4M (ring and f64 outputs)")
     out["S4_mul"] = S.line(c, lambda: c.mul(x, y, trunc_bits=0, out=z), n, "Beaver multiply 4M, no trunc")
     out["S4_mul_trunc"] = S.line(c, lambda: c.mul(x, y, trunc_bits=16, out=z), n, "Beaver multiply + trunc 4M")
+    yr = S.share(c, workloads.recip_inputs(n // 128))
+    out["S4_mul_bcast"] = S.line(c, lambda: c.mul_bcast(x, yr, n // 128, 128, trunc_bits=16, out=z), n,
+                                 "broadcast-triple multiply 32768 x 128 by a per-row factor (NEXT #2)")
     out["S4_square"] = S.line(c, lambda: c.square(x, trunc_bits=16, out=z), n, "square-pair triple 4M (NEXT #2)")
     out["S5_trunc"] = S.line(c, lambda: c.trunc(x, 16, out=z), n, "local truncation 4M")
     for w in (33, 64):
@@ -161,6 +164,9 @@ def sec_cfg2(S):
     out["softmax_cone"] = S.line(c, lambda: c.softmax(x, rows, cols, out=z), n, "cfg2 carry cone", circuit=1)
     out["softmax_cone_square"] = S.line(c, lambda: c.softmax(x, rows, cols, exp_square=1, recip_square=1, out=z),
                                         n, "cfg2 carry cone + square triples", circuit=1)
+    out["softmax_bcast"] = S.line(c, lambda: c.softmax(x, rows, cols, bcast=1, out=z), n, "cfg2 broadcast triple")
+    out["softmax_next_all"] = S.line(c, lambda: c.softmax(x, rows, cols, exp_square=1, recip_square=1, bcast=1,
+                                                          out=z), n, "cfg2 cone + square + broadcast", circuit=1)
     return out
 
 
@@ -178,6 +184,10 @@ def sec_cfg3(S):
                                      f"cfg3 GELU erf-series K={K}, B=2.5")
     out["gelu_poly_abs4_cone"] = S.line(c, lambda: c.gelu(g, form="poly_abs", degree=4, out=z), n,
                                         "cfg3 GELU |x|-form deg 4, carry cone", circuit=1)
+    out["gelu_poly_abs4_power"] = S.line(c, lambda: c.gelu(g, form="poly_abs", degree=4, basis=1, out=z), n,
+                                         "cfg3 GELU |x|-form deg 4, power basis (NEXT #2)")
+    out["gelu_poly_x4_power"] = S.line(c, lambda: c.gelu(g, form="poly_x", degree=4, basis=1, out=z), n,
+                                       "cfg3 GELU x-form deg 4, power basis (NEXT #2)")
     return out
 
 
