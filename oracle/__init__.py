@@ -64,6 +64,7 @@ def lib():
         L.orc_act.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, INT, INT, INT, DBL,
                               ctypes.c_void_p, INT, INT, INT]
         L.orc_mul_bcast.argtypes = [CP, u64p, u64p, u64p, u64p, u64p, u64p, I64, I64, I64, I64, INT]
+        L.orc_matmul.argtypes = [CP, u64p, u64p, u64p, u64p, u64p, u64p, I64, I64, I64, I64, I64, INT]
         L.orc_max.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, INT]
         L.orc_maxpool2d.argtypes = [CP, u64p, u64p, u64p, u64p, INT, INT, INT, INT, INT, INT, INT,
                                     I64, INT]
@@ -154,6 +155,13 @@ class Oracle:
         (x0, x1), (y0, y1) = map(lambda p: (_u(p[0]), _u(p[1])), (x, y))
         z0, z1 = _pair(rows * cols)
         lib().orc_mul_bcast(ctypes.byref(self.c), x0, x1, y0, y1, z0, z1, rows, cols, off, row_off, trunc_bits)
+        return z0, z1
+
+    def matmul(self, x, y, batch, M, K, N, batch_off=0, trunc_bits=0):
+        """Z[b] = X[b] (M x K) @ Y[b] (K x N) with a matrix Beaver triple."""
+        (x0, x1), (y0, y1) = map(lambda p: (_u(p[0]), _u(p[1])), (x, y))
+        z0, z1 = _pair(batch * M * N)
+        lib().orc_matmul(ctypes.byref(self.c), x0, x1, y0, y1, z0, z1, batch, M, K, N, batch_off, trunc_bits)
         return z0, z1
 
     @staticmethod

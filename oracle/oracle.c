@@ -822,6 +822,83 @@ void orc_layernorm(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
 }
 
 /* ------------------------------------------------------------------------ */
+/* Beaver MATMUL over Z_2^64 (the CrypTen++ Beaver       */
+/* matmul, P:563 / P:846; the same algebra as S4 with matrix triples).        */
+/* Z = X Y for `batch` independent products X[b] (M x K), Y[b] (K x N),       */
+/* row-major, contiguous.  One step s.  Units (global batch index g = boff+b):  */
+/*   uA = g*M*K + m*K + k ; uB = g*K*N + k*N + n ; uC = g*M*N + m*N + n        */
+/* Triple:                                                    */
+/*   A_p = half (uA&1) of PRG(K_p, uA>>1, s, 8)   (p = 0, 1)                     */
+/*   B_p = half (uB&1) of PRG(K_p, uB>>1, s, 9)                                  */
+/*   C0  = half (uC&1) of PRG(K_0, uC>>1, s, 10) ; C1 = (A0+A1)(B0+B1) - C0     */
+/*   (matrix product mod 2^64; dealer correction to party 1, R7)               */
+/* E = open(X - A), F = open(Y - B) (one round, 8 (MK + KN) B per party);      */
+/* Z0 = C0 + E B0 + A0 F + E F ;  Z1 = C1 + E B1 + A1 F  (party 0 adds E F).    */
+/* ------------------------------------------------------------------------ */
+static u64 prg_half(u64 key, u64 u, u64 s, u32 slot)
+{
+    u32 w[4];
+    prg(key, u >> 1, s, slot, w);
+    return (u & 1) ? w64(w[2], w[3]) : w64(w[0], w[1]);
+}
+
+/* R = P Q (rows x inner) (inner x cols), mod 2^64, plain triple loop */
+static void ring_matmul(const u64* P, const u64* Q, u64* R, i64 rows, i64 inner, i64 cols)
+{
+    for (i64 i = 0; i < rows; ++i)
+        for (i64 j = 0; j < cols; ++j) {
+            u64 acc = 0;
+            for (i64 k = 0; k < inner; ++k) acc += P[i * inner + k] * Q[k * cols + j];
+            R[i * cols + j] = acc;
+        }
+}
+
+void orc_matmul(orc_ctx* ctx, const u64* x0, const u64* x1, const u64* y0, const u64* y1,
+                u64* z0, u64* z1, i64 batch, i64 M, i64 K, i64 N, i64 batch_off, int trunc_bits)
+{
+    u64 s = ctx->step++;
+    i64 MK = M * K, KN = K * N, MN = M * N;
+    u64 *A0 = A(MK), *A1 = A(MK), *As = A(MK), *E = A(MK);
+    u64 *B0 = A(KN), *B1 = A(KN), *Bs = A(KN), *F = A(KN);
+    u64 *C0 = A(MN), *C1 = A(MN), *T = A(MN);
+    for (i64 b = 0; b < batch; ++b) {
+        u64 g = (u64)(batch_off + b);
+        const u64 *xb0 = x0 + b * MK, *xb1 = x1 + b * MK, *yb0 = y0 + b * KN, *yb1 = y1 + b * KN;
+        for (i64 i = 0; i < MK; ++i) {
+            u64 u = g * (u64)MK + (u64)i;
+            A0[i] = prg_half(ctx->key_p0, u, s, 8);
+            A1[i] = prg_half(ctx->key_p1, u, s, 8);
+            As[i] = A0[i] + A1[i];
+            E[i] = (xb0[i] - A0[i]) + (xb1[i] - A1[i]);          /* opened */
+        }
+        for (i64 i = 0; i < KN; ++i) {
+            u64 u = g * (u64)KN + (u64)i;
+            B0[i] = prg_half(ctx->key_p0, u, s, 9);
+            B1[i] = prg_half(ctx->key_p1, u, s, 9);
+            Bs[i] = B0[i] + B1[i];
+            F[i] = (yb0[i] - B0[i]) + (yb1[i] - B1[i]);          /* opened */
+        }
+        for (i64 i = 0; i < MN; ++i) C0[i] = prg_half(ctx->key_p0, g * (u64)MN + (u64)i, s, 10);
+        ring_matmul(As, Bs, C1, M, K, N);                          /* dealer: A B */
+        for (i64 i = 0; i < MN; ++i) C1[i] -= C0[i];
+        u64 *zb0 = z0 + b * MN, *zb1 = z1 + b * MN;
+        /* party 0: C0 + E B0 + A0 F + E F */
+        memcpy(zb0, C0, sizeof(u64) * (size_t)MN);
+        ring_matmul(E, B0, T, M, K, N);  for (i64 i = 0; i < MN; ++i) zb0[i] += T[i];
+        ring_matmul(A0, F, T, M, K, N);  for (i64 i = 0; i < MN; ++i) zb0[i] += T[i];
+        ring_matmul(E, F, T, M, K, N);   for (i64 i = 0; i < MN; ++i) zb0[i] += T[i];
+        /* party 1: C1 + E B1 + A1 F */
+        memcpy(zb1, C1, sizeof(u64) * (size_t)MN);
+        ring_matmul(E, B1, T, M, K, N);  for (i64 i = 0; i < MN; ++i) zb1[i] += T[i];
+        ring_matmul(A1, F, T, M, K, N);  for (i64 i = 0; i < MN; ++i) zb1[i] += T[i];
+        if (trunc_bits)
+            for (i64 i = 0; i < MN; ++i) { zb0[i] = shr(zb0[i], trunc_bits); zb1[i] = shr(zb1[i], trunc_bits); }
+    }
+    free(A0); free(A1); free(As); free(E); free(B0); free(B1); free(Bs); free(F);
+    free(C0); free(C1); free(T);
+}
+
+/* ------------------------------------------------------------------------ */
 /* Small-ring truncation statistics (acceptance 4): ring Z_2^N with    */
 /* N < 64, shares uniform in the ring, per-share arithmetic shift by k bits.  */
 /* Returns the number of trials whose reconstruction is not within            */
