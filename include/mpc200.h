@@ -161,6 +161,14 @@ mpc_status mpc_square(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int64
  * party.  off = global element index of x[0] (multiple of 2), row_off = global row of y[0]. */
 mpc_status mpc_mul_bcast(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z, int64_t rows,
                          int64_t cols, int64_t off, int64_t row_off, int trunc_bits);
+/* NEXT #3 Beaver matrix multiplication over Z_2^64 (CrypTen++'s Beaver matmul, P:563,
+ * P:846): for b < batch, Z[b] = X[b] Y[b] mod 2^64 with X[b] M x K, Y[b]
+ * K x N, Z[b] M x N, all row-major and contiguous; then per-share shift by trunc_bits (0 or
+ * 16).  A matrix Beaver triple (A, B, C = AB) from the PRG keyed by global units (batch_off =
+ * global index of the first product); 1 step, 1 round, 8 (MK + KN) B per product per party.
+ * Caller-owned device buffers; the library keeps 32 (MK + KN) B per product of scratch. */
+mpc_status mpc_matmul(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z, int64_t batch,
+                      int64_t M, int64_t K, int64_t N, int64_t batch_off, int trunc_bits);
 /* S5 local truncation: z_i = (int64)x_i >> bits, bits in [0,63].
  * No step, no communication. */
 mpc_status mpc_trunc(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t n, int bits);

@@ -99,6 +99,7 @@ _SIGS = {
     "mpc_mul": [VP, Shares, Shares, Shares, i64, i64, INT],
     "mpc_square": [VP, Shares, Shares, i64, i64, INT],
     "mpc_mul_bcast": [VP, Shares, Shares, Shares, i64, i64, i64, i64, INT],
+    "mpc_matmul": [VP, Shares, Shares, Shares, i64, i64, i64, i64, i64, INT],
     "mpc_trunc": [VP, Shares, Shares, i64, INT],
     "mpc_cmp": [VP, Shares, Shares, i64, i64, INT],
     "mpc_relu": [VP, Shares, Shares, i64, i64, INT],
@@ -297,6 +298,13 @@ class Ctx:
         self._stream()
         self._chk(_L.mpc_mul_bcast(self._h, _sh(x), _sh(y), _sh(z), rows, cols, off, row_off, trunc_bits),
                   "mpc_mul_bcast")
+        return z
+
+    def matmul(self, x, y, batch, M, K, N, batch_off=0, trunc_bits=0, out=None):
+        """Z[b] = X[b] (M x K) @ Y[b] (K x N) over Z_2^64 with a matrix Beaver triple."""
+        z = out if out is not None else self._empty(batch * M * N)
+        self._stream()
+        self._chk(_L.mpc_matmul(self._h, _sh(x), _sh(y), _sh(z), batch, M, K, N, batch_off, trunc_bits), "mpc_matmul")
         return z
 
     def square(self, x, off=0, trunc_bits=0, out=None):

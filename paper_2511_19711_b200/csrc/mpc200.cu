@@ -17,6 +17,7 @@
 
 #include "mpc200.h"
 #include "kernels.cuh"
+#include "matmul.cuh"
 
 using namespace mpc;
 
@@ -834,6 +835,48 @@ mpc_status mpc_mul_bcast(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, i
         if (st) return st;
         acct_bcast(c, (u64)n, (u64)rows);
     }
+    finish(c, 1);
+    return MPC_OK;
+}
+
+// NEXT #3 Beaver matrix multiplication: masks + openings, then the ring GEMMs
+mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int64_t batch, int64_t M, int64_t K,
+                      int64_t N, int64_t batch_off, int tb)
+{
+    mpc_status st = begin(c, 1);
+    if (st) return st;
+    if (tb != 0 && tb != 16) return fail(c, MPC_ERR_RANGE, "trunc_bits must be 0 or 16");
+    if (batch < 0 || M < 1 || K < 1 || N < 1 || batch_off < 0 || M > 65535 * 64 || N > (1ll << 30) ||
+        batch * M * K >= (1ll << 40) || batch * K * N >= (1ll << 40) || batch > 65535)
+        return fail(c, MPC_ERR_INVALID, "matmul: bad shape");
+    if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "matmul: null pointer");
+    if (batch == 0) { finish(c, 1); return MPC_OK; }
+    const i64 nA = batch * M * K, nB = batch * K * N;
+    u64* pl = (u64*)scratch(c, sizeof(u64) * 4 * (size_t)(nA + nB));
+    if (!pl) return fail(c, MPC_ERR_NOMEM, "matmul scratch");
+    u64 *PA = pl, *PB = pl + 4 * nA;
+    const u32 s = (u32)c->step;
+    if ((st = launch_pairs(c, nA, (u64)(batch_off * M * K), MmMaskBody{s, 8u, spv(c, x), nA, PA, 0}, "mm_mask"))) return st;
+    if ((st = launch_pairs(c, nB, (u64)(batch_off * K * N), MmMaskBody{s, 9u, spv(c, y), nB, PB, 1}, "mm_mask"))) return st;
+    MmArgs a;
+    memset(&a, 0, sizeof a);
+    a.K = c->K; a.s = s; a.M = (int)M; a.Kd = (int)K; a.N = (int)N; a.batch = (int)batch; a.goff = (u64)batch_off; a.tb = tb;
+    const u64 *E = PA, *A0 = PA + nA, *A1 = PA + 2 * nA, *As = PA + 3 * nA;
+    const u64 *F = PB, *G = PB + nB, *B1 = PB + 2 * nB, *Bs = PB + 3 * nB;
+    a.t[0][0] = MmTerm{E, G}; a.t[0][1] = MmTerm{A0, F}; a.nt[0] = 2;                          // C0 + E(B0+F) + A0 F
+    a.t[1][0] = MmTerm{As, Bs}; a.t[1][1] = MmTerm{E, B1}; a.t[1][2] = MmTerm{A1, F}; a.nt[1] = 3; // AB - C0 + E B1 + A1 F
+    a.z[0] = z.sh[0]; a.z[1] = z.sh[1];
+    if (c->cfg.mode == MPC_MODE_PAIR) { a.p0 = c->cfg.party; a.np = 1; }
+    else { a.p0 = 0; a.np = 2; }
+    const dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)(batch * a.np));
+    rec_begin(c, "matmul", (u64)(batch * M * N));
+    k_mm_simt<<<grid, 256, 0, c->stream>>>(a);
+    rec_end(c);
+    c->st.launches++;
+    if ((st = cuda_check(c, "matmul"))) return st;
+    c->last_philox += (u64)(nA + nB) + (u64)(batch * M * N + 1) / 2;
+    c->st.bytes_per_party += 8ull * (u64)(nA + nB);
+    c->st.rounds += 1;
     finish(c, 1);
     return MPC_OK;
 }

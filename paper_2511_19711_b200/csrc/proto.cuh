@@ -94,6 +94,9 @@ struct BothP {
     }
     __device__ __forceinline__ void sq2(u64 u, u32 s, S y0, S y1, S& z0, S& z1) { mpc::sq2(*Kp, u, s, y0, y1, z0, z1); }
     __device__ __forceinline__ u64 open(S x) const { return x.s0 + x.s1; }
+    // matrix-triple masking: this party's share minus its mask half; two openings
+    __device__ __forceinline__ S mask2(S x, u64 r0, u64 r1) const { return {x.s0 - r0, x.s1 - r1}; }
+    __device__ __forceinline__ void open2(S a, S b, u64& ea, u64& eb) const { ea = a.s0 + a.s1; eb = b.s0 + b.s1; }
     template <int V>
     __device__ __forceinline__ void bm2v(const u64 (&u)[V], u32 s, const S (&x0)[V], const S (&y0)[V],
                                          const S (&x1)[V], const S (&y1)[V], S (&z0)[V], S (&z1)[V]) {
@@ -641,6 +644,13 @@ struct PairP {
         put(lane, 0, x);
         exch(lane);
         return x + get(lane, 0);
+    }
+    __device__ __forceinline__ S mask2(S x, u64 r0, u64 r1) const { return pty == 0 ? x - r0 : x - r1; }
+    __device__ __forceinline__ void open2(S a, S b, u64& ea, u64& eb) {
+        const int lane = threadIdx.x & 31;
+        put(lane, 0, a); put(lane, 1, b);
+        exch(lane);
+        ea = a + get(lane, 0); eb = b + get(lane, 1);
     }
 };
 
