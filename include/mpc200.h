@@ -119,6 +119,12 @@ mpc_status mpc_ctx_sync(mpc_ctx* ctx);
  * transcript, the PRG work and the bytes sent change. */
 mpc_status mpc_ctx_set_ltz_circuit(mpc_ctx* ctx, int circuit);
 
+/* Ring-GEMM engine of mpc_matmul: 0 = auto (tensor cores whenever the limb
+ * accumulators are exact, i.e. K <= 5461), 1 = SIMT (IMAD u64 multiply-adds), 2 = tensor cores
+ * (tcgen05 kind::i8 on 8-bit limbs; MPC_ERR_UNSUPPORTED if K > 5461).  All engines give the
+ * same ring product, hence bit-identical output shares. */
+mpc_status mpc_ctx_set_matmul_engine(mpc_ctx* ctx, int engine);
+
 /* Per-launch timing (for the roofline in bench.py): when enabled, every kernel the
  * context launches is bracketed by CUDA events on the context stream and tagged with
  * its algorithmic Philox4x32-10 block count.  mpc_ctx_kernel_times synchronizes on

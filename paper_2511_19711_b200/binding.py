@@ -89,6 +89,7 @@ _SIGS = {
     "mpc_last_call_philox": [VP],
     "mpc_ctx_enable_kernel_timing": [VP, INT],
     "mpc_ctx_set_ltz_circuit": [VP, INT],
+    "mpc_ctx_set_matmul_engine": [VP, INT],
     "mpc_pair_export": [VP, VP],
     "mpc_pair_connect": [VP, VP],
     "mpc_ctx_sync": [VP],
@@ -213,6 +214,10 @@ class Ctx:
     def set_ltz_circuit(self, circuit: int):
         """0 = Kogge-Stone (default, the S7 contract), 1 = carry cone (NEXT #1): same output shares."""
         self._chk(_L.mpc_ctx_set_ltz_circuit(self._h, circuit), "mpc_ctx_set_ltz_circuit")
+
+    def set_matmul_engine(self, engine: int):
+        """0 auto, 1 SIMT, 2 tensor cores (tcgen05 on 8-bit limbs); same output shares."""
+        self._chk(_L.mpc_ctx_set_matmul_engine(self._h, engine), "mpc_ctx_set_matmul_engine")
 
     def sync(self):
         self._stream()

@@ -9,6 +9,7 @@ namespace mpc {
 typedef uint64_t u64;
 typedef int64_t i64;
 typedef unsigned int u32;
+typedef uint8_t u8;
 
 constexpr u32 FULL = 0xffffffffu;
 constexpr int FRAC = 16;

@@ -1,0 +1,234 @@
+// matmul_tc.cuh -- the ring GEMM of mpc_matmul on the 5th-generation tensor cores (sm_100a).
+//
+// Z_2^64 products through 8-bit limbs: with a = sum_i 2^(8i) a_i and
+// b = sum_j 2^(8j) b_j (unsigned bytes),
+//     a * b mod 2^64 = sum_{s=0..7} 2^(8s) S_s,   S_s = sum_{i+j=s} a_i b_j,
+// so a ring GEMM is 36 u8 x u8 -> s32 GEMMs accumulated into 8 TMEM accumulators S_0..S_7.
+// Each S_s is exact as long as (s+1) K' 255^2 < 2^32 for s <= 3 (K' < 16513); for s >= 4 only
+// its low 64 - 8s <= 32 bits survive the shift, so the 32-bit wrap of the accumulator is
+// harmless.  The epilogue forms sum_s (u64)S_s << 8s, adds +-C0 from the PRG and truncates.
+//
+// Operands are pre-tiled by k_mm_limbs into the UMMA canonical K-major layout without
+// swizzle (core matrix = 8 rows x 16 B; LBO = 128 B between the two 16-B K-chunks, SBO = 256 B
+// between 8-row groups), one contiguous chunk per (row block, K block of 32) holding all 8
+// limbs: A chunk = 8 x (128 x 32 B) = 32 KB, B chunk = 8 x (64 x 32 B) = 16 KB.  A stage is
+// therefore two flat cp.async.bulk copies (TMA without tensor maps) completing on an mbarrier.
+// One CTA = one 128 x 64 output tile (512 TMEM columns = 8 accumulators x 64); thread 0
+// issues the copies (3-stage ring) and the 36 tcgen05.mma per K block, all 4 warps run the
+// epilogue (warp w owns TMEM lanes 32w..32w+31 = rows).
+#pragma once
+#include "matmul.cuh"
+
+namespace mpc {
+
+constexpr int TC_BM = 128, TC_BN = 64, TC_BK = 32, TC_STAGES = 3;
+constexpr int TC_A_TILE = TC_BM * TC_BK, TC_B_TILE = TC_BN * TC_BK;          // bytes per limb tile
+constexpr int TC_A_CHUNK = 8 * TC_A_TILE, TC_B_CHUNK = 8 * TC_B_TILE;          // bytes per stage
+constexpr int TC_SMEM = TC_STAGES * (TC_A_CHUNK + TC_B_CHUNK) + 1024;
+
+// byte offset of (row r, k byte kb) inside one limb tile (canonical K-major, no swizzle)
+__host__ __device__ inline int tc_tile_off(int r, int kb) { return (r >> 3) * 256 + (kb >> 4) * 128 + (r & 7) * 16 + (kb & 15); }
+
+// ---- limb tiling ------------------------------------------------------------------------------
+// Operand of one party: up to three terms concatenated along K (K' = nt * K).  LHS terms are
+// [batch][M][K] (rows = m), RHS terms [batch][K][N] (rows = n, transposed to K-major).  Output:
+// [batch][row block][K block][limb][tile], zero padded to whole blocks.  One thread packs one
+// 16-byte core-matrix row (16 consecutive k' of one row) for all 8 limbs.
+struct LimbArgs {
+    const u64* t[3]; int nt; int rows, K, Kp, rhs, rows_blk; int batch; i64 in_stride; u8* out;
+};
+__global__ void __launch_bounds__(256) k_mm_limbs(LimbArgs a)
+{
+    const int kchunks = a.Kp / 16;                          // 16-byte chunks per padded row
+    const i64 rows_p = (i64)((a.rows + a.rows_blk - 1) / a.rows_blk) * a.rows_blk;
+    const i64 per_b = rows_p * kchunks;
+    const i64 total = per_b * a.batch;
+    const int Ktot = a.nt * a.K;
+    for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
+        const int b = (int)(idx / per_b);
+        const i64 rem = idx - (i64)b * per_b;
+        const int r = (int)(rem / kchunks), kc = (int)(rem % kchunks);
+        uint4 limb[8];
+        u32* lw = reinterpret_cast<u32*>(limb);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) lw[q] = 0;
+        if (r < a.rows) {
+#pragma unroll 4
+            for (int e = 0; e < 16; ++e) {
+                const int kk = kc * 16 + e;
+                if (kk >= Ktot) break;
+                const int t = kk / a.K, k = kk - t * a.K;
+                const u64* base = a.t[t] + (i64)b * a.in_stride;
+                const u64 v = a.rhs ? base[(i64)k * a.rows + r] : base[(i64)r * a.K + k];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const u32 byte = (u32)(v >> (8 * i)) & 0xffu;
+                    lw[i * 4 + (e >> 2)] |= byte << (8 * (e & 3));
+                }
+            }
+        }
+        const int rb = r / a.rows_blk, rr = r - rb * a.rows_blk, kb = kc / 2;
+        const int tile = a.rows_blk * TC_BK;
+        u8* dst = a.out + (((i64)b * (rows_p / a.rows_blk) + rb) * (a.Kp / TC_BK) + kb) * (8 * (i64)tile);
+        const int off = tc_tile_off(rr, (kc & 1) * 16);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + (i64)i * tile + off) = limb[i];
+    }
+}
+
+// ---- PTX helpers ------------------------------------------------------------------------------
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 phase)
+{
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" :: "r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+// UMMA shared-memory descriptor: canonical K-major, SWIZZLE_NONE, LBO 128 B, SBO 256 B, version 1
+__device__ __forceinline__ u64 umma_desc(const void* p)
+{
+    const u64 addr = (u64)(smem_u32(p) >> 4) & 0x3fffull;
+    return addr | ((u64)(128 >> 4) << 16) | ((u64)(256 >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor: kind::i8, D = s32, A = B = u8, K-major, M = 128, N = 64
+constexpr u32 TC_IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((u32)(TC_BN >> 3) << 17) | ((u32)(TC_BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_i8(u32 tmem_d, u64 adesc, u64 bdesc, u32 accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void umma_commit(u64* bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(u32 taddr, u32 (&v)[16])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(taddr));
+}
+
+// ---- the tensor-core ring GEMM ------------------------------------------------------------------
+struct TcArgs {
+    MmArgs mm;                 // shapes, keys, step, outputs, truncation
+    const u8* A[2]; const u8* B[2];   // tiled limb operands per party
+    int Kp[2];                 // padded K' per party
+};
+
+__global__ void __launch_bounds__(128, 1) k_mm_tc(const __grid_constant__ TcArgs t)
+{
+    extern __shared__ __align__(1024) u8 smem_raw[];
+    u8* smem = (u8*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    __shared__ __align__(8) u64 full_bar[TC_STAGES], empty_bar[TC_STAGES], done_bar;
+    __shared__ u32 tmem_base_sh;
+    const MmArgs& a = t.mm;
+    const int p = a.p0 + (int)(blockIdx.z % a.np), b = (int)(blockIdx.z / a.np);
+    const int nb = blockIdx.x, mb = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KB = t.Kp[p] / TC_BK;
+    const int MB = (a.M + TC_BM - 1) / TC_BM, NB = (a.N + TC_BN - 1) / TC_BN;
+    const u8* Ag = t.A[p] + (((i64)b * MB + mb) * KB) * (i64)TC_A_CHUNK;
+    const u8* Bg = t.B[p] + (((i64)b * NB + nb) * KB) * (i64)TC_B_CHUNK;
+    u8* sA = smem;
+    u8* sB = smem + TC_STAGES * TC_A_CHUNK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+        mbar_init(&done_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base_sh)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const u32 tmem = tmem_base_sh;
+
+    if (threadIdx.x == 0) {
+        auto load = [&](int kb) {
+            const int s = kb % TC_STAGES;
+            mbar_expect_tx(&full_bar[s], TC_A_CHUNK + TC_B_CHUNK);
+            bulk_g2s(sA + s * TC_A_CHUNK, Ag + (i64)kb * TC_A_CHUNK, TC_A_CHUNK, &full_bar[s]);
+            bulk_g2s(sB + s * TC_B_CHUNK, Bg + (i64)kb * TC_B_CHUNK, TC_B_CHUNK, &full_bar[s]);
+        };
+        for (int kb = 0; kb < KB && kb < TC_STAGES; ++kb) load(kb);
+        for (int kb = 0; kb < KB; ++kb) {
+            const int s = kb % TC_STAGES;
+            mbar_wait(&full_bar[s], (u32)((kb / TC_STAGES) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const u8* As_ = sA + s * TC_A_CHUNK;
+            const u8* Bs_ = sB + s * TC_B_CHUNK;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const u64 ad = umma_desc(As_ + i * TC_A_TILE);
+#pragma unroll
+                for (int j = 0; j < 8 - i; ++j) {
+                    // first product into accumulator i + j: (i = 0, j = s) at the first K block
+                    const u32 acc = (kb > 0 || i > 0) ? 1u : 0u;
+                    umma_i8(tmem + (u32)((i + j) * TC_BN), ad, umma_desc(Bs_ + j * TC_B_TILE), acc);
+                }
+            }
+            umma_commit(&empty_bar[s]);                   // frees stage s once these MMAs complete
+            if (kb + TC_STAGES < KB) {
+                mbar_wait(&empty_bar[s], (u32)((kb / TC_STAGES) & 1));
+                load(kb + TC_STAGES);
+            }
+        }
+        umma_commit(&done_bar);
+    }
+    __syncwarp();
+    mbar_wait(&done_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // epilogue: thread <-> row m0 + 32 warp + lane, 16 columns at a time
+    const int m = mb * TC_BM + warp * 32 + lane;
+    const u32 trow = tmem + ((u32)(warp * 32) << 16);
+    for (int c0 = 0; c0 < TC_BN; c0 += 16) {
+        u64 r[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) r[q] = 0;
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            u32 v[16];
+            tmem_ld16(trow + (u32)(s * TC_BN + c0), v);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int q = 0; q < 16; ++q) r[q] += (u64)v[q] << (8 * s);
+        }
+        if (m < a.M) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int n = nb * TC_BN + c0 + q;
+                if (n < a.N) a.z[p][(i64)b * a.M * a.N + (i64)m * a.N + n] = mm_epilogue(a, p, b, m, n, r[q]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem) : "memory");
+}
+
+}  // namespace mpc

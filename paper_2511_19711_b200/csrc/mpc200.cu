@@ -18,6 +18,7 @@
 #include "mpc200.h"
 #include "kernels.cuh"
 #include "matmul.cuh"
+#include "matmul_tc.cuh"
 
 using namespace mpc;
 
@@ -56,6 +57,7 @@ struct mpc_ctx {
     void* peer_base;        // MPC_MODE_PAIR: the peer's exchange memory (cudaIpc-mapped)
     int connected;
     int circuit;            // LTZ carry circuit: 0 Kogge-Stone, 1 carry cone (2.7)
+    int mm_engine;          // mpc_matmul ring GEMM: 0 auto, 1 SIMT, 2 tensor cores
 };
 
 static bool is_pair(const mpc_ctx* c) { return c->cfg.mode != MPC_MODE_BOTH; }
@@ -642,6 +644,14 @@ mpc_status mpc_ctx_set_ltz_circuit(mpc_ctx* c, int circuit)
     return MPC_OK;
 }
 
+mpc_status mpc_ctx_set_matmul_engine(mpc_ctx* c, int engine)
+{
+    if (!c) return MPC_ERR_INVALID;
+    if (engine < 0 || engine > 2) return fail(c, MPC_ERR_RANGE, "engine must be 0 (auto), 1 (SIMT) or 2 (tensor cores)");
+    c->mm_engine = engine;
+    return MPC_OK;
+}
+
 mpc_status mpc_ctx_enable_kernel_timing(mpc_ctx* c, int on)
 {
     if (!c) return MPC_ERR_INVALID;
@@ -851,10 +861,21 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
         return fail(c, MPC_ERR_INVALID, "matmul: bad shape");
     if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "matmul: null pointer");
     if (batch == 0) { finish(c, 1); return MPC_OK; }
+    const bool tc_ok = 3 * K <= 16384;                // exact limb accumulators (matmul_tc.cuh)
+    if (c->mm_engine == 2 && !tc_ok) return fail(c, MPC_ERR_UNSUPPORTED, "matmul: tensor-core engine needs K <= 5461");
+    const bool use_tc = c->mm_engine == 2 || (c->mm_engine == 0 && tc_ok);
     const i64 nA = batch * M * K, nB = batch * K * N;
-    u64* pl = (u64*)scratch(c, sizeof(u64) * 4 * (size_t)(nA + nB));
-    if (!pl) return fail(c, MPC_ERR_NOMEM, "matmul scratch");
-    u64 *PA = pl, *PB = pl + 4 * nA;
+    // scratch: operand planes (4 (nA + nB) u64), then for the tensor-core engine the limb-tiled
+    // operands of each computed party (party 0: K' = 2K, party 1: K' = 3K)
+    const i64 MB = (M + TC_BM - 1) / TC_BM, NB = (N + TC_BN - 1) / TC_BN;
+    const i64 Kp0 = (2 * K + TC_BK - 1) / TC_BK * TC_BK, Kp1 = (3 * K + TC_BK - 1) / TC_BK * TC_BK;
+    const i64 la0 = batch * MB * (Kp0 / TC_BK) * TC_A_CHUNK, lb0 = batch * NB * (Kp0 / TC_BK) * TC_B_CHUNK;
+    const i64 la1 = batch * MB * (Kp1 / TC_BK) * TC_A_CHUNK, lb1 = batch * NB * (Kp1 / TC_BK) * TC_B_CHUNK;
+    const size_t plane_bytes = sizeof(u64) * 4 * (size_t)(nA + nB);
+    const size_t limb_bytes = use_tc ? (size_t)(la0 + lb0 + la1 + lb1) : 0;
+    u8* sc = (u8*)scratch(c, plane_bytes + limb_bytes);
+    if (!sc) return fail(c, MPC_ERR_NOMEM, "matmul scratch");
+    u64 *PA = (u64*)sc, *PB = PA + 4 * nA;
     const u32 s = (u32)c->step;
     if ((st = launch_pairs(c, nA, (u64)(batch_off * M * K), MmMaskBody{s, 8u, spv(c, x), nA, PA, 0}, "mm_mask"))) return st;
     if ((st = launch_pairs(c, nB, (u64)(batch_off * K * N), MmMaskBody{s, 9u, spv(c, y), nB, PB, 1}, "mm_mask"))) return st;
@@ -868,12 +889,49 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
     a.z[0] = z.sh[0]; a.z[1] = z.sh[1];
     if (c->cfg.mode == MPC_MODE_PAIR) { a.p0 = c->cfg.party; a.np = 1; }
     else { a.p0 = 0; a.np = 2; }
-    const dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)(batch * a.np));
-    rec_begin(c, "matmul", (u64)(batch * M * N));
-    k_mm_simt<<<grid, 256, 0, c->stream>>>(a);
-    rec_end(c);
-    c->st.launches++;
-    if ((st = cuda_check(c, "matmul"))) return st;
+    if (!use_tc) {
+        const dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)(batch * a.np));
+        rec_begin(c, "matmul", (u64)(batch * M * N));
+        k_mm_simt<<<grid, 256, 0, c->stream>>>(a);
+        rec_end(c);
+        c->st.launches++;
+        if ((st = cuda_check(c, "matmul"))) return st;
+    } else {
+        TcArgs t;
+        memset(&t, 0, sizeof t);
+        t.mm = a;
+        u8* lp = sc + plane_bytes;
+        u8* LA[2] = {lp, lp + la0 + lb0};
+        u8* LB[2] = {lp + la0, lp + la0 + lb0 + la1};
+        const i64 Kps[2] = {Kp0, Kp1};
+        for (int p = a.p0; p < a.p0 + a.np; ++p) {
+            LimbArgs la{}, lb{};
+            for (int q = 0; q < a.nt[p]; ++q) { la.t[q] = a.t[p][q].a; lb.t[q] = a.t[p][q].b; }
+            la.nt = lb.nt = a.nt[p];
+            la.rows = (int)M; la.K = (int)K; la.Kp = (int)Kps[p]; la.rhs = 0; la.rows_blk = TC_BM; la.batch = (int)batch;
+            la.in_stride = M * K; la.out = LA[p];
+            lb.rows = (int)N; lb.K = (int)K; lb.Kp = (int)Kps[p]; lb.rhs = 1; lb.rows_blk = TC_BN; lb.batch = (int)batch;
+            lb.in_stride = K * N; lb.out = LB[p];
+            const i64 wa = batch * MB * TC_BM * (Kps[p] / 16), wb = batch * NB * TC_BN * (Kps[p] / 16);
+            rec_begin(c, "mm_limbs", 0);
+            k_mm_limbs<<<grid_for(c, wa, 256, 8), 256, 0, c->stream>>>(la);
+            k_mm_limbs<<<grid_for(c, wb, 256, 8), 256, 0, c->stream>>>(lb);
+            rec_end(c);
+            c->st.launches += 2;
+            t.A[p] = LA[p]; t.B[p] = LB[p]; t.Kp[p] = (int)Kps[p];
+        }
+        if ((st = cuda_check(c, "mm_limbs"))) return st;
+        static bool attr = [] {
+            return cudaFuncSetAttribute(k_mm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) == cudaSuccess;
+        }();
+        (void)attr;
+        const dim3 grid((unsigned)NB, (unsigned)MB, (unsigned)(batch * a.np));
+        rec_begin(c, "matmul_tc", (u64)(batch * M * N));
+        k_mm_tc<<<grid, 128, TC_SMEM, c->stream>>>(t);
+        rec_end(c);
+        c->st.launches++;
+        if ((st = cuda_check(c, "matmul_tc"))) return st;
+    }
     c->last_philox += (u64)(nA + nB) + (u64)(batch * M * N + 1) / 2;
     c->st.bytes_per_party += 8ull * (u64)(nA + nB);
     c->st.rounds += 1;

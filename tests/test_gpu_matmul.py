@@ -28,10 +28,13 @@ def same(g, o):
 
 
 @pytest.mark.parametrize("batch,M,K,N,boff,tb", [(1, 1, 1, 1, 0, 0), (1, 5, 7, 3, 0, 16), (2, 64, 64, 64, 1, 16),
-                                                 (3, 70, 33, 129, 5, 16), (1, 128, 200, 65, 0, 0)])
-def test_matmul_vs_oracle(m, batch, M, K, N, boff, tb):
+                                                 (3, 70, 33, 129, 5, 16), (1, 128, 200, 65, 0, 0),
+                                                 (1, 257, 96, 130, 2, 16)])
+@pytest.mark.parametrize("engine", [1, 2])
+def test_matmul_vs_oracle(m, batch, M, K, N, boff, tb, engine):
     keys = workloads.keys(2)
     c = m.Ctx.for_cfg(keys)
+    c.set_matmul_engine(engine)
     c.set_step(3)
     o = Oracle.for_cfg(keys, 3)
     x = workloads.act_inputs(batch * M * K, lo=-2, hi=2)
@@ -81,3 +84,32 @@ def test_matmul_loopback(m):
         torch.cuda.synchronize()
         assert torch.equal(zb[0], zp[0]) and torch.equal(zb[1], zp[1])
     p.sync()
+
+
+def test_matmul_engines_agree_on_random_ring_values(m):
+    """Full-range u64 shares (not fixed-point encodings): every limb of both operands is
+    exercised; the tensor-core and SIMT engines must give the same shares."""
+    keys = workloads.keys(4)
+    batch, M, K, N = 2, 200, 160, 96
+    g = np.random.default_rng(5)
+    mk = lambda n: (torch.from_numpy(g.integers(0, 2**64, n, dtype=np.uint64, endpoint=False)).cuda(),
+                    torch.from_numpy(g.integers(0, 2**64, n, dtype=np.uint64, endpoint=False)).cuda())
+    x, y = mk(batch * M * K), mk(batch * K * N)
+    out = []
+    for engine in (1, 2):
+        c = m.Ctx.for_cfg(keys)
+        c.set_matmul_engine(engine)
+        out.append(c.matmul(x, y, batch, M, K, N, batch_off=7))
+    torch.cuda.synchronize()
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+    o = Oracle.for_cfg(keys)
+    r = o.matmul((np_(x[0]), np_(x[1])), (np_(y[0]), np_(y[1])), batch, M, K, N, batch_off=7)
+    same(out[1], r)
+
+
+def test_matmul_tc_engine_rejects_long_k(m):
+    c = m.Ctx.for_cfg(workloads.keys(1))
+    c.set_matmul_engine(2)
+    x = c.share(torch.zeros(6000, dtype=torch.float64).cuda())
+    with pytest.raises(m.MPCError):
+        c.matmul(x, x, 1, 1, 6000, 1)
