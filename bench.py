@@ -388,6 +388,15 @@ def time_per_op(job, m, ctx, flush, args):
                                 "cfg4 ReLU shard, carry-cone LTZ (NEXT #1)")
     del r, z
     ctx.set_ltz_circuit(0)
+    Bm, Mm, Km, Nm = 1, 1024, 768, 3072           # BERT-base FFN Linear (8 x 128 tokens), NEXT #3
+    xm = job.share(ctx, workloads.act_inputs(Mm * Km, lo=-2, hi=2), k * Mm * Km)
+    ym = job.share(ctx, workloads.act_inputs(Km * Nm, seed_cfg=5, lo=-2, hi=2), k * Km * Nm)
+    z = ctx._empty(Mm * Nm)
+    out["matmul_tc"] = _op_line(job, ctx, lambda: ctx.matmul(xm, ym, Bm, Mm, Km, Nm, batch_off=k, trunc_bits=16,
+                                                             out=z), Mm * Nm, flush, args,
+                                "Beaver matmul 1024 x 768 x 3072 (BERT FFN Linear), tcgen05 kind::i8 on 8-bit limbs "
+                                "(elements = outputs; 2.4 G ring MACs)")
+    del xm, ym, z
     nm = 1 << 24
     a = job.share(ctx, workloads.act_inputs(nm), k * nm)
     b = job.share(ctx, workloads.act_inputs(nm, seed_cfg=7), k * nm)

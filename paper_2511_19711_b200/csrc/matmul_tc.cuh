@@ -76,6 +76,50 @@ __global__ void __launch_bounds__(256) k_mm_limbs(LimbArgs a)
     }
 }
 
+// RHS limb tiling through a shared-memory transpose: one CTA per (batch, 64-column block, K block
+// of 32): coalesced loads of 32 rows x 64 columns, then 128 threads pack the 64 x 2 core-matrix
+// rows of all 8 limbs and write the 16 KB chunk contiguously.
+__global__ void __launch_bounds__(256) k_mm_limbs_rhs(LimbArgs a)
+{
+    __shared__ u64 sm[TC_BK][TC_BN + 1];
+    const int KB = a.Kp / TC_BK, NB = (a.rows + TC_BN - 1) / TC_BN;
+    const int Ktot = a.nt * a.K;
+    const i64 ntile = (i64)a.batch * NB * KB;
+    for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int b = (int)(tile / ((i64)NB * KB));
+        const int rem = (int)(tile - (i64)b * NB * KB), nb = rem / KB, kb = rem - (rem / KB) * KB;
+        for (int l = threadIdx.x; l < TC_BK * TC_BN; l += blockDim.x) {
+            const int kr = l / TC_BN, nc = l - kr * TC_BN;
+            const int kk = kb * TC_BK + kr, n = nb * TC_BN + nc;
+            u64 v = 0;
+            if (kk < Ktot && n < a.rows) {
+                const int t = kk / a.K, k = kk - t * a.K;
+                v = a.t[t][(i64)b * a.in_stride + (i64)k * a.rows + n];
+            }
+            sm[kr][nc] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < 2 * TC_BN) {
+            const int n = threadIdx.x >> 1, ch = threadIdx.x & 1;
+            uint4 limb[8];
+            u32* lw = reinterpret_cast<u32*>(limb);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) lw[q] = 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const u64 v = sm[ch * 16 + e][n];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) lw[i * 4 + (e >> 2)] |= ((u32)(v >> (8 * i)) & 0xffu) << (8 * (e & 3));
+            }
+            u8* dst = a.out + (((i64)b * NB + nb) * KB + kb) * (i64)TC_B_CHUNK;
+            const int off = tc_tile_off(n, ch * 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + (i64)i * TC_B_TILE + off) = limb[i];
+        }
+        __syncthreads();
+    }
+}
+
 // ---- PTX helpers ------------------------------------------------------------------------------
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* bar, u32 count)

@@ -263,8 +263,27 @@ def sec_cfg5(S):
     return out
 
 
+def sec_matmul(S):
+    """NEXT #3 Beaver matmul on BERT-base shapes, SIMT vs tensor-core engine (same shares)."""
+    c = S.ctx(2)
+    out = {}
+    for name, (B, M, K, N) in {"qkT_96x128x64x128": (96, 128, 64, 128), "av_96x128x128x64": (96, 128, 128, 64),
+                               "ffn_1024x768x3072": (1, 1024, 768, 3072)}.items():
+        x = S.share(c, workloads.act_inputs(B * M * K, lo=-2, hi=2))
+        y = S.share(c, workloads.act_inputs(B * K * N, seed_cfg=5, lo=-2, hi=2))
+        z = c._empty(B * M * N)
+        for eng, tag in ((1, "simt"), (2, "tc")):
+            c.set_matmul_engine(eng)
+            r = S.line(c, lambda: c.matmul(x, y, B, M, K, N, trunc_bits=16, out=z), B * M * N,
+                       f"Beaver matmul {name}, engine {tag} (elements = outputs)")
+            r["ring_macs_per_s"] = B * M * K * N / (r["ms"] / 1e3)
+            out[f"{name}_{tag}"] = r
+        c.set_matmul_engine(0)
+    return out
+
+
 SECTIONS = {"rows": sec_rows, "cfg1": sec_cfg1, "cfg2": sec_cfg2, "cfg3": sec_cfg3, "cfg4": sec_cfg4,
-            "cfg5": sec_cfg5}
+            "cfg5": sec_cfg5, "matmul": sec_matmul}
 
 
 def main():
