@@ -14,8 +14,9 @@
 // limbs: A chunk = 8 x (128 x 32 B) = 32 KB, B chunk = 8 x (64 x 32 B) = 16 KB.  A stage is
 // therefore two flat cp.async.bulk copies (TMA without tensor maps) completing on an mbarrier.
 // One CTA = one 128 x 64 output tile (512 TMEM columns = 8 accumulators x 64); thread 0
-// issues the copies (3-stage ring) and the 36 tcgen05.mma per K block, all 4 warps run the
-// epilogue (warp w owns TMEM lanes 32w..32w+31 = rows).
+// issues the copies (3-stage ring) and 12 tcgen05.mma per K block (A limb i against the
+// stacked B limbs 0..7-i, N up to 256), all 4 warps run the epilogue (warp w owns TMEM lanes
+// 32w..32w+31 = rows).
 #pragma once
 #include "matmul.cuh"
 
@@ -149,16 +150,19 @@ __device__ __forceinline__ u64 umma_desc(const void* p)
     const u64 addr = (u64)(smem_u32(p) >> 4) & 0x3fffull;
     return addr | ((u64)(128 >> 4) << 16) | ((u64)(256 >> 4) << 32) | (1ull << 46);
 }
-// instruction descriptor: kind::i8, D = s32, A = B = u8, K-major, M = 128, N = 64
-constexpr u32 TC_IDESC = (2u << 4) | (0u << 7) | (0u << 10) | ((u32)(TC_BN >> 3) << 17) | ((u32)(TC_BM >> 4) << 24);
+// instruction descriptor: kind::i8, D = s32, A = B = u8, K-major, M = 128, N = n (multiple of 16, <= 256)
+__host__ __device__ constexpr u32 tc_idesc(int n)
+{
+    return (2u << 4) | (0u << 7) | (0u << 10) | ((u32)(n >> 3) << 17) | ((u32)(TC_BM >> 4) << 24);
+}
 
-__device__ __forceinline__ void umma_i8(u32 tmem_d, u64 adesc, u64 bdesc, u32 accumulate)
+__device__ __forceinline__ void umma_i8(u32 tmem_d, u64 adesc, u64 bdesc, u32 idesc, u32 accumulate)
 {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate) : "memory");
+        :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
 }
 __device__ __forceinline__ void umma_commit(u64* bar)
 {
@@ -225,15 +229,20 @@ __global__ void __launch_bounds__(128, 1) k_mm_tc(const __grid_constant__ TcArgs
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const u8* As_ = sA + s * TC_A_CHUNK;
             const u8* Bs_ = sB + s * TC_B_CHUNK;
+            // A limb i times ALL B limbs j = 0 .. 7-i at once: the 8 B limb tiles are stacked along
+            // N in the canonical layout (tile j = rows 64j .. 64j+63), and accumulators S_i .. S_7
+            // are the contiguous TMEM columns [64 i, 512) -- one MMA of N = 64 (8 - i), split at
+            // N = 256: 12 MMAs per K block instead of 36 (each A tile is read from shared memory
+            // 1-2 times instead of 8 - i times).
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const u64 ad = umma_desc(As_ + i * TC_A_TILE);
-#pragma unroll
-                for (int j = 0; j < 8 - i; ++j) {
-                    // first product into accumulator i + j: (i = 0, j = s) at the first K block
-                    const u32 acc = (kb > 0 || i > 0) ? 1u : 0u;
-                    umma_i8(tmem + (u32)((i + j) * TC_BN), ad, umma_desc(Bs_ + j * TC_B_TILE), acc);
-                }
+                const u32 acc = (kb > 0 || i > 0) ? 1u : 0u;     // S_0..S_7 all first written at i = 0
+                const int nj = 8 - i;
+                const int n1 = nj > 4 ? 4 : nj;
+                umma_i8(tmem + (u32)(i * TC_BN), ad, umma_desc(Bs_), tc_idesc(n1 * TC_BN), acc);
+                if (nj > 4)
+                    umma_i8(tmem + (u32)((i + 4) * TC_BN), ad, umma_desc(Bs_ + 4 * TC_B_TILE), tc_idesc((nj - 4) * TC_BN), acc);
             }
             umma_commit(&empty_bar[s]);                   // frees stage s once these MMAs complete
             if (kb + TC_STAGES < KB) {

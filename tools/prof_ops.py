@@ -38,6 +38,13 @@ def main(which):
         x = ctx.share(torch.from_numpy(workloads.maxpool_inputs((N, C, H, W))).to(dev))
         for _ in range(2):
             ctx.maxpool2d(x, N, C, H, W, 3, 2, 1)
+    if "matmul" in which:
+        B, M, K, N = 1, 1024, 768, 3072        # BERT-base FFN Linear, tensor-core engine
+        x = ctx.share(torch.from_numpy(workloads.act_inputs(B * M * K, lo=-2, hi=2)).to(dev))
+        y = ctx.share(torch.from_numpy(workloads.act_inputs(B * K * N, seed_cfg=5, lo=-2, hi=2)).to(dev))
+        ctx.set_matmul_engine(2)
+        for _ in range(2):
+            ctx.matmul(x, y, B, M, K, N, trunc_bits=16)
     if "ln" in which:
         rows, cols = workloads.SHAPES["cfg5_ln"]
         x = ctx.share(torch.from_numpy(workloads.layernorm_inputs(rows, cols)).to(dev))
