@@ -251,6 +251,20 @@ typedef struct { double eps; int mean_mode; mpc_nr_p rsqrt; int bcast; } mpc_ln_
 mpc_status mpc_layernorm(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols,
                          int64_t row_off, const mpc_ln_p* p);
 
+/* ---- NEXT #4: the auto-tuner's evaluator ---------------------------------------------- */
+/* Plaintext fixed-point emulation of one approximation schedule, the scoring
+ * step of CrypTorch's auto-tuner, which evaluates candidate approximations on a non-MPC runtime
+ * (P:237-241).  x, y: DEVICE float64 arrays of rows x cols (rows = 1 for element-wise ops);
+ * x is encoded at 2^16 (round half even), the op's schedule runs on the plaintext ring values
+ * with floor truncation, y is decoded.  The MPC output differs from it only by the per-share
+ * truncation's (-1, 0] ulp per product.  knobs points to the op's knob struct (mpc_exp_p,
+ * mpc_nr_p, mpc_act_p, mpc_softmax_p, mpc_ln_p).  No step, no randomness, no communication. */
+typedef enum { MPC_PLAIN_EXP = 0, MPC_PLAIN_RECIP = 1, MPC_PLAIN_RSQRT = 2, MPC_PLAIN_GELU = 3,
+               MPC_PLAIN_SILU = 4, MPC_PLAIN_SIGMOID = 5, MPC_PLAIN_SOFTMAX = 6,
+               MPC_PLAIN_LAYERNORM = 7 } mpc_plain_op;
+mpc_status mpc_plain_eval(mpc_ctx* ctx, int op, const void* knobs, const double* x, double* y,
+                          int64_t rows, int64_t cols);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,7 @@ _SIGS = {
     "mpc_square": [VP, Shares, Shares, i64, i64, INT],
     "mpc_mul_bcast": [VP, Shares, Shares, Shares, i64, i64, i64, i64, INT],
     "mpc_matmul": [VP, Shares, Shares, Shares, i64, i64, i64, i64, i64, INT],
+    "mpc_plain_eval": [VP, INT, VP, VP, VP, i64, i64],
     "mpc_trunc": [VP, Shares, Shares, i64, INT],
     "mpc_cmp": [VP, Shares, Shares, i64, i64, INT],
     "mpc_relu": [VP, Shares, Shares, i64, i64, INT],
@@ -311,6 +312,44 @@ class Ctx:
         self._stream()
         self._chk(_L.mpc_matmul(self._h, _sh(x), _sh(y), _sh(z), batch, M, K, N, batch_off, trunc_bits), "mpc_matmul")
         return z
+
+    # ---- NEXT #4: plaintext fixed-point emulation (the auto-tuner's evaluator) ----
+    PLAIN = {"exp": 0, "recip": 1, "rsqrt": 2, "gelu": 3, "silu": 4, "sigmoid": 5, "softmax": 6, "layernorm": 7}
+
+    def plain_eval(self, op: str, x: torch.Tensor, rows: int = 1, cols: int | None = None, **kw):
+        """Run one approximation schedule on plaintext fixed-point values (float64 in / out, device).
+        Knobs as the MPC op's keyword arguments."""
+        if x.dtype != torch.float64 or not x.is_cuda:
+            raise ValueError("plain_eval takes a float64 CUDA tensor")
+        x = x.contiguous().view(-1)
+        cols = x.numel() // rows if cols is None else cols
+        y = torch.empty_like(x)
+        if op == "exp":
+            knobs = ExpP(kw.get("t", 8), int(kw.get("clamp", 0)), kw.get("window", 33), 0)
+        elif op in ("recip", "rsqrt"):
+            knobs = NrP(kw.get("iters", 10 if op == "recip" else 3),
+                        ExpP(kw.get("t", 8), int(kw.get("clamp", 0)), kw.get("window", 33), 0))
+        elif op in ("gelu", "silu", "sigmoid"):
+            k = default_act(op, **{a: b for a, b in kw.items() if a in ("form", "degree", "erf_terms", "window", "B",
+                                                                       "coeffs", "basis")})
+            coeffs = k.get("coeffs")
+            arr = (ctypes.c_double * len(coeffs))(*coeffs) if coeffs else None
+            knobs = ActP(FORM[k["form"]], int(k.get("degree", 0)), float(k.get("B", 5.0)),
+                         ctypes.cast(arr, ctypes.POINTER(ctypes.c_double)) if arr is not None else None,
+                         int(k.get("erf_terms", 0)), int(k.get("window", 33)), int(k.get("basis", 0)))
+        elif op == "softmax":
+            knobs = SoftmaxP(kw.get("window", 33), ExpP(kw.get("exp_t", 8), int(kw.get("exp_clamp", 0)), 33, 0),
+                             NrP(kw.get("recip_iters", 10), ExpP(kw.get("recip_t", 8), int(kw.get("recip_clamp", 0)),
+                                                                  33, 0)), 0)
+        elif op == "layernorm":
+            knobs = LnP(kw.get("eps", 1e-5), kw.get("mean_mode", 0),
+                        NrP(kw.get("rsqrt_iters", 3), ExpP(kw.get("rsqrt_t", 8), int(kw.get("rsqrt_clamp", 0)), 33, 0)), 0)
+        else:
+            raise ValueError(op)
+        self._stream()
+        self._chk(_L.mpc_plain_eval(self._h, self.PLAIN[op], ctypes.byref(knobs), _ptr(x), _ptr(y), rows, cols),
+                  "mpc_plain_eval")
+        return y
 
     def square(self, x, off=0, trunc_bits=0, out=None):
         n = x[0].numel() if x[0] is not None else x[1].numel()

@@ -19,6 +19,7 @@
 #include "kernels.cuh"
 #include "matmul.cuh"
 #include "matmul_tc.cuh"
+#include "plain.cuh"
 
 using namespace mpc;
 
@@ -1024,9 +1025,9 @@ static u64 act_steps(int act, const mpc_act_p* p)
     return 2 + 1 + (u64)(p->erf_terms - 2) + 2 + tail;   // ERF
 }
 
-static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p)
+// S13 knob validation + the device knob struct (shared by the MPC ops and the plaintext evaluator)
+static mpc_status act_knobs(mpc_ctx* c, int act, const mpc_act_p* p, ActK& k)
 {
-    if (!c) return MPC_ERR_INVALID;
     if (!p || p->window < 1 || p->window > 64) return fail(c, MPC_ERR_RANGE, "window");
     if (p->form < 0 || p->form > 3) return fail(c, MPC_ERR_RANGE, "form");
     if ((p->form == MPC_FORM_POLY_X || p->form == MPC_FORM_POLY_ABS) && (p->degree < 0 || p->degree > 4))
@@ -1038,11 +1039,6 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
         return fail(c, MPC_ERR_INVALID, "coeffs");
     if (p->basis != 0 && p->basis != 1) return fail(c, MPC_ERR_RANGE, "basis must be 0 (Horner) or 1 (power)");
     if (p->basis == 1 && p->form == MPC_FORM_ERF) return fail(c, MPC_ERR_RANGE, "power basis: x- and |x|-forms only");
-    const u64 steps = act_steps(act, p);
-    mpc_status st = begin(c, steps);
-    if (st) return st;
-    if (bad_sh(c, x) || bad_sh(c, z) || n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "act args (off % 32)");
-    ActK k;
     memset(&k, 0, sizeof k);
     k.act = act; k.form = p->form; k.w = p->window; k.basis = p->form == MPC_FORM_ERF ? 0 : p->basis;
     k.e_B = E(p->B); k.e_mB = E(-p->B); k.e_half = E(0.5); k.e_one = E(1.0);
@@ -1061,6 +1057,19 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
         k.deg = p->degree;
         for (int i = 0; i <= p->degree; ++i) k.c[i] = E(p->coeffs[i]);
     }
+    return MPC_OK;
+}
+
+static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p)
+{
+    if (!c) return MPC_ERR_INVALID;
+    ActK k;
+    mpc_status st = act_knobs(c, act, p, k);
+    if (st) return st;
+    const u64 steps = act_steps(act, p);
+    st = begin(c, steps);
+    if (st) return st;
+    if (bad_sh(c, x) || bad_sh(c, z) || n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "act args (off % 32)");
     const char* name = act == 0 ? "gelu" : act == 1 ? "silu" : "sigmoid";
     if (use_cone(c, k.w))
         st = launch_cone(c, n, (u64)off, ActConeBody{(u32)c->step, k, spv(c, x), sov(c, z), n}, name);
@@ -1082,6 +1091,52 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
 }
 
 extern "C" {
+// NEXT #4: the auto-tuner's plaintext fixed-point evaluator
+mpc_status mpc_plain_eval(mpc_ctx* c, int op, const void* knobs, const double* x, double* y, int64_t rows, int64_t cols)
+{
+    if (!c) return MPC_ERR_INVALID;
+    if (!knobs || !x || !y || rows < 0 || cols < 1) return fail(c, MPC_ERR_INVALID, "plain_eval args");
+    PlainArgs a;
+    memset(&a, 0, sizeof a);
+    a.x = x; a.y = y; a.rows = rows; a.cols = cols;
+    mpc_status st = MPC_OK;
+    switch (op) {
+    case MPC_PLAIN_EXP: {
+        const mpc_exp_p* p = (const mpc_exp_p*)knobs;
+        if (!exp_ok(p)) return fail(c, MPC_ERR_RANGE, "exp knobs");
+        a.op = 0; a.ek = mk_exp(p); break;
+    }
+    case MPC_PLAIN_RECIP: case MPC_PLAIN_RSQRT: {
+        const mpc_nr_p* p = (const mpc_nr_p*)knobs;
+        if (!nr_ok(p)) return fail(c, MPC_ERR_RANGE, "NR knobs");
+        a.op = op == MPC_PLAIN_RECIP ? 1 : 2; a.nk = mk_nr(p); break;
+    }
+    case MPC_PLAIN_GELU: case MPC_PLAIN_SILU: case MPC_PLAIN_SIGMOID:
+        if ((st = act_knobs(c, op - MPC_PLAIN_GELU, (const mpc_act_p*)knobs, a.ak))) return st;
+        a.op = 3; break;
+    case MPC_PLAIN_SOFTMAX: {
+        const mpc_softmax_p* p = (const mpc_softmax_p*)knobs;
+        if (p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip)) return fail(c, MPC_ERR_RANGE, "softmax knobs");
+        a.op = 4; a.ek = mk_exp(&p->exp); a.nk = mk_nr(&p->recip); a.w = p->window; break;
+    }
+    case MPC_PLAIN_LAYERNORM: {
+        const mpc_ln_p* p = (const mpc_ln_p*)knobs;
+        if (!nr_ok(&p->rsqrt) || (p->mean_mode != 0 && p->mean_mode != 1)) return fail(c, MPC_ERR_RANGE, "layernorm knobs");
+        a.op = 5; a.nk = mk_nr(&p->rsqrt); a.mean_mode = p->mean_mode; a.e_invd = E(1.0 / (double)cols); a.e_eps = E(p->eps);
+        break;
+    }
+    default: return fail(c, MPC_ERR_RANGE, "plain_eval: unknown op");
+    }
+    if (rows == 0) return MPC_OK;
+    const i64 work = a.op <= 3 ? rows * cols : rows;
+    rec_begin(c, "plain_eval", (u64)(rows * cols));
+    k_plain<<<grid_for(c, work, 256, 8), 256, 0, c->stream>>>(a);
+    rec_end(c);
+    c->st.launches++;
+    rec_close(c);
+    return cuda_check(c, "plain_eval");
+}
+
 mpc_status mpc_recip(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_nr_p* p) { return nr_common<0>(c, x, z, n, off, p); }
 mpc_status mpc_rsqrt(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_nr_p* p) { return nr_common<1>(c, x, z, n, off, p); }
 mpc_status mpc_gelu(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int64_t off, const mpc_act_p* p) { return act_common(c, 0, x, z, n, off, p); }

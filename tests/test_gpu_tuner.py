@@ -1,0 +1,83 @@
+"""NEXT #4 on the GPU: the plaintext fixed-point evaluator (mpc_plain_eval) against the
+approximation formulas (DESIGN.md 5 bounds, the same as the MPC path's) and against the MPC
+outputs themselves (which differ only by per-share truncation), and an end-to-end tuning run."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import float_ref as fr
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ULP = 2.0 ** -16
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_2511_19711_b200 as mod
+    return mod
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+@pytest.mark.parametrize("t,clamp", [(8, 0), (8, 1), (2, 1), (0, 1)])
+def test_plain_exp_vs_formula_and_mpc(m, t, clamp):
+    c = m.Ctx.for_cfg(workloads.keys(1))
+    x = workloads.exp_inputs(4096, tail_frac=0.05 if clamp else 0.0)
+    xs = c.share(dev(x))
+    xd = c.open(xs)[1]
+    y = c.plain_eval("exp", xd, t=t, clamp=clamp).cpu().numpy()
+    f = fr.exp_limit(xd.cpu().numpy(), t, clamp)
+    mask = np.ones_like(f, bool) if clamp else xd.cpu().numpy() >= -(2.0 ** t)
+    assert np.all(np.abs(y - f)[mask] <= (4 * 2 ** t * ULP * np.maximum(1, np.abs(f)))[mask])
+    ym = c.open(c.exp(xs, t=t, clamp=clamp))[1].cpu().numpy()
+    assert np.all(np.abs(y - ym)[mask] <= (4 * 2 ** t * ULP * np.maximum(1, np.abs(f)))[mask])
+
+
+def test_plain_softmax_layernorm_gelu_vs_formula(m):
+    c = m.Ctx.for_cfg(workloads.keys(2))
+    rows, cols = 64, 128
+    xs = c.share(dev(workloads.softmax_inputs(rows, cols)))
+    xd = c.open(xs)[1]
+    y = c.plain_eval("softmax", xd, rows=rows, cols=cols).cpu().numpy().reshape(rows, cols)
+    assert np.max(np.abs(y - fr.softmax_formula(xd.cpu().numpy().reshape(rows, cols)))) <= (2 * 4 * 256 + 8) * ULP
+    ym = c.open(c.softmax(xs, rows, cols))[1].cpu().numpy().reshape(rows, cols)
+    assert np.max(np.abs(y - ym)) <= 1e-2
+    ls = c.share(dev(workloads.layernorm_inputs(32, 768)))
+    ld = c.open(ls)[1]
+    yl = c.plain_eval("layernorm", ld, rows=32, cols=768).cpu().numpy().reshape(32, 768)
+    assert np.max(np.abs(yl - fr.layernorm_formula(ld.cpu().numpy().reshape(32, 768)))) <= 2e-3
+    k = m.default_act("gelu", "poly_abs", degree=4)
+    gs = c.share(dev(workloads.act_inputs(4096)))
+    gd = c.open(gs)[1]
+    yg = c.plain_eval("gelu", gd, form="poly_abs", degree=4).cpu().numpy()
+    f = fr.act_formula(gd.cpu().numpy(), "gelu", "poly_abs", 4, k["B"], k["coeffs"])
+    assert np.max(np.abs(yg - f)) <= 5e-3
+    ym = c.open(c.gelu(gs, form="poly_abs", degree=4))[1].cpu().numpy()
+    assert np.max(np.abs(yg - ym)) <= 1e-3
+
+
+def test_tuner_end_to_end(m):
+    from paper_2511_19711_b200 import tuner
+    c = m.Ctx.for_cfg(workloads.keys(5))
+    L = [tuner.Layer("attn", "softmax", 256, 128, dev(workloads.softmax_inputs(256, 128)), 256),
+         tuner.Layer("ffn", "gelu", 1, 8192, dev(workloads.normal_inputs(8192, 5)), 1),
+         tuner.Layer("ln", "layernorm", 64, 768, dev(workloads.layernorm_inputs(64, 768)), 64)]
+    ev = tuner.Evaluator(c, objective="gpu")
+    tight = tuner.GreedyTuner(L, ev, threshold=0.0).run()
+    # only moves that change nothing are taken: on these scores (x - max >= -20 > -2^8) the
+    # clamp of exp t=8 never fires, so t=8 without clamp emulates bit-identically
+    assert tight["quality_loss"] == 0.0
+    assert tight["state"][0] <= 1 and tight["state"][1:] == [0, 0]
+    loose = tuner.GreedyTuner(L, ev, threshold=float("inf")).run()
+    assert loose["state"] == [len(l.cands()) - 1 for l in L]
+    # rsqrt with exp t = 0 diverges on variances up to 16 (the NR initializer leaves the domain,
+    # R18): a finite budget rejects it however loose the rest is
+    assert ev.error(L[2], 3) > 1.0
+    mid = tuner.HillClimbTuner(L, ev, threshold=0.05).run()
+    assert mid["quality_loss"] <= 0.05
+    assert mid["cost"] <= mid["cost_most_accurate"]
+    wan = tuner.GreedyTuner(L, tuner.Evaluator(c, objective="wan"), threshold=0.05).run()
+    assert wan["quality_loss"] <= 0.05
