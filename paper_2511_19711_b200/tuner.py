@@ -65,7 +65,10 @@ class Layer:
 class Evaluator:
     """Quality (plaintext emulation) and cost (one MPC run) of candidate knob sets, cached."""
 
-    def __init__(self, ctx, mpc_inputs: Optional[Dict[str, object]] = None, objective: str = "gpu"):
+    def __init__(self, ctx, mpc_inputs: Optional[Dict[str, tuple]] = None, objective: str = "gpu"):
+        """mpc_inputs: op kind -> (shares, rows) of the MPC shape to cost on (default: the layer's
+        calibration inputs); costs are cached per (op, shape, knobs), so layers of the same shape
+        are measured once."""
         self.ctx = ctx
         self.objective = objective
         self.mpc_inputs = mpc_inputs or {}
@@ -86,9 +89,11 @@ class Evaluator:
         return self._err[key]
 
     def cost(self, layer: Layer, k: int) -> dict:
-        key = (layer.name, k)
+        knobs = layer.cands()[k]
+        shares, rows = self.mpc_inputs.get(layer.op, (None, layer.mpc_rows or layer.calib_rows))
+        key = (layer.op, rows, layer.cols, tuple(sorted(knobs.items())))
         if key not in self._cost:
-            self._cost[key] = measure_cost(self.ctx, layer, layer.cands()[k], self.mpc_inputs.get(layer.name))
+            self._cost[key] = measure_cost(self.ctx, layer, knobs, shares, rows)
         return self._cost[key]
 
     def objective_value(self, layer: Layer, k: int) -> float:
@@ -99,11 +104,11 @@ class Evaluator:
         return 1e3 * (c["rounds"] * lat + c["bytes_per_party"] / bw) + c["ms"]
 
 
-def measure_cost(ctx, layer: Layer, knobs: dict, shares=None, reps: int = 3) -> dict:
+def measure_cost(ctx, layer: Layer, knobs: dict, shares=None, rows: Optional[int] = None, reps: int = 3) -> dict:
     """One MPC run of the layer's op with these knobs (BOTH mode): ms (CUDA events, mean of reps after
     a warm-up), bytes per party and rounds from the context's protocol counters."""
     import torch
-    rows = layer.mpc_rows or layer.calib_rows
+    rows = rows or layer.mpc_rows or layer.calib_rows
     if shares is None:
         shares = ctx.share(layer.calib.reshape(-1)[: rows * layer.cols].contiguous())
     fn = _mpc_call(ctx, layer, knobs, shares, rows)

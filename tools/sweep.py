@@ -256,6 +256,39 @@ def sec_cfg5(S):
         out[f"gpt2_12layers_{name}"] = S.line(c, step, 12 * n_layer + rl * d,
                                               f"cfg5 GPT-2 small 12 layers x (LN, softmax 24576x1024, LN, GELU "
                                               f"2048x3072) + final LN, 2 sequences, schedule {name}")
+    # BASELINE cfg5 "per-layer auto-tuned approximation choices": the NEXT #4 tuner over the 49
+    # layers, calibration samples per layer (score spread and LN row statistics vary with depth),
+    # quality = summed per-layer max error vs the most accurate candidate, cost = measured MPC
+    # time on this shard's shapes plus the paper's LAN model
+    from paper_2511_19711_b200 import tuner as T
+    dev = S.job.dev
+    layers = []
+    for l in range(12):
+        sig = 1.0 + 0.25 * l
+        layers.append(T.Layer(f"ln1_{l}", "layernorm", rl, d, torch.from_numpy(
+            workloads.layernorm_inputs(64, d, seed_cfg=100 + l)).to(dev), 64))
+        layers.append(T.Layer(f"attn_{l}", "softmax", rs, cs, torch.from_numpy(
+            workloads.softmax_inputs(64, cs, seed_cfg=200 + l, sigma=sig)).to(dev), 64))
+        layers.append(T.Layer(f"ln2_{l}", "layernorm", rl, d, torch.from_numpy(
+            workloads.layernorm_inputs(64, d, seed_cfg=300 + l) * (0.5 + 0.1 * l)).to(dev), 64))
+        layers.append(T.Layer(f"ffn_{l}", "gelu", 1, 8192, torch.from_numpy(
+            workloads.normal_inputs(8192, 400 + l, sigma=sig)).to(dev), 1))
+    ev = T.Evaluator(c, mpc_inputs={"softmax": (sm, rs), "layernorm": (ln, rl), "gelu": (g, 1)}, objective="lan")
+    tuned = T.HillClimbTuner(layers, ev, threshold=0.25).run()
+    knobs = tuned["knobs"]
+
+    def step_tuned():
+        for l in range(12):
+            c.layernorm(ln, rl, d, out=zl, **knobs[f"ln1_{l}"])
+            c.softmax(sm, rs, cs, out=zs, **knobs[f"attn_{l}"])
+            c.layernorm(ln, rl, d, out=zl, **knobs[f"ln2_{l}"])
+            c.gelu(g, out=zg, **knobs[f"ffn_{l}"])
+        c.layernorm(ln, rl, d, out=zl)
+    r = S.line(c, step_tuned, 12 * n_layer + rl * d, "cfg5 GPT-2 small 12 layers, per-layer knobs from the "
+               "NEXT #4 hill-climbing tuner (LAN objective, summed max-error budget 0.25)")
+    r["tuned"] = {"knobs": knobs, "quality_loss": tuned["quality_loss"], "lan_cost_ms": tuned["cost"],
+                  "lan_cost_most_accurate_ms": tuned["cost_most_accurate"], "steps": tuned["steps"]}
+    out["gpt2_12layers_autotuned"] = r
     out["softmax1024_t8"] = S.line(c, lambda: c.softmax(sm, rs, cs, out=zs), rs * cs, "cfg5 softmax layer, t=8 NR 10")
     out["gelu_poly_abs4"] = S.line(c, lambda: c.gelu(g, form="poly_abs", degree=4, out=zg), ng,
                                    "cfg5 GELU layer |x|-form deg 4")
