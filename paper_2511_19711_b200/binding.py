@@ -114,6 +114,7 @@ _SIGS = {
     "mpc_max": [VP, Shares, Shares, i64, i64, i64, INT],
     "mpc_maxpool2d": [VP, Shares, Shares, INT, INT, INT, INT, INT, INT, INT, i64, INT],
     "mpc_softmax": [VP, Shares, Shares, i64, i64, i64, C(SoftmaxP)],
+    "mpc_softmax_hostio": [VP, Shares, Shares, i64, i64, i64, C(SoftmaxP), i64],
     "mpc_layernorm": [VP, Shares, Shares, i64, i64, i64, C(LnP)],
 }
 _RESTYPE = {"mpc_ctx_get_step": u64, "mpc_last_error": ctypes.c_char_p, "mpc_version": ctypes.c_char_p,
@@ -170,6 +171,19 @@ def _sh(pair):
     s = Shares()
     s.sh[0] = _ptr(pair[0]) if pair[0] is not None else None
     s.sh[1] = _ptr(pair[1]) if pair[1] is not None else None
+    return s
+
+
+def _sh_host(pair):
+    s = Shares()
+    for p in (0, 1):
+        t = pair[p]
+        if t is None:
+            s.sh[p] = None
+            continue
+        if t.is_cuda or t.dtype != torch.uint64 or not t.is_contiguous():
+            raise ValueError("host-buffer calls take contiguous CPU uint64 tensors (pinned for overlap)")
+        s.sh[p] = t.data_ptr()
     return s
 
 
@@ -432,6 +446,18 @@ class Ctx:
         self._stream()
         self._chk(_L.mpc_softmax(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)), "mpc_softmax")
         return z
+
+    def softmax_hostio(self, hx, hz, rows, cols, row_off=0, chunk_rows=2048, window=33, exp_t=8, exp_clamp=0,
+                       exp_window=33, recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0,
+                       recip_square=0, bcast=0):
+        """Softmax over HOST buffers (hx, hz: per-party CPU uint64 tensors, pinned): chunked, with the
+        H2D copies, the compute and the D2H copies of neighbouring chunks overlapped."""
+        p = SoftmaxP(window, ExpP(exp_t, int(exp_clamp), exp_window, int(exp_square)),
+                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))), int(bcast))
+        self._stream()
+        self._chk(_L.mpc_softmax_hostio(self._h, _sh_host(hx), _sh_host(hz), rows, cols, row_off, ctypes.byref(p),
+                                        chunk_rows), "mpc_softmax_hostio")
+        return hz
 
     def layernorm(self, x, rows, cols, row_off=0, eps=1e-5, mean_mode=0, rsqrt_iters=3, rsqrt_t=8,
                   rsqrt_clamp=0, rsqrt_window=33, rsqrt_square=0, bcast=0, out=None):

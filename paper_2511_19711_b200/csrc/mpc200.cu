@@ -59,6 +59,19 @@ struct mpc_ctx {
     int connected;
     int circuit;            // LTZ carry circuit: 0 Kogge-Stone, 1 carry cone (2.7)
     int mm_engine;          // mpc_matmul ring GEMM: 0 auto, 1 SIMT, 2 tensor cores
+    struct HostIO* hio;     // pipelined host-buffer execution (mpc_softmax_hostio), lazily created
+};
+
+// Pipelined host-buffer execution: chunk i goes H2D on `h2d`, computes on cs[i % HIO_SLOTS] with its
+// own staging buffers and kernel scratch, and comes back D2H on `d2h` -- the copy engines (both
+// PCIe directions) overlap each other and the compute of the neighbouring chunks.
+constexpr int HIO_SLOTS = 4;
+struct HostIO {
+    cudaStream_t h2d, d2h, cs[HIO_SLOTS];
+    cudaEvent_t in_ready[HIO_SLOTS], comp_done[HIO_SLOTS], out_done[HIO_SLOTS], start;
+    u64* dbuf[HIO_SLOTS]; size_t dbuf_bytes[HIO_SLOTS];
+    void* scr[HIO_SLOTS]; size_t scr_bytes[HIO_SLOTS];
+    bool used[HIO_SLOTS];
 };
 
 static bool is_pair(const mpc_ctx* c) { return c->cfg.mode != MPC_MODE_BOTH; }
@@ -593,6 +606,19 @@ mpc_status mpc_ctx_destroy(mpc_ctx* c)
     for (int i = 0; i < c->npool; ++i) cudaEventDestroy(c->pool[i]);
     free(c->recs); free(c->pool);
     if (c->scratch) { cudaFreeAsync(c->scratch, c->stream); cudaStreamSynchronize(c->stream); }
+    if (c->hio) {
+        HostIO* h = c->hio;
+        for (int b = 0; b < HIO_SLOTS; ++b) {
+            cudaStreamSynchronize(h->cs[b]);
+            if (h->dbuf[b]) cudaFree(h->dbuf[b]);
+            if (h->scr[b]) cudaFree(h->scr[b]);
+            cudaStreamDestroy(h->cs[b]);
+            cudaEventDestroy(h->in_ready[b]); cudaEventDestroy(h->comp_done[b]); cudaEventDestroy(h->out_done[b]);
+        }
+        cudaStreamSynchronize(h->h2d); cudaStreamSynchronize(h->d2h);
+        cudaStreamDestroy(h->h2d); cudaStreamDestroy(h->d2h); cudaEventDestroy(h->start);
+        delete h;
+    }
     if (c->peer_base) cudaIpcCloseMemHandle(c->peer_base);
     for (int i = 0; i < 2; ++i) if (c->xa[i].base) cudaFree(c->xa[i].base);
     delete c;
@@ -1216,6 +1242,10 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
     return MPC_OK;
 }
 
+static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off,
+                               const mpc_softmax_p* p, u32 s0);
+static void acct_softmax(mpc_ctx* c, int64_t rows, int64_t cols, const mpc_softmax_p* p);
+
 mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off,
                        const mpc_softmax_p* p)
 {
@@ -1229,8 +1259,108 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
     if (bad_sh(c, x) || bad_sh(c, z) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31))
         return fail(c, MPC_ERR_INVALID, "softmax args (row_off % 32)");
     if (rows > 0) {
+        if ((st = softmax_core(c, x, z, rows, cols, row_off, p, (u32)c->step))) return st;
+        acct_softmax(c, rows, cols, p);
+    }
+    finish(c, steps);
+    return MPC_OK;
+}
+
+// pipelined host-buffer softmax (see HostIO): same steps, units and output shares as mpc_softmax
+mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t rows, int64_t cols, int64_t row_off,
+                              const mpc_softmax_p* p, int64_t chunk_rows)
+{
+    if (!c) return MPC_ERR_INVALID;
+    if (!p || p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip))
+        return fail(c, MPC_ERR_RANGE, "softmax knobs");
+    const int L = max_levels_h(cols);
+    const u64 steps = 2ull * (u64)L + exp_steps_h(&p->exp) + exp_steps_h(&p->recip.exp) + 2ull * (u64)p->recip.iters + 1;
+    mpc_status st = begin(c, steps);
+    if (st) return st;
+    if (bad_sh(c, hx) || bad_sh(c, hz) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31) ||
+        chunk_rows < 32 || (chunk_rows & 31))
+        return fail(c, MPC_ERR_INVALID, "softmax_hostio args (row_off, chunk_rows % 32)");
+    if (rows == 0) { finish(c, steps); return MPC_OK; }
+    if (!c->hio) {
+        HostIO* h = new HostIO();
+        memset(h, 0, sizeof *h);
+        cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming);
+        for (int b = 0; b < HIO_SLOTS; ++b) {
+            cudaStreamCreateWithFlags(&h->cs[b], cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&h->in_ready[b], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&h->comp_done[b], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&h->out_done[b], cudaEventDisableTiming);
+        }
+        c->hio = h;
+        if ((st = cuda_check(c, "hostio setup"))) return st;
+    }
+    HostIO* h = c->hio;
+    const int parties[2] = {0, 1};
+    const int np = c->cfg.mode == MPC_MODE_PAIR ? 1 : 2;
+    const int p0 = c->cfg.mode == MPC_MODE_PAIR ? c->cfg.party : 0;
+    // PAIR kernels own the per-warp exchange slots: their chunks run one after another
+    const int nslots = is_pair(c) ? 1 : HIO_SLOTS;
+    const size_t half = sizeof(u64) * (size_t)chunk_rows * (size_t)cols;       // one party, one array
+    cudaStream_t user = c->stream;
+    cudaEventRecord(h->start, user);
+    cudaStreamWaitEvent(h->h2d, h->start, 0);
+    const u32 s0 = (u32)c->step;
+    const i64 nchunks = (rows + chunk_rows - 1) / chunk_rows;
+    for (i64 i = 0; i < nchunks; ++i) {
+        const int b = (int)(i % HIO_SLOTS);
+        const int cb = (int)(i % nslots);
+        const i64 r0 = i * chunk_rows, ri = std::min<i64>(chunk_rows, rows - r0);
+        const size_t bytes = sizeof(u64) * (size_t)(ri * cols);
+        if (!h->dbuf[b] || h->dbuf_bytes[b] < 4 * half) {
+            if (h->dbuf[b]) { cudaStreamSynchronize(h->d2h); cudaFree(h->dbuf[b]); }
+            if (cudaMalloc(&h->dbuf[b], 4 * half) != cudaSuccess) { h->dbuf[b] = nullptr; return fail(c, MPC_ERR_NOMEM, "hostio staging"); }
+            h->dbuf_bytes[b] = 4 * half;
+        }
+        u64* dx[2] = {h->dbuf[b], h->dbuf[b] + half / 8};
+        u64* dz[2] = {h->dbuf[b] + 2 * (half / 8), h->dbuf[b] + 3 * (half / 8)};
+        if (h->used[b]) cudaStreamWaitEvent(h->h2d, h->out_done[b], 0);
+        for (int q = 0; q < np; ++q) {
+            const int pp = parties[p0 + q];
+            cudaMemcpyAsync(dx[pp], hx.sh[pp] + r0 * cols, bytes, cudaMemcpyHostToDevice, h->h2d);
+        }
+        cudaEventRecord(h->in_ready[b], h->h2d);
+        cudaStreamWaitEvent(h->cs[cb], h->in_ready[b], 0);
+        // launch on the slot's stream with the slot's own scratch
+        void* save_scr = c->scratch; size_t save_bytes = c->scratch_bytes;
+        c->stream = h->cs[cb]; c->scratch = h->scr[cb]; c->scratch_bytes = h->scr_bytes[cb];
+        mpc_shares xs{{dx[0], dx[1]}}, zs{{dz[0], dz[1]}};
+        if (c->cfg.mode == MPC_MODE_PAIR) { xs.sh[1 - c->cfg.party] = nullptr; zs.sh[1 - c->cfg.party] = nullptr; }
+        st = softmax_core(c, xs, zs, ri, cols, row_off + r0, p, s0);
+        h->scr[cb] = c->scratch; h->scr_bytes[cb] = c->scratch_bytes;
+        c->scratch = save_scr; c->scratch_bytes = save_bytes; c->stream = user;
+        if (st) return st;
+        cudaEventRecord(h->comp_done[b], h->cs[cb]);
+        cudaStreamWaitEvent(h->d2h, h->comp_done[b], 0);
+        for (int q = 0; q < np; ++q) {
+            const int pp = parties[p0 + q];
+            cudaMemcpyAsync(hz.sh[pp] + r0 * cols, dz[pp], bytes, cudaMemcpyDeviceToHost, h->d2h);
+        }
+        cudaEventRecord(h->out_done[b], h->d2h);
+        h->used[b] = true;
+    }
+    cudaEventRecord(h->start, h->d2h);
+    cudaStreamWaitEvent(user, h->start, 0);          // the call completes in the caller's stream order
+    if ((st = cuda_check(c, "softmax_hostio"))) return st;
+    acct_softmax(c, rows, cols, p);
+    finish(c, steps);
+    return MPC_OK;
+}
+
+static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off,
+                               const mpc_softmax_p* p, u32 s0)
+{
+    const int L = max_levels_h(cols);
+    mpc_status st;
+    {
         SoftmaxArgs a;
-        a.s_max = (u32)c->step;
+        a.s_max = s0;
         a.s_exp = a.s_max + 2u * (u32)L;
         a.s_rec = a.s_exp + (u32)exp_steps_h(&p->exp);
         a.s_mul = a.s_rec + (u32)exp_steps_h(&p->recip.exp) + 2u * (u32)p->recip.iters;
@@ -1244,16 +1374,18 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
         st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax")
            : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax")
                     : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax");
-        if (st) return st;
-        const i64 n = rows * cols;
-        acct_max(c, rows, cols, p->window);
-        acct_exp(c, (u64)n, &p->exp);
-        acct_exp(c, (u64)rows, &p->recip.exp);
-        for (int i = 0; i < 2 * p->recip.iters; ++i) acct_beaver(c, (u64)rows);
-        if (p->bcast) acct_bcast(c, (u64)n, (u64)rows); else acct_beaver(c, (u64)n);
     }
-    finish(c, steps);
-    return MPC_OK;
+    return st;
+}
+
+static void acct_softmax(mpc_ctx* c, int64_t rows, int64_t cols, const mpc_softmax_p* p)
+{
+    const i64 n = rows * cols;
+    acct_max(c, rows, cols, p->window);
+    acct_exp(c, (u64)n, &p->exp);
+    acct_exp(c, (u64)rows, &p->recip.exp);
+    for (int i = 0; i < 2 * p->recip.iters; ++i) acct_beaver(c, (u64)rows);
+    if (p->bcast) acct_bcast(c, (u64)n, (u64)rows); else acct_beaver(c, (u64)n);
 }
 
 mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off,
