@@ -43,6 +43,31 @@ def run(mode, circuit):
     c.maxpool2d(p, 1, 4, 9, 10)
     ln = sh(workloads.layernorm_inputs(40, 96))
     c.layernorm(ln, 40, 96)
+    # round-1b additions: short-row max / MaxPool windows, NEXT #2 (broadcast triple, power basis),
+    # NEXT #3 (Beaver matmul, both engines), NEXT #4 (plaintext evaluator), host-buffer softmax
+    c.max(s, 45, 9)
+    c.maxpool2d(p, 1, 4, 9, 10, k=2, stride=2, pad=0)
+    y = sh(workloads.recip_inputs(45))
+    c.mul_bcast(s, y, 45, 77, off=1, row_off=3, trunc_bits=16)
+    c.softmax(s, 45, 77, bcast=1)
+    c.layernorm(ln, 40, 96, bcast=1)
+    c.gelu(x, form="poly_abs", degree=4, basis=1)
+    c.sigmoid(x, form="poly_x", degree=3, B=4.0, coeffs=[0.5, 0.2, 0.0, -0.01], basis=1)
+    a = sh(workloads.act_inputs(2 * 70 * 33))
+    b = sh(workloads.act_inputs(2 * 33 * 129, seed_cfg=5))
+    # MPC_SAN_TC=0 skips the tensor-core engine (its TMA / tcgen05 async-proxy ordering through
+    # mbarriers is not modelled by racecheck / synccheck, which report false hazards there)
+    for eng in ((1, 2) if os.environ.get("MPC_SAN_TC", "1") == "1" else (1,)):
+        c.set_matmul_engine(eng)
+        c.matmul(a, b, 2, 70, 33, 129, batch_off=1, trunc_bits=16)
+    if mode == m.binding.MODE_BOTH:
+        xd = c.open(s)[1]
+        c.plain_eval("softmax", xd, rows=45, cols=77)
+        c.plain_eval("gelu", c.open(x)[1], form="poly_abs", degree=4)
+        c.plain_eval("layernorm", c.open(ln)[1], rows=40, cols=96)
+    hx = tuple(t.cpu().pin_memory() for t in s)
+    hz = tuple(torch.empty_like(t).pin_memory() for t in hx)
+    c.softmax_hostio(hx, hz, 45, 77, chunk_rows=32)
     if mode != m.binding.MODE_BOTH:
         c.sync()
     torch.cuda.synchronize()
