@@ -13,16 +13,23 @@
 // between 8-row groups), one contiguous chunk per (row block, K block of 32) holding all 8
 // limbs: A chunk = 8 x (128 x 32 B) = 32 KB, B chunk = 8 x (64 x 32 B) = 16 KB.  A stage is
 // therefore two flat cp.async.bulk copies (TMA without tensor maps) completing on an mbarrier.
-// One CTA = one 128 x 64 output tile (512 TMEM columns = 8 accumulators x 64); thread 0
-// issues the copies (3-stage ring) and 12 tcgen05.mma per K block (A limb i against the
-// stacked B limbs 0..7-i, N up to 256), all 4 warps run the epilogue (warp w owns TMEM lanes
-// 32w..32w+31 = rows).
+// One CTA = one 128 x TC_BN output tile (8 accumulators x TC_BN TMEM columns); thread 0 issues
+// the copies (2-3 stage ring) and one tcgen05.mma per A limb i against the stacked B limbs
+// 0..7-i (N = TC_BN (8-i) <= 256; split in two at TC_BN = 64) per K block; all 4 warps run the
+// epilogue (warp w owns TMEM lanes 32w..32w+31 = rows).
 #pragma once
 #include "matmul.cuh"
 
 namespace mpc {
 
-constexpr int TC_BM = 128, TC_BN = 64, TC_BK = 32, TC_STAGES = 3;
+// Output tile 128 x TC_BN: 8 accumulators take 8 * TC_BN TMEM columns.  TC_BN = 32 (default) uses
+// 256 columns and ~80 KB of shared memory, so TWO CTAs share an SM and one CTA's epilogue overlaps
+// the other's MMAs; TC_BN = 64 fills TMEM (one CTA per SM, epilogue serialised with the MMAs).
+#ifndef MPC_TC_BN
+#define MPC_TC_BN 32
+#endif
+constexpr int TC_BM = 128, TC_BN = MPC_TC_BN, TC_BK = 32, TC_STAGES = TC_BN == 32 ? 2 : 3;
+constexpr int TC_CTAS_PER_SM = TC_BN == 32 ? 2 : 1, TC_TMEM_COLS = 8 * TC_BN;
 constexpr int TC_A_TILE = TC_BM * TC_BK, TC_B_TILE = TC_BN * TC_BK;          // bytes per limb tile
 constexpr int TC_A_CHUNK = 8 * TC_A_TILE, TC_B_CHUNK = 8 * TC_B_TILE;          // bytes per stage
 constexpr int TC_SMEM = TC_STAGES * (TC_A_CHUNK + TC_B_CHUNK) + 1024;
@@ -121,6 +128,50 @@ __global__ void __launch_bounds__(256) k_mm_limbs_rhs(LimbArgs a)
     }
 }
 
+// LHS limb tiling through shared memory: one CTA per (batch, 128-row block, K block of 32):
+// coalesced loads of 128 rows x 32 k' (each row 256 contiguous bytes), then 256 threads pack the
+// 128 x 2 core-matrix rows of all 8 limbs and write the 32 KB chunk contiguously.
+__global__ void __launch_bounds__(256) k_mm_limbs_lhs(LimbArgs a)
+{
+    __shared__ u64 sm[TC_BM][TC_BK + 1];
+    const int KB = a.Kp / TC_BK, MB = (a.rows + TC_BM - 1) / TC_BM;
+    const int Ktot = a.nt * a.K;
+    const i64 ntile = (i64)a.batch * MB * KB;
+    for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int b = (int)(tile / ((i64)MB * KB));
+        const int rem = (int)(tile - (i64)b * MB * KB), mb = rem / KB, kb = rem - (rem / KB) * KB;
+        for (int l = threadIdx.x; l < TC_BM * TC_BK; l += blockDim.x) {
+            const int r = l / TC_BK, kc = l - r * TC_BK;
+            const int kk = kb * TC_BK + kc, m = mb * TC_BM + r;
+            u64 v = 0;
+            if (kk < Ktot && m < a.rows) {
+                const int t = kk / a.K, k = kk - t * a.K;
+                v = a.t[t][(i64)b * a.in_stride + (i64)m * a.K + k];
+            }
+            sm[r][kc] = v;
+        }
+        __syncthreads();
+        {
+            const int r = threadIdx.x >> 1, ch = threadIdx.x & 1;
+            uint4 limb[8];
+            u32* lw = reinterpret_cast<u32*>(limb);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) lw[q] = 0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const u64 v = sm[r][ch * 16 + e];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) lw[i * 4 + (e >> 2)] |= ((u32)(v >> (8 * i)) & 0xffu) << (8 * (e & 3));
+            }
+            u8* dst = a.out + (((i64)b * MB + mb) * KB + kb) * (i64)TC_A_CHUNK;
+            const int off = tc_tile_off(r, ch * 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + (i64)i * TC_A_TILE + off) = limb[i];
+        }
+        __syncthreads();
+    }
+}
+
 // ---- PTX helpers ------------------------------------------------------------------------------
 __device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(u64* bar, u32 count)
@@ -184,7 +235,7 @@ struct TcArgs {
     int Kp[2];                 // padded K' per party
 };
 
-__global__ void __launch_bounds__(128, 1) k_mm_tc(const __grid_constant__ TcArgs t)
+__global__ void __launch_bounds__(128, TC_CTAS_PER_SM) k_mm_tc(const __grid_constant__ TcArgs t)
 {
     extern __shared__ __align__(1024) u8 smem_raw[];
     u8* smem = (u8*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -207,7 +258,7 @@ __global__ void __launch_bounds__(128, 1) k_mm_tc(const __grid_constant__ TcArgs
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" :: "r"(smem_u32(&tmem_base_sh)) : "memory");
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(&tmem_base_sh)), "n"(TC_TMEM_COLS) : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -239,10 +290,12 @@ __global__ void __launch_bounds__(128, 1) k_mm_tc(const __grid_constant__ TcArgs
                 const u64 ad = umma_desc(As_ + i * TC_A_TILE);
                 const u32 acc = (kb > 0 || i > 0) ? 1u : 0u;     // S_0..S_7 all first written at i = 0
                 const int nj = 8 - i;
-                const int n1 = nj > 4 ? 4 : nj;
+                constexpr int JMAX = 256 / TC_BN;                 // limbs per MMA (N <= 256)
+                const int n1 = nj > JMAX ? JMAX : nj;
                 umma_i8(tmem + (u32)(i * TC_BN), ad, umma_desc(Bs_), tc_idesc(n1 * TC_BN), acc);
-                if (nj > 4)
-                    umma_i8(tmem + (u32)((i + 4) * TC_BN), ad, umma_desc(Bs_ + 4 * TC_B_TILE), tc_idesc((nj - 4) * TC_BN), acc);
+                if (nj > JMAX)
+                    umma_i8(tmem + (u32)((i + JMAX) * TC_BN), ad, umma_desc(Bs_ + JMAX * TC_B_TILE),
+                            tc_idesc((nj - JMAX) * TC_BN), acc);
             }
             umma_commit(&empty_bar[s]);                   // frees stage s once these MMAs complete
             if (kb + TC_STAGES < KB) {
@@ -281,7 +334,7 @@ __global__ void __launch_bounds__(128, 1) k_mm_tc(const __grid_constant__ TcArgs
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tmem) : "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "n"(TC_TMEM_COLS) : "memory");
 }
 
 }  // namespace mpc

@@ -941,7 +941,8 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
             lb.in_stride = K * N; lb.out = LB[p];
             const i64 wa = batch * MB * TC_BM * (Kps[p] / 16), wb = batch * NB * TC_BN * (Kps[p] / 16);
             rec_begin(c, "mm_limbs", 0);
-            k_mm_limbs<<<grid_for(c, wa, 256, 8), 256, 0, c->stream>>>(la);
+            (void)wa;
+            k_mm_limbs_lhs<<<(unsigned)std::min<i64>(batch * MB * (Kps[p] / TC_BK), (i64)c->sm_count * 8), 256, 0, c->stream>>>(la);
             (void)wb;
             k_mm_limbs_rhs<<<(unsigned)std::min<i64>(batch * NB * (Kps[p] / TC_BK), (i64)c->sm_count * 8), 256, 0, c->stream>>>(lb);
             rec_end(c);
