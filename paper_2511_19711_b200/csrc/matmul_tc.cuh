@@ -8,11 +8,12 @@
 // its low 64 - 8s <= 32 bits survive the shift, so the 32-bit wrap of the accumulator is
 // harmless.  The epilogue forms sum_s (u64)S_s << 8s, adds +-C0 from the PRG and truncates.
 //
-// Operands are pre-tiled by k_mm_limbs into the UMMA canonical K-major layout without
+// Operands are pre-tiled by k_mm_limbs_lhs / _rhs into the UMMA canonical K-major layout without
 // swizzle (core matrix = 8 rows x 16 B; LBO = 128 B between the two 16-B K-chunks, SBO = 256 B
 // between 8-row groups), one contiguous chunk per (row block, K block of 32) holding all 8
-// limbs: A chunk = 8 x (128 x 32 B) = 32 KB, B chunk = 8 x (64 x 32 B) = 16 KB.  A stage is
-// therefore two flat cp.async.bulk copies (TMA without tensor maps) completing on an mbarrier.
+// limbs: A chunk = 8 x (128 x 32 B) = 32 KB, B chunk = 8 x (TC_BN x 32 B) = 8 KB at TC_BN = 32.
+// A stage is therefore two flat cp.async.bulk copies (TMA without tensor maps) completing on an
+// mbarrier.
 // One CTA = one 128 x TC_BN output tile (8 accumulators x TC_BN TMEM columns); thread 0 issues
 // the copies (2-3 stage ring) and one tcgen05.mma per A limb i against the stacked B limbs
 // 0..7-i (N = TC_BN (8-i) <= 256; split in two at TC_BN = 64) per K block; all 4 warps run the
@@ -40,50 +41,11 @@ __host__ __device__ inline int tc_tile_off(int r, int kb) { return (r >> 3) * 25
 // ---- limb tiling ------------------------------------------------------------------------------
 // Operand of one party: up to three terms concatenated along K (K' = nt * K).  LHS terms are
 // [batch][M][K] (rows = m), RHS terms [batch][K][N] (rows = n, transposed to K-major).  Output:
-// [batch][row block][K block][limb][tile], zero padded to whole blocks.  One thread packs one
+// [batch][row block][K block][limb][tile], zero padded to whole blocks.  A thread packs one
 // 16-byte core-matrix row (16 consecutive k' of one row) for all 8 limbs.
 struct LimbArgs {
     const u64* t[3]; int nt; int rows, K, Kp, rhs, rows_blk; int batch; i64 in_stride; u8* out;
 };
-__global__ void __launch_bounds__(256) k_mm_limbs(LimbArgs a)
-{
-    const int kchunks = a.Kp / 16;                          // 16-byte chunks per padded row
-    const i64 rows_p = (i64)((a.rows + a.rows_blk - 1) / a.rows_blk) * a.rows_blk;
-    const i64 per_b = rows_p * kchunks;
-    const i64 total = per_b * a.batch;
-    const int Ktot = a.nt * a.K;
-    for (i64 idx = blockIdx.x * (i64)blockDim.x + threadIdx.x; idx < total; idx += (i64)gridDim.x * blockDim.x) {
-        const int b = (int)(idx / per_b);
-        const i64 rem = idx - (i64)b * per_b;
-        const int r = (int)(rem / kchunks), kc = (int)(rem % kchunks);
-        uint4 limb[8];
-        u32* lw = reinterpret_cast<u32*>(limb);
-#pragma unroll
-        for (int q = 0; q < 32; ++q) lw[q] = 0;
-        if (r < a.rows) {
-#pragma unroll 4
-            for (int e = 0; e < 16; ++e) {
-                const int kk = kc * 16 + e;
-                if (kk >= Ktot) break;
-                const int t = kk / a.K, k = kk - t * a.K;
-                const u64* base = a.t[t] + (i64)b * a.in_stride;
-                const u64 v = a.rhs ? base[(i64)k * a.rows + r] : base[(i64)r * a.K + k];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const u32 byte = (u32)(v >> (8 * i)) & 0xffu;
-                    lw[i * 4 + (e >> 2)] |= byte << (8 * (e & 3));
-                }
-            }
-        }
-        const int rb = r / a.rows_blk, rr = r - rb * a.rows_blk, kb = kc / 2;
-        const int tile = a.rows_blk * TC_BK;
-        u8* dst = a.out + (((i64)b * (rows_p / a.rows_blk) + rb) * (a.Kp / TC_BK) + kb) * (8 * (i64)tile);
-        const int off = tc_tile_off(rr, (kc & 1) * 16);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + (i64)i * tile + off) = limb[i];
-    }
-}
-
 // RHS limb tiling through a shared-memory transpose: one CTA per (batch, 64-column block, K block
 // of 32): coalesced loads of 32 rows x 64 columns, then 128 threads pack the 64 x 2 core-matrix
 // rows of all 8 limbs and write the 16 KB chunk contiguously.

@@ -939,11 +939,8 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
             la.in_stride = M * K; la.out = LA[p];
             lb.rows = (int)N; lb.K = (int)K; lb.Kp = (int)Kps[p]; lb.rhs = 1; lb.rows_blk = TC_BN; lb.batch = (int)batch;
             lb.in_stride = K * N; lb.out = LB[p];
-            const i64 wa = batch * MB * TC_BM * (Kps[p] / 16), wb = batch * NB * TC_BN * (Kps[p] / 16);
             rec_begin(c, "mm_limbs", 0);
-            (void)wa;
             k_mm_limbs_lhs<<<(unsigned)std::min<i64>(batch * MB * (Kps[p] / TC_BK), (i64)c->sm_count * 8), 256, 0, c->stream>>>(la);
-            (void)wb;
             k_mm_limbs_rhs<<<(unsigned)std::min<i64>(batch * NB * (Kps[p] / TC_BK), (i64)c->sm_count * 8), 256, 0, c->stream>>>(lb);
             rec_end(c);
             c->st.launches += 2;
