@@ -170,7 +170,10 @@ __device__ __forceinline__ u64 globaltimer()
 }
 
 struct PairP {
-    static constexpr int kV = 1;   // unit pairs per lane per pass (V = 4 measured slower in loopback)
+#ifndef MPC_PAIR_KV
+#define MPC_PAIR_KV 2
+#endif
+    static constexpr int kV = MPC_PAIR_KV;   // unit pairs per lane per exchange round (2: loopback softmax 5 %, mul 18 % faster than 1)
     const Keys* Kp;          // kernel parameter space (__grid_constant__)
     int pty;                 // 0 | 1
     // per-warp exchange state (set by bind())
