@@ -513,14 +513,22 @@ struct SoftmaxArgs {
     u64* escratch;          // per-CTA exp tile E (2 x 32 x cols), global (L2-resident)
     int cone;               // carry-cone LTZ in the max tree (NEXT #1)
     int bcast;              // broadcast triple for the final e * r (NEXT #2)
+    int esmem;              // E tile in the work area (aliasing the dead max-tree levels), not escratch
 };
 
 // work tile (u64 words), HA = ceil(cols/2), HB = ceil(HA/2): A0 A1 (2 x 32HA), B0 B1 (2 x 32HB),
-// MX0 MX1 S0 S1 R0 R1 (6 x 32), broadcast-triple rows b0 b1 f (3 x 32).  E lives in escratch.
-__host__ __device__ inline i64 softmax_work_u64(i64 cols)
+// then at softmax_x_off: MX0 MX1 S0 S1 R0 R1 (6 x 32), broadcast-triple rows b0 b1 f (3 x 32).
+// With esmem the exp tile E (2 x 32 x cols) reuses the max-tree levels' space (they are dead
+// once the row maxima are in MX), so X starts after max(64 HA + 64 HB, 64 cols); otherwise E
+// lives in the per-CTA global escratch (L2).
+__host__ __device__ inline i64 softmax_x_off(i64 cols, bool esmem)
 {
     const i64 HA = (cols + 1) / 2, HB = (HA + 1) / 2;
-    return 64 * HA + 64 * HB + 9 * 32;
+    return esmem ? (64 * cols > 64 * HA + 64 * HB ? 64 * cols : 64 * HA + 64 * HB) : 64 * HA + 64 * HB;
+}
+__host__ __device__ inline i64 softmax_work_u64(i64 cols, bool esmem = false)
+{
+    return softmax_x_off(cols, esmem) + 9 * 32;
 }
 
 // LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33) --
@@ -539,9 +547,9 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     u64* W = a.use_smem ? smem : a.gscratch + (i64)wslot * a.work_u64;
     const i64 C = a.cols, HA = (C + 1) / 2, HB = (HA + 1) / 2;
     SO A{{W, W + 32 * HA}}, B{{W + 64 * HA, W + 64 * HA + 32 * HB}};
-    u64* Ew = a.escratch + (i64)wslot * 64 * C;
+    u64* Ew = a.esmem ? W : a.escratch + (i64)wslot * 64 * C;
     SO E{{Ew, Ew + 32 * C}};
-    u64* X = W + 64 * HA + 64 * HB;
+    u64* X = W + softmax_x_off(C, a.esmem != 0);
     SO MX{{X, X + 32}}, SS{{X + 64, X + 96}}, RR{{X + 128, X + 160}};
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const i64 ntiles = (a.rows + 31) / 32;

@@ -398,11 +398,12 @@ static const size_t SMEM_LIMIT = 56 * 1024;      // + 16 KB static cone smem: ke
 
 // fused row kernels: work tile in shared memory when it fits, else a per-CTA global tile
 template <class Args, class KB, class KP>
-static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 work_u64, i64 esc_u64, const char* name)
+static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 work_u64, i64 esc_u64, const char* name,
+                              size_t smem_limit = SMEM_LIMIT)
 {
     const i64 ntiles = (rows + 31) / 32;
     const size_t wbytes = sizeof(u64) * (size_t)work_u64;
-    const bool smem = work_u64 > 0 && wbytes <= SMEM_LIMIT;
+    const bool smem = work_u64 > 0 && wbytes <= smem_limit;
     const size_t dyn = smem ? wbytes : 0;
     if (smem) {
         cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes);
@@ -1368,10 +1369,16 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         a.cone = use_cone(c, p->window) ? 1 : 0;
         a.bcast = p->bcast ? 1 : 0;
         const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
-        const i64 wk = softmax_work_u64(cols), ek = 64 * cols;
-        st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax")
-           : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax")
-                    : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax");
+        // E in shared memory when the whole work tile fits 100 KB (two CTAs per SM): cols <= 192
+#ifndef MPC_SOFTMAX_ESMEM
+#define MPC_SOFTMAX_ESMEM 1
+#endif
+        a.esmem = (MPC_SOFTMAX_ESMEM && softmax_work_u64(cols, true) * 8 <= 100 * 1024) ? 1 : 0;
+        const i64 wk = softmax_work_u64(cols, a.esmem != 0), ek = a.esmem ? 0 : 64 * cols;
+        const size_t lim = a.esmem ? 100 * 1024 : SMEM_LIMIT;
+        st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax", lim)
+           : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax", lim)
+                    : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax", lim);
     }
     return st;
 }

@@ -264,7 +264,7 @@ struct PairP {
         }
     }
     __device__ __forceinline__ S bm_finish(u64 a, u64 b, u64 c, u64 e, u64 f) const {
-        return pty == 0 ? c + e * b + f * a + e * f : c + e * b + f * a;
+        return pty == 0 ? c + e * (b + f) + f * a : c + e * b + f * a;   // party 0: e b + e f = e (b + f)
     }
 #if MPC_PAIR_BM_INLINE
     __device__ __forceinline__ S bm(u64 u, u32 s, S x, S y) {
@@ -367,7 +367,7 @@ struct PairP {
         else { a = a1_other_half; const u64 t = a0 + a; c = t * t - c0; }
     }
     __device__ __forceinline__ S sq_finish(u64 a, u64 c, u64 e) const {
-        return pty == 0 ? c + 2ull * e * a + e * e : c + 2ull * e * a;
+        return pty == 0 ? c + e * (2ull * a + e) : c + 2ull * e * a;
     }
     __device__ __forceinline__ S sq(u64 u, u32 s, S y) {
         const int lane = threadIdx.x & 31;

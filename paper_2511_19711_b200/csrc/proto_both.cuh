@@ -29,7 +29,7 @@ __device__ __forceinline__ Sh bm_with_c0(const Keys& K, u64 u, u32 s, Sh x, Sh y
     const u64 c1 = (a0 + a1) * (b0 + b1) - c0;        // dealer correction -> party 1
     const u64 e = (x.s0 - a0) + (x.s1 - a1);           // open(x - a)
     const u64 f = (y.s0 - b0) + (y.s1 - b1);           // open(y - b)
-    return {c0 + e * b0 + f * a0 + e * f, c1 + e * b1 + f * a1};
+    return {c0 + e * (b0 + f) + f * a0, c1 + e * b1 + f * a1};   // party 0: e b0 + e f = e (b0 + f)
 }
 
 __device__ __forceinline__ u64 beaver_c0(const Keys& K, u64 u, u32 s)
@@ -66,7 +66,7 @@ __device__ __forceinline__ Sh sq_with_a1(const Keys& K, u64 u, u32 s, Sh y, u64 
     const u64 a = a0 + a1;
     const u64 c1 = a * a - c0;                         // dealer correction -> party 1
     const u64 e = (y.s0 - a0) + (y.s1 - a1);           // open(y - a)
-    return {c0 + 2ull * e * a0 + e * e, c1 + 2ull * e * a1};
+    return {c0 + e * (2ull * a0 + e), c1 + 2ull * e * a1};
 }
 __device__ __forceinline__ Sh sq1(const Keys& K, u64 u, u32 s, Sh y)
 {
@@ -98,7 +98,7 @@ __device__ __forceinline__ Sh bmb_elem(const Keys& K, u64 u, u32 s, Sh x, const 
     const u64 a0 = w64(A0.x, A0.y), c0 = w64(A0.z, A0.w);
     const u64 c1 = (a0 + a1) * (r.b0 + r.b1) - c0;     // dealer correction -> party 1
     const u64 e = (x.s0 - a0) + (x.s1 - a1);           // open(x - a)
-    return {c0 + e * r.b0 + r.f * a0 + e * r.f, c1 + e * r.b1 + r.f * a1};
+    return {c0 + e * (r.b0 + r.f) + r.f * a0, c1 + e * r.b1 + r.f * a1};
 }
 // unit pair (u even, u+1): one K1 block serves both a1 halves (1.5 blocks per element)
 __device__ __forceinline__ void bmb2(const Keys& K, u64 u, u32 s, Sh x0, Sh x1, const BRow& r0, const BRow& r1,
