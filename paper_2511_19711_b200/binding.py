@@ -328,7 +328,8 @@ class Ctx:
         return z
 
     # ---- NEXT #4: plaintext fixed-point emulation (the auto-tuner's evaluator) ----
-    PLAIN = {"exp": 0, "recip": 1, "rsqrt": 2, "gelu": 3, "silu": 4, "sigmoid": 5, "softmax": 6, "layernorm": 7}
+    PLAIN = {"exp": 0, "recip": 1, "rsqrt": 2, "gelu": 3, "silu": 4, "sigmoid": 5, "softmax": 6, "layernorm": 7,
+             "relu": 3}
 
     def plain_eval(self, op: str, x: torch.Tensor, rows: int = 1, cols: int | None = None, **kw):
         """Run one approximation schedule on plaintext fixed-point values (float64 in / out, device).
@@ -343,9 +344,12 @@ class Ctx:
         elif op in ("recip", "rsqrt"):
             knobs = NrP(kw.get("iters", 10 if op == "recip" else 3),
                         ExpP(kw.get("t", 8), int(kw.get("clamp", 0)), kw.get("window", 33), 0))
-        elif op in ("gelu", "silu", "sigmoid"):
-            k = default_act(op, **{a: b for a, b in kw.items() if a in ("form", "degree", "erf_terms", "window", "B",
-                                                                       "coeffs", "basis")})
+        elif op in ("gelu", "silu", "sigmoid", "relu"):
+            if op == "relu":                         # ReLU = the degree-0 segment form, x * NOT ltz_w(x)
+                kw = dict(form="relu", degree=0, window=kw.get("window", 33))
+            k = default_act("gelu" if op == "relu" else op,
+                            **{a: b for a, b in kw.items() if a in ("form", "degree", "erf_terms", "window", "B",
+                                                                  "coeffs", "basis")})
             coeffs = k.get("coeffs")
             arr = (ctypes.c_double * len(coeffs))(*coeffs) if coeffs else None
             knobs = ActP(FORM[k["form"]], int(k.get("degree", 0)), float(k.get("B", 5.0)),

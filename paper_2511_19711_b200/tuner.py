@@ -6,8 +6,8 @@ is compared with the maximally accurate approximation, and the difference is com
 user-given threshold"), scoring candidates on a non-MPC runtime.  This module is the
 search machinery over the library's knobs:
 
-* a Layer: an op kind ("softmax", "gelu", "silu", "sigmoid", "layernorm", "exp", "recip",
-  "rsqrt"), its MPC shape, calibration inputs (a float64 device tensor) and candidate knob sets
+* a Layer: an op kind ("softmax", "gelu", "silu", "sigmoid", "layernorm", "relu" (comparison
+  window, HummingBird-style), "exp", "recip", "rsqrt"), its MPC shape, calibration inputs (a float64 device tensor) and candidate knob sets
   ordered from the most accurate to the cheapest (``CANDIDATES``);
 * quality: the plaintext fixed-point emulation of each candidate (``Ctx.plain_eval`` ->
   mpc_plain_eval, CUDA) against the most accurate candidate's emulation on the same inputs --
@@ -41,6 +41,9 @@ CANDIDATES: Dict[str, List[dict]] = {
     "sigmoid": [dict(form="poly_x", degree=4), dict(form="poly_x", degree=2), dict(form="relu", degree=0)],
     "layernorm": [dict(rsqrt_iters=3, rsqrt_t=8), dict(rsqrt_iters=2, rsqrt_t=8), dict(rsqrt_iters=3, rsqrt_t=4),
                   dict(rsqrt_iters=3, rsqrt_t=0), dict(rsqrt_iters=2, rsqrt_t=0)],
+    # HummingBird-style per-site comparison windows: the sign is
+    # exact while |x| < 2^(w-17); a smaller window means fewer carry-circuit gates and bytes
+    "relu": [dict(window=33), dict(window=29), dict(window=25), dict(window=21), dict(window=19), dict(window=17)],
     "exp": [dict(t=8, clamp=1), dict(t=8), dict(t=4), dict(t=2), dict(t=0, clamp=1)],
     "recip": [dict(iters=10), dict(iters=8), dict(iters=6)],
     "rsqrt": [dict(iters=3), dict(iters=2), dict(iters=1)],

@@ -81,3 +81,21 @@ def test_tuner_end_to_end(m):
     assert mid["cost"] <= mid["cost_most_accurate"]
     wan = tuner.GreedyTuner(L, tuner.Evaluator(c, objective="wan"), threshold=0.05).run()
     assert wan["quality_loss"] <= 0.05
+
+
+def test_tuner_picks_hummingbird_windows(m):
+    """Per-site comparison windows: with a zero error budget the tuner takes the
+    smallest window that still holds every calibration activation (3 N(0,1) clipped to |x| < 16,
+    max ~11: needs w - 17 >= 4, i.e. w = 21 of the candidates), and a wider-spread site keeps a
+    wider window."""
+    from paper_2511_19711_b200 import tuner
+    c = m.Ctx.for_cfg(workloads.keys(4))
+    x1 = dev(np.clip(workloads.relu_inputs(8192) * 3.0, -15.9, 15.9))
+    x2 = dev(workloads.relu_inputs(8192) * 40.0)              # |x| up to ~200: needs w = 25
+    L = [tuner.Layer("relu_a", "relu", 1, 8192, x1, 1), tuner.Layer("relu_b", "relu", 1, 8192, x2, 1)]
+    r = tuner.GreedyTuner(L, tuner.Evaluator(c, objective="lan"), threshold=0.0).run()
+    assert r["knobs"]["relu_a"]["window"] == 21
+    assert r["knobs"]["relu_b"]["window"] == 25
+    assert r["quality_loss"] == 0.0
+    y = c.plain_eval("relu", x1, window=21).cpu().numpy()
+    assert np.array_equal(y, np.maximum(np.round(x1.cpu().numpy() * 65536) / 65536, 0))
