@@ -721,8 +721,13 @@ mpc_status mpc_ctx_set_stream(mpc_ctx* c, void* s)
 {
     if (!c) return MPC_ERR_INVALID;
     cudaStream_t ns = (cudaStream_t)s;
-    if (ns != c->stream) {
-        // scratch and exchange memory are stream-ordered: order the new stream after the old one
+    cudaStreamCaptureStatus cap_new = cudaStreamCaptureStatusNone, cap_old = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(ns, &cap_new);
+    cudaStreamIsCapturing(c->stream, &cap_old);
+    if (ns != c->stream && cap_new == cudaStreamCaptureStatusNone && cap_old == cudaStreamCaptureStatusNone) {
+        // scratch and exchange memory are stream-ordered: order the new stream after the old one.
+        // (Under CUDA-graph capture an event from outside the capture cannot be waited on: the
+        // capturing caller orders its stream after the context's previous work itself.)
         cudaEvent_t e = ev_get(c);
         cudaEventRecord(e, c->stream);
         cudaStreamWaitEvent(ns, e, 0);

@@ -127,6 +127,31 @@ def sec_rows(S):
     return out
 
 
+def graph_us_per_call(fn, calls=20, replays=10):
+    """Device-side latency of one call: `calls` calls captured into one CUDA graph (the library's
+    launches are stream-capturable), replayed; us per call.  Replays reuse the captured step ids,
+    so this is a timing device only (never reuse randomness in a real protocol run)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()                                            # warm-up: scratch allocated, occupancy cached
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(calls):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(replays):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return round(a.elapsed_time(b) * 1e3 / (replays * calls), 2)
+
+
 def sec_cfg1(S):
     c = S.ctx(1)
     n = workloads.SHAPES["cfg1_elems"]
@@ -143,6 +168,13 @@ def sec_cfg1(S):
         out[f"gelu_{form}{deg}"] = S.line(c, lambda form=form, deg=deg: c.gelu(a, form=form, degree=deg,
                                                                              erf_terms=8, out=z),
                                           n, f"cfg1 GELU {form} deg {deg}, 4096")
+    # the same calls replayed from a CUDA graph: device latency without the host launch path
+    fns = {"exp_t8": lambda: c.exp(e, t=8, out=z), "exp_t8_clamp": lambda: c.exp(e, t=8, clamp=1, out=z),
+           "exp_t2_clamp": lambda: c.exp(e, t=2, clamp=1, out=z), "recip_10": lambda: c.recip(r, out=z),
+           "gelu_poly_abs4": lambda: c.gelu(a, form="poly_abs", degree=4, out=z),
+           "gelu_erf8": lambda: c.gelu(a, form="erf", erf_terms=8, out=z)}
+    for k, fn in fns.items():
+        out[k]["us_per_call_graph"] = graph_us_per_call(fn)
     return out
 
 
@@ -345,7 +377,8 @@ def main():
     for sec, d in res["sections"].items():
         for k, v in d.items():
             print(f"{sec:5s} {k:28s} {v['ms']:9.4f} ms {v['elements_per_s'] / 1e9:8.3f} Gel/s "
-                  f"{v['gphilox_s']:7.1f} Gph/s  B/party {v['bytes_per_party']:>12d} rounds {v['rounds']}")
+                  f"{v['gphilox_s']:7.1f} Gph/s  B/party {v['bytes_per_party']:>12d} rounds {v['rounds']}"
+                  + (f"  graph {v['us_per_call_graph']} us/call" if "us_per_call_graph" in v else ""))
 
 
 if __name__ == "__main__":
