@@ -245,7 +245,8 @@ typedef struct { int window; mpc_exp_p exp; mpc_nr_p recip; int bcast; } mpc_sof
 mpc_status mpc_softmax(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols,
                        int64_t row_off, const mpc_softmax_p* p);
 /* S14 over HOST buffers (pinned for overlap): hx / hz carry host pointers (rows x cols per
- * party).  The rows are processed in chunks of chunk_rows (multiple of 32): chunk i is copied in
+ * party).  The rows are processed in chunks of chunk_rows (multiple of 32; 0 = four equal
+ * chunks): chunk i is copied in
  * on one stream, computed on its own stream with its own staging and scratch, and copied out on
  * a third, so both PCIe directions overlap each other and the compute.  The same steps, units
  * and output shares as mpc_softmax on the same rows; completes in the ctx stream's order. */

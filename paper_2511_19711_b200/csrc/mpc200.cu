@@ -13,6 +13,7 @@
 #include <cstring>
 #include <cstdarg>
 #include <algorithm>
+#include <vector>
 #include <cuda_runtime.h>
 
 #include "mpc200.h"
@@ -1282,7 +1283,7 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
     mpc_status st = begin(c, steps);
     if (st) return st;
     if (bad_sh(c, hx) || bad_sh(c, hz) || rows < 0 || cols < 1 || row_off < 0 || (row_off & 31) ||
-        chunk_rows < 32 || (chunk_rows & 31))
+        chunk_rows < 0 || (chunk_rows > 0 && chunk_rows < 32) || (chunk_rows & 31))
         return fail(c, MPC_ERR_INVALID, "softmax_hostio args (row_off, chunk_rows % 32)");
     if (rows == 0) { finish(c, steps); return MPC_OK; }
     if (!c->hio) {
@@ -1306,16 +1307,26 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
     const int p0 = c->cfg.mode == MPC_MODE_PAIR ? c->cfg.party : 0;
     // PAIR kernels own the per-warp exchange slots: their chunks run one after another
     const int nslots = is_pair(c) ? 1 : HIO_SLOTS;
-    const size_t half = sizeof(u64) * (size_t)chunk_rows * (size_t)cols;       // one party, one array
+    // chunk schedule: chunk_rows, or (0) four equal chunks -- measured best for cfg2 among 768..6144-row
+    // chunks and a short-long-short ramp (tools/perf_e2e.py)
+    std::vector<i64> sched;
+    {
+        const i64 cr = chunk_rows > 0 ? chunk_rows : std::max<i64>(32, ((rows + 3) / 4 + 31) / 32 * 32);
+        for (i64 r = 0; r < rows; r += cr) sched.push_back(std::min<i64>(cr, rows - r));
+    }
+    i64 maxc = 0;
+    for (i64 v : sched) maxc = std::max(maxc, v);
+    const size_t half = sizeof(u64) * (size_t)maxc * (size_t)cols;             // one party, one array
     cudaStream_t user = c->stream;
     cudaEventRecord(h->start, user);
     cudaStreamWaitEvent(h->h2d, h->start, 0);
     const u32 s0 = (u32)c->step;
-    const i64 nchunks = (rows + chunk_rows - 1) / chunk_rows;
-    for (i64 i = 0; i < nchunks; ++i) {
+    const i64 nchunks = (i64)sched.size();
+    i64 r0 = 0;
+    for (i64 i = 0; i < nchunks; r0 += sched[(size_t)i], ++i) {
         const int b = (int)(i % HIO_SLOTS);
         const int cb = (int)(i % nslots);
-        const i64 r0 = i * chunk_rows, ri = std::min<i64>(chunk_rows, rows - r0);
+        const i64 ri = sched[(size_t)i];
         const size_t bytes = sizeof(u64) * (size_t)(ri * cols);
         if (!h->dbuf[b] || h->dbuf_bytes[b] < 4 * half) {
             if (h->dbuf[b]) { cudaStreamSynchronize(h->d2h); cudaFree(h->dbuf[b]); }
