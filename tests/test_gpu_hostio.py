@@ -28,7 +28,6 @@ def test_hostio_equals_device_softmax(m, rows, cols, chunk, mode):
     c.set_step(s0, force=True)
     c.softmax_hostio(hx, hz, rows, cols, row_off=64, chunk_rows=chunk)
     torch.cuda.synchronize()
-    assert c.step == s0 + (c.step - s0)
     assert torch.equal(hz[0], z[0].cpu()) and torch.equal(hz[1], z[1].cpu())
     if mode:
         c.sync()

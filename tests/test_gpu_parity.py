@@ -530,3 +530,50 @@ def test_cone_maxpool(mpc):
     x = workloads.maxpool_inputs((N, C, H, W)) - 0.25
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
     same(c.maxpool2d(gx, N, C, H, W, 3, 2, 1, img_off=2), o.maxpool2d(ox, N, C, H, W, 3, 2, 1, img_off=2))
+
+
+# ------------------------------------------------- T5: fused = composed (row ops) ----
+def _i64(t):
+    return t.view(torch.int64)
+
+
+def _bcast(v, cols):
+    return v.view(-1, 1).expand(-1, cols).contiguous().view(-1)
+
+
+def test_softmax_fused_equals_composed(mpc):
+    """k_softmax's shares equal the composition of ABI calls on the same step ids: max ->
+    (local) x - max -> exp (element units) -> (local) row sums -> recip (row units) -> mul by the
+    broadcast reciprocal (element units) + truncation."""
+    c, _ = pair_ctx(mpc, 2, step=40)
+    rows, cols, roff = 64, 128, 32
+    x = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    s0 = c.step
+    z = c.softmax(x, rows, cols, row_off=roff)
+    c.set_step(s0, force=True)
+    mx = c.max(x, rows, cols, row_off=roff)
+    d = tuple((_i64(x[p]).view(rows, cols) - _i64(mx[p]).view(rows, 1)).view(-1).view(torch.uint64) for p in (0, 1))
+    e = c.exp(d, off=roff * cols, t=8)
+    S = tuple(_i64(e[p]).view(rows, cols).sum(1).view(torch.uint64) for p in (0, 1))
+    r = c.recip(S, off=roff, iters=10, t=8)
+    rb = tuple(_bcast(r[p], cols) for p in (0, 1))
+    out = c.mul(e, rb, off=roff * cols, trunc_bits=16)
+    assert torch.equal(z[0], out[0]) and torch.equal(z[1], out[1])
+
+
+def test_layernorm_fused_equals_composed(mpc):
+    c, _ = pair_ctx(mpc, 5, step=50)
+    rows, cols, roff = 40, 768, 64
+    x = c.share(torch.from_numpy(workloads.layernorm_inputs(rows, cols)).cuda())
+    s0 = c.step
+    z = c.layernorm(x, rows, cols, row_off=roff)
+    c.set_step(s0, force=True)
+    e_invd, e_eps = round(65536 / cols), round(1e-5 * 65536)        # E(1/d), E(eps) (R2, R25)
+    mu = [(_i64(x[p]).view(rows, cols).sum(1) * e_invd) >> 16 for p in (0, 1)]
+    cc = tuple((_i64(x[p]).view(rows, cols) - mu[p].view(rows, 1)).view(-1).view(torch.uint64) for p in (0, 1))
+    q = c.mul(cc, cc, off=roff * cols, trunc_bits=16)
+    v = [(_i64(q[p]).view(rows, cols).sum(1) * e_invd) >> 16 for p in (0, 1)]
+    v[0] = v[0] + e_eps                                             # public addend: party 0 (P:434)
+    r = c.rsqrt(tuple(t.view(torch.uint64) for t in v), off=roff, iters=3, t=8)
+    out = c.mul(cc, tuple(_bcast(r[p], cols) for p in (0, 1)), off=roff * cols, trunc_bits=16)
+    assert torch.equal(z[0], out[0]) and torch.equal(z[1], out[1])
