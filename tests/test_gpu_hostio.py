@@ -23,11 +23,13 @@ def test_hostio_equals_device_softmax(m, rows, cols, chunk, mode):
     x = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
     s0 = c.step
     z = c.softmax(x, rows, cols, row_off=64)
+    s1 = c.step
     hx = tuple(t.cpu().pin_memory() for t in x)
     hz = tuple(torch.empty_like(t).pin_memory() for t in hx)
     c.set_step(s0, force=True)
     c.softmax_hostio(hx, hz, rows, cols, row_off=64, chunk_rows=chunk)
     torch.cuda.synchronize()
+    assert c.step == s1                     # the same step ids as one mpc_softmax call
     assert torch.equal(hz[0], z[0].cpu()) and torch.equal(hz[1], z[1].cpu())
     if mode:
         c.sync()
