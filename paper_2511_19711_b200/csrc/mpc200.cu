@@ -890,9 +890,10 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
     mpc_status st = begin(c, 1);
     if (st) return st;
     if (tb != 0 && tb != 16) return fail(c, MPC_ERR_RANGE, "trunc_bits must be 0 or 16");
-    if (batch < 0 || M < 1 || K < 1 || N < 1 || batch_off < 0 || M > 65535 * 64 || N > (1ll << 30) ||
-        batch * M * K >= (1ll << 40) || batch * K * N >= (1ll << 40) || batch > 65535)
-        return fail(c, MPC_ERR_INVALID, "matmul: bad shape");
+    const i64 nparty = c->cfg.mode == MPC_MODE_PAIR ? 1 : 2;        // parties computed by this GPU
+    if (batch < 0 || M < 1 || K < 1 || N < 1 || batch_off < 0 || M > 65535ll * 64 || N > (1ll << 30) ||
+        batch * M * K >= (1ll << 40) || batch * K * N >= (1ll << 40) || batch * nparty > 65535)
+        return fail(c, MPC_ERR_INVALID, "matmul: bad shape (batch x parties <= 65535 grid z)");
     if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "matmul: null pointer");
     if (batch == 0) { finish(c, 1); return MPC_OK; }
     const bool tc_ok = 3 * K <= 16384;                // exact limb accumulators (matmul_tc.cuh)
