@@ -107,10 +107,20 @@ class Job:
     def __init__(self, m, torch, dist):
         self.m, self.torch, self.dist = m, torch, dist
         self.ws, self.rank, self.local = dist_env()
+        # MPC_BENCH_ONE_GPU=1 (validation only): every rank on cuda:0 with gloo for the host-side
+        # collectives -- exercises the whole N > 1 path (pairs, cudaIpc exchange, max-over-ranks
+        # timing, JSON) on a one-GPU box; the parties' kernels time-slice, so its numbers are not
+        # throughput (tests/test_gpu_bench_pair.py)
+        self.one_gpu = os.environ.get("MPC_BENCH_ONE_GPU") == "1"
+        if self.one_gpu:
+            self.local = 0
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         if self.ws > 1:
-            dist.init_process_group("nccl", device_id=self.dev)
+            if self.one_gpu:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
             from paper_2511_19711_b200 import pair
             self.party, self.peer, self.pair_idx, self.npairs = pair.pair_layout(self.rank, self.ws)
             self.mode = m.binding.MODE_PAIR
@@ -138,7 +148,7 @@ class Job:
     def maxr(self, v):
         if self.ws == 1:
             return v
-        t = self.torch.tensor([v], device=self.dev, dtype=self.torch.float64)
+        t = self.torch.tensor([v], device="cpu" if self.one_gpu else self.dev, dtype=self.torch.float64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
