@@ -14,12 +14,38 @@ from __future__ import annotations
 import json
 import math
 import os
-import sys
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from oracle.float_ref import TRUE_ACT, act_formula  # noqa: E402  (fp64 formulas only)
+from scipy.special import erf
+
+# The fixture is an input of BOTH sides (knob values passed through the ABI), so this tool is
+# self-contained: it imports nothing from oracle/ (test infrastructure) or from the product.
+TRUE_ACT = {
+    "gelu": lambda x: 0.5 * x * (1.0 + erf(x / math.sqrt(2.0))),
+    "silu": lambda x: x * (1.0 / (1.0 + np.exp(-x))),
+    "sigmoid": lambda x: 1.0 / (1.0 + np.exp(-x)),
+}
+
+
+def act_formula(x, act, form, degree, B, coeffs=None, erf_terms=8):
+    """Segment approximation in float64: inside [-B, B) the form's polynomial (x-form S:193,
+    |x|-form P:737) or the erf Maclaurin series (reading R21); outside the asymptote."""
+    if form == "poly_x":
+        inner = np.polyval(list(coeffs)[::-1], x)
+    elif form == "poly_abs":
+        inner = 0.5 * x + np.polyval(list(coeffs)[::-1], np.abs(x))
+    else:
+        z2 = x * x / 2.0
+        S, fact = np.zeros_like(x), 1.0
+        for k in range(erf_terms):
+            fact = fact * k if k > 0 else 1.0
+            S = S + ((-1.0) ** k / (fact * (2 * k + 1))) * z2 ** k
+        inner = 0.5 * x * (1.0 + 2.0 / math.sqrt(math.pi) * (x / math.sqrt(2.0)) * S)
+    mid = (x >= -B) & (x < B)
+    tail = (x >= B) * (1.0 if act == "sigmoid" else x)
+    return np.where(mid, inner, 0.0) + tail
+
 
 FITS = [
     # (act, form, degree, B)
@@ -54,7 +80,7 @@ def main():
         print(f"{act:8s} {form:9s} deg {d}  B={B}: max|err| = {err:.4g}")
     for K, B in ((4, 2.5), (6, 2.5), (8, 2.5)):
         grid = np.linspace(-B - 4.0, B + 4.0, 200001)
-        err = float(np.max(np.abs(act_formula(grid, "gelu", "erf", 0 + 1, B, None, K)
+        err = float(np.max(np.abs(act_formula(grid, "gelu", "erf", 1, B, None, K)
                                   - TRUE_ACT["gelu"](grid))))
         out.append({"op": "gelu", "form": "erf", "erf_terms": K, "interval": [-B, B],
                     "coefficients": None, "max_abs_error": err})
