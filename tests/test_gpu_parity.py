@@ -577,3 +577,26 @@ def test_layernorm_fused_equals_composed(mpc):
     r = c.rsqrt(tuple(t.view(torch.uint64) for t in v), off=roff, iters=3, t=8)
     out = c.mul(cc, tuple(_bcast(r[p], cols) for p in (0, 1)), off=roff * cols, trunc_bits=16)
     assert torch.equal(z[0], out[0]) and torch.equal(z[1], out[1])
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (31, 1), (33, 2), (1, 3), (64, 17), (5, 1025)])
+def test_softmax_edge_shapes(mpc, rows, cols):
+    """Degenerate and ragged softmax shapes: a single column (no max-tree level), two and three
+    columns (odd carry), one row, 17 columns (CTA tree with an odd level), 1025 columns (global
+    work tile and an odd first level)."""
+    c, o = pair_ctx(mpc, 2, step=7)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols, row_off=96), o.softmax(ox, rows, cols, row_off=96))
+    assert c.step == o.step
+
+
+def test_matmul_long_k_tensor_cores(mpc):
+    """K = 5000 (K' = 15000 for party 1, inside the exact-accumulator bound) on the tensor cores."""
+    c, o = pair_ctx(mpc, 3, step=2)
+    c.set_matmul_engine(2)
+    M, K, N = 3, 5000, 5
+    x, y = workloads.act_inputs(M * K, lo=-1, hi=1), workloads.act_inputs(K * N, seed_cfg=5, lo=-1, hi=1)
+    gx, gy = c.share(torch.from_numpy(x).cuda()), c.share(torch.from_numpy(y).cuda())
+    ox, oy = o.share(x), o.share(y)
+    same(c.matmul(gx, gy, 1, M, K, N, trunc_bits=16), o.matmul(ox, oy, 1, M, K, N, trunc_bits=16))
