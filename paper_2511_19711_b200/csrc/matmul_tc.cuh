@@ -49,7 +49,7 @@ struct LimbArgs {
 // RHS limb tiling through a shared-memory transpose: one CTA per (batch, 64-column block, K block
 // of 32): coalesced loads of 32 rows x 64 columns, then 128 threads pack the 64 x 2 core-matrix
 // rows of all 8 limbs and write the 16 KB chunk contiguously.
-__global__ void __launch_bounds__(256) k_mm_limbs_rhs(LimbArgs a)
+__global__ void __launch_bounds__(2 * TC_BN) k_mm_limbs_rhs(LimbArgs a)
 {
     __shared__ u64 sm[TC_BK][TC_BN + 1];
     const int KB = a.Kp / TC_BK, NB = (a.rows + TC_BN - 1) / TC_BN;

@@ -949,7 +949,8 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
             lb.in_stride = K * N; lb.out = LB[p];
             rec_begin(c, "mm_limbs", 0);
             k_mm_limbs_lhs<<<(unsigned)std::min<i64>(batch * MB * (Kps[p] / TC_BK), (i64)c->sm_count * 8), 256, 0, c->stream>>>(la);
-            k_mm_limbs_rhs<<<(unsigned)std::min<i64>(batch * NB * (Kps[p] / TC_BK), (i64)c->sm_count * 8), 256, 0, c->stream>>>(lb);
+            // 2 * TC_BN threads pack a tile's core-matrix rows: CTAs of exactly that size, many per SM
+            k_mm_limbs_rhs<<<(unsigned)std::min<i64>(batch * NB * (Kps[p] / TC_BK), (i64)c->sm_count * 24), 2 * TC_BN, 0, c->stream>>>(lb);
             rec_end(c);
             c->st.launches += 2;
             t.A[p] = LA[p]; t.B[p] = LB[p]; t.Kp[p] = (int)Kps[p];
