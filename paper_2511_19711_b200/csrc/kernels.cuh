@@ -17,6 +17,9 @@
 #ifndef MPC_ROW_TPB
 #define MPC_ROW_TPB 256    // threads per CTA of the row kernels (softmax / max / layernorm)
 #endif
+#ifndef MPC_GROUP_PREFETCH
+#define MPC_GROUP_PREFETCH 1   // element-wise drivers prefetch the next pass's input shares to L2
+#endif
 #ifndef MPC_EW_MINB
 #define MPC_EW_MINB 2      // same for the element-wise drivers
 #endif
@@ -59,8 +62,17 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_groups(const __grid_consta
     auto pr = pa.make(cta, ncta);
     const int lane = threadIdx.x & 31, NW = blockDim.x >> 5;
     const i64 ng = (n + 31) >> 5;
-    for (i64 g = (i64)cta * NW + (threadIdx.x >> 5); g < ng; g += (i64)ncta * NW) {
+    const i64 gstep = (i64)ncta * NW;
+    for (i64 g = (i64)cta * NW + (threadIdx.x >> 5); g < ng; g += gstep) {
         const i64 i = g * 32 + lane;
+        if (MPC_GROUP_PREFETCH) {       // the next group's input shares to L2 while this one computes
+            const i64 inext = i + gstep * 32;
+            if (inext < n) {
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+                    if (body.x.p[p]) asm volatile("prefetch.global.L2 [%0];" :: "l"(body.x.p[p] + inext));
+            }
+        }
         body(pr, off + (u64)i, (off >> 5) + (u64)g, i, lane, i < n);
     }
     pa.done(pr);
@@ -76,7 +88,15 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_pairs(const __grid_constan
     constexpr int V = decltype(pr)::kV;
     const int lane = threadIdx.x & 31, NW = blockDim.x >> 5;
     const u64 p0 = off >> 1, p1 = (off + (u64)n + 1) >> 1;
-    for (u64 base = ((u64)cta * NW + (threadIdx.x >> 5)) * 32 * V; p0 + base < p1; base += (u64)ncta * NW * 32 * V) {
+    const u64 pstep = (u64)ncta * NW * 32 * V;
+    for (u64 base = ((u64)cta * NW + (threadIdx.x >> 5)) * 32 * V; p0 + base < p1; base += pstep) {
+        if (MPC_GROUP_PREFETCH && p0 + base + pstep + lane < p1) {   // next pass's input shares to L2
+            const i64 inext = (i64)(2 * (p0 + base + pstep + lane) - off);
+            if (inext >= 0)
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (body.x.p[q]) asm volatile("prefetch.global.L2 [%0];" :: "l"(body.x.p[q] + inext));
+        }
         u64 u[V];
         i64 i0[V];
         bool ok[V];
@@ -466,6 +486,17 @@ __device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g
     __syncthreads();
 }
 
+// L2 prefetch of the next tile's input rows (rows [r0n, r0n + 32) of a rows x C share array)
+__device__ __forceinline__ void prefetch_rows(SP x, i64 r0n, i64 rows, i64 C)
+{
+    if (!MPC_GROUP_PREFETCH || r0n >= rows) return;
+    const i64 nel = (rows - r0n < 32 ? rows - r0n : 32) * C;
+    for (i64 l = (i64)threadIdx.x * 16; l < nel; l += (i64)blockDim.x * 16)       // one 128-B line each
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+            if (x.p[q]) asm volatile("prefetch.global.L2 [%0];" :: "l"(x.p[q] + r0n * C + l));
+}
+
 // out = MT(x, bcast r) over a tile of R rows x C with the BROADCAST triple (NEXT #2, DESIGN.md
 // 2.8): warp 0 opens f = r - b for the tile's 32 rows (lane <-> row, one round), the CTA then
 // forms the element products (e = x - a opened per element) on unit pairs.  val(e, row) yields
@@ -559,6 +590,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         const int R = (int)min((i64)32, a.rows - r0);
         const u64 g0 = a.row_off + (u64)r0;                       // global row of the tile
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        // (no next-tile prefetch here: measured neutral to 0.6 % slower for softmax, 2 % faster for k_max)
         // 1. m = MAX_row(x)
 #ifndef MPC_SOFTMAX_SKIP
 #define MPC_SOFTMAX_SKIP 0   // profiling only: bitmask of phases to skip (1 max, 2 exp, 4 recip, 8 mul)
@@ -696,6 +728,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         const i64 r0 = tile * 32;
         const int R = (int)min((i64)32, a.rows - r0);
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        prefetch_rows(a.x, r0 + (i64)ncta * 32, a.rows, C);
         tile_max<WIDE, CONE>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, HA, HB, MX, cone_sm);
         const SP MXc{{MX.p[0], MX.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 : nullptr, a.z.p[1] ? a.z.p[1] + r0 : nullptr}};
@@ -892,6 +925,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln(const __grid_co
         const int R = (int)min((i64)32, a.rows - r0);
         const u64 g0 = a.row_off + (u64)r0;
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        prefetch_rows(a.x, r0 + (i64)ncta * 32, a.rows, C);
         for (int rr = warp; rr < R; rr += NW) {
             S acc = pr.zero();
             for (i64 j = lane; j < C; j += 32) acc = pr.add(acc, pr.ld(xt, rr * C + j));
