@@ -356,6 +356,7 @@ class Ctx:
                          ctypes.cast(arr, ctypes.POINTER(ctypes.c_double)) if arr is not None else None,
                          int(k.get("erf_terms", 0)), int(k.get("window", 33)), int(k.get("basis", 0)))
         elif op == "softmax":
+            # (square triples / broadcast triple change only the MPC rounding, not the emulated value)
             knobs = SoftmaxP(kw.get("window", 33), ExpP(kw.get("exp_t", 8), int(kw.get("exp_clamp", 0)), 33, 0),
                              NrP(kw.get("recip_iters", 10), ExpP(kw.get("recip_t", 8), int(kw.get("recip_clamp", 0)),
                                                                   33, 0)), 0)

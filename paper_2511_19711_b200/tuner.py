@@ -33,10 +33,15 @@ NETWORKS = {"lan": (0.3e-3, 10e9 / 8), "wan": (40e-3, 352e6 / 8)}   # (latency s
 
 # candidate knob sets per op kind, most accurate first (the knob ranges of P:206-219)
 CANDIDATES: Dict[str, List[dict]] = {
-    "softmax": [dict(exp_t=8, exp_clamp=1), dict(exp_t=8, exp_clamp=0), dict(exp_t=4, exp_clamp=1),
+    # (the NEXT #2 protocol variants -- square-pair triples, the broadcast triple, power-basis
+    # polynomials -- are candidates too: same approximation, fewer bytes / rounds, their own
+    # fixed-point rounding)
+    "softmax": [dict(exp_t=8, exp_clamp=1), dict(exp_t=8, exp_clamp=0),
+                dict(exp_t=8, exp_clamp=0, exp_square=1, recip_square=1, bcast=1), dict(exp_t=4, exp_clamp=1),
                 dict(exp_t=2, exp_clamp=1), dict(exp_t=2, exp_clamp=1, recip_iters=7),
                 dict(exp_t=0, exp_clamp=1, recip_iters=7)],
-    "gelu": [dict(form="poly_abs", degree=4), dict(form="poly_abs", degree=2), dict(form="relu", degree=0)],
+    "gelu": [dict(form="poly_abs", degree=4), dict(form="poly_abs", degree=4, basis=1), dict(form="poly_abs", degree=2),
+             dict(form="relu", degree=0)],
     "silu": [dict(form="poly_abs", degree=4), dict(form="poly_abs", degree=2), dict(form="relu", degree=0)],
     "sigmoid": [dict(form="poly_x", degree=4), dict(form="poly_x", degree=2), dict(form="relu", degree=0)],
     "layernorm": [dict(rsqrt_iters=3, rsqrt_t=8), dict(rsqrt_iters=2, rsqrt_t=8), dict(rsqrt_iters=3, rsqrt_t=4),
