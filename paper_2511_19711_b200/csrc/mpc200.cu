@@ -564,7 +564,7 @@ static mpc_status xalloc(mpc_ctx* c, XAlloc& a)
 // ------------------------------------------------------------------ ABI ----
 extern "C" {
 
-const char* mpc_version(void) { return "mpc200 0.2 (sm_100a; BOTH, PAIR over peer memory, PAIR_LOOPBACK)"; }
+const char* mpc_version(void) { return "mpc200 0.3 (sm_100a; BOTH, PAIR over peer memory, PAIR_LOOPBACK; tcgen05 matmul)"; }
 
 mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
 {
