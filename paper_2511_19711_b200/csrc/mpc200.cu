@@ -10,6 +10,7 @@
 // No tensor cores: the path is element-wise / bitwise integer work.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cstdarg>
 #include <algorithm>
@@ -66,8 +67,12 @@ struct mpc_ctx {
 // Pipelined host-buffer execution: chunk i goes H2D on `h2d`, computes on cs[i % HIO_SLOTS] with its
 // own staging buffers and kernel scratch, and comes back D2H on `d2h` -- the copy engines (both
 // PCIe directions) overlap each other and the compute of the neighbouring chunks.
-constexpr int HIO_SLOTS = 4;
+constexpr int HIO_SLOTS = 16;           // capacity; h->nslots in use (MPC_HIO_SLOTS, default below)
+#ifndef MPC_HIO_DEFAULT_SLOTS
+#define MPC_HIO_DEFAULT_SLOTS 4
+#endif
 struct HostIO {
+    int nslots;
     cudaStream_t h2d, d2h, cs[HIO_SLOTS];
     cudaEvent_t in_ready[HIO_SLOTS], comp_done[HIO_SLOTS], out_done[HIO_SLOTS], start;
     u64* dbuf[HIO_SLOTS]; size_t dbuf_bytes[HIO_SLOTS];
@@ -610,7 +615,7 @@ mpc_status mpc_ctx_destroy(mpc_ctx* c)
     if (c->scratch) { cudaFreeAsync(c->scratch, c->stream); cudaStreamSynchronize(c->stream); }
     if (c->hio) {
         HostIO* h = c->hio;
-        for (int b = 0; b < HIO_SLOTS; ++b) {
+        for (int b = 0; b < h->nslots; ++b) {
             cudaStreamSynchronize(h->cs[b]);
             if (h->dbuf[b]) cudaFree(h->dbuf[b]);
             if (h->scr[b]) cudaFree(h->scr[b]);
@@ -1273,6 +1278,24 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
     return MPC_OK;
 }
 
+// The two parties' copies of one chunk and direction as one batched DMA submission: with both PCIe
+// directions busy, every separate cudaMemcpyAsync costs ~9 us of link time (tools/pcie_copy.cu: cfg2,
+// 4 chunks x 2 parties both ways, 0.649 ms as single copies vs 0.551 ms batched).  Under stream
+// capture the plain copies are used.
+static void copy_batch(void** dst, void** src, size_t bytes, int n, cudaStream_t s, cudaMemcpyKind kind)
+{
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (n > 1 && cs == cudaStreamCaptureStatusNone) {
+        size_t sz[2] = {bytes, bytes}, idx = 0, fail = 0;
+        cudaMemcpyAttributes at{};
+        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        if (cudaMemcpyBatchAsync(dst, src, sz, (size_t)n, &at, &idx, 1, &fail, s) == cudaSuccess) return;
+        cudaGetLastError();                        // not supported here: fall back to single copies
+    }
+    for (int q = 0; q < n; ++q) cudaMemcpyAsync(dst[q], src[q], bytes, kind, s);
+}
+
 // pipelined host-buffer softmax (see HostIO): same steps, units and output shares as mpc_softmax
 mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t rows, int64_t cols, int64_t row_off,
                               const mpc_softmax_p* p, int64_t chunk_rows)
@@ -1294,7 +1317,9 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         cudaStreamCreateWithFlags(&h->h2d, cudaStreamNonBlocking);
         cudaStreamCreateWithFlags(&h->d2h, cudaStreamNonBlocking);
         cudaEventCreateWithFlags(&h->start, cudaEventDisableTiming);
-        for (int b = 0; b < HIO_SLOTS; ++b) {
+        const char* ev = getenv("MPC_HIO_SLOTS");
+        h->nslots = ev ? std::max(1, std::min(HIO_SLOTS, atoi(ev))) : MPC_HIO_DEFAULT_SLOTS;
+        for (int b = 0; b < h->nslots; ++b) {
             cudaStreamCreateWithFlags(&h->cs[b], cudaStreamNonBlocking);
             cudaEventCreateWithFlags(&h->in_ready[b], cudaEventDisableTiming);
             cudaEventCreateWithFlags(&h->comp_done[b], cudaEventDisableTiming);
@@ -1308,11 +1333,22 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
     const int np = c->cfg.mode == MPC_MODE_PAIR ? 1 : 2;
     const int p0 = c->cfg.mode == MPC_MODE_PAIR ? c->cfg.party : 0;
     // PAIR kernels own the per-warp exchange slots: their chunks run one after another
-    const int nslots = is_pair(c) ? 1 : HIO_SLOTS;
+    const int nslots = is_pair(c) ? 1 : h->nslots;
     // chunk schedule: chunk_rows, or (0) four equal chunks -- measured best for cfg2 among 768..6144-row
     // chunks and a short-long-short ramp (tools/perf_e2e.py)
     std::vector<i64> sched;
-    {
+    static const char* ramp = getenv("MPC_HIO_SCHED");   // experiments: explicit chunk list "r0,r1,..."
+    if (ramp && chunk_rows == 0) {
+        i64 r = 0;
+        for (const char* q = ramp; *q && r < rows;) {
+            const i64 v = std::max<i64>(32, strtoll(q, nullptr, 10) / 32 * 32);
+            sched.push_back(std::min<i64>(v, rows - r));
+            r += sched.back();
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+        while (r < rows) { sched.push_back(std::min<i64>(sched.back(), rows - r)); r += sched.back(); }
+    } else {
         const i64 cr = chunk_rows > 0 ? chunk_rows : std::max<i64>(32, ((rows + 3) / 4 + 31) / 32 * 32);
         for (i64 r = 0; r < rows; r += cr) sched.push_back(std::min<i64>(cr, rows - r));
     }
@@ -1322,11 +1358,22 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
     cudaStream_t user = c->stream;
     cudaEventRecord(h->start, user);
     cudaStreamWaitEvent(h->h2d, h->start, 0);
+    // MPC_HIO_TRACE=1 (diagnostics only): per-chunk timeline of the copies and the compute on stderr
+    static const bool trace = getenv("MPC_HIO_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t s) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        tev.push_back(e);
+    };
+    mark(h->h2d);
     const u32 s0 = (u32)c->step;
     const i64 nchunks = (i64)sched.size();
     i64 r0 = 0;
     for (i64 i = 0; i < nchunks; r0 += sched[(size_t)i], ++i) {
-        const int b = (int)(i % HIO_SLOTS);
+        const int b = (int)(i % h->nslots);
         const int cb = (int)(i % nslots);
         const i64 ri = sched[(size_t)i];
         const size_t bytes = sizeof(u64) * (size_t)(ri * cols);
@@ -1338,12 +1385,16 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         u64* dx[2] = {h->dbuf[b], h->dbuf[b] + half / 8};
         u64* dz[2] = {h->dbuf[b] + 2 * (half / 8), h->dbuf[b] + 3 * (half / 8)};
         if (h->used[b]) cudaStreamWaitEvent(h->h2d, h->out_done[b], 0);
-        for (int q = 0; q < np; ++q) {
-            const int pp = parties[p0 + q];
-            cudaMemcpyAsync(dx[pp], hx.sh[pp] + r0 * cols, bytes, cudaMemcpyHostToDevice, h->h2d);
+        mark(h->h2d);
+        {
+            void* dst[2]; void* src[2];
+            for (int q = 0; q < np; ++q) { dst[q] = dx[parties[p0 + q]]; src[q] = hx.sh[parties[p0 + q]] + r0 * cols; }
+            copy_batch(dst, src, bytes, np, h->h2d, cudaMemcpyHostToDevice);
         }
         cudaEventRecord(h->in_ready[b], h->h2d);
+        mark(h->h2d);
         cudaStreamWaitEvent(h->cs[cb], h->in_ready[b], 0);
+        mark(h->cs[cb]);
         // launch on the slot's stream with the slot's own scratch
         void* save_scr = c->scratch; size_t save_bytes = c->scratch_bytes;
         c->stream = h->cs[cb]; c->scratch = h->scr[cb]; c->scratch_bytes = h->scr_bytes[cb];
@@ -1354,16 +1405,31 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         c->scratch = save_scr; c->scratch_bytes = save_bytes; c->stream = user;
         if (st) return st;
         cudaEventRecord(h->comp_done[b], h->cs[cb]);
+        mark(h->cs[cb]);
         cudaStreamWaitEvent(h->d2h, h->comp_done[b], 0);
-        for (int q = 0; q < np; ++q) {
-            const int pp = parties[p0 + q];
-            cudaMemcpyAsync(hz.sh[pp] + r0 * cols, dz[pp], bytes, cudaMemcpyDeviceToHost, h->d2h);
+        mark(h->d2h);
+        {
+            void* dst[2]; void* src[2];
+            for (int q = 0; q < np; ++q) { dst[q] = hz.sh[parties[p0 + q]] + r0 * cols; src[q] = dz[parties[p0 + q]]; }
+            copy_batch(dst, src, bytes, np, h->d2h, cudaMemcpyDeviceToHost);
         }
         cudaEventRecord(h->out_done[b], h->d2h);
+        mark(h->d2h);
         h->used[b] = true;
     }
     cudaEventRecord(h->start, h->d2h);
     cudaStreamWaitEvent(user, h->start, 0);          // the call completes in the caller's stream order
+    if (trace) {
+        cudaDeviceSynchronize();
+        fprintf(stderr, "hostio trace (ms from start): chunk rows | h2d start end | comp start end | d2h start end\n");
+        for (i64 i = 0; i < nchunks; ++i) {
+            float t[6];
+            for (int j = 0; j < 6; ++j) cudaEventElapsedTime(&t[j], tev[0], tev[1 + 6 * (size_t)i + j]);
+            fprintf(stderr, "  %3lld %5lld | %.3f %.3f | %.3f %.3f | %.3f %.3f\n", (long long)i, (long long)sched[(size_t)i],
+                    t[0], t[1], t[2], t[3], t[4], t[5]);
+        }
+        for (cudaEvent_t e : tev) cudaEventDestroy(e);
+    }
     if ((st = cuda_check(c, "softmax_hostio"))) return st;
     acct_softmax(c, rows, cols, p);
     finish(c, steps);
