@@ -1,6 +1,11 @@
 """PCIe copy microbenchmark: H2D alone, D2H alone and both directions concurrently (separate
 streams, pinned host memory) -- the ceiling of the host-buffer e2e path."""
+import os
+import sys
+
 import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 MB = 1 << 20
 
