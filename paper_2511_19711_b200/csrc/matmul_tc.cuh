@@ -46,6 +46,10 @@ __host__ __device__ inline int tc_tile_off(int r, int kb) { return (r >> 3) * 25
 struct LimbArgs {
     const u64* t[3]; int nt; int rows, K, Kp, rhs, rows_blk; int batch; i64 in_stride; u8* out;
 };
+// Each term occupies its own whole K blocks: term t holds k' in [t Kpad, t Kpad + K), Kpad =
+// 32 ceil(K / 32), the rest zero (zeros add nothing to the products), so Kp = nt Kpad and the
+// fused BOTH-mode kernels below can write a term's tile without touching its neighbours.
+__host__ __device__ inline int tc_kpad(int K) { return (K + TC_BK - 1) / TC_BK * TC_BK; }
 // RHS limb tiling through a shared-memory transpose: one CTA per (batch, 64-column block, K block
 // of 32): coalesced loads of 32 rows x 64 columns, then 128 threads pack the 64 x 2 core-matrix
 // rows of all 8 limbs and write the 16 KB chunk contiguously.
@@ -53,7 +57,7 @@ __global__ void __launch_bounds__(2 * TC_BN) k_mm_limbs_rhs(LimbArgs a)
 {
     __shared__ u64 sm[TC_BK][TC_BN + 1];
     const int KB = a.Kp / TC_BK, NB = (a.rows + TC_BN - 1) / TC_BN;
-    const int Ktot = a.nt * a.K;
+    const int Kpad = tc_kpad(a.K);
     const i64 ntile = (i64)a.batch * NB * KB;
     for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
         const int b = (int)(tile / ((i64)NB * KB));
@@ -62,10 +66,8 @@ __global__ void __launch_bounds__(2 * TC_BN) k_mm_limbs_rhs(LimbArgs a)
             const int kr = l / TC_BN, nc = l - kr * TC_BN;
             const int kk = kb * TC_BK + kr, n = nb * TC_BN + nc;
             u64 v = 0;
-            if (kk < Ktot && n < a.rows) {
-                const int t = kk / a.K, k = kk - t * a.K;
-                v = a.t[t][(i64)b * a.in_stride + (i64)k * a.rows + n];
-            }
+            const int t = kk / Kpad, k = kk - t * Kpad;
+            if (t < a.nt && k < a.K && n < a.rows) v = a.t[t][(i64)b * a.in_stride + (i64)k * a.rows + n];
             sm[kr][nc] = v;
         }
         __syncthreads();
@@ -97,7 +99,7 @@ __global__ void __launch_bounds__(256) k_mm_limbs_lhs(LimbArgs a)
 {
     __shared__ u64 sm[TC_BM][TC_BK + 1];
     const int KB = a.Kp / TC_BK, MB = (a.rows + TC_BM - 1) / TC_BM;
-    const int Ktot = a.nt * a.K;
+    const int Kpad = tc_kpad(a.K);
     const i64 ntile = (i64)a.batch * MB * KB;
     for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
         const int b = (int)(tile / ((i64)MB * KB));
@@ -106,10 +108,8 @@ __global__ void __launch_bounds__(256) k_mm_limbs_lhs(LimbArgs a)
             const int r = l / TC_BK, kc = l - r * TC_BK;
             const int kk = kb * TC_BK + kc, m = mb * TC_BM + r;
             u64 v = 0;
-            if (kk < Ktot && m < a.rows) {
-                const int t = kk / a.K, k = kk - t * a.K;
-                v = a.t[t][(i64)b * a.in_stride + (i64)m * a.K + k];
-            }
+            const int t = kk / Kpad, k = kk - t * Kpad;
+            if (t < a.nt && k < a.K && m < a.rows) v = a.t[t][(i64)b * a.in_stride + (i64)m * a.K + k];
             sm[r][kc] = v;
         }
         __syncthreads();
@@ -131,6 +131,151 @@ __global__ void __launch_bounds__(256) k_mm_limbs_lhs(LimbArgs a)
             for (int i = 0; i < 8; ++i) *reinterpret_cast<uint4*>(dst + (i64)i * TC_A_TILE + off) = limb[i];
         }
         __syncthreads();
+    }
+}
+
+// ---- BOTH mode: Beaver masking fused with the limb tiling ------------------------------------
+// One pass over the input shares of one operand writes every limb tile the GEMM reads (DESIGN.md
+// 2.10): the thread derives the triple shares r0 = A_0 (key K_0), r1 = A_1 (key K_1) of its
+// elements from the PRG (unit = global element index, slot 8 for X, 9 for Y; the same values as
+// the mask pass of the PAIR path), opens E = (x_0 - r0) + (x_1 - r1) in registers, and packs the
+// terms of both parties:
+//   X: party 0 [E, A0],        party 1 [As = A0 + A1, E, A1]
+//   Y: party 0 [B0 + F, F],    party 1 [Bs = B0 + B1, B1, F]
+// in term-padded K blocks (tc_kpad).  The mask pass wrote 4 planes (32 B / element) that the limb
+// pass read back (40 B) before writing the limbs (40 B); here 16 B are read and 40 B written.
+struct FuseArgs {
+    Keys keys; u32 s; const u64* x0; const u64* x1; int rows, K, batch; u64 goff; u8* out0; u8* out1;
+};
+
+// pack FW (4 or 8) u64 into the 8 limbs' FW-byte pieces (piece i = bytes i of v[0..FW-1]) and
+// store them at (row r, k byte kb) of the 8 consecutive limb tiles of a chunk
+constexpr int FW = 4;                                  // elements (k) per thread in the fused kernels
+__device__ __forceinline__ void tc_store(u8* chunk, int tile_bytes, int r, int kb, const u64 (&v)[FW])
+{
+    const int off = tc_tile_off(r, kb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        u32 w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w |= ((u32)(v[e] >> (8 * i)) & 0xffu) << (8 * e);
+        *reinterpret_cast<u32*>(chunk + (i64)i * tile_bytes + off) = w;
+    }
+}
+
+__device__ __forceinline__ u64 prg_pick(const uint4& R, u64 u) { return (u & 1) ? w64(R.z, R.w) : w64(R.x, R.y); }
+
+// X (LHS, [batch][M][K]): CTA = 32 rows x 32 k of one (batch, 128-row block, K block); thread =
+// (row, FW consecutive k): loads first, then the PRG blocks of the (at most 3) unit pairs.
+__global__ void __launch_bounds__(256) k_mm_fuse_lhs(FuseArgs a)
+{
+    constexpr int TPR = TC_BK / FW, RPC = 256 / TPR, QB = TC_BM / RPC;   // threads per row, rows per CTA
+    const int KB = tc_kpad(a.K) / TC_BK, MB = (a.rows + TC_BM - 1) / TC_BM;
+    const i64 ntile = (i64)a.batch * QB * MB * KB;
+    const int kq = threadIdx.x % TPR, rl = threadIdx.x / TPR;
+    for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int b = (int)(tile / ((i64)QB * MB * KB));
+        const int rem = (int)(tile - (i64)b * QB * MB * KB), hb = rem / KB, kb = rem - hb * KB;
+        const int mb = hb / QB, r = (hb % QB) * RPC + rl, m = mb * TC_BM + r, k0 = kb * TC_BK + kq * FW;
+        const i64 base = ((i64)b * a.rows + m) * a.K;
+        const u64 u0 = (a.goff + (u64)b) * (u64)a.rows * (u64)a.K + (u64)m * (u64)a.K + (u64)k0;
+        u64 x0[FW], x1[FW];
+        bool ok[FW];
+#pragma unroll
+        for (int e = 0; e < FW; ++e) {
+            ok[e] = m < a.rows && k0 + e < a.K;
+            x0[e] = ok[e] ? __ldg(a.x0 + base + k0 + e) : 0;
+            x1[e] = ok[e] ? __ldg(a.x1 + base + k0 + e) : 0;
+        }
+        uint4 R0[FW / 2 + 1], R1[FW / 2 + 1];
+#pragma unroll
+        for (int j = 0; j <= FW / 2; ++j) {
+            if (j < FW / 2 || (u0 & 1)) {
+                R0[j] = prg(a.keys.k0, (u0 >> 1) + j, a.s, 8u);
+                R1[j] = prg(a.keys.k1, (u0 >> 1) + j, a.s, 8u);
+            } else R0[j] = R1[j] = make_uint4(0, 0, 0, 0);
+        }
+        u64 E[FW], A0[FW], A1[FW];
+#pragma unroll
+        for (int e = 0; e < FW; ++e) {
+            const u64 u = u0 + e;
+            const int j = (e + (int)(u0 & 1)) >> 1;              // block of unit u (register select, no local array)
+            uint4 P0 = R0[0], P1 = R1[0];
+#pragma unroll
+            for (int q = 1; q <= FW / 2; ++q) if (j == q) { P0 = R0[q]; P1 = R1[q]; }
+            const u64 r0 = ok[e] ? prg_pick(P0, u) : 0, r1 = ok[e] ? prg_pick(P1, u) : 0;
+            A0[e] = r0; A1[e] = r1;
+            E[e] = ok[e] ? (x0[e] - r0) + (x1[e] - r1) : 0;
+        }
+        const int kbyte = kq * FW;
+        u8* c0 = a.out0 + (((i64)b * MB + mb) * 2 * KB) * (i64)TC_A_CHUNK;
+        u8* c1 = a.out1 + (((i64)b * MB + mb) * 3 * KB) * (i64)TC_A_CHUNK;
+        tc_store(c0 + (i64)(0 * KB + kb) * TC_A_CHUNK, TC_A_TILE, r, kbyte, E);
+        tc_store(c0 + (i64)(1 * KB + kb) * TC_A_CHUNK, TC_A_TILE, r, kbyte, A0);
+        tc_store(c1 + (i64)(1 * KB + kb) * TC_A_CHUNK, TC_A_TILE, r, kbyte, E);
+        tc_store(c1 + (i64)(2 * KB + kb) * TC_A_CHUNK, TC_A_TILE, r, kbyte, A1);
+#pragma unroll
+        for (int e = 0; e < FW; ++e) A0[e] += A1[e];
+        tc_store(c1 + (i64)(0 * KB + kb) * TC_A_CHUNK, TC_A_TILE, r, kbyte, A0);
+    }
+}
+
+// Y (RHS, [batch][K][N], packed K-major per column n): CTA = 64 columns x 32 k of one (batch,
+// 64-column group, K block); thread = (2 adjacent columns, FW consecutive k), so both halves of a
+// PRG block are used when the column pair is unit-aligned.
+__global__ void __launch_bounds__(256) k_mm_fuse_rhs(FuseArgs a)
+{
+    constexpr int TPC = TC_BK / FW, CPC = 2 * (256 / TPC);              // threads per column pair, columns per CTA
+    const int KB = tc_kpad(a.K) / TC_BK, NB = (a.rows + TC_BN - 1) / TC_BN, NG = (a.rows + CPC - 1) / CPC;
+    const i64 ntile = (i64)a.batch * NG * KB;
+    const int kq = threadIdx.x % TPC, np = threadIdx.x / TPC;
+    for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+        const int b = (int)(tile / ((i64)NG * KB));
+        const int rem = (int)(tile - (i64)b * NG * KB), ng = rem / KB, kb = rem - ng * KB;
+        const int n = ng * CPC + 2 * np, k0 = kb * TC_BK + kq * FW;
+        const i64 base = (i64)b * a.K * a.rows;
+        const u64 ub = (a.goff + (u64)b) * (u64)a.K * (u64)a.rows;
+        u64 y0[2][FW], y1[2][FW];
+#pragma unroll
+        for (int e = 0; e < FW; ++e)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const bool v = k0 + e < a.K && n + j < a.rows;
+                const i64 idx = base + (i64)(k0 + e) * a.rows + n + j;
+                y0[j][e] = v ? __ldg(a.x0 + idx) : 0;
+                y1[j][e] = v ? __ldg(a.x1 + idx) : 0;
+            }
+        u64 F[2][FW], B0[2][FW], B1[2][FW];
+#pragma unroll
+        for (int e = 0; e < FW; ++e) {
+            const int k = k0 + e;
+            const u64 u = ub + (u64)k * (u64)a.rows + (u64)n;
+            const bool v0 = k < a.K && n < a.rows, v1 = k < a.K && n + 1 < a.rows;
+            uint4 R0 = make_uint4(0, 0, 0, 0), R1 = R0, S0, S1;
+            if (v0) { R0 = prg(a.keys.k0, u >> 1, a.s, 9u); R1 = prg(a.keys.k1, u >> 1, a.s, 9u); }
+            S0 = R0; S1 = R1;
+            if (v1 && (u & 1)) { S0 = prg(a.keys.k0, (u >> 1) + 1, a.s, 9u); S1 = prg(a.keys.k1, (u >> 1) + 1, a.s, 9u); }
+            const u64 r00 = v0 ? prg_pick(R0, u) : 0, r10 = v0 ? prg_pick(R1, u) : 0;
+            const u64 r01 = v1 ? prg_pick(S0, u + 1) : 0, r11 = v1 ? prg_pick(S1, u + 1) : 0;
+            B0[0][e] = r00; B1[0][e] = r10; F[0][e] = v0 ? (y0[0][e] - r00) + (y1[0][e] - r10) : 0;
+            B0[1][e] = r01; B1[1][e] = r11; F[1][e] = v1 ? (y0[1][e] - r01) + (y1[1][e] - r11) : 0;
+        }
+        const int kbyte = kq * FW;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int nn = n + j, nb = nn / TC_BN, rr = nn - nb * TC_BN;
+            if (nb >= NB) continue;
+            u8* c0 = a.out0 + (((i64)b * NB + nb) * 2 * KB) * (i64)TC_B_CHUNK;
+            u8* c1 = a.out1 + (((i64)b * NB + nb) * 3 * KB) * (i64)TC_B_CHUNK;
+            u64 G[FW], Bs[FW];
+#pragma unroll
+            for (int e = 0; e < FW; ++e) { G[e] = B0[j][e] + F[j][e]; Bs[e] = B0[j][e] + B1[j][e]; }
+            tc_store(c0 + (i64)(0 * KB + kb) * TC_B_CHUNK, TC_B_TILE, rr, kbyte, G);
+            tc_store(c0 + (i64)(1 * KB + kb) * TC_B_CHUNK, TC_B_TILE, rr, kbyte, F[j]);
+            tc_store(c1 + (i64)(0 * KB + kb) * TC_B_CHUNK, TC_B_TILE, rr, kbyte, Bs);
+            tc_store(c1 + (i64)(1 * KB + kb) * TC_B_CHUNK, TC_B_TILE, rr, kbyte, B1[j]);
+            tc_store(c1 + (i64)(2 * KB + kb) * TC_B_CHUNK, TC_B_TILE, rr, kbyte, F[j]);
+        }
     }
 }
 

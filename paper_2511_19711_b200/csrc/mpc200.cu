@@ -908,17 +908,21 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
     // scratch: operand planes (4 (nA + nB) u64), then for the tensor-core engine the limb-tiled
     // operands of each computed party (party 0: K' = 2K, party 1: K' = 3K)
     const i64 MB = (M + TC_BM - 1) / TC_BM, NB = (N + TC_BN - 1) / TC_BN;
-    const i64 Kp0 = (2 * K + TC_BK - 1) / TC_BK * TC_BK, Kp1 = (3 * K + TC_BK - 1) / TC_BK * TC_BK;
+    const i64 Kpad = tc_kpad((int)K), Kp0 = 2 * Kpad, Kp1 = 3 * Kpad;     // term-padded K' (matmul_tc.cuh)
     const i64 la0 = batch * MB * (Kp0 / TC_BK) * TC_A_CHUNK, lb0 = batch * NB * (Kp0 / TC_BK) * TC_B_CHUNK;
     const i64 la1 = batch * MB * (Kp1 / TC_BK) * TC_A_CHUNK, lb1 = batch * NB * (Kp1 / TC_BK) * TC_B_CHUNK;
-    const size_t plane_bytes = sizeof(u64) * 4 * (size_t)(nA + nB);
+    // BOTH mode + tensor cores: the masking is fused into the limb tiling (no operand planes)
+    const bool fused = use_tc && c->cfg.mode == MPC_MODE_BOTH;
+    const size_t plane_bytes = fused ? 0 : sizeof(u64) * 4 * (size_t)(nA + nB);
     const size_t limb_bytes = use_tc ? (size_t)(la0 + lb0 + la1 + lb1) : 0;
     u8* sc = (u8*)scratch(c, plane_bytes + limb_bytes);
     if (!sc) return fail(c, MPC_ERR_NOMEM, "matmul scratch");
     u64 *PA = (u64*)sc, *PB = PA + 4 * nA;
     const u32 s = (u32)c->step;
-    if ((st = launch_pairs(c, nA, (u64)(batch_off * M * K), MmMaskBody{s, 8u, spv(c, x), nA, PA, 0}, "mm_mask"))) return st;
-    if ((st = launch_pairs(c, nB, (u64)(batch_off * K * N), MmMaskBody{s, 9u, spv(c, y), nB, PB, 1}, "mm_mask"))) return st;
+    if (!fused) {
+        if ((st = launch_pairs(c, nA, (u64)(batch_off * M * K), MmMaskBody{s, 8u, spv(c, x), nA, PA, 0}, "mm_mask"))) return st;
+        if ((st = launch_pairs(c, nB, (u64)(batch_off * K * N), MmMaskBody{s, 9u, spv(c, y), nB, PB, 1}, "mm_mask"))) return st;
+    }
     MmArgs a;
     memset(&a, 0, sizeof a);
     a.K = c->K; a.s = s; a.M = (int)M; a.Kd = (int)K; a.N = (int)N; a.batch = (int)batch; a.goff = (u64)batch_off; a.tb = tb;
@@ -944,7 +948,19 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
         u8* LA[2] = {lp, lp + la0 + lb0};
         u8* LB[2] = {lp + la0, lp + la0 + lb0 + la1};
         const i64 Kps[2] = {Kp0, Kp1};
-        for (int p = a.p0; p < a.p0 + a.np; ++p) {
+        if (fused) {
+            const i64 KBn = Kpad / TC_BK;
+            FuseArgs fx{c->K, s, x.sh[0], x.sh[1], (int)M, (int)K, (int)batch, (u64)batch_off, LA[0], LA[1]};
+            FuseArgs fy{c->K, s, y.sh[0], y.sh[1], (int)N, (int)K, (int)batch, (u64)batch_off, LB[0], LB[1]};
+            rec_begin(c, "mm_fuse", (u64)(nA + nB));
+            // tiles: LHS 32 rows x 32 k, RHS 64 columns x 32 k (FW = 4 elements per thread)
+            k_mm_fuse_lhs<<<(unsigned)std::min<i64>(batch * 4 * MB * KBn, (i64)c->sm_count * 16), 256, 0, c->stream>>>(fx);
+            k_mm_fuse_rhs<<<(unsigned)std::min<i64>(batch * ((N + 63) / 64) * KBn, (i64)c->sm_count * 16), 256, 0, c->stream>>>(fy);
+            rec_end(c);
+            c->st.launches += 2;
+            for (int p = 0; p < 2; ++p) { t.A[p] = LA[p]; t.B[p] = LB[p]; t.Kp[p] = (int)Kps[p]; }
+        }
+        for (int p = a.p0; p < a.p0 + a.np && !fused; ++p) {
             LimbArgs la{}, lb{};
             for (int q = 0; q < a.nt[p]; ++q) { la.t[q] = a.t[p][q].a; lb.t[q] = a.t[p][q].b; }
             la.nt = lb.nt = a.nt[p];
