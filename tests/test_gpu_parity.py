@@ -579,7 +579,7 @@ def test_layernorm_fused_equals_composed(mpc):
     assert torch.equal(z[0], out[0]) and torch.equal(z[1], out[1])
 
 
-@pytest.mark.parametrize("rows,cols", [(1, 1), (31, 1), (33, 2), (1, 3), (64, 17), (5, 1025)])
+@pytest.mark.parametrize("rows,cols", [(1, 1), (31, 1), (33, 2), (1, 3), (64, 17), (5, 1025), (3, 16384), (2, 20001)])
 def test_softmax_edge_shapes(mpc, rows, cols):
     """Degenerate and ragged softmax shapes: a single column (no max-tree level), two and three
     columns (odd carry), one row, 17 columns (CTA tree with an odd level), 1025 columns (global
@@ -588,6 +588,18 @@ def test_softmax_edge_shapes(mpc, rows, cols):
     x = workloads.softmax_inputs(rows, cols)
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
     same(c.softmax(gx, rows, cols, row_off=96), o.softmax(ox, rows, cols, row_off=96))
+    assert c.step == o.step
+
+
+@pytest.mark.parametrize("rows,cols", [(3, 16384), (2, 20001)])
+def test_long_rows_max_layernorm(mpc, rows, cols):
+    """Rows far beyond the shared-memory staging (16K / 20K elements: the global work tile path)
+    for the row max and LayerNorm."""
+    c, o = pair_ctx(mpc, 2, step=9)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.max(gx, rows, cols, row_off=32), o.max(ox, rows, cols, row_off=32))
+    same(c.layernorm(gx, rows, cols, row_off=64), o.layernorm(ox, rows, cols, row_off=64))
     assert c.step == o.step
 
 
