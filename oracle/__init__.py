@@ -69,7 +69,7 @@ def lib():
         L.orc_maxpool2d.argtypes = [CP, u64p, u64p, u64p, u64p, INT, INT, INT, INT, INT, INT, INT,
                                     I64, INT]
         L.orc_softmax.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, INT,
-                                  INT, INT, INT, INT, INT, INT, INT, INT, INT, INT]
+                                  INT, INT, INT, INT, INT, INT, INT, INT, INT, INT, INT]
         L.orc_layernorm.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, DBL, INT,
                                     INT, INT, INT, INT, INT, INT]
         L.orc_ltz_gate_count.argtypes = [INT]; L.orc_ltz_gate_count.restype = INT
@@ -221,12 +221,12 @@ class Oracle:
 
     def softmax(self, x, rows, cols, row_off=0, window=33, exp_t=8, exp_clamp=0, exp_window=33,
                 recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0, recip_square=0,
-                bcast=0):
+                bcast=0, causal=0):
         x0, x1 = _u(x[0]), _u(x[1])
         z0, z1 = _pair(rows * cols)
         lib().orc_softmax(ctypes.byref(self.c), x0, x1, z0, z1, rows, cols, row_off, window,
                           exp_t, exp_clamp, exp_window, exp_square, recip_iters, recip_t, recip_clamp,
-                          recip_window, recip_square, bcast)
+                          recip_window, recip_square, bcast, int(causal))
         return z0, z1
 
     def layernorm(self, x, rows, cols, row_off=0, eps=1e-5, mean_mode=0, rsqrt_iters=3,

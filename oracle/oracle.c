@@ -735,16 +735,37 @@ void orc_maxpool2d(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
 /*   m = MAX_row(x); d = x - m; e = EXP(d) [units: element index];             */
 /*   S = rowsum(e); r = RECIP(S) [units: row]; out = MT(e, bcast r) [element]  */
 /* ------------------------------------------------------------------------ */
+/* causal (reading R24c): the rows are the T x T score blocks of causal attention,
+ * T = cols; global row g attends to columns j <= g mod T.  The masked entries enter the max as
+ * the public constant -2^(w-2) (below every in-window value, so never the maximum), their
+ * exponentials are replaced by the public 0 before the row sum, and their outputs are the
+ * public 0.  Same units and steps as the dense softmax.                                        */
+static int causal_masked(i64 row_off, i64 r, i64 j, i64 cols) { return j > (row_off + r) % cols; }
+
 void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
                  i64 rows, i64 cols, i64 row_off, int w,
                  int exp_t, int exp_clamp, int exp_w, int exp_sq,
-                 int rc_iters, int rc_t, int rc_clamp, int rc_w, int rc_sq, int bcast)
+                 int rc_iters, int rc_t, int rc_clamp, int rc_w, int rc_sq, int bcast, int causal)
 {
     i64 n = rows * cols;
     u64 *mx0 = A(rows), *mx1 = A(rows), *e0 = A(n), *e1 = A(n), *S0 = A(rows), *S1 = A(rows);
     u64 *r0 = A(rows), *r1 = A(rows), *b0 = A(n), *b1 = A(n);
-    if (rows > 0 && cols > 0) MAXROW(ctx, rows, cols, row_off, w, x0, x1, mx0, mx1);
-    else ctx->step += 2 * (u64)max_levels(cols);
+    if (rows > 0 && cols > 0) {
+        if (causal) {                                  /* masked inputs of the max: public -2^(w-2) */
+            u64 *m0 = A(n), *m1 = A(n);
+            const u64 L = w >= 2 ? (u64)0 - ((u64)1 << (w - 2)) : (u64)0 - 1;
+            for (i64 r = 0; r < rows; ++r)
+                for (i64 j = 0; j < cols; ++j) {
+                    int msk = causal_masked(row_off, r, j, cols);
+                    m0[r * cols + j] = msk ? L : x0[r * cols + j];
+                    m1[r * cols + j] = msk ? 0 : x1[r * cols + j];
+                }
+            MAXROW(ctx, rows, cols, row_off, w, m0, m1, mx0, mx1);
+            free(m0); free(m1);
+        } else {
+            MAXROW(ctx, rows, cols, row_off, w, x0, x1, mx0, mx1);
+        }
+    } else ctx->step += 2 * (u64)max_levels(cols);
     for (i64 r = 0; r < rows; ++r)
         for (i64 j = 0; j < cols; ++j) {
             e0[r * cols + j] = x0[r * cols + j] - mx0[r];
@@ -752,6 +773,10 @@ void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
         }
     u64 Ue = (u64)(row_off * cols);
     EXP(ctx, n, Ue, exp_t, exp_clamp, exp_w, exp_sq, e0, e1, e0, e1);
+    if (causal)
+        for (i64 r = 0; r < rows; ++r)
+            for (i64 j = 0; j < cols; ++j)
+                if (causal_masked(row_off, r, j, cols)) e0[r * cols + j] = e1[r * cols + j] = 0;
     for (i64 r = 0; r < rows; ++r) {
         u64 a = 0, b = 0;
         for (i64 j = 0; j < cols; ++j) { a += e0[r * cols + j]; b += e1[r * cols + j]; }
@@ -766,6 +791,10 @@ void orc_softmax(orc_ctx* ctx, const u64* x0, const u64* x1, u64* z0, u64* z1,
             for (i64 j = 0; j < cols; ++j) { b0[r * cols + j] = r0[r]; b1[r * cols + j] = r1[r]; }
         MT(ctx, n, Ue, e0, e1, b0, b1, z0, z1);
     }
+    if (causal)
+        for (i64 r = 0; r < rows; ++r)
+            for (i64 j = 0; j < cols; ++j)
+                if (causal_masked(row_off, r, j, cols)) z0[r * cols + j] = z1[r * cols + j] = 0;
     free(mx0); free(mx1); free(e0); free(e1); free(S0); free(S1); free(r0); free(r1); free(b0); free(b1);
 }
 
