@@ -68,7 +68,7 @@ class ActP(ctypes.Structure):
 
 
 class SoftmaxP(ctypes.Structure):
-    _fields_ = [("window", INT), ("exp", ExpP), ("recip", NrP), ("bcast", INT)]
+    _fields_ = [("window", INT), ("exp", ExpP), ("recip", NrP), ("bcast", INT), ("causal", INT)]
 
 
 class LnP(ctypes.Structure):
@@ -444,9 +444,10 @@ class Ctx:
 
     def softmax(self, x, rows, cols, row_off=0, window=33, exp_t=8, exp_clamp=0, exp_window=33,
                 recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0, recip_square=0,
-                bcast=0, out=None):
+                bcast=0, causal=0, out=None):
         p = SoftmaxP(window, ExpP(exp_t, int(exp_clamp), exp_window, int(exp_square)),
-                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))), int(bcast))
+                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))), int(bcast),
+                     int(causal))
         z = out if out is not None else self._empty(rows * cols)
         self._stream()
         self._chk(_L.mpc_softmax(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)), "mpc_softmax")
@@ -454,11 +455,12 @@ class Ctx:
 
     def softmax_hostio(self, hx, hz, rows, cols, row_off=0, chunk_rows=2048, window=33, exp_t=8, exp_clamp=0,
                        exp_window=33, recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0,
-                       recip_square=0, bcast=0):
+                       recip_square=0, bcast=0, causal=0):
         """Softmax over HOST buffers (hx, hz: per-party CPU uint64 tensors, pinned): chunked, with the
         H2D copies, the compute and the D2H copies of neighbouring chunks overlapped."""
         p = SoftmaxP(window, ExpP(exp_t, int(exp_clamp), exp_window, int(exp_square)),
-                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))), int(bcast))
+                     NrP(recip_iters, ExpP(recip_t, int(recip_clamp), recip_window, int(recip_square))), int(bcast),
+                     int(causal))
         self._stream()
         self._chk(_L.mpc_softmax_hostio(self._h, _sh_host(hx), _sh_host(hz), rows, cols, row_off, ctypes.byref(p),
                                         chunk_rows), "mpc_softmax_hostio")

@@ -385,9 +385,9 @@ struct OpenBody {
 // the last level writes mx[rr].  Steps s + 2*lv (LTZ), s + 2*lv + 1 (mux BM).
 // A holds levels 0, 2, 4.. (stride HA = ceil(cols/2)), B levels 1, 3, .. (stride HB = ceil(HA/2)).
 // cone: the level's LTZs use the carry-cone circuit, CG groups per warp (ltz_cone.cuh).
-template <bool WIDE, bool CONE, class P>
+template <bool WIDE, bool CONE, class P, bool CAUSAL = false>
 __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i64 cols, int R, u64 g0,
-                                         SO A, SO B, i64 HA, i64 HB, SO mx, ConeSmem<CG>* cone)
+                                         SO A, SO B, i64 HA, i64 HB, SO mx, ConeSmem<CG>* cone, u64 cL = 0)
 {
     using S = typename P::S;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
@@ -395,6 +395,13 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
     int lv = 0;
     SP cur = in;
     i64 li = ldi;
+    // level-0 entry (row rr, column col); causal softmax: columns past the row's
+    // position g mod cols enter as the public constant cL (party 0 holds it)
+    auto ldc = [&](i64 rr, i64 col) -> S {
+        if constexpr (CAUSAL)
+            if (lv == 0 && col > (i64)((g0 + (u64)rr) % (u64)cols)) return pr.addp(pr.zero(), cL);
+        return pr.ld(cur, rr * li + col);
+    };
     while (m > 1) {
         const i64 h = m / 2, mn = h + (m & 1);
         SO o; i64 lo;
@@ -414,7 +421,7 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
                     d[g] = pr.zero();
                     if (b * CG + g < h && v < (i64)R * h) {
                         const i64 rr = fdiv((u32)v, dh), i = v - rr * h;
-                        d[g] = pr.sub(pr.ld(cur, rr * li + i), pr.ld(cur, rr * li + i + h));
+                        d[g] = pr.sub(ldc(rr, i), ldc(rr, i + h));
                     }
                 }
                 pr.template ltz_cone<CG>((ubase >> 5) + (u64)(b * CG), sl, w, d, l, lane, cone[warp]);
@@ -424,11 +431,11 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
                     const bool valid = b * CG + g < h && v < (i64)R * h;
                     i64 rr = 0, i = 0;
                     S y = pr.zero();
-                    if (valid) { rr = fdiv((u32)v, dh); i = v - rr * h; y = pr.ld(cur, rr * li + i + h); }
+                    if (valid) { rr = fdiv((u32)v, dh); i = v - rr * h; y = ldc(rr, i + h); }
                     const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d[g], pr.notb(l[g])));
                     if (valid) {
                         pr.st(o, rr * lo + i, sel);
-                        if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, pr.ld(cur, rr * li + m - 1));
+                        if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, ldc(rr, m - 1));
                     }
                 }
             }
@@ -446,15 +453,15 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
             S d = pr.zero(), y = pr.zero();
             if (valid) {
                 rr = fdiv((u32)v, dh); i = v - rr * h;
-                y = pr.ld(cur, rr * li + i + h);
-                d = pr.sub(pr.ld(cur, rr * li + i), y);
+                y = ldc(rr, i + h);
+                d = pr.sub(ldc(rr, i), y);
             }
             const u64 q = (ubase >> 5) + (u64)g;
             const S c = pr.notb(pr.template ltz_o<WIDE>(q, sl, w, d, lane));
             const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
             if (valid) {
                 pr.st(o, rr * lo + i, sel);
-                if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, pr.ld(cur, rr * li + m - 1));
+                if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, ldc(rr, m - 1));
             }
         }
         __syncthreads();
@@ -545,6 +552,8 @@ struct SoftmaxArgs {
     int cone;               // carry-cone LTZ in the max tree (NEXT #1)
     int bcast;              // broadcast triple for the final e * r (NEXT #2)
     int esmem;              // E tile in the work area (aliasing the dead max-tree levels), not escratch
+    int causal;             // causal attention rows
+    u64 causal_L;           // public constant of the masked max-tree inputs, -2^(w-2)
 };
 
 // work tile (u64 words), HA = ceil(cols/2), HB = ceil(HA/2): A0 A1 (2 x 32HA), B0 B1 (2 x 32HB),
@@ -564,7 +573,7 @@ __host__ __device__ inline i64 softmax_work_u64(i64 cols, bool esmem = false)
 
 // LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33) --
 // separate instantiations so the cone's registers / shared memory do not cost the others occupancy
-template <int LV, class PA>
+template <int LV, class PA, bool CAUSAL = false>
 __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM_MINB) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
 {
     constexpr bool WIDE = LV == 1, CONE = LV == 2;
@@ -596,7 +605,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
 #define MPC_SOFTMAX_SKIP 0   // profiling only: bitmask of phases to skip (1 max, 2 exp, 4 recip, 8 mul)
 #endif
         if (!(MPC_SOFTMAX_SKIP & 1))
-        tile_max<WIDE, CONE>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, HA, HB, MX, cone_sm);
+        tile_max<WIDE, CONE, decltype(pr), CAUSAL>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, HA, HB, MX, cone_sm, a.causal_L);
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;
@@ -657,6 +666,13 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
             }
         }
         __syncthreads();
+        // causal: the masked exponentials are the public 0
+        auto masked = [&](i64 e) { const i64 rr = fdiv((u32)e, dC); return e - rr * C > (i64)((g0 + (u64)rr) % (u64)C); };
+        if constexpr (CAUSAL) {
+            for (i64 e = threadIdx.x; e < ne; e += blockDim.x)
+                if (masked(e)) pr.st(E, e, pr.zero());
+            __syncthreads();
+        }
         // 4. S = rowsum(e) (local): warp per row
         const SP Ec{{E.p[0], E.p[1]}};
         for (int rr = warp; rr < R; rr += NW) {
@@ -694,6 +710,11 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
                     if (e + 1 < ne) pr.st(zt, e + 1, pr.shr_(zb[v], FRAC));
                 }
             }
+        }
+        if constexpr (CAUSAL) {                           // masked outputs: the public 0
+            __syncthreads();
+            for (i64 e = threadIdx.x; e < ne; e += blockDim.x)
+                if (masked(e)) pr.st(zt, e, pr.zero());
         }
         __syncthreads();
     }

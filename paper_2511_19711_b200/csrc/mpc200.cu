@@ -1171,6 +1171,7 @@ mpc_status mpc_plain_eval(mpc_ctx* c, int op, const void* knobs, const double* x
     case MPC_PLAIN_SOFTMAX: {
         const mpc_softmax_p* p = (const mpc_softmax_p*)knobs;
         if (p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip)) return fail(c, MPC_ERR_RANGE, "softmax knobs");
+        if (p->causal) return fail(c, MPC_ERR_UNSUPPORTED, "plain_eval: causal softmax");
         a.op = 4; a.ek = mk_exp(&p->exp); a.nk = mk_nr(&p->recip); a.w = p->window; break;
     }
     case MPC_PLAIN_LAYERNORM: {
@@ -1278,7 +1279,8 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
                        const mpc_softmax_p* p)
 {
     if (!c) return MPC_ERR_INVALID;
-    if (!p || p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip))
+    if (!p || p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip) ||
+        (p->causal != 0 && p->causal != 1))
         return fail(c, MPC_ERR_RANGE, "softmax knobs");
     const int L = max_levels_h(cols);
     const u64 steps = 2ull * (u64)L + exp_steps_h(&p->exp) + exp_steps_h(&p->recip.exp) + 2ull * (u64)p->recip.iters + 1;
@@ -1317,7 +1319,8 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
                               const mpc_softmax_p* p, int64_t chunk_rows)
 {
     if (!c) return MPC_ERR_INVALID;
-    if (!p || p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip))
+    if (!p || p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip) ||
+        (p->causal != 0 && p->causal != 1))
         return fail(c, MPC_ERR_RANGE, "softmax knobs");
     const int L = max_levels_h(cols);
     const u64 steps = 2ull * (u64)L + exp_steps_h(&p->exp) + exp_steps_h(&p->recip.exp) + 2ull * (u64)p->recip.iters + 1;
@@ -1468,6 +1471,8 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         a.rows = rows; a.cols = cols; a.row_off = (u64)row_off;
         a.cone = use_cone(c, p->window) ? 1 : 0;
         a.bcast = p->bcast ? 1 : 0;
+        a.causal = p->causal ? 1 : 0;
+        a.causal_L = p->window >= 2 ? 0ull - (1ull << (p->window - 2)) : 0ull - 1ull;   // public -2^(w-2)
         const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
         // E in shared memory when the whole work tile fits 100 KB (two CTAs per SM): cols <= 192
 #ifndef MPC_SOFTMAX_ESMEM
@@ -1476,9 +1481,14 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         a.esmem = (MPC_SOFTMAX_ESMEM && softmax_work_u64(cols, true) * 8 <= 100 * 1024) ? 1 : 0;
         const i64 wk = softmax_work_u64(cols, a.esmem != 0), ek = a.esmem ? 0 : 64 * cols;
         const size_t lim = a.esmem ? 100 * 1024 : SMEM_LIMIT;
-        st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax", lim)
-           : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax", lim)
-                    : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax", lim);
+        if (a.causal)   // causal instantiations: the dense kernels carry no mask code
+            st = wide ? launch_rows(c, k_softmax<1, BothA, true>, k_softmax<1, PairA, true>, a, rows, wk, ek, "softmax", lim)
+               : a.cone ? launch_rows(c, k_softmax<2, BothA, true>, k_softmax<2, PairA, true>, a, rows, wk, ek, "softmax", lim)
+                        : launch_rows(c, k_softmax<0, BothA, true>, k_softmax<0, PairA, true>, a, rows, wk, ek, "softmax", lim);
+        else
+            st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax", lim)
+               : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax", lim)
+                        : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax", lim);
     }
     return st;
 }

@@ -132,7 +132,7 @@ def _case(r, m):
         kw = dict(window=int(r.choice([25, 33, 40])), exp_t=e["t"], exp_clamp=e["clamp"], exp_window=e["window"],
                   exp_square=e["square"], recip_iters=int(r.integers(1, 13)), recip_t=q["t"],
                   recip_clamp=q["clamp"], recip_window=q["window"], recip_square=q["square"],
-                  bcast=int(r.integers(0, 2)))
+                  bcast=int(r.integers(0, 2)), causal=int(r.integers(0, 2)))
         x = workloads.softmax_inputs(rows, cols, seed_cfg=int(r.integers(1, 9)))
         return op, [x], lambda c, s: c.softmax(s[0], rows, cols, row_off=a32, **kw), \
             lambda o, s: o.softmax(s[0], rows, cols, row_off=a32, **kw)

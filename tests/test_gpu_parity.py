@@ -603,6 +603,35 @@ def test_long_rows_max_layernorm(mpc, rows, cols):
     assert c.step == o.step
 
 
+@pytest.mark.parametrize("rows,cols,row_off,kw", [
+    (256, 128, 0, {}), (200, 40, 32, {}), (96, 128, 64, dict(bcast=1, exp_square=1)),
+    (64, 77, 96, dict(exp_clamp=1, window=40)), (70, 1, 32, {}), (33, 1024, 0, {})])
+def test_softmax_causal(mpc, rows, cols, row_off, kw):
+    """Causal softmax: bit-exact vs the oracle, masked outputs exactly 0, in
+    BOTH mode, with the carry cone, in PAIR loopback and through the host-buffer pipeline."""
+    c, o = pair_ctx(mpc, 5, step=11)
+    x = workloads.softmax_inputs(rows, cols, seed_cfg=5)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    s0 = c.step
+    ref = o.softmax(ox, rows, cols, row_off=row_off, causal=1, **kw)
+    same(c.softmax(gx, rows, cols, row_off=row_off, causal=1, **kw), ref)
+    assert c.step == o.step
+    c.set_ltz_circuit(1)
+    c.set_step(s0, force=True)
+    same(c.softmax(gx, rows, cols, row_off=row_off, causal=1, **kw), ref)
+    p = mpc.Ctx.for_cfg(workloads.keys(5), mode=mpc.binding.MODE_PAIR_LOOPBACK)
+    p.set_step(s0)
+    zp = p.softmax(gx, rows, cols, row_off=row_off, causal=1, **kw)
+    p.sync()
+    same(zp, ref)
+    hx = tuple(t.cpu().pin_memory() for t in gx)
+    hz = tuple(torch.empty_like(t).pin_memory() for t in hx)
+    c.set_step(s0, force=True)
+    c.softmax_hostio(hx, hz, rows, cols, row_off=row_off, chunk_rows=64, causal=1, **kw)
+    torch.cuda.synchronize()
+    same(hz, ref)
+
+
 def test_matmul_long_k_tensor_cores(mpc):
     """K = 5000 (K' = 15000 for party 1, inside the exact-accumulator bound) on the tensor cores."""
     c, o = pair_ctx(mpc, 3, step=2)
