@@ -242,7 +242,7 @@ mpc_status mpc_maxpool2d(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int N, int C,
 /* causal: 0 dense; 1 causal attention (reading R24c): the rows are T x T score
  * blocks with T = cols and global row g attends to columns j <= g mod T; masked entries enter the
  * max as the public -2^(window-2), their exponentials and outputs are the public 0 (both shares
- * 0).  Same units and steps as dense.  mpc_plain_eval rejects causal = 1 (MPC_ERR_UNSUPPORTED). */
+ * 0).  Same units and steps as dense.  mpc_plain_eval: row r of the call sees columns <= r mod cols. */
 typedef struct { int window; mpc_exp_p exp; mpc_nr_p recip; int bcast; int causal; } mpc_softmax_p;
 /* S14 softmax over rows (P:604 footnote).  Steps: 2*levels(cols) + exp +
  * recip + 1.  The library allocates row scratch on the context's device. */

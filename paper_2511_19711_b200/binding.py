@@ -359,7 +359,7 @@ class Ctx:
             # (square triples / broadcast triple change only the MPC rounding, not the emulated value)
             knobs = SoftmaxP(kw.get("window", 33), ExpP(kw.get("exp_t", 8), int(kw.get("exp_clamp", 0)), 33, 0),
                              NrP(kw.get("recip_iters", 10), ExpP(kw.get("recip_t", 8), int(kw.get("recip_clamp", 0)),
-                                                                  33, 0)), 0)
+                                                                  33, 0)), 0, int(kw.get("causal", 0)))
         elif op == "layernorm":
             knobs = LnP(kw.get("eps", 1e-5), kw.get("mean_mode", 0),
                         NrP(kw.get("rsqrt_iters", 3), ExpP(kw.get("rsqrt_t", 8), int(kw.get("rsqrt_clamp", 0)), 33, 0)), 0)

@@ -1171,8 +1171,8 @@ mpc_status mpc_plain_eval(mpc_ctx* c, int op, const void* knobs, const double* x
     case MPC_PLAIN_SOFTMAX: {
         const mpc_softmax_p* p = (const mpc_softmax_p*)knobs;
         if (p->window < 1 || p->window > 64 || !exp_ok(&p->exp) || !nr_ok(&p->recip)) return fail(c, MPC_ERR_RANGE, "softmax knobs");
-        if (p->causal) return fail(c, MPC_ERR_UNSUPPORTED, "plain_eval: causal softmax");
-        a.op = 4; a.ek = mk_exp(&p->exp); a.nk = mk_nr(&p->recip); a.w = p->window; break;
+        if (p->causal != 0 && p->causal != 1) return fail(c, MPC_ERR_RANGE, "softmax knobs");
+        a.op = 4; a.ek = mk_exp(&p->exp); a.nk = mk_nr(&p->recip); a.w = p->window; a.causal = p->causal; break;
     }
     case MPC_PLAIN_LAYERNORM: {
         const mpc_ln_p* p = (const mpc_ln_p*)knobs;

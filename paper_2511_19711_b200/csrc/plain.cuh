@@ -91,7 +91,7 @@ __device__ __forceinline__ double pl_dec(i64 v) { return (double)v * (1.0 / 6553
 
 // op: 0 exp, 1 recip, 2 rsqrt, 3 activation (ActK), 4 softmax rows, 5 layernorm rows
 struct PlainArgs {
-    int op; ExpK ek; NrK nk; ActK ak; int w;
+    int op; ExpK ek; NrK nk; ActK ak; int w; int causal;   // causal: softmax row r sees columns <= r mod cols
     int mean_mode; u64 e_invd, e_eps;
     const double* x; double* y; i64 rows, cols;
 };
@@ -112,13 +112,14 @@ __global__ void __launch_bounds__(256) k_plain(const __grid_constant__ PlainArgs
     for (i64 row = blockIdx.x * (i64)blockDim.x + threadIdx.x; row < a.rows; row += stride) {
         const double* xr = a.x + row * a.cols;
         double* yr = a.y + row * a.cols;
-        if (a.op == 4) {                                  // SOFTMAX
+        if (a.op == 4) {                                  // SOFTMAX (causal 2.12)
+            const i64 nv = a.causal ? row % a.cols + 1 : a.cols;    // visible columns
             i64 m = pl_enc(xr[0]);
-            for (i64 j = 1; j < a.cols; ++j) { const i64 v = pl_enc(xr[j]); if (v - m >= 0) m = v; }   // exact max
+            for (i64 j = 1; j < nv; ++j) { const i64 v = pl_enc(xr[j]); if (v - m >= 0) m = v; }   // exact max
             i64 S = 0;
-            for (i64 j = 0; j < a.cols; ++j) S += pl_exp(pl_enc(xr[j]) - m, a.ek);
+            for (i64 j = 0; j < nv; ++j) S += pl_exp(pl_enc(xr[j]) - m, a.ek);
             const i64 r = pl_recip(S, a.nk);
-            for (i64 j = 0; j < a.cols; ++j) yr[j] = pl_dec(pl_mt(pl_exp(pl_enc(xr[j]) - m, a.ek), r));
+            for (i64 j = 0; j < a.cols; ++j) yr[j] = j < nv ? pl_dec(pl_mt(pl_exp(pl_enc(xr[j]) - m, a.ek), r)) : 0.0;
         } else {                                          // LAYERNORM
             i64 s = 0;
             for (i64 j = 0; j < a.cols; ++j) s += pl_enc(xr[j]);

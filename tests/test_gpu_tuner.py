@@ -100,3 +100,20 @@ def test_tuner_picks_hummingbird_windows(m):
     assert r["quality_loss"] == 0.0
     y = c.plain_eval("relu", x1, window=21).cpu().numpy()
     assert np.array_equal(y, np.maximum(np.round(x1.cpu().numpy() * 65536) / 65536, 0))
+
+
+def test_plain_causal_softmax_vs_mpc(m):
+    """Plaintext evaluator, causal softmax (DESIGN.md 2.12): row r sees columns <= r mod cols;
+    agrees with the opened MPC causal softmax and zeroes the masked columns exactly."""
+    c = m.Ctx.for_cfg(workloads.keys(5))
+    rows, cols = 96, 48
+    xs = c.share(dev(workloads.softmax_inputs(rows, cols, seed_cfg=5)))
+    xd = c.open(xs)[1]
+    y = c.plain_eval("softmax", xd, rows=rows, cols=cols, causal=1).cpu().numpy().reshape(rows, cols)
+    ym = c.open(c.softmax(xs, rows, cols, causal=1))[1].cpu().numpy().reshape(rows, cols)
+    mask = np.arange(cols)[None, :] > (np.arange(rows) % cols)[:, None]
+    assert np.all(y[mask] == 0.0) and np.all(ym[mask] == 0.0)
+    assert np.max(np.abs(y - ym)) <= 1e-2
+    full = np.arange(rows) % cols == cols - 1
+    yd = c.plain_eval("softmax", xd, rows=rows, cols=cols).cpu().numpy().reshape(rows, cols)
+    assert np.array_equal(y[full], yd[full])
