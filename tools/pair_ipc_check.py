@@ -4,7 +4,8 @@ process's cudaIpc-mapped exchange memory -- the remote code path bench.py runs f
 With one GPU both processes share cuda:0 (the driver time-slices their contexts, so every
 exchange round costs a context switch: correctness only, tiny shapes); with two or more GPUs
 rank r uses cuda:r.  Each op's output shares are gathered on rank 0 and compared bit for bit
-with MPC_MODE_BOTH on the same seeds and step ids.
+with MPC_MODE_BOTH on the same seeds and step ids (share, mul, ReLU, GELU, softmax dense /
+cone + square triples / causal, LayerNorm, Beaver matmul).
 
   python tools/pair_ipc_check.py          (prints PAIR_IPC_OK on success, exit code 0)"""
 import os
@@ -38,6 +39,9 @@ def ops(c, x, party, n_rows, n_cols):
     out.append(c.relu(s))
     out.append(c.softmax(s, n_rows, n_cols, exp_square=1, recip_square=1))
     c.set_ltz_circuit(0)
+    out.append(c.softmax(s, n_rows, n_cols, causal=1))
+    # X = s as n_rows x n_cols, Y = the same buffer as n_cols x n_rows (tensor-core engine)
+    out.append(c.matmul(s, s, 1, n_rows, n_cols, n_rows, trunc_bits=16))
     return out
 
 
