@@ -357,6 +357,9 @@ def time_per_op(job, m, ctx, flush, args):
     z = ctx._empty(rs * cs)
     out["softmax1024"] = _op_line(job, ctx, lambda: ctx.softmax(sm, rs, cs, row_off=k * rs, out=z), rs * cs, flush,
                                   args, "cfg5: GPT-2 softmax rows of 1024 (12288 rows = 1/8 layer), t=8, NR 10")
+    out["softmax1024_causal"] = _op_line(job, ctx, lambda: ctx.softmax(sm, rs, cs, row_off=k * rs, causal=1, out=z),
+                                         rs * cs, flush, args,
+                                         "cfg5: GPT-2 causal softmax (12 x 1024 x 1024 blocks, DESIGN.md 2.12)")
     del sm, z
     # NEXT #1 / #2 variants of the same ops (same approximation; the cone's output shares are
     # bit-identical to the Kogge-Stone contract's, square triples change the shares)
