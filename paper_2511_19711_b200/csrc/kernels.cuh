@@ -397,9 +397,14 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
     i64 li = ldi;
     // level-0 entry (row rr, column col); causal softmax: columns past the row's
     // position g mod cols enter as the public constant cL (party 0 holds it)
+    u32 g0m = 0;                                   // g0 mod cols, once per tile (positions g0m + rr, rr < 32)
+    FastDiv dcol{};
+    if constexpr (CAUSAL) { g0m = (u32)(g0 % (u64)cols); dcol = make_fastdiv((u32)cols); }
     auto ldc = [&](i64 rr, i64 col) -> S {
-        if constexpr (CAUSAL)
-            if (lv == 0 && col > (i64)((g0 + (u64)rr) % (u64)cols)) return pr.addp(pr.zero(), cL);
+        if constexpr (CAUSAL) {
+            const u32 v = g0m + (u32)rr, pos = v - fdiv(v, dcol) * (u32)cols;
+            if (lv == 0 && col > (i64)pos) return pr.addp(pr.zero(), cL);
+        }
         return pr.ld(cur, rr * li + col);
     };
     while (m > 1) {
@@ -667,7 +672,11 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         }
         __syncthreads();
         // causal: the masked exponentials are the public 0
-        auto masked = [&](i64 e) { const i64 rr = fdiv((u32)e, dC); return e - rr * C > (i64)((g0 + (u64)rr) % (u64)C); };
+        const u32 g0m = CAUSAL ? (u32)(g0 % (u64)C) : 0u;
+        auto masked = [&](i64 e) {
+            const u32 rr = fdiv((u32)e, dC), v = g0m + rr;
+            return (u32)e - rr * (u32)C > v - fdiv(v, dC) * (u32)C;
+        };
         if constexpr (CAUSAL) {
             for (i64 e = threadIdx.x; e < ne; e += blockDim.x)
                 if (masked(e)) pr.st(E, e, pr.zero());
