@@ -15,7 +15,8 @@
  *  - mpc_shares carries one pointer per party.  MPC_MODE_BOTH and
  *    MPC_MODE_PAIR_LOOPBACK need sh[0] and sh[1]; MPC_MODE_PAIR needs sh[party] only.
  *  - Every call is ASYNCHRONOUS on the context's CUDA stream (cudaStream_t passed
- *    as void*); results are valid after the stream is synchronized.
+ *    as void*); results are valid after the stream is synchronized.  The calling thread's
+ *    current CUDA device must be the context's device (MPC_ERR_INVALID otherwise).
  *  - `off` / `row_off` is the global index of this shard's first element / row:
  *    the PRG is keyed by global unit, so shards reproduce the unsharded shares.
  *    Ops that contain a comparison need off (and row_off * per-row units)

@@ -503,6 +503,10 @@ static mpc_status begin(mpc_ctx* c, u64 steps_needed)
     c->st.calls++;
     if (c->step + steps_needed > (1ull << 32))
         return fail(c, MPC_ERR_RANGE, "step counter would exceed 2^32");
+    // kernels launch on the calling thread's current device: refuse to run on another one
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != c->cfg.device)
+        return fail(c, MPC_ERR_INVALID, "current CUDA device %d is not the context's device %d", cur, c->cfg.device);
     return MPC_OK;
 }
 static void finish(mpc_ctx* c, u64 steps)
@@ -648,6 +652,9 @@ mpc_status mpc_pair_connect(mpc_ctx* c, const void* peer_handle)
     if (!c || !peer_handle || c->cfg.mode != MPC_MODE_PAIR) return MPC_ERR_INVALID;
     cudaIpcMemHandle_t h;
     memcpy(&h, peer_handle, sizeof h);
+    int cur = -1;
+    if (cudaGetDevice(&cur) != cudaSuccess || cur != c->cfg.device)
+        return fail(c, MPC_ERR_INVALID, "pair_connect: current CUDA device %d is not the context's device %d", cur, c->cfg.device);
     void* p = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
     if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
