@@ -50,6 +50,8 @@ def run(mode, circuit):
     y = sh(workloads.recip_inputs(45))
     c.mul_bcast(s, y, 45, 77, off=1, row_off=3, trunc_bits=16)
     c.softmax(s, 45, 77, bcast=1)
+    c.softmax(s, 45, 77, causal=1)                       # causal instantiation
+    c.softmax(s, 45, 77, causal=1, bcast=1, exp_clamp=1)
     c.layernorm(ln, 40, 96, bcast=1)
     c.gelu(x, form="poly_abs", degree=4, basis=1)
     c.sigmoid(x, form="poly_x", degree=3, B=4.0, coeffs=[0.5, 0.2, 0.0, -0.01], basis=1)
@@ -63,6 +65,7 @@ def run(mode, circuit):
     if mode == m.binding.MODE_BOTH:
         xd = c.open(s)[1]
         c.plain_eval("softmax", xd, rows=45, cols=77)
+        c.plain_eval("softmax", xd, rows=45, cols=77, causal=1)
         c.plain_eval("gelu", c.open(x)[1], form="poly_abs", degree=4)
         c.plain_eval("layernorm", c.open(ln)[1], rows=40, cols=96)
     hx = tuple(t.cpu().pin_memory() for t in s)
