@@ -37,7 +37,10 @@ struct BothP {
     const Keys* Kp;          // points into the kernel's parameter space (__grid_constant__)
     using S = Sh;
     static constexpr bool kPair = false;
-    static constexpr int kV = 1;   // unit pairs per lane per pass (registers hold both parties)
+#ifndef MPC_BOTH_KV
+#define MPC_BOTH_KV 1
+#endif
+    static constexpr int kV = MPC_BOTH_KV;   // unit pairs per lane per pass (registers hold both parties)
     __device__ __forceinline__ int party() const { return -1; }
     __device__ __forceinline__ S zero() const { return {0, 0}; }
     __device__ __forceinline__ S ld(SP a, i64 i) const { return {a.p[0][i], a.p[1][i]}; }
