@@ -175,8 +175,9 @@ mpc_status mpc_mul_bcast(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z,
  * global index of the first product); 1 step, 1 round, 8 (MK + KN) B per product per party.
  * Caller-owned device buffers.  Library scratch per product: the operand planes, 32 (MK + KN) B
  * (SIMT engine and PAIR modes), plus for the tensor-core engine the limb tiles of both parties,
- * 40 (M' Kpad + Kpad N') B (5 terms x 8 limb bytes) with Kpad = 32 ceil(K/32) and M', N' rounded up to the tile (in
- * MPC_MODE_BOTH the masking is fused into the limb tiling and only the limb tiles are kept). */
+ * 40 (M' Kpad + Kpad N') B (5 terms x 8 limb bytes; Kpad = 32 ceil(K/32), M' and N' rounded
+ * up to the tile).  In MPC_MODE_BOTH the masking is fused into the limb tiling and only the
+ * limb tiles are kept. */
 mpc_status mpc_matmul(mpc_ctx* ctx, mpc_shares x, mpc_shares y, mpc_shares z, int64_t batch,
                       int64_t M, int64_t K, int64_t N, int64_t batch_off, int trunc_bits);
 /* S5 local truncation: z_i = (int64)x_i >> bits, bits in [0,63].
