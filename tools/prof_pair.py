@@ -1,4 +1,4 @@
-"""One PAIR-loopback GELU (cfg3 size) launch for ncu."""
+"""One PAIR-loopback GELU launch over 2^20 elements (|x|-form deg 4, cfg3 distribution) for ncu."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
