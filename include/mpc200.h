@@ -153,6 +153,13 @@ mpc_status mpc_share(mpc_ctx* ctx, const void* x, int x_is_f64, int owner, mpc_s
  * parties exchange their shares (1 round, 8 B/element) and both receive the result. */
 mpc_status mpc_open(mpc_ctx* ctx, mpc_shares in, int64_t n, uint64_t* ring_out,
                     double* f64_out, int scale_bits);
+/* S2 open to one party (SURVEY 8(b) reveal_to): as mpc_open with reveal_to = -1 (both);
+ * reveal_to = p in {0, 1}: only party p learns rec -- in the PAIR modes p sends zeros in place
+ * of its share (the exchange keeps its lockstep, the peer learns nothing) and only p writes
+ * ring_out / f64_out (the other party may pass NULL).  In MPC_MODE_BOTH the caller holds both
+ * parties and the outputs are written as by mpc_open.  MPC_ERR_INVALID for other reveal_to. */
+mpc_status mpc_open_to(mpc_ctx* ctx, mpc_shares in, int64_t n, int reveal_to, uint64_t* ring_out,
+                       double* f64_out, int scale_bits);
 
 /* ---- S4 / S5 ---------------------------------------------------------------- */
 /* S4 Beaver multiply: z = x*y mod 2^64, then per-share

@@ -97,6 +97,7 @@ _SIGS = {
     "mpc_prg_fill": [VP, u64, u64, ctypes.c_uint32, ctypes.c_uint32, VP, i64, INT],
     "mpc_share": [VP, VP, INT, INT, Shares, i64, i64],
     "mpc_open": [VP, Shares, i64, VP, VP, INT],
+    "mpc_open_to": [VP, Shares, i64, INT, VP, VP, INT],
     "mpc_mul": [VP, Shares, Shares, Shares, i64, i64, INT],
     "mpc_square": [VP, Shares, Shares, i64, i64, INT],
     "mpc_mul_bcast": [VP, Shares, Shares, Shares, i64, i64, i64, i64, INT],
@@ -302,6 +303,16 @@ class Ctx:
         f = torch.empty(n, dtype=torch.float64, device=self.device) if want_f64 else None
         self._stream()
         self._chk(_L.mpc_open(self._h, _sh(s), n, _ptr(ring), _ptr(f), scale_bits), "mpc_open")
+        return ring, f
+
+    def open_to(self, s, reveal_to: int, scale_bits: int = 16, want_ring=True, want_f64=True):
+        """Open to one party (reveal_to 0 | 1; -1 = both): in the PAIR modes only that party learns
+        and writes the result; the other party's outputs are left untouched."""
+        n = (s[0] if s[0] is not None else s[1]).numel()
+        ring = torch.zeros(n, dtype=torch.uint64, device=self.device) if want_ring else None
+        f = torch.zeros(n, dtype=torch.float64, device=self.device) if want_f64 else None
+        self._stream()
+        self._chk(_L.mpc_open_to(self._h, _sh(s), n, int(reveal_to), _ptr(ring), _ptr(f), scale_bits), "mpc_open_to")
         return ring, f
 
     # ---- S4 / S5 ----

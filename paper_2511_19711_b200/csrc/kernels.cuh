@@ -363,14 +363,24 @@ struct ActBody {
 };
 
 // S2 in PAIR modes: exchange the shares, both parties learn rec (reveal_to both)
+// reveal >= 0 (mpc_open_to): only that party learns rec -- it sends zeros in place of its share
+// (the exchange keeps its lockstep; the peer receives nothing about x) and adds its own share.
 struct OpenBody {
     SP x; u64* ring; double* f; i64 n; double inv; int writer;   // writer: party that stores (-1: own)
+    int reveal;                                                  // -1: both parties learn rec
     template <class P>
     __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
         (void)u; (void)q;
         typename P::S mine = pr.zero();
         if (valid) mine = pr.ld(x, i);
-        const u64 v = pr.open(mine);
+        u64 v;
+        if constexpr (std::is_same<typename P::S, u64>::value) {     // PAIR: one party's share per thread
+            const bool recv_only = reveal >= 0 && pr.party() == reveal;
+            v = pr.open(recv_only ? pr.zero() : mine);
+            if (recv_only) v += mine;
+        } else {
+            v = pr.open(mine);
+        }
         if (valid && (writer < 0 || pr.party() == writer)) {
             if (ring) ring[i] = v;
             if (f) f[i] = (double)(i64)v * inv;

@@ -793,14 +793,22 @@ mpc_status mpc_share(mpc_ctx* c, const void* x, int x_is_f64, int owner, mpc_sha
 
 mpc_status mpc_open(mpc_ctx* c, mpc_shares in, int64_t n, uint64_t* ring_out, double* f64_out, int scale_bits)
 {
+    return mpc_open_to(c, in, n, -1, ring_out, f64_out, scale_bits);
+}
+
+mpc_status mpc_open_to(mpc_ctx* c, mpc_shares in, int64_t n, int reveal_to, uint64_t* ring_out, double* f64_out,
+                       int scale_bits)
+{
     mpc_status st = begin(c, 0);
     if (st) return st;
     if (n < 0 || scale_bits < 0 || scale_bits > 62) return fail(c, MPC_ERR_INVALID, "bad n/scale");
+    if (reveal_to < -1 || reveal_to > 1) return fail(c, MPC_ERR_INVALID, "reveal_to must be -1, 0 or 1");
     if (bad_sh(c, in)) return fail(c, MPC_ERR_INVALID, "open: null pointer");
     if (n > 0) {
         if (is_pair(c)) {
+            const int writer = reveal_to >= 0 ? reveal_to : (is_loop(c) ? 0 : -1);
             st = launch_groups(c, n, 0, OpenBody{spv(c, in), ring_out, f64_out, n, 1.0 / (double)(1ull << scale_bits),
-                                                 is_loop(c) ? 0 : -1}, "open");
+                                                 writer, reveal_to}, "open");
         } else {
             rec_begin(c, "open", (u64)n);
             k_open<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(in.sh[0], in.sh[1], n, ring_out, f64_out, scale_bits);

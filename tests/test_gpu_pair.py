@@ -192,3 +192,22 @@ def test_cone_softmax_loopback(m):
     p.set_step(b.step)
     assert eq(b.softmax(x, 96, 128, exp_square=1, recip_square=1), p.softmax(x, 96, 128, exp_square=1, recip_square=1))
     p.sync()
+
+
+@pytest.mark.parametrize("reveal_to", [0, 1])
+def test_open_to_one_party_loopback(m, reveal_to):
+    """mpc_open_to (SURVEY 8(b) reveal_to): only the chosen party learns and writes rec; the
+    other party sends its share, the chosen one sends zeros, and the exchange stays in lockstep
+    (the next op's shares are still bit-identical to BOTH)."""
+    b, p = ctxs(m, step=21)
+    x = torch.from_numpy(workloads.act_inputs(5000 + 7)).cuda()
+    s = b.share(x)
+    rb, fb = b.open(s)
+    rp, fp = p.open_to(s, reveal_to)
+    p.sync()
+    assert torch.equal(rb, rp) and torch.equal(fb, fp)
+    p.set_step(b.step)
+    assert eq(b.mul(s, s, trunc_bits=16), p.mul(s, s, trunc_bits=16))
+    p.sync()
+    with pytest.raises(m.MPCError):
+        p.open_to(s, 2)

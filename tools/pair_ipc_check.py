@@ -5,7 +5,7 @@ With one GPU both processes share cuda:0 (the driver time-slices their contexts,
 exchange round costs a context switch: correctness only, tiny shapes); with two or more GPUs
 rank r uses cuda:r.  Each op's output shares are gathered on rank 0 and compared bit for bit
 with MPC_MODE_BOTH on the same seeds and step ids (share, mul, ReLU, GELU, softmax dense /
-cone + square triples / causal, LayerNorm, Beaver matmul).
+cone + square triples / causal, LayerNorm, Beaver matmul), and an open to party 1 only.
 
   python tools/pair_ipc_check.py          (prints PAIR_IPC_OK on success, exit code 0)"""
 import os
@@ -59,19 +59,25 @@ def worker(rank, world, port, q):
     c = m.Ctx.for_cfg(keys, device=dev, mode=m.binding.MODE_PAIR, party=rank)
     pair.connect(c)
     res = ops(c, x if rank == 0 else None, rank, rows, cols)
+    ring1, _ = c.open_to(res[0], 1)                   # only party 1 learns rec(x)
     c.sync()
-    mine = [r[rank].cpu().numpy() for r in res]
+    mine = [r[rank].cpu().numpy() for r in res] + [ring1.cpu().numpy()]
     gathered = [None, None]
     dist.all_gather_object(gathered, mine)
     if rank == 0:
         b = m.Ctx.for_cfg(keys, device=dev)
         ref = ops(b, x, 0, rows, cols)
+        ring_ref, _ = b.open(ref[0])
         torch.cuda.synchronize()
         bad = []
         for k, r in enumerate(ref):
             for p in (0, 1):
                 if not np.array_equal(gathered[p][k], r[p].cpu().numpy()):
                     bad.append((k, p))
+        if not np.array_equal(gathered[1][-1], ring_ref.cpu().numpy()):
+            bad.append(("open_to", 1))
+        if np.any(gathered[0][-1]):                   # party 0 received nothing, wrote nothing
+            bad.append(("open_to", 0))
         q.put(bad)
     dist.barrier()
     dist.destroy_process_group()
