@@ -109,9 +109,14 @@ uint64_t mpc_last_call_philox(const mpc_ctx* ctx);
 #define MPC_PAIR_HANDLE_BYTES 64
 mpc_status mpc_pair_export(mpc_ctx* ctx, void* handle_out /* MPC_PAIR_HANDLE_BYTES */);
 mpc_status mpc_pair_connect(mpc_ctx* ctx, const void* peer_handle);
-/* Synchronize the context stream; MPC_ERR_TIMEOUT if a PAIR exchange timed out,
- * MPC_ERR_CUDA on an asynchronous CUDA error. */
+/* Synchronize the context stream; MPC_ERR_PROTOCOL if the debug header check found the parties
+ * issuing different calls, MPC_ERR_TIMEOUT if a PAIR exchange timed out, MPC_ERR_CUDA on an
+ * asynchronous CUDA error. */
 mpc_status mpc_ctx_sync(mpc_ctx* ctx);
+/* Debug mode (PAIR modes; default off): before every op the parties exchange an op header (a hash
+ * of the entry point, the step id and the op's step count) in one extra round; a mismatch marks
+ * the context and mpc_ctx_sync returns MPC_ERR_PROTOCOL.  No effect in MPC_MODE_BOTH. */
+mpc_status mpc_ctx_set_debug(mpc_ctx* ctx, int on);
 
 /* LTZ carry circuit: 0 = full Kogge-Stone (the S7 contract, default),
  * 1 = carry cone (only the carry into bit w-1: 94 AND gates at w = 33 instead of 290, same

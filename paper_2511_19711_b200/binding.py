@@ -98,6 +98,7 @@ _SIGS = {
     "mpc_share": [VP, VP, INT, INT, Shares, i64, i64],
     "mpc_open": [VP, Shares, i64, VP, VP, INT],
     "mpc_open_to": [VP, Shares, i64, INT, VP, VP, INT],
+    "mpc_ctx_set_debug": [VP, INT],
     "mpc_mul": [VP, Shares, Shares, Shares, i64, i64, INT],
     "mpc_square": [VP, Shares, Shares, i64, i64, INT],
     "mpc_mul_bcast": [VP, Shares, Shares, Shares, i64, i64, i64, i64, INT],
@@ -226,6 +227,10 @@ class Ctx:
     def pair_connect(self, peer_handle: bytes):
         buf = ctypes.create_string_buffer(bytes(peer_handle), PAIR_HANDLE_BYTES)
         self._chk(_L.mpc_pair_connect(self._h, ctypes.cast(buf, VP)), "mpc_pair_connect")
+
+    def set_debug(self, on: bool = True):
+        """PAIR modes: exchange and compare an op header before every op (MPC_ERR_PROTOCOL at sync)."""
+        self._chk(_L.mpc_ctx_set_debug(self._h, int(on)), "mpc_ctx_set_debug")
 
     def set_ltz_circuit(self, circuit: int):
         """0 = Kogge-Stone (default, the S7 contract), 1 = carry cone (NEXT #1): same output shares."""

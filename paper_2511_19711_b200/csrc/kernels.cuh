@@ -388,6 +388,21 @@ struct OpenBody {
     }
 };
 
+// Debug header exchange (mpc_ctx_set_debug, PAIR modes): each party opens its op header; a
+// mismatch (rec != 2 hdr) marks the context's error word with 2 (MPC_ERR_PROTOCOL at sync).
+struct HdrBody {
+    u64 hdr;
+    SP x;                 // unused (no inputs); keeps the group driver's prefetch interface
+    template <class P>
+    __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
+        (void)u; (void)q; (void)i; (void)lane; (void)valid;
+        if constexpr (std::is_same<typename P::S, u64>::value) {
+            const u64 v = pr.open(hdr);
+            if (v != 2ull * hdr) atomicCAS(pr.err, 0, 2);
+        }
+    }
+};
+
 // ------------------------------------------------------------------ row tiles ----
 // One CTA owns a tile of 32 consecutive rows (32-aligned global row index); persistent loop.
 

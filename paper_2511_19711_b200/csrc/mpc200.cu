@@ -59,6 +59,7 @@ struct mpc_ctx {
     XAlloc xa[2];           // own (and, loopback, the other party's) exchange memory
     void* peer_base;        // MPC_MODE_PAIR: the peer's exchange memory (cudaIpc-mapped)
     int connected;
+    int debug_hdr;          // PAIR: exchange and compare an op header before every op (MPC_ERR_PROTOCOL)
     int circuit;            // LTZ carry circuit: 0 Kogge-Stone, 1 carry cone (2.7)
     int mm_engine;          // mpc_matmul ring GEMM: 0 auto, 1 SIMT, 2 tensor cores
     struct HostIO* hio;     // pipelined host-buffer execution (mpc_softmax_hostio), lazily created
@@ -496,7 +497,17 @@ static SO sov(const mpc_ctx* c, mpc_shares s)
 }
 
 // common prologue of a compute call: validates the step budget, resets the per-call counter
-static mpc_status begin(mpc_ctx* c, u64 steps_needed)
+// debug header (mpc_ctx_set_debug): FNV-1a of the entry point's name, mixed with the step id and
+// the step count the call needs; exchanged and compared by one PAIR launch before the op
+static mpc_status hdr_check(mpc_ctx* c, const char* op, u64 steps_needed)
+{
+    u64 h = 1469598103934665603ull;
+    for (const char* q = op; *q; ++q) { h ^= (u8)*q; h *= 1099511628211ull; }
+    h ^= c->step * 0x9E3779B97F4A7C15ull; h *= 1099511628211ull;
+    h ^= steps_needed; h *= 1099511628211ull;
+    return launch_groups(c, 32, 0, HdrBody{h, SP{{nullptr, nullptr}}}, "op_header");
+}
+static mpc_status begin_op(mpc_ctx* c, u64 steps_needed, const char* op)
 {
     if (!c) return MPC_ERR_INVALID;
     c->last_philox = 0;
@@ -507,8 +518,10 @@ static mpc_status begin(mpc_ctx* c, u64 steps_needed)
     int cur = -1;
     if (cudaGetDevice(&cur) != cudaSuccess || cur != c->cfg.device)
         return fail(c, MPC_ERR_INVALID, "current CUDA device %d is not the context's device %d", cur, c->cfg.device);
+    if (c->debug_hdr && is_pair(c)) return hdr_check(c, op, steps_needed);
     return MPC_OK;
 }
+#define begin(c, steps) begin_op((c), (steps), __func__)
 static void finish(mpc_ctx* c, u64 steps)
 {
     rec_close(c);
@@ -672,8 +685,16 @@ mpc_status mpc_ctx_sync(mpc_ctx* c)
         if (!c->xa[i].base) continue;
         int err = 0;
         cudaMemcpy(&err, (char*)c->xa[i].base + c->xa[i].err_off, sizeof err, cudaMemcpyDeviceToHost);
+        if (err == 2) return fail(c, MPC_ERR_PROTOCOL, "PAIR op headers differ (the parties issued different calls)");
         if (err) return fail(c, MPC_ERR_TIMEOUT, "PAIR exchange timed out (peer not running the same op?)");
     }
+    return MPC_OK;
+}
+
+mpc_status mpc_ctx_set_debug(mpc_ctx* c, int on)
+{
+    if (!c) return MPC_ERR_INVALID;
+    c->debug_hdr = on ? 1 : 0;
     return MPC_OK;
 }
 

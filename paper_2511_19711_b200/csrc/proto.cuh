@@ -228,7 +228,7 @@ struct PairP {
             unsigned spins = 0;
             do {                                 // (a __nanosleep backoff here measured 2x slower)
                 asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
-                if ((++spins & 1023) == 0 && globaltimer() - t0 > kTimeoutNs) { atomicExch(err, 1); dead = 1; break; }
+                if ((++spins & 1023) == 0 && globaltimer() - t0 > kTimeoutNs) { atomicCAS(err, 0, 1); dead = 1; break; }
             } while ((lo >> 32) != want || (hi >> 32) != want);
         }
         return (lo & 0xffffffffull) | (hi << 32);

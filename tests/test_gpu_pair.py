@@ -211,3 +211,14 @@ def test_open_to_one_party_loopback(m, reveal_to):
     p.sync()
     with pytest.raises(m.MPCError):
         p.open_to(s, 2)
+
+
+def test_debug_header_no_false_positive_loopback(m):
+    """Debug header check in loopback: the same calls on both parties pass and change no shares."""
+    b, p = ctxs(m, step=5)
+    p.set_debug(True)
+    x = b.share(torch.from_numpy(workloads.softmax_inputs(64, 128)).cuda())
+    p.set_step(b.step)
+    assert eq(b.softmax(x, 64, 128), p.softmax(x, 64, 128))
+    assert eq(b.relu(x), p.relu(x))
+    p.sync()

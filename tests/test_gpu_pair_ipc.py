@@ -17,3 +17,11 @@ def test_pair_two_processes_bit_identical_to_both():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_ipc_check.py")],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0 and "PAIR_IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_pair_debug_header_detects_mismatched_calls():
+    """mpc_ctx_set_debug: party 0 issues mul while party 1 issues square; both contexts report
+    MPC_ERR_PROTOCOL at sync."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_ipc_check.py"), "--mismatch"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0 and "PAIR_IPC_PROTOCOL_DETECTED" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

@@ -7,7 +7,9 @@ rank r uses cuda:r.  Each op's output shares are gathered on rank 0 and compared
 with MPC_MODE_BOTH on the same seeds and step ids (share, mul, ReLU, GELU, softmax dense /
 cone + square triples / causal, LayerNorm, Beaver matmul), and an open to party 1 only.
 
-  python tools/pair_ipc_check.py          (prints PAIR_IPC_OK on success, exit code 0)"""
+  python tools/pair_ipc_check.py             (prints PAIR_IPC_OK on success, exit code 0)
+  python tools/pair_ipc_check.py --mismatch  (debug header check: the parties issue different ops;
+                                              prints PAIR_IPC_PROTOCOL_DETECTED)"""
 import os
 import sys
 
@@ -45,7 +47,7 @@ def ops(c, x, party, n_rows, n_cols):
     return out
 
 
-def worker(rank, world, port, q):
+def worker(rank, world, port, q, mismatch=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2511_19711_b200 as m
@@ -58,6 +60,28 @@ def worker(rank, world, port, q):
     keys = workloads.keys(2)
     c = m.Ctx.for_cfg(keys, device=dev, mode=m.binding.MODE_PAIR, party=rank)
     pair.connect(c)
+    if mismatch:
+        # debug header check: party 0 issues mul, party 1 square (same step count and rounds, so
+        # the exchange itself completes) -- both must report MPC_ERR_PROTOCOL at sync
+        c.set_debug(True)
+        s = c.share(x if rank == 0 else None, owner=0, n=rows * cols)
+        c.sync()
+        if rank == 0:
+            c.mul(s, s, trunc_bits=16)
+        else:
+            c.square(s, trunc_bits=16)
+        try:
+            c.sync()
+            got = "OK"
+        except m.MPCError as e:
+            got = str(e)
+        res = [None, None]
+        dist.all_gather_object(res, got)
+        if rank == 0:
+            q.put([] if all("PROTOCOL" in r for r in res) else [("mismatch", res)])
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     res = ops(c, x if rank == 0 else None, rank, rows, cols)
     ring1, _ = c.open_to(res[0], 1)                   # only party 1 learns rec(x)
     c.sync()
@@ -87,12 +111,13 @@ def main():
     port = 29600 + (os.getpid() % 1000)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    mp.start_processes(worker, args=(2, port, q), nprocs=2, join=True, start_method="spawn")
+    mismatch = "--mismatch" in sys.argv
+    mp.start_processes(worker, args=(2, port, q, mismatch), nprocs=2, join=True, start_method="spawn")
     bad = q.get(timeout=5)
     if bad:
         print("PAIR_IPC_MISMATCH", bad)
         sys.exit(1)
-    print(f"PAIR_IPC_OK ({torch.cuda.device_count()} GPU(s))")
+    print(("PAIR_IPC_PROTOCOL_DETECTED" if mismatch else "PAIR_IPC_OK") + f" ({torch.cuda.device_count()} GPU(s))")
 
 
 if __name__ == "__main__":
