@@ -296,7 +296,7 @@ def run_mpc200(args):
                                      "bytes_per_party": st["bytes_per_party"] // args.steps,
                                      "rounds": st["rounds"] // args.steps},
                "clocks": clk, "per_op": per_op}
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and job.ws == 1:      # rank 0 at N = 1 only
             res["cpu_baseline"] = cpu_baseline(args)
             res["cpu_baseline_all_cores"] = cpu_baseline_all_cores(args)
     if job.ws > 1:
