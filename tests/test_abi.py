@@ -54,3 +54,10 @@ def test_ctx_create_rejects_bad_config_without_gpu():
     assert b._L.mpc_ctx_create(ctypes.byref(cfg), ctypes.byref(h)) == 2      # MPC_ERR_RANGE
     cfg = b.Config(7, 0, 16, 0, 1, 2, 3, None, None)          # unknown mode
     assert b._L.mpc_ctx_create(ctypes.byref(cfg), ctypes.byref(h)) == 1      # MPC_ERR_INVALID
+
+
+def test_header_is_plain_c99():
+    """The boundary header compiles as strict C99 (no C++ or torch types leak into it)."""
+    r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-fsyntax-only", "-x", "c", HDR],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
