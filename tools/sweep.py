@@ -322,6 +322,8 @@ def sec_cfg5(S):
                   "lan_cost_most_accurate_ms": tuned["cost_most_accurate"], "steps": tuned["steps"]}
     out["gpt2_12layers_autotuned"] = r
     out["softmax1024_t8"] = S.line(c, lambda: c.softmax(sm, rs, cs, out=zs), rs * cs, "cfg5 softmax layer, t=8 NR 10")
+    out["softmax1024_t8_causal"] = S.line(c, lambda: c.softmax(sm, rs, cs, causal=1, out=zs), rs * cs,
+                                          "cfg5 causal softmax layer (DESIGN.md 2.12), t=8 NR 10")
     out["gelu_poly_abs4"] = S.line(c, lambda: c.gelu(g, form="poly_abs", degree=4, out=zg), ng,
                                    "cfg5 GELU layer |x|-form deg 4")
     out["layernorm_r3"] = S.line(c, lambda: c.layernorm(ln, rl, d, out=zl), rl * d, "cfg5 LN 2048 x 768, rsqrt 3 it")
