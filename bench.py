@@ -32,12 +32,29 @@ import workloads  # noqa: E402
 METRIC = "secret-shared elements/s per op (Softmax, GELU, ReLU) at 1/2/4/8 B200; % HBM roofline"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 SM_COUNT, SMSP, LANES = 148, 4, 32
-# Philox4x32-10 = 10 rounds x (2 IMAD.WIDE.U32 + 2 LOP3).  B300_MICROARCH "Pipe rates": IMAD on
-# the fma pipe, LOP3 on the alu pipe, each 2 cycles per warp instruction per SMSP -> 40 pipe
-# cycles per 32 blocks per SMSP.  Peak = 148 * 4 * 32 / 40 * f_max.
-CYCLES_PER_WARP_BLOCK = 40.0
+# ALU roofline.  A Philox4x32-10 block is 10 rounds x (2 IMAD.WIDE.U32 + 2 LOP3).
+# tools/microbench.cu (profiles/r02_microbench.json) measures IMAD.WIDE.U32 in isolation at one warp
+# instruction per 4.04 cycles per SMSP (fmaheavy, quarter rate) and LOP3 at one per 2.02 on the alu
+# pipe, the two overlapping: a block costs 20 x 4.04 = 80.7 fmaheavy cycles per warp, so
+# peak = 148 SM x 4 SMSP x 32 lanes / 80.7 x f_max = 461 G blocks/s at 1965 MHz.
+MICROBENCH_PATH = os.path.join(ROOT, "profiles", "r02_microbench.json")
+IMADW_CYCLES_FALLBACK = 4.037
 NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction
-PHILOX_MICROBENCH_GBS = 530.0  # tools/microbench.cu, ILP 2 at 2048 threads/SM (profiles/)
+LL_WIRE_FACTOR = 2.0         # PAIR exchange: each 8-byte payload word travels as two {half | tag} words
+
+
+def imadw_cycles():
+    try:
+        return float(json.load(open(MICROBENCH_PATH))["derived"]["imad_wide_u32_cycles_per_warp_instr"])
+    except Exception:
+        return IMADW_CYCLES_FALLBACK
+
+
+def philox_only_measured():
+    try:
+        return float(json.load(open(MICROBENCH_PATH))["derived"]["philox_only_best_measured_gblocks_s"])
+    except Exception:
+        return None
 
 
 def load_peaks():
@@ -48,7 +65,7 @@ def load_peaks():
 
 
 def philox_peak_gblocks(sm_mhz):
-    return SM_COUNT * SMSP * LANES / CYCLES_PER_WARP_BLOCK * sm_mhz * 1e6 / 1e9
+    return SM_COUNT * SMSP * LANES / (20.0 * imadw_cycles()) * sm_mhz * 1e6 / 1e9
 
 
 class Clocks:
@@ -210,15 +227,18 @@ def roofline(job, ctx_mode, kt, st, steps, ms_step, n):
          "frac": round(ach / peak, 4), "traffic": traffic, "traffic_source": tsrc,
          "traffic_algorithmic_bytes": 32 * n, "avg_launch_ms": round(dms, 4),
          "share_of_step": round(agg[dom][0] / tot, 3),
-         "peak_basis": f"derived: 148 SM x 4 SMSP x 32 lanes / 40 pipe-cycles per warp-block x {fmax:.0f} MHz "
-                       f"({'measured' if not peaks.get('_fallback') else 'fallback'} sm_max); "
-                       f"measured Philox-only ceiling {PHILOX_MICROBENCH_GBS} Gphilox/s (tools/microbench.cu)",
-         "frac_of_measured_ceiling": round(ach / PHILOX_MICROBENCH_GBS, 4),
+         "peak_basis": f"148 SM x 4 SMSP x 32 lanes / (20 IMAD.WIDE.U32 per block x {imadw_cycles():.3f} cycles, "
+                       f"measured in isolation: profiles/r02_microbench.json) x {fmax:.0f} MHz "
+                       f"({'measured' if not peaks.get('_fallback') else 'fallback'} sm_max, MEASURED_PEAKS.json)",
+         "philox_only_measured": philox_only_measured(),
          "hbm_frac": round(32 * n / (ms_step / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), 5)}
     if ctx_mode != job.m.binding.MODE_BOTH:
         bps = st["bytes_per_party"] / steps
-        r["nvlink"] = {"bytes_per_party_per_step": int(bps), "achieved_gbs": round(bps / (ms_step / 1e3) / 1e9, 2),
-                       "peak_gbs": NVLINK_PEER_GBS, "frac": round(bps / (ms_step / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
+        wps = bps * LL_WIRE_FACTOR
+        r["nvlink"] = {"payload_bytes_per_party_per_step": int(bps), "wire_bytes_per_party_per_step": int(wps),
+                       "wire_gbs": round(wps / (ms_step / 1e3) / 1e9, 2), "peak_gbs": NVLINK_PEER_GBS,
+                       "wire_frac": round(wps / (ms_step / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
+                       "payload_roofline_frac": round(bps / NVLINK_PEER_GBS / 1e9 / (ms_step / 1e3), 4),
                        "rounds_per_step": st["rounds"] // steps}
         r["note"] = ("PAIR: philox counts both parties + dealer (the BOTH-mode work) per pair; "
                      "each party's GPU executes its part plus party 1's dealer corrections")
@@ -244,12 +264,15 @@ def run_mpc200(args):
     def step():
         ctx.softmax(xs, rows, cols, row_off=row_off, out=out, **sm_kw)
 
+    s_before = ctx.step
     for _ in range(args.warmup):
         step()
+    steps_per_call = (ctx.step - s_before) // max(1, args.warmup)
     torch.cuda.synchronize()
     ms_step, kt, st, clk = timed(job, ctx, step, args.steps, flush, Clocks(job.local))
     value = job.npairs * n / (ms_step / 1e3)
     roof = roofline(job, ctx.mode, kt, st, args.steps, ms_step, n)
+    parity = check_timed_output(job, ctx.step - steps_per_call, xs, out, rows, cols, row_off, sm_kw)
 
     # ---- e2e: host buffers through the public API (H2D inputs, D2H outputs inside the region) ----
     # mpc_softmax_hostio: chunks of 3072 rows, H2D / compute / D2H of neighbouring chunks overlapped
@@ -286,6 +309,7 @@ def run_mpc200(args):
                           "recip": "NR 10 iters (exp t=8)", "window": 33, "mode": mode,
                           "l2": "flushed between steps (512 MB write)", "parallelism": f"pairs{job.npairs}"},
                "roofline": roof,
+               "parity_ok": parity.get("ok"), "parity": parity,
                "e2e": {"value": job.npairs * n / (e_ms / 1e3), "unit": "elements/s",
                        "h2d_bytes_per_step": 16 * n * job.npairs, "d2h_bytes_per_step": 16 * n * job.npairs,
                        "ms_per_step": round(e_ms, 4),
@@ -305,6 +329,45 @@ def run_mpc200(args):
     return res
 
 
+def check_timed_output(job, step_id, xs, out, rows, cols, row_off, sm_kw, tiles=8):
+    """Bit-exact check of the TIMED output: `tiles` 32-row tiles spread over the last timed step's
+    output (every share of both parties) against oracle/ run at that step's id on the same input
+    shares (the PRG is keyed by global row, so a 32-row slice with its row_off is exactly that part
+    of the op).  PAIR: pair 0's two ranks contribute their party's shares."""
+    r0s = sorted({int(v) // 32 * 32 for v in np.linspace(0, rows - 32, tiles)})
+    mine = {}
+    for r0 in r0s:
+        sl = slice(r0 * cols, (r0 + 32) * cols)
+        mine[r0] = [(None if xs[p] is None else xs[p][sl].cpu().numpy(),
+                     None if out[p] is None else out[p][sl].cpu().numpy()) for p in (0, 1)]
+    if job.ws > 1:
+        allp = [None] * job.ws
+        job.dist.all_gather_object(allp, (job.pair_idx, job.party, mine))
+        if job.rank != 0:
+            return {"ok": None, "checked_on": "rank 0"}
+        got = {}
+        for pidx, party, d in allp:
+            if pidx != 0:
+                continue
+            for r0, v in d.items():
+                got.setdefault(r0, [None, None])[party] = v[party]
+        mine = {r0: [v[0], v[1]] for r0, v in got.items()}
+    try:
+        from oracle import Oracle                 # test infrastructure: the checker, not the product path
+        bad = []
+        for r0 in r0s:
+            (x0, z0), (x1, z1) = mine[r0]
+            o = Oracle.for_cfg(workloads.keys(2), step_id)
+            r = o.softmax((x0, x1), 32, cols, row_off=row_off + r0, **sm_kw)
+            if not (np.array_equal(r[0], z0) and np.array_equal(r[1], z1)):
+                bad.append(r0)
+        return {"ok": not bad, "rows_checked": 32 * len(r0s), "tile_rows": r0s, "mismatching_tiles": bad,
+                "step_id": int(step_id), "how": "every share of both parties vs oracle/ (plain C) at the last "
+                                                "timed step's id, same input shares"}
+    except Exception as e:                       # never fail the bench line on the checker itself
+        return {"ok": None, "error": f"{type(e).__name__}: {e}"[:200]}
+
+
 def _op_line(job, ctx, fn, n, flush, args, config):
     for _ in range(max(1, args.warmup)):
         fn()
@@ -317,8 +380,18 @@ def _op_line(job, ctx, fn, n, flush, args, config):
             "gphilox_s": round(ph / (kms / 1e3) / 1e9, 2), "alu_frac": round(ph / (kms / 1e3) / 1e9 / peak, 4),
             "bytes_per_party": st["bytes_per_party"] // args.steps, "rounds": st["rounds"] // args.steps,
             "config": config}
-    if ctx.mode != job.m.binding.MODE_BOTH:
-        line["nvlink_frac"] = round(line["bytes_per_party"] / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4)
+    if ctx.mode == job.m.binding.MODE_PAIR_LOOPBACK:
+        # both parties' kernels on ONE GPU exchanging through local HBM: no NVLink involved
+        wire = line["bytes_per_party"] * LL_WIRE_FACTOR
+        line["exchange"] = {"where": "local HBM (loopback, no NVLink)", "payload_bytes_per_party": line["bytes_per_party"],
+                            "wire_bytes_per_party": int(wire), "wire_over_payload": LL_WIRE_FACTOR,
+                            "wire_gbs_per_party": round(wire / (ms / 1e3) / 1e9, 2)}
+    elif ctx.mode == job.m.binding.MODE_PAIR:
+        wire = line["bytes_per_party"] * LL_WIRE_FACTOR
+        line["nvlink"] = {"payload_bytes_per_party": line["bytes_per_party"], "wire_bytes_per_party": int(wire),
+                          "wire_gbs": round(wire / (ms / 1e3) / 1e9, 2), "peak_gbs": NVLINK_PEER_GBS,
+                          "wire_frac": round(wire / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
+                          "payload_roofline_frac": round(line["bytes_per_party"] / NVLINK_PEER_GBS / 1e9 / (ms / 1e3), 4)}
     return line
 
 

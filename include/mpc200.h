@@ -53,7 +53,13 @@ typedef enum {
 typedef enum {
     MPC_MODE_BOTH = 0,          /* one GPU simulates both parties; openings add in registers   */
     MPC_MODE_PAIR = 1,          /* one GPU (process) per party; every opening is exchanged by  *
-                                 * the fused kernels through NVLink peer memory */
+                                 * the fused kernels through NVLink peer memory. *
+                                 * TRUST MODEL: the trusted dealer is SIMULATED by    *
+                                 * party 1, whose context needs key_p0 to form its correction  *
+                                 * terms (c1 = ab - c0, AND-triple c1, daBit r1A; reading R7). *
+                                 * Party 1 can therefore regenerate party 0's masks: this mode *
+                                 * gives NO privacy against party 1 (a benchmark / protocol-   *
+                                 * shape configuration, not a deployment).                    */
     MPC_MODE_PAIR_LOOPBACK = 2  /* both parties' PAIR kernels in one launch on one GPU,        *
                                  * exchanging through local memory (same code path; tests)    */
 } mpc_mode;
@@ -105,7 +111,7 @@ uint64_t mpc_last_call_philox(const mpc_ctx* ctx);
  * (bench/binding use torch.distributed) and connect.  Both parties must then issue the
  * same sequence of calls with the same shapes; each fused kernel exchanges its openings
  * with the peer kernel through peer memory.  An exchange that does not complete within
- * 20 s poisons the context (results undefined) and mpc_ctx_sync returns MPC_ERR_TIMEOUT. */
+ * 10 s poisons the context (results undefined) and mpc_ctx_sync returns MPC_ERR_TIMEOUT. */
 #define MPC_PAIR_HANDLE_BYTES 64
 mpc_status mpc_pair_export(mpc_ctx* ctx, void* handle_out /* MPC_PAIR_HANDLE_BYTES */);
 mpc_status mpc_pair_connect(mpc_ctx* ctx, const void* peer_handle);
@@ -160,7 +166,8 @@ mpc_status mpc_open(mpc_ctx* ctx, mpc_shares in, int64_t n, uint64_t* ring_out,
                     double* f64_out, int scale_bits);
 /* S2 open to one party (SURVEY 8(b) reveal_to): as mpc_open with reveal_to = -1 (both);
  * reveal_to = p in {0, 1}: only party p learns rec -- in the PAIR modes p sends zeros in place
- * of its share (the exchange keeps its lockstep, the peer learns nothing) and only p writes
+ * of its share (the exchange keeps its lockstep and the peer receives no data from p's
+ * share -- but see the MPC_MODE_PAIR trust model: party 1 holds key_p0) and only p writes
  * ring_out / f64_out (the other party may pass NULL).  In MPC_MODE_BOTH the caller holds both
  * parties and the outputs are written as by mpc_open.  MPC_ERR_INVALID for other reveal_to. */
 mpc_status mpc_open_to(mpc_ctx* ctx, mpc_shares in, int64_t n, int reveal_to, uint64_t* ring_out,
@@ -287,7 +294,9 @@ mpc_status mpc_layernorm(mpc_ctx* ctx, mpc_shares x, mpc_shares z, int64_t rows,
  * x is encoded at 2^16 (round half even), the op's schedule runs on the plaintext ring values
  * with floor truncation, y is decoded.  The MPC output differs from it only by the per-share
  * truncation's (-1, 0] ulp per product.  knobs points to the op's knob struct (mpc_exp_p,
- * mpc_nr_p, mpc_act_p, mpc_softmax_p, mpc_ln_p).  No step, no randomness, no communication. */
+ * mpc_nr_p, mpc_act_p, mpc_softmax_p, mpc_ln_p).  No step, no randomness, no communication.
+ * x and y must not overlap (MPC_ERR_INVALID).  Bit-exact contract: oracle orc_plain_* (DESIGN.md
+ * 2.11; the row max is the schedule's half-split tree with LTZ_w, as in MAX_row). */
 typedef enum { MPC_PLAIN_EXP = 0, MPC_PLAIN_RECIP = 1, MPC_PLAIN_RSQRT = 2, MPC_PLAIN_GELU = 3,
                MPC_PLAIN_SILU = 4, MPC_PLAIN_SIGMOID = 5, MPC_PLAIN_SOFTMAX = 6,
                MPC_PLAIN_LAYERNORM = 7 } mpc_plain_op;

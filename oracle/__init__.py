@@ -26,7 +26,8 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so with gcc -O2 (no intrinsics)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-shared", "-fPIC",
+        # -fwrapv: signed int64 arithmetic wraps like the ring Z_2^64 (no UB on overflow)
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fwrapv", "-D_GNU_SOURCE", "-shared", "-fPIC",
                                "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
@@ -73,6 +74,13 @@ def lib():
         L.orc_layernorm.argtypes = [CP, u64p, u64p, u64p, u64p, I64, I64, I64, DBL, INT,
                                     INT, INT, INT, INT, INT, INT]
         L.orc_ltz_gate_count.argtypes = [INT]; L.orc_ltz_gate_count.restype = INT
+        L.orc_plain_exp.argtypes = [f64p, f64p, I64, INT, INT, INT]
+        L.orc_plain_max.argtypes = [f64p, f64p, I64, I64, INT]
+        L.orc_plain_recip.argtypes = [f64p, f64p, I64, INT, INT, INT, INT]
+        L.orc_plain_rsqrt.argtypes = [f64p, f64p, I64, INT, INT, INT, INT]
+        L.orc_plain_act.argtypes = [f64p, f64p, I64, INT, INT, INT, DBL, ctypes.c_void_p, INT, INT, INT]
+        L.orc_plain_softmax.argtypes = [f64p, f64p, I64, I64, INT, INT, INT, INT, INT, INT, INT, INT, INT]
+        L.orc_plain_layernorm.argtypes = [f64p, f64p, I64, I64, DBL, INT, INT, INT, INT, INT]
         L.orc_max_levels.argtypes = [I64]; L.orc_max_levels.restype = INT
         L.orc_trunc_wrap_trials.argtypes = [INT, INT, I64, I64, ctypes.c_uint64]
         L.orc_trunc_wrap_trials.restype = I64
@@ -236,3 +244,61 @@ class Oracle:
         lib().orc_layernorm(ctypes.byref(self.c), x0, x1, z0, z1, rows, cols, row_off, eps,
                             mean_mode, rsqrt_iters, rsqrt_t, rsqrt_clamp, rsqrt_window, rsqrt_square, bcast)
         return z0, z1
+
+
+class Plain:
+    """Plaintext-ring schedules (the auto-tuner's non-MPC evaluator): each
+    schedule of DESIGN.md 2.5 on one int64 ring value per element (scale 2^16), floor
+    truncation, LTZ_w = bit (w-1).  Float64 in, float64 out (decoded ring values)."""
+
+    @staticmethod
+    def _x(x):
+        return np.ascontiguousarray(x, dtype=np.float64).ravel()
+
+    @classmethod
+    def exp(cls, x, t=8, clamp=0, window=33):
+        x = cls._x(x); y = np.empty_like(x)
+        lib().orc_plain_exp(x, y, x.size, t, int(clamp), window)
+        return y
+
+    @classmethod
+    def recip(cls, x, iters=10, t=8, clamp=0, window=33):
+        x = cls._x(x); y = np.empty_like(x)
+        lib().orc_plain_recip(x, y, x.size, iters, t, int(clamp), window)
+        return y
+
+    @classmethod
+    def rsqrt(cls, x, iters=3, t=8, clamp=0, window=33):
+        x = cls._x(x); y = np.empty_like(x)
+        lib().orc_plain_rsqrt(x, y, x.size, iters, t, int(clamp), window)
+        return y
+
+    @classmethod
+    def act(cls, x, act="gelu", form="poly_x", degree=4, B=5.0, coeffs=None, erf_terms=8, window=33, basis=0):
+        x = cls._x(x); y = np.empty_like(x)
+        c = np.ascontiguousarray(coeffs if coeffs is not None else [0.0], dtype=np.float64)
+        lib().orc_plain_act(x, y, x.size, Oracle.ACT[act], Oracle.FORM[form], degree, float(B), c.ctypes.data,
+                            erf_terms, window, basis)
+        return y
+
+    @classmethod
+    def max(cls, x, rows, cols, window=33):
+        x = cls._x(x); y = np.empty(rows, np.float64)
+        lib().orc_plain_max(x, y, rows, cols, window)
+        return y
+
+    @classmethod
+    def softmax(cls, x, rows, cols, window=33, exp_t=8, exp_clamp=0, exp_window=33, recip_iters=10, recip_t=8,
+                recip_clamp=0, recip_window=33, causal=0):
+        x = cls._x(x); y = np.empty_like(x)
+        lib().orc_plain_softmax(x, y, rows, cols, window, exp_t, int(exp_clamp), exp_window, recip_iters, recip_t,
+                                int(recip_clamp), recip_window, int(causal))
+        return y
+
+    @classmethod
+    def layernorm(cls, x, rows, cols, eps=1e-5, mean_mode=0, rsqrt_iters=3, rsqrt_t=8, rsqrt_clamp=0,
+                  rsqrt_window=33):
+        x = cls._x(x); y = np.empty_like(x)
+        lib().orc_plain_layernorm(x, y, rows, cols, float(eps), mean_mode, rsqrt_iters, rsqrt_t, int(rsqrt_clamp),
+                                  rsqrt_window)
+        return y

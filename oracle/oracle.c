@@ -953,3 +953,203 @@ i64 orc_trunc_wrap_trials(int N, int k, i64 x, i64 trials, u64 key)
     }
     return bad;
 }
+
+/* ======================================================================== */
+/* PLAINTEXT-RING SCHEDULES: the auto-tuner's non-MPC evaluator (SURVEY      */
+/* 8(f) NEXT #4; "directly lowering the graph to a (non-MPC)       */
+/* PyTorch GPU runtime").  Each schedule of DESIGN.md 2.5 is  */
+/* run on ONE plaintext ring value per element (int64 at scale 2^16) instead */
+/* of two shares -- no PRG, no openings:                                     */
+/*   BM(x, y)     -> the wrapping ring product x*y mod 2^64                  */
+/*   MT(x, y)     -> floor((x*y mod 2^64) / 2^16)  (arithmetic shift)         */
+/*   pmulF(x, c)  -> floor((x*E(c) mod 2^64) / 2^16)                          */
+/*   addP(x, c)   -> x + E(c)                                                */
+/*   shr(x, k)    -> floor(x / 2^k)                                          */
+/*   LTZ_w(x)     -> bit (w-1) of x  (the value LTZ reconstructs, R12)        */
+/*   NOT(b)       -> 1 - b                                                   */
+/* Inputs are doubles, encoded with E (round half even, R2); outputs are the */
+/* ring results decoded as (double)(int64)v / 2^16.  The MPC schedules differ */
+/* from these only by the per-share truncation of each product.     */
+/* ======================================================================== */
+static i64 pl_mt(i64 x, i64 y) { return (i64)((u64)x * (u64)y) >> FRAC; }
+static i64 pl_mulf(i64 x, double c) { return (i64)((u64)x * (u64)orc_encode(c)) >> FRAC; }
+static i64 pl_ltz(i64 x, int w) { return (i64)(((u64)x >> (w - 1)) & 1); }
+static double pl_dec(i64 v) { return (double)v / 65536.0; }
+
+/* EXP(x; t, clamp, w) on plaintext (R4, R13) */
+static i64 pl_exp(i64 x, int t, int clamp, int w)
+{
+    i64 y = (x >> t) + orc_encode(1.0);
+    if (clamp) y = (i64)((u64)y * (u64)(1 - pl_ltz(x + orc_encode(ldexp(1.0, t)), w)));  /* no truncation */
+    for (int k = 0; k < t; ++k) y = pl_mt(y, y);
+    return y;
+}
+/* RECIP: y0 = 3 EXP(0.5 - x) + 0.003; iters x y <- y (2 - x y) */
+static i64 pl_recip(i64 x, int iters, int t, int clamp, int w)
+{
+    i64 g = pl_exp(orc_encode(0.5) - x, t, clamp, w);
+    i64 y = (i64)((u64)g * 3u) + orc_encode(0.003);
+    for (int it = 0; it < iters; ++it) {
+        i64 p = pl_mt(x, y);
+        y = pl_mt(y, orc_encode(2.0) - p);
+    }
+    return y;
+}
+/* RSQRT: y0 = 2.2 EXP(-(x/2 + 0.2)) + 0.2; iters x y <- (y (3 - x y^2)) * 0.5 */
+static i64 pl_rsqrt(i64 x, int iters, int t, int clamp, int w)
+{
+    i64 g = pl_exp(-((x >> 1) + orc_encode(0.2)), t, clamp, w);
+    i64 y = pl_mulf(g, 2.2) + orc_encode(0.2);
+    for (int it = 0; it < iters; ++it) {
+        i64 q = pl_mt(y, y);
+        i64 p = pl_mt(x, q);
+        i64 u = pl_mt(y, orc_encode(3.0) - p);
+        y = pl_mulf(u, 0.5);
+    }
+    return y;
+}
+/* HORNER(v; c_0..c_d) and POWER(v; c_0..c_d) on plaintext */
+static i64 pl_horner(i64 v, const double* c, int d)
+{
+    i64 h = pl_mulf(v, c[d]) + orc_encode(c[d - 1]);
+    for (int k = d - 2; k >= 0; --k) h = pl_mt(h, v) + orc_encode(c[k]);
+    return h;
+}
+static i64 pl_power(i64 v, const double* c, int d)
+{
+    i64 p[5] = {0, v, 0, 0, 0};
+    if (d >= 2) p[2] = pl_mt(v, v);
+    if (d >= 3) p[3] = pl_mt(p[2], v);
+    if (d >= 4) p[4] = pl_mt(p[2], p[2]);
+    i64 h = 0;
+    for (int k = 1; k <= d; ++k) h += pl_mulf(p[k], c[k]);
+    return h + orc_encode(c[0]);
+}
+/* S13 segment forms on plaintext (R21, R30) */
+static i64 pl_act(i64 x, int act, int form, int degree, double B, const double* coeffs,
+                  const double* erf_a, int erf_terms, int w, int basis)
+{
+    if (form == FORM_RELU || (form != FORM_ERF && degree == 0)) {
+        i64 nl = 1 - pl_ltz(x, w);
+        return act == ACT_SIGMOID ? (i64)((u64)nl << FRAC) : (i64)((u64)x * (u64)nl);
+    }
+    i64 l1 = pl_ltz(x + orc_encode(B), w), l2 = pl_ltz(x + orc_encode(-B), w);
+    i64 h;
+    if (form == FORM_POLY_X) {
+        h = basis ? pl_power(x, coeffs, degree) : pl_horner(x, coeffs, degree);
+    } else if (form == FORM_POLY_ABS) {
+        i64 ax = (i64)((u64)x * (u64)(1 - 2 * pl_ltz(x, w)));      /* |x| = x (1 - 2 s) */
+        h = pl_mulf(x, 0.5) + (basis ? pl_power(ax, coeffs, degree) : pl_horner(ax, coeffs, degree));
+    } else {                                                         /* erf series (R21) */
+        i64 z = pl_mulf(x, 1.0 / sqrt(2.0));
+        i64 z2 = pl_mt(z, z);
+        i64 S = pl_horner(z2, erf_a, erf_terms - 1);
+        i64 erf = pl_mulf(pl_mt(z, S), 2.0 / sqrt(M_PI));
+        h = pl_mulf(pl_mt(x, erf + orc_encode(1.0)), 0.5);
+    }
+    i64 out = (i64)((u64)h * (u64)(l2 - l1));
+    i64 nl2 = 1 - l2;
+    out += act == ACT_SIGMOID ? (i64)((u64)nl2 << FRAC) : (i64)((u64)x * (u64)nl2);
+    return out;
+}
+
+void orc_plain_exp(const double* x, double* y, i64 n, int t, int clamp, int w)
+{
+    for (i64 i = 0; i < n; ++i) y[i] = pl_dec(pl_exp(orc_encode(x[i]), t, clamp, w));
+}
+void orc_plain_recip(const double* x, double* y, i64 n, int iters, int t, int clamp, int w)
+{
+    for (i64 i = 0; i < n; ++i) y[i] = pl_dec(pl_recip(orc_encode(x[i]), iters, t, clamp, w));
+}
+void orc_plain_rsqrt(const double* x, double* y, i64 n, int iters, int t, int clamp, int w)
+{
+    for (i64 i = 0; i < n; ++i) y[i] = pl_dec(pl_rsqrt(orc_encode(x[i]), iters, t, clamp, w));
+}
+void orc_plain_act(const double* x, double* y, i64 n, int act, int form, int degree, double B,
+                   const double* coeffs, int erf_terms, int w, int basis)
+{
+    double a[16];
+    double fact = 1.0;
+    for (int k = 0; k < erf_terms && k < 16; ++k) {                 /* (-1)^k / (k! (2k+1)) */
+        if (k > 0) fact *= (double)k;
+        a[k] = ((k & 1) ? -1.0 : 1.0) / (fact * (double)(2 * k + 1));
+    }
+    for (i64 i = 0; i < n; ++i)
+        y[i] = pl_dec(pl_act(orc_encode(x[i]), act, form, degree, B, coeffs, a, erf_terms, w, basis));
+}
+
+/* MAX_row on plaintext: the half-split tree of DESIGN.md 2.5 (R22) with the mux               */
+/* x_i' = x_{i+h} + d (1 - LTZ_w(d)), d = x_i - x_{i+h}; odd m carries x_{m-1} to position h.   */
+/* In place over v[0..cols); returns the row maximum (exact when every d is inside the window). */
+static i64 pl_maxrow(i64* v, i64 cols, int w)
+{
+    i64 m = cols;
+    while (m > 1) {
+        i64 h = m / 2;
+        for (i64 i = 0; i < h; ++i) {
+            i64 d = v[i] - v[i + h];
+            v[i] = v[i + h] + (i64)((u64)d * (u64)(1 - pl_ltz(d, w)));
+        }
+        if (m & 1) v[h] = v[m - 1];
+        m = h + (m & 1);
+    }
+    return v[0];
+}
+void orc_plain_max(const double* x, double* y, i64 rows, i64 cols, int w)
+{
+    i64* v = (i64*)malloc(sizeof(i64) * (size_t)(cols > 0 ? cols : 1));
+    for (i64 r = 0; r < rows; ++r) {
+        for (i64 j = 0; j < cols; ++j) v[j] = orc_encode(x[r * cols + j]);
+        y[r] = pl_dec(pl_maxrow(v, cols, w));
+    }
+    free(v);
+}
+
+/* SOFTMAX rows on plaintext (causal 2.12 with row r of the call at position  */
+/* r mod cols): MAX_row as the half-split tree with the mux x_i' = x_{i+h} + d (1 - LTZ_w(d)),  */
+/* d = x_i - x_{i+h} (masked entries enter as -2^(w-2)); e = EXP(x - m) (masked -> 0);        */
+/* S = rowsum(e); r = RECIP(S); out = MT(e, r) (masked -> 0).                                  */
+void orc_plain_softmax(const double* x, double* y, i64 rows, i64 cols, int w,
+                       int exp_t, int exp_clamp, int exp_w, int rc_iters, int rc_t, int rc_clamp, int rc_w,
+                       int causal)
+{
+    i64* v = (i64*)malloc(sizeof(i64) * (size_t)(cols > 0 ? cols : 1));
+    i64* e = (i64*)malloc(sizeof(i64) * (size_t)(cols > 0 ? cols : 1));
+    const i64 L = w >= 2 ? -((i64)1 << (w - 2)) : -1;
+    for (i64 r = 0; r < rows; ++r) {
+        const double* xr = x + r * cols;
+        double* yr = y + r * cols;
+        i64 pos = r % cols;
+        for (i64 j = 0; j < cols; ++j) v[j] = (causal && j > pos) ? L : orc_encode(xr[j]);
+        const i64 mx = pl_maxrow(v, cols, w);
+        i64 S = 0;
+        for (i64 j = 0; j < cols; ++j) {
+            e[j] = (causal && j > pos) ? 0 : pl_exp(orc_encode(xr[j]) - mx, exp_t, exp_clamp, exp_w);
+            S += e[j];
+        }
+        const i64 rc = pl_recip(S, rc_iters, rc_t, rc_clamp, rc_w);
+        for (i64 j = 0; j < cols; ++j) yr[j] = (causal && j > pos) ? 0.0 : pl_dec(pl_mt(e[j], rc));
+    }
+    free(v); free(e);
+}
+
+/* LAYERNORM rows on plaintext (R25): mu = pmulF(rowsum x, 1/d) (mode 0) or     */
+/* floor(rowsum x / d) (mode 1); c = x - mu; v = (same mean of rowsum MT(c,c)) + E(eps);    */
+/* r = RSQRT(v); out = MT(c, r).                                                            */
+void orc_plain_layernorm(const double* x, double* y, i64 rows, i64 cols, double eps, int mean_mode,
+                         int rs_iters, int rs_t, int rs_clamp, int rs_w)
+{
+    const double inv_d = 1.0 / (double)cols;
+    for (i64 r = 0; r < rows; ++r) {
+        const double* xr = x + r * cols;
+        double* yr = y + r * cols;
+        i64 s = 0;
+        for (i64 j = 0; j < cols; ++j) s += orc_encode(xr[j]);
+        const i64 mu = mean_mode == 0 ? pl_mulf(s, inv_d) : floordiv(s, cols);
+        i64 q = 0;
+        for (i64 j = 0; j < cols; ++j) { i64 c = orc_encode(xr[j]) - mu; q += pl_mt(c, c); }
+        const i64 v = (mean_mode == 0 ? pl_mulf(q, inv_d) : floordiv(q, cols)) + orc_encode(eps);
+        const i64 rs = pl_rsqrt(v, rs_iters, rs_t, rs_clamp, rs_w);
+        for (i64 j = 0; j < cols; ++j) yr[j] = pl_dec(pl_mt(orc_encode(xr[j]) - mu, rs));
+    }
+}

@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
 
 // mpc_mul_bcast (NEXT #2): rows' masks and openings (warp <-> 32 rows), then the
 // element products on unit pairs (pairs driver) reading the row records.
-struct BmbRowsArgs { u32 s; SP y; i64 rows; u64 row_off; u64* br; };   // br: [3][rows]
+struct BmbRowsArgs { u32 s; SP y; i64 rows; u64 row_off; u64* br; int loop; };   // br: [3][rows] ([2][3][rows] in loopback)
 template <class PA>
 __global__ void __launch_bounds__(256, MPC_EW_MINB) k_bmb_rows(const __grid_constant__ PA pa, BmbRowsArgs a)
 {
@@ -807,13 +807,13 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_bmb_rows(const __grid_cons
         const i64 r = g * 32 + lane;
         const typename decltype(pr)::S y = r < a.rows ? pr.ld(a.y, r) : pr.zero();
         const BRow b = pr.bmb_row(a.row_off + (u64)r, a.s, y);
-        u64* br = a.br + (pr.party() > 0 ? 3 * a.rows : 0);   // loopback: one record set per party
+        u64* br = a.br + (a.loop && pr.party() > 0 ? 3 * a.rows : 0);   // loopback: one record set per party
         if (r < a.rows) { br[r] = b.b0; br[a.rows + r] = b.b1; br[2 * a.rows + r] = b.f; }
     }
     pa.done(pr);
 }
 struct BmbBody {
-    u32 s; SP x; SO z; i64 n; FastDiv dC; const u64* br; i64 rows; int tb;
+    u32 s; SP x; SO z; i64 n; FastDiv dC; const u64* br; i64 rows; int tb; int loop;
     template <int V, class P>
     __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
         using S = typename P::S;
@@ -824,7 +824,7 @@ struct BmbBody {
             i64 ra = 0, rb = 0;
             if (va) { ra = fdiv((u32)i0[v], dC); xa = pr.ld(x, i0[v]); }
             if (vb) { rb = fdiv((u32)(i0[v] + 1), dC); xb = pr.ld(x, i0[v] + 1); }
-            const u64* bp = br + (pr.party() > 0 ? 3 * rows : 0);
+            const u64* bp = br + (loop && pr.party() > 0 ? 3 * rows : 0);   // loopback: party 1's records
             const BRow b0{bp[ra], bp[rows + ra], bp[2 * rows + ra]}, b1{bp[rb], bp[rows + rb], bp[2 * rows + rb]};
             S za, zb;
             pr.bmb2(u[v], s, xa, xb, b0, b1, za, zb);

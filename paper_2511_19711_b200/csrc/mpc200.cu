@@ -346,13 +346,26 @@ static int occupancy(K kern, size_t dyn = 0, int tpb = TPB)
     return nb;
 }
 
+// Per-device launch-setup cache: kernel attributes (cudaFuncSetAttribute) and occupancies belong to
+// a device context, so a process driving contexts on several GPUs sets them up once per device.
+constexpr int MAX_DEV = 64;
+struct DevCache { int v[MAX_DEV]; };
+template <class F>
+static int dev_cached(DevCache& dc, int dev, F compute)
+{
+    if (dev < 0 || dev >= MAX_DEV) return compute();
+    if (!dc.v[dev]) dc.v[dev] = compute();      // racing first calls compute the same value
+    return dc.v[dev];
+}
+
 template <class Body>
 static mpc_status launch_pairs(mpc_ctx* c, i64 n, u64 off, const Body& b, const char* name)
 {
     if (n <= 0) return MPC_OK;
     const i64 npairs = (i64)(((off + (u64)n + 1) >> 1) - (off >> 1));
     if (!is_pair(c)) {
-        static int per_sm = occupancy(k_pairs<BothA, Body>);
+        static DevCache occ;
+        const int per_sm = dev_cached(occ, c->cfg.device, [] { return occupancy(k_pairs<BothA, Body>); });
         rec_begin(c, name, (u64)n);
         k_pairs<BothA, Body><<<grid_for(c, npairs, TPB, per_sm), TPB, 0, c->stream>>>(BothA{c->K}, n, off, b);
         rec_end(c);
@@ -370,10 +383,11 @@ static mpc_status launch_cone(mpc_ctx* c, i64 n, u64 off, const Body& b, const c
     const i64 nw = (((n + 31) / 32) + CG - 1) / CG;       // warps of work
     const size_t dyn = sizeof(u64) * (size_t)Body::kStash * NWARPS;
     if (!is_pair(c)) {
-        static int per_sm = [&] {
+        static DevCache occ;
+        const int per_sm = dev_cached(occ, c->cfg.device, [&] {
             cudaFuncSetAttribute(k_groups_cone<BothA, Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
             return occupancy(k_groups_cone<BothA, Body>, dyn);
-        }();
+        });
         rec_begin(c, name, (u64)n);
         k_groups_cone<BothA, Body><<<grid_for(c, nw * 32, TPB, per_sm), TPB, dyn, c->stream>>>(BothA{c->K}, n, off, b);
         rec_end(c);
@@ -390,7 +404,8 @@ static mpc_status launch_groups(mpc_ctx* c, i64 n, u64 off, const Body& b, const
 {
     if (n <= 0) return MPC_OK;
     if (!is_pair(c)) {
-        static int per_sm = occupancy(k_groups<BothA, Body>);
+        static DevCache occ;
+        const int per_sm = dev_cached(occ, c->cfg.device, [] { return occupancy(k_groups<BothA, Body>); });
         rec_begin(c, name, (u64)n);
         k_groups<BothA, Body><<<grid_for(c, ((n + 31) / 32) * 32, TPB, per_sm), TPB, 0, c->stream>>>(BothA{c->K}, n, off, b);
         rec_end(c);
@@ -902,7 +917,7 @@ mpc_status mpc_mul_bcast(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, i
     if (rows > 0) {
         u64* br = (u64*)scratch(c, sizeof(u64) * 3 * (size_t)rows * (is_loop(c) ? 2 : 1));
         if (!br) return fail(c, MPC_ERR_NOMEM, "mul_bcast scratch");
-        BmbRowsArgs ra{(u32)c->step, spv(c, y), rows, (u64)row_off, br};
+        BmbRowsArgs ra{(u32)c->step, spv(c, y), rows, (u64)row_off, br, is_loop(c) ? 1 : 0};
         const i64 nw = (rows + 31) / 32;
         if (!is_pair(c)) {
             rec_begin(c, "bcast_rows", (u64)rows);
@@ -916,7 +931,7 @@ mpc_status mpc_mul_bcast(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, i
         }
         if (st) return st;
         st = launch_pairs(c, n, (u64)off, BmbBody{(u32)c->step, spv(c, x), sov(c, z), n, make_fastdiv((u32)cols),
-                                                  br, rows, tb}, "mul_bcast");
+                                                  br, rows, tb, is_loop(c) ? 1 : 0}, "mul_bcast");
         if (st) return st;
         acct_bcast(c, (u64)n, (u64)rows);
     }
@@ -1013,10 +1028,10 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
             t.A[p] = LA[p]; t.B[p] = LB[p]; t.Kp[p] = (int)Kps[p];
         }
         if ((st = cuda_check(c, "mm_limbs"))) return st;
-        static bool attr = [] {
-            return cudaFuncSetAttribute(k_mm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) == cudaSuccess;
-        }();
-        (void)attr;
+        static DevCache attr;
+        dev_cached(attr, c->cfg.device, [] {
+            return cudaFuncSetAttribute(k_mm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM) == cudaSuccess ? 1 : -1;
+        });
         const dim3 grid((unsigned)NB, (unsigned)MB, (unsigned)(batch * a.np));
         rec_begin(c, "matmul_tc", (u64)(batch * M * N));
         k_mm_tc<<<grid, 128, TC_SMEM, c->stream>>>(t);
@@ -1186,6 +1201,8 @@ mpc_status mpc_plain_eval(mpc_ctx* c, int op, const void* knobs, const double* x
 {
     if (!c) return MPC_ERR_INVALID;
     if (!knobs || !x || !y || rows < 0 || cols < 1) return fail(c, MPC_ERR_INVALID, "plain_eval args");
+    if (x < y + rows * cols && y < x + rows * cols)      // the softmax rows use y as their max-tree workspace
+        return fail(c, MPC_ERR_INVALID, "plain_eval: x and y must not overlap");
     PlainArgs a;
     memset(&a, 0, sizeof a);
     a.x = x; a.y = y; a.rows = rows; a.cols = cols;
@@ -1402,8 +1419,9 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
             while (*q && *q != ',') ++q;
             if (*q == ',') ++q;
         }
-        while (r < rows) { sched.push_back(std::min<i64>(sched.back(), rows - r)); r += sched.back(); }
-    } else {
+        while (!sched.empty() && r < rows) { sched.push_back(std::min<i64>(sched.back(), rows - r)); r += sched.back(); }
+    }
+    if (sched.empty()) {                                  // default (also for an empty / unparsable MPC_HIO_SCHED)
         const i64 cr = chunk_rows > 0 ? chunk_rows : std::max<i64>(32, ((rows + 3) / 4 + 31) / 32 * 32);
         for (i64 r = 0; r < rows; r += cr) sched.push_back(std::min<i64>(cr, rows - r));
     }

@@ -114,10 +114,23 @@ __global__ void __launch_bounds__(256) k_plain(const __grid_constant__ PlainArgs
         double* yr = a.y + row * a.cols;
         if (a.op == 4) {                                  // SOFTMAX (causal 2.12)
             const i64 nv = a.causal ? row % a.cols + 1 : a.cols;    // visible columns
-            i64 m = pl_enc(xr[0]);
-            for (i64 j = 1; j < nv; ++j) { const i64 v = pl_enc(xr[j]); if (v - m >= 0) m = v; }   // exact max
+            // MAX_row as the schedule's half-split tree (R22) with the mux x_h + d (1 - LTZ_w(d)),
+            // in the output row (reinterpreted as int64) as workspace; masked entries -2^(w-2)
+            i64* v = reinterpret_cast<i64*>(yr);
+            const i64 L = a.w >= 2 ? -((i64)1 << (a.w - 2)) : -1;
+            for (i64 j = 0; j < a.cols; ++j) v[j] = j < nv ? pl_enc(xr[j]) : L;
+            for (i64 m = a.cols; m > 1;) {
+                const i64 h = m / 2;
+                for (i64 i = 0; i < h; ++i) {
+                    const i64 d = (i64)((u64)v[i] - (u64)v[i + h]);
+                    v[i] = (i64)((u64)v[i + h] + (u64)d * (u64)(1 - pl_ltz(d, a.w)));
+                }
+                if (m & 1) v[h] = v[m - 1];
+                m = h + (m & 1);
+            }
+            const i64 m = v[0];
             i64 S = 0;
-            for (i64 j = 0; j < nv; ++j) S += pl_exp(pl_enc(xr[j]) - m, a.ek);
+            for (i64 j = 0; j < nv; ++j) S = (i64)((u64)S + (u64)pl_exp(pl_enc(xr[j]) - m, a.ek));
             const i64 r = pl_recip(S, a.nk);
             for (i64 j = 0; j < a.cols; ++j) yr[j] = j < nv ? pl_dec(pl_mt(pl_exp(pl_enc(xr[j]) - m, a.ek), r)) : 0.0;
         } else {                                          // LAYERNORM

@@ -1,9 +1,9 @@
 """GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact on every
 uint64 share of both parties, on seeded inputs (DESIGN.md section 2 contract).
 
-Small cases span several warps/tiles and a ragged tail; full BASELINE sizes are
-checked on sampled 32-row / 32-element-aligned slices, which the oracle reproduces
-exactly because the PRG is keyed by global unit (shard invariance).
+Small cases span several warps/tiles and a ragged tail; full BASELINE sizes compare EVERY share
+against the whole-array oracle run on all host cores (tests/oracle_pool.py: 32-aligned slices
+with global offsets reproduce the unsharded op exactly, the PRG being keyed by global unit).
 """
 import numpy as np
 import pytest
@@ -264,8 +264,14 @@ def test_determinism(mpc):
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
 
 
-# ---------------------------------------------- full BASELINE sizes, sampled ----
-def test_softmax_cfg2_full_size_sampled(mpc):
+# ---------------------------------------------- full BASELINE sizes, EVERY share ----
+# The oracle runs the whole op on every host core (tests/oracle_pool.py: 32-aligned slices with
+# their global offsets reproduce the unsharded op exactly), and every output share of both parties
+# is compared -- in the launch configuration bench.py / tools/sweep.py time.
+import oracle_pool  # noqa: E402
+
+
+def test_softmax_cfg2_full_size_every_share(mpc):
     rows, cols = workloads.SHAPES["cfg2_softmax"]
     keys = workloads.keys(2)
     c = mpc.Ctx.for_cfg(keys)
@@ -273,13 +279,8 @@ def test_softmax_cfg2_full_size_sampled(mpc):
     gx = c.share(torch.from_numpy(x).cuda())
     s0 = c.step
     z = c.softmax(gx, rows, cols)
-    z0, z1 = np_(z[0]).reshape(rows, cols), np_(z[1]).reshape(rows, cols)
-    x0, x1 = np_(gx[0]).reshape(rows, cols), np_(gx[1]).reshape(rows, cols)
-    for r0 in (0, 4096, rows - 32):
-        o = Oracle.for_cfg(keys, s0)
-        sl = slice(r0, r0 + 32)
-        r = o.softmax((x0[sl].ravel(), x1[sl].ravel()), 32, cols, row_off=r0)
-        assert np.array_equal(z0[sl].ravel(), r[0]) and np.array_equal(z1[sl].ravel(), r[1])
+    r = oracle_pool.rows_op("softmax", keys, s0, (np_(gx[0]), np_(gx[1])), rows, cols)
+    same(z, r)
     # reconstructed floats vs the true softmax: the exp-limit formula itself is
     # 1.02e-2 from the true softmax on the full cfg2 input; fixed point adds <= 2e-3
     _, f = c.open(z)
@@ -289,7 +290,19 @@ def test_softmax_cfg2_full_size_sampled(mpc):
     assert np.max(np.abs(y - fr.softmax(xd))) <= 1.25e-2
 
 
-def test_gelu_cfg3_full_size_sampled(mpc):
+def test_softmax_cfg2_cone_full_size_every_share(mpc):
+    """the carry-cone circuit (NEXT #1) in the headline shape: bit-identical to the same oracle"""
+    rows, cols = workloads.SHAPES["cfg2_softmax"]
+    keys = workloads.keys(2)
+    c = mpc.Ctx.for_cfg(keys)
+    c.set_ltz_circuit(1)
+    gx = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    s0 = c.step
+    z = c.softmax(gx, rows, cols)
+    same(z, oracle_pool.rows_op("softmax", keys, s0, (np_(gx[0]), np_(gx[1])), rows, cols))
+
+
+def test_gelu_cfg3_full_size_every_share(mpc):
     n = workloads.SHAPES["cfg3_gelu"]
     keys = workloads.keys(3)
     c = mpc.Ctx.for_cfg(keys)
@@ -298,19 +311,15 @@ def test_gelu_cfg3_full_size_sampled(mpc):
     s0 = c.step
     z = c.gelu(gx, form="poly_abs", degree=4)
     knobs = mpc.default_act("gelu", "poly_abs", degree=4)
-    z0, z1 = np_(z[0]), np_(z[1])
-    x0, x1 = np_(gx[0]), np_(gx[1])
-    for off in (0, 1_000_000 - 1_000_000 % 32, n - 4096):
-        o = Oracle.for_cfg(keys, s0)
-        sl = slice(off, off + 4096)
-        r = o.act((x0[sl], x1[sl]), "gelu", "poly_abs", 4, knobs["B"], knobs["coeffs"], off=off)
-        assert np.array_equal(z0[sl], r[0]) and np.array_equal(z1[sl], r[1])
+    r = oracle_pool.elems_op("act", keys, s0, (np_(gx[0]), np_(gx[1])), n, act="gelu", form="poly_abs", degree=4,
+                             B=knobs["B"], coeffs=knobs["coeffs"])
+    same(z, r)
     _, f = c.open(z)
     xd = np_(c.open(gx)[1])
     assert np.max(np.abs(np_(f) - fr.gelu(xd))) <= 4.2e-3 + 1e-3
 
 
-def test_relu_cfg4_first_layer_sampled(mpc):
+def test_relu_cfg4_first_layer_shard_every_share(mpc):
     N, C, H, W = workloads.SHAPES["cfg4_relu_first"]
     n = N * C * H * W // 4          # one 8-image shard of the first ReLU layer (4 pairs)
     keys = workloads.keys(4)
@@ -322,17 +331,12 @@ def test_relu_cfg4_first_layer_sampled(mpc):
     ring = np_(c.open(z)[0]).view(np.int64)
     xr = np_(c.open(gx)[0]).view(np.int64)
     assert np.array_equal(ring, np.maximum(xr, 0))      # ReLU is exact
-    z0, z1 = np_(z[0]), np_(z[1])
-    for off in (0, n // 2 - (n // 2) % 32, n - 8192):
-        o = Oracle.for_cfg(keys, s0)
-        sl = slice(off, off + 8192)
-        r = o.relu((np_(gx[0])[sl], np_(gx[1])[sl]), off=off)
-        assert np.array_equal(z0[sl], r[0]) and np.array_equal(z1[sl], r[1])
+    same(z, oracle_pool.elems_op("relu", keys, s0, (np_(gx[0]), np_(gx[1])), n))
 
 
-def test_softmax_cfg5_pair_shard_sampled(mpc):
+def test_softmax_cfg5_pair_shard_every_share(mpc):
     """cfg5: one pair's shard of a GPT-2 attention softmax (2 sequences x 12 heads x 1024 rows of
-    1024), the launch bench/sweep time; sampled 32-row slices bit-exact, floats within §5."""
+    1024), the launch bench/sweep time; every share bit-exact, floats within §5."""
     rows, cols = 2 * 12 * 1024, 1024
     keys = workloads.keys(5)
     c = mpc.Ctx.for_cfg(keys)
@@ -340,13 +344,7 @@ def test_softmax_cfg5_pair_shard_sampled(mpc):
     gx = c.share(torch.from_numpy(x).cuda())
     s0 = c.step
     z = c.softmax(gx, rows, cols)
-    z0, z1 = np_(z[0]).reshape(rows, cols), np_(z[1]).reshape(rows, cols)
-    x0, x1 = np_(gx[0]).reshape(rows, cols), np_(gx[1]).reshape(rows, cols)
-    for r0 in (0, 12288 + 96, rows - 32):
-        o = Oracle.for_cfg(keys, s0)
-        sl = slice(r0, r0 + 32)
-        r = o.softmax((x0[sl].ravel(), x1[sl].ravel()), 32, cols, row_off=r0)
-        assert np.array_equal(z0[sl].ravel(), r[0]) and np.array_equal(z1[sl].ravel(), r[1])
+    same(z, oracle_pool.rows_op("softmax", keys, s0, (np_(gx[0]), np_(gx[1])), rows, cols))
     _, f = c.open(z)
     y = np_(f).reshape(rows, cols)
     xd = np_(c.open(gx)[1]).reshape(rows, cols)
@@ -358,7 +356,7 @@ def test_softmax_cfg5_pair_shard_sampled(mpc):
     assert np.max(np.abs(y[sl] - fr.softmax(xd[sl]))) <= 3e-2
 
 
-def test_layernorm_cfg5_full_size_sampled(mpc):
+def test_layernorm_cfg5_full_size_every_share(mpc):
     rows, cols = workloads.SHAPES["cfg5_ln"]
     keys = workloads.keys(5)
     c = mpc.Ctx.for_cfg(keys)
@@ -366,13 +364,7 @@ def test_layernorm_cfg5_full_size_sampled(mpc):
     gx = c.share(torch.from_numpy(x).cuda())
     s0 = c.step
     z = c.layernorm(gx, rows, cols)
-    z0, z1 = np_(z[0]).reshape(rows, cols), np_(z[1]).reshape(rows, cols)
-    x0, x1 = np_(gx[0]).reshape(rows, cols), np_(gx[1]).reshape(rows, cols)
-    for r0 in (0, 4096, rows - 32):
-        o = Oracle.for_cfg(keys, s0)
-        sl = slice(r0, r0 + 32)
-        r = o.layernorm((x0[sl].ravel(), x1[sl].ravel()), 32, cols, row_off=r0)
-        assert np.array_equal(z0[sl].ravel(), r[0]) and np.array_equal(z1[sl].ravel(), r[1])
+    same(z, oracle_pool.rows_op("layernorm", keys, s0, (np_(gx[0]), np_(gx[1])), rows, cols))
     _, f = c.open(z)
     xd = np_(c.open(gx)[1]).reshape(rows, cols)
     y = np_(f).reshape(rows, cols)
@@ -383,9 +375,9 @@ def test_layernorm_cfg5_full_size_sampled(mpc):
     assert np.max(np.abs(y - fr.layernorm(xd))) <= 1.6e-2
 
 
-def test_maxpool_cfg4_shard_sampled(mpc):
+def test_maxpool_cfg4_shard_every_share(mpc):
     """cfg4 MaxPool 3x3/2 pad 1 on one pair's 8-image shard of 32 x 64 x 112 x 112: exact
-    reconstruction everywhere, output shares of two whole images bit-exact vs the oracle."""
+    reconstruction, and every output share of all 8 images bit-exact vs the oracle."""
     N, C, H, W = 8, 64, 112, 112
     keys = workloads.keys(4)
     c = mpc.Ctx.for_cfg(keys)
@@ -402,12 +394,7 @@ def test_maxpool_cfg4_shard_sampled(mpc):
         for j in range(3):
             ref = np.maximum(ref, pad[:, :, i:i + 2 * Ho:2, j:j + 2 * Wo:2])
     assert np.array_equal(np_(c.open(z)[0]).view(np.int64).reshape(N, C, Ho, Wo), ref)
-    z0, z1 = np_(z[0]).reshape(N, -1), np_(z[1]).reshape(N, -1)
-    x0, x1 = np_(gx[0]).reshape(N, -1), np_(gx[1]).reshape(N, -1)
-    for img in (0, N - 1):
-        o = Oracle.for_cfg(keys, s0)
-        r = o.maxpool2d((x0[img], x1[img]), 1, C, H, W, 3, 2, 1, img_off=img)
-        assert np.array_equal(z0[img], r[0]) and np.array_equal(z1[img], r[1])
+    same(z, oracle_pool.maxpool_op(keys, s0, (np_(gx[0]), np_(gx[1])), N, C, H, W, k=3, stride=2, pad=1))
 
 
 def test_bad_args_raise(mpc):

@@ -117,3 +117,77 @@ def test_plain_causal_softmax_vs_mpc(m):
     full = np.arange(rows) % cols == cols - 1
     yd = c.plain_eval("softmax", xd, rows=rows, cols=cols).cpu().numpy().reshape(rows, cols)
     assert np.array_equal(y[full], yd[full])
+
+
+# ---- bit-exact parity of the GPU evaluator with the oracle's plaintext schedules (oracle.Plain) ----
+def _plain_cases():
+    from paper_2511_19711_b200 import binding
+    cases = []
+    for t in range(0, 9):
+        for clamp in (0, 1):
+            cases.append(("exp", dict(t=t, clamp=clamp), dict(t=t, clamp=clamp), None))
+    cases.append(("exp", dict(t=8, clamp=1, window=21), dict(t=8, clamp=1, window=21), None))
+    for it, t, clamp in ((10, 8, 0), (3, 8, 1), (7, 4, 0), (1, 2, 1)):
+        cases.append(("recip", dict(iters=it, t=t, clamp=clamp), dict(iters=it, t=t, clamp=clamp), None))
+        cases.append(("rsqrt", dict(iters=it, t=t, clamp=clamp), dict(iters=it, t=t, clamp=clamp), None))
+    for f in binding.load_coeffs():
+        if f["form"] == "erf":
+            continue
+        for basis in (0, 1):
+            kw = dict(form=f["form"], degree=f["degree"], basis=basis)
+            o = dict(act=f["op"], form=f["form"], degree=f["degree"], B=f["interval"][1],
+                     coeffs=f["coefficients"], basis=basis)
+            cases.append((f["op"], kw, o, "act"))
+    for K in (2, 4, 8, 12):
+        cases.append(("gelu", dict(form="erf", erf_terms=K), dict(act="gelu", form="erf", degree=1, B=2.5,
+                                                                  erf_terms=K), "act"))
+    for act in ("gelu", "silu", "sigmoid"):
+        cases.append((act, dict(form="relu", degree=0), dict(act=act, form="relu", degree=0, B=5.0), "act"))
+    cases.append(("relu", dict(window=21), dict(act="gelu", form="relu", degree=0, B=5.0, window=21), "act"))
+    return cases
+
+
+@pytest.mark.parametrize("case", range(len(_plain_cases())))
+def test_plain_eval_elementwise_bit_exact_vs_oracle(m, case):
+    from oracle import Plain
+    op, kw, okw, kind = _plain_cases()[case]
+    c = m.Ctx.for_cfg(workloads.keys(1))
+    if op == "exp":
+        x = workloads.exp_inputs(4099, tail_frac=0.05)
+    elif op == "recip":
+        x = workloads.recip_inputs(4099)
+    elif op == "rsqrt":
+        x = np.exp(np.random.default_rng(7).uniform(np.log(0.05), np.log(60), 4099))
+    else:
+        x = workloads.act_inputs(4099)
+    y = c.plain_eval(op, dev(x), **kw).cpu().numpy()
+    if kind == "act":
+        ref = Plain.act(x, **okw)
+    else:
+        ref = getattr(Plain, op)(x, **okw)
+    assert np.array_equal(y, ref), f"{op} {kw}: {np.sum(y != ref)} of {y.size} differ"
+
+
+@pytest.mark.parametrize("rows,cols,kw", [
+    (64, 128, {}), (33, 77, {}), (8, 1024, {}), (5, 1, {}), (7, 2, {}),
+    (64, 128, dict(exp_clamp=1)), (48, 64, dict(causal=1)), (40, 16, dict(causal=1, exp_t=2, exp_clamp=1)),
+    (32, 128, dict(exp_t=4, recip_iters=7, recip_t=4)), (32, 96, dict(window=21))])
+def test_plain_eval_softmax_bit_exact_vs_oracle(m, rows, cols, kw):
+    from oracle import Plain
+    c = m.Ctx.for_cfg(workloads.keys(2))
+    x = workloads.softmax_inputs(rows, cols, spike=bool(kw.get("exp_clamp")))
+    y = c.plain_eval("softmax", dev(x), rows=rows, cols=cols, **kw).cpu().numpy()
+    ref = Plain.softmax(x, rows, cols, **kw)
+    assert np.array_equal(y, ref), f"{np.sum(y != ref)} of {y.size} differ"
+
+
+@pytest.mark.parametrize("rows,cols,kw", [
+    (64, 768, {}), (64, 768, dict(mean_mode=1)), (17, 100, dict(rsqrt_iters=10)),
+    (32, 768, dict(rsqrt_t=4, rsqrt_clamp=1)), (8, 256, dict(eps=1e-3, mean_mode=1))])
+def test_plain_eval_layernorm_bit_exact_vs_oracle(m, rows, cols, kw):
+    from oracle import Plain
+    c = m.Ctx.for_cfg(workloads.keys(5))
+    x = workloads.layernorm_inputs(rows, cols)
+    y = c.plain_eval("layernorm", dev(x), rows=rows, cols=cols, **kw).cpu().numpy()
+    ref = Plain.layernorm(x, rows, cols, **kw)
+    assert np.array_equal(y, ref), f"{np.sum(y != ref)} of {y.size} differ"

@@ -65,6 +65,55 @@ __global__ void k_lop3(uint32_t* out, uint32_t seed)
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+
+// ---- pure-pipe kernels (one SASS instruction per chained step; checked with cuobjdump -sass) ----
+// IMAD.WIDE.U32 alone: p = (u64)hi32(p) * M (one IMAD.WIDE.U32 per step, 8 independent chains)
+__global__ void k_imadw_pure(uint32_t* out, uint32_t seed)
+{
+    uint64_t p[CHAINS];
+    for (int c = 0; c < CHAINS; ++c) p[c] = ((uint64_t)((seed + threadIdx.x) * (c + 3)) << 32) | (uint64_t)(c * 977u + threadIdx.x);
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c)
+            asm volatile("{.reg .u32 lo, hi; mov.b64 {lo, hi}, %0; mul.wide.u32 %0, hi, 0xD2511F53;}" : "+l"(p[c]));
+    }
+    uint32_t s = 0;
+    for (int c = 0; c < CHAINS; ++c) s ^= (uint32_t)p[c] ^ (uint32_t)(p[c] >> 32);
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// LOP3 alone: a = a ^ b ^ d with loop-invariant b, d
+__global__ void k_lop3_pure(uint32_t* out, uint32_t seed)
+{
+    uint32_t a[CHAINS], b = seed * 3 + 1 + threadIdx.x, d = seed * 5 + 7;
+    for (int c = 0; c < CHAINS; ++c) a[c] = seed + threadIdx.x * 7 + c;
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c)
+            asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(b), "r"(d));
+    }
+    uint32_t s = 0;
+    for (int c = 0; c < CHAINS; ++c) s ^= a[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+// the Philox round's instruction pair without the key bumps: IMAD.WIDE + LOP3 per step
+__global__ void k_imadw_lop3(uint32_t* out, uint32_t seed)
+{
+    uint64_t p[CHAINS];
+    uint32_t x[CHAINS];
+    const uint32_t k = seed * 0x9E3779B9u + threadIdx.x;
+    for (int c = 0; c < CHAINS; ++c) { p[c] = (uint64_t)(seed + threadIdx.x + c) << 7; x[c] = c; }
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) {
+            asm volatile("{.reg .u32 lo, hi, plo, phi; mov.b64 {plo, phi}, %1; mul.wide.u32 %1, %0, 0xD2511F53;"
+                         " mov.b64 {lo, hi}, %1; lop3.b32 %0, hi, plo, %2, 0x96;}" : "+r"(x[c]), "+l"(p[c]) : "r"(k));
+        }
+    }
+    uint32_t s = 0;
+    for (int c = 0; c < CHAINS; ++c) s ^= x[c] ^ (uint32_t)p[c];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 struct Key { uint32_t lo, hi; };
 __device__ __forceinline__ uint4 philox(Key key, uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3)
 {
@@ -165,6 +214,12 @@ int main()
     printf(", \"imad_hi_plus_iadd_per_clk_per_sm\": %.2f", nthr * ITERS * CHAINS / (ms * 1e-3) / sms / (clk * 1e3));
     ms = timeit([&] { k_lop3<<<blocks, threads>>>(out, 1); });
     printf(", \"lop3_plus_iadd_per_clk_per_sm\": %.2f", nthr * ITERS * CHAINS / (ms * 1e-3) / sms / (clk * 1e3));
+    ms = timeit([&] { k_imadw_pure<<<blocks, threads>>>(out, 1); });
+    printf(", \"imadw_pure_warp_instr_per_clk_per_smsp\": %.4f", nthr / 32 * ITERS * CHAINS / (ms * 1e-3) / (sms * 4.0) / (clk * 1e3));
+    ms = timeit([&] { k_lop3_pure<<<blocks, threads>>>(out, 1); });
+    printf(", \"lop3_pure_warp_instr_per_clk_per_smsp\": %.4f", nthr / 32 * ITERS * CHAINS / (ms * 1e-3) / (sms * 4.0) / (clk * 1e3));
+    ms = timeit([&] { k_imadw_lop3<<<blocks, threads>>>(out, 1); });
+    printf(", \"imadw_plus_lop3_pairs_per_clk_per_smsp\": %.4f", nthr / 32 * ITERS * CHAINS / (ms * 1e-3) / (sms * 4.0) / (clk * 1e3));
     const int reps = 256;
     for (int tpb : {128, 256, 512, 1024}) {
         const int nb = sms * (2048 / tpb);

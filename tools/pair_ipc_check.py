@@ -5,7 +5,8 @@ With one GPU both processes share cuda:0 (the driver time-slices their contexts,
 exchange round costs a context switch: correctness only, tiny shapes); with two or more GPUs
 rank r uses cuda:r.  Each op's output shares are gathered on rank 0 and compared bit for bit
 with MPC_MODE_BOTH on the same seeds and step ids (share, mul, ReLU, GELU, softmax dense /
-cone + square triples / causal, LayerNorm, Beaver matmul), and an open to party 1 only.
+cone + square triples / causal, LayerNorm, Beaver matmul, broadcast-triple mul / softmax /
+LayerNorm), and an open to party 1 only.
 
   python tools/pair_ipc_check.py             (prints PAIR_IPC_OK on success, exit code 0)
   python tools/pair_ipc_check.py --mismatch  (debug header check: the parties issue different ops;
@@ -44,6 +45,10 @@ def ops(c, x, party, n_rows, n_cols):
     out.append(c.softmax(s, n_rows, n_cols, causal=1))
     # X = s as n_rows x n_cols, Y = the same buffer as n_cols x n_rows (tensor-core engine)
     out.append(c.matmul(s, s, 1, n_rows, n_cols, n_rows, trunc_bits=16))
+    # broadcast triple (NEXT #2): per-row record scratch is per party in PAIR
+    out.append(c.mul_bcast(s, s, n_rows, n_cols, trunc_bits=16))
+    out.append(c.softmax(s, n_rows, n_cols, bcast=1))
+    out.append(c.layernorm(s, n_rows, n_cols, bcast=1))
     return out
 
 

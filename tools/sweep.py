@@ -363,7 +363,7 @@ def main():
     S = Sweep(args.steps, args.warmup)
     res = {"device": torch.cuda.get_device_name(0), "mode": "BOTH", "steps": args.steps, "warmup": args.warmup,
            "peak_gphilox_derived": round(bench.philox_peak_gblocks(1965.0), 2),
-           "philox_measured_ceiling": bench.PHILOX_MICROBENCH_GBS, "sections": {}}
+           "philox_peak_basis": "profiles/r02_microbench.json (IMAD.WIDE.U32 rate)", "philox_only_measured": bench.philox_only_measured(), "sections": {}}
     clocks = bench.Clocks(0)
     clocks.start()
     t0 = time.time()
