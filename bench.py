@@ -40,7 +40,9 @@ SM_COUNT, SMSP, LANES = 148, 4, 32
 MICROBENCH_PATH = os.path.join(ROOT, "profiles", "r02_microbench.json")
 IMADW_CYCLES_FALLBACK = 4.037
 NVLINK_PEER_GBS = 770.0      # B200_PROFILING.md: measured peer copy per direction
-LL_WIRE_FACTOR = 2.0         # PAIR exchange: each 8-byte payload word travels as two {half | tag} words
+# PAIR exchange wire bytes per payload byte: LL (format 0) sends every 8-byte payload word
+# as two {half | round} words; LL63 (format 1, the MPC_MODE_PAIR default) sends 33 tagged words per 32
+WIRE_FACTOR = {0: 2.0, 1: 33.0 / 32.0}
 
 
 def imadw_cycles():
@@ -203,7 +205,7 @@ def timed(job, ctx, fn, steps, flush, clocks=None):
     return job.maxr(ms), kt, st, clk
 
 
-def roofline(job, ctx_mode, kt, st, steps, ms_step, n):
+def roofline(job, ctx_mode, kt, st, steps, ms_step, n, xfmt=1):
     """Dominant kernel's achieved rate vs its roofline."""
     agg = {}
     for name, kms, ph, _u in kt:
@@ -234,12 +236,14 @@ def roofline(job, ctx_mode, kt, st, steps, ms_step, n):
          "hbm_frac": round(32 * n / (ms_step / 1e3) / 1e9 / float(peaks.get("hbm_gbs", 6650.0)), 5)}
     if ctx_mode != job.m.binding.MODE_BOTH:
         bps = st["bytes_per_party"] / steps
-        wps = bps * LL_WIRE_FACTOR
+        fmt = xfmt
+        wps = bps * WIRE_FACTOR[fmt]
         r["nvlink"] = {"payload_bytes_per_party_per_step": int(bps), "wire_bytes_per_party_per_step": int(wps),
                        "wire_gbs": round(wps / (ms_step / 1e3) / 1e9, 2), "peak_gbs": NVLINK_PEER_GBS,
                        "wire_frac": round(wps / (ms_step / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
                        "payload_roofline_frac": round(bps / NVLINK_PEER_GBS / 1e9 / (ms_step / 1e3), 4),
-                       "rounds_per_step": st["rounds"] // steps}
+                       "rounds_per_step": st["rounds"] // steps, "exchange_format": ["LL", "LL63"][fmt],
+                       "wire_over_payload": WIRE_FACTOR[fmt]}
         r["note"] = ("PAIR: philox counts both parties + dealer (the BOTH-mode work) per pair; "
                      "each party's GPU executes its part plus party 1's dealer corrections")
     return r
@@ -271,7 +275,7 @@ def run_mpc200(args):
     torch.cuda.synchronize()
     ms_step, kt, st, clk = timed(job, ctx, step, args.steps, flush, Clocks(job.local))
     value = job.npairs * n / (ms_step / 1e3)
-    roof = roofline(job, ctx.mode, kt, st, args.steps, ms_step, n)
+    roof = roofline(job, ctx.mode, kt, st, args.steps, ms_step, n, ctx.exchange)
     parity = check_timed_output(job, ctx.step - steps_per_call, xs, out, rows, cols, row_off, sm_kw)
 
     # ---- e2e: host buffers through the public API (H2D inputs, D2H outputs inside the region) ----
@@ -382,12 +386,14 @@ def _op_line(job, ctx, fn, n, flush, args, config):
             "config": config}
     if ctx.mode == job.m.binding.MODE_PAIR_LOOPBACK:
         # both parties' kernels on ONE GPU exchanging through local HBM: no NVLink involved
-        wire = line["bytes_per_party"] * LL_WIRE_FACTOR
-        line["exchange"] = {"where": "local HBM (loopback, no NVLink)", "payload_bytes_per_party": line["bytes_per_party"],
-                            "wire_bytes_per_party": int(wire), "wire_over_payload": LL_WIRE_FACTOR,
+        f = WIRE_FACTOR[ctx.exchange]
+        wire = line["bytes_per_party"] * f
+        line["exchange"] = {"where": "local HBM (loopback, no NVLink)", "format": ["LL", "LL63"][ctx.exchange],
+                            "payload_bytes_per_party": line["bytes_per_party"],
+                            "wire_bytes_per_party": int(wire), "wire_over_payload": f,
                             "wire_gbs_per_party": round(wire / (ms / 1e3) / 1e9, 2)}
     elif ctx.mode == job.m.binding.MODE_PAIR:
-        wire = line["bytes_per_party"] * LL_WIRE_FACTOR
+        wire = line["bytes_per_party"] * WIRE_FACTOR[ctx.exchange]
         line["nvlink"] = {"payload_bytes_per_party": line["bytes_per_party"], "wire_bytes_per_party": int(wire),
                           "wire_gbs": round(wire / (ms / 1e3) / 1e9, 2), "peak_gbs": NVLINK_PEER_GBS,
                           "wire_frac": round(wire / (ms / 1e3) / 1e9 / NVLINK_PEER_GBS, 4),
@@ -506,7 +512,18 @@ def time_loopback(job, m, flush, args):
     z2 = c._empty(n3)
     line2 = _op_line(job, c, lambda: c.gelu(g, form="poly_abs", degree=4, out=z2), n3, flush, args,
                      "cfg3 GELU |x|-form deg 4, PAIR protocol in loopback")
-    return {"softmax_pair_loopback": line, "gelu_pair_loopback": line2}
+    # the same two ops with the LL63 wire format (the MPC_MODE_PAIR default): 33/32 wire bytes per
+    # payload byte instead of 2 -- the format whose bytes set a real pair's NVLink time
+    c2 = job.ctx(2, mode=m.binding.MODE_PAIR_LOOPBACK)
+    c2.set_exchange(1)
+    xs2 = c2.share(job.torch.from_numpy(workloads.softmax_inputs(rows, cols).ravel()).to(job.dev))
+    line3 = _op_line(job, c2, lambda: c2.softmax(xs2, rows, cols, out=z), rows * cols, flush, args,
+                     "cfg2 softmax, PAIR protocol in loopback, LL63 wire format")
+    g2 = c2.share(job.torch.from_numpy(workloads.normal_inputs(n3, 3)).to(job.dev))
+    line4 = _op_line(job, c2, lambda: c2.gelu(g2, form="poly_abs", degree=4, out=z2), n3, flush, args,
+                     "cfg3 GELU |x|-form deg 4, PAIR protocol in loopback, LL63 wire format")
+    return {"softmax_pair_loopback": line, "gelu_pair_loopback": line2, "softmax_pair_loopback_ll63": line3,
+            "gelu_pair_loopback_ll63": line4}
 
 
 # ------------------------------------------------------------------------ CPU oracle ----

@@ -123,6 +123,15 @@ mpc_status mpc_ctx_sync(mpc_ctx* ctx);
  * of the entry point, the step id and the op's step count) in one extra round; a mismatch marks
  * the context and mpc_ctx_sync returns MPC_ERR_PROTOCOL.  No effect in MPC_MODE_BOTH. */
 mpc_status mpc_ctx_set_debug(mpc_ctx* ctx, int on);
+/* PAIR exchange wire format (transport only -- openings, rounds and output shares are
+ * unchanged, reading R33): 0 = LL (each 8-byte payload word travels as two {half | round} words:
+ * 2 wire bytes per payload byte, fewest instructions; default in MPC_MODE_PAIR_LOOPBACK), 1 = LL63
+ * (one {63 payload bits | 1 tag bit} word per payload word plus one tagged top-bit word per warp and
+ * word: 33 / 32 wire bytes per payload byte; default in MPC_MODE_PAIR).  Both parties must use the
+ * same format.  Only before the context's first PAIR exchange (MPC_ERR_INVALID afterwards);
+ * MPC_ERR_RANGE for other values; no effect in MPC_MODE_BOTH. */
+mpc_status mpc_ctx_set_exchange(mpc_ctx* ctx, int fmt);
+int        mpc_ctx_get_exchange(const mpc_ctx* ctx);   /* current format, -1 for a NULL context */
 
 /* LTZ carry circuit: 0 = full Kogge-Stone (the S7 contract, default),
  * 1 = carry cone (only the carry into bit w-1: 94 AND gates at w = 33 instead of 290, same

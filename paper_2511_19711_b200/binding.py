@@ -99,6 +99,8 @@ _SIGS = {
     "mpc_open": [VP, Shares, i64, VP, VP, INT],
     "mpc_open_to": [VP, Shares, i64, INT, VP, VP, INT],
     "mpc_ctx_set_debug": [VP, INT],
+    "mpc_ctx_set_exchange": [VP, INT],
+    "mpc_ctx_get_exchange": [VP],
     "mpc_mul": [VP, Shares, Shares, Shares, i64, i64, INT],
     "mpc_square": [VP, Shares, Shares, i64, i64, INT],
     "mpc_mul_bcast": [VP, Shares, Shares, Shares, i64, i64, i64, i64, INT],
@@ -121,8 +123,15 @@ _SIGS = {
 }
 _RESTYPE = {"mpc_ctx_get_step": u64, "mpc_last_error": ctypes.c_char_p, "mpc_version": ctypes.c_char_p,
             "mpc_last_call_philox": u64}
-for _n, _a in _SIGS.items():
-    _f = getattr(_L, _n)
+_OPTIONAL = {"mpc_ctx_set_exchange", "mpc_ctx_get_exchange"}     # absent in older A/B builds (MPC200_LIB)
+for _n, _a in list(_SIGS.items()):
+    try:
+        _f = getattr(_L, _n)
+    except AttributeError:
+        if _n in _OPTIONAL and os.environ.get("MPC200_LIB"):
+            del _SIGS[_n]
+            continue
+        raise
     _f.argtypes = _a
     _f.restype = _RESTYPE.get(_n, INT)
 
@@ -231,6 +240,17 @@ class Ctx:
     def set_debug(self, on: bool = True):
         """PAIR modes: exchange and compare an op header before every op (MPC_ERR_PROTOCOL at sync)."""
         self._chk(_L.mpc_ctx_set_debug(self._h, int(on)), "mpc_ctx_set_debug")
+
+    def set_exchange(self, fmt: int):
+        """PAIR wire format: 0 = LL (2 wire bytes per payload byte), 1 = LL63 (33/32); same shares.
+        Only before the context's first exchange (both parties alike)."""
+        self._chk(_L.mpc_ctx_set_exchange(self._h, int(fmt)), "mpc_ctx_set_exchange")
+
+    @property
+    def exchange(self) -> int:
+        if "mpc_ctx_get_exchange" not in _SIGS:                 # an older A/B build: LL only
+            return 0
+        return int(_L.mpc_ctx_get_exchange(self._h))
 
     def set_ltz_circuit(self, circuit: int):
         """0 = Kogge-Stone (default, the S7 contract), 1 = carry cone (NEXT #1): same output shares."""

@@ -33,10 +33,12 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=(), split=False) -> str:
+    """split: nvcc --split-compile=0 (parallel device compilation, ~2.5x faster builds for
+    development; measured to cost 7-12 % kernel time, so the shipped library is built without)."""
     if out is None and not force and not stale():
         return LIB
-    cmd = [NVCC] + FLAGS + [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else []) + \
+    cmd = [NVCC] + FLAGS + (["--split-compile=0"] if split else []) + [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else []) + \
         ["-o", out or LIB] + sources()
     print("[mpc200] " + " ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)
@@ -46,4 +48,5 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
 if __name__ == "__main__":
     outs = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--out=")]
     defs = [a[2:] for a in sys.argv if a.startswith("-D")]
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else None, defines=defs)
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=outs[0] if outs else None, defines=defs,
+          split="--split" in sys.argv)

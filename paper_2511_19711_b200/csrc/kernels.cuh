@@ -38,6 +38,7 @@ struct PairA {
     int party;        // remote mode: this GPU's party
     int loopback;     // 1: both parties in one launch
     int G;            // CTAs per party
+    int fmt;          // exchange wire format (proto.cuh): 0 LL, 1 LL63
     XMem xm[2];       // exchange memory of party 0 / 1 (remote: xm[0] only)
     __device__ __forceinline__ PairP make(int& cta, int& ncta) const {
         PairP p;
@@ -47,6 +48,7 @@ struct PairA {
         else { p.pty = party; slot_cta = blockIdx.x; }
         cta = slot_cta; ncta = G;
         p.local = loopback;
+        p.fmt = fmt;
         p.bind(xm[loopback ? p.pty : 0], slot_cta * (blockDim.x >> 5) + (threadIdx.x >> 5));
         return p;
     }
@@ -117,7 +119,7 @@ constexpr int CG = 4;
 template <class PA, class Body>
 __global__ void __launch_bounds__(256, MPC_EW_MINB) k_groups_cone(const __grid_constant__ PA pa, i64 n, u64 off, Body body)
 {
-    __shared__ ConeSmem<CG> sm[8];
+    __shared__ ConeSmem<CG, Body::kNL> sm[8];
     extern __shared__ __align__(16) u64 stash[];       // per-warp staging (Body::kStash u64)
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
@@ -128,12 +130,13 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_groups_cone(const __grid_c
     pa.done(pr);
 }
 
-// cmp / relu with the carry-cone LTZ over CG groups per warp
+// cmp / relu with the carry-cone LTZ over CG groups per warp (NL = 32: w <= 33, 64: w <= 64)
+template <int NL>
 struct CmpConeBody {
-    static constexpr int kStash = 0;
+    static constexpr int kStash = 0, kNL = NL;
     u32 s; int w; SP x; SO z; int relu; i64 n;
     template <class P>
-    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG>& sm, u64*) const {
+    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG, NL>& sm, u64*) const {
         using S = typename P::S;
         S xv[CG], l[CG];
 #pragma unroll
@@ -141,7 +144,7 @@ struct CmpConeBody {
             const i64 i = (gb + g) * 32 + lane;
             xv[g] = i < n ? pr.ld(x, i) : pr.zero();
         }
-        pr.template ltz_cone<CG>((off >> 5) + (u64)gb, s, w, xv, l, lane, sm);
+        pr.template ltz_cone<CG, NL>((off >> 5) + (u64)gb, s, w, xv, l, lane, sm);
 #pragma unroll
         for (int g = 0; g < CG; ++g) {
             const i64 i = (gb + g) * 32 + lane;
@@ -157,16 +160,17 @@ struct CmpConeBody {
 // pairs (2p, 2p+1), one c0 block per pair, two independent Beaver chains per thread (act_tail2).
 // Same step ids, units and output bits as act_group.  (The same body with Kogge-Stone LTZs per
 // group measured 10 % slower than ActBody, so the Kogge-Stone path keeps the group layout.)
+template <int NL>
 struct ActConeBody {
-    static constexpr int kStash = 3 * CG * 32 * 2;      // [3 ltz][CG][32 lanes][2 words]
+    static constexpr int kStash = 3 * CG * 32 * 2, kNL = NL;      // [3 ltz][CG][32 lanes][2 words]
     u32 s; ActK p; SP x; SO z; i64 n;
     template <class P>
     __device__ __forceinline__ void ltzs(P& pr, u64 q0, u32 sl, typename P::S (&in)[CG], typename P::S (&out)[CG],
-                                         int lane, ConeSmem<CG>& sm) const {
-        pr.template ltz_cone<CG>(q0, sl, p.w, in, out, lane, sm);
+                                         int lane, ConeSmem<CG, NL>& sm) const {
+        pr.template ltz_cone<CG, NL>(q0, sl, p.w, in, out, lane, sm);
     }
     template <class P>
-    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG>& sm, u64* st) const {
+    __device__ void operator()(P& pr, u64 off, i64 gb, int lane, ConeSmem<CG, NL>& sm, u64* st) const {
         using S = typename P::S;
         static_assert(sizeof(S) <= 16, "stash holds up to two words per share");
         S xv[CG], t[CG];
@@ -231,16 +235,13 @@ struct SquareBody {
         S xa[V], xb[V], za[V], zb[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            xa[v] = xb[v] = pr.zero();
-            if (ok[v] && i0[v] >= 0) xa[v] = pr.ld(x, i0[v]);
-            if (ok[v] && i0[v] + 1 < n) xb[v] = pr.ld(x, i0[v] + 1);
+            pr.ld_pair(x, i0[v], ok[v] && i0[v] >= 0, ok[v] && i0[v] + 1 < n, xa[v], xb[v]);
         }
         pr.template sq2v<V>(u, s, xa, xb, za, zb);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             if (tb) { za[v] = pr.shr_(za[v], tb); zb[v] = pr.shr_(zb[v], tb); }
-            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], za[v]);
-            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, zb[v]);
+            pr.st_pair(z, i0[v], ok[v] && i0[v] >= 0, ok[v] && i0[v] + 1 < n, za[v], zb[v]);
         }
     }
 };
@@ -253,16 +254,15 @@ struct MulBody {
         S xa[V], ya[V], xb[V], yb[V], za[V], zb[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            xa[v] = ya[v] = xb[v] = yb[v] = pr.zero();
-            if (ok[v] && i0[v] >= 0) { xa[v] = pr.ld(x, i0[v]); ya[v] = pr.ld(y, i0[v]); }
-            if (ok[v] && i0[v] + 1 < n) { xb[v] = pr.ld(x, i0[v] + 1); yb[v] = pr.ld(y, i0[v] + 1); }
+            const bool va = ok[v] && i0[v] >= 0, vb = ok[v] && i0[v] + 1 < n;
+            pr.ld_pair(x, i0[v], va, vb, xa[v], xb[v]);
+            pr.ld_pair(y, i0[v], va, vb, ya[v], yb[v]);
         }
         pr.template bm2v<V>(u, s, xa, ya, xb, yb, za, zb);
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             if (tb) { za[v] = pr.shr_(za[v], tb); zb[v] = pr.shr_(zb[v], tb); }
-            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], za[v]);
-            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, zb[v]);
+            pr.st_pair(z, i0[v], ok[v] && i0[v] >= 0, ok[v] && i0[v] + 1 < n, za[v], zb[v]);
         }
     }
 };
@@ -300,17 +300,12 @@ struct ExpPairBody {
         typename P::S a[V], b[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            a[v] = b[v] = pr.zero();
-            if (ok[v] && i0[v] >= 0) a[v] = pr.ld(x, i0[v]);
-            if (ok[v] && i0[v] + 1 < n) b[v] = pr.ld(x, i0[v] + 1);
+            pr.ld_pair(x, i0[v], ok[v] && i0[v] >= 0, ok[v] && i0[v] + 1 < n, a[v], b[v]);
         }
         if (sq_only) exp_squarings_pairv<V>(pr, u, s, p, a, b);
         else exp_pairv<V>(pr, u, s, p, a, b);
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], a[v]);
-            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, b[v]);
-        }
+        for (int v = 0; v < V; ++v) pr.st_pair(z, i0[v], ok[v] && i0[v] >= 0, ok[v] && i0[v] + 1 < n, a[v], b[v]);
     }
 };
 
@@ -336,17 +331,12 @@ struct NrPairBody {
         typename P::S a[V], b[V], ya[V], yb[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            a[v] = b[v] = pr.zero();
-            if (ok[v] && i0[v] >= 0) a[v] = pr.ld(x, i0[v]);
-            if (ok[v] && i0[v] + 1 < n) b[v] = pr.ld(x, i0[v] + 1);
+            pr.ld_pair(x, i0[v], ok[v] && i0[v] >= 0, ok[v] && i0[v] + 1 < n, a[v], b[v]);
         }
         if (KIND == 0) recip_pairv<V>(pr, u, s, p, a, b, ya, yb);
         else rsqrt_pairv<V>(pr, u, s, p, a, b, ya, yb);
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], ya[v]);
-            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, yb[v]);
-        }
+        for (int v = 0; v < V; ++v) pr.st_pair(z, i0[v], ok[v] && i0[v] >= 0, ok[v] && i0[v] + 1 < n, ya[v], yb[v]);
     }
 };
 
@@ -412,7 +402,8 @@ struct HdrBody {
 // cone: the level's LTZs use the carry-cone circuit, CG groups per warp (ltz_cone.cuh).
 template <bool WIDE, bool CONE, class P, bool CAUSAL = false>
 __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i64 cols, int R, u64 g0,
-                                         SO A, SO B, i64 HA, i64 HB, SO mx, ConeSmem<CG>* cone, u64 cL = 0)
+                                         SO A, SO B, i64 HA, i64 HB, SO mx, ConeSmem<CG, WIDE ? 64 : 32>* cone,
+                                         u64 cL = 0)
 {
     using S = typename P::S;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
@@ -432,6 +423,15 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
         }
         return pr.ld(cur, rr * li + col);
     };
+    // Warp-local levels: warp w owns rows [w rw, (w+1) rw) (rw = 32 / NW = 4).  When rw h is a
+    // multiple of 32 (h % 8 == 0: every level of 128-wide rows down to h = 8, i.e. 120 of a tile's 127
+    // comparison groups) the warp's units are whole LTZ groups of its own rows, so the level needs
+    // no CTA barrier -- only the levels whose groups span warps (h = 4, 2, 1) synchronize the CTA.
+    const int rw = 32 / NW;
+#ifndef MPC_MAX_WARP_LOCAL
+#define MPC_MAX_WARP_LOCAL 0   // measured 2 % slower on cfg2 (tools/ab_ops_quick.py, r02)
+#endif
+    auto warp_local = [&](i64 hh) { return MPC_MAX_WARP_LOCAL && 32 % NW == 0 && ((i64)rw * hh) % 32 == 0; };
     while (m > 1) {
         const i64 h = m / 2, mn = h + (m & 1);
         SO o; i64 lo;
@@ -441,24 +441,26 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
         const u32 sl = s + 2u * (u32)lv;
         const u64 ubase = g0 * (u64)h;                 // multiple of 32 (g0 is)
         const FastDiv dh = make_fastdiv((u32)h);
-        if constexpr (!WIDE && CONE) {
-            const i64 nb = (h + CG - 1) / CG;
-            for (i64 b = warp; b < nb; b += NW) {
+        const bool wl = warp_local(h);
+        const i64 gpw = (i64)rw * h / 32;              // groups per warp when warp-local
+        const i64 gend = wl ? (warp + 1) * gpw : h;    // 32*h units = h groups per tile
+        if constexpr (CONE) {
+            for (i64 gb = wl ? warp * gpw : (i64)warp * CG; gb < gend; gb += wl ? CG : (i64)NW * CG) {
                 S d[CG], l[CG];
 #pragma unroll
                 for (int g = 0; g < CG; ++g) {
-                    const i64 v = (b * CG + g) * 32 + lane;
+                    const i64 v = (gb + g) * 32 + lane;
                     d[g] = pr.zero();
-                    if (b * CG + g < h && v < (i64)R * h) {
+                    if (gb + g < gend && v < (i64)R * h) {
                         const i64 rr = fdiv((u32)v, dh), i = v - rr * h;
                         d[g] = pr.sub(ldc(rr, i), ldc(rr, i + h));
                     }
                 }
-                pr.template ltz_cone<CG>((ubase >> 5) + (u64)(b * CG), sl, w, d, l, lane, cone[warp]);
+                pr.template ltz_cone<CG, WIDE ? 64 : 32>((ubase >> 5) + (u64)gb, sl, w, d, l, lane, cone[warp]);
 #pragma unroll
                 for (int g = 0; g < CG; ++g) {
-                    const i64 v = (b * CG + g) * 32 + lane;
-                    const bool valid = b * CG + g < h && v < (i64)R * h;
+                    const i64 v = (gb + g) * 32 + lane;
+                    const bool valid = gb + g < gend && v < (i64)R * h;
                     i64 rr = 0, i = 0;
                     S y = pr.zero();
                     if (valid) { rr = fdiv((u32)v, dh); i = v - rr * h; y = ldc(rr, i + h); }
@@ -469,32 +471,28 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
                     }
                 }
             }
-            __syncthreads();
-            cur = SP{{o.p[0], o.p[1]}};
-            li = lo;
-            m = mn;
-            ++lv;
-            continue;
-        }
-        for (i64 g = warp; g < h; g += NW) {            // 32*h units = h groups
-            const i64 v = g * 32 + lane;
-            const bool valid = v < (i64)R * h;
-            i64 rr = 0, i = 0;
-            S d = pr.zero(), y = pr.zero();
-            if (valid) {
-                rr = fdiv((u32)v, dh); i = v - rr * h;
-                y = ldc(rr, i + h);
-                d = pr.sub(ldc(rr, i), y);
-            }
-            const u64 q = (ubase >> 5) + (u64)g;
-            const S c = pr.notb(pr.template ltz_o<WIDE>(q, sl, w, d, lane));
-            const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
-            if (valid) {
-                pr.st(o, rr * lo + i, sel);
-                if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, ldc(rr, m - 1));
+        } else {
+            for (i64 g = wl ? warp * gpw : warp; g < gend; g += wl ? 1 : NW) {
+                const i64 v = g * 32 + lane;
+                const bool valid = v < (i64)R * h;
+                i64 rr = 0, i = 0;
+                S d = pr.zero(), y = pr.zero();
+                if (valid) {
+                    rr = fdiv((u32)v, dh); i = v - rr * h;
+                    y = ldc(rr, i + h);
+                    d = pr.sub(ldc(rr, i), y);
+                }
+                const u64 q = (ubase >> 5) + (u64)g;
+                const S c = pr.notb(pr.template ltz_o<WIDE>(q, sl, w, d, lane));
+                const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
+                if (valid) {
+                    pr.st(o, rr * lo + i, sel);
+                    if ((m & 1) && i == h - 1) pr.st(o, rr * lo + h, ldc(rr, m - 1));
+                }
             }
         }
-        __syncthreads();
+        if (wl && mn > 1 && warp_local(mn / 2)) __syncwarp();   // next level reads only this warp's rows
+        else __syncthreads();
         cur = SP{{o.p[0], o.p[1]}};
         li = lo;
         m = mn;
@@ -601,14 +599,15 @@ __host__ __device__ inline i64 softmax_work_u64(i64 cols, bool esmem = false)
     return softmax_x_off(cols, esmem) + 9 * 32;
 }
 
-// LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33) --
-// separate instantiations so the cone's registers / shared memory do not cost the others occupancy
+// LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33), 3 carry cone
+// wide (w <= 64) -- separate instantiations so the cone's registers / shared memory do not cost the
+// others occupancy
 template <int LV, class PA, bool CAUSAL = false>
 __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM_MINB) k_softmax(const __grid_constant__ PA pa, SoftmaxArgs a)
 {
-    constexpr bool WIDE = LV == 1, CONE = LV == 2;
+    constexpr bool WIDE = LV == 1 || LV == 3, CONE = LV >= 2;
     extern __shared__ __align__(16) u64 smem[];
-    __shared__ ConeSmem<CG> cone_sm[CONE ? MPC_ROW_TPB / 32 : 1];
+    __shared__ ConeSmem<CG, WIDE ? 64 : 32> cone_sm[CONE ? MPC_ROW_TPB / 32 : 1];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     using S = typename decltype(pr)::S;
@@ -682,16 +681,15 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
                 for (int v = 0; v < V; ++v) {
                     const i64 e = 2 * (base + lane + 32 * v);
                     uv[v] = ub + (u64)e;
-                    da[v] = db[v] = pr.zero();
-                    if (e < ne) da[v] = pr.sub(pr.ld(xt, e), pr.ld(MXc, fdiv((u32)e, dC)));
-                    if (e + 1 < ne) db[v] = pr.sub(pr.ld(xt, e + 1), pr.ld(MXc, fdiv((u32)(e + 1), dC)));
+                    pr.ld_pair(xt, e, e < ne, e + 1 < ne, da[v], db[v]);      // 16-byte loads (row pairs)
+                    if (e < ne) da[v] = pr.sub(da[v], pr.ld(MXc, fdiv((u32)e, dC)));
+                    if (e + 1 < ne) db[v] = pr.sub(db[v], pr.ld(MXc, fdiv((u32)(e + 1), dC)));
                 }
                 exp_pairv<V>(pr, uv, a.s_exp, a.ek, da, db);
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     const i64 e = 2 * (base + lane + 32 * v);
-                    if (e < ne) pr.st(E, e, da[v]);
-                    if (e + 1 < ne) pr.st(E, e + 1, db[v]);
+                    pr.st_pair(E, e, e < ne, e + 1 < ne, da[v], db[v]);
                 }
             }
         }
@@ -732,16 +730,16 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
                 for (int v = 0; v < V; ++v) {
                     const i64 e = 2 * (base + lane + 32 * v);
                     uv[v] = ub + (u64)e;
-                    ea[v] = eb[v] = ra[v] = rb[v] = pr.zero();
-                    if (e < ne) { ea[v] = pr.ld(Ec, e); ra[v] = pr.ld(Rc, fdiv((u32)e, dC)); }
-                    if (e + 1 < ne) { eb[v] = pr.ld(Ec, e + 1); rb[v] = pr.ld(Rc, fdiv((u32)(e + 1), dC)); }
+                    ra[v] = rb[v] = pr.zero();
+                    pr.ld_pair(Ec, e, e < ne, e + 1 < ne, ea[v], eb[v]);
+                    if (e < ne) ra[v] = pr.ld(Rc, fdiv((u32)e, dC));
+                    if (e + 1 < ne) rb[v] = pr.ld(Rc, fdiv((u32)(e + 1), dC));
                 }
                 pr.template bm2v<V>(uv, a.s_mul, ea, ra, eb, rb, za, zb);
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
                     const i64 e = 2 * (base + lane + 32 * v);
-                    if (e < ne) pr.st(zt, e, pr.shr_(za[v], FRAC));
-                    if (e + 1 < ne) pr.st(zt, e + 1, pr.shr_(zb[v], FRAC));
+                    pr.st_pair(zt, e, e < ne, e + 1 < ne, pr.shr_(za[v], FRAC), pr.shr_(zb[v], FRAC));
                 }
             }
         }
@@ -769,9 +767,9 @@ __host__ __device__ inline i64 max_work_u64(i64 cols)
 template <int LV, class PA>   // LV as k_softmax
 __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM_MINB) k_max(const __grid_constant__ PA pa, MaxArgs a)
 {
-    constexpr bool WIDE = LV == 1, CONE = LV == 2;
+    constexpr bool WIDE = LV == 1 || LV == 3, CONE = LV >= 2;
     extern __shared__ __align__(16) u64 smem[];
-    __shared__ ConeSmem<CG> cone_sm[CONE ? MPC_ROW_TPB / 32 : 1];
+    __shared__ ConeSmem<CG, WIDE ? 64 : 32> cone_sm[CONE ? MPC_ROW_TPB / 32 : 1];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
@@ -814,6 +812,7 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_bmb_rows(const __grid_cons
 }
 struct BmbBody {
     u32 s; SP x; SO z; i64 n; FastDiv dC; const u64* br; i64 rows; int tb; int loop;
+    SP mu; int has_mu;      // LayerNorm: the left operand is x - mu[row] (k_ln_stats' means)
     template <int V, class P>
     __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
         using S = typename P::S;
@@ -822,8 +821,8 @@ struct BmbBody {
             const bool va = ok[v] && i0[v] >= 0, vb = ok[v] && i0[v] + 1 < n;
             S xa = pr.zero(), xb = pr.zero();
             i64 ra = 0, rb = 0;
-            if (va) { ra = fdiv((u32)i0[v], dC); xa = pr.ld(x, i0[v]); }
-            if (vb) { rb = fdiv((u32)(i0[v] + 1), dC); xb = pr.ld(x, i0[v] + 1); }
+            if (va) { ra = fdiv((u32)i0[v], dC); xa = pr.ld(x, i0[v]); if (has_mu) xa = pr.sub(xa, pr.ld(mu, ra)); }
+            if (vb) { rb = fdiv((u32)(i0[v] + 1), dC); xb = pr.ld(x, i0[v] + 1); if (has_mu) xb = pr.sub(xb, pr.ld(mu, rb)); }
             const u64* bp = br + (loop && pr.party() > 0 ? 3 * rows : 0);   // loopback: party 1's records
             const BRow b0{bp[ra], bp[rows + ra], bp[2 * rows + ra]}, b1{bp[rb], bp[rows + rb], bp[2 * rows + rb]};
             S za, zb;
@@ -850,9 +849,10 @@ struct MaxSmallArgs {
 template <int LV, class PA>
 __global__ void __launch_bounds__(256, MPC_EW_MINB) k_max_small(const __grid_constant__ PA pa, MaxSmallArgs a)
 {
-    constexpr bool WIDE = LV == 1, CONE = LV == 2;
+    constexpr bool WIDE = LV == 1 || LV == 3, CONE = LV >= 2;
+    constexpr int NL = WIDE ? 64 : 32;
     extern __shared__ __align__(16) u64 smem[];                 // per warp: 2 parties x 32 rows x cols
-    __shared__ ConeSmem<CG> cone_sm[CONE ? 8 : 1];
+    __shared__ ConeSmem<CG, NL> cone_sm[CONE ? 8 : 1];
     int cta, ncta;
     auto pr = pa.make(cta, ncta);
     using S = typename decltype(pr)::S;
@@ -909,14 +909,14 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_max_small(const __grid_con
                     const u64 q = (ubase >> 5) + (u64)b;
                     if (ng == 1) {
                         S d1[1] = {d[0]}, l1[1];
-                        pr.template ltz_cone<1>(q, sl, a.w, d1, l1, lane, *reinterpret_cast<ConeSmem<1>*>(&cone_sm[warp]));
+                        pr.template ltz_cone<1, NL>(q, sl, a.w, d1, l1, lane, *reinterpret_cast<ConeSmem<1, NL>*>(&cone_sm[warp]));
                         l[0] = l1[0];
                     } else if (ng == 2) {
                         S d2[2] = {d[0], d[1]}, l2[2];
-                        pr.template ltz_cone<2>(q, sl, a.w, d2, l2, lane, *reinterpret_cast<ConeSmem<2>*>(&cone_sm[warp]));
+                        pr.template ltz_cone<2, NL>(q, sl, a.w, d2, l2, lane, *reinterpret_cast<ConeSmem<2, NL>*>(&cone_sm[warp]));
                         l[0] = l2[0]; l[1] = l2[1];
                     } else {
-                        pr.template ltz_cone<CG>(q, sl, a.w, d, l, lane, cone_sm[warp]);
+                        pr.template ltz_cone<CG, NL>(q, sl, a.w, d, l, lane, cone_sm[warp]);
                     }
 #pragma unroll
                     for (int g = 0; g < CG; ++g) {
@@ -1035,6 +1035,186 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln(const __grid_co
             }
         }
         __syncthreads();
+    }
+    pa.done(pr);
+}
+
+// LAYERNORM as three launches (rsqrt without clamp; DESIGN.md 2.5 / 6):
+//  k_ln_stats : warp per row -- mu = mean(x) (x E(1/d) or floor / d), v = mean(MT(c, c)) + eps,
+//               element units (unit pairs over the row), step s_sq; writes mu, v per row
+//  RSQRT      : the element-wise Newton-Raphson kernel over the rows (k_pairs<NrPairBody<1>>,
+//               row units g = row_off + r, steps s_rs..) -- a short latency-bound launch instead of
+//               one warp per 32-row tile holding seven warps at a barrier
+//  LnOutBody  : out = MT(x - mu, r) on element unit pairs (step s_mul), perfectly balanced
+// Same steps, units and output bits as k_ln (tests compare both against the oracle).
+struct LnStatsArgs { u32 s_sq; SP x; SO mu; SO var; i64 rows, cols; u64 row_off; int mean_mode; u64 e_invd, e_eps; };
+template <class PA>
+__global__ void __launch_bounds__(256, MPC_EW_MINB) k_ln_stats(const __grid_constant__ PA pa, LnStatsArgs a)
+{
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using S = typename decltype(pr)::S;
+    const int lane = threadIdx.x & 31, NW = blockDim.x >> 5;
+    const i64 C = a.cols;
+    for (i64 r = (i64)cta * NW + (threadIdx.x >> 5); r < a.rows; r += (i64)ncta * NW) {
+        const SP xr{{a.x.p[0] ? a.x.p[0] + r * C : nullptr, a.x.p[1] ? a.x.p[1] + r * C : nullptr}};
+        S acc = pr.zero();
+        for (i64 j = lane; j < C; j += 32) acc = pr.add(acc, pr.ld(xr, j));
+        S mu = pr.sumw(acc);
+        mu = a.mean_mode == 0 ? pr.mulf(mu, a.e_invd) : pr.divp(mu, C);
+        S qs = pr.zero();
+        const u64 ub = (a.row_off + (u64)r) * (u64)C;
+        const i64 j0 = -(i64)(ub & 1);
+        for (i64 j = j0 + 2 * lane, jb = j0; jb < C; j += 64, jb += 64) {
+            const bool va = j >= 0 && j < C, vb = j + 1 >= 0 && j + 1 < C;
+            S ca = pr.zero(), cb = pr.zero();
+            if (va) ca = pr.sub(pr.ld(xr, j), mu);
+            if (vb) cb = pr.sub(pr.ld(xr, j + 1), mu);
+            S za, zb;
+            pr.bm2(ub + (u64)j, a.s_sq, ca, ca, cb, cb, za, zb);
+            if (va) qs = pr.add(qs, pr.shr_(za, FRAC));
+            if (vb) qs = pr.add(qs, pr.shr_(zb, FRAC));
+        }
+        S v = pr.sumw(qs);
+        v = a.mean_mode == 0 ? pr.mulf(v, a.e_invd) : pr.divp(v, C);
+        v = pr.addp(v, a.e_eps);
+        if (lane == 0) { pr.st(a.mu, r, mu); pr.st(a.var, r, v); }
+    }
+    pa.done(pr);
+}
+struct LnOutBody {
+    u32 s; SP x; SO z; i64 n; FastDiv dC; SP mu; SP rs;
+    template <int V, class P>
+    __device__ void run(P& pr, const u64 (&u)[V], const i64 (&i0)[V], const bool (&ok)[V]) const {
+        using S = typename P::S;
+        S ca[V], cb[V], ra[V], rb[V], za[V], zb[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            ca[v] = cb[v] = ra[v] = rb[v] = pr.zero();
+            if (ok[v] && i0[v] >= 0) {
+                const i64 r = fdiv((u32)i0[v], dC);
+                ca[v] = pr.sub(pr.ld(x, i0[v]), pr.ld(mu, r)); ra[v] = pr.ld(rs, r);
+            }
+            if (ok[v] && i0[v] + 1 < n) {
+                const i64 r = fdiv((u32)(i0[v] + 1), dC);
+                cb[v] = pr.sub(pr.ld(x, i0[v] + 1), pr.ld(mu, r)); rb[v] = pr.ld(rs, r);
+            }
+        }
+        pr.template bm2v<V>(u, s, ca, ra, cb, rb, za, zb);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (ok[v] && i0[v] >= 0) pr.st(z, i0[v], pr.shr_(za[v], FRAC));
+            if (ok[v] && i0[v] + 1 < n) pr.st(z, i0[v] + 1, pr.shr_(zb[v], FRAC));
+        }
+    }
+};
+
+// LAYERNORM, warp-granular (rsqrt without clamp: no LTZ, so row units need no 32-row grouping).
+// A warp owns a QUAD of 4 consecutive rows (4-aligned global rows, so the rsqrt unit pairs (2p, 2p+1)
+// are aligned) and runs the whole schedule on them with no CTA barrier: mean and sum MT(c, c) per
+// row (element units, unit pairs over the row), RSQRT over the quad's rows (lanes 0-1 hold the two
+// unit pairs; every lane runs the chain, so it costs one warp's issue, not 8 warps' barrier wait),
+// then the final MT(c, r) (element units).  Same steps, units and output bits as k_ln.  Persistent
+// over quads (8192 rows = 2048 quads, one wave of 2048 warps for cfg5).
+template <bool WIDE, class PA>
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_quad(const __grid_constant__ PA pa, LnArgs a)
+{
+    __shared__ u64 RSH[MPC_ROW_TPB / 32][2][4];          // per warp: r of the quad's rows (per party)
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using S = typename decltype(pr)::S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const i64 C = a.cols;
+    const i64 nq = (a.rows + 3) / 4;
+    const FastDiv dC = make_fastdiv((u32)C);
+    const SO RSo{{RSH[warp][0], RSH[warp][1]}};
+    const SP RSc{{RSH[warp][0], RSH[warp][1]}};
+    for (i64 Q = (i64)cta * NW + warp; Q < nq; Q += (i64)ncta * NW) {
+        const i64 r0 = 4 * Q;
+        const int R = (int)min((i64)4, a.rows - r0);
+        const u64 g0 = a.row_off + (u64)r0;                           // global row of the quad (4-aligned)
+        const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        S mu[4], var[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+            mu[rr] = var[rr] = pr.zero();
+            if (rr >= R) continue;                                   // warp-uniform
+            S acc = pr.zero();
+            for (i64 j = lane; j < C; j += 32) acc = pr.add(acc, pr.ld(xt, rr * C + j));
+            S m = pr.sumw(acc);
+            m = a.mean_mode == 0 ? pr.mulf(m, a.e_invd) : pr.divp(m, C);
+            // q = MT(c, c) over the row, element units; lanes take unit pairs (2j, 2j+1)
+            S qs = pr.zero();
+            const u64 ub = (g0 + (u64)rr) * (u64)C;
+            const i64 j0 = -(i64)(ub & 1);
+            for (i64 j = j0 + 2 * lane, jb = j0; jb < C; j += 64, jb += 64) {
+                const bool va = j >= 0 && j < C, vb = j + 1 >= 0 && j + 1 < C;
+                S ca = pr.zero(), cb = pr.zero();
+                if (va) ca = pr.sub(pr.ld(xt, rr * C + j), m);
+                if (vb) cb = pr.sub(pr.ld(xt, rr * C + j + 1), m);
+                S za, zb;
+                pr.bm2(ub + (u64)j, a.s_sq, ca, ca, cb, cb, za, zb);
+                if (va) qs = pr.add(qs, pr.shr_(za, FRAC));
+                if (vb) qs = pr.add(qs, pr.shr_(zb, FRAC));
+            }
+            S v = pr.sumw(qs);
+            v = a.mean_mode == 0 ? pr.mulf(v, a.e_invd) : pr.divp(v, C);
+            mu[rr] = m;
+            var[rr] = pr.addp(v, a.e_eps);
+        }
+        {   // RSQRT of the quad's rows: lane p (0, 1) <-> unit pair (g0 + 2p, g0 + 2p + 1)
+            const int p = lane & 1;
+            S y0, y1;
+            rsqrt_pair(pr, g0 + 2u * (u64)p, a.s_rs, a.rk, p ? var[2] : var[0], p ? var[3] : var[1], y0, y1);
+            if (lane < 2) { pr.st(RSo, 2 * lane, y0); pr.st(RSo, 2 * lane + 1, y1); }
+        }
+        __syncwarp();
+        const i64 ne = (i64)R * C;
+        const u64 ub = g0 * (u64)C;                                  // even: g0 is a multiple of 4
+        const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
+        auto cval = [&](i64 e, int r) {
+            const S m = r == 0 ? mu[0] : r == 1 ? mu[1] : r == 2 ? mu[2] : mu[3];
+            return pr.sub(pr.ld(xt, e), m);
+        };
+        if (a.bcast) {                                              // broadcast triple (NEXT #2)
+            const S yr = lane < R ? pr.ld(RSc, lane) : pr.zero();
+            const BRow br = pr.bmb_row(g0 + (u64)lane, a.s_mul, yr);   // lanes >= 4: unused rows
+            for (i64 base = 0; base < (ne + 1) / 2; base += 32) {
+                const i64 e = 2 * (base + lane);
+                S xa = pr.zero(), xb = pr.zero();
+                int ra = 0, rb = 0;
+                if (e < ne) { ra = (int)fdiv((u32)e, dC); xa = cval(e, ra); }
+                if (e + 1 < ne) { rb = (int)fdiv((u32)(e + 1), dC); xb = cval(e + 1, rb); }
+                const BRow b0{__shfl_sync(FULL, br.b0, ra), __shfl_sync(FULL, br.b1, ra), __shfl_sync(FULL, br.f, ra)};
+                const BRow b1{__shfl_sync(FULL, br.b0, rb), __shfl_sync(FULL, br.b1, rb), __shfl_sync(FULL, br.f, rb)};
+                S za, zb;
+                pr.bmb2(ub + (u64)e, a.s_mul, xa, xb, b0, b1, za, zb);
+                if (e < ne) pr.st(zt, e, pr.shr_(za, FRAC));
+                if (e + 1 < ne) pr.st(zt, e + 1, pr.shr_(zb, FRAC));
+            }
+        } else {
+            constexpr int V = decltype(pr)::kV;
+            for (i64 base = 0; base < (ne + 1) / 2; base += 32 * V) {
+                u64 uv[V];
+                S ca[V], cb[V], ra[V], rb[V], za[V], zb[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    uv[v] = ub + (u64)e;
+                    ca[v] = cb[v] = ra[v] = rb[v] = pr.zero();
+                    if (e < ne) { const int r = (int)fdiv((u32)e, dC); ca[v] = cval(e, r); ra[v] = pr.ld(RSc, r); }
+                    if (e + 1 < ne) { const int r = (int)fdiv((u32)(e + 1), dC); cb[v] = cval(e + 1, r); rb[v] = pr.ld(RSc, r); }
+                }
+                pr.template bm2v<V>(uv, a.s_mul, ca, ra, cb, rb, za, zb);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 e = 2 * (base + lane + 32 * v);
+                    if (e < ne) pr.st(zt, e, pr.shr_(za[v], FRAC));
+                    if (e + 1 < ne) pr.st(zt, e + 1, pr.shr_(zb[v], FRAC));
+                }
+            }
+        }
+        __syncwarp();
     }
     pa.done(pr);
 }

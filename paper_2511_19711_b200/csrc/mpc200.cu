@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <vector>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>      // header-only NVTX3: no-ops unless a tool (nsys / ncu) is attached
 
 #include "mpc200.h"
 #include "kernels.cuh"
@@ -35,7 +36,7 @@ struct TimingRec { const char* name; cudaEvent_t a, b; u64 philox_at; u64 philox
 struct XAlloc {
     void* base;
     size_t bytes;
-    u64 rx_off, flag_off, round_off, err_off;
+    u64 rx_off, flag_off, round_off, tags_off, err_off;
 };
 
 struct mpc_ctx {
@@ -63,6 +64,9 @@ struct mpc_ctx {
     int circuit;            // LTZ carry circuit: 0 Kogge-Stone, 1 carry cone (2.7)
     int mm_engine;          // mpc_matmul ring GEMM: 0 auto, 1 SIMT, 2 tensor cores
     struct HostIO* hio;     // pipelined host-buffer execution (mpc_softmax_hostio), lazily created
+    int nvtx_open;          // an op-level NVTX range is open (begin_op .. finish)
+    int xfmt;               // PAIR exchange wire format (proto.cuh): 0 LL, 1 LL63
+    int xused;              // a PAIR exchange kernel has been launched (the format is then fixed)
 };
 
 // Pipelined host-buffer execution: chunk i goes H2D on `h2d`, computes on cs[i % HIO_SLOTS] with its
@@ -107,8 +111,28 @@ static void rec_close(mpc_ctx* c)
         if (r.philox == ~0ull) r.philox = c->last_philox - r.philox_at;
     }
 }
+// NVTX ranges (SURVEY 5 tracing): every compute entry point opens an op range in begin_op (named
+// after the ABI function) that finish / the next op closes, and every kernel launch is a nested
+// range named after its kernel family; nsys / ncu --nvtx show the per-op and per-launch timeline.
+static nvtxDomainHandle_t nvtx_domain()
+{
+    static nvtxDomainHandle_t d = nvtxDomainCreateA("mpc200");
+    return d;
+}
+static void nvtx_push(const char* name)
+{
+    nvtxEventAttributes_t ev{};
+    ev.version = NVTX_VERSION;
+    ev.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    ev.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    ev.message.ascii = name;
+    nvtxDomainRangePushEx(nvtx_domain(), &ev);
+}
+static void nvtx_pop() { nvtxDomainRangePop(nvtx_domain()); }
+
 static void rec_begin(mpc_ctx* c, const char* name, u64 units)
 {
+    nvtx_push(name);
     if (!c->timing) return;
     rec_close(c);
     if (c->nrec == c->caprec) {
@@ -122,6 +146,7 @@ static void rec_begin(mpc_ctx* c, const char* name, u64 units)
 static void rec_end(mpc_ctx* c)
 {
     if (c->timing && c->nrec > 0) cudaEventRecord(c->recs[c->nrec - 1].b, c->stream);
+    nvtx_pop();
 }
 
 // grow-only scratch, stream-ordered on the ctx stream (reused by every row op)
@@ -189,7 +214,8 @@ static void acct_bcast(mpc_ctx* c, u64 n, u64 rows)
     c->st.bytes_per_party += 8 * n + 8 * rows;
     c->st.rounds += 2;
 }
-static bool use_cone(const mpc_ctx* c, int w) { return c->circuit == 1 && w <= 33; }
+// the pruned carry cone (ltz_cone.cuh) covers every window 1..64: 32 leaf positions for w <= 33, 64 above
+static bool use_cone(const mpc_ctx* c, int w) { (void)w; return c->circuit == 1; }
 static void acct_ltz(mpc_ctx* c, u64 n, int w)
 {
     const u64 groups = (n + 31) / 32;
@@ -278,6 +304,7 @@ static XMem xmem_of(const mpc_ctx* c, int which)
     char* b = (char*)a.base;
     XMem m;
     m.rx = (u64*)(b + a.rx_off); m.flag = (u64*)(b + a.flag_off); m.round = (u64*)(b + a.round_off);
+    m.tags = (u32*)(b + a.tags_off);
     m.err = (int*)(b + a.err_off); m.slots = c->slots;
     if (is_loop(c)) {
         const XAlloc& o = c->xa[1 - which];
@@ -297,6 +324,7 @@ static PairA pair_args(const mpc_ctx* c, int G)
     pa.party = c->cfg.party;
     pa.loopback = is_loop(c) ? 1 : 0;
     pa.G = G;
+    pa.fmt = c->xfmt;
     pa.xm[0] = xmem_of(c, 0);
     pa.xm[1] = is_loop(c) ? xmem_of(c, 1) : pa.xm[0];
     return pa;
@@ -328,6 +356,7 @@ static mpc_status launch_pair_kernel_tpb(mpc_ctx* c, Kern kern, int G, size_t dy
 {
     if (!is_loop(c) && !c->connected) return fail(c, MPC_ERR_INVALID, "%s: PAIR context not connected", name);
     PairA pa = pair_args(c, G);
+    c->xused = 1;
     void* argv[] = {(void*)&pa, (void*)&args...};
     const int grid = G * (is_loop(c) ? 2 : 1);
     rec_begin(c, name, 0);
@@ -459,6 +488,7 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
 static mpc_status launch_max(mpc_ctx* c, MaxArgs& a, i64 rows, i64 cols, int w, const char* name)
 {
     const i64 wk = max_work_u64(cols);
+    if (a.cone && w > 33) return launch_rows(c, k_max<3, BothA>, k_max<3, PairA>, a, rows, wk, 0, name);
     if (w > 33) return launch_rows(c, k_max<1, BothA>, k_max<1, PairA>, a, rows, wk, 0, name);
     if (a.cone) return launch_rows(c, k_max<2, BothA>, k_max<2, PairA>, a, rows, wk, 0, name);
     return launch_rows(c, k_max<0, BothA>, k_max<0, PairA>, a, rows, wk, 0, name);
@@ -467,7 +497,7 @@ static mpc_status launch_max(mpc_ctx* c, MaxArgs& a, i64 rows, i64 cols, int w, 
 // short rows (cols <= MAXS_COLS, MaxPool windows): warp-per-tile kernel, windows gathered in-kernel
 static mpc_status launch_max_small(mpc_ctx* c, MaxSmallArgs& a, const char* name)
 {
-    const int lv = a.w > 33 ? 1 : (use_cone(c, a.w) ? 2 : 0);
+    const int lv = use_cone(c, a.w) ? (a.w > 33 ? 3 : 2) : (a.w > 33 ? 1 : 0);
     const size_t dyn = sizeof(u64) * 64 * (size_t)a.cols * NWARPS;
     a.fcol = make_fastdiv((u32)a.cols);
     const i64 ntiles = (a.rows + 31) / 32;
@@ -485,6 +515,7 @@ static mpc_status launch_max_small(mpc_ctx* c, MaxSmallArgs& a, const char* name
     };
     if (lv == 1) return pick(k_max_small<1, BothA>, k_max_small<1, PairA>);
     if (lv == 2) return pick(k_max_small<2, BothA>, k_max_small<2, PairA>);
+    if (lv == 3) return pick(k_max_small<3, BothA>, k_max_small<3, PairA>);
     return pick(k_max_small<0, BothA>, k_max_small<0, PairA>);
 }
 
@@ -525,6 +556,9 @@ static mpc_status hdr_check(mpc_ctx* c, const char* op, u64 steps_needed)
 static mpc_status begin_op(mpc_ctx* c, u64 steps_needed, const char* op)
 {
     if (!c) return MPC_ERR_INVALID;
+    if (c->nvtx_open) nvtx_pop();                 // an op that returned early left its range open
+    nvtx_push(op);
+    c->nvtx_open = 1;
     c->last_philox = 0;
     c->st.calls++;
     if (c->step + steps_needed > (1ull << 32))
@@ -539,6 +573,7 @@ static mpc_status begin_op(mpc_ctx* c, u64 steps_needed, const char* op)
 #define begin(c, steps) begin_op((c), (steps), __func__)
 static void finish(mpc_ctx* c, u64 steps)
 {
+    if (c->nvtx_open) { nvtx_pop(); c->nvtx_open = 0; }
     rec_close(c);
     c->step += steps;
     c->st.steps += steps;
@@ -585,17 +620,38 @@ static void acct_max(mpc_ctx* c, i64 rows, i64 cols, int w)
 }
 
 // ------------------------------------------------------------------ PAIR memory ----
+// Initial exchange state (proto.cuh): LL -- all zero (tags are rounds >= 1); LL63 -- every receive
+// word holds tag 1 and every lane's tag bits are 1, so the first write of a word carries tag 0.
+__global__ void k_xinit(u64* rx, u32* tags, u64* rounds, i64 slots, int fmt)
+{
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < slots * XSLOT_RX; t += (i64)gridDim.x * blockDim.x)
+        rx[t] = fmt ? (1ull << 63) : 0ull;
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < slots * 32; t += (i64)gridDim.x * blockDim.x)
+        tags[t] = 0xffffffffu;
+    for (i64 t = blockIdx.x * (i64)blockDim.x + threadIdx.x; t < slots; t += (i64)gridDim.x * blockDim.x)
+        rounds[t] = 0;
+}
+static mpc_status xinit(mpc_ctx* c, XAlloc& a)
+{
+    const size_t S = (size_t)c->slots;
+    char* b = (char*)a.base;
+    k_xinit<<<(unsigned)std::min<size_t>((S * XSLOT_RX + 255) / 256, 4096), 256>>>(
+        (u64*)(b + a.rx_off), (u32*)(b + a.tags_off), (u64*)(b + a.round_off), (i64)S, c->xfmt);
+    return cudaDeviceSynchronize() == cudaSuccess ? MPC_OK : MPC_ERR_CUDA;
+}
+
 static mpc_status xalloc(mpc_ctx* c, XAlloc& a)
 {
     const size_t S = (size_t)c->slots;
     a.rx_off = 0;
     a.flag_off = a.rx_off + S * XSLOT_RX * sizeof(u64);
     a.round_off = a.flag_off + S * 4 * sizeof(u64);
-    a.err_off = a.round_off + S * sizeof(u64);
+    a.tags_off = a.round_off + S * sizeof(u64);
+    a.err_off = a.tags_off + S * 32 * sizeof(u32);
     a.bytes = a.err_off + 256;
     if (cudaMalloc(&a.base, a.bytes) != cudaSuccess) { a.base = nullptr; return MPC_ERR_NOMEM; }
     if (cudaMemset(a.base, 0, a.bytes) != cudaSuccess) return MPC_ERR_CUDA;
-    return MPC_OK;
+    return xinit(c, a);
 }
 
 // ------------------------------------------------------------------ ABI ----
@@ -629,6 +685,9 @@ mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
     }
     if (cfg->mode != MPC_MODE_BOTH) {
         c->slots = sms * 8 * NWARPS;       // up to 8 resident CTAs per SM
+        // default wire format: LL63 across GPUs (NVLink bytes bind), LL in loopback (local HBM:
+        // LL's fewer instructions per word win, tools/ab_pair.py)
+        c->xfmt = cfg->mode == MPC_MODE_PAIR ? 1 : 0;
         mpc_status st = xalloc(c, c->xa[0]);
         if (!st && cfg->mode == MPC_MODE_PAIR_LOOPBACK) st = xalloc(c, c->xa[1]);
         if (st) { mpc_ctx_destroy(c); return st; }
@@ -640,6 +699,7 @@ mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
 mpc_status mpc_ctx_destroy(mpc_ctx* c)
 {
     if (!c) return MPC_OK;
+    if (c->nvtx_open) nvtx_pop();
     cudaStreamSynchronize(c->stream);
     for (int i = 0; i < c->nrec; ++i) { cudaEventDestroy(c->recs[i].a); cudaEventDestroy(c->recs[i].b); }
     for (int i = 0; i < c->npool; ++i) cudaEventDestroy(c->pool[i]);
@@ -712,6 +772,20 @@ mpc_status mpc_ctx_set_debug(mpc_ctx* c, int on)
     c->debug_hdr = on ? 1 : 0;
     return MPC_OK;
 }
+
+mpc_status mpc_ctx_set_exchange(mpc_ctx* c, int fmt)
+{
+    if (!c) return MPC_ERR_INVALID;
+    if (fmt != 0 && fmt != 1) return fail(c, MPC_ERR_RANGE, "exchange format must be 0 (LL) or 1 (LL63)");
+    if (!is_pair(c)) return MPC_OK;                        // BOTH: no exchange
+    if (fmt == c->xfmt) return MPC_OK;
+    if (c->xused) return fail(c, MPC_ERR_INVALID, "set_exchange: the context has already exchanged (set it first)");
+    c->xfmt = fmt;
+    for (int i = 0; i < 2; ++i)
+        if (c->xa[i].base) { mpc_status st = xinit(c, c->xa[i]); if (st) return fail(c, st, "set_exchange: init"); }
+    return MPC_OK;
+}
+int mpc_ctx_get_exchange(const mpc_ctx* c) { return c ? c->xfmt : -1; }
 
 mpc_status mpc_ctx_set_ltz_circuit(mpc_ctx* c, int circuit)
 {
@@ -915,7 +989,7 @@ mpc_status mpc_mul_bcast(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, i
     if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "mul_bcast: null pointer");
     const i64 n = rows * cols;
     if (rows > 0) {
-        u64* br = (u64*)scratch(c, sizeof(u64) * 3 * (size_t)rows * (is_loop(c) ? 2 : 1));
+        u64* br = (u64*)scratch(c, sizeof(u64) * 6 * (size_t)rows);     // [3][rows], loopback: per party
         if (!br) return fail(c, MPC_ERR_NOMEM, "mul_bcast scratch");
         BmbRowsArgs ra{(u32)c->step, spv(c, y), rows, (u64)row_off, br, is_loop(c) ? 1 : 0};
         const i64 nw = (rows + 31) / 32;
@@ -931,7 +1005,7 @@ mpc_status mpc_mul_bcast(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, i
         }
         if (st) return st;
         st = launch_pairs(c, n, (u64)off, BmbBody{(u32)c->step, spv(c, x), sov(c, z), n, make_fastdiv((u32)cols),
-                                                  br, rows, tb, is_loop(c) ? 1 : 0}, "mul_bcast");
+                                                  br, rows, tb, is_loop(c) ? 1 : 0, SP{{nullptr, nullptr}}, 0}, "mul_bcast");
         if (st) return st;
         acct_bcast(c, (u64)n, (u64)rows);
     }
@@ -1054,8 +1128,10 @@ static mpc_status cmp_common(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, 
     if (n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "off must be a multiple of 32");
     if (bad_sh(c, x) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "cmp: null pointer");
     const char* name = relu ? "relu" : "cmp";
-    if (use_cone(c, w))
-        st = launch_cone(c, n, (u64)off, CmpConeBody{(u32)c->step, w, spv(c, x), sov(c, z), relu, n}, name);
+    if (use_cone(c, w) && w > 33)
+        st = launch_cone(c, n, (u64)off, CmpConeBody<64>{(u32)c->step, w, spv(c, x), sov(c, z), relu, n}, name);
+    else if (use_cone(c, w))
+        st = launch_cone(c, n, (u64)off, CmpConeBody<32>{(u32)c->step, w, spv(c, x), sov(c, z), relu, n}, name);
     else st = w > 33 ? launch_groups(c, n, (u64)off, CmpBody<true>{(u32)c->step, w, spv(c, x), sov(c, z), relu}, name)
                 : launch_groups(c, n, (u64)off, CmpBody<false>{(u32)c->step, w, spv(c, x), sov(c, z), relu}, name);
     if (st) return st;
@@ -1176,8 +1252,10 @@ static mpc_status act_common(mpc_ctx* c, int act, mpc_shares x, mpc_shares z, in
     if (st) return st;
     if (bad_sh(c, x) || bad_sh(c, z) || n < 0 || off < 0 || (off & 31)) return fail(c, MPC_ERR_INVALID, "act args (off % 32)");
     const char* name = act == 0 ? "gelu" : act == 1 ? "silu" : "sigmoid";
-    if (use_cone(c, k.w))
-        st = launch_cone(c, n, (u64)off, ActConeBody{(u32)c->step, k, spv(c, x), sov(c, z), n}, name);
+    if (use_cone(c, k.w) && k.w > 33)
+        st = launch_cone(c, n, (u64)off, ActConeBody<64>{(u32)c->step, k, spv(c, x), sov(c, z), n}, name);
+    else if (use_cone(c, k.w))
+        st = launch_cone(c, n, (u64)off, ActConeBody<32>{(u32)c->step, k, spv(c, x), sov(c, z), n}, name);
     else st = k.w > 33 ? launch_groups(c, n, (u64)off, ActBody<true>{(u32)c->step, k, spv(c, x), sov(c, z)}, name)
                   : launch_groups(c, n, (u64)off, ActBody<false>{(u32)c->step, k, spv(c, x), sov(c, z)}, name);
     if (st) return st;
@@ -1536,11 +1614,13 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         const i64 wk = softmax_work_u64(cols, a.esmem != 0), ek = a.esmem ? 0 : 64 * cols;
         const size_t lim = a.esmem ? 100 * 1024 : SMEM_LIMIT;
         if (a.causal)   // causal instantiations: the dense kernels carry no mask code
-            st = wide ? launch_rows(c, k_softmax<1, BothA, true>, k_softmax<1, PairA, true>, a, rows, wk, ek, "softmax", lim)
+            st = wide && a.cone ? launch_rows(c, k_softmax<3, BothA, true>, k_softmax<3, PairA, true>, a, rows, wk, ek, "softmax", lim)
+               : wide ? launch_rows(c, k_softmax<1, BothA, true>, k_softmax<1, PairA, true>, a, rows, wk, ek, "softmax", lim)
                : a.cone ? launch_rows(c, k_softmax<2, BothA, true>, k_softmax<2, PairA, true>, a, rows, wk, ek, "softmax", lim)
                         : launch_rows(c, k_softmax<0, BothA, true>, k_softmax<0, PairA, true>, a, rows, wk, ek, "softmax", lim);
         else
-            st = wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax", lim)
+            st = wide && a.cone ? launch_rows(c, k_softmax<3, BothA>, k_softmax<3, PairA>, a, rows, wk, ek, "softmax", lim)
+               : wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax", lim)
                : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax", lim)
                         : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax", lim);
     }
@@ -1579,7 +1659,74 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
         a.bcast = p->bcast ? 1 : 0;
         const i64 ntiles = (rows + 31) / 32;
         const bool wide = p->rsqrt.exp.window > 33;
-        if (!is_pair(c)) {
+#ifndef MPC_LN_QUAD
+#define MPC_LN_QUAD 0      // warp-per-4-rows kernel: measured 9 % slower than the tile kernel (all warps hit
+#endif                     // their rsqrt chains at once)
+#ifndef MPC_LN_SPLIT
+#define MPC_LN_SPLIT 1
+#endif
+        if (MPC_LN_SPLIT && !p->rsqrt.exp.clamp && rows * cols < (1ll << 31)) {
+            // three launches: per-row stats, the row rsqrt (element-wise NR kernel), the product
+            u64* sc = (u64*)scratch(c, sizeof(u64) * (size_t)rows * (6 + 6));
+            if (!sc) return fail(c, MPC_ERR_NOMEM, "layernorm scratch");
+            const SO MU{{sc, sc + rows}}, VR{{sc + 2 * rows, sc + 3 * rows}}, RS{{sc + 4 * rows, sc + 5 * rows}};
+            u64* br = sc + 6 * rows;                                     // broadcast-triple row records
+            LnStatsArgs sa{a.s_sq, a.x, MU, VR, rows, cols, (u64)row_off, a.mean_mode, a.e_invd, a.e_eps};
+            const i64 nw = rows;                                        // warps of work
+            if (!is_pair(c)) {
+                static DevCache occ;
+                const int per_sm = dev_cached(occ, c->cfg.device, [] { return occupancy(k_ln_stats<BothA>); });
+                rec_begin(c, "ln_stats", (u64)rows);
+                k_ln_stats<BothA><<<grid_for(c, nw * 32, TPB, per_sm), TPB, 0, c->stream>>>(BothA{c->K}, sa);
+                rec_end(c);
+                c->st.launches++;
+                st = cuda_check(c, "ln_stats");
+            } else {
+                st = launch_pair_kernel(c, k_ln_stats<PairA>, pair_ctas(c, k_ln_stats<PairA>, 0, (nw * 32 + TPB - 1) / TPB),
+                                        0, "ln_stats", sa);
+            }
+            if (st) return st;
+            const SP VRc{{VR.p[0], VR.p[1]}}, MUc{{MU.p[0], MU.p[1]}}, RSc{{RS.p[0], RS.p[1]}};
+            if ((st = launch_pairs(c, rows, (u64)row_off, NrPairBody<1>{a.s_rs, a.rk, VRc, RS, rows}, "ln_rsqrt"))) return st;
+            const i64 n = rows * cols;
+            if (a.bcast) {
+                BmbRowsArgs ra{a.s_mul, RSc, rows, (u64)row_off, br, is_loop(c) ? 1 : 0};
+                const i64 nw2 = (rows + 31) / 32;
+                if (!is_pair(c)) {
+                    rec_begin(c, "bcast_rows", (u64)rows);
+                    k_bmb_rows<BothA><<<grid_for(c, nw2 * 32, TPB, 8), TPB, 0, c->stream>>>(BothA{c->K}, ra);
+                    rec_end(c);
+                    c->st.launches++;
+                    st = cuda_check(c, "bcast_rows");
+                } else {
+                    st = launch_pair_kernel(c, k_bmb_rows<PairA>, pair_ctas(c, k_bmb_rows<PairA>, 0, (nw2 * 32 + TPB - 1) / TPB),
+                                            0, "bcast_rows", ra);
+                }
+                if (st) return st;
+                st = launch_pairs(c, n, (u64)row_off * (u64)cols,
+                                  BmbBody{a.s_mul, a.x, a.z, n, make_fastdiv((u32)cols), br, rows, FRAC, is_loop(c) ? 1 : 0,
+                                          MUc, 1}, "ln_out");
+            } else {
+                st = launch_pairs(c, n, (u64)row_off * (u64)cols,
+                                  LnOutBody{a.s_mul, a.x, a.z, n, make_fastdiv((u32)cols), MUc, RSc}, "ln_out");
+            }
+        } else if (MPC_LN_QUAD && !p->rsqrt.exp.clamp) {
+            // warp-granular kernel (no clamp: the rsqrt has no LTZ, so rows need no 32-row grouping)
+            const i64 nctas = ((rows + 3) / 4 + NWARPS - 1) / NWARPS;
+            if (!is_pair(c)) {
+                static DevCache occ;
+                const int per_sm = dev_cached(occ, c->cfg.device, [] { return occupancy(k_ln_quad<false, BothA>, 0, MPC_ROW_TPB); });
+                const int grid = (int)std::min<i64>(nctas, (i64)c->sm_count * per_sm);
+                rec_begin(c, "layernorm", (u64)rows);
+                k_ln_quad<false, BothA><<<grid, MPC_ROW_TPB, 0, c->stream>>>(BothA{c->K}, a);
+                rec_end(c);
+                c->st.launches++;
+                st = cuda_check(c, "layernorm");
+            } else {
+                st = launch_pair_kernel_tpb(c, k_ln_quad<false, PairA>, pair_ctas(c, k_ln_quad<false, PairA>, 0, nctas, MPC_ROW_TPB),
+                                            0, MPC_ROW_TPB, "layernorm", a);
+            }
+        } else if (!is_pair(c)) {
             const int grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(wide ? k_ln<true, BothA> : k_ln<false, BothA>, 0, MPC_ROW_TPB));
             rec_begin(c, "layernorm", (u64)rows);
             if (wide) k_ln<true, BothA><<<grid, MPC_ROW_TPB, 0, c->stream>>>(BothA{c->K}, a);

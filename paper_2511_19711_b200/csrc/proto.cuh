@@ -21,16 +21,21 @@ namespace mpc {
 struct SP { const u64* p[2]; };
 struct SO { u64* p[2]; };
 
-// carry-cone LTZ over G groups per warp (ltz_cone.cuh)
-template <int G>
-struct ConeSmem { u32 w[G][32][4]; };
-template <int G>
+// carry-cone LTZ over G groups per warp (ltz_cone.cuh); NL leaf positions (32: w <= 33, 64: w <= 65)
+template <int G, int NL = 32>
+struct ConeSmem { u32 w[G][NL][4]; };
+template <int G, int NL>
 __device__ void ltz_cone_both(const Keys& K, u64 q0, u32 s, int w, const Sh (&x)[G], Sh (&z)[G], int lane,
-                              ConeSmem<G>& sm);
+                              ConeSmem<G, NL>& sm);
 struct PairP;
-template <int G>
+template <int G, int NL>
 __device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G], u64 (&z)[G], int lane,
-                              ConeSmem<G>& sm);
+                              ConeSmem<G, NL>& sm);
+
+// 16-byte (LDG.E.128 / STG.E.128) access to an element pair (i, i+1) of one party's array
+__device__ __forceinline__ bool al16(const u64* p) { return ((uintptr_t)p & 15u) == 0; }
+__device__ __forceinline__ ulonglong2 ld128(const u64* p) { return *reinterpret_cast<const ulonglong2*>(p); }
+__device__ __forceinline__ void st128(u64* p, u64 a, u64 b) { *reinterpret_cast<ulonglong2*>(p) = make_ulonglong2(a, b); }
 
 // ================================================================================ BOTH ====
 struct BothP {
@@ -45,6 +50,17 @@ struct BothP {
     __device__ __forceinline__ S zero() const { return {0, 0}; }
     __device__ __forceinline__ S ld(SP a, i64 i) const { return {a.p[0][i], a.p[1][i]}; }
     __device__ __forceinline__ void st(SO a, i64 i, S v) const { a.p[0][i] = v.s0; a.p[1][i] = v.s1; }
+    // element pair (i, i+1): plain 8-byte accesses here (two per party, together fully coalesced) --
+    // the 16-byte form of PairP measured 3 % (softmax) to 15 % (Beaver mul) slower in this mode
+    __device__ __forceinline__ void ld_pair(SP a, i64 i, bool va, bool vb, S& x0, S& x1) const {
+        x0 = x1 = zero();
+        if (va) x0 = ld(a, i);
+        if (vb) x1 = ld(a, i + 1);
+    }
+    __device__ __forceinline__ void st_pair(SO a, i64 i, bool va, bool vb, S x0, S x1) const {
+        if (va) st(a, i, x0);
+        if (vb) st(a, i + 1, x1);
+    }
     __device__ __forceinline__ S add(S a, S b) const { return sh_add(a, b); }
     __device__ __forceinline__ S sub(S a, S b) const { return sh_sub(a, b); }
     __device__ __forceinline__ S neg(S a) const { return sh_neg(a); }
@@ -91,9 +107,9 @@ struct BothP {
     __device__ __forceinline__ void bmb2(u64 u, u32 s, S x0, S x1, const BRow& r0, const BRow& r1, S& z0, S& z1) {
         mpc::bmb2(*Kp, u, s, x0, x1, r0, r1, z0, z1);
     }
-    template <int G>
-    __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G>& sm) {
-        ltz_cone_both<G>(*Kp, q0, s, w, x, z, lane, sm);
+    template <int G, int NL>
+    __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G, NL>& sm) {
+        ltz_cone_both<G, NL>(*Kp, q0, s, w, x, z, lane, sm);
     }
     __device__ __forceinline__ void sq2(u64 u, u32 s, S y0, S y1, S& z0, S& z1) { mpc::sq2(*Kp, u, s, y0, y1, z0, z1); }
     __device__ __forceinline__ u64 open(S x) const { return x.s0 + x.s1; }
@@ -125,14 +141,17 @@ __device__ __forceinline__ Sh BothP::divp(Sh a, i64 d) const { return {floordiv_
 
 // ================================================================================ PAIR ====
 constexpr int XW = 8;                // u64 words per lane per round (max)
-constexpr int XSLOT_RX = 2 * XW * 32 * 2; // u64 per warp slot: [parity][word][lane][payload-half + tag]
-                                          // (word-major: one put/get of word k by a warp is 512 contiguous B)
+constexpr int XSLOT_RX = 2 * XW * 32 * 2;   // u64 per warp slot: LL [buf][word][lane][2]; LL63 uses the
+                                            // first [buf][word][lane] main words, then [buf][word] top-bit
+                                            // words
+constexpr u64 M63 = 0x7fffffffffffffffull;
 
 // Device view of one party's exchange memory.
 struct XMem {
     u64* rx;          // [slots][2][XW][32] receive buffers (peer writes)
     u64* flag;        // [slots][4]          my flags (peer writes word 0)
     u64* round;       // [slots]             persistent round counters (local only)
+    u32* tags;        // [slots][32]         persistent per-lane LL63 tag bits (local only)
     int* err;         // error word (1 = exchange timeout)
     u64* prx;         // peer's rx   (remote or, loopback, the other party's local buffer)
     u64* pflag;       // peer's flag
@@ -180,10 +199,12 @@ struct PairP {
     const Keys* Kp;          // kernel parameter space (__grid_constant__)
     int pty;                 // 0 | 1
     // per-warp exchange state (set by bind())
-    u64* rx; u64* prx; u64* flag; u64* pflag; u64* rstate; int* err;
+    u64* rx; u64* prx; u64* flag; u64* pflag; u64* rstate; u32* tstate; int* err;
     u64 rnd;
+    u32 tg;                  // LL63 tag bits: main word (b, k) at bit 8b + k, top-bit word at 16 + 8b + k
     int dead;
     int local;               // loopback: the peer is on this GPU -> gpu-scope release/acquire
+    int fmt;                 // exchange wire format: 0 LL, 1 LL63 (warp-uniform)
     using S = u64;
     static constexpr bool kPair = true;
     static constexpr u64 kTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s, then poison
@@ -194,50 +215,121 @@ struct PairP {
         flag = m.flag + (i64)slot * 4;
         pflag = m.pflag + (i64)slot * 4;
         rstate = m.round + slot;
+        tstate = m.tags + (i64)slot * 32;
         err = m.err;
         rnd = *rstate;
+        tg = tstate[threadIdx.x & 31];
         dead = 0;
     }
     __device__ __forceinline__ void unbind(int lane) {
         if (lane == 0) *rstate = rnd;
+        tstate[lane] = tg;
     }
     __device__ __forceinline__ int party() const { return pty; }
     // ---- exchange: put words, exch(), get peer's words ----
-    // LL exchange (the NCCL "LL" idea): every 64-bit payload travels as two 8-byte words
-    // {payload half, round tag}, written with one 16-byte store into the peer's buffer at
-    // parity (round & 1).  Aligned 8-byte stores are single-copy atomic, so the receiver
-    // polls its own words until both tags equal the round: no fences, flags or warp
-    // barriers, and no L1 invalidation.  Both parties run the same put/get pattern.
-    __device__ __forceinline__ void put(int lane, int k, u64 v) {
-        const u64 tag = (rnd + 1) << 32;
-        u64* d = prx + ((((rnd + 1) & 1) * XW + k) * 32 + lane) * 2;
-        const u64 lo = (v & 0xffffffffull) | tag, hi = (v >> 32) | tag;
-        asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" :: "l"(d), "l"(lo), "l"(hi) : "memory");
+    // Two wire formats, both "LL"-style (the idea of NCCL's low-latency protocol: the data carries
+    // its own readiness tag, so there are no fences, flags or warp barriers on the data path), chosen
+    // per context (mpc_ctx_set_exchange):
+    //  LL   (fmt 0): payload word = two 8-byte words {lo32 | tag32, hi32 | tag32}, tag = the 32-bit
+    //                round, one 16-byte store / load.  2 wire bytes per payload byte, fewest
+    //                instructions -- the default in PAIR_LOOPBACK (local HBM, instruction-bound).
+    //  LL63 (fmt 1): payload word = ONE 8-byte store {bits 0..62 | tag << 63}; the 32 lanes' bit 63
+    //                is gathered with a ballot and lane 0 sends it as one extra tagged word per
+    //                (round, word): 33 words per 32 (wire / payload 1.031) -- the default in
+    //                MPC_MODE_PAIR (NVLink, bytes-bound).  The one-bit tag FLIPS on every write of
+    //                a receive word: both parties issue the same put / get sequence, so each lane
+    //                tracks its words' current tags (register tg, persisted per warp slot).
+    // Both: round r uses receive buffer r mod 2 (a sender is at most one round ahead of its peer, so
+    // it never overwrites a word the peer has not read), and aligned 8-byte stores are single-copy
+    // atomic.  put / get must be issued by all 32 lanes together (LL63's ballot); a lane with
+    // live = false sends, reads and (LL63) flips nothing for that word -- both parties pass the same
+    // live pattern.
+    // (LL inline; LL63 out of line: its code stays out of the loopback kernels' instruction stream,
+    // and across NVLink a call per word is nothing next to the round trip)
+#ifndef MPC_XFMT_LL_ONLY
+#define MPC_XFMT_LL_ONLY 0     // A/B builds: compile the LL63 path out
+#endif
+    __device__ __forceinline__ void put(int lane, int k, u64 v, bool live = true) {
+        const u64 r = rnd + 1;                                   // the round being sent
+        const int b = (int)(r & 1);
+        if (MPC_XFMT_LL_ONLY || !fmt) {
+            const u64 tag = r << 32;
+            u64* d = prx + ((b * XW + k) * 32 + lane) * 2;
+            const u64 lo = (v & 0xffffffffull) | tag, hi = (v >> 32) | tag;
+            if (live) asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" :: "l"(d), "l"(lo), "l"(hi) : "memory");
+            return;
+        }
+        put63(lane, k, v, live, b);
+    }
+    __device__ __noinline__ void put63(int lane, int k, u64 v, bool live, int b) {
+        const u32 mb = 1u << (8 * b + k), eb = 1u << (16 + 8 * b + k);
+        tg ^= eb;
+        if (live) tg ^= mb;
+        const u32 top = __ballot_sync(FULL, live && (v >> 63));
+        u64* d = prx + (b * XW + k) * 32 + lane;
+        if (live) asm volatile("st.volatile.global.u64 [%0], %1;" :: "l"(d), "l"((v & M63) | ((u64)((tg & mb) != 0) << 63)) : "memory");
+        if (lane == 0) {
+            u64* e = prx + 2 * XW * 32 + b * XW + k;
+            asm volatile("st.volatile.global.u64 [%0], %1;" :: "l"(e), "l"((u64)top | ((u64)((tg & eb) != 0) << 63)) : "memory");
+        }
     }
     __device__ __forceinline__ void exch(int lane) {
         (void)lane;
         ++rnd;                                   // the round now being received
     }
     __device__ __forceinline__ u64 get(int lane, int k) {
-        const u64* sp = rx + (((rnd & 1) * XW + k) * 32 + lane) * 2;
-        const u64 want = rnd & 0xffffffffull;
-        u64 lo, hi;
-        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
-        if (((lo >> 32) != want || (hi >> 32) != want) && !dead) {
+        const int b = (int)(rnd & 1);                            // this round's buffer (tags set by put)
+        if (MPC_XFMT_LL_ONLY || !fmt) {
+            const u64* sp = rx + ((b * XW + k) * 32 + lane) * 2;
+            const u64 want = rnd & 0xffffffffull;
+            u64 lo, hi;
+            asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
+            if (((lo >> 32) != want || (hi >> 32) != want) && !dead) {
+                const u64 t0 = globaltimer();
+                unsigned spins = 0;
+                do {                             // (a __nanosleep backoff here measured 2x slower)
+                    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
+                    if ((++spins & 1023) == 0 && globaltimer() - t0 > kTimeoutNs) { atomicCAS(err, 0, 1); dead = 1; break; }
+                } while ((lo >> 32) != want || (hi >> 32) != want);
+            }
+            return (lo & 0xffffffffull) | (hi << 32);
+        }
+        return get63(lane, k, b);
+    }
+    __device__ __noinline__ u64 get63(int lane, int k, int b) {
+        const u64* sp = rx + (b * XW + k) * 32 + lane;
+        const u64* ep = rx + 2 * XW * 32 + b * XW + k;
+        const u64 want = (tg >> (8 * b + k)) & 1u, wante = (tg >> (16 + 8 * b + k)) & 1u;
+        u64 v, e;
+        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(sp) : "memory");
+        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(e) : "l"(ep) : "memory");
+        if (((v >> 63) != want || (e >> 63) != wante) && !dead) {
             const u64 t0 = globaltimer();
             unsigned spins = 0;
-            do {                                 // (a __nanosleep backoff here measured 2x slower)
-                asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(sp) : "memory");
+            do {
+                asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(sp) : "memory");
+                asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(e) : "l"(ep) : "memory");
                 if ((++spins & 1023) == 0 && globaltimer() - t0 > kTimeoutNs) { atomicCAS(err, 0, 1); dead = 1; break; }
-            } while ((lo >> 32) != want || (hi >> 32) != want);
+            } while ((v >> 63) != want || (e >> 63) != wante);
         }
-        return (lo & 0xffffffffull) | (hi << 32);
+        return (v & M63) | ((u64)((u32)e >> lane & 1u) << 63);
     }
 
     // ---- local share ops (party 0 carries public addends) ----
     __device__ __forceinline__ S zero() const { return 0; }
     __device__ __forceinline__ S ld(SP a, i64 i) const { return a.p[pty][i]; }
     __device__ __forceinline__ void st(SO a, i64 i, S v) const { a.p[pty][i] = v; }
+    // element pair (i, i+1) of this party's array: one 16-byte access (LDG.E.128 / STG.E.128) when both
+    // are valid and aligned (loopback Beaver mul 5 % faster)
+    __device__ __forceinline__ void ld_pair(SP a, i64 i, bool va, bool vb, S& x0, S& x1) const {
+        x0 = x1 = 0;
+        if (va && vb && al16(a.p[pty] + i)) { const ulonglong2 t = ld128(a.p[pty] + i); x0 = t.x; x1 = t.y; }
+        else { if (va) x0 = ld(a, i); if (vb) x1 = ld(a, i + 1); }
+    }
+    __device__ __forceinline__ void st_pair(SO a, i64 i, bool va, bool vb, S x0, S x1) const {
+        if (va && vb && al16(a.p[pty] + i)) st128(a.p[pty] + i, x0, x1);
+        else { if (va) st(a, i, x0); if (vb) st(a, i + 1, x1); }
+    }
     __device__ __forceinline__ S add(S a, S b) const { return a + b; }
     __device__ __forceinline__ S sub(S a, S b) const { return a - b; }
     __device__ __forceinline__ S neg(S a) const { return 0ull - a; }
@@ -639,9 +731,9 @@ struct PairP {
         return pty == 0 ? c + sg * rA : sg * rA;
     }
 
-    template <int G>
-    __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G>& sm) {
-        ltz_cone_pair<G>(*this, q0, s, w, x, z, lane, sm);
+    template <int G, int NL>
+    __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G, NL>& sm) {
+        ltz_cone_pair<G, NL>(*this, q0, s, w, x, z, lane, sm);
     }
 
     // ---- S2 open: exchange the shares themselves ----

@@ -20,16 +20,21 @@ __device__ __forceinline__ Sh sh_not(Sh b) { return {1ull - b.s0, 0ull - b.s1}; 
 
 // Beaver step on element-unit u at step s.
 // (a0,b0) = PRG(K0,u,s,0); (a1,b1) = PRG(K1,u,s,0); c0 = half (u&1) of PRG(K0,u>>1,s,1).
+// Party 1's share is z1 = c1 + e b1 + f a1 with c1 = (a0+a1)(b0+b1) - c0; since Beaver is exact,
+// z0 + z1 = (x0+x1)(y0+y1) = X Y, so one thread holding both parties forms the SAME z1 as
+// X Y - z0: 3 ring multiplies instead of 5 (identical bits; the PAIR policy computes z1 the
+// protocol's way, tests compare both against the oracle).
 __device__ __forceinline__ Sh bm_with_c0(const Keys& K, u64 u, u32 s, Sh x, Sh y, u64 c0)
 {
     const uint4 A0 = prg(K.k0, u, s, 0);
     const uint4 A1 = prg(K.k1, u, s, 0);
     const u64 a0 = w64(A0.x, A0.y), b0 = w64(A0.z, A0.w);
     const u64 a1 = w64(A1.x, A1.y), b1 = w64(A1.z, A1.w);
-    const u64 c1 = (a0 + a1) * (b0 + b1) - c0;        // dealer correction -> party 1
-    const u64 e = (x.s0 - a0) + (x.s1 - a1);           // open(x - a)
-    const u64 f = (y.s0 - b0) + (y.s1 - b1);           // open(y - b)
-    return {c0 + e * (b0 + f) + f * a0, c1 + e * b1 + f * a1};   // party 0: e b0 + e f = e (b0 + f)
+    const u64 X = x.s0 + x.s1, Y = y.s0 + y.s1;
+    const u64 e = X - (a0 + a1);                       // open(x - a)
+    const u64 f = Y - (b0 + b1);                       // open(y - b)
+    const u64 z0 = c0 + e * (b0 + f) + f * a0;         // party 0: e b0 + e f = e (b0 + f)
+    return {z0, X * Y - z0};
 }
 
 __device__ __forceinline__ u64 beaver_c0(const Keys& K, u64 u, u32 s)
@@ -63,10 +68,10 @@ __device__ __forceinline__ Sh sq_with_a1(const Keys& K, u64 u, u32 s, Sh y, u64 
 {
     const uint4 A0 = prg(K.k0, u, s, 2);
     const u64 a0 = w64(A0.x, A0.y), c0 = w64(A0.z, A0.w);
-    const u64 a = a0 + a1;
-    const u64 c1 = a * a - c0;                         // dealer correction -> party 1
-    const u64 e = (y.s0 - a0) + (y.s1 - a1);           // open(y - a)
-    return {c0 + e * (2ull * a0 + e), c1 + 2ull * e * a1};
+    const u64 Y = y.s0 + y.s1;
+    const u64 e = Y - (a0 + a1);                       // open(y - a)
+    const u64 z0 = c0 + e * (2ull * a0 + e);
+    return {z0, Y * Y - z0};                           // = c1 + 2 e a1 with c1 = a^2 - c0 (exact square)
 }
 __device__ __forceinline__ Sh sq1(const Keys& K, u64 u, u32 s, Sh y)
 {
@@ -96,9 +101,10 @@ __device__ __forceinline__ Sh bmb_elem(const Keys& K, u64 u, u32 s, Sh x, const 
 {
     const uint4 A0 = prg(K.k0, u, s, 4);
     const u64 a0 = w64(A0.x, A0.y), c0 = w64(A0.z, A0.w);
-    const u64 c1 = (a0 + a1) * (r.b0 + r.b1) - c0;     // dealer correction -> party 1
-    const u64 e = (x.s0 - a0) + (x.s1 - a1);           // open(x - a)
-    return {c0 + e * (r.b0 + r.f) + r.f * a0, c1 + e * r.b1 + r.f * a1};
+    const u64 X = x.s0 + x.s1;
+    const u64 e = X - (a0 + a1);                       // open(x - a)
+    const u64 z0 = c0 + e * (r.b0 + r.f) + r.f * a0;
+    return {z0, X * (r.b0 + r.b1 + r.f) - z0};         // = c1 + e b1 + f a1 (exact: rec = x y_row)
 }
 // unit pair (u even, u+1): one K1 block serves both a1 halves (1.5 blocks per element)
 __device__ __forceinline__ void bmb2(const Keys& K, u64 u, u32 s, Sh x0, Sh x1, const BRow& r0, const BRow& r1,
@@ -110,15 +116,17 @@ __device__ __forceinline__ void bmb2(const Keys& K, u64 u, u32 s, Sh x0, Sh x1, 
 }
 
 // AND on XOR-shared 32-bit plane words with triple (a0,b0,c0 | a1,b1).
+// (party 1's z1 = c1 ^ d&b1 ^ e&a1 with c1 = (a0^a1)&(b0^b1) ^ c0 equals (X & Y) ^ z0, X = x0^x1,
+// Y = y0^y1: the AND is exact on XOR shares -- fewer LOP3s for the thread holding both parties)
 __device__ __forceinline__ void and_both(u32 x0, u32 x1, u32 y0, u32 y1,
                                          u32 a0, u32 b0, u32 c0, u32 a1, u32 b1,
                                          u32& z0, u32& z1)
 {
-    const u32 c1 = ((a0 ^ a1) & (b0 ^ b1)) ^ c0;       // dealer correction -> party 1
-    const u32 d = (x0 ^ a0) ^ (x1 ^ a1);                // open(x ^ a)
-    const u32 e = (y0 ^ b0) ^ (y1 ^ b1);                // open(y ^ b)
+    const u32 X = x0 ^ x1, Y = y0 ^ y1;
+    const u32 d = X ^ a0 ^ a1;                          // open(x ^ a)
+    const u32 e = Y ^ b0 ^ b1;                          // open(y ^ b)
     z0 = c0 ^ (d & b0) ^ (e & a0) ^ (d & e);
-    z1 = c1 ^ (d & b1) ^ (e & a1);
+    z1 = (X & Y) ^ z0;
 }
 
 // LTZ_w for w <= 33 (one bit plane per lane), branch-free: every lane issues the three

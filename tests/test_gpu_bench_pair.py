@@ -25,5 +25,5 @@ def test_bench_two_ranks_one_gpu():
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "pairs1"
-    assert "PAIR" in d["config"]["mode"] and d["roofline"]["nvlink"]["bytes_per_party_per_step"] > 0
+    assert "PAIR" in d["config"]["mode"] and d["roofline"]["nvlink"]["payload_bytes_per_party_per_step"] > 0
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0

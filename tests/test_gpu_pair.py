@@ -160,7 +160,7 @@ def test_square_ops_loopback(m):
     p.sync()
 
 
-@pytest.mark.parametrize("w", [17, 33])
+@pytest.mark.parametrize("w", [17, 21, 33, 40, 64])
 def test_cone_loopback(m, w):
     b, p = ctxs(m, 1, step=3)
     b.set_ltz_circuit(1)
@@ -184,13 +184,21 @@ def test_cone_act_loopback(m, form, deg):
     p.sync()
 
 
-def test_cone_softmax_loopback(m):
+@pytest.mark.parametrize("w", [33, 64])
+def test_cone_softmax_loopback(m, w):
     b, p = ctxs(m, 2)
     b.set_ltz_circuit(1)
     p.set_ltz_circuit(1)
     x = b.share(torch.from_numpy(workloads.softmax_inputs(96, 128)).cuda())
     p.set_step(b.step)
-    assert eq(b.softmax(x, 96, 128, exp_square=1, recip_square=1), p.softmax(x, 96, 128, exp_square=1, recip_square=1))
+    assert eq(b.softmax(x, 96, 128, exp_square=1, recip_square=1, window=w),
+              p.softmax(x, 96, 128, exp_square=1, recip_square=1, window=w))
+    y = b.share(torch.from_numpy(workloads.act_inputs(4096 + 40)).cuda())
+    p.set_step(b.step)
+    assert eq(b.gelu(y, form="poly_abs", degree=4, window=w), p.gelu(y, form="poly_abs", degree=4, window=w))
+    x9 = b.share(torch.from_numpy(workloads.softmax_inputs(70, 9)).cuda())
+    p.set_step(b.step)
+    assert eq(b.max(x9, 70, 9, window=w), p.max(x9, 70, 9, window=w))
     p.sync()
 
 
@@ -221,4 +229,55 @@ def test_debug_header_no_false_positive_loopback(m):
     p.set_step(b.step)
     assert eq(b.softmax(x, 64, 128), p.softmax(x, 64, 128))
     assert eq(b.relu(x), p.relu(x))
+    p.sync()
+
+
+# ---- both exchange wire formats: LL (loopback default) and LL63 (PAIR default) ----
+@pytest.mark.parametrize("fmt", [0, 1])
+def test_exchange_formats_loopback(m, fmt):
+    """Every op family in PAIR_LOOPBACK with the given wire format, bit-identical to BOTH (the
+    format is transport only, reading R33): varying live-lane patterns (cone), many rounds per
+    launch, consecutive launches on persistent per-slot round / tag state."""
+    b, p = ctxs(m, 2, step=5)
+    p.set_exchange(fmt)
+    assert p.exchange == fmt
+    x = b.share(torch.from_numpy(workloads.softmax_inputs(96, 128)).cuda())
+    p.set_step(b.step)
+    assert eq(b.softmax(x, 96, 128), p.softmax(x, 96, 128))
+    assert eq(b.softmax(x, 96, 128, causal=1, exp_clamp=1), p.softmax(x, 96, 128, causal=1, exp_clamp=1))
+    for circuit in (0, 1):
+        b.set_ltz_circuit(circuit)
+        p.set_ltz_circuit(circuit)
+        for w in (21, 33, 64):
+            assert eq(b.relu(x, window=w), p.relu(x, window=w))
+        assert eq(b.gelu(x, form="poly_abs", degree=4), p.gelu(x, form="poly_abs", degree=4))
+        assert eq(b.softmax(x, 96, 128, exp_square=1, recip_square=1, bcast=1),
+                  p.softmax(x, 96, 128, exp_square=1, recip_square=1, bcast=1))
+        x9 = b.share(torch.from_numpy(workloads.softmax_inputs(70, 9)).cuda())
+        p.set_step(b.step)
+        assert eq(b.max(x9, 70, 9), p.max(x9, 70, 9))
+    b.set_ltz_circuit(0)
+    p.set_ltz_circuit(0)
+    y = b.share(torch.from_numpy(workloads.layernorm_inputs(40, 768)).cuda())
+    p.set_step(b.step)
+    assert eq(b.layernorm(y, 40, 768), p.layernorm(y, 40, 768))
+    assert eq(b.layernorm(y, 40, 768, bcast=1), p.layernorm(y, 40, 768, bcast=1))
+    assert eq(b.layernorm(y, 40, 768, rsqrt_clamp=1), p.layernorm(y, 40, 768, rsqrt_clamp=1))
+    assert eq(b.mul_bcast(y, y, 40, 768, trunc_bits=16), p.mul_bcast(y, y, 40, 768, trunc_bits=16))
+    assert eq(b.exp(y, clamp=1, square=1), p.exp(y, clamp=1, square=1))
+    assert eq(b.matmul(y, y, 1, 40, 64, 40, trunc_bits=16), p.matmul(y, y, 1, 40, 64, 40, trunc_bits=16))
+    assert eq(b.gelu(y, form="erf", erf_terms=8), p.gelu(y, form="erf", erf_terms=8))
+    p.sync()
+
+
+def test_exchange_format_is_fixed_after_first_exchange(m):
+    p = m.Ctx.for_cfg(workloads.keys(1), mode=m.binding.MODE_PAIR_LOOPBACK)
+    assert p.exchange == 0                      # loopback default: LL
+    p.set_exchange(1)
+    x = p.share(torch.from_numpy(workloads.act_inputs(64)).cuda())
+    p.relu(x)
+    with pytest.raises(m.MPCError):
+        p.set_exchange(0)
+    with pytest.raises(m.MPCError):
+        p.set_exchange(2)
     p.sync()

@@ -13,8 +13,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_pair_two_processes_bit_identical_to_both():
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_ipc_check.py")],
+@pytest.mark.parametrize("exchange", [1, 0])      # LL63 (the MPC_MODE_PAIR default) and LL
+def test_pair_two_processes_bit_identical_to_both(exchange):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_ipc_check.py"), f"--exchange={exchange}"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0 and "PAIR_IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 

@@ -450,7 +450,7 @@ def test_rsqrt_layernorm_square(mpc):
 
 
 # ------------------------------------------------ carry-cone LTZ (NEXT #1) ----
-@pytest.mark.parametrize("w", [1, 2, 3, 17, 18, 21, 32, 33])
+@pytest.mark.parametrize("w", [1, 2, 3, 5, 17, 18, 21, 32, 33, 34, 35, 47, 48, 63, 64])
 @pytest.mark.parametrize("n", [45, 4096 + 96 + 7])
 def test_cone_ltz_matches_oracle(mpc, w, n):
     """The carry cone computes the same sign bit, so the output shares equal the
@@ -461,6 +461,48 @@ def test_cone_ltz_matches_oracle(mpc, w, n):
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
     same(c.cmp(gx, off=64, window=w), o.ltz(ox, off=64, window=w))
     same(c.relu(gx, off=0, window=w), o.relu(ox, off=0, window=w))
+
+
+def _cone_gates_bruteforce(w):
+    """Pruned carry cone (ltz_cone.cuh) built node by node: leaves j < m real, j >= m public pads;
+    a node whose hi child is all pads IS its lo child (no gate); a node with two real children
+    costs a G gate, plus a P gate when its P is used (it is a hi child, or its parent's P is used)."""
+    m = w - 1
+    if m <= 0:
+        return 0
+    L = (m - 1).bit_length()
+    gates = m                                   # g-layer
+    if L == 0:
+        return gates                            # one leaf: the carry is g_0
+    def node(k, i, need_p):                     # level k over leaves [i 2^(k+1), (i+1) 2^(k+1))
+        nonlocal gates
+        lo_start, hi_start = i << (k + 1), (i << (k + 1)) + (1 << k)
+        if lo_start >= m:
+            return                              # all pads: public (0, 1)
+        if hi_start >= m:                       # copy of the lo child
+            if k > 0:
+                node(k - 1, 2 * i, need_p)
+            return
+        gates += 1 + (1 if need_p else 0)
+        if k > 0:
+            node(k - 1, 2 * i, need_p)
+            node(k - 1, 2 * i + 1, True)
+    node(L - 1, 0, False)
+    return gates
+
+
+@pytest.mark.parametrize("w", [2, 3, 9, 17, 21, 25, 33, 40, 64])
+def test_cone_gate_count_in_stats(mpc, w):
+    """bytes each party sends for one cone LTZ = groups x (8 B per AND gate + 4 B for B2A);
+    the pruned cone's gate count equals the node-by-node construction (89 at w=33, 181 at w=64)."""
+    c, _ = pair_ctx(mpc)
+    c.set_ltz_circuit(1)
+    gx = c.share(torch.zeros(32 * 10, dtype=torch.float64).cuda())
+    c.reset_stats()
+    c.cmp(gx, window=w)
+    g = _cone_gates_bruteforce(w)
+    assert c.stats()["bytes_per_party"] == 10 * (8 * g + 4)
+    assert {33: 89, 64: 181, 21: 53}.get(w, g) == g
 
 
 def test_cone_ltz_large_sampled(mpc):
@@ -499,24 +541,41 @@ def test_cone_activations(mpc, act, form, deg):
     assert c.step == o.step
 
 
-@pytest.mark.parametrize("rows,cols", [(64, 128), (45, 77), (32, 1024), (70, 9), (33, 3)])
-def test_cone_softmax_and_max(mpc, rows, cols):
+@pytest.mark.parametrize("rows,cols,w", [(64, 128, 33), (45, 77, 33), (32, 1024, 33), (70, 9, 33), (33, 3, 33),
+                                         (64, 128, 64), (45, 77, 40), (70, 9, 64), (40, 16, 21)])
+def test_cone_softmax_and_max(mpc, rows, cols, w):
     c, o = pair_ctx(mpc, 2, step=1)
     c.set_ltz_circuit(1)
     x = workloads.softmax_inputs(rows, cols)
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
-    same(c.max(gx, rows, cols, row_off=32), o.max(ox, rows, cols, row_off=32))
-    same(c.softmax(gx, rows, cols, row_off=32), o.softmax(ox, rows, cols, row_off=32))
-    same(c.softmax(gx, rows, cols, exp_square=1, recip_square=1), o.softmax(ox, rows, cols, exp_square=1, recip_square=1))
+    same(c.max(gx, rows, cols, row_off=32, window=w), o.max(ox, rows, cols, row_off=32, window=w))
+    same(c.softmax(gx, rows, cols, row_off=32, window=w), o.softmax(ox, rows, cols, row_off=32, window=w))
+    same(c.softmax(gx, rows, cols, exp_square=1, recip_square=1, window=w),
+         o.softmax(ox, rows, cols, exp_square=1, recip_square=1, window=w))
+    same(c.softmax(gx, rows, cols, causal=1, window=w), o.softmax(ox, rows, cols, causal=1, window=w))
 
 
-def test_cone_maxpool(mpc):
+@pytest.mark.parametrize("w", [33, 21, 64])
+def test_cone_maxpool(mpc, w):
     N, C, H, W = 2, 16, 14, 15
     c, o = pair_ctx(mpc, 4, step=1)
     c.set_ltz_circuit(1)
     x = workloads.maxpool_inputs((N, C, H, W)) - 0.25
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
-    same(c.maxpool2d(gx, N, C, H, W, 3, 2, 1, img_off=2), o.maxpool2d(ox, N, C, H, W, 3, 2, 1, img_off=2))
+    same(c.maxpool2d(gx, N, C, H, W, 3, 2, 1, img_off=2, window=w),
+         o.maxpool2d(ox, N, C, H, W, 3, 2, 1, img_off=2, window=w))
+
+
+@pytest.mark.parametrize("w", [40, 64])
+def test_cone_activations_wide(mpc, w):
+    c, o = pair_ctx(mpc, step=4)
+    c.set_ltz_circuit(1)
+    n = 4096 + 99
+    x = workloads.act_inputs(n)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    knobs = mpc.default_act("gelu", "poly_abs", degree=4)
+    same(c.gelu(gx, form="poly_abs", degree=4, window=w),
+         o.act(ox, "gelu", "poly_abs", 4, knobs["B"], knobs["coeffs"], window=w))
 
 
 # ------------------------------------------------- T5: fused = composed (row ops) ----

@@ -22,7 +22,12 @@ def t(fn, reps=20):
     for _ in range(reps): fn()
     b.record(s); torch.cuda.synchronize()
     return a.elapsed_time(b) / reps
+r5, c5 = workloads.SHAPES["cfg5_ln"]
+l5 = c.share(torch.from_numpy(workloads.layernorm_inputs(r5, c5)).cuda())
+z5 = c._empty(r5 * c5)
 r = [f"softmax {t(lambda: c.softmax(x, rows, cols, out=z)):.4f}",
+     f"layernorm {t(lambda: c.layernorm(l5, r5, c5, out=z5)):.4f}",
+     f"relu {t(lambda: c.relu(g, out=z3)):.4f}",
      f"gelu {t(lambda: c.gelu(g, form='poly_abs', degree=4, out=z3)):.4f}",
      f"exp {t(lambda: c.exp(g, t=8, out=z3)):.4f}",
      f"mul {t(lambda: c.mul(g, g, trunc_bits=16, out=z3)):.4f}"]

@@ -10,7 +10,8 @@ LayerNorm), and an open to party 1 only.
 
   python tools/pair_ipc_check.py             (prints PAIR_IPC_OK on success, exit code 0)
   python tools/pair_ipc_check.py --mismatch  (debug header check: the parties issue different ops;
-                                              prints PAIR_IPC_PROTOCOL_DETECTED)"""
+                                              prints PAIR_IPC_PROTOCOL_DETECTED)
+  python tools/pair_ipc_check.py --exchange=0 (the LL wire format instead of the LL63 default)"""
 import os
 import sys
 
@@ -64,6 +65,8 @@ def worker(rank, world, port, q, mismatch=False):
     x = torch.from_numpy(workloads.softmax_inputs(rows, cols).ravel()).cuda(dev)
     keys = workloads.keys(2)
     c = m.Ctx.for_cfg(keys, device=dev, mode=m.binding.MODE_PAIR, party=rank)
+    if "--exchange=0" in sys.argv:
+        c.set_exchange(0)                             # LL instead of the LL63 default
     pair.connect(c)
     if mismatch:
         # debug header check: party 0 issues mul, party 1 square (same step count and rounds, so
