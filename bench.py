@@ -281,8 +281,21 @@ def run_mpc200(args):
     # ---- e2e: host buffers through the public API (H2D inputs, D2H outputs inside the region) ----
     # mpc_softmax_hostio: chunks of 3072 rows, H2D / compute / D2H of neighbouring chunks overlapped
     # on separate streams (tools/perf_e2e.py: 1.21 ms sequential -> 0.80 ms per cfg2 step)
-    hin = tuple(s.cpu().pin_memory() if s is not None else None for s in xs)
-    hout = tuple(torch.empty_like(h).pin_memory() if h is not None else None for h in hin)
+    # both parties' shares in ONE pinned [2][n] host tensor each way, so a chunk's two party copies
+    # are one pitched 2D DMA submission (copy_pair in mpc200.cu)
+    def pinned_pair(src):
+        live = [s for s in src if s is not None]
+        buf = torch.empty((2, live[0].numel()), dtype=live[0].dtype).pin_memory()
+        out = []
+        for q, s in enumerate(src):
+            if s is None:
+                out.append(None)
+            else:
+                buf[q].copy_(s.reshape(-1).cpu())
+                out.append(buf[q])
+        return tuple(out)
+    hin = pinned_pair(xs)
+    hout = pinned_pair(tuple(torch.empty_like(s) if s is not None else None for s in xs))
     e2e_steps = max(3, min(args.steps, 10))
     ctx.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=3072, **sm_kw)    # warm-up
     job.barrier()

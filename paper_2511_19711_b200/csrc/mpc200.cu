@@ -1427,20 +1427,21 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
     return MPC_OK;
 }
 
-// The two parties' copies of one chunk and direction as one batched DMA submission: with both PCIe
-// directions busy, every separate cudaMemcpyAsync costs ~9 us of link time (tools/pcie_copy.cu: cfg2,
-// 4 chunks x 2 parties both ways, 0.649 ms as single copies vs 0.551 ms batched).  Under stream
-// capture the plain copies are used.
-static void copy_batch(void** dst, void** src, size_t bytes, int n, cudaStream_t s, cudaMemcpyKind kind)
+// The two parties' copies of one chunk and direction as ONE DMA submission: with both PCIe directions
+// busy, every separate cudaMemcpyAsync costs ~9 us of link time (tools/pcie_copy.cu: cfg2, 4 chunks x
+// 2 parties both ways).  The two chunks are the two rows of a pitched 2D copy when both sides' party
+// arrays are ordered and at most 2 GB apart (e.g. one pinned [2][n] host tensor); otherwise one copy
+// per party.
+static void copy_pair(void** dst, void** src, size_t bytes, int n, cudaStream_t s, cudaMemcpyKind kind)
 {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cs);
-    if (n > 1 && cs == cudaStreamCaptureStatusNone) {
-        size_t sz[2] = {bytes, bytes}, idx = 0, fail = 0;
-        cudaMemcpyAttributes at{};
-        at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        if (cudaMemcpyBatchAsync(dst, src, sz, (size_t)n, &at, &idx, 1, &fail, s) == cudaSuccess) return;
-        cudaGetLastError();                        // not supported here: fall back to single copies
+    if (n == 2) {
+        const char *d0 = (const char*)dst[0], *d1 = (const char*)dst[1];
+        const char *s0 = (const char*)src[0], *s1 = (const char*)src[1];
+        const int64_t dp = d1 - d0, sp = s1 - s0, lim = (int64_t)1 << 31;
+        if (dp >= (int64_t)bytes && sp >= (int64_t)bytes && dp < lim && sp < lim) {
+            if (cudaMemcpy2DAsync(dst[0], (size_t)dp, src[0], (size_t)sp, bytes, 2, kind, s) == cudaSuccess) return;
+            cudaGetLastError();                    // pitch not accepted: fall back to single copies
+        }
     }
     for (int q = 0; q < n; ++q) cudaMemcpyAsync(dst[q], src[q], bytes, kind, s);
 }
@@ -1540,7 +1541,7 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         {
             void* dst[2]; void* src[2];
             for (int q = 0; q < np; ++q) { dst[q] = dx[parties[p0 + q]]; src[q] = hx.sh[parties[p0 + q]] + r0 * cols; }
-            copy_batch(dst, src, bytes, np, h->h2d, cudaMemcpyHostToDevice);
+            copy_pair(dst, src, bytes, np, h->h2d, cudaMemcpyHostToDevice);
         }
         cudaEventRecord(h->in_ready[b], h->h2d);
         mark(h->h2d);
@@ -1562,7 +1563,7 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         {
             void* dst[2]; void* src[2];
             for (int q = 0; q < np; ++q) { dst[q] = hz.sh[parties[p0 + q]] + r0 * cols; src[q] = dz[parties[p0 + q]]; }
-            copy_batch(dst, src, bytes, np, h->d2h, cudaMemcpyDeviceToHost);
+            copy_pair(dst, src, bytes, np, h->d2h, cudaMemcpyDeviceToHost);
         }
         cudaEventRecord(h->out_done[b], h->d2h);
         mark(h->d2h);

@@ -71,21 +71,6 @@ int main()
                     cudaMemcpyAsync((char*)hz[q] + i * cb, (char*)dz[q] + i * cb, cb, cudaMemcpyDeviceToHost, s2);
                 }
         }, name);
-        snprintf(name, sizeof name, "DMA batch (cudaMemcpyBatchAsync), %d chunks x 2 parties", nch);
-        timeit([&] {
-            for (int i = 0; i < nch; ++i) {
-                void* d1[2] = {(char*)dx[0] + i * cb, (char*)dx[1] + i * cb};
-                void* s1p[2] = {(char*)hx[0] + i * cb, (char*)hx[1] + i * cb};
-                void* d2[2] = {(char*)hz[0] + i * cb, (char*)hz[1] + i * cb};
-                void* s2p[2] = {(char*)dz[0] + i * cb, (char*)dz[1] + i * cb};
-                size_t sz[2] = {cb, cb};
-                cudaMemcpyAttributes at{};
-                at.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-                size_t idx = 0, fail = 0;
-                cudaMemcpyBatchAsync(d1, s1p, sz, 2, &at, &idx, 1, &fail, s1);
-                cudaMemcpyBatchAsync(d2, s2p, sz, 2, &at, &idx, 1, &fail, s2);
-            }
-        }, name);
         if (hx[1] > hx[0] && hz[1] > hz[0] && dx[1] > dx[0] && dz[1] > dz[0]) {
             snprintf(name, sizeof name, "DMA 2D (both parties one copy), %d chunks", nch);
             timeit([&] {
