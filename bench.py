@@ -147,14 +147,39 @@ class Job:
             self.party, self.peer, self.pair_idx, self.npairs = 0, None, 0, 1
             self.mode = m.binding.MODE_BOTH
         self.stream = torch.cuda.current_stream(self.dev)
+        self.dealer = None                 # PAIR party 1: the trusted dealer's offline context
+        self.stream_words = 0              # correction words party 1 read in the last prefed block
 
     def ctx(self, cfg, mode=None):
         mode = self.mode if mode is None else mode
-        c = self.m.Ctx.for_cfg(workloads.keys(cfg), device=self.local, mode=mode, party=self.party)
+        keys = workloads.keys(cfg)
+        if mode == self.m.binding.MODE_PAIR and self.party == 1 and os.environ.get("MPC_BENCH_DEALER", "1") == "1":
+            # party 1 never receives K_0; the trusted dealer makes its
+            # correction words OFFLINE, before each timed block (prefeed), on party 1's GPU
+            self.dealer = self.m.Ctx.dealer(keys, device=self.local)
+            keys = dict(keys, key_p0=0)
+        c = self.m.Ctx.for_cfg(keys, device=self.local, mode=mode, party=self.party)
         if mode == self.m.binding.MODE_PAIR:
             from paper_2511_19711_b200 import pair
             pair.connect(c)
         return c
+
+    def prefeed(self, ctx, fn, count):
+        """PAIR party 1 with a dealer: the dealer runs the next `count` calls fn(c) offline (same
+        shapes and step ids; it ignores the share pointers) and party 1 will read that stream."""
+        if self.dealer is None or ctx.mode != self.m.binding.MODE_PAIR:
+            return
+        self.torch.cuda.synchronize()
+        d = self.dealer
+        d.dealer_reset()
+        d.set_step(ctx.step, force=True)
+        d.set_ltz_circuit(ctx.circuit)
+        for _ in range(count):
+            fn(d)
+        stream = d.dealer_stream()
+        self.stream_words = stream[1]
+        ctx.set_corrections(stream)
+        self.torch.cuda.synchronize()
 
     def share(self, ctx, x, off):
         """Party 0 owns the activations: in PAIR mode party 1 derives its share r
@@ -265,8 +290,11 @@ def run_mpc200(args):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=job.dev)   # 512 MB > 126 MB L2
     sm_kw = dict(window=33, exp_t=8, exp_clamp=0, recip_iters=10, recip_t=8)
 
-    def step():
-        ctx.softmax(xs, rows, cols, row_off=row_off, out=out, **sm_kw)
+    def step(c=ctx):
+        c.softmax(xs, rows, cols, row_off=row_off, out=out, **sm_kw)
+
+    job.prefeed(ctx, step, args.warmup + args.steps)              # PAIR party 1: the dealer's offline pass
+    stream_words_per_step = job.stream_words / max(1, args.warmup + args.steps)
 
     s_before = ctx.step
     for _ in range(args.warmup):
@@ -276,6 +304,14 @@ def run_mpc200(args):
     ms_step, kt, st, clk = timed(job, ctx, step, args.steps, flush, Clocks(job.local))
     value = job.npairs * n / (ms_step / 1e3)
     roof = roofline(job, ctx.mode, kt, st, args.steps, ms_step, n, ctx.exchange)
+    if job.ws > 1:
+        sw = job.maxr(stream_words_per_step)          # party 1's rank holds the stream
+        roof["dealer"] = ({"party1_stream_bytes_per_step": int(8 * sw),
+                           "party1_stream_hbm_frac": round(8 * sw / (ms_step / 1e3) / 1e9 /
+                                                           float(load_peaks().get("hbm_gbs", 6650.0)), 5),
+                           "how": "party 1 reads the trusted dealer's correction words (made offline before the "
+                                  "timed block, DESIGN.md 7.1); its context has no K_0"}
+                          if dealer_on(job) else {"simulated_by_party1": True})
     parity = check_timed_output(job, ctx.step - steps_per_call, xs, out, rows, cols, row_off, sm_kw)
 
     # ---- e2e: host buffers through the public API (H2D inputs, D2H outputs inside the region) ----
@@ -297,6 +333,8 @@ def run_mpc200(args):
     hin = pinned_pair(xs)
     hout = pinned_pair(tuple(torch.empty_like(s) if s is not None else None for s in xs))
     e2e_steps = max(3, min(args.steps, 10))
+    job.prefeed(ctx, lambda c=ctx: c.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=3072, **sm_kw),
+                1 + e2e_steps)
     ctx.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=3072, **sm_kw)    # warm-up
     job.barrier()
     torch.cuda.synchronize()
@@ -385,7 +423,13 @@ def check_timed_output(job, step_id, xs, out, rows, cols, row_off, sm_kw, tiles=
         return {"ok": None, "error": f"{type(e).__name__}: {e}"[:200]}
 
 
+def dealer_on(job):
+    """PAIR with the trusted dealer's correction stream for party 1 (uniform over ranks)."""
+    return job.ws > 1 and os.environ.get("MPC_BENCH_DEALER", "1") == "1"
+
+
 def _op_line(job, ctx, fn, n, flush, args, config):
+    job.prefeed(ctx, fn, max(1, args.warmup) + args.steps)       # PAIR party 1: the dealer's offline pass
     for _ in range(max(1, args.warmup)):
         fn()
     job.torch.cuda.synchronize()
@@ -421,36 +465,36 @@ def time_per_op(job, m, ctx, flush, args):
     n3 = workloads.SHAPES["cfg3_gelu"]
     g = job.share(ctx, workloads.normal_inputs(n3, 3), k * n3)
     z = ctx._empty(n3)
-    out["gelu"] = _op_line(job, ctx, lambda: ctx.gelu(g, off=k * n3, form="poly_abs", degree=4, out=z), n3, flush,
+    out["gelu"] = _op_line(job, ctx, lambda c=ctx: c.gelu(g, off=k * n3, form="poly_abs", degree=4, out=z), n3, flush,
                            args, "cfg3: BERT-base FFN 8x128x3072, |x|-form deg 4, B=3")
     del g, z
     N, C, H, W = workloads.SHAPES["cfg4_relu_first"]
     n4 = N * C * H * W // 4
     r = job.share(ctx, workloads.relu_inputs(n4), k * n4)
     z = ctx._empty(n4)
-    out["relu"] = _op_line(job, ctx, lambda: ctx.relu(r, off=k * n4, out=z), n4, flush, args,
+    out["relu"] = _op_line(job, ctx, lambda c=ctx: c.relu(r, off=k * n4, out=z), n4, flush, args,
                            "cfg4: ResNet-50 first ReLU, 8 images x 64 x 112 x 112, window 33")
     del r, z
     Np, Cp, Hp, Wp = 8, 64, 112, 112                  # one pair's 8-image shard of the MaxPool input
     mp = job.share(ctx, workloads.maxpool_inputs((Np, Cp, Hp, Wp)), k * Np * Cp * Hp * Wp)
     no = Np * Cp * 56 * 56
     z = ctx._empty(no)
-    out["maxpool"] = _op_line(job, ctx, lambda: ctx.maxpool2d(mp, Np, Cp, Hp, Wp, 3, 2, 1, img_off=k * Np, out=z),
+    out["maxpool"] = _op_line(job, ctx, lambda c=ctx: c.maxpool2d(mp, Np, Cp, Hp, Wp, 3, 2, 1, img_off=k * Np, out=z),
                               no, flush, args, "cfg4: ResNet-50 MaxPool 3x3/2 pad 1, 8 x 64 x 112^2 -> 56^2 "
                               "(elements = outputs, 8 comparisons each)")
     del mp, z
     rows5, cols5 = workloads.SHAPES["cfg5_ln"]
     ln = job.share(ctx, workloads.layernorm_inputs(rows5, cols5), k * rows5 * cols5)
     z = ctx._empty(rows5 * cols5)
-    out["layernorm"] = _op_line(job, ctx, lambda: ctx.layernorm(ln, rows5, cols5, row_off=k * rows5, out=z),
+    out["layernorm"] = _op_line(job, ctx, lambda c=ctx: c.layernorm(ln, rows5, cols5, row_off=k * rows5, out=z),
                                 rows5 * cols5, flush, args, "cfg5: GPT-2 LayerNorm 8192 x 768, rsqrt 3 iters")
     del ln, z
     rs, cs = 8 * 12 * 128, 1024
     sm = job.share(ctx, workloads.softmax_inputs(rs, cs, seed_cfg=5), k * rs * cs)
     z = ctx._empty(rs * cs)
-    out["softmax1024"] = _op_line(job, ctx, lambda: ctx.softmax(sm, rs, cs, row_off=k * rs, out=z), rs * cs, flush,
+    out["softmax1024"] = _op_line(job, ctx, lambda c=ctx: c.softmax(sm, rs, cs, row_off=k * rs, out=z), rs * cs, flush,
                                   args, "cfg5: GPT-2 softmax rows of 1024 (12288 rows = 1/8 layer), t=8, NR 10")
-    out["softmax1024_causal"] = _op_line(job, ctx, lambda: ctx.softmax(sm, rs, cs, row_off=k * rs, causal=1, out=z),
+    out["softmax1024_causal"] = _op_line(job, ctx, lambda c=ctx: c.softmax(sm, rs, cs, row_off=k * rs, causal=1, out=z),
                                          rs * cs, flush, args,
                                          "cfg5: GPT-2 causal softmax (12 x 1024 x 1024 blocks, DESIGN.md 2.12)")
     del sm, z
@@ -458,53 +502,56 @@ def time_per_op(job, m, ctx, flush, args):
     # bit-identical to the Kogge-Stone contract's, square triples change the shares)
     x2 = job.share(ctx, workloads.softmax_inputs(*workloads.SHAPES["cfg2_softmax"]), k * 12288 * 128)
     z = ctx._empty(12288 * 128)
-    out["softmax_clamp"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_clamp=1,
+    out["softmax_clamp"] = _op_line(job, ctx, lambda c=ctx: c.softmax(x2, 12288, 128, row_off=k * 12288, exp_clamp=1,
                                                                   out=z), 12288 * 128, flush, args,
                                     "cfg2 softmax with exp t=8+clamp (max-accuracy knob)")
-    out["softmax_bcast"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, bcast=1, out=z),
+    out["softmax_bcast"] = _op_line(job, ctx, lambda c=ctx: c.softmax(x2, 12288, 128, row_off=k * 12288, bcast=1, out=z),
                                     12288 * 128, flush, args, "cfg2 softmax, broadcast triple for e*r (NEXT #2)")
-    out["softmax_square"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1,
+    out["softmax_square"] = _op_line(job, ctx, lambda c=ctx: c.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1,
                                                                    recip_square=1, out=z), 12288 * 128, flush, args,
                                      "cfg2 softmax with square-pair triples in every exp squaring (NEXT #2)")
     ctx.set_ltz_circuit(1)
-    out["softmax_cone"] = _op_line(job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, out=z),
+    out["softmax_cone"] = _op_line(job, ctx, lambda c=ctx: c.softmax(x2, 12288, 128, row_off=k * 12288, out=z),
                                    12288 * 128, flush, args, "cfg2 softmax, carry-cone LTZ in the max tree (NEXT #1)")
     out["softmax_cone_square"] = _op_line(
-        job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1, recip_square=1, out=z),
+        job, ctx, lambda c=ctx: c.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1, recip_square=1, out=z),
         12288 * 128, flush, args, "cfg2 softmax, carry-cone LTZ + square-pair triples (NEXT #1 + #2)")
     out["softmax_next_all"] = _op_line(
-        job, ctx, lambda: ctx.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1, recip_square=1, bcast=1,
+        job, ctx, lambda c=ctx: c.softmax(x2, 12288, 128, row_off=k * 12288, exp_square=1, recip_square=1, bcast=1,
                                       out=z),
         12288 * 128, flush, args, "cfg2 softmax, carry cone + square-pair triples + broadcast triple (NEXT #1 + #2)")
     del x2, z
     g = job.share(ctx, workloads.normal_inputs(n3, 3), k * n3)
     z = ctx._empty(n3)
-    out["gelu_cone"] = _op_line(job, ctx, lambda: ctx.gelu(g, off=k * n3, form="poly_abs", degree=4, out=z), n3,
+    out["gelu_cone"] = _op_line(job, ctx, lambda c=ctx: c.gelu(g, off=k * n3, form="poly_abs", degree=4, out=z), n3,
                                 flush, args, "cfg3 GELU |x|-form deg 4, carry-cone LTZ (NEXT #1)")
     out["gelu_cone_power"] = _op_line(
-        job, ctx, lambda: ctx.gelu(g, off=k * n3, form="poly_abs", degree=4, basis=1, out=z), n3, flush, args,
+        job, ctx, lambda c=ctx: c.gelu(g, off=k * n3, form="poly_abs", degree=4, basis=1, out=z), n3, flush, args,
         "cfg3 GELU |x|-form deg 4, carry-cone LTZ + power basis (NEXT #1 + #2)")
     del g, z
     r = job.share(ctx, workloads.relu_inputs(n4), k * n4)
     z = ctx._empty(n4)
-    out["relu_cone"] = _op_line(job, ctx, lambda: ctx.relu(r, off=k * n4, out=z), n4, flush, args,
+    out["relu_cone"] = _op_line(job, ctx, lambda c=ctx: c.relu(r, off=k * n4, out=z), n4, flush, args,
                                 "cfg4 ReLU shard, carry-cone LTZ (NEXT #1)")
     del r, z
     ctx.set_ltz_circuit(0)
     Bm, Mm, Km, Nm = 1, 1024, 768, 3072           # BERT-base FFN Linear (8 x 128 tokens), NEXT #3
-    xm = job.share(ctx, workloads.act_inputs(Mm * Km, lo=-2, hi=2), k * Mm * Km)
-    ym = job.share(ctx, workloads.act_inputs(Km * Nm, seed_cfg=5, lo=-2, hi=2), k * Km * Nm)
-    z = ctx._empty(Mm * Nm)
-    out["matmul_tc"] = _op_line(job, ctx, lambda: ctx.matmul(xm, ym, Bm, Mm, Km, Nm, batch_off=k, trunc_bits=16,
-                                                             out=z), Mm * Nm, flush, args,
-                                "Beaver matmul 1024 x 768 x 3072 (BERT FFN Linear), tcgen05 kind::i8 on 8-bit limbs "
-                                "(elements = outputs; 2.4 G ring MACs)")
-    del xm, ym, z
+    if dealer_on(job):                            # the matrix triple is not stream-fed
+        out["matmul_tc"] = {"skipped": "PAIR with the trusted dealer's stream: matmul's C1 is not stream-fed"}
+    else:
+        xm = job.share(ctx, workloads.act_inputs(Mm * Km, lo=-2, hi=2), k * Mm * Km)
+        ym = job.share(ctx, workloads.act_inputs(Km * Nm, seed_cfg=5, lo=-2, hi=2), k * Km * Nm)
+        z = ctx._empty(Mm * Nm)
+        out["matmul_tc"] = _op_line(job, ctx, lambda c=ctx: c.matmul(xm, ym, Bm, Mm, Km, Nm, batch_off=k,
+                                                                     trunc_bits=16, out=z), Mm * Nm, flush, args,
+                                    "Beaver matmul 1024 x 768 x 3072 (BERT FFN Linear), tcgen05 kind::i8 on 8-bit "
+                                    "limbs (elements = outputs; 2.4 G ring MACs)")
+        del xm, ym, z
     nm = 1 << 24
     a = job.share(ctx, workloads.act_inputs(nm), k * nm)
     b = job.share(ctx, workloads.act_inputs(nm, seed_cfg=7), k * nm)
     z = ctx._empty(nm)
-    out["mul"] = _op_line(job, ctx, lambda: ctx.mul(a, b, off=k * nm, trunc_bits=16, out=z), nm, flush, args,
+    out["mul"] = _op_line(job, ctx, lambda c=ctx: c.mul(a, b, off=k * nm, trunc_bits=16, out=z), nm, flush, args,
                           "Beaver multiply + trunc, 16M elements")
     del a, b, z
     torch.cuda.synchronize()

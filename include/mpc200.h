@@ -54,14 +54,22 @@ typedef enum {
     MPC_MODE_BOTH = 0,          /* one GPU simulates both parties; openings add in registers   */
     MPC_MODE_PAIR = 1,          /* one GPU (process) per party; every opening is exchanged by  *
                                  * the fused kernels through NVLink peer memory. *
-                                 * TRUST MODEL: the trusted dealer is SIMULATED by    *
-                                 * party 1, whose context needs key_p0 to form its correction  *
-                                 * terms (c1 = ab - c0, AND-triple c1, daBit r1A; reading R7). *
-                                 * Party 1 can therefore regenerate party 0's masks: this mode *
-                                 * gives NO privacy against party 1 (a benchmark / protocol-   *
-                                 * shape configuration, not a deployment).                    */
-    MPC_MODE_PAIR_LOOPBACK = 2  /* both parties' PAIR kernels in one launch on one GPU,        *
+                                 * TRUST MODEL: party 1's correction terms (Beaver / square /  *
+                                 * broadcast c1, AND-triple c1, daBit r1A) come from the       *
+                                 * trusted dealer as a correction stream              *
+                                 * (mpc_ctx_set_corrections, produced offline by an            *
+                                 * MPC_MODE_DEALER context): party 1's context then never      *
+                                 * uses K_0 (its key_p0 may be 0).  Without a stream, party 1  *
+                                 * SIMULATES the dealer from key_p0 (reading R7) and can       *
+                                 * regenerate party 0's masks: no privacy against party 1.    */
+    MPC_MODE_PAIR_LOOPBACK = 2, /* both parties' PAIR kernels in one launch on one GPU,        *
                                  * exchanging through local memory (same code path; tests)    */
+    MPC_MODE_DEALER = 3         /* the trusted dealer's offline pass for party 1 (DESIGN.md    *
+                                 * 7.1): holds K_0 and K_1, issues the SAME calls with the     *
+                                 * same shapes, offsets and knobs as party 1 (share pointers   *
+                                 * may be NULL: no share is read or written, nothing is        *
+                                 * exchanged) and appends party 1's correction words to its    *
+                                 * stream (mpc_dealer_stream).  cfg.party must be 1.          */
 } mpc_mode;
 
 typedef struct {
@@ -134,11 +142,42 @@ mpc_status mpc_ctx_set_exchange(mpc_ctx* ctx, int fmt);
 int        mpc_ctx_get_exchange(const mpc_ctx* ctx);   /* current format, -1 for a NULL context */
 
 /* LTZ carry circuit: 0 = full Kogge-Stone (the S7 contract, default),
- * 1 = carry cone (only the carry into bit w-1: 94 AND gates at w = 33 instead of 290, same
- * rounds), used for windows <= 33.  The output shares of every op are
+ * 1 = carry cone (only the carry into bit w-1, pruned: 89 AND gates at w = 33 instead of 290,
+ * 181 at w = 64 instead of 693, same rounds), every window 1..64.  The output shares of every op are
  * bit-identical under both circuits (they depend only on the sign and the daBit); only the
  * transcript, the PRG work and the bytes sent change. */
 mpc_status mpc_ctx_set_ltz_circuit(mpc_ctx* ctx, int circuit);
+
+/* ---- the trusted dealer's correction stream ("distributed in advance by a trusted
+ * third-party") ---------------------------------------------------------------
+ * Every PAIR kernel launch of party 1 consumes one SEGMENT of the stream: words
+ * [base, base + depth * threads) of the device word array, where word base + k * threads + t is
+ * the k-th correction of the launch's thread t (threads = the party's CTAs x block size, depth =
+ * corrections per thread, tag = a hash of the kernel family).  A DEALER context appends one
+ * segment per launch, in the order party 1 will launch; it runs the same kernels with the same
+ * grid as party 1 and synchronizes after each launch (an offline pass). */
+typedef struct { uint64_t base, threads, depth, tag; } mpc_corr_seg;
+/* Grid the dealer sizes its launches for: MPC_MODE_PAIR (default, party 1 on its own GPU) or
+ * MPC_MODE_PAIR_LOOPBACK (party 1's CTAs inside a loopback launch).  MPC_ERR_INVALID on a
+ * non-dealer context or another mode. */
+mpc_status mpc_dealer_set_target(mpc_ctx* dealer, int target_mode);
+/* View of the stream so far: *words is a device pointer owned by the dealer context (valid until
+ * its next call or destruction), *segs a host array owned by it. */
+mpc_status mpc_dealer_stream(const mpc_ctx* dealer, const uint64_t** words, uint64_t* n_words,
+                             const mpc_corr_seg** segs, int64_t* n_segs);
+/* Start a new, empty stream (keeps the allocation). */
+mpc_status mpc_dealer_reset(mpc_ctx* dealer);
+/* Party 1 (MPC_MODE_PAIR with party 1, or MPC_MODE_PAIR_LOOPBACK): consume these corrections,
+ * segment by segment in launch order, instead of deriving them from K_0.  words: device pointer
+ * on the context's device, owned by the caller, valid until consumed; segs is copied.  A launch
+ * whose next segment is missing or does not match (tag, threads) fails with MPC_ERR_PROTOCOL.
+ * words == NULL and n_segs == 0 clears the stream (party 1 derives from K_0 again).
+ * MPC_ERR_INVALID on party 0, BOTH or DEALER contexts.  mpc_matmul is not stream-fed
+ * (MPC_ERR_UNSUPPORTED while a stream is set). */
+mpc_status mpc_ctx_set_corrections(mpc_ctx* ctx, const uint64_t* words, uint64_t n_words,
+                                   const mpc_corr_seg* segs, int64_t n_segs);
+/* Segments not consumed yet; -1 when no stream is set. */
+int64_t    mpc_ctx_corrections_left(const mpc_ctx* ctx);
 
 /* Ring-GEMM engine of mpc_matmul: 0 = auto (tensor cores whenever the limb
  * accumulators are exact, i.e. K <= 5461), 1 = SIMT (IMAD u64 multiply-adds), 2 = tensor cores

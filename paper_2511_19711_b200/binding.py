@@ -27,7 +27,7 @@ i64 = ctypes.c_int64
 INT = ctypes.c_int
 VP = ctypes.c_void_p
 
-MODE_BOTH, MODE_PAIR, MODE_PAIR_LOOPBACK = 0, 1, 2
+MODE_BOTH, MODE_PAIR, MODE_PAIR_LOOPBACK, MODE_DEALER = 0, 1, 2, 3
 PAIR_HANDLE_BYTES = 64
 FORM = {"poly_x": 0, "poly_abs": 1, "relu": 2, "erf": 3}
 STATUS = {0: "OK", 1: "INVALID", 2: "RANGE", 3: "CUDA", 4: "NCCL", 5: "PROTOCOL", 6: "REUSE",
@@ -51,6 +51,10 @@ class Stats(ctypes.Structure):
 
 class KernelTime(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char_p), ("ms", ctypes.c_float), ("philox", u64), ("units", u64)]
+
+
+class CorrSeg(ctypes.Structure):
+    _fields_ = [("base", u64), ("threads", u64), ("depth", u64), ("tag", u64)]
 
 
 class ExpP(ctypes.Structure):
@@ -90,6 +94,11 @@ _SIGS = {
     "mpc_ctx_enable_kernel_timing": [VP, INT],
     "mpc_ctx_set_ltz_circuit": [VP, INT],
     "mpc_ctx_set_matmul_engine": [VP, INT],
+    "mpc_dealer_set_target": [VP, INT],
+    "mpc_dealer_stream": [VP, C(VP), C(u64), C(VP), C(i64)],
+    "mpc_dealer_reset": [VP],
+    "mpc_ctx_set_corrections": [VP, VP, u64, VP, i64],
+    "mpc_ctx_corrections_left": [VP],
     "mpc_pair_export": [VP, VP],
     "mpc_pair_connect": [VP, VP],
     "mpc_ctx_sync": [VP],
@@ -122,8 +131,9 @@ _SIGS = {
     "mpc_layernorm": [VP, Shares, Shares, i64, i64, i64, C(LnP)],
 }
 _RESTYPE = {"mpc_ctx_get_step": u64, "mpc_last_error": ctypes.c_char_p, "mpc_version": ctypes.c_char_p,
-            "mpc_last_call_philox": u64}
-_OPTIONAL = {"mpc_ctx_set_exchange", "mpc_ctx_get_exchange"}     # absent in older A/B builds (MPC200_LIB)
+            "mpc_last_call_philox": u64, "mpc_ctx_corrections_left": i64}
+_OPTIONAL = {"mpc_ctx_set_exchange", "mpc_ctx_get_exchange", "mpc_dealer_set_target", "mpc_dealer_stream",
+             "mpc_dealer_reset", "mpc_ctx_set_corrections", "mpc_ctx_corrections_left"}   # absent in older A/B builds
 for _n, _a in list(_SIGS.items()):
     try:
         _f = getattr(_L, _n)
@@ -169,7 +179,7 @@ class MPCError(RuntimeError):
 
 
 def _ptr(t):
-    if t is None:
+    if t is None or t.device.type == "meta":      # meta: a shape-only operand (the dealer's calls)
         return None
     if not t.is_cuda:
         raise ValueError("mpc200 compute calls take CUDA tensors")
@@ -216,6 +226,48 @@ class Ctx:
     def for_cfg(cls, keys: dict, device: int = 0, **kw):
         return cls(keys["key_share"], keys["key_p0"], keys["key_p1"], device, **kw)
 
+    # ---- the trusted dealer's correction stream ----
+    @classmethod
+    def dealer(cls, keys: dict, device: int = 0, target: int = MODE_PAIR):
+        """An MPC_MODE_DEALER context for party 1 of a PAIR (or, target=MODE_PAIR_LOOPBACK, loopback)
+        execution: call the same ops with the same shapes as party 1 (operands may be shape-only
+        `meta` tensors, see `like`); its stream then feeds party 1 (set_corrections)."""
+        d = cls(keys["key_share"], keys["key_p0"], keys["key_p1"], device, mode=MODE_DEALER, party=1)
+        d._chk(_L.mpc_dealer_set_target(d._h, target), "mpc_dealer_set_target")
+        return d
+
+    @staticmethod
+    def like(n: int):
+        """A shape-only share pair for the dealer's calls (no device memory)."""
+        return (torch.empty(n, dtype=torch.uint64, device="meta"), None)
+
+    def dealer_stream(self):
+        """(device word pointer, n_words, [segments]) of the dealer's stream so far; the words stay
+        owned by this (dealer) context."""
+        w, nw, sg, ns = VP(), u64(), VP(), i64()
+        self._chk(_L.mpc_dealer_stream(self._h, ctypes.byref(w), ctypes.byref(nw), ctypes.byref(sg), ctypes.byref(ns)),
+                  "mpc_dealer_stream")
+        segs = (CorrSeg * max(ns.value, 1))()
+        if ns.value:
+            ctypes.memmove(segs, sg.value, ctypes.sizeof(CorrSeg) * ns.value)
+        return w.value, int(nw.value), list(segs)[:ns.value]
+
+    def dealer_reset(self):
+        self._chk(_L.mpc_dealer_reset(self._h), "mpc_dealer_reset")
+
+    def set_corrections(self, stream):
+        """Party 1: read the dealer's correction words (a `dealer_stream()` triple, words on this
+        device) instead of deriving them from K_0; None clears."""
+        if stream is None:
+            self._chk(_L.mpc_ctx_set_corrections(self._h, None, 0, None, 0), "mpc_ctx_set_corrections")
+            return
+        w, nw, segs = stream
+        arr = (CorrSeg * max(len(segs), 1))(*segs)
+        self._chk(_L.mpc_ctx_set_corrections(self._h, w, nw, ctypes.cast(arr, VP), len(segs)), "mpc_ctx_set_corrections")
+
+    def corrections_left(self) -> int:
+        return int(_L.mpc_ctx_corrections_left(self._h))
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
@@ -252,9 +304,12 @@ class Ctx:
             return 0
         return int(_L.mpc_ctx_get_exchange(self._h))
 
+    circuit = 0
+
     def set_ltz_circuit(self, circuit: int):
         """0 = Kogge-Stone (default, the S7 contract), 1 = carry cone (NEXT #1): same output shares."""
         self._chk(_L.mpc_ctx_set_ltz_circuit(self._h, circuit), "mpc_ctx_set_ltz_circuit")
+        self.circuit = circuit
 
     def set_matmul_engine(self, engine: int):
         """0 auto, 1 SIMT, 2 tensor cores (tcgen05 on 8-bit limbs); same output shares."""
@@ -296,6 +351,8 @@ class Ctx:
         return int(_L.mpc_last_call_philox(self._h))
 
     def _empty(self, n):
+        if self.mode == MODE_DEALER:
+            return self.like(n)
         mk = lambda: torch.empty(n, dtype=torch.uint64, device=self.device)  # noqa: E731
         if self.mode in (MODE_BOTH, MODE_PAIR_LOOPBACK):
             return (mk(), mk())
@@ -324,6 +381,8 @@ class Ctx:
 
     def open(self, s, scale_bits: int = 16, want_ring=True, want_f64=True):
         n = (s[0] if s[0] is not None else s[1]).numel()
+        if self.mode == MODE_DEALER:
+            want_ring = want_f64 = False
         ring = torch.empty(n, dtype=torch.uint64, device=self.device) if want_ring else None
         f = torch.empty(n, dtype=torch.float64, device=self.device) if want_f64 else None
         self._stream()

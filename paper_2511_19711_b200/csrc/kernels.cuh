@@ -33,15 +33,27 @@ struct BothA {
     __device__ __forceinline__ void done(BothP&) const {}
 };
 
-struct PairA {
+// launch arguments of both PAIR roles (identical layout: the host fills one PairArgs for either)
+struct PairArgs {
     Keys K;
     int party;        // remote mode: this GPU's party
     int loopback;     // 1: both parties in one launch
     int G;            // CTAs per party
     int fmt;          // exchange wire format (proto.cuh): 0 LL, 1 LL63
     XMem xm[2];       // exchange memory of party 0 / 1 (remote: xm[0] only)
-    __device__ __forceinline__ PairP make(int& cta, int& ncta) const {
-        PairP p;
+    // dealer correction stream (proto.cuh PairP::corr): cmode 1 = party 1 reads it,
+    // 2 = this launch is the dealer and writes it (party 1's role over a self-loop exchange); the
+    // segment is [ccap or depth][G * blockDim] words at cw; kmax: the dealer's words-per-thread
+    // high-water mark.  Used by the stream role (R = 1) only.
+    u64* cw;
+    u32 ccap;
+    int cmode;
+    u32* kmax;
+};
+template <int R>
+struct PairAR : PairArgs {
+    __device__ __forceinline__ PairP<R> make(int& cta, int& ncta) const {
+        PairP<R> p;
         p.Kp = &K;
         int slot_cta;
         if (loopback) { p.pty = blockIdx.x >= (unsigned)G ? 1 : 0; slot_cta = blockIdx.x - p.pty * G; }
@@ -49,11 +61,25 @@ struct PairA {
         cta = slot_cta; ncta = G;
         p.local = loopback;
         p.fmt = fmt;
+        if constexpr (R == 1) {
+            p.cmode = p.pty == 1 ? cmode : 0;
+            p.cst = (u32)G * blockDim.x;
+            p.cw = p.cmode ? cw + (u64)slot_cta * blockDim.x + threadIdx.x : nullptr;
+            p.ck = 0;
+            p.ccap = ccap;
+        }
         p.bind(xm[loopback ? p.pty : 0], slot_cta * (blockDim.x >> 5) + (threadIdx.x >> 5));
         return p;
     }
-    __device__ __forceinline__ void done(PairP& p) const { p.unbind(threadIdx.x & 31); }
+    __device__ __forceinline__ void done(PairP<R>& p) const {
+        p.unbind(threadIdx.x & 31);
+        if constexpr (R == 1)
+            if (p.cmode == 2 && p.ck) atomicMax(kmax, p.ck);
+    }
 };
+using PairA = PairAR<0>;     // party 0; party 1 simulating the dealer; loopback
+using PairAS = PairAR<1>;    // the stream roles: party 1 reading the dealer's stream, the dealer itself
+static_assert(sizeof(PairA) == sizeof(PairArgs) && sizeof(PairAS) == sizeof(PairArgs), "one argument layout");
 
 // ------------------------------------------------------------------ drivers ----
 // GROUP driver: warp <-> 32-unit LTZ group, lane <-> unit.  off % 32 == 0.
@@ -504,9 +530,69 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
     }
 }
 
+// ---- BOTH mode: the per-row Newton-Raphson chain with its triples generated ahead ----------------
+// The NR chain (exp squarings + iters x 2 (recip) / 3 (rsqrt) Beaver steps on the tile's 32 row
+// units) is one warp's serial dependency chain, and each step used to wait on its own 2.5 Philox
+// blocks.  The triples are data-independent, so ALL warps of the CTA generate them first (nr_pregen,
+// unit pairs: 5 blocks per pair and Beaver step, the contract's c0 sharing) into a
+// shared-memory table; the chain (warp 0, BothTabP) then only opens and forms the shares.  Same
+// steps, units, PRG words and output bits as recip_group / rsqrt_group on BothP.  Clamped exp
+// (an LTZ inside the chain) keeps the direct path.
+constexpr int NR_TAB_F = 5;                           // words per (step, row): a0 b0 c0 a b (square: a0 - c0 a)
+__host__ __device__ inline int nr_tab_steps(int kind, int t, int iters) { return t + (kind ? 3 : 2) * iters; }
+#ifndef MPC_NR_TAB_MAX_STEPS
+#define MPC_NR_TAB_MAX_STEPS 32                       // 32 steps x 32 rows x 5 words = 40 KB of shared memory
+#endif
+template <int KIND>
+__device__ __forceinline__ void nr_pregen(const Keys& K, u32 s, const NrK& p, u64 g0, u64* T)
+{
+    const int t = p.exp.t, ns = nr_tab_steps(KIND, t, p.iters);
+    for (int it = threadIdx.x; it < ns * 16; it += blockDim.x) {
+        const int j = it >> 4, l = 2 * (it & 15);
+        const u64 u = g0 + (u64)l;                    // even (g0 is a multiple of 32)
+        const u32 sj = s + (u32)j;
+        u64* R = T + (i64)j * NR_TAB_F * 32 + l;
+        if (j < t && p.exp.sq) {                      // square-pair triple
+            const uint4 A0u = prg(K.k0, u, sj, 2), A0v = prg(K.k0, u + 1, sj, 2), A1 = prg(K.k1, u >> 1, sj, 3);
+            R[0] = w64(A0u.x, A0u.y); R[1] = w64(A0v.x, A0v.y);
+            R[64] = w64(A0u.z, A0u.w); R[65] = w64(A0v.z, A0v.w);
+            R[96] = R[0] + w64(A1.x, A1.y); R[97] = R[1] + w64(A1.z, A1.w);
+        } else {                                      // Beaver triple
+            const uint4 A0u = prg(K.k0, u, sj, 0), A1u = prg(K.k1, u, sj, 0);
+            const uint4 A0v = prg(K.k0, u + 1, sj, 0), A1v = prg(K.k1, u + 1, sj, 0);
+            const uint4 C = prg(K.k0, u >> 1, sj, 1);
+            R[0] = w64(A0u.x, A0u.y); R[1] = w64(A0v.x, A0v.y);
+            R[32] = w64(A0u.z, A0u.w); R[33] = w64(A0v.z, A0v.w);
+            R[64] = w64(C.x, C.y); R[65] = w64(C.z, C.w);
+            R[96] = R[0] + w64(A1u.x, A1u.y); R[97] = R[1] + w64(A1v.x, A1v.y);
+            R[128] = R[32] + w64(A1u.z, A1u.w); R[129] = R[33] + w64(A1v.z, A1v.w);
+        }
+    }
+}
+// BothP with bm / sq of the chain's steps read from the table (lane <-> row unit g0 + lane)
+struct BothTabP : BothP {
+    const u64* T; u32 sb;
+    __device__ __forceinline__ S bm(u64, u32 s, S x, S y) const {
+        const u64* R = T + (i64)(s - sb) * NR_TAB_F * 32 + (threadIdx.x & 31);
+        const u64 a0 = R[0], b0 = R[32], c0 = R[64], a = R[96], b = R[128];
+        const u64 X = x.s0 + x.s1, Y = y.s0 + y.s1;
+        const u64 e = X - a, f = Y - b;               // open(x - a), open(y - b)
+        const u64 z0 = c0 + e * (b0 + f) + f * a0;    // = mpc::bm_with_c0
+        return {z0, X * Y - z0};
+    }
+    __device__ __forceinline__ S sq(u64, u32 s, S y) const {
+        const u64* R = T + (i64)(s - sb) * NR_TAB_F * 32 + (threadIdx.x & 31);
+        const u64 a0 = R[0], c0 = R[64], a = R[96];
+        const u64 Y = y.s0 + y.s1, e = Y - a;
+        const u64 z0 = c0 + e * (2ull * a0 + e);      // = mpc::sq_with_a1
+        return {z0, Y * Y - z0};
+    }
+};
+
 // per-row Newton-Raphson over the tile's rows: warp 0, lane <-> row (LTZ group = the tile)
+// tab (BOTH mode only): the chain's triples, already generated by nr_pregen<KIND> for (s, g0)
 template <int KIND, bool WIDE, class P>
-__device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g0, SP x, SO y)
+__device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g0, SP x, SO y, const u64* tab = nullptr)
 {
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
@@ -514,8 +600,20 @@ __device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g
         typename P::S xv = pr.zero();
         if (valid) xv = pr.ld(x, lane);
         typename P::S r;
-        if (KIND == 0) r = recip_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
-        else r = rsqrt_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
+        bool done = false;
+        if constexpr (!P::kPair) {
+            if (tab) {
+                BothTabP tp;
+                tp.Kp = pr.Kp; tp.T = tab; tp.sb = s;
+                if (KIND == 0) r = recip_group<WIDE>(tp, g0 + lane, g0 >> 5, s, p, xv, lane);
+                else r = rsqrt_group<WIDE>(tp, g0 + lane, g0 >> 5, s, p, xv, lane);
+                done = true;
+            }
+        }
+        if (!done) {
+            if (KIND == 0) r = recip_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
+            else r = rsqrt_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
+        }
         if (valid) pr.st(y, lane, r);
     }
     __syncthreads();
@@ -582,6 +680,7 @@ struct SoftmaxArgs {
     int esmem;              // E tile in the work area (aliasing the dead max-tree levels), not escratch
     int causal;             // causal attention rows
     u64 causal_L;           // public constant of the masked max-tree inputs, -2^(w-2)
+    int nrtab;              // BOTH: the reciprocal chain's triples pre-generated into smem (nr_pregen)
 };
 
 // work tile (u64 words), HA = ceil(cols/2), HB = ceil(HA/2): A0 A1 (2 x 32HA), B0 B1 (2 x 32HB),
@@ -594,9 +693,9 @@ __host__ __device__ inline i64 softmax_x_off(i64 cols, bool esmem)
     const i64 HA = (cols + 1) / 2, HB = (HA + 1) / 2;
     return esmem ? (64 * cols > 64 * HA + 64 * HB ? 64 * cols : 64 * HA + 64 * HB) : 64 * HA + 64 * HB;
 }
-__host__ __device__ inline i64 softmax_work_u64(i64 cols, bool esmem = false)
+__host__ __device__ inline i64 softmax_work_u64(i64 cols, bool esmem = false, i64 tab_u64 = 0)
 {
-    return softmax_x_off(cols, esmem) + 9 * 32;
+    return softmax_x_off(cols, esmem) + 9 * 32 + tab_u64;   // [.. X (9 x 32)] [NR triple table]
 }
 
 // LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33), 3 carry cone
@@ -620,6 +719,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     SO E{{Ew, Ew + 32 * C}};
     u64* X = W + softmax_x_off(C, a.esmem != 0);
     SO MX{{X, X + 32}}, SS{{X + 64, X + 96}}, RR{{X + 128, X + 160}};
+    u64* const nrt = a.nrtab ? X + 9 * 32 : nullptr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const i64 ntiles = (a.rows + 31) / 32;
     const FastDiv dC = make_fastdiv((u32)C);
@@ -635,6 +735,10 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
 #endif
         if (!(MPC_SOFTMAX_SKIP & 1))
         tile_max<WIDE, CONE, decltype(pr), CAUSAL>(pr, a.s_max, a.w, xt, C, C, R, g0, A, B, HA, HB, MX, cone_sm, a.causal_L);
+        // BOTH: every warp generates the reciprocal chain's triples now (tile_nr's warp-0 chain then
+        // only opens and multiplies); the exp phase's closing barrier orders it before the chain
+        if constexpr (!decltype(pr)::kPair)
+            if (nrt) nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0, nrt);
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;
@@ -715,7 +819,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         }
         __syncthreads();
         // 5. r = RECIP(S), row units
-        if (!(MPC_SOFTMAX_SKIP & 4)) tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR);
+        if (!(MPC_SOFTMAX_SKIP & 4)) tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR, nrt);
         // 6. out = MT(e, r), element units
         const SP Rc{{RR.p[0], RR.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
@@ -1220,3 +1324,165 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_quad(const __gr
 }
 
 }  // namespace mpc
+
+// ---------------------------------------------------------------- fused row-block LayerNorm ----
+// LAYERNORM in ONE launch, element-balanced: a CTA owns RB consecutive rows (RB even, <= 32,
+// chosen so that every CTA is resident at once) and its 8 warps split the block's ELEMENT PAIRS
+// evenly (a row is not a warp's unit: 768-wide rows over 8 warps would leave the row chains uneven):
+//   A  row sums (per-lane running sums, flushed to shared memory with u64 atomics when the lane's row
+//      changes -- ring addition, so the order cannot change a bit)  -> mu = x E(1/d) | floor / d
+//   B  MT(c, c), c = x - mu (element units, unit pairs), the same per-row reduction -> v = mean + eps
+//   C  RSQRT(v) over the block's rows (row units; BOTH: the chain's triples generated by all warps
+//      first, nr_pregen<1>), warp 0 lane <-> row
+//   D  out = MT(c, r) (element units, unit pairs)
+// Same steps, units, PRG words and output bits as k_ln / the stats-rsqrt-product launches (units:
+// rows for the rsqrt, global elements for the two Beaver passes); no clamp (an LTZ in the rsqrt would
+// need 32-row groups) and no broadcast triple -- those keep the other paths.  x is read three times
+// (the block's rows stay L2-resident between the passes).
+struct LnFArgs {
+    u32 s_sq, s_rs, s_mul; NrK rk; SP x; SO z; i64 rows, cols; u64 row_off;
+    int mean_mode; u64 e_invd, e_eps;
+    int RB;                 // rows per block (even)
+    int nrtab;              // BOTH: rsqrt triples pre-generated into shared memory
+};
+template <class PA>
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_fused(const __grid_constant__ PA pa, LnFArgs a)
+{
+    extern __shared__ __align__(16) u64 lsm[];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using P = decltype(pr);
+    using S = typename P::S;
+    constexpr int V = P::kV;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const i64 C = a.cols;
+    const FastDiv dC = make_fastdiv((u32)C);
+    // shared: row sums SA (2 x 32), means MU, variance sums SV, rsqrt RS (each 2 x 32), NR table
+    u64* SA = lsm; u64* MUw = lsm + 64; u64* SV = lsm + 128; u64* RSw = lsm + 192;
+    u64* tab = a.nrtab ? lsm + 256 : nullptr;
+    const SO MU{{MUw, MUw + 32}}, RS{{RSw, RSw + 32}};
+    const SP MUc{{MUw, MUw + 32}}, RSc{{RSw, RSw + 32}};
+    auto flush = [&](u64* base, int r, S v) {           // per-row ring sum (both parties in BOTH)
+        if constexpr (P::kPair) atomicAdd((unsigned long long*)&base[32 * pr.party() + r], (unsigned long long)v);
+        else { atomicAdd((unsigned long long*)&base[r], (unsigned long long)v.s0);
+               atomicAdd((unsigned long long*)&base[32 + r], (unsigned long long)v.s1); }
+    };
+    auto getsum = [&](const u64* base, int r) -> S {
+        if constexpr (P::kPair) return base[32 * pr.party() + r];
+        else return S{base[r], base[32 + r]};
+    };
+    const i64 nblk = (a.rows + a.RB - 1) / a.RB;
+    for (i64 blk = cta; blk < nblk; blk += ncta) {
+        const i64 r0 = blk * a.RB;
+        const int R = (int)min((i64)a.RB, a.rows - r0);
+        const u64 g0 = a.row_off + (u64)r0;                   // even
+        const i64 np = (i64)R * C / 2;                       // element pairs of the block (C even)
+        const i64 wbeg = np * warp / NW, wend = np * (warp + 1) / NW;
+        const i64 iters = (wend - wbeg + 32 * V - 1) / (32 * V);   // warp-uniform trip count
+        const u64 ub = g0 * (u64)C;                           // global unit of the block's element 0
+        const SP xb{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
+        const SO zb{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
+        for (int t = threadIdx.x; t < 256; t += blockDim.x) lsm[t] = 0;
+        __syncthreads();
+        // A: row sums
+        {
+            S acc = pr.zero();
+            int cur = -1;
+            for (i64 it = 0; it < iters; ++it)
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 P2 = wbeg + (it * V + v) * 32 + lane;
+                    if (P2 < wend) {
+                        S xa, xc;
+                        pr.ld_pair(xb, 2 * P2, true, true, xa, xc);
+                        const int r = (int)fdiv((u32)(2 * P2), dC);
+                        if (r != cur) { if (cur >= 0) flush(SA, cur, acc); cur = r; acc = pr.zero(); }
+                        acc = pr.add(acc, pr.add(xa, xc));
+                    }
+                }
+            if (cur >= 0) flush(SA, cur, acc);
+        }
+        __syncthreads();
+        if (threadIdx.x < R) {
+            S mu = getsum(SA, threadIdx.x);
+            mu = a.mean_mode == 0 ? pr.mulf(mu, a.e_invd) : pr.divp(mu, C);
+            pr.st(MU, threadIdx.x, mu);
+        }
+        __syncthreads();
+        // B: sum of MT(c, c)
+        {
+            S acc = pr.zero();
+            int cur = -1;
+            for (i64 it = 0; it < iters; ++it) {
+                u64 u[V];
+                S ca[V], cb[V], za[V], zb2[V];
+                int rr[V];
+                bool ok[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 P2 = wbeg + (it * V + v) * 32 + lane;
+                    ok[v] = P2 < wend;
+                    u[v] = ub + 2 * (u64)P2;
+                    ca[v] = cb[v] = pr.zero();
+                    rr[v] = 0;
+                    if (ok[v]) {
+                        pr.ld_pair(xb, 2 * P2, true, true, ca[v], cb[v]);
+                        rr[v] = (int)fdiv((u32)(2 * P2), dC);
+                        const S m = pr.ld(MUc, rr[v]);
+                        ca[v] = pr.sub(ca[v], m);
+                        cb[v] = pr.sub(cb[v], m);
+                    }
+                }
+                pr.template bm2v<V>(u, a.s_sq, ca, ca, cb, cb, za, zb2);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (ok[v]) {
+                        if (rr[v] != cur) { if (cur >= 0) flush(SV, cur, acc); cur = rr[v]; acc = pr.zero(); }
+                        acc = pr.add(acc, pr.add(pr.shr_(za[v], FRAC), pr.shr_(zb2[v], FRAC)));
+                    }
+            }
+            if (cur >= 0) flush(SV, cur, acc);
+        }
+        __syncthreads();
+        if (threadIdx.x < R) {
+            S v = getsum(SV, threadIdx.x);
+            v = a.mean_mode == 0 ? pr.mulf(v, a.e_invd) : pr.divp(v, C);
+            v = pr.addp(v, a.e_eps);
+            pr.st(SO{{SV, SV + 32}}, threadIdx.x, v);     // the variance replaces its sum
+        }
+        if constexpr (!P::kPair)
+            if (tab) nr_pregen<1>(*pr.Kp, a.s_rs, a.rk, g0, tab);
+        __syncthreads();
+        // C: r = RSQRT(v), row units g0 + lane
+        tile_nr<1, false>(pr, a.s_rs, a.rk, R, g0, SP{{SV, SV + 32}}, RS, tab);
+        // D: out = MT(c, r)
+        for (i64 it = 0; it < iters; ++it) {
+            u64 u[V];
+            S ca[V], cb[V], ra[V], za[V], zb2[V];
+            i64 e0[V];
+            bool ok[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const i64 P2 = wbeg + (it * V + v) * 32 + lane;
+                ok[v] = P2 < wend;
+                e0[v] = 2 * P2;
+                u[v] = ub + 2 * (u64)P2;
+                ca[v] = cb[v] = ra[v] = pr.zero();
+                if (ok[v]) {
+                    pr.ld_pair(xb, e0[v], true, true, ca[v], cb[v]);
+                    const int r = (int)fdiv((u32)e0[v], dC);
+                    const S m = pr.ld(MUc, r);
+                    ca[v] = pr.sub(ca[v], m);
+                    cb[v] = pr.sub(cb[v], m);
+                    ra[v] = pr.ld(RSc, r);
+                }
+            }
+            pr.template bm2v<V>(u, a.s_mul, ca, ra, cb, ra, za, zb2);
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                if (ok[v]) pr.st_pair(zb, e0[v], true, true, pr.shr_(za[v], FRAC), pr.shr_(zb2[v], FRAC));
+        }
+        __syncthreads();
+    }
+    pa.done(pr);
+}

@@ -148,8 +148,8 @@ __device__ void ltz_cone_both(const Keys& K, u64 q0, u32 s, int w, const Sh (&x)
 // ---------------------------------------------------------------- PAIR ----
 // Same circuit, one party's shares; the g-layer, every tree level and the B2A are ONE warp
 // exchange each, carrying all G groups' words (so 1 + L + 1 rounds per G groups).
-template <int G, int NL>
-__device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G], u64 (&z)[G], int lane,
+template <int G, int NL, int R>
+__device__ void ltz_cone_pair(PairP<R>& pr, u64 q0, u32 s, int w, const u64 (&x)[G], u64 (&z)[G], int lane,
                               ConeSmem<G, NL>& sm)
 {
     constexpr int H = NL / 32;
@@ -171,7 +171,7 @@ __device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G]
                 ta[g][h] = tb[g][h] = tc[g][h] = 0;
                 dd[g][h] = ee[g][h] = 0;
                 if (j < m) {
-                    const uint4 t0 = prg(K.k0, q0 + g, s, ltz_slot(0, j, 0));
+                    const uint4 t0 = pr.k0ok() ? prg(K.k0, q0 + g, s, ltz_slot(0, j, 0)) : make_uint4(0, 0, 0, 0);
                     uint4 t1 = make_uint4(0, 0, 0, 0);
                     if (pty == 1) t1 = prg(K.k1, q0 + g, s, ltz_slot(0, j, 0));
                     pr.and_triple(t0, t1, 0, ta[g][h], tb[g][h], tc[g][h]);
@@ -219,12 +219,11 @@ __device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G]
                 gh[v] = 0;
                 if (valid) { gl = sm.w[g][lo][0]; pl = sm.w[g][lo][2]; ph = sm.w[g][hi][2]; gh[v] = sm.w[g][hi][0]; }
                 const u64 q = q0 + (u64)g;
-                const uint4 tg = prg(K.k0, q, s, ltz_slot(k + 1, i, 0));
-                const uint4 tp = prg(K.k0, q, s, ltz_slot(k + 1, i, 1));
+                uint4 tg = make_uint4(0, 0, 0, 0), tp = tg;
+                if (pr.k0ok()) { tg = prg(K.k0, q, s, ltz_slot(k + 1, i, 0)); tp = prg(K.k0, q, s, ltz_slot(k + 1, i, 1)); }
                 uint4 t1 = make_uint4(0, 0, 0, 0);
                 if (pty == 1) t1 = prg(K.k1, q, s, ltz_slot(k + 1, i, 0));
-                pr.and_triple(tg, t1, 0, ga[v], gb[v], gc[v]);
-                pr.and_triple(tp, t1, 1, pa[v], pb[v], pc[v]);
+                pr.and_triple2(tg, tp, t1, ga[v], gb[v], gc[v], pa[v], pb[v], pc[v]);
                 dG[v] = ph ^ ga[v]; eG[v] = gl ^ gb[v];
                 dP[v] = ph ^ pa[v]; eP[v] = pl ^ pb[v];
                 pr.put(lane, 2 * v, (u64)dG[v] | ((u64)eG[v] << 32), valid);
@@ -254,13 +253,11 @@ __device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G]
         u32 bp;
         if (m == 0) bp = (u32)(x[g] & 1ull);
         else bp = (u32)((x[g] >> (w - 1)) & 1ull) ^ ((sm.w[g][0][0] >> lane) & 1u);
-        const uint4 D0 = prg(K.k0, q0 + g, s, 2u + (u32)lane);
-        const u64 r0A = w64(D0.x, D0.y);
-        const u32 r0B = D0.z & 1u;
+        const uint4 D0 = pr.k0ok() ? prg(K.k0, q0 + g, s, 2u + (u32)lane) : make_uint4(0, 0, 0, 0);
         const u32 d1x = __shfl_sync(FULL, k1w, g);
         u32 rB;
-        if (pty == 0) { rA[g] = r0A; rB = r0B; }
-        else { rB = (d1x >> lane) & 1u; rA[g] = (u64)(r0B ^ rB) - r0A; }
+        if (pty == 0) { rA[g] = w64(D0.x, D0.y); rB = D0.z & 1u; }
+        else { rB = (d1x >> lane) & 1u; rA[g] = pr.dabit_r1A(D0, rB); }
         mine[g] = bp ^ rB;
         pr.put(lane, g, (u64)mine[g]);
     }

@@ -67,6 +67,17 @@ struct mpc_ctx {
     int nvtx_open;          // an op-level NVTX range is open (begin_op .. finish)
     int xfmt;               // PAIR exchange wire format (proto.cuh): 0 LL, 1 LL63
     int xused;              // a PAIR exchange kernel has been launched (the format is then fixed)
+    // trusted dealer's correction stream
+    int dtarget;            // DEALER: the grid its launches are sized for (MPC_MODE_PAIR / _PAIR_LOOPBACK)
+    u64* dw;                // DEALER: stream words (device), capacity and words used
+    u64 dw_cap, dw_end;
+    u32* dkmax;             // DEALER: device high-water mark (corrections per thread) of one launch
+    u32 dcap;               // DEALER: per-thread capacity the next launch is tried with
+    mpc_corr_seg* segv;     // DEALER: segments produced; party 1: segments to consume
+    i64 nseg, capseg;
+    const u64* cwords;      // party 1: the stream being consumed (caller-owned device words)
+    i64 cnext;              // party 1: next segment
+    int corr_on;            // party 1: corrections come from the stream (K_0 unused)
 };
 
 // Pipelined host-buffer execution: chunk i goes H2D on `h2d`, computes on cs[i % HIO_SLOTS] with its
@@ -85,8 +96,16 @@ struct HostIO {
     bool used[HIO_SLOTS];
 };
 
-static bool is_pair(const mpc_ctx* c) { return c->cfg.mode != MPC_MODE_BOTH; }
+static bool is_pair(const mpc_ctx* c) { return c->cfg.mode != MPC_MODE_BOTH; }   // PAIR, LOOPBACK, DEALER
 static bool is_loop(const mpc_ctx* c) { return c->cfg.mode == MPC_MODE_PAIR_LOOPBACK; }
+static bool is_dealer(const mpc_ctx* c) { return c->cfg.mode == MPC_MODE_DEALER; }
+// FNV-1a of a launch's kernel-family name: the tag of its correction-stream segment
+static u64 fnv_tag(const char* name)
+{
+    u64 h = 1469598103934665603ull;
+    for (const char* q = name; *q; ++q) { h ^= (u8)*q; h *= 1099511628211ull; }
+    return h;
+}
 
 static cudaEvent_t ev_get(mpc_ctx* c)
 {
@@ -306,7 +325,9 @@ static XMem xmem_of(const mpc_ctx* c, int which)
     m.rx = (u64*)(b + a.rx_off); m.flag = (u64*)(b + a.flag_off); m.round = (u64*)(b + a.round_off);
     m.tags = (u32*)(b + a.tags_off);
     m.err = (int*)(b + a.err_off); m.slots = c->slots;
-    if (is_loop(c)) {
+    if (is_dealer(c)) {                               // the dealer's self-loop (proto.cuh PairP)
+        m.prx = m.rx; m.pflag = m.flag;
+    } else if (is_loop(c)) {
         const XAlloc& o = c->xa[1 - which];
         char* ob = (char*)o.base;
         m.prx = (u64*)(ob + o.rx_off); m.pflag = (u64*)(ob + o.flag_off);
@@ -317,9 +338,9 @@ static XMem xmem_of(const mpc_ctx* c, int which)
     return m;
 }
 
-static PairA pair_args(const mpc_ctx* c, int G)
+static PairArgs pair_args(const mpc_ctx* c, int G)
 {
-    PairA pa;
+    PairArgs pa;
     pa.K = c->K;
     pa.party = c->cfg.party;
     pa.loopback = is_loop(c) ? 1 : 0;
@@ -330,37 +351,111 @@ static PairA pair_args(const mpc_ctx* c, int G)
     return pa;
 }
 
-// CTAs per party for a PAIR launch: every CTA of both parties must be co-resident
-template <class Kern>
-static int pair_ctas(mpc_ctx* c, Kern kern, size_t dyn, i64 want, int tpb = TPB)
+// A PAIR kernel in its two roles (kernels.cuh PairAR): r0 = PairA (party 0, the simulated dealer,
+// loopback), r1 = PairAS (party 1 reading the dealer's stream, the dealer's own pass)
+template <class K0, class K1> struct KRoles { K0 r0; K1 r1; };
+template <class K0, class K1> static KRoles<K0, K1> kroles(K0 a, K1 b) { return {a, b}; }
+static bool stream_role(const mpc_ctx* c) { return is_dealer(c) || c->corr_on; }
+template <class KR>
+static void set_smem_attr(KR k, int bytes)
 {
-    int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, tpb, dyn) != cudaSuccess || nb < 1) nb = 1;
-    i64 cap = (i64)nb * c->sm_count / (is_loop(c) ? 2 : 1);
+    cudaFuncSetAttribute(k.r0, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(k.r1, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+// CTAs per party for a PAIR launch: every CTA of both parties must be co-resident.  The same G for
+// both roles (min occupancy), so party 0 (role 0), party 1 (either role) and the dealer pair up.
+template <class KR>
+static int pair_ctas(mpc_ctx* c, KR kk, size_t dyn, i64 want, int tpb = TPB)
+{
+    int nb = 0, nb1 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kk.r0, tpb, dyn) != cudaSuccess || nb < 1) nb = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb1, kk.r1, tpb, dyn) != cudaSuccess || nb1 < 1) nb1 = 1;
+    nb = std::min(nb, nb1);
+    const bool halves = is_loop(c) || (is_dealer(c) && c->dtarget == MPC_MODE_PAIR_LOOPBACK);
+    i64 cap = (i64)nb * c->sm_count / (halves ? 2 : 1);
     cap = std::min<i64>(cap, c->slots / (tpb / 32));
     i64 G = std::min<i64>(want, cap);
     return (int)std::max<i64>(G, 1);
 }
 
-template <class Kern, class... Args>
-static mpc_status launch_pair_kernel_tpb(mpc_ctx* c, Kern kern, int G, size_t dyn, int tpb, const char* name, Args... args);
+template <class KR, class... Args>
+static mpc_status launch_pair_kernel_tpb(mpc_ctx* c, KR kk, int G, size_t dyn, int tpb, const char* name, Args... args);
 
-template <class Kern, class... Args>
-static mpc_status launch_pair_kernel(mpc_ctx* c, Kern kern, int G, size_t dyn, const char* name, Args... args)
+template <class KR, class... Args>
+static mpc_status launch_pair_kernel(mpc_ctx* c, KR kk, int G, size_t dyn, const char* name, Args... args)
 {
-    return launch_pair_kernel_tpb(c, kern, G, dyn, TPB, name, args...);
+    return launch_pair_kernel_tpb(c, kk, G, dyn, TPB, name, args...);
 }
 
+// The dealer's offline pass of one launch: party 1's kernel with the same grid in
+// the dealer role (cmode 2: no exchange, no share access), writing the launch's corrections as one
+// stream segment; relaunched with a larger per-thread capacity if the high-water mark exceeds it.
 template <class Kern, class... Args>
-static mpc_status launch_pair_kernel_tpb(mpc_ctx* c, Kern kern, int G, size_t dyn, int tpb, const char* name, Args... args)
+static mpc_status dealer_launch(mpc_ctx* c, Kern kern, int G, size_t dyn, int tpb, const char* name, Args... args)
 {
+    PairArgs pa;
+    memset(&pa, 0, sizeof pa);
+    pa.K = c->K; pa.party = 1; pa.loopback = 0; pa.G = G; pa.fmt = c->xfmt; pa.cmode = 2;
+    pa.xm[0] = pa.xm[1] = xmem_of(c, 0);
+    const u64 T = (u64)G * (u64)tpb;
+    if (!c->dkmax && cudaMalloc(&c->dkmax, sizeof(u32)) != cudaSuccess) { c->dkmax = nullptr; return fail(c, MPC_ERR_NOMEM, "dealer counter"); }
+    if (!c->dcap) c->dcap = 64;
+    u32 kmax = 0;
+    for (;;) {
+        const u64 need = c->dw_end + (u64)c->dcap * T;
+        if (need > c->dw_cap) {                       // grow (offline: synchronous is fine)
+            const u64 ncap = std::max<u64>(need, 2 * c->dw_cap);
+            u64* nw = nullptr;
+            if (cudaMalloc(&nw, ncap * sizeof(u64)) != cudaSuccess) return fail(c, MPC_ERR_NOMEM, "dealer stream %llu words", (unsigned long long)ncap);
+            if (c->dw) { cudaMemcpyAsync(nw, c->dw, c->dw_end * sizeof(u64), cudaMemcpyDeviceToDevice, c->stream); cudaStreamSynchronize(c->stream); cudaFree(c->dw); }
+            c->dw = nw; c->dw_cap = ncap;
+        }
+        pa.cw = c->dw + c->dw_end; pa.ccap = c->dcap; pa.kmax = c->dkmax;
+        cudaMemsetAsync(c->dkmax, 0, sizeof(u32), c->stream);
+        void* argv[] = {(void*)&pa, (void*)&args...};
+        rec_begin(c, name, 0);
+        cudaError_t e = cudaLaunchKernel((const void*)kern, G, tpb, argv, dyn, c->stream);
+        rec_end(c);
+        c->st.launches++;
+        if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: dealer launch: %s", name, cudaGetErrorString(e));
+        cudaMemcpyAsync(&kmax, c->dkmax, sizeof(u32), cudaMemcpyDeviceToHost, c->stream);
+        if (cudaStreamSynchronize(c->stream) != cudaSuccess) return cuda_check(c, name);
+        if (kmax <= c->dcap) break;
+        c->dcap = kmax;                               // too deep: run the launch again with room for all
+    }
+    if (c->nseg == c->capseg) {
+        c->capseg = c->capseg ? 2 * c->capseg : 64;
+        c->segv = (mpc_corr_seg*)realloc(c->segv, sizeof(mpc_corr_seg) * (size_t)c->capseg);
+    }
+    c->segv[c->nseg++] = mpc_corr_seg{c->dw_end, T, kmax, fnv_tag(name)};
+    c->dw_end += (u64)kmax * T;
+    return cuda_check(c, name);
+}
+
+template <class KR, class... Args>
+static mpc_status launch_pair_kernel_tpb(mpc_ctx* c, KR kk, int G, size_t dyn, int tpb, const char* name, Args... args)
+{
+    if (is_dealer(c)) return dealer_launch(c, kk.r1, G, dyn, tpb, name, args...);
     if (!is_loop(c) && !c->connected) return fail(c, MPC_ERR_INVALID, "%s: PAIR context not connected", name);
-    PairA pa = pair_args(c, G);
+    PairArgs pa = pair_args(c, G);
+    pa.cw = nullptr; pa.ccap = 0; pa.cmode = 0; pa.kmax = nullptr;
+    if (c->corr_on) {                                 // party 1 reads this launch's corrections
+        if (c->cnext >= c->nseg)
+            return fail(c, MPC_ERR_PROTOCOL, "%s: the dealer's correction stream is exhausted (%lld segments)", name, (long long)c->nseg);
+        const mpc_corr_seg& g = c->segv[c->cnext];
+        if (g.tag != fnv_tag(name) || g.threads != (u64)G * (u64)tpb)
+            return fail(c, MPC_ERR_PROTOCOL, "%s: correction segment %lld is for another launch (tag / %llu threads vs %llu)",
+                        name, (long long)c->cnext, (unsigned long long)g.threads, (unsigned long long)G * (u64)tpb);
+        ++c->cnext;
+        pa.cw = const_cast<u64*>(c->cwords) + g.base; pa.ccap = (u32)g.depth; pa.cmode = 1;
+    }
     c->xused = 1;
     void* argv[] = {(void*)&pa, (void*)&args...};
     const int grid = G * (is_loop(c) ? 2 : 1);
     rec_begin(c, name, 0);
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, grid, tpb, argv, dyn, c->stream);
+    const void* kern = stream_role(c) ? (const void*)kk.r1 : (const void*)kk.r0;
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, grid, tpb, argv, dyn, c->stream);
     rec_end(c);
     c->st.launches++;
     if (e != cudaSuccess) return fail(c, MPC_ERR_CUDA, "%s: cooperative launch: %s", name, cudaGetErrorString(e));
@@ -401,8 +496,9 @@ static mpc_status launch_pairs(mpc_ctx* c, i64 n, u64 off, const Body& b, const 
         c->st.launches++;
         return cuda_check(c, name);
     }
-    const int G = pair_ctas(c, k_pairs<PairA, Body>, 0, (npairs + TPB - 1) / TPB);
-    return launch_pair_kernel(c, k_pairs<PairA, Body>, G, 0, name, n, off, b);
+    const auto kk = kroles(k_pairs<PairA, Body>, k_pairs<PairAS, Body>);
+    const int G = pair_ctas(c, kk, 0, (npairs + TPB - 1) / TPB);
+    return launch_pair_kernel(c, kk, G, 0, name, n, off, b);
 }
 
 template <class Body>
@@ -423,9 +519,10 @@ static mpc_status launch_cone(mpc_ctx* c, i64 n, u64 off, const Body& b, const c
         c->st.launches++;
         return cuda_check(c, name);
     }
-    cudaFuncSetAttribute(k_groups_cone<PairA, Body>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    const int G = pair_ctas(c, k_groups_cone<PairA, Body>, dyn, (nw * 32 + TPB - 1) / TPB);
-    return launch_pair_kernel(c, k_groups_cone<PairA, Body>, G, dyn, name, n, off, b);
+    const auto kk = kroles(k_groups_cone<PairA, Body>, k_groups_cone<PairAS, Body>);
+    set_smem_attr(kk, (int)dyn);
+    const int G = pair_ctas(c, kk, dyn, (nw * 32 + TPB - 1) / TPB);
+    return launch_pair_kernel(c, kk, G, dyn, name, n, off, b);
 }
 
 template <class Body>
@@ -441,8 +538,9 @@ static mpc_status launch_groups(mpc_ctx* c, i64 n, u64 off, const Body& b, const
         c->st.launches++;
         return cuda_check(c, name);
     }
-    const int G = pair_ctas(c, k_groups<PairA, Body>, 0, (((n + 31) / 32) * 32 + TPB - 1) / TPB);
-    return launch_pair_kernel(c, k_groups<PairA, Body>, G, 0, name, n, off, b);
+    const auto kk = kroles(k_groups<PairA, Body>, k_groups<PairAS, Body>);
+    const int G = pair_ctas(c, kk, 0, (((n + 31) / 32) * 32 + TPB - 1) / TPB);
+    return launch_pair_kernel(c, kk, G, 0, name, n, off, b);
 }
 
 static const size_t SMEM_LIMIT = 56 * 1024;      // + 16 KB static cone smem: keep 3 CTAs per SM
@@ -458,7 +556,7 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
     const size_t dyn = smem ? wbytes : 0;
     if (smem) {
         cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes);
-        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wbytes);
+        set_smem_attr(kp, (int)wbytes);
     }
     int grid;
     if (!is_pair(c)) grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(kb, dyn, MPC_ROW_TPB));
@@ -488,10 +586,10 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
 static mpc_status launch_max(mpc_ctx* c, MaxArgs& a, i64 rows, i64 cols, int w, const char* name)
 {
     const i64 wk = max_work_u64(cols);
-    if (a.cone && w > 33) return launch_rows(c, k_max<3, BothA>, k_max<3, PairA>, a, rows, wk, 0, name);
-    if (w > 33) return launch_rows(c, k_max<1, BothA>, k_max<1, PairA>, a, rows, wk, 0, name);
-    if (a.cone) return launch_rows(c, k_max<2, BothA>, k_max<2, PairA>, a, rows, wk, 0, name);
-    return launch_rows(c, k_max<0, BothA>, k_max<0, PairA>, a, rows, wk, 0, name);
+    if (a.cone && w > 33) return launch_rows(c, k_max<3, BothA>, kroles(k_max<3, PairA>, k_max<3, PairAS>), a, rows, wk, 0, name);
+    if (w > 33) return launch_rows(c, k_max<1, BothA>, kroles(k_max<1, PairA>, k_max<1, PairAS>), a, rows, wk, 0, name);
+    if (a.cone) return launch_rows(c, k_max<2, BothA>, kroles(k_max<2, PairA>, k_max<2, PairAS>), a, rows, wk, 0, name);
+    return launch_rows(c, k_max<0, BothA>, kroles(k_max<0, PairA>, k_max<0, PairAS>), a, rows, wk, 0, name);
 }
 
 // short rows (cols <= MAXS_COLS, MaxPool windows): warp-per-tile kernel, windows gathered in-kernel
@@ -504,7 +602,7 @@ static mpc_status launch_max_small(mpc_ctx* c, MaxSmallArgs& a, const char* name
     const i64 nctas = (ntiles + NWARPS - 1) / NWARPS;
     auto pick = [&](auto kb, auto kp) -> mpc_status {
         cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        set_smem_attr(kp, (int)dyn);
         if (is_pair(c)) return launch_pair_kernel_tpb(c, kp, pair_ctas(c, kp, dyn, nctas, TPB), dyn, TPB, name, a);
         const int grid = (int)std::min<i64>(nctas, (i64)c->sm_count * occupancy(kb, dyn, TPB));
         rec_begin(c, name, (u64)a.rows);
@@ -513,16 +611,17 @@ static mpc_status launch_max_small(mpc_ctx* c, MaxSmallArgs& a, const char* name
         c->st.launches++;
         return cuda_check(c, name);
     };
-    if (lv == 1) return pick(k_max_small<1, BothA>, k_max_small<1, PairA>);
-    if (lv == 2) return pick(k_max_small<2, BothA>, k_max_small<2, PairA>);
-    if (lv == 3) return pick(k_max_small<3, BothA>, k_max_small<3, PairA>);
-    return pick(k_max_small<0, BothA>, k_max_small<0, PairA>);
+    if (lv == 1) return pick(k_max_small<1, BothA>, kroles(k_max_small<1, PairA>, k_max_small<1, PairAS>));
+    if (lv == 2) return pick(k_max_small<2, BothA>, kroles(k_max_small<2, PairA>, k_max_small<2, PairAS>));
+    if (lv == 3) return pick(k_max_small<3, BothA>, kroles(k_max_small<3, PairA>, k_max_small<3, PairAS>));
+    return pick(k_max_small<0, BothA>, kroles(k_max_small<0, PairA>, k_max_small<0, PairAS>));
 }
 
 // ------------------------------------------------------------------ validation helpers ----
 // shares argument valid for the mode: both pointers (BOTH / LOOPBACK) or sh[party] (PAIR)
 static bool bad_sh(const mpc_ctx* c, mpc_shares s)
 {
+    if (is_dealer(c)) return false;                   // the dealer reads and writes no shares
     if (c->cfg.mode == MPC_MODE_PAIR) {
         const uint64_t* p = s.sh[c->cfg.party];
         return !p || ((uintptr_t)p & 7);
@@ -533,12 +632,14 @@ static SP spv(const mpc_ctx* c, mpc_shares s)
 {
     SP r{{s.sh[0], s.sh[1]}};
     if (c->cfg.mode == MPC_MODE_PAIR) r.p[1 - c->cfg.party] = nullptr;
+    if (is_dealer(c)) r.p[0] = r.p[1] = nullptr;
     return r;
 }
 static SO sov(const mpc_ctx* c, mpc_shares s)
 {
     SO r{{s.sh[0], s.sh[1]}};
     if (c->cfg.mode == MPC_MODE_PAIR) r.p[1 - c->cfg.party] = nullptr;
+    if (is_dealer(c)) r.p[0] = r.p[1] = nullptr;
     return r;
 }
 
@@ -663,9 +764,11 @@ mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
 {
     if (!cfg || !out) return MPC_ERR_INVALID;
     if (cfg->frac_bits != 16) return MPC_ERR_RANGE;
-    if (cfg->mode != MPC_MODE_BOTH && cfg->mode != MPC_MODE_PAIR && cfg->mode != MPC_MODE_PAIR_LOOPBACK)
+    if (cfg->mode != MPC_MODE_BOTH && cfg->mode != MPC_MODE_PAIR && cfg->mode != MPC_MODE_PAIR_LOOPBACK &&
+        cfg->mode != MPC_MODE_DEALER)
         return MPC_ERR_INVALID;
     if (cfg->mode == MPC_MODE_PAIR && (cfg->party < 0 || cfg->party > 1)) return MPC_ERR_INVALID;
+    if (cfg->mode == MPC_MODE_DEALER && cfg->party != 1) return MPC_ERR_INVALID;   // the dealer serves party 1
     mpc_ctx* c = new mpc_ctx();
     memset(c, 0, sizeof *c);
     c->cfg = *cfg;
@@ -683,7 +786,13 @@ mpc_status mpc_ctx_create(const mpc_config* cfg, mpc_ctx** out)
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    if (cfg->mode != MPC_MODE_BOTH) {
+    c->dtarget = MPC_MODE_PAIR;
+    if (cfg->mode == MPC_MODE_DEALER) {
+        c->slots = sms * 8 * NWARPS;       // the parties' launch sizing (pair_ctas)
+        c->xfmt = 0;                       // self-loop exchange memory (LL: fewest instructions)
+        mpc_status st = xalloc(c, c->xa[0]);
+        if (st) { mpc_ctx_destroy(c); return st; }
+    } else if (cfg->mode != MPC_MODE_BOTH) {
         c->slots = sms * 8 * NWARPS;       // up to 8 resident CTAs per SM
         // default wire format: LL63 across GPUs (NVLink bytes bind), LL in loopback (local HBM:
         // LL's fewer instructions per word win, tools/ab_pair.py)
@@ -720,6 +829,9 @@ mpc_status mpc_ctx_destroy(mpc_ctx* c)
     }
     if (c->peer_base) cudaIpcCloseMemHandle(c->peer_base);
     for (int i = 0; i < 2; ++i) if (c->xa[i].base) cudaFree(c->xa[i].base);
+    if (c->dw) cudaFree(c->dw);
+    if (c->dkmax) cudaFree(c->dkmax);
+    free(c->segv);
     delete c;
     return MPC_OK;
 }
@@ -793,6 +905,63 @@ mpc_status mpc_ctx_set_ltz_circuit(mpc_ctx* c, int circuit)
     if (circuit != 0 && circuit != 1) return fail(c, MPC_ERR_RANGE, "circuit must be 0 (Kogge-Stone) or 1 (carry cone)");
     c->circuit = circuit;
     return MPC_OK;
+}
+
+mpc_status mpc_dealer_set_target(mpc_ctx* c, int target_mode)
+{
+    if (!c || !is_dealer(c) || (target_mode != MPC_MODE_PAIR && target_mode != MPC_MODE_PAIR_LOOPBACK))
+        return c ? fail(c, MPC_ERR_INVALID, "dealer_set_target: a DEALER context and MPC_MODE_PAIR / _LOOPBACK") : MPC_ERR_INVALID;
+    c->dtarget = target_mode;
+    return MPC_OK;
+}
+
+mpc_status mpc_dealer_stream(const mpc_ctx* c, const uint64_t** words, uint64_t* n_words, const mpc_corr_seg** segs,
+                             int64_t* n_segs)
+{
+    if (!c || !is_dealer(c)) return MPC_ERR_INVALID;
+    cudaStreamSynchronize(c->stream);
+    if (words) *words = c->dw;
+    if (n_words) *n_words = c->dw_end;
+    if (segs) *segs = c->segv;
+    if (n_segs) *n_segs = c->nseg;
+    return MPC_OK;
+}
+
+mpc_status mpc_dealer_reset(mpc_ctx* c)
+{
+    if (!c || !is_dealer(c)) return MPC_ERR_INVALID;
+    cudaStreamSynchronize(c->stream);
+    c->dw_end = 0;
+    c->nseg = 0;
+    return MPC_OK;
+}
+
+mpc_status mpc_ctx_set_corrections(mpc_ctx* c, const uint64_t* words, uint64_t n_words, const mpc_corr_seg* segs,
+                                   int64_t n_segs)
+{
+    if (!c) return MPC_ERR_INVALID;
+    const bool p1 = (c->cfg.mode == MPC_MODE_PAIR && c->cfg.party == 1) || is_loop(c);
+    if (!p1) return fail(c, MPC_ERR_INVALID, "set_corrections: only party 1 (PAIR party 1 or PAIR_LOOPBACK) reads a dealer stream");
+    if (!words && n_segs == 0) { c->corr_on = 0; c->cwords = nullptr; c->nseg = 0; c->cnext = 0; return MPC_OK; }
+    if (!words || n_segs < 0 || (n_segs > 0 && !segs) || ((uintptr_t)words & 7))
+        return fail(c, MPC_ERR_INVALID, "set_corrections: words / segs");
+    for (int64_t i = 0; i < n_segs; ++i)
+        if (segs[i].base + segs[i].depth * segs[i].threads > n_words || segs[i].depth >= (1ull << 32))
+            return fail(c, MPC_ERR_INVALID, "set_corrections: segment %lld outside the %llu words", (long long)i,
+                        (unsigned long long)n_words);
+    if (n_segs > c->capseg) {
+        c->capseg = n_segs;
+        c->segv = (mpc_corr_seg*)realloc(c->segv, sizeof(mpc_corr_seg) * (size_t)c->capseg);
+    }
+    if (n_segs) memcpy(c->segv, segs, sizeof(mpc_corr_seg) * (size_t)n_segs);
+    c->nseg = n_segs; c->cnext = 0; c->cwords = words; c->corr_on = 1;
+    return MPC_OK;
+}
+
+int64_t mpc_ctx_corrections_left(const mpc_ctx* c)
+{
+    if (!c || !c->corr_on) return -1;
+    return c->nseg - c->cnext;
 }
 
 mpc_status mpc_ctx_set_matmul_engine(mpc_ctx* c, int engine)
@@ -885,11 +1054,11 @@ mpc_status mpc_share(mpc_ctx* c, const void* x, int x_is_f64, int owner, mpc_sha
     if (n < 0 || off < 0) return fail(c, MPC_ERR_INVALID, "bad n/off");
     const bool pair = c->cfg.mode == MPC_MODE_PAIR;
     if (bad_sh(c, out)) return fail(c, MPC_ERR_INVALID, "share: null/misaligned output");
-    const bool need_x = !pair || c->cfg.party == owner;
+    const bool need_x = !is_dealer(c) && (!pair || c->cfg.party == owner);
     if (need_x && !x && n > 0) return fail(c, MPC_ERR_INVALID, "share: the owner needs x");
     u64* s0 = !pair || c->cfg.party == 0 ? out.sh[0] : nullptr;
     u64* s1 = !pair || c->cfg.party == 1 ? out.sh[1] : nullptr;
-    if (n > 0) {
+    if (n > 0 && !is_dealer(c)) {                      // (no corrections: the dealer has nothing to do)
         rec_begin(c, "share", (u64)n);
         k_share<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(need_x ? x : nullptr, x_is_f64, owner, s0, s1, n, (u64)off, (u32)c->step, c->K.ks);
         rec_end(c);
@@ -915,6 +1084,7 @@ mpc_status mpc_open_to(mpc_ctx* c, mpc_shares in, int64_t n, int reveal_to, uint
     if (reveal_to < -1 || reveal_to > 1) return fail(c, MPC_ERR_INVALID, "reveal_to must be -1, 0 or 1");
     if (bad_sh(c, in)) return fail(c, MPC_ERR_INVALID, "open: null pointer");
     if (n > 0) {
+        if (is_dealer(c)) { ring_out = nullptr; f64_out = nullptr; }   // same launch as party 1, no output
         if (is_pair(c)) {
             const int writer = reveal_to >= 0 ? reveal_to : (is_loop(c) ? 0 : -1);
             st = launch_groups(c, n, 0, OpenBody{spv(c, in), ring_out, f64_out, n, 1.0 / (double)(1ull << scale_bits),
@@ -940,7 +1110,7 @@ mpc_status mpc_trunc(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t n, int bits
     if (st) return st;
     if (bits < 0 || bits > 63) return fail(c, MPC_ERR_RANGE, "bits");
     if (bad_sh(c, x) || bad_sh(c, z) || n < 0) return fail(c, MPC_ERR_INVALID, "trunc args");
-    if (n > 0) {
+    if (n > 0 && !is_dealer(c)) {
         rec_begin(c, "trunc", (u64)n);
         k_trunc<<<grid_for(c, n, TPB, 16), TPB, 0, c->stream>>>(spv(c, x), sov(c, z), n, bits);
         rec_end(c);
@@ -1000,7 +1170,7 @@ mpc_status mpc_mul_bcast(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, i
             c->st.launches++;
             st = cuda_check(c, "bcast_rows");
         } else {
-            st = launch_pair_kernel(c, k_bmb_rows<PairA>, pair_ctas(c, k_bmb_rows<PairA>, 0, (nw * 32 + TPB - 1) / TPB),
+            st = launch_pair_kernel(c, kroles(k_bmb_rows<PairA>, k_bmb_rows<PairAS>), pair_ctas(c, kroles(k_bmb_rows<PairA>, k_bmb_rows<PairAS>), 0, (nw * 32 + TPB - 1) / TPB),
                                     0, "bcast_rows", ra);
         }
         if (st) return st;
@@ -1025,6 +1195,8 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
         batch * M * K >= (1ll << 40) || batch * K * N >= (1ll << 40) || batch * nparty > 65535)
         return fail(c, MPC_ERR_INVALID, "matmul: bad shape (batch x parties <= 65535 grid z)");
     if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "matmul: null pointer");
+    if (is_dealer(c) || c->corr_on)          // the matrix triple's C1 is not stream-fed
+        return fail(c, MPC_ERR_UNSUPPORTED, "matmul: no dealer correction stream for the matrix triple");
     if (batch == 0) { finish(c, 1); return MPC_OK; }
     const bool tc_ok = 3 * K <= 16384;                // exact limb accumulators (matmul_tc.cuh)
     if (c->mm_engine == 2 && !tc_ok) return fail(c, MPC_ERR_UNSUPPORTED, "matmul: tensor-core engine needs K <= 5461");
@@ -1387,11 +1559,13 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
         u64* Rw = (u64*)scratch(c, 2 * gb);
         if (!Rw) return fail(c, MPC_ERR_NOMEM, "maxpool scratch");
         SO rowsbuf = sov(c, mpc_shares{{Rw, Rw + rows * cols}});
+        if (!is_dealer(c)) {
         rec_begin(c, "pool_gather", (u64)rows);
         k_pool_gather<<<grid_for(c, rows * cols, TPB, 16), TPB, 0, c->stream>>>(spv(c, x), rowsbuf, N, C, H, W, k, stride, pad, Ho, Wo);
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "pool_gather"))) return st;
+        }
         MaxArgs a{(u32)c->step, w, SP{{rowsbuf.p[0], rowsbuf.p[1]}}, sov(c, z), rows, cols, row_off, nullptr, 0, 0,
                   nullptr, use_cone(c, w) ? 1 : 0};
         st = launch_max(c, a, rows, cols, w, "maxpool");
@@ -1507,6 +1681,17 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
     i64 maxc = 0;
     for (i64 v : sched) maxc = std::max(maxc, v);
     const size_t half = sizeof(u64) * (size_t)maxc * (size_t)cols;             // one party, one array
+    if (is_dealer(c)) {                                  // party 1's chunk computes, no copies
+        i64 rr = 0;
+        const mpc_shares none{{nullptr, nullptr}};
+        for (i64 v : sched) {
+            if ((st = softmax_core(c, none, none, v, cols, row_off + rr, p, (u32)c->step))) return st;
+            rr += v;
+        }
+        acct_softmax(c, rows, cols, p);
+        finish(c, steps);
+        return MPC_OK;
+    }
     cudaStream_t user = c->stream;
     cudaEventRecord(h->start, user);
     cudaStreamWaitEvent(h->h2d, h->start, 0);
@@ -1612,18 +1797,28 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
 #define MPC_SOFTMAX_ESMEM 1
 #endif
         a.esmem = (MPC_SOFTMAX_ESMEM && softmax_work_u64(cols, true) * 8 <= 100 * 1024) ? 1 : 0;
-        const i64 wk = softmax_work_u64(cols, a.esmem != 0), ek = a.esmem ? 0 : 64 * cols;
-        const size_t lim = a.esmem ? 100 * 1024 : SMEM_LIMIT;
+        // BOTH with E in shared memory and no clamp in the reciprocal's exp: the NR chain's triples
+        // are pre-generated by every warp into a shared-memory table (kernels.cuh nr_pregen)
+#ifndef MPC_SOFTMAX_NRTAB
+#define MPC_SOFTMAX_NRTAB 1
+#endif
+        const int nsteps = nr_tab_steps(0, p->recip.exp.t, p->recip.iters);
+        // (not with the carry cone: its 16 KB of static shared memory would leave one CTA per SM)
+        a.nrtab = (MPC_SOFTMAX_NRTAB && !is_pair(c) && a.esmem && !p->recip.exp.clamp && !a.cone &&
+                   nsteps <= MPC_NR_TAB_MAX_STEPS) ? 1 : 0;
+        const i64 tab = a.nrtab ? (i64)nsteps * NR_TAB_F * 32 : 0;
+        const i64 wk = softmax_work_u64(cols, a.esmem != 0, tab), ek = a.esmem ? 0 : 64 * cols;
+        const size_t lim = a.esmem ? 100 * 1024 + (size_t)tab * 8 : SMEM_LIMIT;
         if (a.causal)   // causal instantiations: the dense kernels carry no mask code
-            st = wide && a.cone ? launch_rows(c, k_softmax<3, BothA, true>, k_softmax<3, PairA, true>, a, rows, wk, ek, "softmax", lim)
-               : wide ? launch_rows(c, k_softmax<1, BothA, true>, k_softmax<1, PairA, true>, a, rows, wk, ek, "softmax", lim)
-               : a.cone ? launch_rows(c, k_softmax<2, BothA, true>, k_softmax<2, PairA, true>, a, rows, wk, ek, "softmax", lim)
-                        : launch_rows(c, k_softmax<0, BothA, true>, k_softmax<0, PairA, true>, a, rows, wk, ek, "softmax", lim);
+            st = wide && a.cone ? launch_rows(c, k_softmax<3, BothA, true>, kroles(k_softmax<3, PairA, true>, k_softmax<3, PairAS, true>), a, rows, wk, ek, "softmax", lim)
+               : wide ? launch_rows(c, k_softmax<1, BothA, true>, kroles(k_softmax<1, PairA, true>, k_softmax<1, PairAS, true>), a, rows, wk, ek, "softmax", lim)
+               : a.cone ? launch_rows(c, k_softmax<2, BothA, true>, kroles(k_softmax<2, PairA, true>, k_softmax<2, PairAS, true>), a, rows, wk, ek, "softmax", lim)
+                        : launch_rows(c, k_softmax<0, BothA, true>, kroles(k_softmax<0, PairA, true>, k_softmax<0, PairAS, true>), a, rows, wk, ek, "softmax", lim);
         else
-            st = wide && a.cone ? launch_rows(c, k_softmax<3, BothA>, k_softmax<3, PairA>, a, rows, wk, ek, "softmax", lim)
-               : wide ? launch_rows(c, k_softmax<1, BothA>, k_softmax<1, PairA>, a, rows, wk, ek, "softmax", lim)
-               : a.cone ? launch_rows(c, k_softmax<2, BothA>, k_softmax<2, PairA>, a, rows, wk, ek, "softmax", lim)
-                        : launch_rows(c, k_softmax<0, BothA>, k_softmax<0, PairA>, a, rows, wk, ek, "softmax", lim);
+            st = wide && a.cone ? launch_rows(c, k_softmax<3, BothA>, kroles(k_softmax<3, PairA>, k_softmax<3, PairAS>), a, rows, wk, ek, "softmax", lim)
+               : wide ? launch_rows(c, k_softmax<1, BothA>, kroles(k_softmax<1, PairA>, k_softmax<1, PairAS>), a, rows, wk, ek, "softmax", lim)
+               : a.cone ? launch_rows(c, k_softmax<2, BothA>, kroles(k_softmax<2, PairA>, k_softmax<2, PairAS>), a, rows, wk, ek, "softmax", lim)
+                        : launch_rows(c, k_softmax<0, BothA>, kroles(k_softmax<0, PairA>, k_softmax<0, PairAS>), a, rows, wk, ek, "softmax", lim);
     }
     return st;
 }
@@ -1666,7 +1861,44 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
 #ifndef MPC_LN_SPLIT
 #define MPC_LN_SPLIT 1
 #endif
-        if (MPC_LN_SPLIT && !p->rsqrt.exp.clamp && rows * cols < (1ll << 31)) {
+#ifndef MPC_LN_FUSED
+#define MPC_LN_FUSED 1
+#endif
+        const int nsteps_rs = nr_tab_steps(1, p->rsqrt.exp.t, p->rsqrt.iters);
+        if (MPC_LN_FUSED && !p->rsqrt.exp.clamp && !p->bcast && !(cols & 1) && rows * cols < (1ll << 31)) {
+            // one launch, row blocks of RB rows with every block resident (kernels.cuh k_ln_fused)
+            LnFArgs f{a.s_sq, a.s_rs, a.s_mul, a.rk, a.x, a.z, rows, cols, (u64)row_off, a.mean_mode, a.e_invd,
+                      a.e_eps, 2, 0};
+            f.nrtab = (!is_pair(c) && nsteps_rs <= MPC_NR_TAB_MAX_STEPS) ? 1 : 0;
+            const size_t dyn = sizeof(u64) * (256 + (f.nrtab ? (size_t)nsteps_rs * NR_TAB_F * 32 : 0));
+            auto rb_for = [&](i64 slots) {
+                i64 rb = (rows + slots - 1) / std::max<i64>(1, slots);
+                rb = std::max<i64>(2, std::min<i64>(32, (rb + 1) / 2 * 2));
+                return (int)rb;
+            };
+            if (!is_pair(c)) {
+                static DevCache occ;
+                const int per_sm = dev_cached(occ, c->cfg.device, [&] {
+                    cudaFuncSetAttribute(k_ln_fused<BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+                    return occupancy(k_ln_fused<BothA>, 64 * 1024, MPC_ROW_TPB);
+                });
+                f.RB = rb_for((i64)c->sm_count * per_sm);
+                const i64 nblk = (rows + f.RB - 1) / f.RB;
+                const int grid = (int)std::min<i64>(nblk, (i64)c->sm_count * per_sm);
+                rec_begin(c, "layernorm", (u64)rows);
+                k_ln_fused<BothA><<<grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, f);
+                rec_end(c);
+                c->st.launches++;
+                st = cuda_check(c, "layernorm");
+            } else {
+                const auto kk = kroles(k_ln_fused<PairA>, k_ln_fused<PairAS>);
+                set_smem_attr(kk, 64 * 1024);
+                f.RB = rb_for(pair_ctas(c, kk, dyn, 1ll << 40, MPC_ROW_TPB));
+                const i64 nblk = (rows + f.RB - 1) / f.RB;
+                st = launch_pair_kernel_tpb(c, kk, pair_ctas(c, kk, dyn, nblk, MPC_ROW_TPB), dyn, MPC_ROW_TPB,
+                                            "layernorm", f);
+            }
+        } else if (MPC_LN_SPLIT && !p->rsqrt.exp.clamp && rows * cols < (1ll << 31)) {
             // three launches: per-row stats, the row rsqrt (element-wise NR kernel), the product
             u64* sc = (u64*)scratch(c, sizeof(u64) * (size_t)rows * (6 + 6));
             if (!sc) return fail(c, MPC_ERR_NOMEM, "layernorm scratch");
@@ -1683,7 +1915,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
                 c->st.launches++;
                 st = cuda_check(c, "ln_stats");
             } else {
-                st = launch_pair_kernel(c, k_ln_stats<PairA>, pair_ctas(c, k_ln_stats<PairA>, 0, (nw * 32 + TPB - 1) / TPB),
+                st = launch_pair_kernel(c, kroles(k_ln_stats<PairA>, k_ln_stats<PairAS>), pair_ctas(c, kroles(k_ln_stats<PairA>, k_ln_stats<PairAS>), 0, (nw * 32 + TPB - 1) / TPB),
                                         0, "ln_stats", sa);
             }
             if (st) return st;
@@ -1700,7 +1932,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
                     c->st.launches++;
                     st = cuda_check(c, "bcast_rows");
                 } else {
-                    st = launch_pair_kernel(c, k_bmb_rows<PairA>, pair_ctas(c, k_bmb_rows<PairA>, 0, (nw2 * 32 + TPB - 1) / TPB),
+                    st = launch_pair_kernel(c, kroles(k_bmb_rows<PairA>, k_bmb_rows<PairAS>), pair_ctas(c, kroles(k_bmb_rows<PairA>, k_bmb_rows<PairAS>), 0, (nw2 * 32 + TPB - 1) / TPB),
                                             0, "bcast_rows", ra);
                 }
                 if (st) return st;
@@ -1724,7 +1956,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
                 c->st.launches++;
                 st = cuda_check(c, "layernorm");
             } else {
-                st = launch_pair_kernel_tpb(c, k_ln_quad<false, PairA>, pair_ctas(c, k_ln_quad<false, PairA>, 0, nctas, MPC_ROW_TPB),
+                st = launch_pair_kernel_tpb(c, kroles(k_ln_quad<false, PairA>, k_ln_quad<false, PairAS>), pair_ctas(c, kroles(k_ln_quad<false, PairA>, k_ln_quad<false, PairAS>), 0, nctas, MPC_ROW_TPB),
                                             0, MPC_ROW_TPB, "layernorm", a);
             }
         } else if (!is_pair(c)) {
@@ -1736,9 +1968,9 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
             c->st.launches++;
             st = cuda_check(c, "layernorm");
         } else if (wide) {
-            st = launch_pair_kernel_tpb(c, k_ln<true, PairA>, pair_ctas(c, k_ln<true, PairA>, 0, ntiles, MPC_ROW_TPB), 0, MPC_ROW_TPB, "layernorm", a);
+            st = launch_pair_kernel_tpb(c, kroles(k_ln<true, PairA>, k_ln<true, PairAS>), pair_ctas(c, kroles(k_ln<true, PairA>, k_ln<true, PairAS>), 0, ntiles, MPC_ROW_TPB), 0, MPC_ROW_TPB, "layernorm", a);
         } else {
-            st = launch_pair_kernel_tpb(c, k_ln<false, PairA>, pair_ctas(c, k_ln<false, PairA>, 0, ntiles, MPC_ROW_TPB), 0, MPC_ROW_TPB, "layernorm", a);
+            st = launch_pair_kernel_tpb(c, kroles(k_ln<false, PairA>, k_ln<false, PairAS>), pair_ctas(c, kroles(k_ln<false, PairA>, k_ln<false, PairAS>), 0, ntiles, MPC_ROW_TPB), 0, MPC_ROW_TPB, "layernorm", a);
         }
         if (st) return st;
         const i64 n = rows * cols;

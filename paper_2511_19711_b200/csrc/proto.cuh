@@ -27,9 +27,9 @@ struct ConeSmem { u32 w[G][NL][4]; };
 template <int G, int NL>
 __device__ void ltz_cone_both(const Keys& K, u64 q0, u32 s, int w, const Sh (&x)[G], Sh (&z)[G], int lane,
                               ConeSmem<G, NL>& sm);
-struct PairP;
-template <int G, int NL>
-__device__ void ltz_cone_pair(PairP& pr, u64 q0, u32 s, int w, const u64 (&x)[G], u64 (&z)[G], int lane,
+template <int R> struct PairP;
+template <int G, int NL, int R>
+__device__ void ltz_cone_pair(PairP<R>& pr, u64 q0, u32 s, int w, const u64 (&x)[G], u64 (&z)[G], int lane,
                               ConeSmem<G, NL>& sm);
 
 // 16-byte (LDG.E.128 / STG.E.128) access to an element pair (i, i+1) of one party's array
@@ -191,7 +191,23 @@ __device__ __forceinline__ u64 globaltimer()
     return t;
 }
 
-struct PairP {
+// Dealer correction-stream state: only the stream role (R = 1) carries it, so the
+// R = 0 kernels (party 0, the simulated dealer, loopback without a stream) compile exactly as
+// without the feature.
+template <int R> struct StreamState {
+    static constexpr int cmode = 0;
+};
+template <> struct StreamState<1> {
+    u64* cw;                 // this thread's column of the launch's stream segment
+    u32 cst, ck, ccap;       // stride (threads of the party's launch), next k, dealer capacity (words per thread)
+    int cmode;               // 0 (party 0 CTAs of a loopback launch), 1 read the stream, 2 the dealer
+};
+
+// R: 0 = party 0, or party 1 simulating the dealer from K_0 (reading R7); 1 = the stream roles:
+// party 1 reading the dealer's correction stream (cmode 1) or the dealer's own pass (cmode 2).
+template <int R>
+struct PairP : StreamState<R> {
+    using StreamState<R>::cmode;
 #ifndef MPC_PAIR_KV
 #define MPC_PAIR_KV 2
 #endif
@@ -205,11 +221,21 @@ struct PairP {
     int dead;
     int local;               // loopback: the peer is on this GPU -> gpu-scope release/acquire
     int fmt;                 // exchange wire format: 0 LL, 1 LL63 (warp-uniform)
+    // Dealer correction stream: party 1's correction words -- Beaver / square /
+    // broadcast c1, AND-triple c1 (G and P gate of a level packed in one word), daBit r1A -- are the
+    // only values party 1 would need K_0 for.  cmode 0: derived from K_0 (the dealer simulated by
+    // party 1, reading R7); 1: read from the dealer's stream (party 1 never touches K_0); 2: this
+    // launch IS the dealer (derives them and writes the stream; its exchange memory is a self-loop --
+    // every put comes back to the same warp -- so it runs party 1's exact code path).  The k-th
+    // correction of thread t is word cw[k * cst] (cw = stream base + t): coalesced across a warp,
+    // and the same (thread, k) in the dealer's launch and party 1's because both run the same kernel
+    // with the same grid and data-independent control flow.
     using S = u64;
     static constexpr bool kPair = true;
     static constexpr u64 kTimeoutNs = 10ull * 1000 * 1000 * 1000;   // 10 s, then poison
 
     __device__ __forceinline__ void bind(const XMem& m, int slot) {
+        dead = 0;
         rx = m.rx + (i64)slot * XSLOT_RX;
         prx = m.prx + (i64)slot * XSLOT_RX;
         flag = m.flag + (i64)slot * 4;
@@ -226,6 +252,27 @@ struct PairP {
         tstate[lane] = tg;
     }
     __device__ __forceinline__ int party() const { return pty; }
+    // K_0 is this thread's to use: party 0 always; party 1 only while it simulates the dealer
+    __device__ __forceinline__ bool k0ok() const {
+        if constexpr (R == 0) return true;
+        else return pty == 0 || cmode != 1;
+    }
+    __device__ __forceinline__ bool sread() const {          // party 1 reads the stream
+        if constexpr (R == 0) return false;
+        else return cmode == 1;
+    }
+    // party 1's next correction word: derive() (K_0) unless it comes from the dealer's stream
+    template <class F>
+    __device__ __forceinline__ u64 corr(F derive) {
+        if constexpr (R == 0) {
+            return derive();
+        } else {
+            if (cmode == 1) { const u64 v = this->cw[(u64)this->ck * this->cst]; ++this->ck; return v; }
+            const u64 v = derive();
+            if (cmode == 2) { if (this->ck < this->ccap) this->cw[(u64)this->ck * this->cst] = v; ++this->ck; }
+            return v;
+        }
+    }
     // ---- exchange: put words, exch(), get peer's words ----
     // Two wire formats, both "LL"-style (the idea of NCCL's low-latency protocol: the data carries
     // its own readiness tag, so there are no fences, flags or warp barriers on the data path), chosen
@@ -317,16 +364,25 @@ struct PairP {
 
     // ---- local share ops (party 0 carries public addends) ----
     __device__ __forceinline__ S zero() const { return 0; }
-    __device__ __forceinline__ S ld(SP a, i64 i) const { return a.p[pty][i]; }
-    __device__ __forceinline__ void st(SO a, i64 i, S v) const { a.p[pty][i] = v; }
+#ifndef MPC_DEALER_LDST
+#define MPC_DEALER_LDST 1     // A/B only: 0 drops the dealer's share-access guards (unsafe for the dealer)
+#endif
+    __device__ __forceinline__ bool nosh() const {          // the dealer: no shares
+        if constexpr (R == 0) return false;
+        else return MPC_DEALER_LDST && cmode == 2;
+    }
+    __device__ __forceinline__ S ld(SP a, i64 i) const { return nosh() ? 0ull : a.p[pty][i]; }
+    __device__ __forceinline__ void st(SO a, i64 i, S v) const { if (!nosh()) a.p[pty][i] = v; }
     // element pair (i, i+1) of this party's array: one 16-byte access (LDG.E.128 / STG.E.128) when both
     // are valid and aligned (loopback Beaver mul 5 % faster)
     __device__ __forceinline__ void ld_pair(SP a, i64 i, bool va, bool vb, S& x0, S& x1) const {
         x0 = x1 = 0;
+        if (nosh()) return;
         if (va && vb && al16(a.p[pty] + i)) { const ulonglong2 t = ld128(a.p[pty] + i); x0 = t.x; x1 = t.y; }
         else { if (va) x0 = ld(a, i); if (vb) x1 = ld(a, i + 1); }
     }
     __device__ __forceinline__ void st_pair(SO a, i64 i, bool va, bool vb, S x0, S x1) const {
+        if (nosh()) return;
         if (va && vb && al16(a.p[pty] + i)) st128(a.p[pty] + i, x0, x1);
         else { if (va) st(a, i, x0); if (vb) st(a, i + 1, x1); }
     }
@@ -348,15 +404,44 @@ struct PairP {
     __device__ __forceinline__ S divp(S a, i64 d) const { return floordiv_share(a, d); }
 
     // ---- Beaver (DESIGN.md 2.3/2.4); party 1 also plays the dealer's correction (R7) ----
-    __device__ __forceinline__ void triple(u64 u, u32 s, u64 c0, u64& a, u64& b, u64& c) const {
-        const uint4 A0 = prg(Kp->k0, u, s, 0);
+    // c0: party 0's c share (K_0; ignored -- and not computed by the caller -- when party 1 reads the stream)
+    __device__ __forceinline__ void triple(u64 u, u32 s, u64 c0, u64& a, u64& b, u64& c) {
         if (pty == 0) {
+            const uint4 A0 = prg(Kp->k0, u, s, 0);
             a = w64(A0.x, A0.y); b = w64(A0.z, A0.w); c = c0;
-        } else {
+        } else if (sread()) {                         // the dealer's c1 from the stream
             const uint4 A1 = prg(Kp->k1, u, s, 0);
             a = w64(A1.x, A1.y); b = w64(A1.z, A1.w);
-            c = (w64(A0.x, A0.y) + a) * (w64(A0.z, A0.w) + b) - c0;
+            c = corr([] { return 0ull; });
+        } else {                                      // both blocks in one basic block (ILP)
+            const uint4 A0 = prg(Kp->k0, u, s, 0), A1 = prg(Kp->k1, u, s, 0);
+            a = w64(A1.x, A1.y); b = w64(A1.z, A1.w);
+            const u64 cc = (w64(A0.x, A0.y) + a) * (w64(A0.z, A0.w) + b) - c0;
+            c = corr([&] { return cc; });
         }
+    }
+    // the triples of unit pair (u, u+1) (u even): one c0 block serves both; each path keeps all its
+    // Philox blocks in one basic block so they interleave (ILP)
+    __device__ __forceinline__ void triple_pair(u64 u, u32 s, u64& a0, u64& b0, u64& c0, u64& a1, u64& b1, u64& c1) {
+        if (pty == 0) {
+            const uint4 C = prg(Kp->k0, u >> 1, s, 1), Au = prg(Kp->k0, u, s, 0), Av = prg(Kp->k0, u + 1, s, 0);
+            a0 = w64(Au.x, Au.y); b0 = w64(Au.z, Au.w); a1 = w64(Av.x, Av.y); b1 = w64(Av.z, Av.w);
+            c0 = w64(C.x, C.y); c1 = w64(C.z, C.w);
+        } else if (sread()) {
+            const uint4 Au = prg(Kp->k1, u, s, 0), Av = prg(Kp->k1, u + 1, s, 0);
+            a0 = w64(Au.x, Au.y); b0 = w64(Au.z, Au.w); a1 = w64(Av.x, Av.y); b1 = w64(Av.z, Av.w);
+            c0 = corr([] { return 0ull; }); c1 = corr([] { return 0ull; });
+        } else {
+            const uint4 C = prg(Kp->k0, u >> 1, s, 1), Au = prg(Kp->k0, u, s, 0), Av = prg(Kp->k0, u + 1, s, 0);
+            const uint4 Bu = prg(Kp->k1, u, s, 0), Bv = prg(Kp->k1, u + 1, s, 0);
+            a0 = w64(Bu.x, Bu.y); b0 = w64(Bu.z, Bu.w); a1 = w64(Bv.x, Bv.y); b1 = w64(Bv.z, Bv.w);
+            const u64 cu = (w64(Au.x, Au.y) + a0) * (w64(Au.z, Au.w) + b0) - w64(C.x, C.y);
+            const u64 cv = (w64(Av.x, Av.y) + a1) * (w64(Av.z, Av.w) + b1) - w64(C.z, C.w);
+            c0 = corr([&] { return cu; }); c1 = corr([&] { return cv; });
+        }
+    }
+    __device__ __forceinline__ uint4 cblk(u64 u, u32 s) const {          // the c0 block of unit pair (u, u+1)
+        return k0ok() ? prg(Kp->k0, u >> 1, s, 1) : make_uint4(0, 0, 0, 0);
     }
     __device__ __forceinline__ S bm_finish(u64 a, u64 b, u64 c, u64 e, u64 f) const {
         return pty == 0 ? c + e * (b + f) + f * a : c + e * b + f * a;   // party 0: e b + e f = e (b + f)
@@ -368,7 +453,8 @@ struct PairP {
 #endif
         const int lane = threadIdx.x & 31;
         u64 a, b, c;
-        triple(u, s, beaver_c0(*Kp, u, s), a, b, c);
+        const uint4 C = cblk(u, s);
+        triple(u, s, (u & 1) ? w64(C.z, C.w) : w64(C.x, C.y), a, b, c);
         put(lane, 0, x - a); put(lane, 1, y - b);
         exch(lane);
         const u64 e = (x - a) + get(lane, 0), f = (y - b) + get(lane, 1);
@@ -380,10 +466,8 @@ struct PairP {
     __device__ __noinline__ void bm2(u64 u, u32 s, S x0, S y0, S x1, S y1, S& z0, S& z1) {
 #endif
         const int lane = threadIdx.x & 31;
-        const uint4 C = prg(Kp->k0, u >> 1, s, 1);
         u64 a0, b0, c0, a1, b1, c1;
-        triple(u, s, w64(C.x, C.y), a0, b0, c0);
-        triple(u + 1, s, w64(C.z, C.w), a1, b1, c1);
+        triple_pair(u, s, a0, b0, c0, a1, b1, c1);
         put(lane, 0, x0 - a0); put(lane, 1, y0 - b0); put(lane, 2, x1 - a1); put(lane, 3, y1 - b1);
         exch(lane);
         z0 = bm_finish(a0, b0, c0, (x0 - a0) + get(lane, 0), (y0 - b0) + get(lane, 1));
@@ -394,8 +478,9 @@ struct PairP {
     __device__ __forceinline__ void bm_dual(u64 u, u32 sA, S xA, S yA, u32 sB, S xB, S yB, S& zA, S& zB) {
         const int lane = threadIdx.x & 31;
         u64 aA, bA, cA, aB, bB, cB;
-        triple(u, sA, beaver_c0(*Kp, u, sA), aA, bA, cA);
-        triple(u, sB, beaver_c0(*Kp, u, sB), aB, bB, cB);
+        const uint4 CA = cblk(u, sA), CB = cblk(u, sB);
+        triple(u, sA, (u & 1) ? w64(CA.z, CA.w) : w64(CA.x, CA.y), aA, bA, cA);
+        triple(u, sB, (u & 1) ? w64(CB.z, CB.w) : w64(CB.x, CB.y), aB, bB, cB);
         put(lane, 0, xA - aA); put(lane, 1, yA - bA); put(lane, 2, xB - aB); put(lane, 3, yB - bB);
         exch(lane);
         zA = bm_finish(aA, bA, cA, (xA - aA) + get(lane, 0), (yA - bA) + get(lane, 1));
@@ -405,12 +490,9 @@ struct PairP {
                                              S yB1, S& zA0, S& zA1, S& zB0, S& zB1) {
         static_assert(8 <= XW, "exchange width");
         const int lane = threadIdx.x & 31;
-        const uint4 CA = prg(Kp->k0, u >> 1, sA, 1), CB = prg(Kp->k0, u >> 1, sB, 1);
         u64 a[4], b[4], c[4];
-        triple(u, sA, w64(CA.x, CA.y), a[0], b[0], c[0]);
-        triple(u + 1, sA, w64(CA.z, CA.w), a[1], b[1], c[1]);
-        triple(u, sB, w64(CB.x, CB.y), a[2], b[2], c[2]);
-        triple(u + 1, sB, w64(CB.z, CB.w), a[3], b[3], c[3]);
+        triple_pair(u, sA, a[0], b[0], c[0], a[1], b[1], c[1]);
+        triple_pair(u, sB, a[2], b[2], c[2], a[3], b[3], c[3]);
         const S xs[4] = {xA0, xA1, xB0, xB1}, ys[4] = {yA0, yA1, yB0, yB1};
 #pragma unroll
         for (int k = 0; k < 4; ++k) { put(lane, 2 * k, xs[k] - a[k]); put(lane, 2 * k + 1, ys[k] - b[k]); }
@@ -425,25 +507,27 @@ struct PairP {
     // ---- broadcast triple (NEXT #2): f opened once per row, e per element ----
     __device__ __forceinline__ BRow bmb_row(u64 r, u32 s, S y) {
         const int lane = threadIdx.x & 31;
-        const uint4 B0 = prg(Kp->k0, r, s, 6);
-        BRow R;
-        R.b0 = w64(B0.x, B0.y); R.b1 = 0;
-        if (pty == 1) { const uint4 B1 = prg(Kp->k1, r, s, 6); R.b1 = w64(B1.x, B1.y); }
-        const u64 m = y - (pty == 0 ? R.b0 : R.b1);
+        const uint4 B0 = k0ok() ? prg(Kp->k0, r, s, 6) : make_uint4(0, 0, 0, 0);
+        BRow Rw;
+        Rw.b0 = w64(B0.x, B0.y); Rw.b1 = 0;
+        if (pty == 1) { const uint4 B1 = prg(Kp->k1, r, s, 6); Rw.b1 = w64(B1.x, B1.y); }
+        const u64 m = y - (pty == 0 ? Rw.b0 : Rw.b1);
         put(lane, 0, m);
         exch(lane);
-        R.f = m + get(lane, 0);
-        return R;
+        Rw.f = m + get(lane, 0);
+        return Rw;
     }
     __device__ __forceinline__ void bmb2(u64 u, u32 s, S x0, S x1, const BRow& r0, const BRow& r1, S& z0, S& z1) {
         const int lane = threadIdx.x & 31;
-        const uint4 Au = prg(Kp->k0, u, s, 4), Av = prg(Kp->k0, u + 1, s, 4);
+        uint4 Au = make_uint4(0, 0, 0, 0), Av = Au;
+        if (k0ok()) { Au = prg(Kp->k0, u, s, 4); Av = prg(Kp->k0, u + 1, s, 4); }
         u64 au = w64(Au.x, Au.y), cu = w64(Au.z, Au.w), av = w64(Av.x, Av.y), cv = w64(Av.z, Av.w);
         if (pty == 1) {                                  // party 1: own a1, dealer's c1
             const uint4 A1 = prg(Kp->k1, u >> 1, s, 5);
             const u64 a1u = w64(A1.x, A1.y), a1v = w64(A1.z, A1.w);
-            cu = (au + a1u) * (r0.b0 + r0.b1) - cu;
-            cv = (av + a1v) * (r1.b0 + r1.b1) - cv;
+            const u64 a0u = au, c0u = cu, a0v = av, c0v = cv;
+            cu = corr([&] { return (a0u + a1u) * (r0.b0 + r0.b1) - c0u; });
+            cv = corr([&] { return (a0v + a1v) * (r1.b0 + r1.b1) - c0v; });
             au = a1u; av = a1v;
         }
         put(lane, 0, x0 - au); put(lane, 1, x1 - av);
@@ -455,11 +539,13 @@ struct PairP {
     }
 
     // ---- squares with square-pair triples (NEXT #2): one word per element per round ----
-    __device__ __forceinline__ void sq_triple(u64 u, u32 s, u64 a1_other_half, u64& a, u64& c) const {
-        const uint4 A0 = prg(Kp->k0, u, s, 2);
-        const u64 a0 = w64(A0.x, A0.y), c0 = w64(A0.z, A0.w);
-        if (pty == 0) { a = a0; c = c0; }
-        else { a = a1_other_half; const u64 t = a0 + a; c = t * t - c0; }
+    __device__ __forceinline__ void sq_triple(u64 u, u32 s, u64 a1_other_half, u64& a, u64& c) {
+        if (pty == 0) { const uint4 A0 = prg(Kp->k0, u, s, 2); a = w64(A0.x, A0.y); c = w64(A0.z, A0.w); }
+        else {
+            a = a1_other_half;
+            const u64 a1 = a;
+            c = corr([&] { const uint4 A0 = prg(Kp->k0, u, s, 2); const u64 t = w64(A0.x, A0.y) + a1; return t * t - w64(A0.z, A0.w); });
+        }
     }
     __device__ __forceinline__ S sq_finish(u64 a, u64 c, u64 e) const {
         return pty == 0 ? c + e * (2ull * a + e) : c + 2ull * e * a;
@@ -496,9 +582,7 @@ struct PairP {
         u64 a0[V], b0[V], c0[V], a1[V], b1[V], c1[V];
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-            const uint4 C = prg(Kp->k0, u[v] >> 1, s, 1);
-            triple(u[v], s, w64(C.x, C.y), a0[v], b0[v], c0[v]);
-            triple(u[v] + 1, s, w64(C.z, C.w), a1[v], b1[v], c1[v]);
+            triple_pair(u[v], s, a0[v], b0[v], c0[v], a1[v], b1[v], c1[v]);
             put(lane, 4 * v + 0, x0[v] - a0[v]); put(lane, 4 * v + 1, y0[v] - b0[v]);
             put(lane, 4 * v + 2, x1[v] - a1[v]); put(lane, 4 * v + 3, y1[v] - b1[v]);
         }
@@ -532,11 +616,25 @@ struct PairP {
     }
 
     // ---- AND gates on XOR-shared plane words; up to 2 gates (4 words) per round ----
-    __device__ __forceinline__ void and_triple(uint4 t0, uint4 t1, int which, u32& a, u32& b, u32& c) const {
+    __device__ __forceinline__ void and_triple(uint4 t0, uint4 t1, int which, u32& a, u32& b, u32& c) {
         // which = 0: (a1,b1) = t1.x,t1.y ; 1: t1.z,t1.w
         const u32 a1 = which ? t1.z : t1.x, b1 = which ? t1.w : t1.y;
         if (pty == 0) { a = t0.x; b = t0.y; c = t0.z; }
-        else { a = a1; b = b1; c = ((t0.x ^ a1) & (t0.y ^ b1)) ^ t0.z; }
+        else { a = a1; b = b1; c = (u32)corr([&] { return (u64)(((t0.x ^ a1) & (t0.y ^ b1)) ^ t0.z); }); }
+    }
+    // the G and P gates of one Kogge-Stone / cone node: party 1's two c1 words in ONE stream word
+    __device__ __forceinline__ void and_triple2(uint4 tg, uint4 tp, uint4 t1, u32& ga, u32& gb, u32& gc,
+                                                u32& pa, u32& pb, u32& pc) {
+        if (pty == 0) { ga = tg.x; gb = tg.y; gc = tg.z; pa = tp.x; pb = tp.y; pc = tp.z; return; }
+        ga = t1.x; gb = t1.y; pa = t1.z; pb = t1.w;
+        const u64 cc = corr([&] {
+            return (u64)(((tg.x ^ t1.x) & (tg.y ^ t1.y)) ^ tg.z) | ((u64)(((tp.x ^ t1.z) & (tp.y ^ t1.w)) ^ tp.z) << 32);
+        });
+        gc = (u32)cc; pc = (u32)(cc >> 32);
+    }
+    // this lane's daBit r1A (party 1): (r0B ^ r1B) - r0A with D0 = PRG(K_0, q, s, 2 + lane)
+    __device__ __forceinline__ u64 dabit_r1A(uint4 D0, u32 r1B) {
+        return corr([&] { return (u64)((D0.z & 1u) ^ r1B) - w64(D0.x, D0.y); });
     }
     __device__ __forceinline__ u32 and_finish(u32 a, u32 b, u32 c, u32 d, u32 e) const {
         return pty == 0 ? (c ^ (d & b) ^ (e & a) ^ (d & e)) : (c ^ (d & b) ^ (e & a));
@@ -545,10 +643,11 @@ struct PairP {
     // w <= 33, branch-free, daBit words in the idle slots of the last level (as ltz_narrow)
     __device__ __forceinline__ S ltz_narrow(u64 q, u32 s, int w, S x, int lane) {
         const int m = w - 1;
+        const bool k0 = k0ok();
         const PrgQ Q0 = prg_q(Kp->k0, q, s), Q1 = prg_q(Kp->k1, q, s);
         u32 Pp = transpose32((u32)x, lane), Gp = 0;
         {
-            const uint4 t0 = prg(Q0, ltz_slot(0, lane, 0));
+            const uint4 t0 = k0 ? prg(Q0, ltz_slot(0, lane, 0)) : make_uint4(0, 0, 0, 0);
             uint4 t1 = make_uint4(0, 0, 0, 0);
             if (pty == 1) t1 = prg(Q1, ltz_slot(0, lane, 0));
             u32 ta, tb, tc;
@@ -570,13 +669,12 @@ struct PairP {
             const u32 g = __shfl_sync(FULL, Gp, src), p = __shfl_sync(FULL, Pp, src);
             const bool act = lane >= dl && lane < m;
             const bool dab = trick && k == L - 1 && lane < 16;
-            const uint4 tg = prg(Q0, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0));
-            const uint4 tp = prg(Q0, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1));
+            uint4 tg = make_uint4(0, 0, 0, 0), tp = tg;
+            if (k0) { tg = prg(Q0, dab ? 2u + (u32)lane : ltz_slot(k + 1, lane, 0)); tp = prg(Q0, dab ? 18u + (u32)lane : ltz_slot(k + 1, lane, 1)); }
             uint4 t1 = make_uint4(0, 0, 0, 0);
             if (pty == 1) t1 = prg(Q1, dab ? 1u : ltz_slot(k + 1, lane, 0));
             u32 ga, gb, gc, pa, pb, pc;
-            and_triple(tg, t1, 0, ga, gb, gc);
-            and_triple(tp, t1, 1, pa, pb, pc);
+            and_triple2(tg, tp, t1, ga, gb, gc, pa, pb, pc);
             const u32 dG = Pp ^ ga, eG = g ^ gb, dP = Pp ^ pa, eP = p ^ pb;
             put(lane, 0, (u64)dG | ((u64)eG << 32));
             put(lane, 1, (u64)dP | ((u64)eP << 32));
@@ -598,15 +696,13 @@ struct PairP {
             D0 = lane < 16 ? Dlo : make_uint4(hx, hy, hz, 0u);
             d1x = __shfl_sync(FULL, k1w, 0);
         } else {
-            D0 = prg(Q0, 2u + (u32)lane);
+            D0 = k0 ? prg(Q0, 2u + (u32)lane) : make_uint4(0, 0, 0, 0);
             if (pty == 1) d1x = prg(Q1, 1u).x;
         }
-        const u64 r0A = w64(D0.x, D0.y);
-        const u32 r0B = D0.z & 1u;
         u64 rA;
         u32 rB;
-        if (pty == 0) { rA = r0A; rB = r0B; }
-        else { rB = (d1x >> lane) & 1u; rA = (u64)(r0B ^ rB) - r0A; }
+        if (pty == 0) { rA = w64(D0.x, D0.y); rB = D0.z & 1u; }
+        else { rB = (d1x >> lane) & 1u; rA = dabit_r1A(D0, rB); }
         const u32 mine = bp ^ rB;
         put(lane, 0, (u64)mine);
         exch(lane);
@@ -628,6 +724,7 @@ struct PairP {
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) {
         if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(q, s, w, x, lane);
         const int m = w - 1;
+        const bool k0 = k0ok();
         const PrgQ Q0 = prg_q(Kp->k0, q, s), Q1 = prg_q(Kp->k1, q, s);
         constexpr int H = WIDE ? 2 : 1;
         u32 Pp[2], Gp[2];                                  // this party's shares of P_j, G_j
@@ -641,7 +738,7 @@ struct PairP {
                 const int j = lane + 32 * h;
                 ta[h] = tb[h] = tc[h] = 0;
                 if (j < m) {
-                    const uint4 t0 = prg(Q0, ltz_slot(0, j, 0));
+                    const uint4 t0 = k0 ? prg(Q0, ltz_slot(0, j, 0)) : make_uint4(0, 0, 0, 0);
                     uint4 t1 = make_uint4(0, 0, 0, 0);
                     if (pty == 1) t1 = prg(Q1, ltz_slot(0, j, 0));
                     and_triple(t0, t1, 0, ta[h], tb[h], tc[h]);
@@ -678,12 +775,11 @@ struct PairP {
                 if (WIDE && dl == 32) { g = Gp[0]; p = Pp[0]; }
                 ga[h] = gb[h] = gc[h] = pa[h] = pb[h] = pc[h] = 0;
                 if (act[h]) {
-                    const uint4 tg = prg(Q0, ltz_slot(k + 1, j, 0));
-                    const uint4 tp = prg(Q0, ltz_slot(k + 1, j, 1));
+                    uint4 tg = make_uint4(0, 0, 0, 0), tp = tg;
+                    if (k0) { tg = prg(Q0, ltz_slot(k + 1, j, 0)); tp = prg(Q0, ltz_slot(k + 1, j, 1)); }
                     uint4 t1 = make_uint4(0, 0, 0, 0);
                     if (pty == 1) t1 = prg(Q1, ltz_slot(k + 1, j, 0));
-                    and_triple(tg, t1, 0, ga[h], gb[h], gc[h]);
-                    and_triple(tp, t1, 1, pa[h], pb[h], pc[h]);
+                    and_triple2(tg, tp, t1, ga[h], gb[h], gc[h], pa[h], pb[h], pc[h]);
                 }
                 dG[h] = Pp[h] ^ ga[h]; eG[h] = g ^ gb[h];
                 dP[h] = Pp[h] ^ pa[h]; eP[h] = p ^ pb[h];
@@ -712,16 +808,14 @@ struct PairP {
             bp = (u32)((x >> (w - 1)) & 1ull) ^ ((gm >> lane) & 1u);
         }
         // daBit + B2A: party 0 holds (r0A, r0B); party 1 (r1A, r1B), r1A = (r0B ^ r1B) - r0A
-        const uint4 D0 = prg(Q0, 2u + (u32)lane);
-        const u64 r0A = w64(D0.x, D0.y);
-        const u32 r0B = D0.z & 1u;
+        const uint4 D0 = k0 ? prg(Q0, 2u + (u32)lane) : make_uint4(0, 0, 0, 0);
         u64 rA;
         u32 rB;
-        if (pty == 0) { rA = r0A; rB = r0B; }
+        if (pty == 0) { rA = w64(D0.x, D0.y); rB = D0.z & 1u; }
         else {
             const uint4 D1 = prg(Q1, 1u);
             rB = (D1.x >> lane) & 1u;
-            rA = (u64)(r0B ^ rB) - r0A;
+            rA = dabit_r1A(D0, rB);
         }
         const u32 mine = bp ^ rB;
         put(lane, 0, (u64)mine);
@@ -733,7 +827,7 @@ struct PairP {
 
     template <int G, int NL>
     __device__ __forceinline__ void ltz_cone(u64 q0, u32 s, int w, const S (&x)[G], S (&z)[G], int lane, ConeSmem<G, NL>& sm) {
-        ltz_cone_pair<G, NL>(*this, q0, s, w, x, z, lane, sm);
+        ltz_cone_pair<G, NL, R>(*this, q0, s, w, x, z, lane, sm);
     }
 
     // ---- S2 open: exchange the shares themselves ----

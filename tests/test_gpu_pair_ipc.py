@@ -26,3 +26,11 @@ def test_pair_debug_header_detects_mismatched_calls():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_ipc_check.py"), "--mismatch"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0 and "PAIR_IPC_PROTOCOL_DETECTED" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_pair_two_processes_party1_without_k0_reads_the_dealer_stream():
+    """party 1's context is created with key_p0 = 0 and reads its correction words
+    from an MPC_MODE_DEALER context's offline stream; every op's shares still equal MPC_MODE_BOTH's."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "pair_ipc_check.py"), "--dealer"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0 and "PAIR_IPC_OK" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

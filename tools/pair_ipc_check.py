@@ -11,7 +11,11 @@ LayerNorm), and an open to party 1 only.
   python tools/pair_ipc_check.py             (prints PAIR_IPC_OK on success, exit code 0)
   python tools/pair_ipc_check.py --mismatch  (debug header check: the parties issue different ops;
                                               prints PAIR_IPC_PROTOCOL_DETECTED)
-  python tools/pair_ipc_check.py --exchange=0 (the LL wire format instead of the LL63 default)"""
+  python tools/pair_ipc_check.py --exchange=0 (the LL wire format instead of the LL63 default)
+  python tools/pair_ipc_check.py --dealer    (party 1's context is created WITHOUT K_0 (key_p0 = 0) and
+                                              reads its corrections from a trusted-dealer stream made
+                                              offline by an MPC_MODE_DEALER context, DESIGN.md 7.1;
+                                              the matrix triple is not stream-fed, so no matmul)"""
 import os
 import sys
 
@@ -25,11 +29,11 @@ import torch.multiprocessing as mp  # noqa: E402
 import workloads  # noqa: E402
 
 
-def ops(c, x, party, n_rows, n_cols):
+def ops(c, x, party, n_rows, n_cols, matmul=True):
     """The op sequence both modes run; returns the list of this party's output shares."""
     out = []
     xs = x if x is not None else None
-    if c.mode == 1 and party == 1:
+    if c.mode in (1, 3) and party == 1:
         s = c.share(None, owner=0, n=n_rows * n_cols)
     else:
         s = c.share(xs, owner=0)
@@ -45,7 +49,8 @@ def ops(c, x, party, n_rows, n_cols):
     c.set_ltz_circuit(0)
     out.append(c.softmax(s, n_rows, n_cols, causal=1))
     # X = s as n_rows x n_cols, Y = the same buffer as n_cols x n_rows (tensor-core engine)
-    out.append(c.matmul(s, s, 1, n_rows, n_cols, n_rows, trunc_bits=16))
+    if matmul:
+        out.append(c.matmul(s, s, 1, n_rows, n_cols, n_rows, trunc_bits=16))
     # broadcast triple (NEXT #2): per-row record scratch is per party in PAIR
     out.append(c.mul_bcast(s, s, n_rows, n_cols, trunc_bits=16))
     out.append(c.softmax(s, n_rows, n_cols, bcast=1))
@@ -64,7 +69,17 @@ def worker(rank, world, port, q, mismatch=False):
     rows, cols = 32, 64
     x = torch.from_numpy(workloads.softmax_inputs(rows, cols).ravel()).cuda(dev)
     keys = workloads.keys(2)
-    c = m.Ctx.for_cfg(keys, device=dev, mode=m.binding.MODE_PAIR, party=rank)
+    dealer = "--dealer" in sys.argv
+    if dealer and rank == 1:
+        # party 1 never receives K_0: its corrections come from the dealer's offline pass
+        c = m.Ctx(keys["key_share"], 0, keys["key_p1"], dev, mode=m.binding.MODE_PAIR, party=1)
+        d = m.Ctx.dealer(keys, device=dev)
+        d.set_step(c.step)
+        ops(d, None, 1, rows, cols, matmul=False)
+        d.open_to(m.Ctx.like(rows * cols), 1)          # the final open's (empty) segment
+        c.set_corrections(d.dealer_stream())
+    else:
+        c = m.Ctx.for_cfg(keys, device=dev, mode=m.binding.MODE_PAIR, party=rank)
     if "--exchange=0" in sys.argv:
         c.set_exchange(0)                             # LL instead of the LL63 default
     pair.connect(c)
@@ -90,15 +105,17 @@ def worker(rank, world, port, q, mismatch=False):
         dist.barrier()
         dist.destroy_process_group()
         return
-    res = ops(c, x if rank == 0 else None, rank, rows, cols)
+    res = ops(c, x if rank == 0 else None, rank, rows, cols, matmul=not dealer)
     ring1, _ = c.open_to(res[0], 1)                   # only party 1 learns rec(x)
     c.sync()
+    if dealer and rank == 1 and c.corrections_left() != 0:
+        raise RuntimeError(f"party 1 left {c.corrections_left()} correction segments")
     mine = [r[rank].cpu().numpy() for r in res] + [ring1.cpu().numpy()]
     gathered = [None, None]
     dist.all_gather_object(gathered, mine)
     if rank == 0:
         b = m.Ctx.for_cfg(keys, device=dev)
-        ref = ops(b, x, 0, rows, cols)
+        ref = ops(b, x, 0, rows, cols, matmul=not dealer)
         ring_ref, _ = b.open(ref[0])
         torch.cuda.synchronize()
         bad = []
