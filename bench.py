@@ -345,6 +345,7 @@ def run_mpc200(args):
     eb.record(job.stream)
     torch.cuda.synchronize()
     e_ms = job.maxr(ea.elapsed_time(eb) / e2e_steps)
+    pcie = pcie_floor(job, hin, hout)
 
     per_op = {"softmax": {"elements": n, "elements_per_s": value / job.npairs, "ms": round(ms_step, 4)}}
     if not args.no_per_op:
@@ -368,7 +369,10 @@ def run_mpc200(args):
                "e2e": {"value": job.npairs * n / (e_ms / 1e3), "unit": "elements/s",
                        "h2d_bytes_per_step": 16 * n * job.npairs, "d2h_bytes_per_step": 16 * n * job.npairs,
                        "ms_per_step": round(e_ms, 4),
-                       "api": "mpc_softmax_hostio (pinned host shares in/out, 3072-row chunks, copies overlapped)"},
+                       "api": "mpc_softmax_hostio (pinned host shares in/out, 3072-row chunks, copies overlapped)",
+                       "pcie_floor_ms": pcie, "frac_of_pcie_floor": round(pcie / e_ms, 3) if pcie else None,
+                       "pcie_floor_how": "the step's H2D and D2H bytes as one copy per direction on two streams "
+                                         "at once (no compute): the transfer-only time of a step"},
                "gpu_launches": st["launches"],
                "launches_per_step": st["launches"] / args.steps,
                "protocol_per_step": {"philox_blocks": st["philox_calls"] // args.steps,
@@ -382,6 +386,34 @@ def run_mpc200(args):
         job.barrier()
         dist.destroy_process_group()
     return res
+
+
+def pcie_floor(job, hin, hout, reps=5):
+    """Transfer-only floor of one e2e step: every party buffer H2D and D2H, one copy per direction
+    per buffer, the two directions on two streams at once."""
+    torch = job.torch
+    try:
+        dev_in = [torch.empty_like(h, device=job.dev) if h is not None else None for h in hin]
+        s1, s2 = torch.cuda.Stream(job.dev), torch.cuda.Stream(job.dev)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(job.stream)
+        for _ in range(reps):
+            s1.wait_stream(job.stream); s2.wait_stream(job.stream)
+            with torch.cuda.stream(s1):
+                for h, d in zip(hin, dev_in):
+                    if h is not None:
+                        d.copy_(h, non_blocking=True)
+            with torch.cuda.stream(s2):
+                for h, d in zip(hout, dev_in):
+                    if h is not None:
+                        h.copy_(d, non_blocking=True)
+            job.stream.wait_stream(s1); job.stream.wait_stream(s2)
+        b.record(job.stream)
+        torch.cuda.synchronize()
+        return round(a.elapsed_time(b) / reps, 4)
+    except Exception:
+        return None
 
 
 def check_timed_output(job, step_id, xs, out, rows, cols, row_off, sm_kw, tiles=8):
@@ -536,9 +568,7 @@ def time_per_op(job, m, ctx, flush, args):
     del r, z
     ctx.set_ltz_circuit(0)
     Bm, Mm, Km, Nm = 1, 1024, 768, 3072           # BERT-base FFN Linear (8 x 128 tokens), NEXT #3
-    if dealer_on(job):                            # the matrix triple is not stream-fed
-        out["matmul_tc"] = {"skipped": "PAIR with the trusted dealer's stream: matmul's C1 is not stream-fed"}
-    else:
+    if True:
         xm = job.share(ctx, workloads.act_inputs(Mm * Km, lo=-2, hi=2), k * Mm * Km)
         ym = job.share(ctx, workloads.act_inputs(Km * Nm, seed_cfg=5, lo=-2, hi=2), k * Km * Nm)
         z = ctx._empty(Mm * Nm)

@@ -172,8 +172,9 @@ mpc_status mpc_dealer_reset(mpc_ctx* dealer);
  * on the context's device, owned by the caller, valid until consumed; segs is copied.  A launch
  * whose next segment is missing or does not match (tag, threads) fails with MPC_ERR_PROTOCOL.
  * words == NULL and n_segs == 0 clears the stream (party 1 derives from K_0 again).
- * MPC_ERR_INVALID on party 0, BOTH or DEALER contexts.  mpc_matmul is not stream-fed
- * (MPC_ERR_UNSUPPORTED while a stream is set). */
+ * MPC_ERR_INVALID on party 0, BOTH or DEALER contexts.  mpc_matmul's matrix correction
+ * C1 = (A0+A1)(B0+B1) - C0 is one segment of batch*M*N words (tag "matmul_c1", depth 1) that the
+ * dealer forms with a ring GEMM and party 1 adds in its GEMM epilogue. */
 mpc_status mpc_ctx_set_corrections(mpc_ctx* ctx, const uint64_t* words, uint64_t n_words,
                                    const mpc_corr_seg* segs, int64_t n_segs);
 /* Segments not consumed yet; -1 when no stream is set. */

@@ -1323,15 +1323,14 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_quad(const __gr
     pa.done(pr);
 }
 
-}  // namespace mpc
-
 // ---------------------------------------------------------------- fused row-block LayerNorm ----
 // LAYERNORM in ONE launch, element-balanced: a CTA owns RB consecutive rows (RB even, <= 32,
 // chosen so that every CTA is resident at once) and its 8 warps split the block's ELEMENT PAIRS
-// evenly (a row is not a warp's unit: 768-wide rows over 8 warps would leave the row chains uneven):
-//   A  row sums (per-lane running sums, flushed to shared memory with u64 atomics when the lane's row
-//      changes -- ring addition, so the order cannot change a bit)  -> mu = x E(1/d) | floor / d
-//   B  MT(c, c), c = x - mu (element units, unit pairs), the same per-row reduction -> v = mean + eps
+// evenly; a warp walks its range ROW SEGMENT by row segment (the row is warp-uniform inside a segment:
+// mu / r are one register, and the per-row sums are a warp reduction into wpart[warp][segment] --
+// no shared-memory atomics, which are CAS loops for u64):
+//   A  row sums -> mu = x E(1/d) | floor / d
+//   B  MT(c, c), c = x - mu (element units, unit pairs), summed per row -> v = mean + eps
 //   C  RSQRT(v) over the block's rows (row units; BOTH: the chain's triples generated by all warps
 //      first, nr_pregen<1>), warp 0 lane <-> row
 //   D  out = MT(c, r) (element units, unit pairs)
@@ -1345,6 +1344,8 @@ struct LnFArgs {
     int RB;                 // rows per block (even)
     int nrtab;              // BOTH: rsqrt triples pre-generated into shared memory
 };
+constexpr int LNF_SEG = 34;                    // row segments per warp (<= RB + 1)
+__host__ __device__ inline int lnf_smem_u64(int nsteps_tab) { return 256 + 8 * LNF_SEG * 2 + nsteps_tab * NR_TAB_F * 32; }
 template <class PA>
 __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_fused(const __grid_constant__ PA pa, LnFArgs a)
 {
@@ -1355,134 +1356,153 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_fused(const __g
     using S = typename P::S;
     constexpr int V = P::kV;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-    const i64 C = a.cols;
-    const FastDiv dC = make_fastdiv((u32)C);
-    // shared: row sums SA (2 x 32), means MU, variance sums SV, rsqrt RS (each 2 x 32), NR table
-    u64* SA = lsm; u64* MUw = lsm + 64; u64* SV = lsm + 128; u64* RSw = lsm + 192;
-    u64* tab = a.nrtab ? lsm + 256 : nullptr;
-    const SO MU{{MUw, MUw + 32}}, RS{{RSw, RSw + 32}};
-    const SP MUc{{MUw, MUw + 32}}, RSc{{RSw, RSw + 32}};
-    auto flush = [&](u64* base, int r, S v) {           // per-row ring sum (both parties in BOTH)
-        if constexpr (P::kPair) atomicAdd((unsigned long long*)&base[32 * pr.party() + r], (unsigned long long)v);
-        else { atomicAdd((unsigned long long*)&base[r], (unsigned long long)v.s0);
-               atomicAdd((unsigned long long*)&base[32 + r], (unsigned long long)v.s1); }
+    const i64 C = a.cols, hc = C / 2;                        // pairs per row (C even)
+    // shared: means MU, variances VR, rsqrt RS (each 2 x 32), per-warp segment sums, NR table
+    u64* MUw = lsm; u64* VRw = lsm + 64; u64* RSw = lsm + 128;
+    u64* wpart = lsm + 256;                                   // [NW][LNF_SEG][2]
+    u64* tab = a.nrtab ? lsm + 256 + 8 * LNF_SEG * 2 : nullptr;
+    const SO MU{{MUw, MUw + 32}}, VR{{VRw, VRw + 32}}, RS{{RSw, RSw + 32}};
+    const SP MUc{{MUw, MUw + 32}}, VRc{{VRw, VRw + 32}}, RSc{{RSw, RSw + 32}};
+    auto put_part = [&](int seg, S v) {                       // lane 0: the warp's sum of one segment
+        if constexpr (P::kPair) wpart[(warp * LNF_SEG + seg) * 2 + pr.party()] = v;
+        else { wpart[(warp * LNF_SEG + seg) * 2] = v.s0; wpart[(warp * LNF_SEG + seg) * 2 + 1] = v.s1; }
     };
-    auto getsum = [&](const u64* base, int r) -> S {
-        if constexpr (P::kPair) return base[32 * pr.party() + r];
-        else return S{base[r], base[32 + r]};
+    auto get_part = [&](int w, int seg) -> S {
+        if constexpr (P::kPair) return wpart[(w * LNF_SEG + seg) * 2 + pr.party()];
+        else return S{wpart[(w * LNF_SEG + seg) * 2], wpart[(w * LNF_SEG + seg) * 2 + 1]};
     };
     const i64 nblk = (a.rows + a.RB - 1) / a.RB;
     for (i64 blk = cta; blk < nblk; blk += ncta) {
         const i64 r0 = blk * a.RB;
         const int R = (int)min((i64)a.RB, a.rows - r0);
         const u64 g0 = a.row_off + (u64)r0;                   // even
-        const i64 np = (i64)R * C / 2;                       // element pairs of the block (C even)
+        const i64 np = (i64)R * hc;                          // element pairs of the block
         const i64 wbeg = np * warp / NW, wend = np * (warp + 1) / NW;
-        const i64 iters = (wend - wbeg + 32 * V - 1) / (32 * V);   // warp-uniform trip count
+        const int rw0 = (int)(wbeg / hc);                     // the warp's first row (segment 0)
+        const int nseg = wend > wbeg ? (int)((wend - 1) / hc) - rw0 + 1 : 0;
         const u64 ub = g0 * (u64)C;                           // global unit of the block's element 0
         const SP xb{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
         const SO zb{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
-        for (int t = threadIdx.x; t < 256; t += blockDim.x) lsm[t] = 0;
-        __syncthreads();
-        // A: row sums
-        {
+        // row sum of the warps' segments that cover row r (a row spans at most a few warps)
+        auto row_total = [&](int r) -> S {
+            S t = pr.zero();
+            for (int w = 0; w < NW; ++w) {
+                const i64 b0 = np * w / NW, e0 = np * (w + 1) / NW;
+                if (e0 <= b0) continue;
+                const int f = (int)(b0 / hc), l = (int)((e0 - 1) / hc);
+                if (r >= f && r <= l) t = pr.add(t, get_part(w, r - f));
+            }
+            return t;
+        };
+        // A: row sums (loads LA pairs ahead: this pass has no arithmetic to hide them)
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int r = rw0 + sg;
+            const i64 sb = max(wbeg, (i64)r * hc), se = min(wend, (i64)(r + 1) * hc);
+            constexpr int LA = 8;
             S acc = pr.zero();
-            int cur = -1;
-            for (i64 it = 0; it < iters; ++it)
+            for (i64 base = sb + lane; base < se; base += 32 * LA) {
+                S xa[LA], xc[LA];
 #pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    const i64 P2 = wbeg + (it * V + v) * 32 + lane;
-                    if (P2 < wend) {
-                        S xa, xc;
-                        pr.ld_pair(xb, 2 * P2, true, true, xa, xc);
-                        const int r = (int)fdiv((u32)(2 * P2), dC);
-                        if (r != cur) { if (cur >= 0) flush(SA, cur, acc); cur = r; acc = pr.zero(); }
-                        acc = pr.add(acc, pr.add(xa, xc));
-                    }
+                for (int q = 0; q < LA; ++q) {
+                    xa[q] = xc[q] = pr.zero();
+                    if (base + 32 * q < se) pr.ld_pair(xb, 2 * (base + 32 * q), true, true, xa[q], xc[q]);
                 }
-            if (cur >= 0) flush(SA, cur, acc);
+#pragma unroll
+                for (int q = 0; q < LA; ++q) acc = pr.add(acc, pr.add(xa[q], xc[q]));
+            }
+            acc = pr.sumw(acc);
+            if (lane == 0) put_part(sg, acc);
         }
         __syncthreads();
         if (threadIdx.x < R) {
-            S mu = getsum(SA, threadIdx.x);
+            S mu = row_total(threadIdx.x);
             mu = a.mean_mode == 0 ? pr.mulf(mu, a.e_invd) : pr.divp(mu, C);
             pr.st(MU, threadIdx.x, mu);
         }
         __syncthreads();
-        // B: sum of MT(c, c)
-        {
+        // B: sum of MT(c, c); the next iteration's pairs load while this one computes
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int r = rw0 + sg;
+            const i64 sb = max(wbeg, (i64)r * hc), se = min(wend, (i64)(r + 1) * hc);
+            const S m = pr.ld(MUc, r);
+            const i64 iters = (se - sb + 32 * V - 1) / (32 * V);
             S acc = pr.zero();
-            int cur = -1;
+            S nxa[V], nxc[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                nxa[v] = nxc[v] = pr.zero();
+                if (sb + v * 32 + lane < se) pr.ld_pair(xb, 2 * (sb + v * 32 + lane), true, true, nxa[v], nxc[v]);
+            }
             for (i64 it = 0; it < iters; ++it) {
                 u64 u[V];
-                S ca[V], cb[V], za[V], zb2[V];
-                int rr[V];
+                S ca[V], cb[V], za[V], zz[V];
                 bool ok[V];
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    const i64 P2 = wbeg + (it * V + v) * 32 + lane;
-                    ok[v] = P2 < wend;
+                    const i64 P2 = sb + (it * V + v) * 32 + lane;
+                    ok[v] = P2 < se;
                     u[v] = ub + 2 * (u64)P2;
-                    ca[v] = cb[v] = pr.zero();
-                    rr[v] = 0;
-                    if (ok[v]) {
-                        pr.ld_pair(xb, 2 * P2, true, true, ca[v], cb[v]);
-                        rr[v] = (int)fdiv((u32)(2 * P2), dC);
-                        const S m = pr.ld(MUc, rr[v]);
-                        ca[v] = pr.sub(ca[v], m);
-                        cb[v] = pr.sub(cb[v], m);
-                    }
+                    ca[v] = pr.sub(nxa[v], m); cb[v] = pr.sub(nxc[v], m);
+                    const i64 Q2 = P2 + 32 * V;
+                    nxa[v] = nxc[v] = pr.zero();
+                    if (Q2 < se) pr.ld_pair(xb, 2 * Q2, true, true, nxa[v], nxc[v]);
                 }
-                pr.template bm2v<V>(u, a.s_sq, ca, ca, cb, cb, za, zb2);
+                pr.template bm2v<V>(u, a.s_sq, ca, ca, cb, cb, za, zz);
 #pragma unroll
                 for (int v = 0; v < V; ++v)
-                    if (ok[v]) {
-                        if (rr[v] != cur) { if (cur >= 0) flush(SV, cur, acc); cur = rr[v]; acc = pr.zero(); }
-                        acc = pr.add(acc, pr.add(pr.shr_(za[v], FRAC), pr.shr_(zb2[v], FRAC)));
-                    }
+                    if (ok[v]) acc = pr.add(acc, pr.add(pr.shr_(za[v], FRAC), pr.shr_(zz[v], FRAC)));
             }
-            if (cur >= 0) flush(SV, cur, acc);
+            acc = pr.sumw(acc);
+            if (lane == 0) put_part(sg, acc);
         }
         __syncthreads();
         if (threadIdx.x < R) {
-            S v = getsum(SV, threadIdx.x);
+            S v = row_total(threadIdx.x);
             v = a.mean_mode == 0 ? pr.mulf(v, a.e_invd) : pr.divp(v, C);
-            v = pr.addp(v, a.e_eps);
-            pr.st(SO{{SV, SV + 32}}, threadIdx.x, v);     // the variance replaces its sum
+            pr.st(VR, threadIdx.x, pr.addp(v, a.e_eps));
         }
         if constexpr (!P::kPair)
             if (tab) nr_pregen<1>(*pr.Kp, a.s_rs, a.rk, g0, tab);
         __syncthreads();
         // C: r = RSQRT(v), row units g0 + lane
-        tile_nr<1, false>(pr, a.s_rs, a.rk, R, g0, SP{{SV, SV + 32}}, RS, tab);
+        tile_nr<1, false>(pr, a.s_rs, a.rk, R, g0, VRc, RS, tab);
         // D: out = MT(c, r)
-        for (i64 it = 0; it < iters; ++it) {
-            u64 u[V];
-            S ca[V], cb[V], ra[V], za[V], zb2[V];
-            i64 e0[V];
-            bool ok[V];
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int r = rw0 + sg;
+            const i64 sb = max(wbeg, (i64)r * hc), se = min(wend, (i64)(r + 1) * hc);
+            const S m = pr.ld(MUc, r), rr = pr.ld(RSc, r);
+            const i64 iters = (se - sb + 32 * V - 1) / (32 * V);
+            S nxa[V], nxc[V];
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-                const i64 P2 = wbeg + (it * V + v) * 32 + lane;
-                ok[v] = P2 < wend;
-                e0[v] = 2 * P2;
-                u[v] = ub + 2 * (u64)P2;
-                ca[v] = cb[v] = ra[v] = pr.zero();
-                if (ok[v]) {
-                    pr.ld_pair(xb, e0[v], true, true, ca[v], cb[v]);
-                    const int r = (int)fdiv((u32)e0[v], dC);
-                    const S m = pr.ld(MUc, r);
-                    ca[v] = pr.sub(ca[v], m);
-                    cb[v] = pr.sub(cb[v], m);
-                    ra[v] = pr.ld(RSc, r);
-                }
+                nxa[v] = nxc[v] = pr.zero();
+                if (sb + v * 32 + lane < se) pr.ld_pair(xb, 2 * (sb + v * 32 + lane), true, true, nxa[v], nxc[v]);
             }
-            pr.template bm2v<V>(u, a.s_mul, ca, ra, cb, ra, za, zb2);
+            for (i64 it = 0; it < iters; ++it) {
+                u64 u[V];
+                S ca[V], cb[V], rv[V], za[V], zz[V];
+                i64 e0[V];
+                bool ok[V];
 #pragma unroll
-            for (int v = 0; v < V; ++v)
-                if (ok[v]) pr.st_pair(zb, e0[v], true, true, pr.shr_(za[v], FRAC), pr.shr_(zb2[v], FRAC));
+                for (int v = 0; v < V; ++v) {
+                    const i64 P2 = sb + (it * V + v) * 32 + lane;
+                    ok[v] = P2 < se;
+                    e0[v] = 2 * P2;
+                    u[v] = ub + 2 * (u64)P2;
+                    ca[v] = pr.sub(nxa[v], m); cb[v] = pr.sub(nxc[v], m); rv[v] = rr;
+                    const i64 Q2 = P2 + 32 * V;
+                    nxa[v] = nxc[v] = pr.zero();
+                    if (Q2 < se) pr.ld_pair(xb, 2 * Q2, true, true, nxa[v], nxc[v]);
+                }
+                pr.template bm2v<V>(u, a.s_mul, ca, rv, cb, rv, za, zz);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (ok[v]) pr.st_pair(zb, e0[v], true, true, pr.shr_(za[v], FRAC), pr.shr_(zz[v], FRAC));
+            }
         }
         __syncthreads();
     }
     pa.done(pr);
 }
+
+}  // namespace mpc

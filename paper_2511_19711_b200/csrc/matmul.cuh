@@ -16,8 +16,9 @@ namespace mpc {
 // Operand planes of one part (A part: n = batch*M*K units; B part: batch*K*N):
 //   A part: [0] E = open(X - A), [1] A0, [2] A1, [3] A0 + A1
 //   B part: [0] F = open(Y - B), [1] B0 + F, [2] B1, [3] B0 + B1
-// In PAIR mode each party writes the planes its GEMM reads (party 0: E, A0 / F, B0+F; party 1 --
-// which also plays the dealer -- E, A1, A0+A1 / F, B1, B0+B1).
+// In PAIR mode each party writes the planes its GEMM reads (party 0: E, A0 / F, B0+F; party 1
+// simulating the dealer: E, A1, A0+A1 / F, B1, B0+B1 -- with the dealer's stream only E, A1 / F, B1
+// are used: party 1's GEMM reads the dealer's C1).
 struct MmMaskBody {
     u32 s, slot; SP x; i64 n; u64* out; int bpart;
     template <int V, class P>
@@ -27,7 +28,7 @@ struct MmMaskBody {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
             const bool va = ok[v] && i0[v] >= 0, vb = ok[v] && i0[v] + 1 < n;
-            const uint4 R0 = prg(pr.Kp->k0, u[v] >> 1, s, slot);
+            const uint4 R0 = pr.k0ok() ? prg(pr.Kp->k0, u[v] >> 1, s, slot) : make_uint4(0, 0, 0, 0);
             uint4 R1 = make_uint4(0, 0, 0, 0);
             if (p != 0) R1 = prg(pr.Kp->k1, u[v] >> 1, s, slot);
             const u64 r0a = w64(R0.x, R0.y), r0b = w64(R0.z, R0.w), r1a = w64(R1.x, R1.y), r1b = w64(R1.z, R1.w);
@@ -53,15 +54,21 @@ struct MmArgs {
     int p0, np;                                      // parties computed by this launch
     MmTerm t[2][3]; int nt[2];
     u64* z[2];
+    const u64* cin[2];      // party p's C term read from memory (party 1: the dealer's C1)
 };
 
 // C0 epilogue + truncation for output element (b, m, n) of party p
 __device__ __forceinline__ u64 mm_epilogue(const MmArgs& a, int p, int b, int m, int n, u64 acc)
 {
-    const u64 uC = (a.goff + (u64)b) * (u64)a.M * (u64)a.N + (u64)m * (u64)a.N + (u64)n;
-    const uint4 C = prg(a.K.k0, uC >> 1, a.s, 10);
-    const u64 c0 = (uC & 1) ? w64(C.z, C.w) : w64(C.x, C.y);
-    const u64 v = p == 0 ? acc + c0 : acc - c0;
+    u64 v;
+    if (a.cin[p]) {
+        v = acc + a.cin[p][(i64)b * a.M * a.N + (i64)m * a.N + n];
+    } else {
+        const u64 uC = (a.goff + (u64)b) * (u64)a.M * (u64)a.N + (u64)m * (u64)a.N + (u64)n;
+        const uint4 C = prg(a.K.k0, uC >> 1, a.s, 10);
+        const u64 c0 = (uC & 1) ? w64(C.z, C.w) : w64(C.x, C.y);
+        v = p == 0 ? acc + c0 : acc - c0;
+    }
     return a.tb ? shr(v, a.tb) : v;
 }
 

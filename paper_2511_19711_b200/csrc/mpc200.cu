@@ -1195,8 +1195,6 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
         batch * M * K >= (1ll << 40) || batch * K * N >= (1ll << 40) || batch * nparty > 65535)
         return fail(c, MPC_ERR_INVALID, "matmul: bad shape (batch x parties <= 65535 grid z)");
     if (bad_sh(c, x) || bad_sh(c, y) || bad_sh(c, z)) return fail(c, MPC_ERR_INVALID, "matmul: null pointer");
-    if (is_dealer(c) || c->corr_on)          // the matrix triple's C1 is not stream-fed
-        return fail(c, MPC_ERR_UNSUPPORTED, "matmul: no dealer correction stream for the matrix triple");
     if (batch == 0) { finish(c, 1); return MPC_OK; }
     const bool tc_ok = 3 * K <= 16384;                // exact limb accumulators (matmul_tc.cuh)
     if (c->mm_engine == 2 && !tc_ok) return fail(c, MPC_ERR_UNSUPPORTED, "matmul: tensor-core engine needs K <= 5461");
@@ -1230,6 +1228,27 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
     a.z[0] = z.sh[0]; a.z[1] = z.sh[1];
     if (c->cfg.mode == MPC_MODE_PAIR) { a.p0 = c->cfg.party; a.np = 1; }
     else { a.p0 = 0; a.np = 2; }
+    // the trusted dealer's matrix correction C1 = (A0+A1)(B0+B1) - C0: the dealer forms
+    // it with ONE GEMM term and writes it as a stream segment; party 1 reads it in its epilogue and
+    // multiplies only E B1 + A1 F (K' = 2K instead of 3K)
+    const u64 nC = (u64)(batch * M * N);
+    if (is_dealer(c)) {
+        if (c->dw_end + nC > c->dw_cap) {
+            const u64 ncap = std::max<u64>(c->dw_end + nC, 2 * c->dw_cap);
+            u64* nw = nullptr;
+            if (cudaMalloc(&nw, ncap * sizeof(u64)) != cudaSuccess) return fail(c, MPC_ERR_NOMEM, "dealer stream");
+            if (c->dw) { cudaMemcpyAsync(nw, c->dw, c->dw_end * sizeof(u64), cudaMemcpyDeviceToDevice, c->stream); cudaStreamSynchronize(c->stream); cudaFree(c->dw); }
+            c->dw = nw; c->dw_cap = ncap;
+        }
+        a.nt[1] = 1; a.tb = 0; a.p0 = 1; a.np = 1;
+        a.z[1] = c->dw + c->dw_end;
+    } else if (c->corr_on && a.p0 + a.np > 1) {
+        if (c->cnext >= c->nseg || c->segv[c->cnext].tag != fnv_tag("matmul_c1") || c->segv[c->cnext].threads != nC)
+            return fail(c, MPC_ERR_PROTOCOL, "matmul: the next correction segment is not this product's C1");
+        a.cin[1] = c->cwords + c->segv[c->cnext].base;
+        ++c->cnext;
+        a.t[1][0] = MmTerm{E, B1}; a.t[1][1] = MmTerm{A1, F}; a.nt[1] = 2;                     // C1 + E B1 + A1 F
+    }
     if (!use_tc) {
         const dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64), (unsigned)(batch * a.np));
         rec_begin(c, "matmul", (u64)(batch * M * N));
@@ -1244,7 +1263,7 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
         u8* lp = sc + plane_bytes;
         u8* LA[2] = {lp, lp + la0 + lb0};
         u8* LB[2] = {lp + la0, lp + la0 + lb0 + la1};
-        const i64 Kps[2] = {Kp0, Kp1};
+        const i64 Kps[2] = {Kp0, a.nt[1] * Kpad};
         if (fused) {
             const i64 KBn = Kpad / TC_BK;
             FuseArgs fx{c->K, s, x.sh[0], x.sh[1], (int)M, (int)K, (int)batch, (u64)batch_off, LA[0], LA[1]};
@@ -1284,6 +1303,15 @@ mpc_status mpc_matmul(mpc_ctx* c, mpc_shares x, mpc_shares y, mpc_shares z, int6
         rec_end(c);
         c->st.launches++;
         if ((st = cuda_check(c, "matmul_tc"))) return st;
+    }
+    if (is_dealer(c)) {
+        if ((st = cuda_check(c, "matmul_c1"))) return st;
+        if (c->nseg == c->capseg) {
+            c->capseg = c->capseg ? 2 * c->capseg : 64;
+            c->segv = (mpc_corr_seg*)realloc(c->segv, sizeof(mpc_corr_seg) * (size_t)c->capseg);
+        }
+        c->segv[c->nseg++] = mpc_corr_seg{c->dw_end, nC, 1, fnv_tag("matmul_c1")};
+        c->dw_end += nC;
     }
     c->last_philox += (u64)(nA + nB) + (u64)(batch * M * N + 1) / 2;
     c->st.bytes_per_party += 8ull * (u64)(nA + nB);
@@ -1870,7 +1898,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
             LnFArgs f{a.s_sq, a.s_rs, a.s_mul, a.rk, a.x, a.z, rows, cols, (u64)row_off, a.mean_mode, a.e_invd,
                       a.e_eps, 2, 0};
             f.nrtab = (!is_pair(c) && nsteps_rs <= MPC_NR_TAB_MAX_STEPS) ? 1 : 0;
-            const size_t dyn = sizeof(u64) * (256 + (f.nrtab ? (size_t)nsteps_rs * NR_TAB_F * 32 : 0));
+            const size_t dyn = sizeof(u64) * (size_t)lnf_smem_u64(f.nrtab ? nsteps_rs : 0);
             auto rb_for = [&](i64 slots) {
                 i64 rb = (rows + slots - 1) / std::max<i64>(1, slots);
                 rb = std::max<i64>(2, std::min<i64>(32, (rb + 1) / 2 * 2));

@@ -47,6 +47,7 @@ struct BothP {
 #endif
     static constexpr int kV = MPC_BOTH_KV;   // unit pairs per lane per pass (registers hold both parties)
     __device__ __forceinline__ int party() const { return -1; }
+    __device__ __forceinline__ bool k0ok() const { return true; }
     __device__ __forceinline__ S zero() const { return {0, 0}; }
     __device__ __forceinline__ S ld(SP a, i64 i) const { return {a.p[0][i], a.p[1][i]}; }
     __device__ __forceinline__ void st(SO a, i64 i, S v) const { a.p[0][i] = v.s0; a.p[1][i] = v.s1; }

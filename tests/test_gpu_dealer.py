@@ -79,6 +79,9 @@ CASES = {
     "layernorm_bcast_mode1": (64 * 300, lambda c, x: c.layernorm(x, 64, 300, bcast=1, mean_mode=1)),
     "layernorm_clamp": (64 * 256, lambda c, x: c.layernorm(x, 64, 256, rsqrt_clamp=1, rsqrt_t=4)),
     "open": (5000, lambda c, x: (c.mul(x, x, trunc_bits=16), c.open(x)[0])[0]),
+    # the matrix triple: the dealer's GEMM writes C1 = (A0+A1)(B0+B1) - C0 as one segment
+    "matmul_tc": (64 * 96, lambda c, x: c.matmul(x, x, 1, 64, 96, 64, trunc_bits=16)),
+    "matmul_batched": (3 * 40 * 32, lambda c, x: c.matmul(x, x, 3, 40, 32, 40, batch_off=2)),
 }
 
 
@@ -153,11 +156,17 @@ def test_dealer_hostio_softmax(m):
     assert torch.equal(hz[0], zb[0].cpu()) and torch.equal(hz[1], zb[1].cpu())
 
 
-def test_dealer_refuses_matmul_and_party0(m):
+def test_dealer_matmul_simt_engine(m):
+    def fn(c, x):
+        c.set_matmul_engine(1)
+        return c.matmul(x, x, 2, 24, 40, 24, trunc_bits=16)
+    zb, zp, _ = run_case(m, 2 * 24 * 40, fn)
+    assert eq(zb, zp)
+
+
+def test_dealer_refuses_party0(m):
     keys = workloads.keys(1)
     d = m.Ctx.dealer(keys)
-    with pytest.raises(m.MPCError, match="UNSUPPORTED"):
-        d.matmul(m.Ctx.like(64), m.Ctx.like(64), 1, 8, 8, 8)
     b = m.Ctx.for_cfg(keys)
     with pytest.raises(m.MPCError, match="INVALID"):
         b.set_corrections(d.dealer_stream())

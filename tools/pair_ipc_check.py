@@ -14,8 +14,7 @@ LayerNorm), and an open to party 1 only.
   python tools/pair_ipc_check.py --exchange=0 (the LL wire format instead of the LL63 default)
   python tools/pair_ipc_check.py --dealer    (party 1's context is created WITHOUT K_0 (key_p0 = 0) and
                                               reads its corrections from a trusted-dealer stream made
-                                              offline by an MPC_MODE_DEALER context, DESIGN.md 7.1;
-                                              the matrix triple is not stream-fed, so no matmul)"""
+                                              offline by an MPC_MODE_DEALER context)"""
 import os
 import sys
 
@@ -75,7 +74,7 @@ def worker(rank, world, port, q, mismatch=False):
         c = m.Ctx(keys["key_share"], 0, keys["key_p1"], dev, mode=m.binding.MODE_PAIR, party=1)
         d = m.Ctx.dealer(keys, device=dev)
         d.set_step(c.step)
-        ops(d, None, 1, rows, cols, matmul=False)
+        ops(d, None, 1, rows, cols)
         d.open_to(m.Ctx.like(rows * cols), 1)          # the final open's (empty) segment
         c.set_corrections(d.dealer_stream())
     else:
@@ -105,7 +104,7 @@ def worker(rank, world, port, q, mismatch=False):
         dist.barrier()
         dist.destroy_process_group()
         return
-    res = ops(c, x if rank == 0 else None, rank, rows, cols, matmul=not dealer)
+    res = ops(c, x if rank == 0 else None, rank, rows, cols)
     ring1, _ = c.open_to(res[0], 1)                   # only party 1 learns rec(x)
     c.sync()
     if dealer and rank == 1 and c.corrections_left() != 0:
@@ -115,7 +114,7 @@ def worker(rank, world, port, q, mismatch=False):
     dist.all_gather_object(gathered, mine)
     if rank == 0:
         b = m.Ctx.for_cfg(keys, device=dev)
-        ref = ops(b, x, 0, rows, cols, matmul=not dealer)
+        ref = ops(b, x, 0, rows, cols)
         ring_ref, _ = b.open(ref[0])
         torch.cuda.synchronize()
         bad = []
