@@ -206,6 +206,14 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
     if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(K, q, s, w, x, lane);
     const int m = w - 1;
     const PrgQ Q0 = prg_q(K.k0, q, s), Q1 = prg_q(K.k1, q, s);
+#ifndef MPC_LTZ_HOIST
+#define MPC_LTZ_HOIST 1       // the daBit blocks first (interleave with the g-layer's); with UNIFORM: max tree -4 %
+#endif
+#ifndef MPC_LTZ_UNIFORM
+#define MPC_LTZ_UNIFORM 1     // every lane issues each level's blocks (no divergence; SIMT issues them anyway)
+#endif
+    uint4 D0h = make_uint4(0, 0, 0, 0), D1h = D0h;
+    if (MPC_LTZ_HOIST) { D0h = prg(Q0, 2u + (u32)lane); D1h = prg(Q1, 1u); }
     // A2B (local): lane j receives plane j of both parties' shares.
     u32 P0[2], P1[2], G0[2], G1[2];
     P0[0] = transpose32((u32)x.s0, lane);
@@ -242,7 +250,8 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
 #pragma unroll
         for (int h = 0; h < H; ++h) {
             const int j = lane + 32 * h;
-            if (j >= d && j < m) {
+            const bool act = j >= d && j < m;
+            if (MPC_LTZ_UNIFORM || act) {
                 // source plane j-d lives in lane src, half h (if lane >= d) or h-1
                 int hs = h;
                 if (d < 32) hs = (lane >= d) ? h : h - 1;
@@ -256,8 +265,10 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
                 u32 ng0, ng1, np0, np1;
                 and_both(P0[h], P1[h], g0, g1, tg.x, tg.y, tg.z, t1.x, t1.y, ng0, ng1);
                 and_both(P0[h], P1[h], p0, p1, tp.x, tp.y, tp.z, t1.z, t1.w, np0, np1);
-                G0[h] ^= ng0; G1[h] ^= ng1;
-                P0[h] = np0; P1[h] = np1;
+                if (act) {
+                    G0[h] ^= ng0; G1[h] ^= ng1;
+                    P0[h] = np0; P1[h] = np1;
+                }
             }
         }
     }
@@ -275,8 +286,8 @@ __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int 
         b1 = (u32)((x.s1 >> (w - 1)) & 1ull) ^ ((gm1 >> lane) & 1u);
     }
     // daBit + B2A: c = open(b ^ r); z0 = c + (1-2c) r0A; z1 = (1-2c) r1A
-    const uint4 D0 = prg(Q0, 2u + (u32)lane);
-    const uint4 D1 = prg(Q1, 1u);
+    const uint4 D0 = MPC_LTZ_HOIST ? D0h : prg(Q0, 2u + (u32)lane);
+    const uint4 D1 = MPC_LTZ_HOIST ? D1h : prg(Q1, 1u);
     const u64 r0A = w64(D0.x, D0.y);
     const u32 r0B = D0.z & 1u;
     const u32 r1B = (D1.x >> lane) & 1u;
