@@ -1631,16 +1631,19 @@ mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int
 
 // The two parties' copies of one chunk and direction as ONE DMA submission: with both PCIe directions
 // busy, every separate cudaMemcpyAsync costs ~9 us of link time (tools/pcie_copy.cu: cfg2, 4 chunks x
-// 2 parties both ways).  The two chunks are the two rows of a pitched 2D copy when both sides' party
-// arrays are ordered and at most 2 GB apart (e.g. one pinned [2][n] host tensor); otherwise one copy
-// per party.
-static void copy_pair(void** dst, void** src, size_t bytes, int n, cudaStream_t s, cudaMemcpyKind kind)
+// 2 parties both ways).  The two chunks are the two rows of a pitched 2D copy when each side's party
+// arrays are one allocation: the device staging always is, the host arrays when they are ADJACENT
+// (party 1's array starts right after party 0's, e.g. one pinned [2][n] tensor: pitch == adj bytes;
+// the driver refuses a pitch that spans two allocations).  Otherwise one copy per party.
+static void copy_pair(void** dst, void** src, size_t bytes, int n, cudaStream_t s, cudaMemcpyKind kind,
+                      size_t host_adj)
 {
     if (n == 2) {
         const char *d0 = (const char*)dst[0], *d1 = (const char*)dst[1];
         const char *s0 = (const char*)src[0], *s1 = (const char*)src[1];
         const int64_t dp = d1 - d0, sp = s1 - s0, lim = (int64_t)1 << 31;
-        if (dp >= (int64_t)bytes && sp >= (int64_t)bytes && dp < lim && sp < lim) {
+        const int64_t hp = kind == cudaMemcpyHostToDevice ? sp : dp;      // the host side's pitch
+        if (hp == (int64_t)host_adj && dp >= (int64_t)bytes && sp >= (int64_t)bytes && dp < lim && sp < lim) {
             if (cudaMemcpy2DAsync(dst[0], (size_t)dp, src[0], (size_t)sp, bytes, 2, kind, s) == cudaSuccess) return;
             cudaGetLastError();                    // pitch not accepted: fall back to single copies
         }
@@ -1754,7 +1757,7 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         {
             void* dst[2]; void* src[2];
             for (int q = 0; q < np; ++q) { dst[q] = dx[parties[p0 + q]]; src[q] = hx.sh[parties[p0 + q]] + r0 * cols; }
-            copy_pair(dst, src, bytes, np, h->h2d, cudaMemcpyHostToDevice);
+            copy_pair(dst, src, bytes, np, h->h2d, cudaMemcpyHostToDevice, sizeof(u64) * (size_t)(rows * cols));
         }
         cudaEventRecord(h->in_ready[b], h->h2d);
         mark(h->h2d);
@@ -1776,7 +1779,7 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         {
             void* dst[2]; void* src[2];
             for (int q = 0; q < np; ++q) { dst[q] = hz.sh[parties[p0 + q]] + r0 * cols; src[q] = dz[parties[p0 + q]]; }
-            copy_pair(dst, src, bytes, np, h->d2h, cudaMemcpyDeviceToHost);
+            copy_pair(dst, src, bytes, np, h->d2h, cudaMemcpyDeviceToHost, sizeof(u64) * (size_t)(rows * cols));
         }
         cudaEventRecord(h->out_done[b], h->d2h);
         mark(h->d2h);

@@ -5,7 +5,8 @@ Each case draws its parameters from a counter-seeded numpy Generator, so a failu
 the case id that reproduces it.  The fixed-parameter tests (test_gpu_parity.py, ...) pin the
 known edge cases; this sweep covers the combinations between them: ragged sizes, odd row
 lengths, large step ids, LTZ circuit (Kogge-Stone / cone), protocol variants (square pairs,
-broadcast triple, power basis), matmul engines, and a share of the cases in PAIR_LOOPBACK.
+broadcast triple, power basis), matmul engines, and a share of the cases in PAIR_LOOPBACK (half of
+those with party 1 reading the trusted dealer's correction stream).
 """
 import os
 
@@ -162,16 +163,28 @@ def test_fuzz_case(m, case):
     keys = workloads.keys(int(r.integers(1, 6)))
     step = int(r.integers(0, 1 << 24))
     loopback = case % 4 == 3
+    dealer = loopback and case % 8 == 7          # half the loopback cases: party 1 reads the dealer's stream
     c = m.Ctx.for_cfg(keys, mode=m.binding.MODE_PAIR_LOOPBACK) if loopback else m.Ctx.for_cfg(keys)
-    c.set_ltz_circuit(int(r.integers(0, 2)))
-    c.set_matmul_engine(int(r.integers(0, 3)))
+    circuit, engine = int(r.integers(0, 2)), int(r.integers(0, 3))
+    c.set_ltz_circuit(circuit)
+    c.set_matmul_engine(engine)
     o = Oracle.for_cfg(keys, step)
     # input sharing through the oracle: both sides start from the same shares
     osh = [o.share(x, owner=int(r.integers(0, 2)), off=int(r.integers(0, 1 << 20))) for x in xs]
     gsh = [tuple(torch.from_numpy(np.ascontiguousarray(p)).cuda() for p in s) for s in osh]
     c.set_step(o.step)
+    if dealer:                                   # the dealer's offline pass first
+        d = m.Ctx.dealer(keys, target=m.binding.MODE_PAIR_LOOPBACK)
+        d.set_ltz_circuit(circuit)
+        d.set_matmul_engine(engine)
+        d.set_step(o.step)
+        gpu_call(d, [m.Ctx.like(len(s[0])) for s in osh])
+        c.set_corrections(d.dealer_stream())
     g = gpu_call(c, gsh)
     c.sync()
+    if dealer:
+        # (an op with no PAIR launch, e.g. trunc, leaves an empty stream: set_corrections then clears)
+        assert c.corrections_left() in (0, -1), f"case {case} ({name}): dealer stream not consumed"
     ref = orc_call(o, osh)
-    _same(g, ref, f"case {case} ({name}, {'loopback' if loopback else 'both'})")
+    _same(g, ref, f"case {case} ({name}, {'loopback + dealer' if dealer else 'loopback' if loopback else 'both'})")
     assert c.step == o.step, f"case {case} ({name}): step {c.step} != oracle {o.step}"

@@ -33,3 +33,24 @@ def test_hostio_equals_device_softmax(m, rows, cols, chunk, mode):
     assert torch.equal(hz[0], z[0].cpu()) and torch.equal(hz[1], z[1].cpu())
     if mode:
         c.sync()
+
+
+@pytest.mark.parametrize("mode", [0, 2])
+def test_hostio_adjacent_party_buffers(m, mode):
+    """Both parties' host shares in ONE pinned [2][n] tensor each way: every chunk's two party
+    copies go as one pitched 2D DMA (copy_pair); same output shares as the device softmax."""
+    keys = workloads.keys(2)
+    rows, cols = 3000, 128
+    c = m.Ctx.for_cfg(keys, mode=mode)
+    x = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    s0 = c.step
+    z = c.softmax(x, rows, cols)
+    hin = torch.empty((2, rows * cols), dtype=torch.uint64).pin_memory()
+    hout = torch.empty((2, rows * cols), dtype=torch.uint64).pin_memory()
+    hin[0].copy_(x[0].cpu()); hin[1].copy_(x[1].cpu())
+    c.set_step(s0, force=True)
+    c.softmax_hostio((hin[0], hin[1]), (hout[0], hout[1]), rows, cols, chunk_rows=768)
+    torch.cuda.synchronize()
+    assert torch.equal(hout[0], z[0].cpu()) and torch.equal(hout[1], z[1].cpu())
+    if mode:
+        c.sync()

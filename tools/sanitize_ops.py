@@ -72,6 +72,24 @@ def run(mode, circuit):
     hz = tuple(torch.empty_like(t).pin_memory() for t in hx)
     c.softmax_hostio(hx, hz, 45, 77, chunk_rows=32)
     if mode != m.binding.MODE_BOTH:
+        # round 2: the trusted dealer's stream -- the dealer's pass (stream role,
+        # writes) and party 1 reading it (stream role, loads) over the same op sequence
+        d = m.Ctx.dealer(workloads.keys(1), target=mode)
+        d.set_ltz_circuit(circuit)
+        def seq(cc, xx, ss, lnn, aa, bb):
+            cc.mul(xx, xx, trunc_bits=16)
+            cc.relu(xx)
+            cc.gelu(xx, form="poly_abs", degree=4)
+            cc.softmax(ss, 45, 77)
+            cc.layernorm(lnn, 40, 96)
+            cc.matmul(aa, bb, 2, 70, 33, 129, trunc_bits=16)
+        d.set_step(c.step)
+        like = m.Ctx.like
+        seq(d, like(1000), like(45 * 77), like(40 * 96), like(2 * 70 * 33), like(2 * 33 * 129))
+        c.set_corrections(d.dealer_stream())
+        seq(c, x, s, ln, a, b)
+        c.sync()
+        c.set_corrections(None)
         c.sync()
     torch.cuda.synchronize()
 
