@@ -20,6 +20,9 @@
 #ifndef MPC_GROUP_PREFETCH
 #define MPC_GROUP_PREFETCH 1   // element-wise drivers prefetch the next pass's input shares to L2
 #endif
+#ifndef MPC_MAXS_PAIRS
+#define MPC_MAXS_PAIRS 0      // A/B: short-row max with the cone in BOTH: 4-group batches as 2 x 2 flat
+#endif
 #ifndef MPC_EW_MINB
 #define MPC_EW_MINB 2      // same for the element-wise drivers
 #endif
@@ -471,10 +474,11 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
         const i64 gpw = (i64)rw * h / 32;              // groups per warp when warp-local
         const i64 gend = wl ? (warp + 1) * gpw : h;    // 32*h units = h groups per tile
         if constexpr (CONE) {
-            for (i64 gb = wl ? warp * gpw : (i64)warp * CG; gb < gend; gb += wl ? CG : (i64)NW * CG) {
-                S d[CG], l[CG];
+            constexpr int GB = CG;     // (one group per call in BOTH measured 4 % slower on softmax_cone)
+            for (i64 gb = wl ? warp * gpw : (i64)warp * GB; gb < gend; gb += wl ? GB : (i64)NW * GB) {
+                S d[GB], l[GB];
 #pragma unroll
-                for (int g = 0; g < CG; ++g) {
+                for (int g = 0; g < GB; ++g) {
                     const i64 v = (gb + g) * 32 + lane;
                     d[g] = pr.zero();
                     if (gb + g < gend && v < (i64)R * h) {
@@ -482,9 +486,10 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
                         d[g] = pr.sub(ldc(rr, i), ldc(rr, i + h));
                     }
                 }
-                pr.template ltz_cone<CG, WIDE ? 64 : 32>((ubase >> 5) + (u64)gb, sl, w, d, l, lane, cone[warp]);
+                pr.template ltz_cone<GB, WIDE ? 64 : 32>((ubase >> 5) + (u64)gb, sl, w, d, l, lane,
+                                                         *reinterpret_cast<ConeSmem<GB, WIDE ? 64 : 32>*>(&cone[warp]));
 #pragma unroll
-                for (int g = 0; g < CG; ++g) {
+                for (int g = 0; g < GB; ++g) {
                     const i64 v = (gb + g) * 32 + lane;
                     const bool valid = gb + g < gend && v < (i64)R * h;
                     i64 rr = 0, i = 0;
@@ -1011,7 +1016,9 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_max_small(const __grid_con
                     }
                     const int ng = min(CG, h - b);
                     const u64 q = (ubase >> 5) + (u64)b;
-                    if (ng == 1) {
+                    if (ng == 3 || (ng == 4 && !(!decltype(pr)::kPair && MPC_MAXS_PAIRS))) {
+                        pr.template ltz_cone<CG, NL>(q, sl, a.w, d, l, lane, cone_sm[warp]);
+                    } else if (ng == 1) {
                         S d1[1] = {d[0]}, l1[1];
                         pr.template ltz_cone<1, NL>(q, sl, a.w, d1, l1, lane, *reinterpret_cast<ConeSmem<1, NL>*>(&cone_sm[warp]));
                         l[0] = l1[0];
@@ -1019,6 +1026,12 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_max_small(const __grid_con
                         S d2[2] = {d[0], d[1]}, l2[2];
                         pr.template ltz_cone<2, NL>(q, sl, a.w, d2, l2, lane, *reinterpret_cast<ConeSmem<2, NL>*>(&cone_sm[warp]));
                         l[0] = l2[0]; l[1] = l2[1];
+                    } else if (!decltype(pr)::kPair && MPC_MAXS_PAIRS) {
+                        // BOTH: two flat-triple calls of 2 groups (ltz_cone.cuh) instead of one of 4
+                        S da[2] = {d[0], d[1]}, la[2], db[2] = {d[2], d[3]}, lb[2];
+                        pr.template ltz_cone<2, NL>(q, sl, a.w, da, la, lane, *reinterpret_cast<ConeSmem<2, NL>*>(&cone_sm[warp]));
+                        pr.template ltz_cone<2, NL>(q + 2, sl, a.w, db, lb, lane, *reinterpret_cast<ConeSmem<2, NL>*>(&cone_sm[warp]));
+                        l[0] = la[0]; l[1] = la[1]; l[2] = lb[0]; l[3] = lb[1];
                     } else {
                         pr.template ltz_cone<CG, NL>(q, sl, a.w, d, l, lane, cone_sm[warp]);
                     }
@@ -1345,6 +1358,12 @@ struct LnFArgs {
     int nrtab;              // BOTH: rsqrt triples pre-generated into shared memory
 };
 constexpr int LNF_SEG = 34;                    // row segments per warp (<= RB + 1)
+#ifndef MPC_LN_NEXT_PREFETCH
+#define MPC_LN_NEXT_PREFETCH 0     // A/B: 2 blocks per CTA + the next block's rows to L2 during the rsqrt
+#endif                             // phase -- measured 2 % slower than one resident block per CTA (r02)
+#ifndef MPC_LN_BLOCKS_PER_CTA
+#define MPC_LN_BLOCKS_PER_CTA 1
+#endif
 __host__ __device__ inline int lnf_smem_u64(int nsteps_tab) { return 256 + 8 * LNF_SEG * 2 + nsteps_tab * NR_TAB_F * 32; }
 template <class PA>
 __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_fused(const __grid_constant__ PA pa, LnFArgs a)
@@ -1463,6 +1482,15 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_fused(const __g
         }
         if constexpr (!P::kPair)
             if (tab) nr_pregen<1>(*pr.Kp, a.s_rs, a.rk, g0, tab);
+        // the CTA's NEXT block: its rows to L2 now (the rsqrt chain below leaves 7 warps idle and the
+        // product pass is ALU-bound), so its row-sum pass reads L2 instead of waiting on HBM
+        if (MPC_LN_NEXT_PREFETCH && blk + ncta < nblk) {
+            const i64 rn = (blk + ncta) * a.RB, nel = min((i64)a.RB, a.rows - rn) * C;
+            for (i64 l = (i64)threadIdx.x * 16; l < nel; l += (i64)blockDim.x * 16)      // one 128-B line each
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                    if (a.x.p[q]) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.x.p[q] + rn * C + l));
+        }
         __syncthreads();
         // C: r = RSQRT(v), row units g0 + lane
         tile_nr<1, false>(pr, a.s_rs, a.rk, R, g0, VRc, RS, tab);

@@ -93,6 +93,49 @@ __device__ void ltz_cone_both(const Keys& K, u64 q0, u32 s, int w, const Sh (&x)
         }
     }
     __syncwarp();
+    // Flat gate triples (G x the tree's gate nodes <= 64): the tree's Philox blocks are data-
+    // independent, so every lane generates the blocks of its items t = lane + 32 r (level-major over
+    // all levels) up front -- one or two passes of 3 blocks with full ILP instead of a pass per level
+    // with most lanes idle -- and evaluates those items in the level passes from registers.
+    constexpr int RF = (G * (NL - 1) + 31) / 32;
+#ifndef MPC_CONE_FLAT
+#define MPC_CONE_FLAT 1
+#endif
+    if constexpr (MPC_CONE_FLAT && RF <= 2) {
+        int tot = 0;
+        for (int k = 0; k < L; ++k) tot += G * cone_nodes(m, k);
+        uint4 TG[RF], TP[RF], T1[RF];
+        int kk[RF], gg[RF], ii[RF];
+#pragma unroll
+        for (int r = 0; r < RF; ++r) {
+            int t = lane + 32 * r, k = 0, ng = 0;
+            kk[r] = -1; gg[r] = 0; ii[r] = 0;
+            if (t < tot) {
+                for (; k < L; ++k) { ng = cone_nodes(m, k); if (t < G * ng) break; t -= G * ng; }
+                kk[r] = k; gg[r] = G == 1 ? 0 : cone_div(t, ng); ii[r] = t - gg[r] * ng;
+            }
+            const u64 q = q0 + (u64)gg[r];
+            const int kq = kk[r] < 0 ? 0 : kk[r];
+            TG[r] = prg(K.k0, q, s, ltz_slot(kq + 1, ii[r], 0));
+            TP[r] = prg(K.k0, q, s, ltz_slot(kq + 1, ii[r], 1));
+            T1[r] = prg(K.k1, q, s, ltz_slot(kq + 1, ii[r], 0));
+        }
+        for (int k = 0; k < L; ++k) {
+#pragma unroll
+            for (int r = 0; r < RF; ++r) {
+                if (kk[r] != k) continue;
+                const int g = gg[r], i = ii[r], lo = i << (k + 1), hi = lo + (1 << k);
+                const u32 gl0 = sm.w[g][lo][0], gl1 = sm.w[g][lo][1], pl0 = sm.w[g][lo][2], pl1 = sm.w[g][lo][3];
+                const u32 gh0 = sm.w[g][hi][0], gh1 = sm.w[g][hi][1], ph0 = sm.w[g][hi][2], ph1 = sm.w[g][hi][3];
+                u32 ng0, ng1, np0, np1;
+                and_both(ph0, ph1, gl0, gl1, TG[r].x, TG[r].y, TG[r].z, T1[r].x, T1[r].y, ng0, ng1);
+                and_both(ph0, ph1, pl0, pl1, TP[r].x, TP[r].y, TP[r].z, T1[r].z, T1[r].w, np0, np1);
+                sm.w[g][lo][0] = gh0 ^ ng0; sm.w[g][lo][1] = gh1 ^ ng1;
+                if (i > 0) { sm.w[g][lo][2] = np0; sm.w[g][lo][3] = np1; }   // P off the left spine only
+            }
+            __syncwarp();
+        }
+    } else
     for (int k = 0; k < L; ++k) {
         const int ng = cone_nodes(m, k), items = G * ng;
         for (int base = 0; base < items; base += 32) {

@@ -1913,7 +1913,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
                     cudaFuncSetAttribute(k_ln_fused<BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
                     return occupancy(k_ln_fused<BothA>, 64 * 1024, MPC_ROW_TPB);
                 });
-                f.RB = rb_for((i64)c->sm_count * per_sm);
+                f.RB = rb_for((i64)c->sm_count * per_sm * MPC_LN_BLOCKS_PER_CTA);
                 const i64 nblk = (rows + f.RB - 1) / f.RB;
                 const int grid = (int)std::min<i64>(nblk, (i64)c->sm_count * per_sm);
                 rec_begin(c, "layernorm", (u64)rows);
@@ -1924,7 +1924,7 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
             } else {
                 const auto kk = kroles(k_ln_fused<PairA>, k_ln_fused<PairAS>);
                 set_smem_attr(kk, 64 * 1024);
-                f.RB = rb_for(pair_ctas(c, kk, dyn, 1ll << 40, MPC_ROW_TPB));
+                f.RB = rb_for(pair_ctas(c, kk, dyn, 1ll << 40, MPC_ROW_TPB) * MPC_LN_BLOCKS_PER_CTA);
                 const i64 nblk = (rows + f.RB - 1) / f.RB;
                 st = launch_pair_kernel_tpb(c, kk, pair_ctas(c, kk, dyn, nblk, MPC_ROW_TPB), dyn, MPC_ROW_TPB,
                                             "layernorm", f);
