@@ -139,7 +139,13 @@ class Job:
             if self.one_gpu:
                 dist.init_process_group("gloo")
             else:
+                # NCCL's own init lines (rank / nRanks per communicator) on stderr, so the driver's
+                # scaling run can check the rank count; the JSON line stays alone on stdout
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
                 dist.init_process_group("nccl", device_id=self.dev)
+                print(f"[bench] rank {self.rank}: NCCL process group of {self.ws} ranks on cuda:{self.local}",
+                      file=sys.stderr, flush=True)
             from paper_2511_19711_b200 import pair
             self.party, self.peer, self.pair_idx, self.npairs = pair.pair_layout(self.rank, self.ws)
             self.mode = m.binding.MODE_PAIR

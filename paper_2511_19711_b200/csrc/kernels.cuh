@@ -303,7 +303,7 @@ struct CmpBody {
     __device__ void operator()(P& pr, u64 u, u64 q, i64 i, int lane, bool valid) const {
         typename P::S xv = pr.zero();
         if (valid) xv = pr.ld(x, i);
-        typename P::S l = pr.template ltz<WIDE>(q, s, w, xv, lane);
+        typename P::S l = pr.template ltz_rb<WIDE>(q, s, w, xv, lane);
         if (relu) l = pr.bm(u, s + 1, xv, pr.notb(l));
         if (valid) pr.st(z, i, l);
     }
@@ -514,7 +514,11 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
                     d = pr.sub(ldc(rr, i), y);
                 }
                 const u64 q = (ubase >> 5) + (u64)g;
-                const S c = pr.notb(pr.template ltz_o<WIDE>(q, sl, w, d, lane));
+#ifndef MPC_MAXTREE_REBAL
+#define MPC_MAXTREE_REBAL 0      // A/B: the softmax / max tree with the rebalanced w = 33 LTZ
+#endif
+                const S c = pr.notb(MPC_MAXTREE_REBAL ? pr.template ltz_rb<WIDE>(q, sl, w, d, lane)
+                                                      : pr.template ltz_o<WIDE>(q, sl, w, d, lane));
                 const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
                 if (valid) {
                     pr.st(o, rr * lo + i, sel);
@@ -1053,7 +1057,7 @@ __global__ void __launch_bounds__(256, MPC_EW_MINB) k_max_small(const __grid_con
                         y = pr.ld(Xc, at + h);
                         d = pr.sub(pr.ld(Xc, at), y);
                     }
-                    const S c = pr.notb(pr.template ltz<WIDE>((ubase >> 5) + (u64)g, sl, a.w, d, lane));
+                    const S c = pr.notb(pr.template ltz_rb<WIDE>((ubase >> 5) + (u64)g, sl, a.w, d, lane));
                     const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
                     if (at >= 0) pr.st(X, at, sel);
                 }

@@ -84,6 +84,10 @@ struct BothP {
     }
     template <bool WIDE>
     __device__ __forceinline__ S ltz(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE>(*Kp, q, s, w, x, lane); }
+    // w = 33 with the levels' Philox rebalanced over idle lanes (proto_both.cuh ltz33_rebal): faster where
+    // the kernel has registers to spare (cmp / ReLU -9 %, short-row max), slower inside GELU's schedule
+    template <bool WIDE>
+    __device__ __forceinline__ S ltz_rb(u64 q, u32 s, int w, S x, int lane) { return mpc::ltz<WIDE, true>(*Kp, q, s, w, x, lane); }
 #ifndef MPC_BOTH_LTZ_O_INLINE
 #define MPC_BOTH_LTZ_O_INLINE 1
 #endif
@@ -718,6 +722,8 @@ struct PairP : StreamState<R> {
     // instruction fetch the top stall); single-site kernels (ReLU) stay inlined (8 % faster).
     template <bool WIDE>
     __device__ __noinline__ S ltz_o(u64 q, u32 s, int w, S x, int lane) { return ltz<WIDE>(q, s, w, x, lane); }
+    template <bool WIDE>
+    __device__ __forceinline__ S ltz_rb(u64 q, u32 s, int w, S x, int lane) { return ltz<WIDE>(q, s, w, x, lane); }
 #ifndef MPC_PAIR_BM_INLINE
 #define MPC_PAIR_BM_INLINE 1
 #endif

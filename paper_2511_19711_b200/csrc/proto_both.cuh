@@ -194,16 +194,91 @@ __device__ __forceinline__ Sh ltz_narrow(const Keys& K, u64 q, u32 s, int w, Sh 
     return {c + sg * r0A, sg * r1A};
 }
 
+// LTZ at w = 33 (m = 32 planes, L = 5 Kogge-Stone levels) with the levels' Philox rebalanced over
+// idle lanes.  At level k the lanes j < 2^k have no gate; instead of issuing blocks nobody uses they
+// generate the blocks of the LAST level's gate nodes (planes 16..31; item t = 2^k - 1 + lane, t < 15)
+// into a per-warp shared-memory stash, and lanes 1..3 generate item 15 (plane 31) in the daBit pass in
+// place of the redundant copies of the K1 daBit word.  The last level then issues no Philox at all:
+// 16 warp-blocks per LTZ instead of 19 (the algorithmic count is 15.1).  Same blocks, same gate
+// words, same output bits as ltz<false> (DESIGN.md 2.3 / 2.4); needs <= 8 warps per CTA.
+__device__ __forceinline__ Sh ltz33_rebal(const Keys& K, u64 q, u32 s, Sh x, int lane)
+{
+    __shared__ __align__(16) u32 stash_all[8][16][12];          // [warp][item][tg.xyz tp.xyz t1.xyzw]
+    u32 (*stash)[12] = stash_all[(threadIdx.x >> 5) & 7];
+    const PrgQ Q0 = prg_q(K.k0, q, s), Q1 = prg_q(K.k1, q, s);
+    // daBit pass: D0 on every lane; the K1 word D1 on lane 0 (broadcast); item 15 on lanes 1..3
+    const uint4 D0 = prg(Q0, 2u + (u32)lane);
+    const u32 sd = lane == 1 ? ltz_slot(5, 31, 0) : lane == 2 ? ltz_slot(5, 31, 1) : lane == 3 ? ltz_slot(5, 31, 0) : 1u;
+    const uint4 DX = prg((lane == 1 || lane == 2) ? K.k0 : K.k1, q, s, sd);       // (a key select: 2 registers)
+    const u32 d1x = __shfl_sync(FULL, DX.x, 0);
+    if (lane == 1) { stash[15][0] = DX.x; stash[15][1] = DX.y; stash[15][2] = DX.z; }
+    if (lane == 2) { stash[15][3] = DX.x; stash[15][4] = DX.y; stash[15][5] = DX.z; }
+    if (lane == 3) { stash[15][6] = DX.x; stash[15][7] = DX.y; stash[15][8] = DX.z; stash[15][9] = DX.w; }
+    // A2B and the g-layer (every plane is a leaf at m = 32)
+    u32 P0 = transpose32((u32)x.s0, lane), P1 = transpose32((u32)x.s1, lane), G0, G1;
+    {
+        const uint4 t0 = prg(Q0, ltz_slot(0, lane, 0)), t1 = prg(Q1, ltz_slot(0, lane, 0));
+        and_both(P0, 0u, 0u, P1, t0.x, t0.y, t0.z, t1.x, t1.y, G0, G1);
+    }
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int d = 1 << k;
+        const int src = (lane - d) & 31;
+        const u32 g0 = __shfl_sync(FULL, G0, src), g1 = __shfl_sync(FULL, G1, src);
+        const u32 p0 = __shfl_sync(FULL, P0, src), p1 = __shfl_sync(FULL, P1, src);
+        const bool act = lane >= d;
+        uint4 tg, tp, t1;
+        if (k < 4) {
+            const int t = d - 1 + lane;                            // the last level's item of an idle lane
+            const int jj = act ? lane : 16 + t, kk = act ? k : 4;
+            tg = prg(Q0, ltz_slot(kk + 1, jj, 0));
+            tp = prg(Q0, ltz_slot(kk + 1, jj, 1));
+            t1 = prg(Q1, ltz_slot(kk + 1, jj, 0));
+            if (!act) {
+                u32* w = stash[t];
+                w[0] = tg.x; w[1] = tg.y; w[2] = tg.z; w[3] = tp.x; w[4] = tp.y; w[5] = tp.z;
+                w[6] = t1.x; w[7] = t1.y; w[8] = t1.z; w[9] = t1.w;
+            }
+            if (k == 3) __syncwarp();
+        } else {                                                     // every item is in the stash
+            const u32* w = stash[lane & 15];
+            tg = make_uint4(w[0], w[1], w[2], 0u); tp = make_uint4(w[3], w[4], w[5], 0u);
+            t1 = make_uint4(w[6], w[7], w[8], w[9]);
+        }
+        u32 ng0, ng1, np0, np1;
+        and_both(P0, P1, g0, g1, tg.x, tg.y, tg.z, t1.x, t1.y, ng0, ng1);
+        and_both(P0, P1, p0, p1, tp.x, tp.y, tp.z, t1.z, t1.w, np0, np1);
+        if (act) { G0 ^= ng0; G1 ^= ng1; P0 = np0; P1 = np1; }
+    }
+    __syncwarp();                                                    // the stash is free for the next call
+    // sign b = p_32 ^ G_31, then the daBit B2A (as ltz<false>)
+    const u32 gm0 = __shfl_sync(FULL, G0, 31), gm1 = __shfl_sync(FULL, G1, 31);
+    const u32 b0 = (u32)((x.s0 >> 32) & 1ull) ^ ((gm0 >> lane) & 1u);
+    const u32 b1 = (u32)((x.s1 >> 32) & 1ull) ^ ((gm1 >> lane) & 1u);
+    const u64 r0A = w64(D0.x, D0.y);
+    const u32 r0B = D0.z & 1u;
+    const u32 r1B = (d1x >> lane) & 1u;
+    const u64 r1A = (u64)(r0B ^ r1B) - r0A;
+    const u64 c = (u64)((b0 ^ r0B) ^ (b1 ^ r1B));
+    const u64 sg = 1ull - 2ull * c;
+    return {c + sg * r0A, sg * r1A};
+}
+
 // LTZ_w on the warp's 32-element group q (lane l <-> element 32q+l); DESIGN.md 2.4.
 // All 32 lanes must call it (tail lanes with any value).  Returns the scale-1
 // arithmetic sharing of bit (w-1) of rec(x).  WIDE: w > 33 (two planes per lane).
-template <bool WIDE>
+template <bool WIDE, bool RB = false>
 __device__ __forceinline__ Sh ltz(const Keys& K, u64 q, u32 s, int w, Sh x, int lane)
 {
 #ifndef MPC_LTZ_NARROW
 #define MPC_LTZ_NARROW 0   // measured: the branchy form is 3-7% faster (register pressure)
 #endif
     if constexpr (!WIDE && MPC_LTZ_NARROW) return ltz_narrow(K, q, s, w, x, lane);
+#ifndef MPC_LTZ_REBAL
+#define MPC_LTZ_REBAL 1
+#endif
+    if constexpr (!WIDE && RB && MPC_LTZ_REBAL)
+        if (w == 33 && blockDim.x <= 256) return ltz33_rebal(K, q, s, x, lane);
     const int m = w - 1;
     const PrgQ Q0 = prg_q(K.k0, q, s), Q1 = prg_q(K.k1, q, s);
 #ifndef MPC_LTZ_HOIST

@@ -27,3 +27,6 @@ def test_bench_two_ranks_one_gpu():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "pairs1"
     assert "PAIR" in d["config"]["mode"] and d["roofline"]["nvlink"]["payload_bytes_per_party_per_step"] > 0
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    # party 1 is fed by the trusted dealer's offline stream, its context has no K_0
+    assert d["roofline"]["dealer"]["party1_stream_bytes_per_step"] > 0
+    assert d["parity_ok"] is True
