@@ -429,7 +429,7 @@ struct HdrBody {
 // the last level writes mx[rr].  Steps s + 2*lv (LTZ), s + 2*lv + 1 (mux BM).
 // A holds levels 0, 2, 4.. (stride HA = ceil(cols/2)), B levels 1, 3, .. (stride HB = ceil(HA/2)).
 // cone: the level's LTZs use the carry-cone circuit, CG groups per warp (ltz_cone.cuh).
-template <bool WIDE, bool CONE, class P, bool CAUSAL = false>
+template <bool WIDE, bool CONE, class P, bool CAUSAL = false, bool RBL = false>
 __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i64 cols, int R, u64 g0,
                                          SO A, SO B, i64 HA, i64 HB, SO mx, ConeSmem<CG, WIDE ? 64 : 32>* cone,
                                          u64 cL = 0)
@@ -517,8 +517,8 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
 #ifndef MPC_MAXTREE_REBAL
 #define MPC_MAXTREE_REBAL 0      // A/B: the softmax / max tree with the rebalanced w = 33 LTZ
 #endif
-                const S c = pr.notb(MPC_MAXTREE_REBAL ? pr.template ltz_rb<WIDE>(q, sl, w, d, lane)
-                                                      : pr.template ltz_o<WIDE>(q, sl, w, d, lane));
+                const S c = pr.notb((MPC_MAXTREE_REBAL || RBL) ? pr.template ltz_rb<WIDE>(q, sl, w, d, lane)
+                                                               : pr.template ltz_o<WIDE>(q, sl, w, d, lane));
                 const S sel = pr.add(y, pr.bm(ubase + (u64)v, sl + 1, d, c));
                 if (valid) {
                     pr.st(o, rr * lo + i, sel);
@@ -895,7 +895,8 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         const int R = (int)min((i64)32, a.rows - r0);
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
         prefetch_rows(a.x, r0 + (i64)ncta * 32, a.rows, C);
-        tile_max<WIDE, CONE>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, HA, HB, MX, cone_sm);
+        // standalone max (and softmax's split max pass): the rebalanced w = 33 LTZ (k_max has the registers)
+        tile_max<WIDE, CONE, decltype(pr), false, true>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, HA, HB, MX, cone_sm);
         const SP MXc{{MX.p[0], MX.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 : nullptr, a.z.p[1] ? a.z.p[1] + r0 : nullptr}};
         for (int rr = threadIdx.x; rr < R; rr += blockDim.x) pr.st(zt, rr, pr.ld(MXc, rr));
@@ -1530,6 +1531,140 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_fused(const __g
 #pragma unroll
                 for (int v = 0; v < V; ++v)
                     if (ok[v]) pr.st_pair(zb, e0[v], true, true, pr.shr_(za[v], FRAC), pr.shr_(zz[v], FRAC));
+            }
+        }
+        __syncthreads();
+    }
+    pa.done(pr);
+}
+
+
+// ------------------------------------------------- softmax after the max tree (BOTH, split form) ----
+// cfg2-shaped softmax as two launches: the row max tree (k_max, 32-row tiles, the rebalanced w = 33
+// LTZ) and this kernel -- e = EXP(x - m), S = rowsum(e), r = RECIP(S), out = MT(e, r) -- on row
+// blocks of RB <= 64 rows sized so that every block is resident at once (no tail wave), the warps
+// splitting the block's element pairs evenly along warp-uniform row segments (as k_ln_fused), E in
+// an L2-resident per-block scratch, the reciprocal chains' triples pre-generated (two 32-row
+// tables, warps 0 and 1).  Same steps, units and output bits as k_softmax (dense, no clamp, the
+// expanded product).
+struct SmRestArgs {
+    u32 s_exp, s_rec, s_mul; ExpK ek; NrK rk; SP x; SP mx; SO z; i64 rows, cols; u64 row_off;
+    int RB;                 // rows per block (even, <= 64)
+    u64* escr;              // per-CTA E scratch: 2 x RB x cols u64
+    int tab_u64;            // u64 words of one 32-row NR table
+};
+constexpr int SMR_SEG = 66;                    // row segments per warp (<= RB + 2)
+__host__ __device__ inline int smr_smem_u64(int tab_u64) { return 6 * 64 + 8 * SMR_SEG * 2 + 2 * tab_u64; }
+template <class PA>
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_softmax_rest(const __grid_constant__ PA pa, SmRestArgs a)
+{
+    extern __shared__ __align__(16) u64 rsm[];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using P = decltype(pr);
+    using S = typename P::S;
+    static_assert(!P::kPair, "BOTH only (PAIR keeps the fused k_softmax)");
+    constexpr int V = P::kV;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const i64 C = a.cols, hc = C / 2;
+    u64* MXw = rsm; u64* SSw = rsm + 128; u64* RRw = rsm + 256;
+    u64* wpart = rsm + 384;                                        // [NW][SMR_SEG][2]
+    u64* tab = rsm + 384 + 8 * SMR_SEG * 2;                        // two 32-row NR tables
+    const SO MX{{MXw, MXw + 64}}, SS{{SSw, SSw + 64}}, RR{{RRw, RRw + 64}};
+    const SP MXc{{MXw, MXw + 64}}, SSc{{SSw, SSw + 64}}, RRc{{RRw, RRw + 64}};
+    u64* Ew = a.escr + (i64)blockIdx.x * 2 * a.RB * C;
+    const SO E{{Ew, Ew + (i64)a.RB * C}};
+    const SP Ec{{Ew, Ew + (i64)a.RB * C}};
+    const i64 nblk = (a.rows + a.RB - 1) / a.RB;
+    for (i64 blk = cta; blk < nblk; blk += ncta) {
+        const i64 r0 = blk * a.RB;
+        const int R = (int)min((i64)a.RB, a.rows - r0);
+        const u64 g0 = a.row_off + (u64)r0;                         // even
+        const i64 np = (i64)R * hc;
+        const i64 wbeg = np * warp / NW, wend = np * (warp + 1) / NW;
+        const int rw0 = (int)(wbeg / hc);
+        const int nseg = wend > wbeg ? (int)((wend - 1) / hc) - rw0 + 1 : 0;
+        const u64 ub = g0 * (u64)C;
+        const SP xb{{a.x.p[0] + r0 * C, a.x.p[1] + r0 * C}};
+        const SO zb{{a.z.p[0] + r0 * C, a.z.p[1] + r0 * C}};
+        for (int r = threadIdx.x; r < R; r += blockDim.x) pr.st(MX, r, pr.ld(a.mx, r0 + r));
+        __syncthreads();
+        // 1. e = EXP(x - m) into E, and the per-row sums of e
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int r = rw0 + sg;
+            const i64 sb = max(wbeg, (i64)r * hc), se = min(wend, (i64)(r + 1) * hc);
+            const S m = pr.ld(MXc, r);
+            S acc = pr.zero();
+            for (i64 base = sb + lane; base - lane < se; base += 32 * V) {     // warp-uniform trip count
+                u64 uv[V];
+                S da[V], db[V];
+                bool ok[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 P2 = base + 32 * v;
+                    ok[v] = P2 < se;
+                    uv[v] = ub + 2 * (u64)P2;
+                    da[v] = db[v] = pr.zero();
+                    if (ok[v]) { pr.ld_pair(xb, 2 * P2, true, true, da[v], db[v]); da[v] = pr.sub(da[v], m); db[v] = pr.sub(db[v], m); }
+                }
+                exp_pairv<V>(pr, uv, a.s_exp, a.ek, da, db);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (ok[v]) {
+                        const i64 P2 = base + 32 * v;
+                        pr.st_pair(E, 2 * P2, true, true, da[v], db[v]);
+                        acc = pr.add(acc, pr.add(da[v], db[v]));
+                    }
+            }
+            acc = pr.sumw(acc);
+            if (lane == 0) { wpart[(warp * SMR_SEG + sg) * 2] = acc.s0; wpart[(warp * SMR_SEG + sg) * 2 + 1] = acc.s1; }
+        }
+        __syncthreads();
+        if (threadIdx.x < R) {                                       // S[r] = the warps' segments of row r
+            S t = pr.zero();
+            for (int w = 0; w < NW; ++w) {
+                const i64 b0 = np * w / NW, e0 = np * (w + 1) / NW;
+                if (e0 <= b0) continue;
+                const int f = (int)(b0 / hc), l = (int)((e0 - 1) / hc);
+                if ((int)threadIdx.x >= f && (int)threadIdx.x <= l)
+                    t = pr.add(t, S{wpart[(w * SMR_SEG + (threadIdx.x - f)) * 2], wpart[(w * SMR_SEG + (threadIdx.x - f)) * 2 + 1]});
+            }
+            pr.st(SS, threadIdx.x, t);
+        }
+        nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0, tab);
+        if (R > 32) nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0 + 32, tab + a.tab_u64);
+        __syncthreads();
+        // 2. r = RECIP(S): warp w < 2 runs rows 32 w + lane, units g0 + 32 w + lane
+        if (warp < 2 && 32 * warp < R) {
+            const int row = 32 * warp + lane;
+            BothTabP tp;
+            tp.Kp = pr.Kp; tp.T = tab + warp * a.tab_u64; tp.sb = a.s_rec;
+            const S xv = row < R ? pr.ld(SSc, row) : pr.zero();
+            const S rv = recip_group<false>(tp, g0 + (u64)row, (g0 + 32 * warp) >> 5, a.s_rec, a.rk, xv, lane);
+            if (row < R) pr.st(RR, row, rv);
+        }
+        __syncthreads();
+        // 3. out = MT(e, r)
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int r = rw0 + sg;
+            const i64 sb = max(wbeg, (i64)r * hc), se = min(wend, (i64)(r + 1) * hc);
+            const S rv = pr.ld(RRc, r);
+            for (i64 base = sb + lane; base - lane < se; base += 32 * V) {
+                u64 uv[V];
+                S ea[V], eb[V], rr[V], za[V], zz[V];
+                bool ok[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 P2 = base + 32 * v;
+                    ok[v] = P2 < se;
+                    uv[v] = ub + 2 * (u64)P2;
+                    ea[v] = eb[v] = pr.zero(); rr[v] = rv;
+                    if (ok[v]) pr.ld_pair(Ec, 2 * P2, true, true, ea[v], eb[v]);
+                }
+                pr.template bm2v<V>(uv, a.s_mul, ea, rr, eb, rr, za, zz);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (ok[v]) pr.st_pair(zb, 2 * (base + 32 * v), true, true, pr.shr_(za[v], FRAC), pr.shr_(zz[v], FRAC));
             }
         }
         __syncthreads();

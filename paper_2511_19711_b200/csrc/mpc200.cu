@@ -1838,6 +1838,40 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         a.nrtab = (MPC_SOFTMAX_NRTAB && !is_pair(c) && a.esmem && !p->recip.exp.clamp && !a.cone &&
                    nsteps <= MPC_NR_TAB_MAX_STEPS) ? 1 : 0;
         const i64 tab = a.nrtab ? (i64)nsteps * NR_TAB_F * 32 : 0;
+        // BOTH split form (kernels.cuh k_softmax_rest): the max tree as its own launch (k_max, 32-row
+        // tiles, the rebalanced w = 33 LTZ), then exp / row sums / reciprocal / product on row blocks
+        // that are all resident at once -- no tail wave of lone tiles
+#ifndef MPC_SOFTMAX_SPLIT
+#define MPC_SOFTMAX_SPLIT 0     // A/B: measured 2.6 % slower on cfg2 (0.268 vs 0.261 ms unflushed, r02)
+#endif
+        if (MPC_SOFTMAX_SPLIT && !is_pair(c) && !a.causal && !a.bcast && !p->exp.clamp && !p->recip.exp.clamp &&
+            !a.cone && !wide && !(cols & 1) && (size_t)max_work_u64(cols) * 8 <= SMEM_LIMIT &&
+            nsteps <= MPC_NR_TAB_MAX_STEPS) {   // (k_max's tiles in shared memory: no scratch of its own)
+            static DevCache occ;
+            const int tabw = nsteps * NR_TAB_F * 32;
+            const size_t dyn = sizeof(u64) * (size_t)smr_smem_u64(tabw);
+            const int per_sm = dev_cached(occ, c->cfg.device, [&] {
+                cudaFuncSetAttribute(k_softmax_rest<BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+                return occupancy(k_softmax_rest<BothA>, dyn, MPC_ROW_TPB);
+            });
+            const i64 slots = (i64)c->sm_count * per_sm;
+            i64 rb = (rows + slots - 1) / slots;
+            rb = std::max<i64>(2, std::min<i64>(64, (rb + 1) / 2 * 2));
+            const i64 nblk = (rows + rb - 1) / rb;
+            const int grid = (int)std::min<i64>(nblk, slots);
+            // scratch: row maxima (2 x rows) then the per-CTA E tiles (k_max keeps its work tiles in smem)
+            u64* sc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * rows + (i64)grid * 2 * rb * cols));
+            if (!sc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
+            MaxArgs ma{a.s_max, a.w, a.x, SO{{sc, sc + rows}}, rows, cols, (u64)row_off, nullptr, 0, 0, nullptr, 0};
+            if ((st = launch_max(c, ma, rows, cols, a.w, "softmax"))) return st;
+            SmRestArgs ra{a.s_exp, a.s_rec, a.s_mul, a.ek, a.rk, a.x, SP{{sc, sc + rows}}, a.z, rows, cols, (u64)row_off,
+                          (int)rb, sc + 2 * rows, tabw};
+            rec_begin(c, "softmax", (u64)rows);
+            k_softmax_rest<BothA><<<grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, ra);
+            rec_end(c);
+            c->st.launches++;
+            return cuda_check(c, "softmax");
+        }
         const i64 wk = softmax_work_u64(cols, a.esmem != 0, tab), ek = a.esmem ? 0 : 64 * cols;
         const size_t lim = a.esmem ? 100 * 1024 + (size_t)tab * 8 : SMEM_LIMIT;
         if (a.causal)   // causal instantiations: the dense kernels carry no mask code
