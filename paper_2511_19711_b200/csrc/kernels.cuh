@@ -424,6 +424,25 @@ struct HdrBody {
 
 // ------------------------------------------------------------------ row tiles ----
 // One CTA owns a tile of 32 consecutive rows (32-aligned global row index); persistent loop.
+// Tile plan: tiles of 32 rows, round-robin over the ncta CTAs.  When the last round would hold
+// P = ntiles mod ncta tiles with 2P <= ncta (cfg2: 384 tiles on 296 CTAs leave 88 lone tiles on 88
+// SMs while 60 idle), those P tiles run as 2P half tiles of 16 rows on twice the CTAs: the tail wave
+// is one half-tile latency instead of one tile latency.  A half tile starts at a row = 16 mod 32, so
+// the levels whose LTZ groups span more than 16 rows see a group offset (tile_max handles any
+// alignment: the group's lanes outside the tile are evaluated and dropped).
+struct TilePlan { i64 nfull, ntot; };
+__device__ __forceinline__ TilePlan tile_plan(i64 rows, int ncta, int half)
+{
+    const i64 nt = (rows + 31) / 32, P = nt % ncta;
+    if (!half || nt <= ncta || P == 0 || 2 * P > ncta) return TilePlan{nt, nt};
+    return TilePlan{nt - P, nt + P};
+}
+// rows [r0, r0 + R) of plan tile t (R <= 0: past the end)
+__device__ __forceinline__ void tile_rows(const TilePlan& tp, i64 t, i64 rows, i64& r0, int& R)
+{
+    if (t < tp.nfull) { r0 = t * 32; R = (int)min((i64)32, rows - r0); }
+    else { r0 = tp.nfull * 32 + (t - tp.nfull) * 16; R = (int)min((i64)16, rows - r0); }
+}
 
 // MAX_row tree (R22): levels ping-pong in A/B (stride H = ceil(cols/2));
 // the last level writes mx[rr].  Steps s + 2*lv (LTZ), s + 2*lv + 1 (mux BM).
@@ -468,30 +487,33 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
         else if (lv & 1) { o = B; lo = HB; }
         else { o = A; lo = HA; }
         const u32 sl = s + 2u * (u32)lv;
-        const u64 ubase = g0 * (u64)h;                 // multiple of 32 (g0 is)
+        const u64 ubase = g0 * (u64)h;                 // multiple of 32 for a full tile (g0 is); a half
+        const int ua = (int)(ubase & 31);              // tile may start inside a group: ua lanes before it
+        const u64 qb = ubase >> 5;
+        const i64 nu = (i64)R * h;                     // the tile's units at this level
         const FastDiv dh = make_fastdiv((u32)h);
-        const bool wl = warp_local(h);
+        const bool wl = warp_local(h) && R == 32 && ua == 0;
         const i64 gpw = (i64)rw * h / 32;              // groups per warp when warp-local
-        const i64 gend = wl ? (warp + 1) * gpw : h;    // 32*h units = h groups per tile
+        const i64 gend = wl ? (warp + 1) * gpw : (ua + nu + 31) / 32;
         if constexpr (CONE) {
             constexpr int GB = CG;     // (one group per call in BOTH measured 4 % slower on softmax_cone)
             for (i64 gb = wl ? warp * gpw : (i64)warp * GB; gb < gend; gb += wl ? GB : (i64)NW * GB) {
                 S d[GB], l[GB];
 #pragma unroll
                 for (int g = 0; g < GB; ++g) {
-                    const i64 v = (gb + g) * 32 + lane;
+                    const i64 v = (gb + g) * 32 + lane - ua;
                     d[g] = pr.zero();
-                    if (gb + g < gend && v < (i64)R * h) {
+                    if (gb + g < gend && v >= 0 && v < nu) {
                         const i64 rr = fdiv((u32)v, dh), i = v - rr * h;
                         d[g] = pr.sub(ldc(rr, i), ldc(rr, i + h));
                     }
                 }
-                pr.template ltz_cone<GB, WIDE ? 64 : 32>((ubase >> 5) + (u64)gb, sl, w, d, l, lane,
+                pr.template ltz_cone<GB, WIDE ? 64 : 32>(qb + (u64)gb, sl, w, d, l, lane,
                                                          *reinterpret_cast<ConeSmem<GB, WIDE ? 64 : 32>*>(&cone[warp]));
 #pragma unroll
                 for (int g = 0; g < GB; ++g) {
-                    const i64 v = (gb + g) * 32 + lane;
-                    const bool valid = gb + g < gend && v < (i64)R * h;
+                    const i64 v = (gb + g) * 32 + lane - ua;
+                    const bool valid = gb + g < gend && v >= 0 && v < nu;
                     i64 rr = 0, i = 0;
                     S y = pr.zero();
                     if (valid) { rr = fdiv((u32)v, dh); i = v - rr * h; y = ldc(rr, i + h); }
@@ -504,8 +526,8 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
             }
         } else {
             for (i64 g = wl ? warp * gpw : warp; g < gend; g += wl ? 1 : NW) {
-                const i64 v = g * 32 + lane;
-                const bool valid = v < (i64)R * h;
+                const i64 v = g * 32 + lane - ua;
+                const bool valid = v >= 0 && v < nu;
                 i64 rr = 0, i = 0;
                 S d = pr.zero(), y = pr.zero();
                 if (valid) {
@@ -513,7 +535,7 @@ __device__ __forceinline__ void tile_max(P& pr, u32 s, int w, SP in, i64 ldi, i6
                     y = ldc(rr, i + h);
                     d = pr.sub(ldc(rr, i), y);
                 }
-                const u64 q = (ubase >> 5) + (u64)g;
+                const u64 q = qb + (u64)g;
 #ifndef MPC_MAXTREE_REBAL
 #define MPC_MAXTREE_REBAL 0      // A/B: the softmax / max tree with the rebalanced w = 33 LTZ
 #endif
@@ -600,30 +622,35 @@ struct BothTabP : BothP {
 
 // per-row Newton-Raphson over the tile's rows: warp 0, lane <-> row (LTZ group = the tile)
 // tab (BOTH mode only): the chain's triples, already generated by nr_pregen<KIND> for (s, g0)
+// R > 32 (the balanced softmax plan, BOTH): warp w < ceil(R / 32) runs rows 32 w + lane (units g0 + 32 w
+// + lane) from the w-th table (tab + w * tab2)
 template <int KIND, bool WIDE, class P>
-__device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g0, SP x, SO y, const u64* tab = nullptr)
+__device__ __forceinline__ void tile_nr(P& pr, u32 s, const NrK& p, int R, u64 g0, SP x, SO y, const u64* tab = nullptr,
+                                        i64 tab2 = 0)
 {
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        const bool valid = lane < R;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0 || 32 * warp < R) {
+        const int lane = threadIdx.x & 31, row = (int)threadIdx.x;
+        const u64 gw = g0 + 32u * (u64)warp;
+        const bool valid = row < R;
         typename P::S xv = pr.zero();
-        if (valid) xv = pr.ld(x, lane);
+        if (valid) xv = pr.ld(x, row);
         typename P::S r;
         bool done = false;
         if constexpr (!P::kPair) {
             if (tab) {
                 BothTabP tp;
-                tp.Kp = pr.Kp; tp.T = tab; tp.sb = s;
-                if (KIND == 0) r = recip_group<WIDE>(tp, g0 + lane, g0 >> 5, s, p, xv, lane);
-                else r = rsqrt_group<WIDE>(tp, g0 + lane, g0 >> 5, s, p, xv, lane);
+                tp.Kp = pr.Kp; tp.T = tab + warp * tab2; tp.sb = s;
+                if (KIND == 0) r = recip_group<WIDE>(tp, gw + lane, gw >> 5, s, p, xv, lane);
+                else r = rsqrt_group<WIDE>(tp, gw + lane, gw >> 5, s, p, xv, lane);
                 done = true;
             }
         }
         if (!done) {
-            if (KIND == 0) r = recip_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
-            else r = rsqrt_group<WIDE>(pr, g0 + lane, g0 >> 5, s, p, xv, lane);
+            if (KIND == 0) r = recip_group<WIDE>(pr, gw + lane, gw >> 5, s, p, xv, lane);
+            else r = rsqrt_group<WIDE>(pr, gw + lane, gw >> 5, s, p, xv, lane);
         }
-        if (valid) pr.st(y, lane, r);
+        if (valid) pr.st(y, row, r);
     }
     __syncthreads();
 }
@@ -690,7 +717,27 @@ struct SoftmaxArgs {
     int causal;             // causal attention rows
     u64 causal_L;           // public constant of the masked max-tree inputs, -2^(w-2)
     int nrtab;              // BOTH: the reciprocal chain's triples pre-generated into smem (nr_pregen)
+    int half;               // tail tiles as 16-row half tiles (tile_plan)
+    int bal;                // BOTH balanced plan: ONE row range of <= tr rows per CTA (softmax_bal_*)
+    int tr;                 // rows per CTA capacity of the balanced plan
+    i64 tab_u64;            // balanced plan: u64 words of one 32-row NR table
 };
+
+// Balanced plan (BOTH, no clamp / broadcast triple / cone): CTA c of ncta owns rows
+// [2 floor(c hr / ncta), 2 floor((c+1) hr / ncta)), hr = ceil(rows / 2) -- every CTA resident at once,
+// each SM ~rows / #SMs rows (cfg2: 41-42 rows per CTA instead of 384 32-row tiles on 296 CTAs, whose
+// last round left 88 SMs with a third tile).  Work area: the max-tree levels A0 A1 B0 B1 (2 tr HA +
+// 2 tr HB), aliased after the tree by the reciprocal chains' triple tables (two 32-row tables); then
+// X: MX0 MX1 S0 S1 R0 R1 (6 tr).  E (2 x tr x cols) lives in the per-CTA global escratch (L2).
+__host__ __device__ inline i64 softmax_bal_x_off(i64 cols, i64 tr, i64 tab_u64)
+{
+    const i64 HA = (cols + 1) / 2, HB = (HA + 1) / 2, lv = 2 * tr * (HA + HB);
+    return lv > 2 * tab_u64 ? lv : 2 * tab_u64;
+}
+__host__ __device__ inline i64 softmax_bal_work_u64(i64 cols, i64 tr, i64 tab_u64)
+{
+    return softmax_bal_x_off(cols, tr, tab_u64) + 6 * tr;
+}
 
 // work tile (u64 words), HA = ceil(cols/2), HB = ceil(HA/2): A0 A1 (2 x 32HA), B0 B1 (2 x 32HB),
 // then at softmax_x_off: MX0 MX1 S0 S1 R0 R1 (6 x 32), broadcast-triple rows b0 b1 f (3 x 32).
@@ -723,18 +770,28 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     const int wslot = blockIdx.x;
     u64* W = a.use_smem ? smem : a.gscratch + (i64)wslot * a.work_u64;
     const i64 C = a.cols, HA = (C + 1) / 2, HB = (HA + 1) / 2;
-    SO A{{W, W + 32 * HA}}, B{{W + 64 * HA, W + 64 * HA + 32 * HB}};
-    u64* Ew = a.esmem ? W : a.escratch + (i64)wslot * 64 * C;
-    SO E{{Ew, Ew + 32 * C}};
-    u64* X = W + softmax_x_off(C, a.esmem != 0);
-    SO MX{{X, X + 32}}, SS{{X + 64, X + 96}}, RR{{X + 128, X + 160}};
-    u64* const nrt = a.nrtab ? X + 9 * 32 : nullptr;
+    const i64 TR = a.bal ? a.tr : 32;                             // rows per tile capacity
+    SO A{{W, W + TR * HA}}, B{{W + 2 * TR * HA, W + 2 * TR * HA + TR * HB}};
+    u64* Ew = a.esmem ? W : a.escratch + (i64)wslot * 2 * TR * C;
+    SO E{{Ew, Ew + TR * C}};
+    u64* X = W + (a.bal ? softmax_bal_x_off(C, TR, a.tab_u64) : softmax_x_off(C, a.esmem != 0));
+    SO MX{{X, X + TR}}, SS{{X + 2 * TR, X + 3 * TR}}, RR{{X + 4 * TR, X + 5 * TR}};
+    u64* const nrt = a.nrtab ? (a.bal ? W : X + 9 * 32) : nullptr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-    const i64 ntiles = (a.rows + 31) / 32;
+    const TilePlan tp = tile_plan(a.rows, ncta, a.half);
     const FastDiv dC = make_fastdiv((u32)C);
-    for (i64 tile = cta; tile < ntiles; tile += ncta) {
-        const i64 r0 = tile * 32;
-        const int R = (int)min((i64)32, a.rows - r0);
+    const i64 ntl = a.bal ? (i64)ncta : tp.ntot;
+    for (i64 tile = cta; tile < ntl; tile += ncta) {
+        i64 r0; int R;
+        if (a.bal) {
+            const i64 hr = (a.rows + 1) / 2;
+            r0 = min(a.rows, 2 * (tile * hr / ncta));
+            R = (int)(min(a.rows, 2 * ((tile + 1) * hr / ncta)) - r0);
+            if (R <= 0) continue;
+        } else {
+            tile_rows(tp, tile, a.rows, r0, R);
+            if (R <= 0) break;
+        }
         const u64 g0 = a.row_off + (u64)r0;                       // global row of the tile
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
         // (no next-tile prefetch here: measured neutral to 0.6 % slower for softmax, 2 % faster for k_max)
@@ -747,7 +804,10 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         // BOTH: every warp generates the reciprocal chain's triples now (tile_nr's warp-0 chain then
         // only opens and multiplies); the exp phase's closing barrier orders it before the chain
         if constexpr (!decltype(pr)::kPair)
-            if (nrt) nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0, nrt);
+            if (nrt) {
+                nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0, nrt);
+                if (R > 32) nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0 + 32, nrt + a.tab_u64);
+            }
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;
@@ -828,7 +888,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         }
         __syncthreads();
         // 5. r = RECIP(S), row units
-        if (!(MPC_SOFTMAX_SKIP & 4)) tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR, nrt);
+        if (!(MPC_SOFTMAX_SKIP & 4)) tile_nr<0, WIDE>(pr, a.s_rec, a.rk, R, g0, SP{{SS.p[0], SS.p[1]}}, RR, nrt, a.tab_u64);
         // 6. out = MT(e, r), element units
         const SP Rc{{RR.p[0], RR.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
@@ -870,6 +930,7 @@ struct MaxArgs {
     u32 s; int w; SP x; SO z; i64 rows, cols; u64 row_off;
     u64* gscratch; i64 work_u64; int use_smem;
     u64* escratch; int cone;
+    int half;               // tail tiles as 16-row half tiles (tile_plan)
 };
 __host__ __device__ inline i64 max_work_u64(i64 cols)
 {
@@ -889,10 +950,11 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     const i64 C = a.cols, HA = (C + 1) / 2, HB = (HA + 1) / 2;
     SO A{{W, W + 32 * HA}}, B{{W + 64 * HA, W + 64 * HA + 32 * HB}};
     SO MX{{W + 64 * HA + 64 * HB, W + 64 * HA + 64 * HB + 32}};
-    const i64 ntiles = (a.rows + 31) / 32;
-    for (i64 tile = cta; tile < ntiles; tile += ncta) {
-        const i64 r0 = tile * 32;
-        const int R = (int)min((i64)32, a.rows - r0);
+    const TilePlan tp = tile_plan(a.rows, ncta, a.half);
+    for (i64 tile = cta; tile < tp.ntot; tile += ncta) {
+        i64 r0; int R;
+        tile_rows(tp, tile, a.rows, r0, R);
+        if (R <= 0) break;
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
         prefetch_rows(a.x, r0 + (i64)ncta * 32, a.rows, C);
         // standalone max (and softmax's split max pass): the rebalanced w = 33 LTZ (k_max has the registers)
@@ -1538,6 +1600,173 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_fused(const __g
     pa.done(pr);
 }
 
+
+// ------------------------------------------------------------- warp-per-row LayerNorm (BOTH) ----
+// LAYERNORM with one WARP per row and no CTA barrier: the row's element pairs are the
+// lanes' (pair p = lane + 32 k, 16-byte loads of both shares), the row sums are warp reductions, and
+// the row's RSQRT chain (row unit g) runs on every lane from a per-warp table of its triples that
+// lanes 0..ns-1 generate one step each while the row's first pass is in flight (3 Philox blocks per
+// lane instead of ns x 2.5 serial blocks on the chain).  x is read from HBM once per pass A (the next
+// row is prefetched to L2) and from L2 in passes B and D.  Same steps, units, PRG words and output
+// bits as k_ln_fused (units: global rows for the rsqrt, global elements for the two Beaver passes);
+// BOTH only, no clamp in the rsqrt's exp, no broadcast triple, ns <= 32.
+struct LnRArgs {
+    u32 s_sq, s_rs, s_mul; NrK rk; SP x; SO z; i64 rows, cols; u64 row_off;
+    int mean_mode; u64 e_invd, e_eps;
+};
+// BothP with the chain's bm / sq read from a per-warp table [step][5] (a0 b0 c0 a b; square-pair
+// steps: a0 . c0 a), all lanes reading the same words (shared-memory broadcast)
+struct BothRowTabP : BothP {
+    const u64* T; u32 sb;
+    __device__ __forceinline__ S bm(u64, u32 s, S x, S y) const {
+        const u64* R = T + (i64)(s - sb) * NR_TAB_F;
+        const u64 a0 = R[0], b0 = R[1], c0 = R[2], a = R[3], b = R[4];
+        const u64 X = x.s0 + x.s1, Y = y.s0 + y.s1;
+        const u64 e = X - a, f = Y - b;               // open(x - a), open(y - b)
+        const u64 z0 = c0 + e * (b0 + f) + f * a0;    // = mpc::bm_with_c0
+        return {z0, X * Y - z0};
+    }
+    __device__ __forceinline__ S sq(u64, u32 s, S y) const {
+        const u64* R = T + (i64)(s - sb) * NR_TAB_F;
+        const u64 a0 = R[0], c0 = R[2], a = R[3];
+        const u64 Y = y.s0 + y.s1, e = Y - a;
+        const u64 z0 = c0 + e * (2ull * a0 + e);      // = mpc::sq_with_a1
+        return {z0, Y * Y - z0};
+    }
+};
+// one step's triple of row unit u (the words nr_pregen writes for a unit, DESIGN.md 2.3 / 2.6)
+__device__ __forceinline__ void row_tab_step(const Keys& K, u64 u, u32 sj, bool square, u64* R)
+{
+    if (square) {
+        const uint4 A0 = prg(K.k0, u, sj, 2), A1 = prg(K.k1, u >> 1, sj, 3);
+        const u64 a0 = w64(A0.x, A0.y);
+        R[0] = a0; R[1] = 0; R[2] = w64(A0.z, A0.w);
+        R[3] = a0 + ((u & 1) ? w64(A1.z, A1.w) : w64(A1.x, A1.y)); R[4] = 0;
+    } else {
+        const uint4 A0 = prg(K.k0, u, sj, 0), A1 = prg(K.k1, u, sj, 0), Cb = prg(K.k0, u >> 1, sj, 1);
+        const u64 a0 = w64(A0.x, A0.y), b0 = w64(A0.z, A0.w);
+        R[0] = a0; R[1] = b0; R[2] = (u & 1) ? w64(Cb.z, Cb.w) : w64(Cb.x, Cb.y);
+        R[3] = a0 + w64(A1.x, A1.y); R[4] = b0 + w64(A1.z, A1.w);
+    }
+}
+#ifndef MPC_LNR_V
+#define MPC_LNR_V 1            // unit pairs per lane per Beaver call in passes B and D
+#endif
+template <class PA>
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_ln_row(const __grid_constant__ PA pa, LnRArgs a)
+{
+    __shared__ u64 tabs[MPC_ROW_TPB / 32][MPC_NR_TAB_MAX_STEPS * NR_TAB_F];
+    int cta, ncta;
+    auto pr = pa.make(cta, ncta);
+    using P = decltype(pr);
+    using S = typename P::S;
+    static_assert(!P::kPair, "BOTH only (PAIR keeps k_ln_fused)");
+    constexpr int V = MPC_LNR_V;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const i64 C = a.cols, hc = C / 2;                        // pairs per row (C even)
+    const i64 nk = (hc + 31) / 32;                           // pair chunks per lane
+    const i64 nwarp = (i64)ncta * NW;
+    const int ns = nr_tab_steps(1, a.rk.exp.t, a.rk.iters);
+    u64* T = tabs[warp];
+    for (i64 r = (i64)cta * NW + warp; r < a.rows; r += nwarp) {
+        const u64 g = a.row_off + (u64)r;                    // global row = the rsqrt's unit
+        const u64 ub = g * (u64)C;                           // even (C is)
+        const SP xr{{a.x.p[0] + r * C, a.x.p[1] + r * C}};
+        const SO zr{{a.z.p[0] + r * C, a.z.p[1] + r * C}};
+        if (MPC_GROUP_PREFETCH && r + nwarp < a.rows)        // the warp's next row to L2 (128-B lines)
+            for (i64 l = (i64)lane * 16; l < C; l += 32 * 16)
+#pragma unroll
+                for (int q = 0; q < 2; ++q) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.x.p[q] + (r + nwarp) * C + l));
+        // A: row sum -> mu (all chunks' loads in flight at once)
+        S acc = pr.zero();
+        for (i64 k0 = 0; k0 < nk; k0 += 4) {
+            S xa[4], xc[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                xa[q] = xc[q] = pr.zero();
+                const i64 p2 = lane + 32 * (k0 + q);
+                if (k0 + q < nk && p2 < hc) pr.ld_pair(xr, 2 * p2, true, true, xa[q], xc[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc = pr.add(acc, pr.add(xa[q], xc[q]));
+        }
+        S mu = pr.sumw(acc);
+        mu = a.mean_mode == 0 ? pr.mulf(mu, a.e_invd) : pr.divp(mu, C);
+        // the chain's triples: lane j < ns generates step j (data-independent; overlaps pass B)
+        if (lane < ns) row_tab_step(*pr.Kp, g, a.s_rs + (u32)lane, lane < a.rk.exp.t && a.rk.exp.sq, T + lane * NR_TAB_F);
+        // B: sum of MT(c, c), c = x - mu; the next chunk's pairs load while this one computes
+        S qs = pr.zero();
+        {
+            S nxa[V], nxc[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                nxa[v] = nxc[v] = pr.zero();
+                const i64 p2 = lane + 32 * v;
+                if (v < nk && p2 < hc) pr.ld_pair(xr, 2 * p2, true, true, nxa[v], nxc[v]);
+            }
+            for (i64 k0 = 0; k0 < nk; k0 += V) {
+                u64 u[V];
+                S ca[V], cb[V], za[V], zz[V];
+                bool ok[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 p2 = lane + 32 * (k0 + v);
+                    ok[v] = k0 + v < nk && p2 < hc;
+                    u[v] = ub + 2 * (u64)p2;
+                    ca[v] = pr.sub(nxa[v], mu); cb[v] = pr.sub(nxc[v], mu);
+                    const i64 q2 = p2 + 32 * V;
+                    nxa[v] = nxc[v] = pr.zero();
+                    if (k0 + v + V < nk && q2 < hc) pr.ld_pair(xr, 2 * q2, true, true, nxa[v], nxc[v]);
+                }
+                pr.template bm2v<V>(u, a.s_sq, ca, ca, cb, cb, za, zz);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (ok[v]) qs = pr.add(qs, pr.add(pr.shr_(za[v], FRAC), pr.shr_(zz[v], FRAC)));
+            }
+        }
+        S var = pr.sumw(qs);
+        var = a.mean_mode == 0 ? pr.mulf(var, a.e_invd) : pr.divp(var, C);
+        var = pr.addp(var, a.e_eps);
+        __syncwarp();
+        // C: r = RSQRT(var), unit g, every lane the same chain from the table
+        BothRowTabP tp;
+        tp.Kp = pr.Kp; tp.T = T; tp.sb = a.s_rs;
+        const S rr = rsqrt_group<false>(tp, g, g >> 5, a.s_rs, a.rk, var, lane);
+        // D: out = MT(c, r)
+        {
+            S nxa[V], nxc[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                nxa[v] = nxc[v] = pr.zero();
+                const i64 p2 = lane + 32 * v;
+                if (v < nk && p2 < hc) pr.ld_pair(xr, 2 * p2, true, true, nxa[v], nxc[v]);
+            }
+            for (i64 k0 = 0; k0 < nk; k0 += V) {
+                u64 u[V];
+                S ca[V], cb[V], rv[V], za[V], zz[V];
+                bool ok[V];
+                i64 e0[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    const i64 p2 = lane + 32 * (k0 + v);
+                    ok[v] = k0 + v < nk && p2 < hc;
+                    e0[v] = 2 * p2;
+                    u[v] = ub + 2 * (u64)p2;
+                    ca[v] = pr.sub(nxa[v], mu); cb[v] = pr.sub(nxc[v], mu); rv[v] = rr;
+                    const i64 q2 = p2 + 32 * V;
+                    nxa[v] = nxc[v] = pr.zero();
+                    if (k0 + v + V < nk && q2 < hc) pr.ld_pair(xr, 2 * q2, true, true, nxa[v], nxc[v]);
+                }
+                pr.template bm2v<V>(u, a.s_mul, ca, rv, cb, rv, za, zz);
+#pragma unroll
+                for (int v = 0; v < V; ++v)
+                    if (ok[v]) pr.st_pair(zr, e0[v], true, true, pr.shr_(za[v], FRAC), pr.shr_(zz[v], FRAC));
+            }
+        }
+        __syncwarp();                                         // T is rewritten for the next row
+    }
+    pa.done(pr);
+}
 
 // ------------------------------------------------- softmax after the max tree (BOTH, split form) ----
 // cfg2-shaped softmax as two launches: the row max tree (k_max, 32-row tiles, the rebalanced w = 33

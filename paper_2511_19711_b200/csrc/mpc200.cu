@@ -546,6 +546,16 @@ static mpc_status launch_groups(mpc_ctx* c, i64 n, u64 off, const Body& b, const
 static const size_t SMEM_LIMIT = 56 * 1024;      // + 16 KB static cone smem: keep 3 CTAs per SM
 
 // fused row kernels: work tile in shared memory when it fits, else a per-CTA global tile
+// Row kernels' tail tiles as 16-row half tiles (kernels.cuh tile_plan): off by default -- cfg2 softmax
+// 0.282 vs 0.271 ms, max 0.147 vs 0.141 ms (tools/ab_half.py, r02): a lone tile is latency-bound, so
+// a half tile is hardly shorter, and the SMs that held 3 tiles still hold 2 + 2 halves.
+// MPC_TAIL_HALF=1 in the environment turns it on (read per call: A/B and tests without a rebuild).
+static int tail_half()
+{
+    const char* e = getenv("MPC_TAIL_HALF");
+    return e ? atoi(e) : 0;
+}
+
 template <class Args, class KB, class KP>
 static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 work_u64, i64 esc_u64, const char* name,
                               size_t smem_limit = SMEM_LIMIT)
@@ -561,6 +571,9 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
     int grid;
     if (!is_pair(c)) grid = (int)std::min<i64>(ntiles, (i64)c->sm_count * occupancy(kb, dyn, MPC_ROW_TPB));
     else grid = pair_ctas(c, kp, dyn, ntiles, MPC_ROW_TPB);
+    // tests: cap the row kernels' grid (MPC_ROW_GRID_CAP) so small inputs take the multi-round and
+    // half-tile paths of tile_plan
+    if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < grid) grid = g; }
     const int launched = grid * (is_loop(c) ? 2 : 1);
     a.use_smem = smem ? 1 : 0;
     a.gscratch = nullptr;
@@ -1548,7 +1561,7 @@ mpc_status mpc_max(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t
         acct_max(c, rows, cols, w);
     } else if (rows > 0) {
         MaxArgs a{(u32)c->step, w, spv(c, x), sov(c, z), rows, cols, (u64)row_off, nullptr, 0, 0, nullptr,
-                  use_cone(c, w) ? 1 : 0};
+                  use_cone(c, w) ? 1 : 0, tail_half()};
         st = launch_max(c, a, rows, cols, w, "max");
         if (st) return st;
         acct_max(c, rows, cols, w);
@@ -1595,7 +1608,7 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
         if ((st = cuda_check(c, "pool_gather"))) return st;
         }
         MaxArgs a{(u32)c->step, w, SP{{rowsbuf.p[0], rowsbuf.p[1]}}, sov(c, z), rows, cols, row_off, nullptr, 0, 0,
-                  nullptr, use_cone(c, w) ? 1 : 0};
+                  nullptr, use_cone(c, w) ? 1 : 0, tail_half()};
         st = launch_max(c, a, rows, cols, w, "maxpool");
         if (st) return st;
         acct_max(c, rows, cols, w);
@@ -1822,6 +1835,9 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         a.bcast = p->bcast ? 1 : 0;
         a.causal = p->causal ? 1 : 0;
         a.causal_L = p->window >= 2 ? 0ull - (1ull << (p->window - 2)) : 0ull - 1ull;   // public -2^(w-2)
+        // half tiles start at row 16 mod 32: not with a clamp in the reciprocal's exp (an LTZ over the
+        // tile's row units) nor a clamped exp over odd rows (element groups would start mid-group)
+        a.half = (tail_half() && !p->recip.exp.clamp && !(p->exp.clamp && (cols & 1))) ? 1 : 0;
         const bool wide = p->window > 33 || p->exp.window > 33 || p->recip.exp.window > 33;
         // E in shared memory when the whole work tile fits 100 KB (two CTAs per SM): cols <= 192
 #ifndef MPC_SOFTMAX_ESMEM
@@ -1871,6 +1887,39 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
             rec_end(c);
             c->st.launches++;
             return cuda_check(c, "softmax");
+        }
+        a.bal = 0; a.tr = 32; a.tab_u64 = tab;
+        // BOTH balanced plan (kernels.cuh softmax_bal_*): when the 32-row tiles need more than one round,
+        // ONE row range of ~rows / grid rows per CTA, every CTA resident at once
+        const char* bal_env = getenv("MPC_SOFTMAX_BAL");      // 0: off (A/B, tests; read per call)
+        if (!(bal_env && atoi(bal_env) == 0) && !is_pair(c) && !wide && !a.cone && !a.bcast && !p->exp.clamp && !p->recip.exp.clamp && a.nrtab) {
+            static DevCache occb;
+            const int per_sm = dev_cached(occb, c->cfg.device, [] {
+                cudaFuncSetAttribute(k_softmax<0, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                return occupancy(k_softmax<0, BothA>, 100 * 1024, MPC_ROW_TPB);
+            });
+            i64 grid = (i64)c->sm_count * per_sm;
+            if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < grid) grid = g; }
+            const i64 hr = (rows + 1) / 2;
+            const i64 tr = 2 * ((hr + grid - 1) / grid);
+            const i64 wkb = softmax_bal_work_u64(cols, tr, tab);
+            if (rows > 32 * grid && tr <= 64 && wkb * 8 <= 100 * 1024) {
+                a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 1;
+                a.gscratch = nullptr; a.work_u64 = wkb;
+                u64* esc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * tr * cols * grid));
+                if (!esc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
+                a.escratch = esc;
+                const size_t dyn = sizeof(u64) * (size_t)wkb;
+                // every launch: launch_rows sets the same kernels' attribute to other tiles' sizes
+                cudaFuncSetAttribute(a.causal ? k_softmax<0, BothA, true> : k_softmax<0, BothA>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+                rec_begin(c, "softmax", (u64)rows);
+                if (a.causal) k_softmax<0, BothA, true><<<(int)grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, a);
+                else k_softmax<0, BothA><<<(int)grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, a);
+                rec_end(c);
+                c->st.launches++;
+                return cuda_check(c, "softmax");
+            }
         }
         const i64 wk = softmax_work_u64(cols, a.esmem != 0, tab), ek = a.esmem ? 0 : 64 * cols;
         const size_t lim = a.esmem ? 100 * 1024 + (size_t)tab * 8 : SMEM_LIMIT;
@@ -1930,7 +1979,32 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
 #define MPC_LN_FUSED 1
 #endif
         const int nsteps_rs = nr_tab_steps(1, p->rsqrt.exp.t, p->rsqrt.iters);
-        if (MPC_LN_FUSED && !p->rsqrt.exp.clamp && !p->bcast && !(cols & 1) && rows * cols < (1ll << 31)) {
+        // BOTH: one warp per row (kernels.cuh k_ln_row) when its rows fill the warps' rounds evenly
+        // (ceil(rows / warps) rounds at >= 90 % of the work, or one round); otherwise the row-block
+        // kernel.  Measured (tools/ab_ln.py, r02): 24576 x 768 0.413 vs 0.447 ms, 1024 x 768 0.029 vs
+        // 0.035; cfg5 8192 x 768 (3.46 rows per warp) 0.161 vs 0.148 -> k_ln_fused.  A warp's row is
+        // latency-bound (fewer warps per CTA to even the rounds measured slower: 7 warps 0.162 ms)
+        const char* lnr_env = getenv("MPC_LN_ROW");          // 0 / 1 force (A/B, tests); read per call
+        bool ln_row = false;
+        if (!is_pair(c) && !p->rsqrt.exp.clamp && !p->bcast && !(cols & 1) && nsteps_rs <= MPC_NR_TAB_MAX_STEPS) {
+            static DevCache occr;
+            const int per_sm = dev_cached(occr, c->cfg.device, [&] { return occupancy(k_ln_row<BothA>, 0, MPC_ROW_TPB); });
+            const i64 nw = (i64)c->sm_count * per_sm * (MPC_ROW_TPB / 32), rounds = (rows + nw - 1) / nw;
+            ln_row = rounds == 1 || (double)rows >= 0.9 * (double)(rounds * nw);
+            if (lnr_env) ln_row = atoi(lnr_env) != 0;
+        }
+        if (ln_row) {
+            LnRArgs f{a.s_sq, a.s_rs, a.s_mul, a.rk, a.x, a.z, rows, cols, (u64)row_off, a.mean_mode, a.e_invd, a.e_eps};
+            static DevCache occ;
+            const int per_sm = dev_cached(occ, c->cfg.device, [&] { return occupancy(k_ln_row<BothA>, 0, MPC_ROW_TPB); });
+            const i64 nctas = (rows + MPC_ROW_TPB / 32 - 1) / (MPC_ROW_TPB / 32);
+            const int grid = (int)std::min<i64>(nctas, (i64)c->sm_count * per_sm);
+            rec_begin(c, "layernorm", (u64)rows);
+            k_ln_row<BothA><<<grid, MPC_ROW_TPB, 0, c->stream>>>(BothA{c->K}, f);
+            rec_end(c);
+            c->st.launches++;
+            st = cuda_check(c, "layernorm");
+        } else if (MPC_LN_FUSED && !p->rsqrt.exp.clamp && !p->bcast && !(cols & 1) && rows * cols < (1ll << 31)) {
             // one launch, row blocks of RB rows with every block resident (kernels.cuh k_ln_fused)
             LnFArgs f{a.s_sq, a.s_rs, a.s_mul, a.rk, a.x, a.z, rows, cols, (u64)row_off, a.mean_mode, a.e_invd,
                       a.e_eps, 2, 0};

@@ -1,0 +1,226 @@
+"""Row kernels' tail as 16-row half tiles (kernels.cuh tile_plan): when the last round
+of 32-row tiles would leave P = ntiles mod ncta tiles with 2P <= ncta, those P tiles run as 2P half
+tiles of 16 rows.  A half tile starts at a row = 16 mod 32, so the max tree's levels whose LTZ groups
+span 32 rows evaluate a group with half its lanes outside the tile.  The contract (steps, units,
+PRG words) does not depend on the tiling: every share must equal the oracle's.  MPC_ROW_GRID_CAP
+caps the grid so that small inputs take the multi-round and half-tile paths; the half tiles are
+off by default (measured slower) and MPC_TAIL_HALF=1 turns them on per call."""
+import numpy as np
+import pytest
+
+import workloads
+from oracle import Oracle
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_2511_19711_b200 as mod
+    return mod
+
+
+def same(g, o):
+    a0, a1 = g[0].cpu().numpy(), g[1].cpu().numpy()
+    bad = np.nonzero((a0 != o[0]) | (a1 != o[1]))[0]
+    assert bad.size == 0, f"{bad.size} mismatching shares, first at {bad[:5]}"
+
+
+def ctx(m, cfg, step, mode=None):
+    keys = workloads.keys(cfg)
+    c = m.Ctx.for_cfg(keys) if mode is None else m.Ctx.for_cfg(keys, mode=mode)
+    c.set_step(step)
+    return c, Oracle.for_cfg(keys, step)
+
+
+# (rows, cap): 5 tiles on 4 CTAs -> 4 full + 2 halves (the last one ragged: 150 rows); 7 on 3 -> 6 +
+# 2; 5 on 2 -> 2P > ncta, no split (multi-round only); 3 tiles on 4 -> one round
+PLANS = [(150, 4), (160, 4), (224, 3), (150, 2), (96, 4), (140, 4)]
+
+
+@pytest.mark.parametrize("rows,cap", PLANS)
+@pytest.mark.parametrize("cols", [128, 77, 9])
+def test_softmax_half_tiles(m, monkeypatch, rows, cap, cols):
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    monkeypatch.setenv("MPC_TAIL_HALF", "1")
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    c, o = ctx(m, 2, 3)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols, row_off=32), o.softmax(ox, rows, cols, row_off=32))
+
+
+@pytest.mark.parametrize("rows,cap", [(150, 4), (224, 3)])
+@pytest.mark.parametrize("kw", [dict(exp_clamp=1), dict(causal=1), dict(bcast=1), dict(window=64)])
+def test_softmax_half_tiles_knobs(m, monkeypatch, rows, cap, kw):
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    monkeypatch.setenv("MPC_TAIL_HALF", "1")
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    cols = 64
+    c, o = ctx(m, 2, 5)
+    x = workloads.softmax_inputs(rows, cols, spike="exp_clamp" in kw)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols, row_off=64, **kw), o.softmax(ox, rows, cols, row_off=64, **kw))
+
+
+@pytest.mark.parametrize("rows,cap", [(150, 4), (224, 3)])
+def test_softmax_half_tiles_cone(m, monkeypatch, rows, cap):
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    monkeypatch.setenv("MPC_TAIL_HALF", "1")
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    cols = 128
+    c, o = ctx(m, 2, 7)
+    c.set_ltz_circuit(1)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols), o.softmax(ox, rows, cols))
+
+
+@pytest.mark.parametrize("rows,cap", [(150, 4), (224, 3)])
+@pytest.mark.parametrize("cols", [128, 33])
+def test_max_half_tiles(m, monkeypatch, rows, cap, cols):
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    monkeypatch.setenv("MPC_TAIL_HALF", "1")
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    c, o = ctx(m, 2, 1)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.max(gx, rows, cols, row_off=32), o.max(ox, rows, cols, row_off=32))
+
+
+def test_softmax_half_tiles_off_equals_on(m, monkeypatch):
+    """the capped grid with half tiles equals the uncapped one share for share"""
+    rows, cols = 224, 128
+    c, _ = ctx(m, 2, 9)
+    gx = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    s0 = c.step
+    a = c.softmax(gx, rows, cols)
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", "3")
+    monkeypatch.setenv("MPC_TAIL_HALF", "1")
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    c.set_step(s0, force=True)
+    b = c.softmax(gx, rows, cols)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("rows,cap", [(150, 4), (224, 3)])
+def test_softmax_half_tiles_loopback(m, monkeypatch, rows, cap):
+    """PAIR protocol in loopback: each party's CTAs follow the same plan (the cap is per party)"""
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    monkeypatch.setenv("MPC_TAIL_HALF", "1")
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    cols = 128
+    c, o = ctx(m, 2, 11, mode=m.binding.MODE_PAIR_LOOPBACK)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    z = c.softmax(gx, rows, cols, row_off=32)
+    c.sync()
+    same(z, o.softmax(ox, rows, cols, row_off=32))
+
+
+# ---- balanced softmax plan (BOTH: one row range of ~rows / grid rows per CTA, kernels.cuh
+# softmax_bal_*): taken when the 32-row tiles need more than one round; the cap shrinks the grid ----
+BAL = [(150, 4), (140, 4), (160, 4), (255, 5), (1000, 16), (129, 4)]
+
+
+@pytest.mark.parametrize("rows,cap", BAL)
+@pytest.mark.parametrize("cols", [128, 77, 9, 2])
+def test_softmax_balanced(m, monkeypatch, rows, cap, cols):
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    c, o = ctx(m, 2, 13)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols, row_off=96), o.softmax(ox, rows, cols, row_off=96))
+
+
+@pytest.mark.parametrize("rows,cap", [(150, 4), (255, 5)])
+@pytest.mark.parametrize("kw", [dict(causal=1), dict(exp_square=1, recip_square=1), dict(recip_iters=3, exp_t=4)])
+def test_softmax_balanced_knobs(m, monkeypatch, rows, cap, kw):
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    cols = 64
+    c, o = ctx(m, 2, 15)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols, row_off=32, **kw), o.softmax(ox, rows, cols, row_off=32, **kw))
+
+
+def test_softmax_balanced_after_other_tiles(m, monkeypatch):
+    """the balanced launch sets its own dynamic shared-memory size after launches of the same kernel
+    with other tile sizes (a stale attribute made the first full-size run fail)"""
+    c, o = ctx(m, 2, 17)
+    for rows, cols in [(64, 9), (40, 77)]:
+        x = workloads.softmax_inputs(rows, cols)
+        gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+        same(c.softmax(gx, rows, cols), o.softmax(ox, rows, cols))
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", "4")
+    rows, cols = 150, 128
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols), o.softmax(ox, rows, cols))
+
+
+def test_softmax_balanced_equals_tiles(m, monkeypatch):
+    """balanced plan = 32-row tiles, share for share, on the same call"""
+    rows, cols = 1000, 128
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", "16")
+    c, _ = ctx(m, 2, 19)
+    gx = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    s0 = c.step
+    a = c.softmax(gx, rows, cols)
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    c.set_step(s0, force=True)
+    b = c.softmax(gx, rows, cols)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ---- warp-per-row LayerNorm (kernels.cuh k_ln_row, BOTH): every share vs the oracle ----
+@pytest.mark.parametrize("rows,cols", [(1, 2), (3, 64), (70, 768), (45, 100), (9, 1030), (33, 2048)])
+@pytest.mark.parametrize("mean_mode", [0, 1])
+def test_layernorm_row_kernel(m, monkeypatch, rows, cols, mean_mode):
+    monkeypatch.setenv("MPC_LN_ROW", "1")
+    c, o = ctx(m, 5, 2)
+    x = workloads.layernorm_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    kw = dict(mean_mode=mean_mode)
+    same(c.layernorm(gx, rows, cols, row_off=32, **kw), o.layernorm(ox, rows, cols, row_off=32, **kw))
+    assert c.step == o.step
+
+
+@pytest.mark.parametrize("kw", [dict(rsqrt_iters=10), dict(rsqrt_square=1), dict(rsqrt_t=4, rsqrt_iters=1),
+                                dict(rsqrt_iters=8, rsqrt_t=8)])
+def test_layernorm_row_kernel_knobs(m, monkeypatch, kw):
+    monkeypatch.setenv("MPC_LN_ROW", "1")
+    rows, cols = 150, 768
+    c, o = ctx(m, 5, 4)
+    x = workloads.layernorm_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.layernorm(gx, rows, cols, row_off=64, **kw), o.layernorm(ox, rows, cols, row_off=64, **kw))
+
+
+def test_layernorm_row_kernel_many_rows_per_warp(m, monkeypatch):
+    """a long input gives every warp several rows (forced: the heuristic picks k_ln_fused here)"""
+    monkeypatch.setenv("MPC_LN_ROW", "1")
+    rows, cols = 6000, 128
+    c, o = ctx(m, 5, 6)
+    x = workloads.layernorm_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.layernorm(gx, rows, cols), o.layernorm(ox, rows, cols))
+
+
+@pytest.mark.parametrize("rows", [4700, 2368 * 2])
+def test_layernorm_kernel_choice_both_exact(m, monkeypatch, rows):
+    """k_ln_row and k_ln_fused on the same call: the same shares"""
+    cols = 256
+    c, _ = ctx(m, 5, 8)
+    gx = c.share(torch.from_numpy(workloads.layernorm_inputs(rows, cols)).cuda())
+    s0 = c.step
+    monkeypatch.setenv("MPC_LN_ROW", "1")
+    a = c.layernorm(gx, rows, cols)
+    monkeypatch.setenv("MPC_LN_ROW", "0")
+    c.set_step(s0, force=True)
+    b = c.layernorm(gx, rows, cols)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
