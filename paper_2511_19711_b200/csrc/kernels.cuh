@@ -754,6 +754,9 @@ __host__ __device__ inline i64 softmax_work_u64(i64 cols, bool esmem = false, i6
     return softmax_x_off(cols, esmem) + 9 * 32 + tab_u64;   // [.. X (9 x 32)] [NR triple table]
 }
 
+#ifndef MPC_SOFTMAX_EXP_V
+#define MPC_SOFTMAX_EXP_V 1    // BOTH: unit pairs per thread and pass in the softmax exp phase
+#endif
 // LV: 0 Kogge-Stone LTZ (w <= 33), 1 Kogge-Stone wide (w > 33), 2 carry cone (w <= 33), 3 carry cone
 // wide (w <= 64) -- separate instantiations so the cone's registers / shared memory do not cost the
 // others occupancy
@@ -846,7 +849,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
                 }
             }
         } else {
-            constexpr int V = decltype(pr)::kV;
+            constexpr int V = decltype(pr)::kPair ? decltype(pr)::kV : MPC_SOFTMAX_EXP_V;   // BOTH: A/B knob
             for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {
                 u64 uv[V];
                 S da[V], db[V];

@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "matmul.cuh"
 #include "matmul_tc.cuh"
+#include "ln_blk.cuh"
 #include "plain.cuh"
 
 using namespace mpc;
@@ -1618,7 +1619,7 @@ mpc_status mpc_maxpool2d(mpc_ctx* c, mpc_shares x, mpc_shares z, int N, int C, i
 }
 
 static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off,
-                               const mpc_softmax_p* p, u32 s0);
+                               const mpc_softmax_p* p, u32 s0, int bal_default = 2);
 static void acct_softmax(mpc_ctx* c, int64_t rows, int64_t cols, const mpc_softmax_p* p);
 
 mpc_status mpc_softmax(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off,
@@ -1781,7 +1782,9 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         c->stream = h->cs[cb]; c->scratch = h->scr[cb]; c->scratch_bytes = h->scr_bytes[cb];
         mpc_shares xs{{dx[0], dx[1]}}, zs{{dz[0], dz[1]}};
         if (c->cfg.mode == MPC_MODE_PAIR) { xs.sh[1 - c->cfg.party] = nullptr; zs.sh[1 - c->cfg.party] = nullptr; }
-        st = softmax_core(c, xs, zs, ri, cols, row_off + r0, p, s0);
+        // (chunks keep the 32-row tiles unless they need several rounds: concurrent chunks on their own
+        // streams share the GPU -- every chunk on all CTAs measured 0.80 vs 0.755 ms for cfg2, r02)
+        st = softmax_core(c, xs, zs, ri, cols, row_off + r0, p, s0, 1);
         h->scr[cb] = c->scratch; h->scr_bytes[cb] = c->scratch_bytes;
         c->scratch = save_scr; c->scratch_bytes = save_bytes; c->stream = user;
         if (st) return st;
@@ -1818,7 +1821,7 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
 }
 
 static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, int64_t cols, int64_t row_off,
-                               const mpc_softmax_p* p, u32 s0)
+                               const mpc_softmax_p* p, u32 s0, int bal_default)
 {
     const int L = max_levels_h(cols);
     mpc_status st;
@@ -1900,10 +1903,17 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
             });
             i64 grid = (i64)c->sm_count * per_sm;
             if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < grid) grid = g; }
+            // 2 (default): always, on min(grid, rows / 2) CTAs (>= 2 rows each) -- fewer rows per CTA
+            // means a shorter critical path (1024 rows: 0.050 vs 0.113 ms on 32 tiles; 3072: 0.089 vs
+            // 0.115; 8192: 0.172 vs 0.186, tools/ab_rows.py, r02) for more LTZ groups shared at range
+            // boundaries; 1: only when the 32-row tiles need more than one round (the host-buffer chunks)
+            const int bal_mode = bal_env ? atoi(bal_env) : bal_default;
+            if (bal_mode >= 2) grid = std::max<i64>(1, std::min<i64>(grid, rows / 2));
             const i64 hr = (rows + 1) / 2;
             const i64 tr = 2 * ((hr + grid - 1) / grid);
             const i64 wkb = softmax_bal_work_u64(cols, tr, tab);
-            if (rows > 32 * grid && tr <= 64 && wkb * 8 <= 100 * 1024) {
+            const bool want = bal_mode >= 2 ? true : rows > 32 * grid;
+            if (want && tr <= 64 && wkb * 8 <= 100 * 1024) {
                 a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 1;
                 a.gscratch = nullptr; a.work_u64 = wkb;
                 u64* esc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * tr * cols * grid));
@@ -1993,7 +2003,33 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
             ln_row = rounds == 1 || (double)rows >= 0.9 * (double)(rounds * nw);
             if (lnr_env) ln_row = atoi(lnr_env) != 0;
         }
-        if (ln_row) {
+        // BOTH: row blocks staged in shared memory by double-buffered bulk copies (ln_blk.cuh): the
+        // largest RB in {8, 4, 2, 1} whose two buffers fit 96 KB.  MPC_LN_BLK=0: off (A/B; per call)
+        const char* lnb_env = getenv("MPC_LN_BLK");
+        int lnb_rb = 0;
+        if (!(lnb_env && atoi(lnb_env) == 0) && !is_pair(c) && !p->rsqrt.exp.clamp && !p->bcast && !(cols & 1) &&
+            nsteps_rs <= MPC_NR_TAB_MAX_STEPS)
+            for (int rb = 8; rb >= 1 && !lnb_rb; rb /= 2)
+                if (lnb_smem_bytes(cols, rb) <= 96 * 1024) lnb_rb = rb;
+        if (lnb_rb) {
+            LnBArgs f{a.s_sq, a.s_rs, a.s_mul, a.rk, a.x, a.z, rows, cols, (u64)row_off, a.mean_mode, a.e_invd, a.e_eps,
+                      lnb_rb};
+            const size_t dyn = lnb_smem_bytes(cols, lnb_rb);
+            static DevCache occb;
+            const int per_sm = dev_cached(occb, c->cfg.device, [&] {
+                cudaFuncSetAttribute(k_ln_blk<BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+                return occupancy(k_ln_blk<BothA>, 96 * 1024, MPC_ROW_TPB);
+            });
+            cudaFuncSetAttribute(k_ln_blk<BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            const i64 nblk = (rows + lnb_rb - 1) / lnb_rb;
+            int grid = (int)std::min<i64>(nblk, (i64)c->sm_count * per_sm);
+            if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < grid) grid = g; }
+            rec_begin(c, "layernorm", (u64)rows);
+            k_ln_blk<BothA><<<grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, f);
+            rec_end(c);
+            c->st.launches++;
+            st = cuda_check(c, "layernorm");
+        } else if (ln_row) {
             LnRArgs f{a.s_sq, a.s_rs, a.s_mul, a.rk, a.x, a.z, rows, cols, (u64)row_off, a.mean_mode, a.e_invd, a.e_eps};
             static DevCache occ;
             const int per_sm = dev_cached(occ, c->cfg.device, [&] { return occupancy(k_ln_row<BothA>, 0, MPC_ROW_TPB); });

@@ -296,8 +296,8 @@ struct PairP : StreamState<R> {
     // atomic.  put / get must be issued by all 32 lanes together (LL63's ballot); a lane with
     // live = false sends, reads and (LL63) flips nothing for that word -- both parties pass the same
     // live pattern.
-    // (LL inline; LL63 out of line: its code stays out of the loopback kernels' instruction stream,
-    // and across NVLink a call per word is nothing next to the round trip)
+    // (both inline: an out-of-line LL63 put / get kept its code out of the loopback kernels' stream
+    // but cost 20 % in LL63 loopback -- call overhead per word; inline costs LL 2 %)
 #ifndef MPC_XFMT_LL_ONLY
 #define MPC_XFMT_LL_ONLY 0     // A/B builds: compile the LL63 path out
 #endif
@@ -313,7 +313,14 @@ struct PairP : StreamState<R> {
         }
         put63(lane, k, v, live, b);
     }
+#ifndef MPC_LL63_INLINE
+#define MPC_LL63_INLINE 1      // LL63 put / get inline: loopback LL63 softmax 2.03 -> 1.63 ms, GELU 1M 1.59 -> 1.34 ms; LL +2 % (r02)
+#endif
+#if MPC_LL63_INLINE
+    __device__ __forceinline__ void put63(int lane, int k, u64 v, bool live, int b) {
+#else
     __device__ __noinline__ void put63(int lane, int k, u64 v, bool live, int b) {
+#endif
         const u32 mb = 1u << (8 * b + k), eb = 1u << (16 + 8 * b + k);
         tg ^= eb;
         if (live) tg ^= mb;
@@ -348,7 +355,11 @@ struct PairP : StreamState<R> {
         }
         return get63(lane, k, b);
     }
+#if MPC_LL63_INLINE
+    __device__ __forceinline__ u64 get63(int lane, int k, int b) {
+#else
     __device__ __noinline__ u64 get63(int lane, int k, int b) {
+#endif
         const u64* sp = rx + (b * XW + k) * 32 + lane;
         const u64* ep = rx + 2 * XW * 32 + b * XW + k;
         const u64 want = (tg >> (8 * b + k)) & 1u, wante = (tg >> (16 + 8 * b + k)) & 1u;

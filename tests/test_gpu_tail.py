@@ -181,6 +181,7 @@ def test_softmax_balanced_equals_tiles(m, monkeypatch):
 @pytest.mark.parametrize("mean_mode", [0, 1])
 def test_layernorm_row_kernel(m, monkeypatch, rows, cols, mean_mode):
     monkeypatch.setenv("MPC_LN_ROW", "1")
+    monkeypatch.setenv("MPC_LN_BLK", "0")
     c, o = ctx(m, 5, 2)
     x = workloads.layernorm_inputs(rows, cols)
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
@@ -193,6 +194,7 @@ def test_layernorm_row_kernel(m, monkeypatch, rows, cols, mean_mode):
                                 dict(rsqrt_iters=8, rsqrt_t=8)])
 def test_layernorm_row_kernel_knobs(m, monkeypatch, kw):
     monkeypatch.setenv("MPC_LN_ROW", "1")
+    monkeypatch.setenv("MPC_LN_BLK", "0")
     rows, cols = 150, 768
     c, o = ctx(m, 5, 4)
     x = workloads.layernorm_inputs(rows, cols)
@@ -203,6 +205,7 @@ def test_layernorm_row_kernel_knobs(m, monkeypatch, kw):
 def test_layernorm_row_kernel_many_rows_per_warp(m, monkeypatch):
     """a long input gives every warp several rows (forced: the heuristic picks k_ln_fused here)"""
     monkeypatch.setenv("MPC_LN_ROW", "1")
+    monkeypatch.setenv("MPC_LN_BLK", "0")
     rows, cols = 6000, 128
     c, o = ctx(m, 5, 6)
     x = workloads.layernorm_inputs(rows, cols)
@@ -218,7 +221,51 @@ def test_layernorm_kernel_choice_both_exact(m, monkeypatch, rows):
     gx = c.share(torch.from_numpy(workloads.layernorm_inputs(rows, cols)).cuda())
     s0 = c.step
     monkeypatch.setenv("MPC_LN_ROW", "1")
+    monkeypatch.setenv("MPC_LN_BLK", "0")
     a = c.layernorm(gx, rows, cols)
+    monkeypatch.setenv("MPC_LN_ROW", "0")
+    c.set_step(s0, force=True)
+    b = c.layernorm(gx, rows, cols)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ---- LayerNorm on shared-memory row blocks (ln_blk.cuh k_ln_blk, BOTH): every share vs the oracle ----
+@pytest.mark.parametrize("rows,cols", [(1, 2), (7, 64), (70, 768), (45, 100), (9, 1030), (33, 2048), (5, 3072),
+                                       (13, 4000)])
+@pytest.mark.parametrize("cap", ["0", "3"])
+def test_layernorm_blocks(m, monkeypatch, rows, cols, cap):
+    """RB = 8 / 4 / 2 / 1 rows per block by width (4000: no block fits, another kernel); cap 3: several
+    blocks per CTA through both buffers; ragged last blocks"""
+    if cap != "0":
+        monkeypatch.setenv("MPC_ROW_GRID_CAP", cap)
+    c, o = ctx(m, 5, 12)
+    x = workloads.layernorm_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    for mm in (0, 1):
+        same(c.layernorm(gx, rows, cols, row_off=32, mean_mode=mm), o.layernorm(ox, rows, cols, row_off=32, mean_mode=mm))
+    assert c.step == o.step
+
+
+@pytest.mark.parametrize("kw", [dict(rsqrt_iters=10), dict(rsqrt_square=1), dict(rsqrt_t=4, rsqrt_iters=1),
+                                dict(rsqrt_iters=8, rsqrt_t=8), dict(eps=0.5)])
+def test_layernorm_blocks_knobs(m, monkeypatch, kw):
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", "5")
+    rows, cols = 150, 768
+    c, o = ctx(m, 5, 14)
+    x = workloads.layernorm_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.layernorm(gx, rows, cols, row_off=64, **kw), o.layernorm(ox, rows, cols, row_off=64, **kw))
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 768), (3001, 256)])
+def test_layernorm_blocks_equal_fused(m, monkeypatch, rows, cols):
+    """k_ln_blk and k_ln_fused on the same call: the same shares"""
+    c, _ = ctx(m, 5, 16)
+    gx = c.share(torch.from_numpy(workloads.layernorm_inputs(rows, cols)).cuda())
+    s0 = c.step
+    a = c.layernorm(gx, rows, cols)
+    monkeypatch.setenv("MPC_LN_BLK", "0")
     monkeypatch.setenv("MPC_LN_ROW", "0")
     c.set_step(s0, force=True)
     b = c.layernorm(gx, rows, cols)
