@@ -321,7 +321,7 @@ def run_mpc200(args):
     parity = check_timed_output(job, ctx.step - steps_per_call, xs, out, rows, cols, row_off, sm_kw)
 
     # ---- e2e: host buffers through the public API (H2D inputs, D2H outputs inside the region) ----
-    # mpc_softmax_hostio: chunks of 3072 rows, H2D / compute / D2H of neighbouring chunks overlapped
+    # mpc_softmax_hostio: chunks of 1536 rows, H2D / compute / D2H of neighbouring chunks overlapped
     # on separate streams (tools/perf_e2e.py: 1.21 ms sequential -> 0.80 ms per cfg2 step)
     # both parties' shares in ONE pinned [2][n] host tensor each way, so a chunk's two party copies
     # are one pitched 2D DMA submission (copy_pair in mpc200.cu)
@@ -339,15 +339,15 @@ def run_mpc200(args):
     hin = pinned_pair(xs)
     hout = pinned_pair(tuple(torch.empty_like(s) if s is not None else None for s in xs))
     e2e_steps = max(3, min(args.steps, 10))
-    job.prefeed(ctx, lambda c=ctx: c.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=3072, **sm_kw),
+    job.prefeed(ctx, lambda c=ctx: c.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=1536, **sm_kw),
                 1 + e2e_steps)
-    ctx.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=3072, **sm_kw)    # warm-up
+    ctx.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=1536, **sm_kw)    # warm-up
     job.barrier()
     torch.cuda.synchronize()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ea.record(job.stream)
     for _ in range(e2e_steps):
-        ctx.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=3072, **sm_kw)
+        ctx.softmax_hostio(hin, hout, rows, cols, row_off=row_off, chunk_rows=1536, **sm_kw)
     eb.record(job.stream)
     torch.cuda.synchronize()
     e_ms = job.maxr(ea.elapsed_time(eb) / e2e_steps)
@@ -375,7 +375,7 @@ def run_mpc200(args):
                "e2e": {"value": job.npairs * n / (e_ms / 1e3), "unit": "elements/s",
                        "h2d_bytes_per_step": 16 * n * job.npairs, "d2h_bytes_per_step": 16 * n * job.npairs,
                        "ms_per_step": round(e_ms, 4),
-                       "api": "mpc_softmax_hostio (pinned host shares in/out, 3072-row chunks, copies overlapped)",
+                       "api": "mpc_softmax_hostio (pinned host shares in/out, 1536-row chunks, copies overlapped)",
                        "pcie_floor_ms": pcie, "frac_of_pcie_floor": round(pcie / e_ms, 3) if pcie else None,
                        "pcie_floor_how": "the step's H2D and D2H bytes as one copy per direction on two streams "
                                          "at once (no compute): the transfer-only time of a step"},

@@ -548,7 +548,7 @@ class Ctx:
         self._chk(_L.mpc_softmax(self._h, _sh(x), _sh(z), rows, cols, row_off, ctypes.byref(p)), "mpc_softmax")
         return z
 
-    def softmax_hostio(self, hx, hz, rows, cols, row_off=0, chunk_rows=2048, window=33, exp_t=8, exp_clamp=0,
+    def softmax_hostio(self, hx, hz, rows, cols, row_off=0, chunk_rows=1536, window=33, exp_t=8, exp_clamp=0,
                        exp_window=33, recip_iters=10, recip_t=8, recip_clamp=0, recip_window=33, exp_square=0,
                        recip_square=0, bcast=0, causal=0):
         """Softmax over HOST buffers (hx, hz: per-party CPU uint64 tensors, pinned): chunked, with the

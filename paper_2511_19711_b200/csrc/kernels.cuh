@@ -934,11 +934,12 @@ struct MaxArgs {
     u64* gscratch; i64 work_u64; int use_smem;
     u64* escratch; int cone;
     int half;               // tail tiles as 16-row half tiles (tile_plan)
+    int tr;                 // > 0: the balanced plan (k_softmax's): one range of <= tr rows per CTA
 };
-__host__ __device__ inline i64 max_work_u64(i64 cols)
+__host__ __device__ inline i64 max_work_u64(i64 cols, i64 tr = 32)
 {
     const i64 HA = (cols + 1) / 2, HB = (HA + 1) / 2;
-    return 64 * HA + 64 * HB + 2 * 32;
+    return 2 * tr * HA + 2 * tr * HB + 2 * tr;
 }
 
 template <int LV, class PA>   // LV as k_softmax
@@ -951,15 +952,24 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     auto pr = pa.make(cta, ncta);
     u64* W = a.use_smem ? smem : a.gscratch + (i64)blockIdx.x * a.work_u64;
     const i64 C = a.cols, HA = (C + 1) / 2, HB = (HA + 1) / 2;
-    SO A{{W, W + 32 * HA}}, B{{W + 64 * HA, W + 64 * HA + 32 * HB}};
-    SO MX{{W + 64 * HA + 64 * HB, W + 64 * HA + 64 * HB + 32}};
+    const i64 TR = a.tr > 0 ? a.tr : 32;
+    SO A{{W, W + TR * HA}}, B{{W + 2 * TR * HA, W + 2 * TR * HA + TR * HB}};
+    SO MX{{W + 2 * TR * HA + 2 * TR * HB, W + 2 * TR * HA + 2 * TR * HB + TR}};
     const TilePlan tp = tile_plan(a.rows, ncta, a.half);
-    for (i64 tile = cta; tile < tp.ntot; tile += ncta) {
+    const i64 ntl = a.tr > 0 ? (i64)ncta : tp.ntot;
+    for (i64 tile = cta; tile < ntl; tile += ncta) {
         i64 r0; int R;
-        tile_rows(tp, tile, a.rows, r0, R);
-        if (R <= 0) break;
+        if (a.tr > 0) {                                   // balanced plan (k_softmax's softmax_bal_*)
+            const i64 hr = (a.rows + 1) / 2;
+            r0 = min(a.rows, 2 * (tile * hr / ncta));
+            R = (int)(min(a.rows, 2 * ((tile + 1) * hr / ncta)) - r0);
+            if (R <= 0) continue;
+        } else {
+            tile_rows(tp, tile, a.rows, r0, R);
+            if (R <= 0) break;
+        }
         const SP xt{{a.x.p[0] ? a.x.p[0] + r0 * C : nullptr, a.x.p[1] ? a.x.p[1] + r0 * C : nullptr}};
-        prefetch_rows(a.x, r0 + (i64)ncta * 32, a.rows, C);
+        if (a.tr <= 0) prefetch_rows(a.x, r0 + (i64)ncta * 32, a.rows, C);
         // standalone max (and softmax's split max pass): the rebalanced w = 33 LTZ (k_max has the registers)
         tile_max<WIDE, CONE, decltype(pr), false, true>(pr, a.s, a.w, xt, C, C, R, a.row_off + (u64)r0, A, B, HA, HB, MX, cone_sm);
         const SP MXc{{MX.p[0], MX.p[1]}};
@@ -1786,9 +1796,12 @@ struct SmRestArgs {
     int tab_u64;            // u64 words of one 32-row NR table
 };
 constexpr int SMR_SEG = 66;                    // row segments per warp (<= RB + 2)
-__host__ __device__ inline int smr_smem_u64(int tab_u64) { return 6 * 64 + 8 * SMR_SEG * 2 + 2 * tab_u64; }
+__host__ __device__ inline int smr_smem_u64(int tab_u64, int ntab = 2) { return 6 * 64 + 8 * SMR_SEG * 2 + ntab * tab_u64; }
+#ifndef MPC_SMR_MINB
+#define MPC_SMR_MINB 3         // resident CTAs per SM of k_softmax_rest (<= 85 registers: 24 warps per SM)
+#endif
 template <class PA>
-__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SM_MINB) k_softmax_rest(const __grid_constant__ PA pa, SmRestArgs a)
+__global__ void __launch_bounds__(MPC_ROW_TPB, MPC_SMR_MINB) k_softmax_rest(const __grid_constant__ PA pa, SmRestArgs a)
 {
     extern __shared__ __align__(16) u64 rsm[];
     int cta, ncta;

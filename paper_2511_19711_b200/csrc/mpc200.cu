@@ -1782,9 +1782,11 @@ mpc_status mpc_softmax_hostio(mpc_ctx* c, mpc_shares hx, mpc_shares hz, int64_t 
         c->stream = h->cs[cb]; c->scratch = h->scr[cb]; c->scratch_bytes = h->scr_bytes[cb];
         mpc_shares xs{{dx[0], dx[1]}}, zs{{dz[0], dz[1]}};
         if (c->cfg.mode == MPC_MODE_PAIR) { xs.sh[1 - c->cfg.party] = nullptr; zs.sh[1 - c->cfg.party] = nullptr; }
-        // (chunks keep the 32-row tiles unless they need several rounds: concurrent chunks on their own
-        // streams share the GPU -- every chunk on all CTAs measured 0.80 vs 0.755 ms for cfg2, r02)
-        st = softmax_core(c, xs, zs, ri, cols, row_off + r0, p, s0, 1);
+        // (the chunks' kernels take the balanced plan too: cfg2 in 1536-row chunks 0.716-0.730 ms vs
+        // 0.756-0.768 for 3072-row chunks on 32-row tiles -- the pipeline's head and tail are one chunk's
+        // latency; 3072-row chunks on the balanced plan 0.82 ms: concurrent chunks then contend,
+        // tools/ab_hostio.py, r02)
+        st = softmax_core(c, xs, zs, ri, cols, row_off + r0, p, s0, 2);
         h->scr[cb] = c->scratch; h->scr_bytes[cb] = c->scratch_bytes;
         c->scratch = save_scr; c->scratch_bytes = save_bytes; c->stream = user;
         if (st) return st;
@@ -1857,39 +1859,56 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         a.nrtab = (MPC_SOFTMAX_NRTAB && !is_pair(c) && a.esmem && !p->recip.exp.clamp && !a.cone &&
                    nsteps <= MPC_NR_TAB_MAX_STEPS) ? 1 : 0;
         const i64 tab = a.nrtab ? (i64)nsteps * NR_TAB_F * 32 : 0;
-        // BOTH split form (kernels.cuh k_softmax_rest): the max tree as its own launch (k_max, 32-row
-        // tiles, the rebalanced w = 33 LTZ), then exp / row sums / reciprocal / product on row blocks
-        // that are all resident at once -- no tail wave of lone tiles
+        // BOTH split form: the max tree as its own launch (k_max on the balanced plan: one range of ~rows /
+        // grid rows per CTA, the rebalanced w = 33 LTZ), then exp / row sums / reciprocal / product
+        // (kernels.cuh k_softmax_rest) on row blocks that are all resident at once, compiled for 3 CTAs
+        // per SM: the fused kernel's 127 registers (the LTZ's) hold its exp phase to 16 warps per SM,
+        // where the standalone exp kernel (80 registers, 24 warps) runs at 0.77 of the ALU peak.  One
+        // timing record spans both launches.  MPC_SOFTMAX_SPLIT=0 / 1 in the environment (per call).
 #ifndef MPC_SOFTMAX_SPLIT
-#define MPC_SOFTMAX_SPLIT 0     // A/B: measured 2.6 % slower on cfg2 (0.268 vs 0.261 ms unflushed, r02)
+#define MPC_SOFTMAX_SPLIT 0
 #endif
-        if (MPC_SOFTMAX_SPLIT && !is_pair(c) && !a.causal && !a.bcast && !p->exp.clamp && !p->recip.exp.clamp &&
-            !a.cone && !wide && !(cols & 1) && (size_t)max_work_u64(cols) * 8 <= SMEM_LIMIT &&
-            nsteps <= MPC_NR_TAB_MAX_STEPS) {   // (k_max's tiles in shared memory: no scratch of its own)
-            static DevCache occ;
+        const char* split_env = getenv("MPC_SOFTMAX_SPLIT");
+        const int split = split_env ? atoi(split_env) : MPC_SOFTMAX_SPLIT;
+        if (split && !is_pair(c) && !a.causal && !a.bcast && !p->exp.clamp && !p->recip.exp.clamp &&
+            !a.cone && !wide && !(cols & 1) && nsteps <= MPC_NR_TAB_MAX_STEPS && rows >= 2) {
             const int tabw = nsteps * NR_TAB_F * 32;
-            const size_t dyn = sizeof(u64) * (size_t)smr_smem_u64(tabw);
+            static DevCache occ, occm;
             const int per_sm = dev_cached(occ, c->cfg.device, [&] {
                 cudaFuncSetAttribute(k_softmax_rest<BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
-                return occupancy(k_softmax_rest<BothA>, dyn, MPC_ROW_TPB);
+                return occupancy(k_softmax_rest<BothA>, sizeof(u64) * (size_t)smr_smem_u64(tabw, 1), MPC_ROW_TPB);
+            });
+            const int per_sm_m = dev_cached(occm, c->cfg.device, [&] {
+                cudaFuncSetAttribute(k_max<0, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                return occupancy(k_max<0, BothA>, 100 * 1024, MPC_ROW_TPB);
             });
             const i64 slots = (i64)c->sm_count * per_sm;
             i64 rb = (rows + slots - 1) / slots;
             rb = std::max<i64>(2, std::min<i64>(64, (rb + 1) / 2 * 2));
             const i64 nblk = (rows + rb - 1) / rb;
             const int grid = (int)std::min<i64>(nblk, slots);
-            // scratch: row maxima (2 x rows) then the per-CTA E tiles (k_max keeps its work tiles in smem)
-            u64* sc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * rows + (i64)grid * 2 * rb * cols));
-            if (!sc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
-            MaxArgs ma{a.s_max, a.w, a.x, SO{{sc, sc + rows}}, rows, cols, (u64)row_off, nullptr, 0, 0, nullptr, 0};
-            if ((st = launch_max(c, ma, rows, cols, a.w, "softmax"))) return st;
-            SmRestArgs ra{a.s_exp, a.s_rec, a.s_mul, a.ek, a.rk, a.x, SP{{sc, sc + rows}}, a.z, rows, cols, (u64)row_off,
-                          (int)rb, sc + 2 * rows, tabw};
-            rec_begin(c, "softmax", (u64)rows);
-            k_softmax_rest<BothA><<<grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, ra);
-            rec_end(c);
-            c->st.launches++;
-            return cuda_check(c, "softmax");
+            const int ntab = rb > 32 ? 2 : 1;
+            const size_t dyn = sizeof(u64) * (size_t)smr_smem_u64(tabw, ntab);
+            i64 gm = std::max<i64>(1, std::min<i64>((i64)c->sm_count * per_sm_m, rows / 2));
+            if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < gm) gm = g; }
+            const i64 tr = 2 * (((rows + 1) / 2 + gm - 1) / gm), wkm = max_work_u64(cols, tr);
+            if (tr <= 64 && wkm * 8 <= 100 * 1024) {
+                // scratch: row maxima (2 x rows) then the per-CTA E tiles
+                u64* sc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * rows + (i64)grid * 2 * rb * cols));
+                if (!sc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
+                MaxArgs ma{a.s_max, a.w, a.x, SO{{sc, sc + rows}}, rows, cols, (u64)row_off, nullptr, wkm, 1, nullptr, 0};
+                ma.tr = (int)tr;
+                cudaFuncSetAttribute(k_max<0, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wkm * 8));
+                cudaFuncSetAttribute(k_softmax_rest<BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+                SmRestArgs ra{a.s_exp, a.s_rec, a.s_mul, a.ek, a.rk, a.x, SP{{sc, sc + rows}}, a.z, rows, cols, (u64)row_off,
+                              (int)rb, sc + 2 * rows, tabw};
+                rec_begin(c, "softmax", (u64)rows);
+                k_max<0, BothA><<<(int)gm, MPC_ROW_TPB, wkm * 8, c->stream>>>(BothA{c->K}, ma);
+                k_softmax_rest<BothA><<<grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, ra);
+                rec_end(c);
+                c->st.launches += 2;
+                return cuda_check(c, "softmax");
+            }
         }
         a.bal = 0; a.tr = 32; a.tab_u64 = tab;
         // BOTH balanced plan (kernels.cuh softmax_bal_*): when the 32-row tiles need more than one round,
@@ -1908,6 +1927,7 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
             // 0.115; 8192: 0.172 vs 0.186, tools/ab_rows.py, r02) for more LTZ groups shared at range
             // boundaries; 1: only when the 32-row tiles need more than one round (the host-buffer chunks)
             const int bal_mode = bal_env ? atoi(bal_env) : bal_default;
+            if (bal_mode >= 3) grid = std::max<i64>(1, grid / 2);   // 3: one CTA per SM (concurrent chunks)
             if (bal_mode >= 2) grid = std::max<i64>(1, std::min<i64>(grid, rows / 2));
             const i64 hr = (rows + 1) / 2;
             const i64 tr = 2 * ((hr + grid - 1) / grid);
@@ -1929,6 +1949,31 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
                 rec_end(c);
                 c->st.launches++;
                 return cuda_check(c, "softmax");
+            }
+        }
+        // PAIR modes: the same balanced plan on min(CTAs, rows / 2) CTAs.  The ranges, groups and the
+        // exchange sequence of CTA c depend only on (rows, grid), so party 0's CTA c, party 1's and the
+        // dealer's pass run the same rows.  MPC_SOFTMAX_BAL_PAIR=0: off (A/B; per call)
+        const char* balp_env = getenv("MPC_SOFTMAX_BAL_PAIR");
+        if (is_pair(c) && !(balp_env && atoi(balp_env) == 0) && !(bal_env && atoi(bal_env) == 0) && !wide && !a.cone &&
+            !a.bcast && !p->exp.clamp && !p->recip.exp.clamp) {
+            const auto kk = a.causal ? kroles(k_softmax<0, PairA, true>, k_softmax<0, PairAS, true>)
+                                     : kroles(k_softmax<0, PairA>, k_softmax<0, PairAS>);
+            set_smem_attr(kk, 100 * 1024);
+            i64 G = pair_ctas(c, kk, 100 * 1024, std::max<i64>(1, rows / 2), MPC_ROW_TPB);
+            if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < G) G = g; }
+            const i64 hr = (rows + 1) / 2, tr = 2 * ((hr + G - 1) / G);
+            const i64 wkb = softmax_bal_work_u64(cols, tr, 0);
+            if (tr <= 64 && wkb * 8 <= 100 * 1024) {
+                a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 1; a.nrtab = 0; a.tab_u64 = 0;
+                a.gscratch = nullptr; a.work_u64 = wkb;
+                const i64 launched = G * (is_loop(c) ? 2 : 1);
+                u64* esc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * tr * cols * launched));
+                if (!esc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
+                a.escratch = esc;
+                const size_t dyn = sizeof(u64) * (size_t)wkb;
+                set_smem_attr(kk, (int)dyn);
+                return launch_pair_kernel_tpb(c, kk, (int)G, dyn, MPC_ROW_TPB, "softmax", a);
             }
         }
         const i64 wk = softmax_work_u64(cols, a.esmem != 0, tab), ek = a.esmem ? 0 : 64 * cols;

@@ -271,3 +271,74 @@ def test_layernorm_blocks_equal_fused(m, monkeypatch, rows, cols):
     b = c.layernorm(gx, rows, cols)
     torch.cuda.synchronize()
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+# ---- balanced softmax plan in the PAIR protocol (loopback) and with the dealer's stream ----
+@pytest.mark.parametrize("rows,cap,cols", [(150, 4, 128), (1000, 16, 128), (255, 5, 77), (64, 0, 128),
+                                           (12288, 0, 128)])
+def test_softmax_balanced_pair_loopback(m, monkeypatch, rows, cap, cols):
+    """both parties' CTA c run the same row range and exchange sequence: bit-identical to BOTH"""
+    if cap:
+        monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    keys = workloads.keys(2)
+    b = m.Ctx.for_cfg(keys)
+    p = m.Ctx.for_cfg(keys, mode=m.binding.MODE_PAIR_LOOPBACK)
+    b.set_step(23)
+    p.set_step(23)
+    x = b.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    p.set_step(b.step)
+    zb = b.softmax(x, rows, cols, row_off=32)
+    zp = p.softmax(x, rows, cols, row_off=32)
+    p.sync()
+    torch.cuda.synchronize()
+    assert torch.equal(zb[0], zp[0]) and torch.equal(zb[1], zp[1])
+    if rows <= 1000:
+        o = Oracle.for_cfg(keys, 23)
+        ox = o.share(workloads.softmax_inputs(rows, cols))
+        same(zp, o.softmax(ox, rows, cols, row_off=32))
+
+
+@pytest.mark.parametrize("rows,cap", [(150, 4), (1000, 16)])
+def test_softmax_balanced_dealer_stream(m, monkeypatch, rows, cap):
+    """the dealer's offline pass runs party 1's balanced kernel with the same grid: party 1 consumes
+    exactly the stream and the shares equal BOTH's"""
+    monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    cols = 128
+    keys = workloads.keys(2)
+    b = m.Ctx.for_cfg(keys)
+    p = m.Ctx.for_cfg(keys, mode=m.binding.MODE_PAIR_LOOPBACK)
+    d = m.Ctx.dealer(keys, target=m.binding.MODE_PAIR_LOOPBACK)
+    for c in (b, p, d):
+        c.set_step(5)
+    xs = b.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    p.set_step(b.step)
+    d.set_step(b.step)
+    zb = b.softmax(xs, rows, cols)
+    d.softmax(m.Ctx.like(rows * cols), rows, cols)
+    p.set_corrections(d.dealer_stream())
+    zp = p.softmax(xs, rows, cols)
+    p.sync()
+    assert p.corrections_left() == 0
+    torch.cuda.synchronize()
+    assert torch.equal(zb[0], zp[0]) and torch.equal(zb[1], zp[1])
+
+
+# ---- split softmax: balanced k_max launch + k_softmax_rest (3 CTAs per SM); MPC_SOFTMAX_SPLIT=1 ----
+@pytest.mark.parametrize("rows,cap,cols", [(150, 4, 128), (1000, 0, 128), (255, 5, 78), (12288, 0, 128), (64, 0, 2)])
+def test_softmax_split(m, monkeypatch, rows, cap, cols):
+    monkeypatch.setenv("MPC_SOFTMAX_SPLIT", "1")
+    if cap:
+        monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    c, o = ctx(m, 2, 25)
+    x = workloads.softmax_inputs(rows, cols)
+    gx = c.share(torch.from_numpy(x).cuda())
+    s0 = c.step
+    a = c.softmax(gx, rows, cols, row_off=32)
+    monkeypatch.setenv("MPC_SOFTMAX_SPLIT", "0")
+    c.set_step(s0, force=True)
+    b = c.softmax(gx, rows, cols, row_off=32)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    if rows <= 1000:
+        ox = o.share(x)
+        same(a, o.softmax(ox, rows, cols, row_off=32))

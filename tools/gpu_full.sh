@@ -6,3 +6,4 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${tag}_smoke.log
 python bench.py > gpurun_out/${tag}_bench_n1.json 2> gpurun_out/${tag}_bench_n1.err; echo "bench rc=$?"
 python bench.py --impl reference > gpurun_out/${tag}_bench_reference.json 2> gpurun_out/${tag}_bench_reference.err; echo "ref rc=$?"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${tag}_launches.csv python bench.py --steps 2 --warmup 1 > gpurun_out/${tag}_ncu_bench.log 2>&1; echo "ncu rc=$?"
+python tools/sweep.py --out gpurun_out/${tag}_sweep.json > gpurun_out/${tag}_sweep.txt 2>&1; echo "sweep rc=$?"
