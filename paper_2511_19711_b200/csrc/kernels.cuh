@@ -672,14 +672,15 @@ __device__ __forceinline__ void prefetch_rows(SP x, i64 r0n, i64 rows, i64 C)
 // the element's share.  brs: 3 x 32 u64 of shared / per-CTA scratch (b0, b1, f per row).
 template <class P, class Val>
 __device__ __forceinline__ void tile_bcast_mul(P& pr, u32 s, int R, i64 C, u64 g0, const FastDiv& dC,
-                                               SP Rr, SO zt, u64* brs, Val val)
+                                               SP Rr, SO zt, u64* brs, Val val, int BS = 32)
 {
     using S = typename P::S;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
-    if (warp == 0) {
-        const S y = lane < R ? pr.ld(Rr, lane) : pr.zero();
-        const BRow b = pr.bmb_row(g0 + (u64)lane, s, y);
-        brs[lane] = b.b0; brs[32 + lane] = b.b1; brs[64 + lane] = b.f;
+    if (warp == 0 || 32 * warp < R) {                   // BS > 32 (balanced plan): warp w < ceil(R / 32)
+        const int row = (int)threadIdx.x;
+        const S y = row < R ? pr.ld(Rr, row) : pr.zero();
+        const BRow b = pr.bmb_row(g0 + (u64)row, s, y);
+        if (row < BS) { brs[row] = b.b0; brs[BS + row] = b.b1; brs[2 * BS + row] = b.f; }
     }
     __syncthreads();
     const i64 ne = (i64)R * C;
@@ -690,7 +691,7 @@ __device__ __forceinline__ void tile_bcast_mul(P& pr, u32 s, int R, i64 C, u64 g
         int ra = 0, rb = 0;
         if (e < ne) { ra = (int)fdiv((u32)e, dC); xa = val(e, ra); }
         if (e + 1 < ne) { rb = (int)fdiv((u32)(e + 1), dC); xb = val(e + 1, rb); }
-        const BRow b0{brs[ra], brs[32 + ra], brs[64 + ra]}, b1{brs[rb], brs[32 + rb], brs[64 + rb]};
+        const BRow b0{brs[ra], brs[BS + ra], brs[2 * BS + ra]}, b1{brs[rb], brs[BS + rb], brs[2 * BS + rb]};
         S za, zb;
         pr.bmb2(ub + (u64)e, s, xa, xb, b0, b1, za, zb);
         if (e < ne) pr.st(zt, e, pr.shr_(za, FRAC));
@@ -736,7 +737,7 @@ __host__ __device__ inline i64 softmax_bal_x_off(i64 cols, i64 tr, i64 tab_u64)
 }
 __host__ __device__ inline i64 softmax_bal_work_u64(i64 cols, i64 tr, i64 tab_u64)
 {
-    return softmax_bal_x_off(cols, tr, tab_u64) + 6 * tr;
+    return softmax_bal_x_off(cols, tr, tab_u64) + 9 * tr;        // X: MX S R (6 tr), broadcast rows (3 tr)
 }
 
 // work tile (u64 words), HA = ceil(cols/2), HB = ceil(HA/2): A0 A1 (2 x 32HA), B0 B1 (2 x 32HB),
@@ -896,7 +897,7 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         const SP Rc{{RR.p[0], RR.p[1]}};
         const SO zt{{a.z.p[0] ? a.z.p[0] + r0 * C : nullptr, a.z.p[1] ? a.z.p[1] + r0 * C : nullptr}};
         if (a.bcast) {
-            tile_bcast_mul(pr, a.s_mul, R, C, g0, dC, Rc, zt, X + 192, [&](i64 e, int) { return pr.ld(Ec, e); });
+            tile_bcast_mul(pr, a.s_mul, R, C, g0, dC, Rc, zt, X + 6 * TR, [&](i64 e, int) { return pr.ld(Ec, e); }, (int)TR);
         } else if (!(MPC_SOFTMAX_SKIP & 8)) {
             constexpr int V = decltype(pr)::kV;
             for (i64 base = (i64)warp * 32 * V; base < (ne + 1) / 2; base += (i64)NW * 32 * V) {

@@ -1914,12 +1914,22 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         // BOTH balanced plan (kernels.cuh softmax_bal_*): when the 32-row tiles need more than one round,
         // ONE row range of ~rows / grid rows per CTA, every CTA resident at once
         const char* bal_env = getenv("MPC_SOFTMAX_BAL");      // 0: off (A/B, tests; read per call)
-        if (!(bal_env && atoi(bal_env) == 0) && !is_pair(c) && !wide && !a.cone && !a.bcast && !p->exp.clamp && !p->recip.exp.clamp && a.nrtab) {
-            static DevCache occb;
-            const int per_sm = dev_cached(occb, c->cfg.device, [] {
+        // (the carry cone too, w <= 33: its 16 KB of static shared memory beside the 74 KB work area still
+        // leaves two CTAs per SM; the triple tables alias the level buffers, so no esmem condition)
+        const bool bal_tab = !p->recip.exp.clamp && nsteps <= MPC_NR_TAB_MAX_STEPS;
+        // (a clamped exp's LTZ groups are element groups from g0 cols: whole groups iff 32 | g0 cols, and the
+        // plan's g0 are even, so cols % 16 == 0)
+        if (!(bal_env && atoi(bal_env) == 0) && !is_pair(c) && !wide && (!p->exp.clamp || cols % 16 == 0) && bal_tab &&
+            cols <= 192) {
+            static DevCache occb, occc;
+            const int per_sm = a.cone ? dev_cached(occc, c->cfg.device, [] {
+                cudaFuncSetAttribute(k_softmax<2, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                return occupancy(k_softmax<2, BothA>, 80 * 1024, MPC_ROW_TPB);
+            }) : dev_cached(occb, c->cfg.device, [] {
                 cudaFuncSetAttribute(k_softmax<0, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
                 return occupancy(k_softmax<0, BothA>, 100 * 1024, MPC_ROW_TPB);
             });
+            const i64 tab = (i64)nsteps * NR_TAB_F * 32;
             i64 grid = (i64)c->sm_count * per_sm;
             if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < grid) grid = g; }
             // 2 (default): always, on min(grid, rows / 2) CTAs (>= 2 rows each) -- fewer rows per CTA
@@ -1933,19 +1943,19 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
             const i64 tr = 2 * ((hr + grid - 1) / grid);
             const i64 wkb = softmax_bal_work_u64(cols, tr, tab);
             const bool want = bal_mode >= 2 ? true : rows > 32 * grid;
-            if (want && tr <= 64 && wkb * 8 <= 100 * 1024) {
-                a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 1;
+            if (want && tr <= 64 && wkb * 8 <= (a.cone ? 80 : 100) * 1024) {
+                a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 1; a.nrtab = 1; a.tab_u64 = tab;
                 a.gscratch = nullptr; a.work_u64 = wkb;
                 u64* esc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * tr * cols * grid));
                 if (!esc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
                 a.escratch = esc;
                 const size_t dyn = sizeof(u64) * (size_t)wkb;
                 // every launch: launch_rows sets the same kernels' attribute to other tiles' sizes
-                cudaFuncSetAttribute(a.causal ? k_softmax<0, BothA, true> : k_softmax<0, BothA>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+                auto kb = a.cone ? (a.causal ? k_softmax<2, BothA, true> : k_softmax<2, BothA>)
+                                 : (a.causal ? k_softmax<0, BothA, true> : k_softmax<0, BothA>);
+                cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
                 rec_begin(c, "softmax", (u64)rows);
-                if (a.causal) k_softmax<0, BothA, true><<<(int)grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, a);
-                else k_softmax<0, BothA><<<(int)grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, a);
+                kb<<<(int)grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, a);
                 rec_end(c);
                 c->st.launches++;
                 return cuda_check(c, "softmax");
@@ -1956,7 +1966,7 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         // dealer's pass run the same rows.  MPC_SOFTMAX_BAL_PAIR=0: off (A/B; per call)
         const char* balp_env = getenv("MPC_SOFTMAX_BAL_PAIR");
         if (is_pair(c) && !(balp_env && atoi(balp_env) == 0) && !(bal_env && atoi(bal_env) == 0) && !wide && !a.cone &&
-            !a.bcast && !p->exp.clamp && !p->recip.exp.clamp) {
+            (!p->exp.clamp || cols % 16 == 0) && !p->recip.exp.clamp) {
             const auto kk = a.causal ? kroles(k_softmax<0, PairA, true>, k_softmax<0, PairAS, true>)
                                      : kroles(k_softmax<0, PairA>, k_softmax<0, PairAS>);
             set_smem_attr(kk, 100 * 1024);

@@ -136,12 +136,14 @@ def test_softmax_balanced(m, monkeypatch, rows, cap, cols):
 
 
 @pytest.mark.parametrize("rows,cap", [(150, 4), (255, 5)])
-@pytest.mark.parametrize("kw", [dict(causal=1), dict(exp_square=1, recip_square=1), dict(recip_iters=3, exp_t=4)])
+@pytest.mark.parametrize("kw", [dict(causal=1), dict(exp_square=1, recip_square=1), dict(recip_iters=3, exp_t=4),
+                                dict(bcast=1), dict(bcast=1, exp_square=1, recip_square=1, causal=1),
+                                dict(exp_clamp=1), dict(exp_clamp=1, causal=1)])
 def test_softmax_balanced_knobs(m, monkeypatch, rows, cap, kw):
     monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
     cols = 64
     c, o = ctx(m, 2, 15)
-    x = workloads.softmax_inputs(rows, cols)
+    x = workloads.softmax_inputs(rows, cols, spike="exp_clamp" in kw)
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
     same(c.softmax(gx, rows, cols, row_off=32, **kw), o.softmax(ox, rows, cols, row_off=32, **kw))
 
@@ -276,7 +278,8 @@ def test_layernorm_blocks_equal_fused(m, monkeypatch, rows, cols):
 # ---- balanced softmax plan in the PAIR protocol (loopback) and with the dealer's stream ----
 @pytest.mark.parametrize("rows,cap,cols", [(150, 4, 128), (1000, 16, 128), (255, 5, 77), (64, 0, 128),
                                            (12288, 0, 128)])
-def test_softmax_balanced_pair_loopback(m, monkeypatch, rows, cap, cols):
+@pytest.mark.parametrize("bcast", [0, 1])
+def test_softmax_balanced_pair_loopback(m, monkeypatch, rows, cap, cols, bcast):
     """both parties' CTA c run the same row range and exchange sequence: bit-identical to BOTH"""
     if cap:
         monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
@@ -287,15 +290,15 @@ def test_softmax_balanced_pair_loopback(m, monkeypatch, rows, cap, cols):
     p.set_step(23)
     x = b.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
     p.set_step(b.step)
-    zb = b.softmax(x, rows, cols, row_off=32)
-    zp = p.softmax(x, rows, cols, row_off=32)
+    zb = b.softmax(x, rows, cols, row_off=32, bcast=bcast)
+    zp = p.softmax(x, rows, cols, row_off=32, bcast=bcast)
     p.sync()
     torch.cuda.synchronize()
     assert torch.equal(zb[0], zp[0]) and torch.equal(zb[1], zp[1])
     if rows <= 1000:
         o = Oracle.for_cfg(keys, 23)
         ox = o.share(workloads.softmax_inputs(rows, cols))
-        same(zp, o.softmax(ox, rows, cols, row_off=32))
+        same(zp, o.softmax(ox, rows, cols, row_off=32, bcast=bcast))
 
 
 @pytest.mark.parametrize("rows,cap", [(150, 4), (1000, 16)])
@@ -342,3 +345,16 @@ def test_softmax_split(m, monkeypatch, rows, cap, cols):
     if rows <= 1000:
         ox = o.share(x)
         same(a, o.softmax(ox, rows, cols, row_off=32))
+
+
+@pytest.mark.parametrize("rows,cap,cols", [(150, 4, 128), (1000, 16, 128), (255, 5, 77), (96, 0, 64)])
+@pytest.mark.parametrize("causal", [0, 1])
+def test_softmax_balanced_cone(m, monkeypatch, rows, cap, cols, causal):
+    """the carry-cone max tree (NEXT #1) on the balanced plan: groups offset at range boundaries"""
+    if cap:
+        monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    c, o = ctx(m, 2, 27)
+    c.set_ltz_circuit(1)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols, row_off=32, causal=causal), o.softmax(ox, rows, cols, row_off=32, causal=causal))

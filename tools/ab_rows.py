@@ -39,5 +39,5 @@ out.append(f"hostio {t(hio):.4f}")
 print("MPC_SOFTMAX_BAL=" + os.environ.get("MPC_SOFTMAX_BAL", "1"), " | ".join(out), flush=True)
 '''
 for rep in range(2):
-    for v in ("1", "2"):
+    for v in ("2",):
         subprocess.run([sys.executable, "-c", code], env=dict(os.environ, MPC_SOFTMAX_BAL=v), check=True)
