@@ -1930,7 +1930,22 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
                 return occupancy(k_softmax<0, BothA>, 100 * 1024, MPC_ROW_TPB);
             });
             const i64 tab = (i64)nsteps * NR_TAB_F * 32;
-            i64 grid = (i64)c->sm_count * per_sm;
+            // CTAs per SM: the most whose work areas fit (the query above assumed 100 KB each)
+            int ps = per_sm;
+            {
+                auto kq = a.cone ? k_softmax<2, BothA> : k_softmax<0, BothA>;
+                static DevCache occr0, occr2;                  // register / thread limit (no shared memory)
+                const int ps_max = dev_cached(a.cone ? occr2 : occr0, c->cfg.device, [&] { return occupancy(kq, 0, MPC_ROW_TPB); });
+                for (int k = ps_max; k > per_sm; --k) {
+                    const i64 g = (i64)c->sm_count * k, t = 2 * (((rows + 1) / 2 + g - 1) / g);
+                    const size_t d = sizeof(u64) * (size_t)softmax_bal_work_u64(cols, t, (i64)nsteps * NR_TAB_F * 32);
+                    if (d <= 100 * 1024) {
+                        cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d);
+                        if (occupancy(kq, d, MPC_ROW_TPB) >= k) { ps = k; break; }
+                    }
+                }
+            }
+            i64 grid = (i64)c->sm_count * ps;
             if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int g = atoi(cap); if (g > 0 && g < grid) grid = g; }
             // 2 (default): always, on min(grid, rows / 2) CTAs (>= 2 rows each) -- fewer rows per CTA
             // means a shorter critical path (1024 rows: 0.050 vs 0.113 ms on 32 tiles; 3072: 0.089 vs
