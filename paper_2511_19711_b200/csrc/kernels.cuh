@@ -575,11 +575,12 @@ __host__ __device__ inline int nr_tab_steps(int kind, int t, int iters) { return
 #define MPC_NR_TAB_MAX_STEPS 32                       // 32 steps x 32 rows x 5 words = 40 KB of shared memory
 #endif
 template <int KIND>
-__device__ __forceinline__ void nr_pregen(const Keys& K, u32 s, const NrK& p, u64 g0, u64* T)
+__device__ __forceinline__ void nr_pregen(const Keys& K, u32 s, const NrK& p, u64 g0, u64* T, int nrows = 32)
 {
-    const int t = p.exp.t, ns = nr_tab_steps(KIND, t, p.iters);
-    for (int it = threadIdx.x; it < ns * 16; it += blockDim.x) {
-        const int j = it >> 4, l = 2 * (it & 15);
+    // the table's first nrows rows (unit pairs; the chain reads rows < R only)
+    const int t = p.exp.t, ns = nr_tab_steps(KIND, t, p.iters), np = (min(nrows, 32) + 1) / 2;
+    for (int it = threadIdx.x; it < ns * np; it += blockDim.x) {
+        const int j = it / np, l = 2 * (it - j * np);
         const u64 u = g0 + (u64)l;                    // even (g0 is a multiple of 32)
         const u32 sj = s + (u32)j;
         u64* R = T + (i64)j * NR_TAB_F * 32 + l;
@@ -809,8 +810,8 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         // only opens and multiplies); the exp phase's closing barrier orders it before the chain
         if constexpr (!decltype(pr)::kPair)
             if (nrt) {
-                nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0, nrt);
-                if (R > 32) nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0 + 32, nrt + a.tab_u64);
+                nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0, nrt, R);
+                if (R > 32) nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0 + 32, nrt + a.tab_u64, R - 32);
             }
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
