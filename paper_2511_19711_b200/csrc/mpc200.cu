@@ -2077,8 +2077,10 @@ mpc_status mpc_layernorm(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t rows, i
         // largest RB in {8, 4, 2, 1} whose two buffers fit 96 KB.  MPC_LN_BLK=0: off (A/B; per call)
         const char* lnb_env = getenv("MPC_LN_BLK");
         int lnb_rb = 0;
+        // (cp.async.bulk needs 16-byte aligned sources: both share arrays' bases, cols even)
+        const bool al16x = ((uintptr_t)a.x.p[0] % 16 == 0) && ((uintptr_t)a.x.p[1] % 16 == 0);
         if (!(lnb_env && atoi(lnb_env) == 0) && !is_pair(c) && !p->rsqrt.exp.clamp && !p->bcast && !(cols & 1) &&
-            nsteps_rs <= MPC_NR_TAB_MAX_STEPS)
+            nsteps_rs <= MPC_NR_TAB_MAX_STEPS && al16x)
             for (int rb = 8; rb >= 1 && !lnb_rb; rb /= 2)
                 if (lnb_smem_bytes(cols, rb) <= 96 * 1024) lnb_rb = rb;
         if (lnb_rb) {

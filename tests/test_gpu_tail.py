@@ -358,3 +358,17 @@ def test_softmax_balanced_cone(m, monkeypatch, rows, cap, cols, causal):
     x = workloads.softmax_inputs(rows, cols)
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
     same(c.softmax(gx, rows, cols, row_off=32, causal=causal), o.softmax(ox, rows, cols, row_off=32, causal=causal))
+
+
+def test_layernorm_unaligned_shares(m):
+    """share arrays that start 8 bytes past a 16-byte boundary (cp.async.bulk cannot read them): the
+    row-block kernel is not taken, the result is still the oracle's"""
+    rows, cols = 33, 768
+    c, o = ctx(m, 5, 30)
+    x = workloads.layernorm_inputs(rows, cols)
+    gx = c.share(torch.from_numpy(np.concatenate([[0.0], x.ravel()])).cuda())
+    gv = (gx[0][1:], gx[1][1:])
+    assert gv[0].data_ptr() % 16 == 8
+    ov = (o.share(np.concatenate([[0.0], x.ravel()])))
+    ox = (ov[0][1:], ov[1][1:])
+    same(c.layernorm(gv, rows, cols), o.layernorm(ox, rows, cols))
