@@ -1,10 +1,15 @@
-"""Row kernels' tail as 16-row half tiles (kernels.cuh tile_plan): when the last round
-of 32-row tiles would leave P = ntiles mod ncta tiles with 2P <= ncta, those P tiles run as 2P half
-tiles of 16 rows.  A half tile starts at a row = 16 mod 32, so the max tree's levels whose LTZ groups
-span 32 rows evaluate a group with half its lanes outside the tile.  The contract (steps, units,
-PRG words) does not depend on the tiling: every share must equal the oracle's.  MPC_ROW_GRID_CAP
-caps the grid so that small inputs take the multi-round and half-tile paths; the half tiles are
-off by default (measured slower) and MPC_TAIL_HALF=1 turns them on per call."""
+"""Row-kernel plans and LayerNorm kernels, every share against the oracle (or the other plan on the
+same call).  Covered here:
+* the 32-row tiles' last round as 16-row half tiles (kernels.cuh tile_plan; off by default, measured
+  slower -- MPC_TAIL_HALF=1 turns it on per call);
+* the balanced softmax plan (softmax_bal_*: one range of ~rows / grid rows per CTA, any row alignment
+  in the max tree) in BOTH, with the carry cone, the broadcast triple, a clamped exp, causal rows,
+  in the PAIR protocol (loopback) and with the dealer's correction stream;
+* the split softmax (balanced k_max + k_softmax_rest; MPC_SOFTMAX_SPLIT=1, A/B path);
+* LayerNorm: k_ln_row (one warp per row), k_ln_blk (shared-memory row blocks by bulk copies) and
+  k_ln_fused on the same calls.
+The contract (steps, units, PRG words) does not depend on the plan.  MPC_ROW_GRID_CAP caps the grid
+so that small inputs take the multi-round, half-tile and multi-block paths."""
 import numpy as np
 import pytest
 
