@@ -781,7 +781,9 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     SO E{{Ew, Ew + TR * C}};
     u64* X = W + (a.bal ? softmax_bal_x_off(C, TR, a.tab_u64) : softmax_x_off(C, a.esmem != 0));
     SO MX{{X, X + TR}}, SS{{X + 2 * TR, X + 3 * TR}}, RR{{X + 4 * TR, X + 5 * TR}};
-    u64* const nrt = a.nrtab ? (a.bal ? W : X + 9 * 32) : nullptr;
+    // balanced plan: the triple tables alias the dead level buffers in shared memory, or (global work
+    // area, wide rows) are the dynamic shared memory itself
+    u64* const nrt = a.nrtab ? (a.bal ? (a.use_smem ? W : smem) : X + 9 * 32) : nullptr;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const TilePlan tp = tile_plan(a.rows, ncta, a.half);
     const FastDiv dC = make_fastdiv((u32)C);
@@ -809,10 +811,9 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
         // BOTH: every warp generates the reciprocal chain's triples now (tile_nr's warp-0 chain then
         // only opens and multiplies); the exp phase's closing barrier orders it before the chain
         if constexpr (!decltype(pr)::kPair)
-            if (nrt) {
-                nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0, nrt, R);
-                if (R > 32) nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0 + 32, nrt + a.tab_u64, R - 32);
-            }
+            if (nrt)                                              // one 32-row table per 32 rows (<= 3)
+                for (int t = 0; 32 * t < R; ++t)
+                    nr_pregen<0>(*pr.Kp, a.s_rec, a.rk, g0 + 32u * (u64)t, nrt + t * a.tab_u64, R - 32 * t);
         // 2-3. e = EXP(x - m), element units g0*C + e
         const i64 ne = (i64)R * C;
         const u64 ub = g0 * (u64)C;

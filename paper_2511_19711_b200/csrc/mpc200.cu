@@ -1919,8 +1919,12 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
         const bool bal_tab = !p->recip.exp.clamp && nsteps <= MPC_NR_TAB_MAX_STEPS;
         // (a clamped exp's LTZ groups are element groups from g0 cols: whole groups iff 32 | g0 cols, and the
         // plan's g0 are even, so cols % 16 == 0)
+        // Rows whose level buffers do not fit shared memory (cols > 192, e.g. GPT-2's 1024) keep them in a
+        // per-CTA global work area (L2) and only the two triple tables in shared memory ("gwork").
+        const char* balw_env = getenv("MPC_SOFTMAX_BAL_WIDE");
+        const bool gwork_ok = !(balw_env && atoi(balw_env) == 0);
         if (!(bal_env && atoi(bal_env) == 0) && !is_pair(c) && !wide && (!p->exp.clamp || cols % 16 == 0) && bal_tab &&
-            cols <= 192) {
+            (cols <= 192 || gwork_ok)) {
             static DevCache occb, occc;
             const int per_sm = a.cone ? dev_cached(occc, c->cfg.device, [] {
                 cudaFuncSetAttribute(k_softmax<2, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
@@ -1958,7 +1962,29 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
             const i64 tr = 2 * ((hr + grid - 1) / grid);
             const i64 wkb = softmax_bal_work_u64(cols, tr, tab);
             const bool want = bal_mode >= 2 ? true : rows > 32 * grid;
-            if (want && tr <= 64 && wkb * 8 <= (a.cone ? 80 : 100) * 1024) {
+            // (up to 96 rows per CTA here: three 32-row tables, 107 KB of shared memory -- the 24576-row
+            // GPT-2 shard of a pair has 84 rows per CTA)
+            const i64 ntab = (tr + 31) / 32;
+            const bool gwork = cols > 192 && gwork_ok && ntab * tab * 8 <= (a.cone ? 80 : 110) * 1024;
+            if (want && tr <= 96 && gwork) {
+                a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 0; a.nrtab = 1; a.tab_u64 = tab;
+                a.work_u64 = wkb;
+                // scratch: [E tiles: 2 tr cols per CTA] [work areas: wkb per CTA]
+                u64* esc = (u64*)scratch(c, sizeof(u64) * (size_t)((2 * tr * cols + wkb) * grid));
+                if (!esc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
+                a.escratch = esc;
+                a.gscratch = esc + (size_t)(2 * tr * cols) * (size_t)grid;
+                const size_t dyn = sizeof(u64) * (size_t)(ntab * tab);
+                auto kb = a.cone ? (a.causal ? k_softmax<2, BothA, true> : k_softmax<2, BothA>)
+                                 : (a.causal ? k_softmax<0, BothA, true> : k_softmax<0, BothA>);
+                cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+                rec_begin(c, "softmax", (u64)rows);
+                kb<<<(int)grid, MPC_ROW_TPB, dyn, c->stream>>>(BothA{c->K}, a);
+                rec_end(c);
+                c->st.launches++;
+                return cuda_check(c, "softmax");
+            }
+            if (want && tr <= 64 && cols <= 192 && wkb * 8 <= (a.cone ? 80 : 100) * 1024) {
                 a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 1; a.nrtab = 1; a.tab_u64 = tab;
                 a.gscratch = nullptr; a.work_u64 = wkb;
                 u64* esc = (u64*)scratch(c, sizeof(u64) * (size_t)(2 * tr * cols * grid));

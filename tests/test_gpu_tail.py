@@ -377,3 +377,31 @@ def test_layernorm_unaligned_shares(m):
     ov = (o.share(np.concatenate([[0.0], x.ravel()])))
     ox = (ov[0][1:], ov[1][1:])
     same(c.layernorm(gv, rows, cols), o.layernorm(ox, rows, cols))
+
+
+@pytest.mark.parametrize("rows,cap,cols", [(150, 4, 1024), (300, 0, 1024), (255, 5, 300), (64, 0, 200),
+                                           (340, 4, 1024), (370, 4, 256)])
+@pytest.mark.parametrize("kw", [dict(), dict(causal=1), dict(bcast=1)])
+def test_softmax_balanced_wide_rows(m, monkeypatch, rows, cap, cols, kw):
+    """rows wider than the shared-memory work area (cols > 192): the balanced plan with its level
+    buffers in a per-CTA global work area and the triple tables in shared memory (340 / 370 rows on 4
+    CTAs: 86 / 94 rows per CTA, three tables and three reciprocal-chain warps)"""
+    if cap:
+        monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    c, o = ctx(m, 2, 29)
+    x = workloads.softmax_inputs(rows, cols)
+    gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
+    same(c.softmax(gx, rows, cols, row_off=64, **kw), o.softmax(ox, rows, cols, row_off=64, **kw))
+
+
+def test_softmax_balanced_wide_equals_tiles(m, monkeypatch):
+    rows, cols = 2000, 1024
+    c, _ = ctx(m, 2, 31)
+    gx = c.share(torch.from_numpy(workloads.softmax_inputs(rows, cols)).cuda())
+    s0 = c.step
+    a = c.softmax(gx, rows, cols)
+    monkeypatch.setenv("MPC_SOFTMAX_BAL_WIDE", "0")
+    c.set_step(s0, force=True)
+    b = c.softmax(gx, rows, cols)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
