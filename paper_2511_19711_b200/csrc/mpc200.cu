@@ -2026,6 +2026,19 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
                 set_smem_attr(kk, (int)dyn);
                 return launch_pair_kernel_tpb(c, kk, (int)G, dyn, MPC_ROW_TPB, "softmax", a);
             }
+            // the level buffers in a per-CTA global work area when they do not fit (loopback's half grid at
+            // cfg2: 84 rows per CTA; wide rows); no triple tables in PAIR, so up to 96 rows per CTA
+            const char* balw = getenv("MPC_SOFTMAX_BAL_WIDE");
+            if (tr <= 96 && !(balw && atoi(balw) == 0)) {
+                a.bal = 1; a.tr = (int)tr; a.esmem = 0; a.use_smem = 0; a.nrtab = 0; a.tab_u64 = 0;
+                a.work_u64 = wkb;
+                const i64 launched = G * (is_loop(c) ? 2 : 1);
+                u64* esc = (u64*)scratch(c, sizeof(u64) * (size_t)((2 * tr * cols + wkb) * launched));
+                if (!esc) return fail(c, MPC_ERR_NOMEM, "softmax scratch");
+                a.escratch = esc;
+                a.gscratch = esc + (size_t)(2 * tr * cols) * (size_t)launched;
+                return launch_pair_kernel_tpb(c, kk, (int)G, 0, MPC_ROW_TPB, "softmax", a);
+            }
         }
         const i64 wk = softmax_work_u64(cols, a.esmem != 0, tab), ek = a.esmem ? 0 : 64 * cols;
         const size_t lim = a.esmem ? 100 * 1024 + (size_t)tab * 8 : SMEM_LIMIT;

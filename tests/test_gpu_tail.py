@@ -282,7 +282,7 @@ def test_layernorm_blocks_equal_fused(m, monkeypatch, rows, cols):
 
 # ---- balanced softmax plan in the PAIR protocol (loopback) and with the dealer's stream ----
 @pytest.mark.parametrize("rows,cap,cols", [(150, 4, 128), (1000, 16, 128), (255, 5, 77), (64, 0, 128),
-                                           (12288, 0, 128)])
+                                           (12288, 0, 128), (340, 4, 128), (150, 4, 1024)])
 @pytest.mark.parametrize("bcast", [0, 1])
 def test_softmax_balanced_pair_loopback(m, monkeypatch, rows, cap, cols, bcast):
     """both parties' CTA c run the same row range and exchange sequence: bit-identical to BOTH"""
@@ -306,7 +306,7 @@ def test_softmax_balanced_pair_loopback(m, monkeypatch, rows, cap, cols, bcast):
         same(zp, o.softmax(ox, rows, cols, row_off=32, bcast=bcast))
 
 
-@pytest.mark.parametrize("rows,cap", [(150, 4), (1000, 16)])
+@pytest.mark.parametrize("rows,cap", [(150, 4), (1000, 16), (340, 4)])
 def test_softmax_balanced_dealer_stream(m, monkeypatch, rows, cap):
     """the dealer's offline pass runs party 1's balanced kernel with the same grid: party 1 consumes
     exactly the stream and the shares equal BOTH's"""
