@@ -599,6 +599,28 @@ static mpc_status launch_rows(mpc_ctx* c, KB kb, KP kp, Args& a, i64 rows, i64 w
 
 static mpc_status launch_max(mpc_ctx* c, MaxArgs& a, i64 rows, i64 cols, int w, const char* name)
 {
+    // BOTH, Kogge-Stone w <= 33: the softmax's balanced plan (one range of ~rows / grid rows per CTA, on
+    // min(grid, rows / 2) CTAs) when the level buffers fit shared memory; MPC_MAX_BAL=0: off (per call)
+    const char* mb_env = getenv("MPC_MAX_BAL");
+    if (!is_pair(c) && !a.cone && w <= 33 && !(mb_env && atoi(mb_env) == 0) && rows >= 2) {
+        static DevCache occ;
+        const int per_sm = dev_cached(occ, c->cfg.device, [] {
+            cudaFuncSetAttribute(k_max<0, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            return occupancy(k_max<0, BothA>, 100 * 1024, MPC_ROW_TPB);
+        });
+        i64 g = std::max<i64>(1, std::min<i64>((i64)c->sm_count * per_sm, rows / 2));
+        if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int v = atoi(cap); if (v > 0 && v < g) g = v; }
+        const i64 tr = 2 * (((rows + 1) / 2 + g - 1) / g), wkm = max_work_u64(cols, tr);
+        if (tr <= 64 && wkm * 8 <= 100 * 1024) {
+            a.tr = (int)tr; a.use_smem = 1; a.work_u64 = wkm; a.gscratch = nullptr;
+            cudaFuncSetAttribute(k_max<0, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wkm * 8));
+            rec_begin(c, name, (u64)rows);
+            k_max<0, BothA><<<(int)g, MPC_ROW_TPB, wkm * 8, c->stream>>>(BothA{c->K}, a);
+            rec_end(c);
+            c->st.launches++;
+            return cuda_check(c, name);
+        }
+    }
     const i64 wk = max_work_u64(cols);
     if (a.cone && w > 33) return launch_rows(c, k_max<3, BothA>, kroles(k_max<3, PairA>, k_max<3, PairAS>), a, rows, wk, 0, name);
     if (w > 33) return launch_rows(c, k_max<1, BothA>, kroles(k_max<1, PairA>, k_max<1, PairAS>), a, rows, wk, 0, name);

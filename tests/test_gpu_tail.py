@@ -88,6 +88,7 @@ def test_max_half_tiles(m, monkeypatch, rows, cap, cols):
     monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
     monkeypatch.setenv("MPC_TAIL_HALF", "1")
     monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    monkeypatch.setenv("MPC_MAX_BAL", "0")
     c, o = ctx(m, 2, 1)
     x = workloads.softmax_inputs(rows, cols)
     gx, ox = c.share(torch.from_numpy(x).cuda()), o.share(x)
@@ -405,3 +406,24 @@ def test_softmax_balanced_wide_equals_tiles(m, monkeypatch):
     b = c.softmax(gx, rows, cols)
     torch.cuda.synchronize()
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("rows,cap,cols", [(150, 4, 128), (1000, 0, 128), (255, 5, 77), (12288, 0, 128), (3, 0, 33),
+                                           (200, 0, 17)])
+def test_max_balanced(m, monkeypatch, rows, cap, cols):
+    """the standalone row max on the balanced plan (k_max with one range per CTA) = the 32-row tiles and
+    the oracle"""
+    if cap:
+        monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    c, o = ctx(m, 2, 33)
+    x = workloads.softmax_inputs(rows, cols)
+    gx = c.share(torch.from_numpy(x).cuda())
+    s0 = c.step
+    a = c.max(gx, rows, cols, row_off=32)
+    monkeypatch.setenv("MPC_MAX_BAL", "0")
+    c.set_step(s0, force=True)
+    b = c.max(gx, rows, cols, row_off=32)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    if rows <= 1000:
+        same(a, o.max(o.share(x), rows, cols, row_off=32))
