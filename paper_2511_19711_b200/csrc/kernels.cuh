@@ -723,6 +723,7 @@ struct SoftmaxArgs {
     int bal;                // BOTH balanced plan: ONE row range of <= tr rows per CTA (softmax_bal_*)
     int tr;                 // rows per CTA capacity of the balanced plan
     i64 tab_u64;            // balanced plan: u64 words of one 32-row NR table
+    i64 nrange;             // balanced plan: ranges (0: one per CTA; k x grid: k rounds per CTA)
 };
 
 // Balanced plan (BOTH, no clamp / broadcast triple / cone): CTA c of ncta owns rows
@@ -787,13 +788,14 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const TilePlan tp = tile_plan(a.rows, ncta, a.half);
     const FastDiv dC = make_fastdiv((u32)C);
-    const i64 ntl = a.bal ? (i64)ncta : tp.ntot;
+    // balanced plan: nrange ranges (a multiple of the grid: k equal rounds per CTA), default one per CTA
+    const i64 ntl = a.bal ? (a.nrange > 0 ? a.nrange : (i64)ncta) : tp.ntot;
     for (i64 tile = cta; tile < ntl; tile += ncta) {
         i64 r0; int R;
         if (a.bal) {
             const i64 hr = (a.rows + 1) / 2;
-            r0 = min(a.rows, 2 * (tile * hr / ncta));
-            R = (int)(min(a.rows, 2 * ((tile + 1) * hr / ncta)) - r0);
+            r0 = min(a.rows, 2 * (tile * hr / ntl));
+            R = (int)(min(a.rows, 2 * ((tile + 1) * hr / ntl)) - r0);
             if (R <= 0) continue;
         } else {
             tile_rows(tp, tile, a.rows, r0, R);
@@ -938,6 +940,7 @@ struct MaxArgs {
     u64* escratch; int cone;
     int half;               // tail tiles as 16-row half tiles (tile_plan)
     int tr;                 // > 0: the balanced plan (k_softmax's): one range of <= tr rows per CTA
+    i64 nrange;             // balanced plan: ranges (0: one per CTA; k x grid: k rounds per CTA)
 };
 __host__ __device__ inline i64 max_work_u64(i64 cols, i64 tr = 32)
 {
@@ -959,13 +962,13 @@ __global__ void __launch_bounds__(MPC_ROW_TPB, LV == 0 ? MPC_SM_MINB_KS : MPC_SM
     SO A{{W, W + TR * HA}}, B{{W + 2 * TR * HA, W + 2 * TR * HA + TR * HB}};
     SO MX{{W + 2 * TR * HA + 2 * TR * HB, W + 2 * TR * HA + 2 * TR * HB + TR}};
     const TilePlan tp = tile_plan(a.rows, ncta, a.half);
-    const i64 ntl = a.tr > 0 ? (i64)ncta : tp.ntot;
+    const i64 ntl = a.tr > 0 ? (a.nrange > 0 ? a.nrange : (i64)ncta) : tp.ntot;
     for (i64 tile = cta; tile < ntl; tile += ncta) {
         i64 r0; int R;
         if (a.tr > 0) {                                   // balanced plan (k_softmax's softmax_bal_*)
             const i64 hr = (a.rows + 1) / 2;
-            r0 = min(a.rows, 2 * (tile * hr / ncta));
-            R = (int)(min(a.rows, 2 * ((tile + 1) * hr / ncta)) - r0);
+            r0 = min(a.rows, 2 * (tile * hr / ntl));
+            R = (int)(min(a.rows, 2 * ((tile + 1) * hr / ntl)) - r0);
             if (R <= 0) continue;
         } else {
             tile_rows(tp, tile, a.rows, r0, R);

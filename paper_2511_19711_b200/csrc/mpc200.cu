@@ -610,9 +610,11 @@ static mpc_status launch_max(mpc_ctx* c, MaxArgs& a, i64 rows, i64 cols, int w, 
         });
         i64 g = std::max<i64>(1, std::min<i64>((i64)c->sm_count * per_sm, rows / 2));
         if (const char* cap = getenv("MPC_ROW_GRID_CAP")) { const int v = atoi(cap); if (v > 0 && v < g) g = v; }
-        const i64 tr = 2 * (((rows + 1) / 2 + g - 1) / g), wkm = max_work_u64(cols, tr);
+        const i64 hr = (rows + 1) / 2;
+        const i64 nrange = hr > 32 * g ? g * ((hr + 32 * g - 1) / (32 * g)) : g;   // k rounds of ranges per CTA
+        const i64 tr = 2 * ((hr + nrange - 1) / nrange), wkm = max_work_u64(cols, tr);
         if (tr <= 64 && wkm * 8 <= 100 * 1024) {
-            a.tr = (int)tr; a.use_smem = 1; a.work_u64 = wkm; a.gscratch = nullptr;
+            a.tr = (int)tr; a.nrange = nrange; a.use_smem = 1; a.work_u64 = wkm; a.gscratch = nullptr;
             cudaFuncSetAttribute(k_max<0, BothA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wkm * 8));
             rec_begin(c, name, (u64)rows);
             k_max<0, BothA><<<(int)g, MPC_ROW_TPB, wkm * 8, c->stream>>>(BothA{c->K}, a);
@@ -1932,7 +1934,7 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
                 return cuda_check(c, "softmax");
             }
         }
-        a.bal = 0; a.tr = 32; a.tab_u64 = tab;
+        a.bal = 0; a.tr = 32; a.tab_u64 = tab; a.nrange = 0;
         // BOTH balanced plan (kernels.cuh softmax_bal_*): when the 32-row tiles need more than one round,
         // ONE row range of ~rows / grid rows per CTA, every CTA resident at once
         const char* bal_env = getenv("MPC_SOFTMAX_BAL");      // 0: off (A/B, tests; read per call)
@@ -1981,9 +1983,14 @@ static mpc_status softmax_core(mpc_ctx* c, mpc_shares x, mpc_shares z, int64_t r
             if (bal_mode >= 3) grid = std::max<i64>(1, grid / 2);   // 3: one CTA per SM (concurrent chunks)
             if (bal_mode >= 2) grid = std::max<i64>(1, std::min<i64>(grid, rows / 2));
             const i64 hr = (rows + 1) / 2;
-            const i64 tr = 2 * ((hr + grid - 1) / grid);
+            // rows that would exceed 64 per CTA (shared-memory work area) run as k equal rounds of ranges
+            // per CTA (nrange = k x grid): still one balanced plan, 32768 rows = 2 rounds of 55-56 rows
+            i64 nrange = grid;
+            if (cols <= 192 && hr > 32 * grid) nrange = grid * ((hr + 32 * grid - 1) / (32 * grid));
+            const i64 tr = 2 * ((hr + nrange - 1) / nrange);
             const i64 wkb = softmax_bal_work_u64(cols, tr, tab);
             const bool want = bal_mode >= 2 ? true : rows > 32 * grid;
+            a.nrange = nrange;
             // (up to 96 rows per CTA here: three 32-row tables, 107 KB of shared memory -- the 24576-row
             // GPT-2 shard of a pair has 84 rows per CTA)
             const i64 ntab = (tr + 31) / 32;

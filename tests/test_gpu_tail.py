@@ -427,3 +427,28 @@ def test_max_balanced(m, monkeypatch, rows, cap, cols):
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
     if rows <= 1000:
         same(a, o.max(o.share(x), rows, cols, row_off=32))
+
+
+@pytest.mark.parametrize("rows,cap,cols", [(1000, 4, 128), (777, 3, 77), (32768, 0, 128), (5000, 8, 2)])
+def test_balanced_rounds(m, monkeypatch, rows, cap, cols):
+    """more than 64 rows per CTA: k equal rounds of ranges per CTA (nrange = k x grid), softmax and the
+    standalone max; equal to the 32-row tiles and (small cases) the oracle"""
+    if cap:
+        monkeypatch.setenv("MPC_ROW_GRID_CAP", str(cap))
+    c, o = ctx(m, 2, 35)
+    x = workloads.softmax_inputs(rows, cols)
+    gx = c.share(torch.from_numpy(x).cuda())
+    s0 = c.step
+    a = c.softmax(gx, rows, cols, row_off=32)
+    am = c.max(gx, rows, cols, row_off=32)
+    monkeypatch.setenv("MPC_SOFTMAX_BAL", "0")
+    monkeypatch.setenv("MPC_MAX_BAL", "0")
+    c.set_step(s0, force=True)
+    b = c.softmax(gx, rows, cols, row_off=32)
+    bm = c.max(gx, rows, cols, row_off=32)
+    torch.cuda.synchronize()
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    assert torch.equal(am[0], bm[0]) and torch.equal(am[1], bm[1])
+    if rows <= 1000:
+        ox = o.share(x)
+        same(a, o.softmax(ox, rows, cols, row_off=32))
